@@ -1,0 +1,207 @@
+/* ridgemg_b200 — B200-native (sm_100a) solve path for the clustering-based
+ * multilevel preconditioner of (X^T X + beta I) w = X^T b  (arXiv:1806.05826).
+ *
+ * Plain C ABI: opaque handles, plain pointers and sizes, int status codes.
+ * Every entry point replaces one piece of the reference's C++ interface in
+ * /root/reference/proj/include/ridgemg (cited per function).  The C++ mirror
+ * of that interface over this ABI is include/ridgemg_b200.hpp; the ctypes
+ * binding is paper_1806_05826_b200/_lib.py.
+ *
+ * Error model (mirrors the reference's exception types):
+ *   RMG_OK                     success
+ *   RMG_ERR_INVALID_ARGUMENT   where the reference throws std::invalid_argument
+ *   RMG_ERR_RUNTIME            where it throws std::runtime_error (breakdown,
+ *                              indefinite coarse factorization)
+ *   RMG_ERR_CUDA               CUDA / device failure (no CPU fallback exists)
+ *   RMG_ERR_INTERNAL           anything else
+ * rmg_last_error() returns the thread-local message of the last failure.
+ * Non-convergence is not an error: report->converged == 0.
+ *
+ * Pointers flagged `on_device` are CUDA device pointers on the context's
+ * device; otherwise host pointers (pinned or pageable), copied inside the call.
+ */
+#ifndef RIDGEMG_B200_H
+#define RIDGEMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMG_OK 0
+#define RMG_ERR_INVALID_ARGUMENT 1
+#define RMG_ERR_RUNTIME 2
+#define RMG_ERR_CUDA 3
+#define RMG_ERR_INTERNAL 4
+
+#define RMG_MAX_LEVELS 8
+
+typedef struct rmg_context rmg_context;
+typedef struct rmg_matrix rmg_matrix;
+typedef struct rmg_method rmg_method;
+
+/* krylov.hpp:207 MethodKind (fgmres_twolevel is out of scope) */
+typedef enum {
+  RMG_METHOD_CG = 0,
+  RMG_METHOD_JACOBI_CG = 1,
+  RMG_METHOD_FCG_TWOLEVEL = 2,
+  RMG_METHOD_FCG_MULTILEVEL = 3
+} rmg_method_kind;
+
+/* krylov.hpp:135-146 ClusteringChoice::Kind (+ imported labels for parity runs) */
+typedef enum {
+  RMG_CLUSTER_LEADER_TOLERANCE = 0,
+  RMG_CLUSTER_LEADER_TARGET = 1,
+  RMG_CLUSTER_KMEANS = 2,
+  RMG_CLUSTER_IMPORTED = 100
+} rmg_clustering_kind;
+
+/* krylov.hpp:154-160 CoarseSolveChoice::Kind */
+typedef enum {
+  RMG_COARSE_DIRECT_CHOLESKY = 0,
+  RMG_COARSE_INNER_CG = 1,
+  RMG_COARSE_INNER_FCG = 2
+} rmg_coarse_kind;
+
+/* krylov.hpp:16-23 SolverConfig (omega_* of the reference is a dead knob,
+ * SURVEY.md App. A.9; per-level omega overrides live in rmg_level_spec). */
+typedef struct {
+  double tol;          /* relative residual ||r|| / ||rhs||, default 1e-6 */
+  uint64_t max_iters;  /* default 1000 */
+  uint64_t truncation; /* FCG history bound m, default 20 */
+} rmg_solver_config;
+
+/* krylov.hpp:162-167 LevelSpec (+ ClusteringChoice :135-146, CoarseSolveChoice :154-160) */
+typedef struct {
+  int32_t clustering_kind;    /* rmg_clustering_kind */
+  double tolerance;           /* leader_tolerance */
+  uint64_t target_size;       /* leader_target / kmeans */
+  uint64_t seed;              /* kmeans++ seed */
+  uint64_t kmeans_max_iters;  /* default 100 */
+  int32_t normalize_columns;  /* BASELINE cfg 2: cluster x_j/||x_j|| (extension) */
+  const int64_t* labels;      /* RMG_CLUSTER_IMPORTED: membership per feature (host) */
+  uint64_t n_clusters;        /* RMG_CLUSTER_IMPORTED: number of clusters */
+  int32_t coarse_kind;        /* rmg_coarse_kind */
+  double coarse_tol;          /* default 1e-6 */
+  uint64_t coarse_max_iters;  /* default 500 */
+  uint64_t coarse_truncation; /* default 20 */
+  int32_t has_beta_override;
+  double beta_override;
+  int32_t has_omega_override; /* parity runs: import the oracle's omega_k */
+  double omega_override;
+} rmg_level_spec;
+
+/* krylov.hpp:25-31 SolveReport; history arrays are caller buffers (may be NULL). */
+typedef struct {
+  uint64_t iterations;
+  int32_t converged;
+  double wall_time_s;            /* Krylov loop only, like krylov.cpp:163,225 */
+  double final_relative_residual;
+  double* residual_history;      /* out: relative residual after each iteration */
+  uint64_t residual_capacity;
+  uint64_t* inner_iterations;    /* out: inner iterations per outer step */
+  uint64_t inner_capacity;
+  uint64_t kernel_launches;      /* kernels this solve launched (diagnostics) */
+} rmg_solve_report;
+
+/* ---------------------------------------------------------------- context */
+const char* rmg_last_error(void);
+int rmg_version(int32_t* major, int32_t* minor);
+/* device ordinal on this process; creates a private stream */
+int rmg_context_create(int32_t device, rmg_context** out);
+int rmg_context_destroy(rmg_context* ctx);
+/* run subsequent work on an external cudaStream_t (e.g. torch's current stream) */
+int rmg_context_set_stream(rmg_context* ctx, void* cuda_stream);
+int rmg_context_synchronize(rmg_context* ctx);
+
+/* ---------------------------------------------------------------- matrix
+ * FeatureMatrix (sparse.hpp:24-32): canonical CSR, size_t offsets/indices,
+ * strictly increasing columns per row.  values == NULL (or all-ones with
+ * detect_pattern != 0) selects the binary-pattern storage (4 B/nnz).
+ * Uploads X and its transpose (X^T as CSR) to HBM with int32 indices.     */
+int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n_samples, uint64_t n_features,
+                          const uint64_t* row_offsets, const uint64_t* column_indices,
+                          const double* values, int32_t detect_pattern, rmg_matrix** out);
+int rmg_matrix_destroy(rmg_matrix* m);
+int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n_samples, uint64_t* n_features,
+                     uint64_t* nnz, int32_t* is_pattern);
+
+/* y = X v            (sparse.hpp:61, sparse.cpp:127-144)   */
+int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device);
+/* y = X^T u          (sparse.hpp:66, sparse.cpp:152-176)   */
+int rmg_spmv_transpose(rmg_matrix* m, const double* u, double* y, int32_t on_device);
+/* out = X^T X w + beta w   (RidgeOperator::apply, ridge.cpp:16-24) */
+int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, int32_t on_device);
+/* d_j = beta + ||X(:,j)||^2 (gram_diagonal, ridge.cpp:30-37) */
+int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device);
+/* largest eigenvalue of X^T X by power iteration (estimate_lambda_max, krylov.cpp:62-92) */
+int rmg_lambda_max(rmg_matrix* m, double tol, uint64_t max_iters, uint64_t seed, double* value,
+                   uint64_t* iterations, int32_t* converged);
+
+/* ---------------------------------------------------------------- host helpers
+ * generate_rhs (analysis.cpp:225-232): b_i = CounterRng(seed) normals
+ * (rng.hpp:25-72, glibc libm), rhs = X^T b on the device.  rhs may be NULL. */
+int rmg_generate_rhs(rmg_matrix* m, uint64_t seed, double* b_out, double* rhs_out);
+/* n standard normals of CounterRng(seed) (rng.hpp:50-61) */
+int rmg_rng_normals(uint64_t seed, uint64_t n, double* out);
+
+/* BASELINE.json synthetic inputs, generated on the host with
+ * CounterRng + glibc libm so every arm sees identical bytes.  Two-step:
+ * rmg_synth_* returns an opaque host CSR and its sizes; rmg_host_csr_export
+ * copies it into caller arrays (values may be NULL for binary patterns). */
+typedef struct rmg_host_csr rmg_host_csr;
+/* cfg 1: X[:,j] = Z[:, j mod groups] + noise * N(0,1), Z ~ N(0,1) (N x groups) */
+int rmg_synth_dense_clustered(uint64_t n, uint64_t f, uint64_t groups, double noise, uint64_t seed,
+                              rmg_host_csr** out, uint64_t* nnz);
+/* cfg 2/3/5: nnz per row max(1, Poisson(mean)), Zipf(s) column popularity over a
+ * seeded permutation, without replacement per row; values 1.0 or |N(0,1)| */
+int rmg_synth_sparse_zipf(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
+                          uint64_t seed, rmg_host_csr** out, uint64_t* nnz);
+int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* row_offsets, uint64_t* column_indices, double* values);
+int rmg_host_csr_destroy(rmg_host_csr* h);
+
+/* ---------------------------------------------------------------- methods
+ * PreparedMethod(x, beta, spec) (krylov.hpp:222-242, krylov.cpp:617-649):
+ * clustering, aggregation, coarse matrices, omegas and coarse factorization
+ * all done here.  `levels` is ignored by cg / jacobi_cg.  The matrix must
+ * outlive the method (ridge.hpp:37 lifetime contract).                  */
+int rmg_method_prepare(rmg_matrix* m, double beta, int32_t method_kind,
+                       const rmg_level_spec* levels, uint64_t n_levels,
+                       const rmg_solver_config* solver, rmg_method** out);
+int rmg_method_destroy(rmg_method* pm);
+/* PreparedMethod::solve (krylov.cpp:651-668): rhs = X^T b, then the Krylov
+ * solve; b has n_samples entries, w_out n_features.                     */
+int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_report* report,
+                     int32_t on_device);
+/* Same solve from a prebuilt rhs = X^T b (the reference's timed region). */
+int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out,
+                         rmg_solve_report* report, int32_t on_device);
+/* Apply the level-0 preconditioner once: z = M^{-1} r (two_level_apply, krylov.cpp:379-425). */
+int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device);
+/* PreparedMethod::coarse_size (krylov.hpp:229) and per-level introspection */
+int rmg_method_info(const rmg_method* pm, uint64_t* n_levels, uint64_t* coarse_size);
+int rmg_method_level(const rmg_method* pm, uint64_t level, uint64_t* n_features, uint64_t* nnz,
+                     double* beta, double* omega);
+/* labels of the aggregation from `level` to `level+1` (membership per feature) */
+int rmg_method_level_labels(const rmg_method* pm, uint64_t level, int64_t* labels_out);
+/* export the coarse matrix X_{level} (level >= 1) in CSR (for parity checks) */
+int rmg_method_level_matrix(const rmg_method* pm, uint64_t level, uint64_t* row_offsets,
+                            uint64_t* column_indices, double* values);
+
+/* SystemSolution solve_system(x, beta, b, spec) (krylov.hpp:251-252) */
+int rmg_solve_system(rmg_matrix* m, double beta, int32_t method_kind, const rmg_level_spec* levels,
+                     uint64_t n_levels, const rmg_solver_config* solver, const double* b,
+                     double* w_out, rmg_solve_report* report, uint64_t* coarse_size);
+
+/* ---------------------------------------------------------------- profiling
+ * Average device time (CUDA events on the context stream) of `reps`
+ * applications of the level-`level` operator kernels, for the roofline. */
+int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int32_t flush_l2,
+                             double* ms_per_apply, double* ms_k1, double* ms_k2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RIDGEMG_B200_H */

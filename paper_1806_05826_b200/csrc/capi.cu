@@ -1,0 +1,447 @@
+// extern "C" boundary of ridgemg_b200 (include/ridgemg_b200.h).  Each entry
+// point translates C++ exceptions into the status codes of the header and
+// keeps the message in a thread-local buffer (rmg_last_error).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "ridgemg_b200.h"
+#include "runtime.cuh"
+
+struct rmg_context {
+  rmg::Context c;
+  explicit rmg_context(int dev) : c(dev) {}
+};
+struct rmg_matrix {
+  rmg::Matrix m;
+  rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect) : m(ctx, std::move(h), detect) {}
+};
+struct rmg_host_csr {
+  rmg::HostCsr h;
+};
+struct rmg_method {
+  rmg::Method m;
+  rmg::DBuf<double> b, rhs, w;  // staging for host-pointer calls
+  template <class... A>
+  explicit rmg_method(A&&... a) : m(std::forward<A>(a)...) {}
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return RMG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return RMG_ERR_INVALID_ARGUMENT;
+  } catch (const rmg::CudaError& e) {
+    g_err = e.what();
+    return RMG_ERR_CUDA;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return RMG_ERR_RUNTIME;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RMG_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RMG_ERR_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return RMG_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (p == nullptr) throw rmg::InvalidArgument(std::string(what) + " must not be NULL");
+}
+
+// Device view of a caller vector: either the pointer itself or a staged copy.
+const double* stage_in(rmg::Context& c, const double* p, size_t n, int32_t on_device, rmg::DBuf<double>& buf) {
+  if (on_device) return p;
+  if (buf.size() < std::max<size_t>(n, 1)) buf.alloc(std::max<size_t>(n, 1));
+  if (n) RMG_CK(cudaMemcpyAsync(buf.get(), p, n * 8, cudaMemcpyHostToDevice, c.stream));
+  return buf.get();
+}
+double* stage_out(size_t n, int32_t on_device, double* p, rmg::DBuf<double>& buf) {
+  if (on_device) return p;
+  if (buf.size() < std::max<size_t>(n, 1)) buf.alloc(std::max<size_t>(n, 1));
+  return buf.get();
+}
+void finish_out(rmg::Context& c, const double* dev, double* host, size_t n, int32_t on_device) {
+  if (!on_device && n) RMG_CK(cudaMemcpyAsync(host, dev, n * 8, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+}
+
+void fill_report(const rmg::SolveResult& r, uint64_t launches, rmg_solve_report* out) {
+  if (!out) return;
+  out->iterations = r.iterations;
+  out->converged = r.converged ? 1 : 0;
+  out->wall_time_s = r.wall;
+  out->final_relative_residual = r.final_rel;
+  out->kernel_launches = launches;
+  if (out->residual_history)
+    std::memcpy(out->residual_history, r.hist.data(), std::min<size_t>(out->residual_capacity, r.hist.size()) * 8);
+  if (out->inner_iterations) {
+    const size_t n = std::min<size_t>(out->inner_capacity, r.inner.size());
+    for (size_t i = 0; i < n; ++i) out->inner_iterations[i] = r.inner[i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rmg_last_error(void) { return g_err.c_str(); }
+
+int rmg_version(int32_t* major, int32_t* minor) {
+  return guard([&] {
+    need(major, "major");
+    need(minor, "minor");
+    *major = 0;
+    *minor = 1;
+  });
+}
+
+int rmg_context_create(int32_t device, rmg_context** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new rmg_context(device);
+  });
+}
+
+int rmg_context_destroy(rmg_context* ctx) {
+  return guard([&] { delete ctx; });
+}
+
+int rmg_context_set_stream(rmg_context* ctx, void* stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    RMG_CK(cudaStreamSynchronize(ctx->c.stream));
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+    ctx->c.own_stream = false;
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int rmg_context_synchronize(rmg_context* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c.sync();
+  });
+}
+
+int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n, uint64_t f, const uint64_t* rp, const uint64_t* ci,
+                          const double* values, int32_t detect_pattern, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    need(rp, "row_offsets");
+    rmg::HostCsr h;
+    h.n = static_cast<int64_t>(n);
+    h.f = static_cast<int64_t>(f);
+    h.ptr.assign(rp, rp + n + 1);
+    const uint64_t nnz = rp[n];
+    if (nnz) need(ci, "column_indices");
+    h.idx.assign(ci, ci + nnz);
+    if (values) h.val.assign(values, values + nnz);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, std::move(h), detect_pattern != 0);
+  });
+}
+
+int rmg_matrix_destroy(rmg_matrix* m) {
+  return guard([&] { delete m; });
+}
+
+int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n, uint64_t* f, uint64_t* nnz, int32_t* is_pattern) {
+  return guard([&] {
+    need(m, "matrix");
+    if (n) *n = m->m.n();
+    if (f) *f = m->m.f();
+    if (nnz) *nnz = m->m.nnz();
+    if (is_pattern) *is_pattern = m->m.pattern ? 1 : 0;
+  });
+}
+
+int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device) {
+  return guard([&] {
+    need(m, "matrix");
+    rmg::Context& c = *m->m.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    rmg::DBuf<double> bi, bo;
+    const double* dv = stage_in(c, v, m->m.f(), on_device, bi);
+    double* dy = stage_out(m->m.n(), on_device, y, bo);
+    m->m.spmv(dv, dy);
+    finish_out(c, dy, y, m->m.n(), on_device);
+  });
+}
+
+int rmg_spmv_transpose(rmg_matrix* m, const double* u, double* y, int32_t on_device) {
+  return guard([&] {
+    need(m, "matrix");
+    rmg::Context& c = *m->m.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    rmg::DBuf<double> bi, bo;
+    const double* du = stage_in(c, u, m->m.n(), on_device, bi);
+    double* dy = stage_out(m->m.f(), on_device, y, bo);
+    m->m.spmv_t(du, dy);
+    finish_out(c, dy, y, m->m.f(), on_device);
+  });
+}
+
+int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, int32_t on_device) {
+  return guard([&] {
+    need(m, "matrix");
+    if (beta < 0.0) throw rmg::InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
+    rmg::Context& c = *m->m.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    rmg::DBuf<double> bi, bo;
+    const double* dw = stage_in(c, w, m->m.f(), on_device, bi);
+    double* dout = stage_out(m->m.f(), on_device, out, bo);
+    rmg::XtArgs a;
+    a.v = dw;
+    a.out = dout;
+    a.beta = beta;
+    m->m.apply(dw, rmg::Epi::Axpby, a);
+    finish_out(c, dout, out, m->m.f(), on_device);
+  });
+}
+
+int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device) {
+  return guard([&] {
+    need(m, "matrix");
+    rmg::Context& c = *m->m.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    rmg::DBuf<double> bo;
+    double* d = stage_out(m->m.f(), on_device, out, bo);
+    rmg::launch_diag_gram(m->m.xt.view, beta, d, c.stream);
+    finish_out(c, d, out, m->m.f(), on_device);
+  });
+}
+
+int rmg_lambda_max(rmg_matrix* m, double tol, uint64_t max_iters, uint64_t seed, double* value, uint64_t* iterations,
+                   int32_t* converged) {
+  return guard([&] {
+    need(m, "matrix");
+    need(value, "value");
+    RMG_CK(cudaSetDevice(m->m.ctx->device));
+    uint64_t it = 0;
+    bool cv = false;
+    *value = m->m.lambda_max(tol, max_iters, seed, &it, &cv);
+    if (iterations) *iterations = it;
+    if (converged) *converged = cv ? 1 : 0;
+  });
+}
+
+int rmg_rng_normals(uint64_t seed, uint64_t n, double* out) {
+  return guard([&] {
+    need(out, "out");
+    rmg::CounterRng rng(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = rng.next_normal();
+  });
+}
+
+int rmg_generate_rhs(rmg_matrix* m, uint64_t seed, double* b_out, double* rhs_out) {
+  return guard([&] {
+    need(m, "matrix");
+    need(b_out, "b_out");
+    rmg::CounterRng rng(seed);
+    const int64_t n = m->m.n();
+    for (int64_t i = 0; i < n; ++i) b_out[i] = rng.next_normal();
+    if (rhs_out) {
+      rmg::Context& c = *m->m.ctx;
+      RMG_CK(cudaSetDevice(c.device));
+      rmg::DBuf<double> bi, bo;
+      const double* db = stage_in(c, b_out, n, 0, bi);
+      double* dr = stage_out(m->m.f(), 0, rhs_out, bo);
+      m->m.spmv_t(db, dr);
+      finish_out(c, dr, rhs_out, m->m.f(), 0);
+    }
+  });
+}
+
+int rmg_synth_dense_clustered(uint64_t n, uint64_t f, uint64_t groups, double noise, uint64_t seed,
+                              rmg_host_csr** out, uint64_t* nnz) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new rmg_host_csr{rmg::synth_dense_clustered(static_cast<int64_t>(n), static_cast<int64_t>(f),
+                                                          static_cast<int64_t>(groups), noise, seed)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+  });
+}
+
+int rmg_synth_sparse_zipf(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
+                          uint64_t seed, rmg_host_csr** out, uint64_t* nnz) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new rmg_host_csr{rmg::synth_sparse_zipf(static_cast<int64_t>(n), static_cast<int64_t>(f), mean_nnz,
+                                                      zipf_s, abs_normal_values != 0, seed)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+  });
+}
+
+int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* rp, uint64_t* ci, double* v) {
+  return guard([&] {
+    need(h, "host csr");
+    if (rp)
+      for (int64_t i = 0; i <= h->h.n; ++i) rp[i] = static_cast<uint64_t>(h->h.ptr[i]);
+    if (ci)
+      for (int64_t k = 0; k < h->h.nnz(); ++k) ci[k] = static_cast<uint64_t>(h->h.idx[k]);
+    if (v) {
+      if (h->h.val.empty())
+        std::fill(v, v + h->h.nnz(), 1.0);
+      else
+        std::memcpy(v, h->h.val.data(), h->h.val.size() * 8);
+    }
+  });
+}
+
+int rmg_host_csr_destroy(rmg_host_csr* h) {
+  return guard([&] { delete h; });
+}
+
+int rmg_method_prepare(rmg_matrix* m, double beta, int32_t kind, const rmg_level_spec* levels, uint64_t n_levels,
+                       const rmg_solver_config* solver, rmg_method** out) {
+  return guard([&] {
+    need(m, "matrix");
+    need(out, "out");
+    rmg_solver_config cfg{1e-6, 1000, 20};
+    if (solver) cfg = *solver;
+    RMG_CK(cudaSetDevice(m->m.ctx->device));
+    *out = new rmg_method(&m->m, beta, kind, levels, n_levels, cfg);
+  });
+}
+
+int rmg_method_destroy(rmg_method* pm) {
+  return guard([&] { delete pm; });
+}
+
+int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out, rmg_solve_report* report, int32_t on_device) {
+  return guard([&] {
+    need(pm, "method");
+    need(rhs, "rhs");
+    need(w_out, "w_out");
+    rmg::Matrix& x = *pm->m.fine();
+    rmg::Context& c = *x.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    const uint64_t l0 = c.launches;
+    const double* drhs = stage_in(c, rhs, x.f(), on_device, pm->rhs);
+    double* dw = stage_out(x.f(), on_device, w_out, pm->w);
+    const rmg::SolveResult r = pm->m.solve_rhs(drhs, dw);
+    finish_out(c, dw, w_out, x.f(), on_device);
+    fill_report(r, c.launches - l0, report);
+  });
+}
+
+int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_report* report, int32_t on_device) {
+  return guard([&] {
+    need(pm, "method");
+    need(b, "b");
+    need(w_out, "w_out");
+    rmg::Matrix& x = *pm->m.fine();
+    rmg::Context& c = *x.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    const uint64_t l0 = c.launches;
+    const double* db = stage_in(c, b, x.n(), on_device, pm->b);
+    if (pm->rhs.size() < static_cast<size_t>(std::max<int64_t>(1, x.f()))) pm->rhs.alloc(std::max<int64_t>(1, x.f()));
+    x.spmv_t(db, pm->rhs.get());  // krylov.cpp:655, outside the solver timer
+    double* dw = stage_out(x.f(), on_device, w_out, pm->w);
+    const rmg::SolveResult r = pm->m.solve_rhs(pm->rhs.get(), dw);
+    finish_out(c, dw, w_out, x.f(), on_device);
+    fill_report(r, c.launches - l0, report);
+  });
+}
+
+int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device) {
+  return guard([&] {
+    need(pm, "method");
+    rmg::Matrix& x = *pm->m.fine();
+    rmg::Context& c = *x.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    const double* dr = stage_in(c, r, x.f(), on_device, pm->rhs);
+    double* dz = stage_out(x.f(), on_device, z, pm->w);
+    pm->m.precondition(dr, dz);
+    finish_out(c, dz, z, x.f(), on_device);
+  });
+}
+
+int rmg_method_info(const rmg_method* pm, uint64_t* n_levels, uint64_t* coarse_size) {
+  return guard([&] {
+    need(pm, "method");
+    if (n_levels) *n_levels = pm->m.n_levels();
+    if (coarse_size) *coarse_size = pm->m.coarse_size();
+  });
+}
+
+int rmg_method_level(const rmg_method* pm, uint64_t level, uint64_t* n_features, uint64_t* nnz, double* beta,
+                     double* omega) {
+  return guard([&] {
+    need(pm, "method");
+    if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
+    const rmg::Matrix& mk = pm->m.level_matrix(level);
+    if (n_features) *n_features = mk.f();
+    if (nnz) *nnz = mk.nnz();
+    if (beta) *beta = pm->m.level_beta(level);
+    if (omega) *omega = pm->m.omega(level);
+  });
+}
+
+int rmg_method_level_labels(const rmg_method* pm, uint64_t level, int64_t* labels_out) {
+  return guard([&] {
+    need(pm, "method");
+    need(labels_out, "labels_out");
+    const auto& l = pm->m.labels(level);
+    std::memcpy(labels_out, l.data(), l.size() * sizeof(int64_t));
+  });
+}
+
+int rmg_method_level_matrix(const rmg_method* pm, uint64_t level, uint64_t* rp, uint64_t* ci, double* v) {
+  return guard([&] {
+    need(pm, "method");
+    if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
+    const rmg::HostCsr& h = pm->m.level_matrix(level).host;
+    if (rp)
+      for (int64_t i = 0; i <= h.n; ++i) rp[i] = static_cast<uint64_t>(h.ptr[i]);
+    if (ci)
+      for (int64_t k = 0; k < h.nnz(); ++k) ci[k] = static_cast<uint64_t>(h.idx[k]);
+    if (v) std::memcpy(v, h.val.data(), h.val.size() * 8);
+  });
+}
+
+int rmg_solve_system(rmg_matrix* m, double beta, int32_t kind, const rmg_level_spec* levels, uint64_t n_levels,
+                     const rmg_solver_config* solver, const double* b, double* w_out, rmg_solve_report* report,
+                     uint64_t* coarse_size) {
+  rmg_method* pm = nullptr;
+  int rc = rmg_method_prepare(m, beta, kind, levels, n_levels, solver, &pm);
+  if (rc != RMG_OK) return rc;
+  rc = rmg_method_solve(pm, b, w_out, report, 0);
+  if (rc == RMG_OK && coarse_size) *coarse_size = pm->m.coarse_size();
+  const std::string keep = g_err;
+  rmg_method_destroy(pm);
+  g_err = keep;
+  return rc;
+}
+
+int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int32_t flush_l2, double* ms_per_apply,
+                             double* ms_k1, double* ms_k2) {
+  return guard([&] {
+    need(pm, "method");
+    double k1 = 0.0, k2 = 0.0;
+    RMG_CK(cudaSetDevice(pm->m.fine()->ctx->device));
+    const double t = pm->m.time_operator(level, reps, flush_l2 != 0, &k1, &k2);
+    if (ms_per_apply) *ms_per_apply = t;
+    if (ms_k1) *ms_k1 = k1;
+    if (ms_k2) *ms_k2 = k2;
+  });
+}
+
+}  // extern "C"

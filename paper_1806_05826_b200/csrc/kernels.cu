@@ -1,0 +1,725 @@
+// sm_100a kernels for the ridgemg_b200 solve path.  See kernels.cuh for the
+// data layout and DESIGN.md §4 for the per-kernel roofline.
+//
+// All of this path is HBM/L2-bandwidth or latency bound integer-indexed fp64
+// work (2 flops per nonzero), so it deliberately uses CUDA cores, coalesced
+// index streams, read-only gathers and fixed-order reductions rather than
+// tensor cores.
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace rmg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int W>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-tree block sum; the result is valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// "Last block" detection for single-kernel grid reductions: every block's
+// thread 0 publishes its slot before the ticket; the final arriver then owns
+// all slots (threadFenceReduction pattern).  Deterministic: slots are summed
+// in index order by the last block, whoever it is.
+__device__ __forceinline__ bool grid_last(unsigned* ticket) {
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1) ? 1u : 0u;
+    if (s_last) {
+      __threadfence();
+      *ticket = 0u;  // ready for the next launch
+    }
+  }
+  __syncthreads();
+  return s_last != 0u;
+}
+
+// Sum `n` slots (stride `stride`, component `c`) in a fixed order with the
+// whole block; result valid in thread 0.
+__device__ __forceinline__ double sum_slots(const double* slots, int n, int stride, int c, double* sh) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += __ldcg(slots + (size_t)i * stride + c);
+  return block_sum(acc, sh);
+}
+
+__device__ __forceinline__ int ring_slot(const KrylovScalars* sc) { return sc->it % (sc->keep + 1); }
+
+// ------------------------------------------------------------------ K1: t = X v
+// Row-parallel CSR gather; W lanes per row, warp-uniform trip counts so the
+// group reductions never diverge.  Per-row sum order: lane-strided partials
+// then an xor tree (deterministic).
+template <int W, bool PAT>
+__global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restrict__ ptr,
+                                                        const int32_t* __restrict__ idx,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ v,
+                                                        double* __restrict__ t, int64_t rows,
+                                                        const int32_t* done,
+                                                        const KrylovScalars* sc, int ring_stride) {
+  if (done != nullptr && *done) return;
+  if (sc != nullptr) {
+    if (sc->done) return;
+    v += (size_t)ring_slot(sc) * ring_stride;
+  }
+  constexpr int G = 32 / W;  // rows per warp
+  const int lane = threadIdx.x & (W - 1);
+  const int grp = (threadIdx.x & 31) / W;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t rb = warp * G; rb < rows; rb += nwarps * G) {
+    const int64_t row = rb + grp;
+    double s = 0.0;
+    if (row < rows) {
+      const int k1 = ptr[row + 1];
+      for (int k = ptr[row] + lane; k < k1; k += W) {
+        const double x = __ldg(v + idx[k]);
+        s += PAT ? x : val[k] * x;
+      }
+    }
+    s = group_sum<W>(s);
+    if (row < rows && lane == 0) t[row] = s;
+  }
+}
+
+// ------------------------------------------------------------------ K2: X^T pass + epilogue
+template <Epi E>
+__device__ __forceinline__ void xt_epilogue(int col, double s, const XtArgs& a, const double* v,
+                                            double* out, double& d0, double& d1) {
+  if constexpr (E == Epi::Plain) {
+    out[col] = s;
+  } else if constexpr (E == Epi::Axpby) {
+    out[col] = s + a.beta * v[col];
+  } else if constexpr (E == Epi::Fcg) {
+    const double pj = v[col];
+    const double apj = s + a.beta * pj;
+    out[col] = apj;
+    d0 += pj * apj;
+    d1 += pj * a.r[col];
+  } else if constexpr (E == Epi::Cg) {
+    const double pj = v[col];
+    const double apj = s + a.beta * pj;
+    out[col] = apj;
+    d0 += pj * apj;
+  } else if constexpr (E == Epi::Rich) {
+    const double z1 = v[col];
+    const double az1 = s + a.beta * z1;
+    out[col] = z1 + a.omega * (a.r[col] - az1);
+  } else {  // Gram
+    out[col] = s;
+    d0 += s * s;
+  }
+}
+
+template <Epi E>
+constexpr bool has_dots() {
+  return E == Epi::Fcg || E == Epi::Cg || E == Epi::Gram;
+}
+
+template <int W, bool PAT, Epi E>
+__global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr,
+                                                 const int32_t* __restrict__ idx,
+                                                 const double* __restrict__ val, XtSchedule sch,
+                                                 XtArgs a) {
+  if (a.done != nullptr && *a.done) return;
+  const double* v = a.v;
+  double* out = a.out;
+  if constexpr (E == Epi::Fcg) {
+    if (a.sc->done) return;
+    const size_t off = (size_t)ring_slot(a.sc) * a.ring_stride;
+    v += off;
+    out += off;
+  } else if constexpr (E == Epi::Cg) {
+    if (a.sc->done) return;
+  }
+  __shared__ double sh[kWarps];
+  __shared__ int s_fin;
+  const double* __restrict__ t = a.t;
+  const int4 item = sch.items[blockIdx.x];
+  double d0 = 0.0, d1 = 0.0;
+  if (item.z < 0) {
+    // short columns [item.x, item.y): W lanes per column
+    constexpr int G = 32 / W;
+    const int lane = threadIdx.x & (W - 1);
+    const int grp = (threadIdx.x & 31) / W;
+    const int wid = threadIdx.x >> 5;
+    for (int cb = item.x + wid * G; cb < item.y; cb += kWarps * G) {
+      const int col = cb + grp;
+      double s = 0.0;
+      if (col < item.y) {
+        const int k1 = ptr[col + 1];
+        for (int k = ptr[col] + lane; k < k1; k += W) {
+          const double x = __ldg(t + idx[k]);
+          s += PAT ? x : val[k] * x;
+        }
+      }
+      s = group_sum<W>(s);
+      if (col < item.y && lane == 0) xt_epilogue<E>(col, s, a, v, out, d0, d1);
+    }
+    if constexpr (has_dots<E>()) {
+      const double b0 = block_sum(d0, sh);
+      const double b1 = (E == Epi::Fcg) ? block_sum(d1, sh) : 0.0;
+      if (threadIdx.x == 0) {
+        sch.slots[(size_t)item.w * 2] = b0;
+        sch.slots[(size_t)item.w * 2 + 1] = b1;
+      }
+    }
+  } else {
+    // one fixed segment [item.y, item.z) of long column item.x
+    double s = 0.0;
+    for (int k = item.y + threadIdx.x; k < item.z; k += kThreads) {
+      const double x = __ldg(t + idx[k]);
+      s += PAT ? x : val[k] * x;
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+      sch.seg_partial[item.w] = s;
+      __threadfence();
+      const unsigned tk = atomicAdd(sch.col_ticket + item.x, 1u);
+      s_fin = (tk == (unsigned)sch.long_nseg[item.x] - 1u) ? 1 : 0;
+      if (s_fin) {
+        __threadfence();
+        sch.col_ticket[item.x] = 0u;
+        const int first = sch.long_first_seg[item.x], nseg = sch.long_nseg[item.x];
+        double tot = 0.0;
+        for (int q = 0; q < nseg; ++q) tot += __ldcg(sch.seg_partial + first + q);
+        xt_epilogue<E>(sch.long_col[item.x], tot, a, v, out, d0, d1);
+        if constexpr (has_dots<E>()) {
+          const int slot = sch.long_slot[item.x];
+          sch.slots[(size_t)slot * 2] = d0;
+          sch.slots[(size_t)slot * 2 + 1] = d1;
+        }
+      }
+    }
+  }
+  if constexpr (has_dots<E>()) {
+    if (grid_last(sch.grid_ticket)) {
+      const double s0 = sum_slots(sch.slots, sch.n_slots, 2, 0, sh);
+      const double s1 = (E == Epi::Fcg) ? sum_slots(sch.slots, sch.n_slots, 2, 1, sh) : 0.0;
+      if (threadIdx.x == 0) {
+        KrylovScalars* sc = a.sc;
+        if constexpr (E == Epi::Fcg) {  // krylov.cpp:199-208
+          sc->pap = s0;
+          sc->pr = s1;
+          if (s0 == 0.0) {
+            sc->status = 1;
+            sc->done = 1;
+          } else if (s0 < 0.0) {
+            sc->status = 2;
+            sc->done = 1;
+          } else {
+            sc->alpha = s1 / s0;
+            sc->pap_ring[ring_slot(sc)] = s0;
+          }
+        } else if constexpr (E == Epi::Cg) {  // krylov.cpp:126-134
+          sc->pap = s0;
+          if (!(s0 > 0.0)) {
+            sc->status = 2;
+            sc->done = 1;
+          } else {
+            sc->alpha = sc->rz / s0;
+          }
+        } else {  // Gram: lambda = ||A v|| (krylov.cpp:80-81)
+          sc->lambda = sqrt(s0);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Krylov vector kernels
+template <class F>
+__device__ __forceinline__ void grid_stride(int64_t n, F&& f) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) f(i);
+}
+
+// x = 0, r = b, nb = ||b|| (krylov.cpp:164-176), rhs finiteness (krylov.cpp:23-31)
+__global__ void __launch_bounds__(kThreads) k_krylov_begin(const double* __restrict__ b, double* __restrict__ x,
+                                                           double* __restrict__ r, int64_t n, KrylovScalars* sc,
+                                                           double* hist, double* slots, unsigned* ticket) {
+  __shared__ double sh[kWarps];
+  double acc = 0.0, bad = 0.0;
+  grid_stride(n, [&](int64_t i) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    acc += bi * bi;
+    if (!isfinite(bi)) bad += 1.0;
+  });
+  const double s0 = block_sum(acc, sh);
+  const double s1 = block_sum(bad, sh);
+  if (threadIdx.x == 0) {
+    slots[blockIdx.x * 2] = s0;
+    slots[blockIdx.x * 2 + 1] = s1;
+  }
+  if (grid_last(ticket)) {
+    const double t0 = sum_slots(slots, gridDim.x, 2, 0, sh);
+    const double t1 = sum_slots(slots, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      sc->it = 0;
+      sc->use = 0;
+      sc->status = t1 > 0.0 ? 3 : 0;
+      sc->nb = sqrt(t0);
+      sc->converged = 0;
+      sc->done = sc->status != 0 ? 1 : 0;
+      sc->rel = 1.0;
+      if (sc->status == 0 && sc->nb == 0.0) {  // krylov.cpp:170-175
+        sc->converged = 1;
+        sc->done = 1;
+        sc->rel = 0.0;
+        hist[0] = 0.0;
+      }
+    }
+  }
+}
+
+// Gram-Schmidt coefficients c_q = <z, Ap_q> / <p_q, Ap_q> over the newest
+// use = min(m_i, |history|) directions (krylov.cpp:189-197).
+__global__ void __launch_bounds__(kThreads) k_fcg_gs_dots(const double* __restrict__ z,
+                                                          const double* __restrict__ ap_ring, int64_t n,
+                                                          KrylovScalars* sc, double* slots, unsigned* ticket) {
+  if (sc->done) return;
+  const int it = sc->it, keep = sc->keep;
+  const int mi = it == 0 ? 0 : max(1, it % (keep + 1));
+  const int use = min(mi, min(it, keep));
+  if (use == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->use = 0;
+    return;
+  }
+  __shared__ double sh[kWarps];
+  const int R = keep + 1;
+  for (int q = 0; q < use; ++q) {
+    const double* aph = ap_ring + (size_t)((it - use + q) % R) * n;
+    double acc = 0.0;
+    grid_stride(n, [&](int64_t i) { acc += z[i] * aph[i]; });
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) slots[(size_t)blockIdx.x * 32 + q] = s;
+  }
+  if (grid_last(ticket)) {
+    for (int q = 0; q < use; ++q) {
+      const double s = sum_slots(slots + q, gridDim.x, 32, 0, sh);
+      if (threadIdx.x == 0) sc->coeff[q] = s / sc->pap_ring[(it - use + q) % R];
+    }
+    if (threadIdx.x == 0) sc->use = use;
+  }
+}
+
+// p = z - sum_q c_q p_q, oldest -> newest, written into ring slot it % (m+1)
+__global__ void __launch_bounds__(kThreads) k_fcg_update_p(const double* __restrict__ z, double* p_ring, int64_t n,
+                                                           const KrylovScalars* sc) {
+  if (sc->done) return;
+  const int it = sc->it, R = sc->keep + 1, use = sc->use;
+  double* p = p_ring + (size_t)(it % R) * n;
+  grid_stride(n, [&](int64_t i) {
+    double pi = z[i];
+    for (int q = 0; q < use; ++q) pi -= sc->coeff[q] * p_ring[(size_t)((it - use + q) % R) * n + i];
+    p[i] = pi;
+  });
+}
+
+// x += alpha p; r -= alpha Ap; rel = ||r|| / ||rhs|| (krylov.cpp:208-223)
+__global__ void __launch_bounds__(kThreads) k_fcg_axpy(double* __restrict__ x, double* __restrict__ r,
+                                                       const double* __restrict__ p_ring,
+                                                       const double* __restrict__ ap_ring, int64_t n,
+                                                       KrylovScalars* sc, double* hist, double* slots,
+                                                       unsigned* ticket) {
+  if (sc->done) return;
+  __shared__ double sh[kWarps];
+  const size_t off = (size_t)ring_slot(sc) * n;
+  const double* p = p_ring + off;
+  const double* ap = ap_ring + off;
+  const double alpha = sc->alpha;
+  double acc = 0.0;
+  grid_stride(n, [&](int64_t i) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * ap[i];
+    r[i] = ri;
+    acc += ri * ri;
+  });
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) slots[blockIdx.x * 2] = s;
+  if (grid_last(ticket)) {
+    const double rr = sum_slots(slots, gridDim.x, 2, 0, sh);
+    if (threadIdx.x == 0) {
+      const double rel = sqrt(rr) / sc->nb;
+      hist[sc->it] = rel;
+      sc->rel = rel;
+      sc->it += 1;
+      if (rel <= sc->tol) {
+        sc->converged = 1;
+        sc->done = 1;
+      } else if (sc->it >= sc->max_iters) {
+        sc->done = 1;
+      }
+    }
+  }
+}
+
+// CG start (krylov.cpp:100-123): x = 0, r = b, z = D^-1 r (or r), p = z, rz = <r,z>
+__global__ void __launch_bounds__(kThreads) k_cg_begin(const double* __restrict__ b, const double* __restrict__ inv,
+                                                       double* x, double* r, double* z, double* p, int64_t n,
+                                                       KrylovScalars* sc, double* hist, double* slots,
+                                                       unsigned* ticket) {
+  __shared__ double sh[kWarps];
+  double bb = 0.0, rz = 0.0, bad = 0.0;
+  grid_stride(n, [&](int64_t i) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    const double zi = inv != nullptr ? inv[i] * bi : bi;
+    if (inv != nullptr) z[i] = zi;
+    p[i] = zi;
+    bb += bi * bi;
+    rz += bi * zi;
+    if (!isfinite(bi)) bad += 1.0;
+  });
+  const double s0 = block_sum(bb, sh), s1 = block_sum(rz, sh), s2 = block_sum(bad, sh);
+  if (threadIdx.x == 0) {
+    slots[blockIdx.x * 4] = s0;
+    slots[blockIdx.x * 4 + 1] = s1;
+    slots[blockIdx.x * 4 + 2] = s2;
+  }
+  if (grid_last(ticket)) {
+    const double t0 = sum_slots(slots, gridDim.x, 4, 0, sh);
+    const double t1 = sum_slots(slots, gridDim.x, 4, 1, sh);
+    const double t2 = sum_slots(slots, gridDim.x, 4, 2, sh);
+    if (threadIdx.x == 0) {
+      sc->it = 0;
+      sc->status = t2 > 0.0 ? 3 : 0;
+      sc->nb = sqrt(t0);
+      sc->rz = t1;
+      sc->converged = 0;
+      sc->done = sc->status != 0 ? 1 : 0;
+      sc->rel = 1.0;
+      if (sc->status == 0 && sc->nb == 0.0) {
+        sc->converged = 1;
+        sc->done = 1;
+        sc->rel = 0.0;
+        hist[0] = 0.0;
+      }
+    }
+  }
+}
+
+// x += alpha p; r -= alpha Ap; rel; z = D^-1 r; rz' = <r,z>; beta = rz'/rz (krylov.cpp:134-153)
+__global__ void __launch_bounds__(kThreads) k_cg_axpy(double* __restrict__ x, double* __restrict__ r, double* z,
+                                                      const double* __restrict__ inv, const double* __restrict__ p,
+                                                      const double* __restrict__ ap, int64_t n, KrylovScalars* sc,
+                                                      double* hist, double* slots, unsigned* ticket) {
+  if (sc->done) return;
+  __shared__ double sh[kWarps];
+  const double alpha = sc->alpha;
+  double rr = 0.0, rz = 0.0;
+  grid_stride(n, [&](int64_t i) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * ap[i];
+    r[i] = ri;
+    rr += ri * ri;
+    const double zi = inv != nullptr ? inv[i] * ri : ri;
+    if (inv != nullptr) z[i] = zi;
+    rz += ri * zi;
+  });
+  const double s0 = block_sum(rr, sh), s1 = block_sum(rz, sh);
+  if (threadIdx.x == 0) {
+    slots[blockIdx.x * 2] = s0;
+    slots[blockIdx.x * 2 + 1] = s1;
+  }
+  if (grid_last(ticket)) {
+    const double t0 = sum_slots(slots, gridDim.x, 2, 0, sh);
+    const double t1 = sum_slots(slots, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      const double rel = sqrt(t0) / sc->nb;
+      hist[sc->it] = rel;
+      sc->rel = rel;
+      sc->it += 1;
+      if (rel <= sc->tol) {
+        sc->converged = 1;
+        sc->done = 1;
+      } else {
+        sc->beta_cg = t1 / sc->rz;
+        sc->rz = t1;
+        if (sc->it >= sc->max_iters) sc->done = 1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_update_p(double* __restrict__ p, const double* __restrict__ z,
+                                                          int64_t n, const KrylovScalars* sc) {
+  if (sc->done) return;
+  const double b = sc->beta_cg;
+  grid_stride(n, [&](int64_t i) { p[i] = z[i] + b * p[i]; });
+}
+
+// ------------------------------------------------------------------ aggregation
+// r_c(s) = sum over members i of s, increasing i, of w_i r_i; zero r_i skipped
+// (coarsening.cpp:43-55 scatter order == this gather order, bit for bit).
+__global__ void __launch_bounds__(kThreads) k_restrict(const int32_t* __restrict__ mptr,
+                                                       const int32_t* __restrict__ members,
+                                                       const double* __restrict__ weight,
+                                                       const double* __restrict__ fine, double* __restrict__ coarse,
+                                                       int64_t nc, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(nc, [&](int64_t s) {
+    double acc = 0.0;
+    for (int q = mptr[s]; q < mptr[s + 1]; ++q) {
+      const int i = members[q];
+      const double fi = fine[i];
+      if (fi == 0.0) continue;
+      acc = __dadd_rn(acc, __dmul_rn(weight[i], fi));  // no contraction: bit-equal to the reference
+    }
+    coarse[s] = acc;
+  });
+}
+
+// z1_i = 0.0 + w_i e_c(label_i)   (coarsening.cpp:30-41)
+__global__ void __launch_bounds__(kThreads) k_prolong(const int32_t* __restrict__ label,
+                                                      const double* __restrict__ weight,
+                                                      const double* __restrict__ coarse, double* __restrict__ fine,
+                                                      int64_t nf, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(nf, [&](int64_t i) {
+    fine[i] = __dadd_rn(0.0, __dmul_rn(weight[i], coarse[label[i]]));
+  });
+}
+
+// y = A x, warp per row
+__global__ void __launch_bounds__(kThreads) k_dense_gemv(const double* __restrict__ a, const double* __restrict__ x,
+                                                         double* __restrict__ y, int64_t n, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t row = warp; row < n; row += nw) {
+    const double* ar = a + row * n;
+    double s = 0.0;
+    for (int64_t j = lane; j < n; j += 32) s += ar[j] * __ldg(x + j);
+    s = warp_sum(s);
+    if (lane == 0) y[row] = s;
+  }
+}
+
+__global__ void k_scale_by_lambda(const double* __restrict__ w, double* __restrict__ v, int64_t n,
+                                  const KrylovScalars* sc) {
+  const double lam = sc->lambda;
+  if (lam == 0.0) return;
+  grid_stride(n, [&](int64_t i) { v[i] = w[i] / lam; });
+}
+
+// d_j = beta + sum_r X(r,j)^2 in increasing r (ridge.cpp:30-37 storage order)
+template <bool PAT>
+__global__ void k_diag_gram(const int32_t* __restrict__ ptr, const double* __restrict__ val, int64_t f,
+                            double beta, double* __restrict__ out) {
+  grid_stride(f, [&](int64_t j) {
+    double d = beta;
+    for (int k = ptr[j]; k < ptr[j + 1]; ++k) {
+      const double x = PAT ? 1.0 : val[k];
+      d = __dadd_rn(d, __dmul_rn(x, x));  // uncontracted: bit-equal to ridge.cpp:34
+    }
+    out[j] = d;
+  });
+}
+
+__global__ void k_fill(double* p, double v, int64_t n) {
+  grid_stride(n, [&](int64_t i) { p[i] = v; });
+}
+
+__global__ void k_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer, uint64_t* hist) {
+  if (outer->done) return;
+  hist[outer->it] = (uint64_t)inner->it;
+}
+
+inline void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
+}
+
+int grid_for(int64_t work_threads, int cap) {
+  const int64_t g = (work_threads + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
+}
+
+template <int W, bool PAT>
+void spmv_rows_impl(const SparseDev& x, const double* v, double* t, const int32_t* done,
+                    const KrylovScalars* sc, int ring_stride, cudaStream_t s) {
+  const int grid = grid_for(x.rows * W, 148 * 16);
+  k_spmv_rows<W, PAT><<<grid, kThreads, 0, s>>>(x.ptr, x.idx, x.val, v, t, x.rows, done, sc, ring_stride);
+}
+
+template <bool PAT>
+void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* done, const KrylovScalars* sc,
+                 int ring_stride, cudaStream_t s) {
+  switch (x.width) {
+    case 4: spmv_rows_impl<4, PAT>(x, v, t, done, sc, ring_stride, s); break;
+    case 8: spmv_rows_impl<8, PAT>(x, v, t, done, sc, ring_stride, s); break;
+    case 16: spmv_rows_impl<16, PAT>(x, v, t, done, sc, ring_stride, s); break;
+    default: spmv_rows_impl<32, PAT>(x, v, t, done, sc, ring_stride, s); break;
+  }
+}
+
+template <int W, bool PAT>
+void xt_impl_w(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
+  const dim3 grid(sch.n_items), block(kThreads);
+  switch (epi) {
+    case Epi::Plain: k_xt<W, PAT, Epi::Plain><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Axpby: k_xt<W, PAT, Epi::Axpby><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Fcg: k_xt<W, PAT, Epi::Fcg><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Cg: k_xt<W, PAT, Epi::Cg><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Rich: k_xt<W, PAT, Epi::Rich><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Gram: k_xt<W, PAT, Epi::Gram><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+  }
+}
+
+template <bool PAT>
+void xt_impl(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
+  switch (sch.width) {
+    case 4: xt_impl_w<4, PAT>(xt, sch, epi, a, s); break;
+    case 8: xt_impl_w<8, PAT>(xt, sch, epi, a, s); break;
+    case 16: xt_impl_w<16, PAT>(xt, sch, epi, a, s); break;
+    default: xt_impl_w<32, PAT>(xt, sch, epi, a, s); break;
+  }
+}
+
+}  // namespace
+
+int vec_grid(int64_t n) { return grid_for((n + 3) / 4, 296); }
+
+void launch_spmv_rows(const SparseDev& x, const double* v, double* t, const int32_t* done, cudaStream_t s) {
+  if (x.rows == 0) return;
+  if (x.val == nullptr)
+    spmv_rows_w<true>(x, v, t, done, nullptr, 0, s);
+  else
+    spmv_rows_w<false>(x, v, t, done, nullptr, 0, s);
+  check_launch("spmv_rows");
+}
+
+void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_stride, const KrylovScalars* sc,
+                           double* t, cudaStream_t s) {
+  if (x.rows == 0) return;
+  if (x.val == nullptr)
+    spmv_rows_w<true>(x, v_ring, t, nullptr, sc, ring_stride, s);
+  else
+    spmv_rows_w<false>(x, v_ring, t, nullptr, sc, ring_stride, s);
+  check_launch("spmv_rows_ring");
+}
+
+void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
+  if (sch.n_items == 0) return;
+  if (xt.val == nullptr)
+    xt_impl<true>(xt, sch, epi, a, s);
+  else
+    xt_impl<false>(xt, sch, epi, a, s);
+  check_launch("xt");
+}
+
+void launch_krylov_begin(const double* b, double* x, double* r, int64_t n, KrylovScalars* sc, double* hist,
+                         const VecWork& w, cudaStream_t s) {
+  k_krylov_begin<<<w.grid, kThreads, 0, s>>>(b, x, r, n, sc, hist, w.slots, w.ticket);
+  check_launch("krylov_begin");
+}
+
+void launch_fcg_gs(const double* z, const double* ap_ring, double* p_ring, int64_t n, KrylovScalars* sc,
+                   const VecWork& w, cudaStream_t s) {
+  k_fcg_gs_dots<<<w.grid, kThreads, 0, s>>>(z, ap_ring, n, sc, w.slots, w.ticket);
+  k_fcg_update_p<<<w.grid, kThreads, 0, s>>>(z, p_ring, n, sc);
+  check_launch("fcg_gs");
+}
+
+void launch_fcg_axpy(double* x, double* r, const double* p_ring, const double* ap_ring, int64_t n,
+                     KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s) {
+  k_fcg_axpy<<<w.grid, kThreads, 0, s>>>(x, r, p_ring, ap_ring, n, sc, hist, w.slots, w.ticket);
+  check_launch("fcg_axpy");
+}
+
+void launch_cg_begin(const double* b, const double* inv_diag, double* x, double* r, double* z, double* p, int64_t n,
+                     KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s) {
+  k_cg_begin<<<w.grid, kThreads, 0, s>>>(b, inv_diag, x, r, z, p, n, sc, hist, w.slots, w.ticket);
+  check_launch("cg_begin");
+}
+
+void launch_cg_axpy(double* x, double* r, double* z, const double* inv_diag, const double* p, const double* ap,
+                    int64_t n, KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s) {
+  k_cg_axpy<<<w.grid, kThreads, 0, s>>>(x, r, z, inv_diag, p, ap, n, sc, hist, w.slots, w.ticket);
+  check_launch("cg_axpy");
+}
+
+void launch_cg_update_p(double* p, const double* z, int64_t n, const KrylovScalars* sc, cudaStream_t s) {
+  k_cg_update_p<<<vec_grid(n), kThreads, 0, s>>>(p, z, n, sc);
+  check_launch("cg_update_p");
+}
+
+void launch_restrict(const int32_t* mptr, const int32_t* members, const double* weight, const double* fine,
+                     double* coarse, int64_t n_coarse, const int32_t* done, cudaStream_t s) {
+  k_restrict<<<grid_for(n_coarse, 148 * 4), kThreads, 0, s>>>(mptr, members, weight, fine, coarse, n_coarse, done);
+  check_launch("restrict");
+}
+
+void launch_prolong(const int32_t* label, const double* weight, const double* coarse, double* fine, int64_t n_fine,
+                    const int32_t* done, cudaStream_t s) {
+  k_prolong<<<vec_grid(n_fine), kThreads, 0, s>>>(label, weight, coarse, fine, n_fine, done);
+  check_launch("prolong");
+}
+
+void launch_dense_gemv(const double* a, const double* x, double* y, int64_t n, const int32_t* done, cudaStream_t s) {
+  k_dense_gemv<<<grid_for(n * 32, 148 * 8), kThreads, 0, s>>>(a, x, y, n, done);
+  check_launch("dense_gemv");
+}
+
+void launch_scale_by_lambda(const double* w, double* v, int64_t n, const KrylovScalars* sc, cudaStream_t s) {
+  k_scale_by_lambda<<<vec_grid(n), kThreads, 0, s>>>(w, v, n, sc);
+  check_launch("scale_by_lambda");
+}
+
+void launch_diag_gram(const SparseDev& xt, double beta, double* out, cudaStream_t s) {
+  if (xt.val == nullptr)
+    k_diag_gram<true><<<grid_for(xt.rows, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, xt.rows, beta, out);
+  else
+    k_diag_gram<false><<<grid_for(xt.rows, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, xt.rows, beta, out);
+  check_launch("diag_gram");
+}
+
+void launch_fill(double* p, double v, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  k_fill<<<vec_grid(n), kThreads, 0, s>>>(p, v, n);
+  check_launch("fill");
+}
+
+void launch_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer, uint64_t* inner_hist,
+                             cudaStream_t s) {
+  k_copy_inner_count<<<1, 1, 0, s>>>(inner, outer, inner_hist);
+  check_launch("copy_inner_count");
+}
+
+}  // namespace rmg

@@ -1,0 +1,141 @@
+// Device kernels of the ridgemg_b200 solve path (sm_100a).
+//
+// Layout in HBM:
+//   X    : CSR over samples  (ptr int32[N+1], idx int32[nnz], val fp64[nnz] or none)
+//   X^T  : CSR over features (ptr int32[F+1], idx int32[nnz], val fp64[nnz] or none),
+//          plus an nnz-balanced work-item schedule (Xt_Schedule) that splits
+//          Zipf-heavy feature columns into fixed segments.
+//   all vectors fp64, Krylov history as two contiguous rings [(m+1) x F].
+// Every reduction is fixed-order (per-block tree + last-block sequential
+// combine over slots), so results are run-to-run bit reproducible.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rmg {
+
+// Per-solve device scalars (one instance per Krylov solver / level).
+struct KrylovScalars {
+  double nb;        // ||rhs||
+  double alpha;     // step length
+  double pap;       // <p, Ap> of the current iteration
+  double pr;        // <p, r>
+  double rz;        // CG: <r, z>
+  double beta_cg;   // CG: rz_next / rz
+  double rel;       // ||r|| / ||rhs|| after the last iteration
+  double tol;
+  double lambda;    // power iteration
+  int32_t it;       // iterations completed
+  int32_t max_iters;
+  int32_t done;     // 1 -> every kernel of this solver is a no-op
+  int32_t converged;
+  int32_t status;   // 0 ok, 1 <p,Ap> == 0, 2 <p,Ap> < 0 (or !>0 for CG), 3 non-finite rhs
+  int32_t keep;     // FCG truncation m (ring has keep+1 slots)
+  int32_t use;      // FCG: directions orthogonalized against in this iteration
+  int32_t pad;
+  double coeff[32]; // FCG Gram-Schmidt coefficients, oldest -> newest
+  double pap_ring[33];
+};
+
+enum : int { kMaxKeep = 31 };
+
+// Value storage of a sparse orientation.
+enum class Val : int { Pattern = 0, F64 = 1 };
+
+struct SparseDev {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  const int32_t* ptr = nullptr;
+  const int32_t* idx = nullptr;
+  const double* val = nullptr;  // nullptr -> binary pattern
+  int width = 8;                // lanes per row (4, 8, 16, 32)
+};
+
+// Work items for the X^T pass.  Short item: a contiguous range of feature
+// columns whose total nnz fits one CTA; long item: one fixed segment of a
+// feature column that is longer than that.
+struct XtSchedule {
+  const int4* items = nullptr;  // short: {col_begin, col_end, -1, slot}
+                                // long : {long_id, nz_begin, nz_end, seg_id}
+  int n_items = 0;
+  const int32_t* long_col = nullptr;
+  const int32_t* long_first_seg = nullptr;
+  const int32_t* long_nseg = nullptr;
+  const int32_t* long_slot = nullptr;
+  int n_long = 0, n_segs = 0, n_slots = 0;
+  double* seg_partial = nullptr;  // [n_segs]
+  unsigned* col_ticket = nullptr; // [n_long]
+  double* slots = nullptr;        // [n_slots * 2]
+  unsigned* grid_ticket = nullptr;
+  int width = 8;                  // lanes per short column
+};
+
+// Epilogue of the X^T pass, s_j = sum_r X(r,j) t_r:
+enum class Epi : int {
+  Plain = 0,   // out_j = s_j                                  (spmv_transpose)
+  Axpby = 1,   // out_j = s_j + beta v_j                       (ridge / Galerkin apply)
+  Fcg = 2,     // out_j = s_j + beta p_j; <p,Ap>, <p,r> -> alpha  (krylov.cpp:199-208)
+  Cg = 3,      // out_j = s_j + beta p_j; <p,Ap> -> alpha = rz/pap (krylov.cpp:126-134)
+  Rich = 4,    // out_j = z1_j + omega (r_j - (s_j + beta z1_j))   (krylov.cpp:417-418)
+  Gram = 5     // out_j = s_j; ||out||^2 -> lambda               (krylov.cpp:80-81)
+};
+
+struct XtArgs {
+  const double* t = nullptr;   // gathered N-vector
+  const double* v = nullptr;   // p / z1 / w (beta term)
+  const double* r = nullptr;   // residual (Fcg dots, Rich)
+  double* out = nullptr;
+  double beta = 0.0, omega = 0.0;
+  KrylovScalars* sc = nullptr; // Fcg / Cg / Gram finalization
+  const int32_t* done = nullptr;
+  int ring_stride = 0;         // Fcg/Cg: v/out are ring bases, offset by (it % (keep+1)) * stride
+};
+
+// ---------------------------------------------------------------- launchers
+void launch_spmv_rows(const SparseDev& x, const double* v, double* t, const int32_t* done,
+                      cudaStream_t s);
+void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_stride,
+                           const KrylovScalars* sc, double* t, cudaStream_t s);
+void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a,
+               cudaStream_t s);
+
+// Krylov vector work (all read their dynamic scalars from KrylovScalars)
+struct VecWork {
+  double* slots = nullptr;     // [grid * 32]
+  unsigned* ticket = nullptr;
+  int grid = 1;
+};
+int vec_grid(int64_t n);
+void launch_krylov_begin(const double* b, double* x, double* r, int64_t n, KrylovScalars* sc,
+                         double* hist, const VecWork& w, cudaStream_t s);
+void launch_fcg_gs(const double* z, const double* ap_ring, double* p_ring, int64_t n,
+                   KrylovScalars* sc, const VecWork& w, cudaStream_t s);
+void launch_fcg_axpy(double* x, double* r, const double* p_ring, const double* ap_ring, int64_t n,
+                     KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s);
+void launch_cg_begin(const double* b, const double* inv_diag, double* x, double* r, double* z,
+                     double* p, int64_t n, KrylovScalars* sc, double* hist, const VecWork& w,
+                     cudaStream_t s);
+void launch_cg_axpy(double* x, double* r, double* z, const double* inv_diag, const double* p,
+                    const double* ap, int64_t n, KrylovScalars* sc, double* hist,
+                    const VecWork& w, cudaStream_t s);
+void launch_cg_update_p(double* p, const double* z, int64_t n, const KrylovScalars* sc,
+                        cudaStream_t s);
+
+// Aggregation (adjusted average, coarsening.cpp:30-55,82-100)
+void launch_restrict(const int32_t* mptr, const int32_t* members, const double* weight,
+                     const double* fine, double* coarse, int64_t n_coarse, const int32_t* done,
+                     cudaStream_t s);
+void launch_prolong(const int32_t* label, const double* weight, const double* coarse,
+                    double* fine, int64_t n_fine, const int32_t* done, cudaStream_t s);
+// dense y = A x (row-major n x n), coarsest direct solve through A_c^{-1}
+void launch_dense_gemv(const double* a, const double* x, double* y, int64_t n,
+                       const int32_t* done, cudaStream_t s);
+// out = v / nrm (power iteration renormalization, krylov.cpp:84)
+void launch_scale_by_lambda(const double* w, double* v, int64_t n, const KrylovScalars* sc,
+                            cudaStream_t s);
+void launch_diag_gram(const SparseDev& xt, double beta, double* out, cudaStream_t s);
+void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
+void launch_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer,
+                             uint64_t* inner_hist, cudaStream_t s);
+
+}  // namespace rmg

@@ -1,0 +1,592 @@
+// Host orchestration of the ridgemg_b200 solve path.  See runtime.cuh.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "runtime.cuh"
+
+namespace rmg {
+
+// ------------------------------------------------------------------ Context
+Context::Context(int dev) : device(dev) {
+  int n = 0;
+  RMG_CK(cudaGetDeviceCount(&n));
+  if (dev < 0 || dev >= n) throw InvalidArgument("rmg_context_create: device " + std::to_string(dev) + " not present");
+  RMG_CK(cudaSetDevice(dev));
+  RMG_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  own_stream = true;
+  RMG_CK(cudaMallocHost(&pinned_sc, sizeof(KrylovScalars)));
+}
+
+Context::~Context() {
+  if (pinned_sc) cudaFreeHost(pinned_sc);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void Context::sync() { RMG_CK(cudaStreamSynchronize(stream)); }
+
+KrylovScalars Context::read(const KrylovScalars* dev) {
+  RMG_CK(cudaMemcpyAsync(pinned_sc, dev, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, stream));
+  RMG_CK(cudaStreamSynchronize(stream));
+  return *pinned_sc;
+}
+
+// ------------------------------------------------------------------ sparse upload
+namespace {
+
+int lanes_for(double avg) {
+  if (avg <= 6.0) return 4;
+  if (avg <= 24.0) return 8;
+  if (avg <= 96.0) return 16;
+  return 32;
+}
+
+std::vector<int32_t> narrow(const std::vector<int64_t>& v, const char* what) {
+  std::vector<int32_t> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (v[i] < 0 || v[i] > INT32_MAX) throw InvalidArgument(std::string(what) + " exceeds the int32 device index range");
+    o[i] = static_cast<int32_t>(v[i]);
+  }
+  return o;
+}
+
+}  // namespace
+
+void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s) {
+  const auto p32 = narrow(h.ptr, "row offsets");
+  const auto i32 = narrow(h.idx, "column indices");
+  ptr.upload(p32.data(), p32.size(), s);
+  idx.upload(i32.data(), i32.size(), s);
+  if (!pattern) val.upload(h.val.data(), h.val.size(), s);
+  RMG_CK(cudaStreamSynchronize(s));
+  view.rows = h.n;
+  view.cols = h.f;
+  view.nnz = h.nnz();
+  view.ptr = ptr.get();
+  view.idx = idx.get();
+  view.val = pattern ? nullptr : val.get();
+  view.width = lanes_for(h.n ? static_cast<double>(h.nnz()) / static_cast<double>(h.n) : 1.0);
+}
+
+// nnz-balanced work items over the rows of X^T (= feature columns of X).
+void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s) {
+  const int64_t F = xt.n, nnz = xt.nnz();
+  const int64_t C = std::max<int64_t>(256, std::min<int64_t>(16384, nnz / (148 * 4)));
+  std::vector<int4> it;
+  std::vector<int32_t> lcol, lfirst, lnseg, lslot;
+  std::vector<int64_t> short_lens;
+  int slot = 0, segs = 0;
+  int64_t cs = 0, acc = 0;
+  auto flush = [&](int64_t end) {
+    if (cs < end) it.push_back(make_int4((int)cs, (int)end, -1, slot++));
+    cs = end;
+    acc = 0;
+  };
+  for (int64_t j = 0; j < F; ++j) {
+    const int64_t len = xt.ptr[j + 1] - xt.ptr[j];
+    if (len > C) {
+      flush(j);
+      const int id = static_cast<int>(lcol.size());
+      const int nseg = static_cast<int>((len + C - 1) / C);
+      lcol.push_back((int)j);
+      lfirst.push_back(segs);
+      lnseg.push_back(nseg);
+      lslot.push_back(slot++);
+      for (int q = 0; q < nseg; ++q) {
+        const int64_t b = xt.ptr[j] + q * C, e = std::min<int64_t>(xt.ptr[j + 1], b + C);
+        it.push_back(make_int4(id, (int)b, (int)e, segs++));
+      }
+      cs = j + 1;
+    } else {
+      if ((acc + len > C || j - cs >= 4096) && cs < j) flush(j);
+      acc += len;
+      short_lens.push_back(len);
+    }
+  }
+  flush(F);
+  int width = 8;
+  if (!short_lens.empty()) {
+    std::nth_element(short_lens.begin(), short_lens.begin() + short_lens.size() / 2, short_lens.end());
+    width = lanes_for(static_cast<double>(short_lens[short_lens.size() / 2]));
+  }
+  items.upload(it.data(), it.size(), s);
+  long_col.upload(lcol.data(), lcol.size(), s);
+  long_first.upload(lfirst.data(), lfirst.size(), s);
+  long_nseg.upload(lnseg.data(), lnseg.size(), s);
+  long_slot.upload(lslot.data(), lslot.size(), s);
+  seg_partial.alloc(std::max(1, segs));
+  slots.alloc(std::max(1, slot) * 2);
+  col_ticket.alloc(std::max<size_t>(1, lcol.size()));
+  grid_ticket.alloc(1);
+  RMG_CK(cudaMemsetAsync(col_ticket.get(), 0, col_ticket.size() * sizeof(unsigned), s));
+  RMG_CK(cudaMemsetAsync(grid_ticket.get(), 0, sizeof(unsigned), s));
+  RMG_CK(cudaStreamSynchronize(s));
+  view.items = items.get();
+  view.n_items = static_cast<int>(it.size());
+  view.long_col = long_col.get();
+  view.long_first_seg = long_first.get();
+  view.long_nseg = long_nseg.get();
+  view.long_slot = long_slot.get();
+  view.n_long = static_cast<int>(lcol.size());
+  view.n_segs = segs;
+  view.n_slots = slot;
+  view.seg_partial = seg_partial.get();
+  view.col_ticket = col_ticket.get();
+  view.slots = slots.get();
+  view.grid_ticket = grid_ticket.get();
+  view.width = width;
+}
+
+// ------------------------------------------------------------------ Matrix
+Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern) : ctx(c), host(std::move(h)) {
+  validate_csr(host);
+  if (host.n > INT32_MAX || host.f > INT32_MAX || host.nnz() > INT32_MAX)
+    throw InvalidArgument("FeatureMatrix: dimensions exceed the single-device int32 index range");
+  pattern = host.val.empty();
+  if (!pattern && detect_pattern)
+    pattern = std::all_of(host.val.begin(), host.val.end(), [](double v) { return v == 1.0; });
+  if (host.val.empty()) host.val.assign(host.nnz(), 1.0);
+  RMG_CK(cudaSetDevice(ctx->device));
+  x.upload(host, pattern, ctx->stream);
+  const HostCsr ht = transpose(host);
+  xt.upload(ht, pattern, ctx->stream);
+  sched.build(ht, ctx->stream);
+  t.alloc(std::max<int64_t>(1, host.n));
+  gram_sc.alloc(1);
+}
+
+void Matrix::apply(const double* v, Epi epi, const XtArgs& args) {
+  launch_spmv_rows(x.view, v, t.get(), args.done, ctx->stream);
+  XtArgs a = args;
+  a.t = t.get();
+  launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  ctx->launches += 2;
+}
+
+void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args) {
+  launch_spmv_rows_ring(x.view, v_ring, stride, sc, t.get(), ctx->stream);
+  XtArgs a = args;
+  a.t = t.get();
+  launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  ctx->launches += 2;
+}
+
+void Matrix::spmv(const double* v, double* y) {
+  launch_spmv_rows(x.view, v, y, nullptr, ctx->stream);
+  ctx->launches += 1;
+}
+
+void Matrix::spmv_t(const double* u, double* y) {
+  XtArgs a;
+  a.t = u;
+  a.out = y;
+  launch_xt(xt.view, sched.view, Epi::Plain, a, ctx->stream);
+  ctx->launches += 1;
+}
+
+// estimate_lambda_max (krylov.cpp:62-92) with the Gram operator on the device
+double Matrix::lambda_max(double tol, uint64_t max_iters, uint64_t seed, uint64_t* iters, bool* conv) {
+  const int64_t nf = f();
+  std::vector<double> v(nf);
+  CounterRng rng(seed);
+  for (auto& e : v) e = rng.next_normal();
+  double nv = 0.0;
+  for (double e : v) nv += e * e;
+  nv = std::sqrt(nv);
+  if (nv == 0.0) nv = 1.0;
+  for (auto& e : v) e /= nv;
+  DBuf<double> dv, dw(std::max<int64_t>(1, nf));
+  dv.upload(v.data(), v.size(), ctx->stream);
+  double prev = 0.0, lam = 0.0;
+  *conv = false;
+  *iters = 0;
+  for (uint64_t it = 0; it < max_iters; ++it) {
+    XtArgs a;
+    a.v = dv.get();
+    a.out = dw.get();
+    a.sc = gram_sc.get();
+    apply(dv.get(), Epi::Gram, a);
+    lam = ctx->read(gram_sc.get()).lambda;
+    *iters = it + 1;
+    if (lam == 0.0) {
+      *conv = true;
+      return lam;
+    }
+    launch_scale_by_lambda(dw.get(), dv.get(), nf, gram_sc.get(), ctx->stream);
+    ctx->launches += 1;
+    if (it > 0 && std::abs(lam - prev) <= tol * lam) {
+      *conv = true;
+      return lam;
+    }
+    prev = lam;
+  }
+  return lam;
+}
+
+// ------------------------------------------------------------------ Krylov workspace
+KrylovWork::KrylovWork(int64_t n_, int keep_, uint64_t max_iters_, double tol, cudaStream_t s) : n(n_), keep(keep_) {
+  if (keep > kMaxKeep) throw InvalidArgument("truncation above the supported maximum of " + std::to_string(kMaxKeep));
+  const size_t m = std::max<int64_t>(1, n);
+  b.alloc(m);
+  x.alloc(m);
+  r.alloc(m);
+  z.alloc(m);
+  z1.alloc(m);
+  p_ring.alloc(m * (keep + 1));
+  ap_ring.alloc(m * (keep + 1));
+  vw.grid = vec_grid(n);
+  slots.alloc(static_cast<size_t>(vw.grid) * 32);
+  ticket.alloc(1);
+  RMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
+  vw.slots = slots.get();
+  vw.ticket = ticket.get();
+  sc.alloc(1);
+  set_params(tol, max_iters_, keep, s);
+}
+
+void KrylovWork::set_params(double tol, uint64_t max_iters_, int keep_m, cudaStream_t s) {
+  max_iters = max_iters_;
+  hist.alloc(max_iters + 1);
+  inner_hist.alloc(max_iters + 1);
+  KrylovScalars h;
+  std::memset(&h, 0, sizeof(h));
+  h.tol = tol;
+  h.max_iters = static_cast<int32_t>(std::min<uint64_t>(max_iters, INT32_MAX));
+  h.keep = keep_m;
+  h.done = 1;
+  RMG_CK(cudaMemcpyAsync(sc.get(), &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  RMG_CK(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ Method
+namespace {
+
+std::vector<int64_t> run_clustering(const HostCsr& cur, const LevelSpecHost& ls, int64_t* nc) {
+  const rmg_level_spec& s = ls.spec;
+  if (s.clustering_kind == RMG_CLUSTER_IMPORTED) {
+    if (static_cast<int64_t>(ls.labels.size()) != cur.f)
+      throw InvalidArgument("imported labels: expected one label per feature of the level");
+    *nc = static_cast<int64_t>(s.n_clusters);
+    return ls.labels;
+  }
+  const HostCsr src = s.normalize_columns ? normalized_columns(cur) : cur;
+  const HostCsr cols = transpose(src);
+  const unsigned threads = std::max(1u, std::thread::hardware_concurrency());
+  Clustering c;
+  switch (s.clustering_kind) {
+    case RMG_CLUSTER_LEADER_TOLERANCE: c = leader_follower(cols, s.tolerance); break;
+    case RMG_CLUSTER_LEADER_TARGET: c = leader_follower_target(cols, static_cast<int64_t>(s.target_size)); break;
+    case RMG_CLUSTER_KMEANS:
+      c = kmeans(cols, static_cast<int64_t>(s.target_size), s.kmeans_max_iters, s.seed, threads);
+      break;
+    default: throw InvalidArgument("unknown clustering kind " + std::to_string(s.clustering_kind));
+  }
+  *nc = c.n_clusters;
+  return c.labels;
+}
+
+}  // namespace
+
+Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, uint64_t n_levels,
+               const rmg_solver_config& sol)
+    : solver(sol), ctx_(x->ctx), fine_(x), beta_(beta), kind_(kind) {
+  if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
+  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_FCG_MULTILEVEL)
+    throw InvalidArgument("unknown method kind " + std::to_string(kind));
+  if (solver.max_iters > static_cast<uint64_t>(INT32_MAX)) throw InvalidArgument("max_iters too large");
+  const int keep0 = static_cast<int>(std::max<uint64_t>(solver.truncation, 1));
+  RMG_CK(cudaSetDevice(ctx_->device));
+  cudaStream_t s = ctx_->stream;
+
+  if (kind == RMG_METHOD_CG || kind == RMG_METHOD_JACOBI_CG) {
+    work_.push_back(std::make_unique<KrylovWork>(x->f(), 1, solver.max_iters, solver.tol, s));
+    if (kind == RMG_METHOD_JACOBI_CG) {  // krylov.cpp:623-626, 41-47
+      DBuf<double> d(std::max<int64_t>(1, x->f()));
+      launch_diag_gram(x->xt.view, beta, d.get(), s);
+      std::vector<double> h(x->f());
+      if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), d.get(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+      ctx_->sync();
+      for (double& v : h) {
+        if (!(v > 0.0)) throw InvalidArgument("JacobiPreconditioner: diagonal must be positive");
+        v = 1.0 / v;
+      }
+      inv_diag_.upload(h.data(), h.size(), s);
+      ctx_->sync();
+    }
+    return;
+  }
+
+  if (n_levels == 0 || levels == nullptr)
+    throw InvalidArgument(kind == RMG_METHOD_FCG_TWOLEVEL ? "two-level method requires one level spec"
+                                                          : "multilevel method requires level specs");
+  const uint64_t L = kind == RMG_METHOD_FCG_TWOLEVEL ? 1 : n_levels;
+  if (L > RMG_MAX_LEVELS) throw InvalidArgument("too many levels");
+  for (uint64_t k = 0; k < L; ++k) {
+    LevelSpecHost ls;
+    ls.spec = levels[k];
+    if (ls.spec.clustering_kind == RMG_CLUSTER_IMPORTED) {
+      if (ls.spec.labels == nullptr) throw InvalidArgument("imported clustering without labels");
+      const int64_t f = k == 0 ? x->f() : -1;  // sizes of deeper levels are checked when reached
+      (void)f;
+    }
+    ls.spec.labels = nullptr;
+    specs_.push_back(ls);
+  }
+  if (kind == RMG_METHOD_FCG_TWOLEVEL) specs_[0].spec.coarse_kind = RMG_COARSE_DIRECT_CHOLESKY;  // krylov.cpp:632-634
+  // krylov.cpp:495-505
+  for (uint64_t k = 0; k + 1 < L; ++k)
+    if (specs_[k].spec.coarse_kind == RMG_COARSE_DIRECT_CHOLESKY)
+      throw InvalidArgument("build_hierarchy: only the last level may use direct_cholesky");
+  if (specs_[L - 1].spec.coarse_kind != RMG_COARSE_DIRECT_CHOLESKY)
+    throw InvalidArgument("build_hierarchy: the coarsest level must use direct_cholesky");
+
+  // levels (krylov.cpp:512-530)
+  double beta_run = beta;
+  for (uint64_t k = 0; k < L; ++k) {
+    const HostCsr& cur = level_matrix(k).host;
+    if (levels[k].clustering_kind == RMG_CLUSTER_IMPORTED)
+      specs_[k].labels.assign(levels[k].labels, levels[k].labels + cur.f);
+    const double next_beta = specs_[k].spec.has_beta_override ? specs_[k].spec.beta_override : beta_run;
+    int64_t nc = 0;
+    std::vector<int64_t> lab = run_clustering(cur, specs_[k], &nc);
+    if (nc >= cur.f)
+      throw InvalidArgument("build_hierarchy: level " + std::to_string(k + 1) + " has " + std::to_string(nc) +
+                            " clusters, not smaller than its fine level (" + std::to_string(cur.f) + " features)");
+    auto lvl = std::make_unique<CoarseLevelDev>();
+    lvl->agg = make_aggregation(lab, nc);
+    lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(cur, lvl->agg), true);
+    lvl->beta = next_beta;
+    lvl->label.upload(lvl->agg.label.data(), lvl->agg.label.size(), s);
+    lvl->weight.upload(lvl->agg.weight.data(), lvl->agg.weight.size(), s);
+    lvl->mptr.upload(lvl->agg.mptr.data(), lvl->agg.mptr.size(), s);
+    lvl->members.upload(lvl->agg.members.data(), lvl->agg.members.size(), s);
+    labels_.push_back(std::move(lab));
+    coarse_.push_back(std::move(lvl));
+    beta_run = next_beta;
+  }
+  const int64_t fc_last = coarse_.back()->mat->f();
+  if (fc_last > 4096)  // kDirectSolveCap, krylov.hpp:170
+    throw InvalidArgument("build_hierarchy: coarsest level has " + std::to_string(fc_last) +
+                          " features, above the direct-solve cap 4096");
+  // omega_k = 2 / (beta_k + lambda_max(X_k^T X_k)) (krylov.cpp:539-546)
+  for (uint64_t k = 0; k < L; ++k) {
+    if (specs_[k].spec.has_omega_override) {
+      if (!(specs_[k].spec.omega_override > 0.0))
+        throw InvalidArgument("TwoLevelPreconditioner: omega must be positive");
+      omega_.push_back(specs_[k].spec.omega_override);
+      continue;
+    }
+    uint64_t its;
+    bool cv;
+    const double lmax = level_matrix(k).lambda_max(1e-4, 200, 0x5eed + k, &its, &cv);
+    omega_.push_back(2.0 / (level_beta(k) + lmax));
+  }
+  // coarsest dense solve (krylov.cpp:349-376), through A_c^{-1}
+  {
+    const std::vector<double> ac = coarse_gram(coarse_.back()->mat->host, coarse_.back()->beta);
+    const std::vector<double> inv =
+        spd_inverse(ac, fc_last, "level " + std::to_string(L - 1) + " -> " + std::to_string(L));
+    ainv_.upload(inv.data(), inv.size(), s);
+    rc_last_.alloc(std::max<int64_t>(1, fc_last));
+    ec_last_.alloc(std::max<int64_t>(1, fc_last));
+  }
+  // workspaces: level 0 = outer FCG, level k >= 1 = inner solve configured by spec k-1
+  work_.push_back(std::make_unique<KrylovWork>(x->f(), keep0, solver.max_iters, solver.tol, s));
+  for (uint64_t k = 1; k < L; ++k) {
+    const rmg_level_spec& sp = specs_[k - 1].spec;
+    const int keep = static_cast<int>(std::max<uint64_t>(sp.coarse_truncation, 1));
+    work_.push_back(std::make_unique<KrylovWork>(level_matrix(k).f(), keep, sp.coarse_max_iters, sp.coarse_tol, s));
+  }
+  ctx_->sync();
+}
+
+const std::vector<int64_t>& Method::labels(size_t k) const {
+  if (k >= labels_.size()) throw InvalidArgument("level index out of range");
+  return labels_[k];
+}
+
+// TwoLevelPreconditioner::apply (krylov.cpp:379-420)
+uint64_t Method::precond(size_t k, const double* r, double* z) {
+  CoarseLevelDev& c = *coarse_[k];
+  const size_t L = coarse_.size();
+  const int64_t nc = c.mat->f(), nf = level_matrix(k).f();
+  cudaStream_t s = ctx_->stream;
+  double* rc = (k + 1 == L) ? rc_last_.get() : work_[k + 1]->b.get();
+  launch_restrict(c.mptr.get(), c.members.get(), c.weight.get(), r, rc, nc, nullptr, s);
+  const double* ec;
+  uint64_t inner = 0;
+  if (k + 1 == L) {
+    launch_dense_gemv(ainv_.get(), rc, ec_last_.get(), nc, nullptr, s);
+    ec = ec_last_.get();
+    ctx_->launches += 2;
+  } else {
+    ctx_->launches += 1;
+    inner = specs_[k].spec.coarse_kind == RMG_COARSE_INNER_FCG ? run_fcg(k + 1, rc, false, nullptr)
+                                                                : run_cg(k + 1, rc, nullptr, false, nullptr);
+    ec = work_[k + 1]->x.get();
+  }
+  double* z1 = work_[k]->z1.get();
+  launch_prolong(c.label.get(), c.weight.get(), ec, z1, nf, nullptr, s);
+  ctx_->launches += 1;
+  XtArgs a;
+  a.v = z1;
+  a.r = r;
+  a.out = z;
+  a.beta = level_beta(k);
+  a.omega = omega_[k];
+  level_matrix(k).apply(z1, Epi::Rich, a);
+  return inner;
+}
+
+namespace {
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+void record(Context* ctx, KrylovWork& w, const KrylovScalars& hs, const std::vector<uint64_t>& inner,
+            Clock::time_point t0, SolveResult* out) {
+  out->wall = secs(t0);
+  out->iterations = static_cast<uint64_t>(hs.it);
+  out->converged = hs.converged != 0;
+  out->final_rel = hs.rel;
+  const size_t nh = hs.it == 0 && hs.converged ? 1 : static_cast<size_t>(hs.it);
+  out->hist.resize(nh);
+  if (nh) RMG_CK(cudaMemcpyAsync(out->hist.data(), w.hist.get(), nh * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  out->inner = inner;
+}
+}  // namespace
+
+// fcg (krylov.cpp:159-227) at level k with the level-k preconditioner
+uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out) {
+  KrylovWork& w = *work_[k];
+  Matrix& m = level_matrix(k);
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  const auto t0 = Clock::now();
+  launch_krylov_begin(rhs, w.x.get(), w.r.get(), n, w.sc.get(), w.hist.get(), w.vw, s);
+  ctx_->launches += 1;
+  KrylovScalars hs = ctx_->read(w.sc.get());
+  if (hs.status == 3) throw InvalidArgument("fcg: non-finite rhs");
+  std::vector<uint64_t> inner;
+  while (!hs.done) {
+    const uint64_t in = precond(k, w.r.get(), w.z.get());
+    launch_fcg_gs(w.z.get(), w.ap_ring.get(), w.p_ring.get(), n, w.sc.get(), w.vw, s);
+    XtArgs a;
+    a.v = w.p_ring.get();
+    a.r = w.r.get();
+    a.out = w.ap_ring.get();
+    a.beta = level_beta(k);
+    a.sc = w.sc.get();
+    a.ring_stride = static_cast<int>(n);
+    m.apply_ring(w.p_ring.get(), static_cast<int>(n), w.sc.get(), Epi::Fcg, a);
+    launch_fcg_axpy(w.x.get(), w.r.get(), w.p_ring.get(), w.ap_ring.get(), n, w.sc.get(), w.hist.get(), w.vw, s);
+    ctx_->launches += 3;
+    hs = ctx_->read(w.sc.get());
+    if (rec) inner.push_back(in);
+    if (hs.status == 1) throw RuntimeError("fcg: breakdown, <p, Ap> = 0 at iteration " + std::to_string(hs.it));
+    if (hs.status == 2)
+      throw RuntimeError("fcg: <p, Ap> < 0 at iteration " + std::to_string(hs.it) +
+                         "; operator is not positive definite");
+  }
+  if (rec) record(ctx_, w, hs, inner, t0, out);
+  return static_cast<uint64_t>(hs.it);
+}
+
+// cg (krylov.cpp:94-157), optionally Jacobi-preconditioned
+uint64_t Method::run_cg(size_t k, const double* rhs, const double* inv, bool rec, SolveResult* out) {
+  KrylovWork& w = *work_[k];
+  Matrix& m = level_matrix(k);
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  double* p = w.p_ring.get();
+  double* ap = w.ap_ring.get();
+  double* z = inv ? w.z.get() : w.r.get();
+  const auto t0 = Clock::now();
+  launch_cg_begin(rhs, inv, w.x.get(), w.r.get(), w.z.get(), p, n, w.sc.get(), w.hist.get(), w.vw, s);
+  ctx_->launches += 1;
+  KrylovScalars hs = ctx_->read(w.sc.get());
+  if (hs.status == 3) throw InvalidArgument("cg: non-finite rhs");
+  while (!hs.done) {
+    XtArgs a;
+    a.v = p;
+    a.out = ap;
+    a.beta = level_beta(k);
+    a.sc = w.sc.get();
+    m.apply(p, Epi::Cg, a);
+    launch_cg_axpy(w.x.get(), w.r.get(), w.z.get(), inv, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s);
+    launch_cg_update_p(p, z, n, w.sc.get(), s);
+    ctx_->launches += 2;
+    hs = ctx_->read(w.sc.get());
+    if (hs.status == 2)
+      throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
+                         "; operator is not positive definite");
+  }
+  if (rec) record(ctx_, w, hs, {}, t0, out);
+  return static_cast<uint64_t>(hs.it);
+}
+
+SolveResult Method::solve_rhs(const double* rhs, double* w_out) {
+  RMG_CK(cudaSetDevice(ctx_->device));
+  SolveResult res;
+  if (kind_ == RMG_METHOD_CG)
+    run_cg(0, rhs, nullptr, true, &res);
+  else if (kind_ == RMG_METHOD_JACOBI_CG)
+    run_cg(0, rhs, inv_diag_.get(), true, &res);
+  else
+    run_fcg(0, rhs, true, &res);
+  const int64_t n = fine_->f();
+  if (n) RMG_CK(cudaMemcpyAsync(w_out, work_[0]->x.get(), n * 8, cudaMemcpyDeviceToDevice, ctx_->stream));
+  return res;
+}
+
+void Method::precondition(const double* r, double* z) {
+  if (coarse_.empty()) throw InvalidArgument("precondition: method has no hierarchy");
+  precond(0, r, z);
+}
+
+double Method::time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms) {
+  if (level >= static_cast<size_t>(n_levels())) throw InvalidArgument("level index out of range");
+  Matrix& m = level_matrix(level);
+  cudaStream_t s = ctx_->stream;
+  DBuf<double> v(std::max<int64_t>(1, m.f())), out(std::max<int64_t>(1, m.f()));
+  launch_fill(v.get(), 1.0, m.f(), s);
+  DBuf<char> scratch;
+  const size_t flush_bytes = size_t(256) << 20;
+  if (flush) scratch.alloc(flush_bytes);
+  cudaEvent_t e0, e1, e2;
+  RMG_CK(cudaEventCreate(&e0));
+  RMG_CK(cudaEventCreate(&e1));
+  RMG_CK(cudaEventCreate(&e2));
+  double t1 = 0.0, t2 = 0.0;
+  XtArgs a;
+  a.v = v.get();
+  a.out = out.get();
+  a.beta = level_beta(level);
+  a.t = m.t.get();
+  for (uint64_t r = 0; r < reps + 2; ++r) {  // 2 warm-ups
+    if (flush) RMG_CK(cudaMemsetAsync(scratch.get(), static_cast<int>(r & 0xff), flush_bytes, s));
+    RMG_CK(cudaEventRecord(e0, s));
+    launch_spmv_rows(m.x.view, v.get(), m.t.get(), nullptr, s);
+    RMG_CK(cudaEventRecord(e1, s));
+    launch_xt(m.xt.view, m.sched.view, Epi::Axpby, a, s);
+    RMG_CK(cudaEventRecord(e2, s));
+    RMG_CK(cudaEventSynchronize(e2));
+    float a1 = 0.f, a2 = 0.f;
+    RMG_CK(cudaEventElapsedTime(&a1, e0, e1));
+    RMG_CK(cudaEventElapsedTime(&a2, e1, e2));
+    if (r >= 2) {
+      t1 += a1;
+      t2 += a2;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  *k1_ms = t1 / static_cast<double>(std::max<uint64_t>(reps, 1));
+  *k2_ms = t2 / static_cast<double>(std::max<uint64_t>(reps, 1));
+  return *k1_ms + *k2_ms;
+}
+
+}  // namespace rmg

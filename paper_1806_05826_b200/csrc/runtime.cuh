@@ -1,0 +1,189 @@
+// Host orchestration of the ridgemg_b200 solve path (device-resident data,
+// host-sequenced kernels).  The C ABI in capi.cu wraps these classes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_setup.hpp"
+#include "kernels.cuh"
+#include "ridgemg_b200.h"
+
+namespace rmg {
+
+#define RMG_CK(expr)                                                                           \
+  do {                                                                                         \
+    const cudaError_t rmg_e_ = (expr);                                                         \
+    if (rmg_e_ != cudaSuccess)                                                                 \
+      throw ::rmg::CudaError(std::string(#expr) + " failed: " + cudaGetErrorString(rmg_e_)); \
+  } while (0)
+
+template <class T>
+class DBuf {
+ public:
+  DBuf() = default;
+  explicit DBuf(size_t n) { alloc(n); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    n_ = n;
+    if (n) RMG_CK(cudaMalloc(&p_, n * sizeof(T)));
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  void upload(const T* h, size_t n, cudaStream_t s) {
+    if (n > n_) alloc(n);
+    if (n) RMG_CK(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  KrylovScalars* pinned_sc = nullptr;  // host mirror for per-iteration readback
+  uint64_t launches = 0;               // kernels issued (diagnostics)
+  explicit Context(int dev);
+  ~Context();
+  void sync();
+  KrylovScalars read(const KrylovScalars* dev);
+};
+
+// One orientation of a sparse matrix on the device.
+struct DeviceSparse {
+  SparseDev view;
+  DBuf<int32_t> ptr, idx;
+  DBuf<double> val;
+  void upload(const HostCsr& h, bool pattern, cudaStream_t s);
+};
+
+struct DeviceSchedule {
+  XtSchedule view;
+  DBuf<int4> items;
+  DBuf<int32_t> long_col, long_first, long_nseg, long_slot;
+  DBuf<double> seg_partial, slots;
+  DBuf<unsigned> col_ticket, grid_ticket;
+  void build(const HostCsr& xt, cudaStream_t s);
+};
+
+// X (N x F) and X^T on the device, with the X^T schedule and an N-vector scratch.
+struct Matrix {
+  Context* ctx = nullptr;
+  HostCsr host;  // canonical CSR kept for setup (clustering, coarsening)
+  bool pattern = false;
+  DeviceSparse x, xt;
+  DeviceSchedule sched;
+  DBuf<double> t;             // X v scratch
+  DBuf<KrylovScalars> gram_sc;  // power-iteration scalars
+  Matrix(Context* c, HostCsr h, bool detect_pattern);
+  int64_t n() const { return host.n; }
+  int64_t f() const { return host.f; }
+  int64_t nnz() const { return host.nnz(); }
+  // t = X v then the X^T epilogue; v may live in a ring (sc != nullptr)
+  void apply(const double* v, Epi epi, const XtArgs& args);
+  void apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args);
+  void spmv(const double* v, double* y);
+  void spmv_t(const double* u, double* y);
+  double lambda_max(double tol, uint64_t max_iters, uint64_t seed, uint64_t* iters, bool* conv);
+};
+
+// Solver workspace for one level.
+struct KrylovWork {
+  int64_t n = 0;
+  int keep = 20;
+  DBuf<double> b, x, r, z, z1, p_ring, ap_ring, hist, inv_diag;
+  DBuf<uint64_t> inner_hist;
+  DBuf<KrylovScalars> sc;
+  DBuf<double> slots;
+  DBuf<unsigned> ticket;
+  VecWork vw;
+  KrylovWork(int64_t n, int keep, uint64_t max_iters, double tol, cudaStream_t s);
+  void set_params(double tol, uint64_t max_iters, int keep_m, cudaStream_t s);
+  uint64_t max_iters = 0;
+};
+
+struct LevelSpecHost {
+  rmg_level_spec spec{};
+  std::vector<int64_t> labels;  // imported labels (copied)
+};
+
+struct CoarseLevelDev {
+  std::unique_ptr<Matrix> mat;  // X_k, k >= 1
+  Aggregation agg;              // level k-1 -> k
+  DBuf<int32_t> label, mptr, members;
+  DBuf<double> weight;
+  double beta = 0.0;
+};
+
+struct SolveResult {
+  uint64_t iterations = 0;
+  bool converged = false;
+  double wall = 0.0;
+  double final_rel = 0.0;
+  std::vector<double> hist;
+  std::vector<uint64_t> inner;
+};
+
+class Method {
+ public:
+  Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, uint64_t n_levels,
+         const rmg_solver_config& solver);
+  SolveResult solve_rhs(const double* rhs_dev, double* w_dev);
+  void precondition(const double* r_dev, double* z_dev);
+  int64_t n_levels() const { return static_cast<int64_t>(coarse_.size()) + 1; }
+  int64_t coarse_size() const { return coarse_.empty() ? 0 : coarse_[0]->mat->f(); }
+  Matrix& level_matrix(size_t k) const { return k == 0 ? *fine_ : *coarse_[k - 1]->mat; }
+  double level_beta(size_t k) const { return k == 0 ? beta_ : coarse_[k - 1]->beta; }
+  double omega(size_t k) const { return k < omega_.size() ? omega_[k] : 0.0; }
+  const std::vector<int64_t>& labels(size_t k) const;
+  Matrix* fine() const { return fine_; }
+  int kind() const { return kind_; }
+  rmg_solver_config solver;
+  double time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms);
+
+ private:
+  uint64_t precond(size_t k, const double* r, double* z);
+  uint64_t run_fcg(size_t k, const double* rhs, bool record, SolveResult* out);
+  uint64_t run_cg(size_t k, const double* rhs, const double* inv_diag, bool record, SolveResult* out);
+  Context* ctx_;
+  Matrix* fine_;
+  double beta_;
+  int kind_;
+  std::vector<LevelSpecHost> specs_;
+  std::vector<std::unique_ptr<CoarseLevelDev>> coarse_;
+  std::vector<double> omega_;
+  std::vector<std::unique_ptr<KrylovWork>> work_;  // per level 0..L-1
+  DBuf<double> ainv_, rc_last_, ec_last_;
+  DBuf<double> inv_diag_;
+  std::vector<std::vector<int64_t>> labels_;
+};
+
+}  // namespace rmg

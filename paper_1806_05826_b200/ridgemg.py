@@ -1,0 +1,495 @@
+"""Python mirror of the reference's solver interface (proj/include/ridgemg),
+backed by the B200 C ABI (include/ridgemg_b200.h).
+
+Names, argument meanings and error types follow the reference:
+``ValueError`` where it throws ``std::invalid_argument`` and ``RuntimeError``
+where it throws ``std::runtime_error``; non-convergence is reported through
+``SolveReport.converged``.  Every numerical call runs on the GPU; there is no
+CPU code path here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+# ---------------------------------------------------------------- enums (krylov.hpp)
+CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL = 0, 1, 2, 3
+METHOD_NAMES = {"cg": CG, "jacobi_cg": JACOBI_CG, "fcg_twolevel": FCG_TWOLEVEL, "fcg_multilevel": FCG_MULTILEVEL}
+LEADER_TOLERANCE, LEADER_TARGET, KMEANS, IMPORTED = 0, 1, 2, 100
+DIRECT_CHOLESKY, INNER_CG, INNER_FCG = 0, 1, 2
+
+
+def method_from_string(s: str) -> int:
+    """krylov.cpp:574-581 (fgmres_twolevel is out of scope here)."""
+    if s not in METHOD_NAMES:
+        raise ValueError(f"unknown method: '{s}'")
+    return METHOD_NAMES[s]
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- data (sparse.hpp)
+@dataclass
+class FeatureMatrix:
+    """CSR sample-by-feature matrix (sparse.hpp:24-32); values None = binary pattern."""
+
+    n_samples: int
+    n_features: int
+    row_offsets: np.ndarray
+    column_indices: np.ndarray
+    values: Optional[np.ndarray] = None
+
+    @property
+    def nnz(self) -> int:
+        return int(len(self.column_indices))
+
+    def dense(self) -> np.ndarray:
+        d = np.zeros((self.n_samples, self.n_features))
+        rows = np.repeat(np.arange(self.n_samples), np.diff(self.row_offsets).astype(np.int64))
+        d[rows, self.column_indices.astype(np.int64)] = 1.0 if self.values is None else self.values
+        return d
+
+    def value_array(self) -> np.ndarray:
+        return np.ones(self.nnz) if self.values is None else self.values
+
+
+def csr_from_triplets(n_samples: int, n_features: int, rows, cols, vals) -> FeatureMatrix:
+    """sparse.cpp:27-73: validate, sort by (row, col), sum duplicates in input order."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    vals = np.asarray(vals, np.float64)
+    if len(rows) and (rows.min() < 0 or rows.max() >= n_samples or cols.min() < 0 or cols.max() >= n_features):
+        raise ValueError(f"csr_from_triplets: entry outside {n_samples}x{n_features}")
+    if not np.all(np.isfinite(vals)):
+        raise ValueError("csr_from_triplets: non-finite value")
+    order = np.lexsort((cols, rows))  # stable: duplicates keep input order
+    r, c, v = rows[order], cols[order], vals[order]
+    keep_c, keep_v, keep_r = [], [], []
+    for i in range(len(r)):
+        if keep_r and keep_r[-1] == r[i] and keep_c[-1] == c[i]:
+            keep_v[-1] += v[i]
+        else:
+            keep_r.append(r[i])
+            keep_c.append(c[i])
+            keep_v.append(v[i])
+    rp = np.zeros(n_samples + 1, np.uint64)
+    np.add.at(rp, np.asarray(keep_r, np.int64) + 1, 1)
+    rp = np.cumsum(rp).astype(np.uint64)
+    return FeatureMatrix(n_samples, n_features, rp, np.asarray(keep_c, np.uint64), np.asarray(keep_v, np.float64))
+
+
+def from_dense(a: np.ndarray) -> FeatureMatrix:
+    a = np.asarray(a, np.float64)
+    r, c = np.nonzero(a)
+    rp = np.zeros(a.shape[0] + 1, np.uint64)
+    np.add.at(rp, r + 1, 1)
+    return FeatureMatrix(a.shape[0], a.shape[1], np.cumsum(rp).astype(np.uint64), c.astype(np.uint64),
+                         a[r, c].copy())
+
+
+def read_matrix_market(path: str) -> FeatureMatrix:
+    """matrix_market.cpp:34-148 (coordinate/array; real/integer/pattern; general/symmetric)."""
+    with open(path) as fh:
+        header = fh.readline().split()
+        if len(header) < 5 or header[0] != "%%MatrixMarket":
+            raise RuntimeError(f"{path}: malformed header")
+        obj, fmt, fld, sym = (h.lower() for h in header[1:5])
+        if obj != "matrix" or fmt not in ("coordinate", "array") or fld not in ("real", "integer", "pattern") \
+                or sym not in ("general", "symmetric") or (fmt == "array" and fld == "pattern"):
+            raise RuntimeError(f"{path}: unsupported Matrix Market variant {obj} {fmt} {fld} {sym}")
+        line = fh.readline()
+        while line and (not line.strip() or line.startswith("%")):
+            line = fh.readline()
+        dims = [int(t) for t in line.split()]
+        body = [ln for ln in fh if ln.strip() and not ln.startswith("%")]
+    rows_, cols_, vals_ = [], [], []
+    if fmt == "coordinate":
+        n, f, nz = dims[:3]
+        if len(body) != nz:
+            raise RuntimeError(f"{path}: entry count mismatch: header declares {nz}, file holds {len(body)}")
+        for ln in body:
+            t = ln.split()
+            r, c = int(t[0]) - 1, int(t[1]) - 1
+            v = 1.0 if fld == "pattern" else float(t[2])
+            rows_.append(r), cols_.append(c), vals_.append(v)
+            if sym == "symmetric" and r != c:
+                rows_.append(c), cols_.append(r), vals_.append(v)
+    else:
+        n, f = dims[:2]
+        vals = [float(t) for ln in body for t in ln.split()]
+        idx = 0
+        for c in range(f):
+            for r in range(c if sym == "symmetric" else 0, n):
+                v = vals[idx]
+                idx += 1
+                if v != 0.0:
+                    rows_.append(r), cols_.append(c), vals_.append(v)
+                    if sym == "symmetric" and r != c:
+                        rows_.append(c), cols_.append(r), vals_.append(v)
+    return csr_from_triplets(n, f, rows_, cols_, vals_)
+
+
+def _host_csr_to_matrix(h, n: int, f: int, nnz: int, pattern: bool) -> FeatureMatrix:
+    lib = _lib.load()
+    rp = np.zeros(n + 1, np.uint64)
+    ci = np.zeros(nnz, np.uint64)
+    v = np.zeros(nnz, np.float64)
+    try:
+        _lib.check(lib.rmg_host_csr_export(h, _ptr(rp), _ptr(ci), _ptr(v)))
+    finally:
+        lib.rmg_host_csr_destroy(h)
+    return FeatureMatrix(n, f, rp, ci, None if pattern else v)
+
+
+def synth_dense_clustered(n: int, f: int, groups: int = 50, noise: float = 0.1, seed: int = 0) -> FeatureMatrix:
+    """BASELINE cfg 1 generator."""
+    lib = _lib.load()
+    h, nnz = C.c_void_p(), C.c_uint64()
+    _lib.check(lib.rmg_synth_dense_clustered(n, f, groups, noise, seed, C.byref(h), C.byref(nnz)))
+    return _host_csr_to_matrix(h, n, f, nnz.value, False)
+
+
+def synth_sparse_zipf(n: int, f: int, mean_nnz: float, zipf_s: float, abs_normal_values: bool = False,
+                      seed: int = 0) -> FeatureMatrix:
+    """BASELINE cfg 2/3/5 generator."""
+    lib = _lib.load()
+    h, nnz = C.c_void_p(), C.c_uint64()
+    _lib.check(lib.rmg_synth_sparse_zipf(n, f, mean_nnz, zipf_s, int(abs_normal_values), seed, C.byref(h),
+                                         C.byref(nnz)))
+    return _host_csr_to_matrix(h, n, f, nnz.value, not abs_normal_values)
+
+
+def rng_normals(seed: int, n: int) -> np.ndarray:
+    out = np.zeros(n)
+    _lib.check(_lib.load().rmg_rng_normals(seed, n, _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------- device objects
+class Context:
+    """One GPU and one stream (rmg_context)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        self.h = C.c_void_p()
+        _lib.check(self.lib.rmg_context_create(device, C.byref(self.h)))
+        self.device = device
+
+    def set_stream(self, cuda_stream: int) -> None:
+        _lib.check(self.lib.rmg_context_set_stream(self.h, C.c_void_p(cuda_stream)))
+
+    def synchronize(self) -> None:
+        _lib.check(self.lib.rmg_context_synchronize(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.rmg_context_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class DeviceMatrix:
+    """X and X^T resident in HBM (rmg_matrix).  Mirrors the FeatureMatrix-level
+    free functions of the reference: spmv, spmv_transpose, RidgeOperator::apply,
+    gram_diagonal, estimate_lambda_max(GramOperator)."""
+
+    def __init__(self, x: FeatureMatrix, ctx: Optional[Context] = None, detect_pattern: bool = True):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.x = x
+        rp = np.ascontiguousarray(x.row_offsets, np.uint64)
+        ci = np.ascontiguousarray(x.column_indices, np.uint64)
+        v = None if x.values is None else np.ascontiguousarray(x.values, np.float64)
+        self.h = C.c_void_p()
+        _lib.check(self.lib.rmg_matrix_create_csr(self.ctx.h, x.n_samples, x.n_features, _ptr(rp), _ptr(ci), _ptr(v),
+                                                  int(detect_pattern), C.byref(self.h)))
+        n, f, z, pat = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int32()
+        _lib.check(self.lib.rmg_matrix_shape(self.h, C.byref(n), C.byref(f), C.byref(z), C.byref(pat)))
+        self.n_samples, self.n_features, self.nnz, self.is_pattern = n.value, f.value, z.value, bool(pat.value)
+
+    def close(self):
+        if self.h:
+            self.lib.rmg_matrix_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _vec(self, a, n):
+        a = np.ascontiguousarray(a, np.float64)
+        if a.shape != (n,):
+            raise ValueError(f"length {a.shape[0] if a.ndim else 0}, expected {n}")
+        return a
+
+    def spmv(self, v) -> np.ndarray:
+        v = self._vec(v, self.n_features)
+        y = np.zeros(self.n_samples)
+        _lib.check(self.lib.rmg_spmv(self.h, _ptr(v), _ptr(y), 0))
+        return y
+
+    def spmv_transpose(self, u) -> np.ndarray:
+        u = self._vec(u, self.n_samples)
+        y = np.zeros(self.n_features)
+        _lib.check(self.lib.rmg_spmv_transpose(self.h, _ptr(u), _ptr(y), 0))
+        return y
+
+    def ridge_apply(self, beta: float, w) -> np.ndarray:
+        w = self._vec(w, self.n_features)
+        out = np.zeros(self.n_features)
+        _lib.check(self.lib.rmg_ridge_apply(self.h, beta, _ptr(w), _ptr(out), 0))
+        return out
+
+    def gram_diagonal(self, beta: float) -> np.ndarray:
+        out = np.zeros(self.n_features)
+        _lib.check(self.lib.rmg_gram_diagonal(self.h, beta, _ptr(out), 0))
+        return out
+
+    def lambda_max(self, tol: float = 1e-4, max_iters: int = 200, seed: int = 0x5EED):
+        v, it, cv = C.c_double(), C.c_uint64(), C.c_int32()
+        _lib.check(self.lib.rmg_lambda_max(self.h, tol, max_iters, seed, C.byref(v), C.byref(it), C.byref(cv)))
+        return v.value, it.value, bool(cv.value)
+
+
+@dataclass
+class RhsSample:
+    b: np.ndarray
+    rhs: np.ndarray
+
+
+def generate_rhs(x: DeviceMatrix, seed: int) -> RhsSample:
+    """analysis.cpp:225-232: b = CounterRng(seed) normals, rhs = X^T b."""
+    b = np.zeros(x.n_samples)
+    rhs = np.zeros(x.n_features)
+    _lib.check(x.lib.rmg_generate_rhs(x.h, seed, _ptr(b), _ptr(rhs)))
+    return RhsSample(b, rhs)
+
+
+# ---------------------------------------------------------------- specs (krylov.hpp:16-23,135-218)
+@dataclass
+class SolverConfig:
+    tol: float = 1e-6
+    max_iters: int = 1000
+    truncation: int = 20
+
+
+@dataclass
+class ClusteringChoice:
+    kind: int = LEADER_TOLERANCE
+    tolerance: float = 1.0
+    target_size: int = 0
+    seed: int = 0
+    kmeans_max_iters: int = 100
+    normalize_columns: bool = False  # BASELINE cfg 2 extension
+    labels: Optional[np.ndarray] = None  # IMPORTED
+    n_clusters: int = 0
+
+
+@dataclass
+class CoarseSolveChoice:
+    kind: int = DIRECT_CHOLESKY
+    tol: float = 1e-6
+    max_iters: int = 500
+    truncation: int = 20
+
+
+@dataclass
+class LevelSpec:
+    clustering: ClusteringChoice = field(default_factory=ClusteringChoice)
+    solver: CoarseSolveChoice = field(default_factory=CoarseSolveChoice)
+    beta_override: Optional[float] = None
+    omega_override: Optional[float] = None  # parity runs
+
+
+@dataclass
+class MethodSpec:
+    kind: int = CG
+    levels: Sequence[LevelSpec] = ()
+    solver: SolverConfig = field(default_factory=SolverConfig)
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    converged: bool = False
+    wall_time_s: float = 0.0
+    inner_iterations: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    kernel_launches: int = 0
+
+
+def _level_array(levels: Sequence[LevelSpec]):
+    arr = (_lib.LevelSpecC * max(1, len(levels)))()
+    keep = []
+    for i, lv in enumerate(levels):
+        s = arr[i]
+        c = lv.clustering
+        s.clustering_kind = c.kind
+        s.tolerance = c.tolerance
+        s.target_size = c.target_size
+        s.seed = c.seed
+        s.kmeans_max_iters = c.kmeans_max_iters
+        s.normalize_columns = int(c.normalize_columns)
+        if c.kind == IMPORTED:
+            if c.labels is None:
+                raise ValueError("imported clustering without labels")
+            lab = np.ascontiguousarray(c.labels, np.int64)
+            keep.append(lab)
+            s.labels = lab.ctypes.data
+            s.n_clusters = int(c.n_clusters if c.n_clusters else lab.max() + 1)
+        s.coarse_kind = lv.solver.kind
+        s.coarse_tol = lv.solver.tol
+        s.coarse_max_iters = lv.solver.max_iters
+        s.coarse_truncation = lv.solver.truncation
+        if lv.beta_override is not None:
+            s.has_beta_override, s.beta_override = 1, lv.beta_override
+        if lv.omega_override is not None:
+            s.has_omega_override, s.omega_override = 1, lv.omega_override
+    return arr, keep
+
+
+class PreparedMethod:
+    """krylov.hpp:222-242: setup in the constructor, then solve(b) for any b."""
+
+    def __init__(self, x: DeviceMatrix, beta: float, spec: MethodSpec):
+        self.x, self.beta, self.spec = x, beta, spec
+        self.lib = x.lib
+        arr, self._keep = _level_array(spec.levels)
+        cfg = _lib.SolverConfigC(spec.solver.tol, spec.solver.max_iters, spec.solver.truncation)
+        self.h = C.c_void_p()
+        _lib.check(self.lib.rmg_method_prepare(x.h, beta, spec.kind, arr, len(spec.levels), C.byref(cfg),
+                                               C.byref(self.h)))
+        nl, cs = C.c_uint64(), C.c_uint64()
+        _lib.check(self.lib.rmg_method_info(self.h, C.byref(nl), C.byref(cs)))
+        self.n_levels, self._coarse_size = nl.value, cs.value
+
+    def close(self):
+        if self.h:
+            self.lib.rmg_method_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def coarse_size(self) -> int:
+        return self._coarse_size
+
+    def _report(self):
+        cap = self.spec.solver.max_iters + 1
+        hist = np.zeros(cap)
+        inner = np.zeros(cap, np.uint64)
+        rep = _lib.SolveReportC()
+        rep.residual_history, rep.residual_capacity = hist.ctypes.data, cap
+        rep.inner_iterations, rep.inner_capacity = inner.ctypes.data, cap
+        return rep, hist, inner
+
+    def _finish(self, rep, hist, inner) -> SolveReport:
+        it = rep.iterations
+        nh = it if it else (1 if rep.converged else 0)
+        flexible = self.spec.kind in (FCG_TWOLEVEL, FCG_MULTILEVEL)
+        return SolveReport(iterations=it, residual_history=hist[:nh].copy(), converged=bool(rep.converged),
+                           wall_time_s=rep.wall_time_s,
+                           inner_iterations=inner[:it].copy() if flexible else np.zeros(0, np.uint64),
+                           kernel_launches=rep.kernel_launches)
+
+    def solve(self, b) -> tuple[np.ndarray, SolveReport]:
+        """PreparedMethod::solve (krylov.cpp:651-668): rhs = X^T b, then the Krylov solve."""
+        b = np.ascontiguousarray(b, np.float64)
+        if b.shape != (self.x.n_samples,):
+            raise ValueError("PreparedMethod::solve: b length != n_samples")
+        w = np.zeros(self.x.n_features)
+        rep, hist, inner = self._report()
+        _lib.check(self.lib.rmg_method_solve(self.h, _ptr(b), _ptr(w), C.byref(rep), 0))
+        return w, self._finish(rep, hist, inner)
+
+    def solve_rhs(self, rhs) -> tuple[np.ndarray, SolveReport]:
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        if rhs.shape != (self.x.n_features,):
+            raise ValueError("fcg: rhs length != operator dimension")
+        w = np.zeros(self.x.n_features)
+        rep, hist, inner = self._report()
+        _lib.check(self.lib.rmg_method_solve_rhs(self.h, _ptr(rhs), _ptr(w), C.byref(rep), 0))
+        return w, self._finish(rep, hist, inner)
+
+    def solve_device(self, b_ptr: int, w_ptr: int, from_rhs: bool = False) -> SolveReport:
+        """Device-pointer solve (inputs already resident in HBM)."""
+        rep, hist, inner = self._report()
+        fn = self.lib.rmg_method_solve_rhs if from_rhs else self.lib.rmg_method_solve
+        _lib.check(fn(self.h, C.c_void_p(b_ptr), C.c_void_p(w_ptr), C.byref(rep), 1))
+        return self._finish(rep, hist, inner)
+
+    def precondition(self, r) -> np.ndarray:
+        """two_level_apply (krylov.cpp:422-426) with the level-0 preconditioner."""
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.zeros(self.x.n_features)
+        _lib.check(self.lib.rmg_method_precondition(self.h, _ptr(r), _ptr(z), 0))
+        return z
+
+    def level(self, k: int) -> dict:
+        nf, nnz, beta, omega = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_double()
+        _lib.check(self.lib.rmg_method_level(self.h, k, C.byref(nf), C.byref(nnz), C.byref(beta), C.byref(omega)))
+        return {"n_features": nf.value, "nnz": nnz.value, "beta": beta.value, "omega": omega.value}
+
+    def labels(self, k: int) -> np.ndarray:
+        out = np.zeros(self.level(k)["n_features"], np.int64)
+        _lib.check(self.lib.rmg_method_level_labels(self.h, k, _ptr(out)))
+        return out
+
+    def level_matrix(self, k: int) -> FeatureMatrix:
+        info = self.level(k)
+        n = self.x.n_samples
+        rp = np.zeros(n + 1, np.uint64)
+        ci = np.zeros(info["nnz"], np.uint64)
+        v = np.zeros(info["nnz"])
+        _lib.check(self.lib.rmg_method_level_matrix(self.h, k, _ptr(rp), _ptr(ci), _ptr(v)))
+        return FeatureMatrix(n, info["n_features"], rp, ci, v)
+
+    def time_operator(self, level: int = 0, reps: int = 20, flush_l2: bool = True):
+        t, k1, k2 = C.c_double(), C.c_double(), C.c_double()
+        _lib.check(self.lib.rmg_method_time_operator(self.h, level, reps, int(flush_l2), C.byref(t), C.byref(k1),
+                                                     C.byref(k2)))
+        return t.value, k1.value, k2.value
+
+
+@dataclass
+class SystemSolution:
+    w: np.ndarray
+    report: SolveReport
+    coarse_size: int = 0
+
+
+def solve_system(x: DeviceMatrix, beta: float, b, spec: MethodSpec) -> SystemSolution:
+    """krylov.cpp:670-679: setup plus a single solve."""
+    pm = PreparedMethod(x, beta, spec)
+    try:
+        w, rep = pm.solve(b)
+        return SystemSolution(w, rep, pm.coarse_size())
+    finally:
+        pm.close()
