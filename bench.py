@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the ridgemg_b200 solve path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+
+One step = one preconditioned Krylov solve of (X^T X + beta I) w = X^T b to
+relative residual 1e-6 for a fresh right-hand side b (seeded N(0,1)), with X,
+the hierarchy and b already resident in HBM; the step runs from b on the
+device to w on the device (rhs = X^T b formation included).  Default workload
+is BASELINE configs[1] (cfg2).  L2 is flushed (256 MiB write) before every
+timed step, outside the step's event pair.  Multi-GPU (torchrun): independent
+replicas, one per rank, max-over-ranks device time.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, the unmodified reference sources) on the
+same config with all host threads, on bounded samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG time-to-1e-6 rel. residual per solve; XᵀX-operator HBM GB/s vs roofline"
+
+CONFIGS = {
+    "cfg2": dict(
+        workload="cfg2: sparse binary CSR N=100000 x F=20000, nnz/row max(1,Poisson(40)), Zipf(1.1) columns; "
+                 "3-level hierarchy k-means(unit-normalised columns, seed 0) 2000/200, inner FCG tol 1e-6; "
+                 "beta=1; outer FCG(m=20) to rel. residual 1e-6",
+        kind="zipf", n=100000, f=20000, mean=40.0, zipf=1.1, abs_values=False, seed=0, beta=1.0,
+        ks=[2000, 200], normalize=True, method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg2_full"),
+    "cfg1": dict(
+        workload="cfg1: dense clustered N=2000 x F=500 fp64 (stored CSR); 2-level k-means 50; beta=1e-2; "
+                 "FCG(m=20) to rel. residual 1e-6",
+        kind="dense", n=2000, f=500, groups=50, noise=0.1, seed=0, beta=1e-2, ks=[50], normalize=False,
+        method="fcg_twolevel", tol=1e-6, max_iters=1000, golden="cfg1"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_matrix(cfg):
+    import paper_1806_05826_b200 as R
+    if cfg["kind"] == "zipf":
+        return R.synth_sparse_zipf(cfg["n"], cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"])
+    return R.synth_dense_clustered(cfg["n"], cfg["f"], cfg["groups"], cfg["noise"], cfg["seed"])
+
+
+def level_specs(cfg, labels=None):
+    import paper_1806_05826_b200 as R
+    specs = []
+    for i, k in enumerate(cfg["ks"]):
+        last = i == len(cfg["ks"]) - 1
+        if labels is not None:
+            cl = R.ClusteringChoice(kind=R.IMPORTED, labels=labels[i], n_clusters=k)
+        else:
+            cl = R.ClusteringChoice(kind=R.KMEANS, target_size=k, seed=0, kmeans_max_iters=100,
+                                    normalize_columns=cfg["normalize"])
+        sv = R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if last else R.INNER_FCG, tol=1e-6, max_iters=500)
+        specs.append(R.LevelSpec(clustering=cl, solver=sv))
+    return specs
+
+
+def algorithmic_bytes(n, f, nnz, pattern):
+    """one operator application, S = 2 sweeps (X, then X^T):
+    indices (4 B) + values (0 or 8 B) per nonzero per sweep, int32 row pointers
+    of both sweeps, and the compulsory vector traffic 8(F + 2N + 2F)."""
+    s_val = 0 if pattern else 8
+    return 2 * nnz * (4 + s_val) + 4 * (n + 1) + 4 * (f + 1) + 8 * (f + 2 * n + 2 * f)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_golden_labels(cfg):
+    path = os.path.join(ROOT, "tests", "golden", cfg["golden"] + ".npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    if "labels0" not in g.files:
+        return None
+    return [g[f"labels{i}"].astype(np.int64) for i in range(len(cfg["ks"]))]
+
+
+# ---------------------------------------------------------------- reference arm / CPU baseline
+def reference_solve_sample(cfg, x, labels, threads, sample_iters, rhs_seed=42):
+    """The reference's own PreparedMethod-equivalent solve (oracle/_ref: the
+    unmodified reference sources) capped at `sample_iters` outer iterations;
+    returns (seconds per outer iteration, kind, iterations run)."""
+    import oracle
+    kind = "reference" if oracle.available("ref") else "port"
+    chk = oracle.Checker("ref" if kind == "reference" else "oracle")
+    chk.set_num_threads(threads)
+    m = chk.matrix(x.n_samples, x.n_features, x.row_offsets, x.column_indices, x.value_array())
+    levels = []
+    for i, k in enumerate(cfg["ks"]):
+        last = i == len(cfg["ks"]) - 1
+        levels.append(dict(labels=labels[i], n_clusters=k,
+                           coarse_kind=oracle.COARSE_DIRECT if last else oracle.COARSE_INNER_FCG,
+                           coarse_tol=1e-6, coarse_max_iters=500))
+    b = chk.normals(rhs_seed, x.n_samples)
+    s = chk.solve(m, cfg["beta"], b, cfg["method"], levels=levels, tol=cfg["tol"], max_iters=sample_iters)
+    return s.wall_time_s / max(1, s.iterations), kind, s.iterations
+
+
+def run_reference_arm(args, cfg):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    x = make_matrix(cfg)
+    labels = load_golden_labels(cfg)
+    if labels is None:
+        import oracle
+        o = oracle.Checker("oracle")
+        o.set_num_threads(os.cpu_count() or 1)
+        m = o.matrix(x.n_samples, x.n_features, x.row_offsets, x.column_indices, x.value_array())
+        labels, cur = [], m
+        for k in cfg["ks"]:
+            lab, _, _ = o.kmeans(cur, k, 100, 0, normalize=cfg["normalize"])
+            labels.append(lab)
+            cur = o.coarsen(cur, lab, k)
+    threads = os.cpu_count() or 1
+    full_iters = None
+    g = os.path.join(ROOT, "tests", "golden", cfg["golden"] + ".npz")
+    if os.path.exists(g):
+        gz = np.load(g)
+        key = "ml_iterations" if "ml_iterations" in gz.files else "fcg_iterations"
+        if key in gz.files:
+            full_iters = int(gz[key])
+    per_iter = []
+    t0 = time.time()
+    for step in range(args.warmup + args.steps):
+        sec, kind, ran = reference_solve_sample(cfg, x, labels, threads, args.ref_sample_iters, 42 + step)
+        if step >= args.warmup:
+            per_iter.append(sec)
+    iters = full_iters or ran
+    value = statistics.mean(per_iter) * iters * 1e3
+    sample = (f"{args.ref_sample_iters} outer FCG iterations per step (setup untimed, the reference's own "
+              f"krylov.cpp timer), extrapolated x {iters} iterations")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "ms/solve", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "ms/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0}), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def run_b200(args, cfg):
+    import torch
+    import paper_1806_05826_b200 as R
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    ctx = R.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    t_setup = time.time()
+    x = make_matrix(cfg)
+    m = R.DeviceMatrix(x, ctx)
+    labels = None
+    if world > 1:  # rank 0 clusters once; replicas import its labels
+        obj = [None]
+        if rank == 0:
+            pm0 = R.PreparedMethod(m, cfg["beta"], R.MethodSpec(kind=R.method_from_string(cfg["method"]),
+                                                                levels=level_specs(cfg),
+                                                                solver=R.SolverConfig(cfg["tol"], cfg["max_iters"])))
+            obj = [[pm0.labels(i) for i in range(len(cfg["ks"]))]]
+            pm0.close()
+        pg.broadcast_object_list(obj, src=0)
+        labels = obj[0]
+    spec = R.MethodSpec(kind=R.method_from_string(cfg["method"]), levels=level_specs(cfg, labels),
+                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"]))
+    pm = R.PreparedMethod(m, cfg["beta"], spec)
+    setup_s = time.time() - t_setup
+    if labels is None:
+        labels = [pm.labels(i) for i in range(len(cfg["ks"]))]
+
+    dev = torch.device("cuda", local)
+    nsteps = args.warmup + args.steps
+    bs = [torch.from_numpy(R.rng_normals(42 + rank * 10007 + s, x.n_samples)).to(dev) for s in range(nsteps)]
+    w = torch.empty(x.n_features, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    reports = []
+    for s in range(args.warmup):
+        flush.random_(0, 255)
+        reports.append(pm.solve_device(bs[s].data_ptr(), w.data_ptr()))
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    timed = []
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            flush.random_(0, 255)  # L2 flush, outside the step's events
+            ev[s][0].record(stream)
+            timed.append(pm.solve_device(bs[args.warmup + s].data_ptr(), w.data_ptr()))
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if pg:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms = float(t.item())
+    solves = args.steps * world
+    value = total_ms / solves  # whole-job ms per solve (replicas: aggregate throughput)
+    ms_per_step = total_ms / args.steps
+
+    # in-situ operator profile over the same kind of steps (events around every
+    # K1 / K2 launch of every level), run right after the timed region
+    pm.set_profiling(True)
+    for s in range(min(args.steps, 3)):
+        flush.random_(0, 255)
+        pm.solve_device(bs[args.warmup + s].data_ptr(), w.data_ptr())
+    torch.cuda.synchronize()
+    prof = []
+    for lv in range(pm.n_levels):
+        napp, k1, k2 = pm.profile(lv)
+        info = pm.level(lv) if lv > 0 else {"n_features": x.n_features, "nnz": m.nnz}
+        prof.append(dict(level=lv, applications=napp, ms_k1=k1, ms_k2=k2, n_features=info["n_features"],
+                         nnz=info["nnz"]))
+    pm.set_profiling(False)
+    dom = max(prof, key=lambda p: p["ms_k1"] + p["ms_k2"])
+    pattern = m.is_pattern if dom["level"] == 0 else False
+    bytes_per_apply = algorithmic_bytes(x.n_samples, dom["n_features"], dom["nnz"], pattern)
+    ms_apply = (dom["ms_k1"] + dom["ms_k2"]) / max(1, dom["applications"])
+    peak, peak_kind = peaks()
+    achieved = bytes_per_apply / (ms_apply * 1e-3) / 1e9 if ms_apply > 0 else 0.0
+    prof_total = sum(p["ms_k1"] + p["ms_k2"] for p in prof)
+
+    # cold / warm fine-operator timing (dedicated loop, L2 flushed or not)
+    cold = pm.time_operator(0, 20, True)
+    warm = pm.time_operator(0, 20, False)
+    fine_bytes = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
+
+    # e2e: host buffers through the C ABI (H2D of b, D2H of w inside each step)
+    pinned_b = [torch.from_numpy(R.rng_normals(42 + rank * 10007 + s, x.n_samples)).pin_memory()
+                for s in range(args.steps)]
+    pinned_w = torch.empty(x.n_features, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for s in range(args.steps):
+        flush.random_(0, 255)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        R.ridgemg._lib.check(pm.lib.rmg_method_solve(pm.h, R.ridgemg._ptr(pinned_b[s].numpy()),
+                                                     R.ridgemg._ptr(pinned_w.numpy()), None, 0))
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_total = sum(e2e_ms)
+    if pg:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = e2e_total / solves
+
+    # CPU baseline: the reference on this host, rank 0 at N=1 only, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sec, kind, ran = reference_solve_sample(cfg, x, labels, 1, args.ref_sample_iters)
+            iters = statistics.mean(r.iterations for r in timed)
+            cpu = {"value": sec * iters * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
+                   "sample": f"{ran} outer FCG iterations of the same solve (reference timer, setup untimed), "
+                             f"x {iters:.1f} iterations/solve"}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_apply")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        its = [r.iterations for r in timed]
+        inner = [float(np.mean(r.inner_iterations)) if len(r.inner_iterations) else 0.0 for r in timed]
+        line = {
+            "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
+            "config": {"workload": cfg["workload"], "n_samples": x.n_samples, "n_features": x.n_features,
+                       "nnz": m.nnz, "levels": [x.n_features] + list(cfg["ks"]), "beta": cfg["beta"],
+                       "tol": cfg["tol"], "method": cfg["method"],
+                       "l2": "flushed (256 MiB write) before every timed step, outside its events",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "iterations": its, "inner_iterations_mean": inner, "converged": all(r.converged for r in timed),
+            "setup_s": setup_s,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"level-{dom['level']} operator (K1 X v + K2 X^T pass), in-situ events",
+                         "algorithmic_bytes_per_apply": bytes_per_apply, "ms_per_apply": ms_apply,
+                         "peak_kind": peak_kind, "share_of_step": prof_total and (dom['ms_k1'] + dom['ms_k2']) /
+                         (sum(step_ms[:min(args.steps, 3)]) or 1.0)},
+            "operator_profile": prof,
+            "fine_operator": {"bytes_per_apply": fine_bytes, "cold_ms": cold[0], "warm_ms": warm[0],
+                              "cold_gbs": fine_bytes / (cold[0] * 1e6), "warm_gbs": fine_bytes / (warm[0] * 1e6),
+                              "cold_k1_ms": cold[1], "cold_k2_ms": cold[2]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
+                    "d2h_bytes_per_step": x.n_features * 8},
+            "gpu_launches": int(sum(r.kernel_launches for r in timed)),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample-iters", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -200,6 +200,13 @@ int rmg_solve_system(rmg_matrix* m, double beta, int32_t method_kind, const rmg_
  * applications of the level-`level` operator kernels, for the roofline. */
 int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int32_t flush_l2,
                              double* ms_per_apply, double* ms_k1, double* ms_k2);
+/* In-situ profiling: with `on`, every operator application of every level
+ * inside real solves is bracketed by CUDA events (K1 = X v, K2 = X^T pass);
+ * rmg_method_profile returns the accumulated applications and milliseconds
+ * since profiling was (re)enabled. */
+int rmg_method_set_profiling(rmg_method* pm, int32_t on);
+int rmg_method_profile(const rmg_method* pm, uint64_t level, uint64_t* applications, double* ms_k1,
+                       double* ms_k2);
 
 #ifdef __cplusplus
 }

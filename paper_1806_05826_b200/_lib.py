@@ -95,6 +95,8 @@ SIGNATURES = {
     "rmg_method_level_matrix": [_P, _U64, _P, _P, _P],
     "rmg_solve_system": [_P, _D, _I32, _P, _U64, _P, _P, _P, _P, _P],
     "rmg_method_time_operator": [_P, _U64, _U64, _I32, _P, _P, _P],
+    "rmg_method_set_profiling": [_P, _I32],
+    "rmg_method_profile": [_P, _U64, _P, _P, _P],
 }
 
 _lib = None

@@ -444,4 +444,22 @@ int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int3
   });
 }
 
+int rmg_method_set_profiling(rmg_method* pm, int32_t on) {
+  return guard([&] {
+    need(pm, "method");
+    pm->m.set_profiling(on != 0);
+  });
+}
+
+int rmg_method_profile(const rmg_method* pm, uint64_t level, uint64_t* applications, double* ms_k1, double* ms_k2) {
+  return guard([&] {
+    need(pm, "method");
+    if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
+    const rmg::OpProfile& p = pm->m.profile(level);
+    if (applications) *applications = p.count;
+    if (ms_k1) *ms_k1 = p.ms_k1;
+    if (ms_k2) *ms_k2 = p.ms_k2;
+  });
+}
+
 }  // extern "C"

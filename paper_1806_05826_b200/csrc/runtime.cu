@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -17,7 +18,15 @@ Context::Context(int dev) : device(dev) {
   RMG_CK(cudaSetDevice(dev));
   RMG_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   own_stream = true;
-  RMG_CK(cudaMallocHost(&pinned_sc, sizeof(KrylovScalars)));
+  RMG_CK(cudaMallocHost(&pinned_sc, 2 * sizeof(KrylovScalars)));
+}
+
+void Context::read2(const KrylovScalars* a, KrylovScalars* ha, const KrylovScalars* b, KrylovScalars* hb) {
+  RMG_CK(cudaMemcpyAsync(pinned_sc, a, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, stream));
+  RMG_CK(cudaMemcpyAsync(pinned_sc + 1, b, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, stream));
+  RMG_CK(cudaStreamSynchronize(stream));
+  *ha = pinned_sc[0];
+  *hb = pinned_sc[1];
 }
 
 Context::~Context() {
@@ -139,6 +148,35 @@ void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s) {
   view.width = width;
 }
 
+// ------------------------------------------------------------------ profiling
+OpProfile::~OpProfile() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+void OpProfile::mark(cudaStream_t s) {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    RMG_CK(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  RMG_CK(cudaEventRecord(pool[used++], s));
+}
+void OpProfile::collect() {
+  for (size_t i = 0; i + 3 <= used; i += 3) {
+    float a = 0.f, b = 0.f;
+    RMG_CK(cudaEventElapsedTime(&a, pool[i], pool[i + 1]));
+    RMG_CK(cudaEventElapsedTime(&b, pool[i + 1], pool[i + 2]));
+    ms_k1 += a;
+    ms_k2 += b;
+    ++count;
+  }
+  used = 0;
+}
+void OpProfile::reset() {
+  used = 0;
+  count = 0;
+  ms_k1 = ms_k2 = 0.0;
+}
+
 // ------------------------------------------------------------------ Matrix
 Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern) : ctx(c), host(std::move(h)) {
   validate_csr(host);
@@ -157,19 +195,26 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern) : ctx(c), host(std::m
   gram_sc.alloc(1);
 }
 
-void Matrix::apply(const double* v, Epi epi, const XtArgs& args) {
+void Matrix::apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof) {
+  if (prof) prof->mark(ctx->stream);
   launch_spmv_rows(x.view, v, t.get(), args.done, ctx->stream);
+  if (prof) prof->mark(ctx->stream);
   XtArgs a = args;
   a.t = t.get();
   launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  if (prof) prof->mark(ctx->stream);
   ctx->launches += 2;
 }
 
-void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args) {
+void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args,
+                        OpProfile* prof) {
+  if (prof) prof->mark(ctx->stream);
   launch_spmv_rows_ring(x.view, v_ring, stride, sc, t.get(), ctx->stream);
+  if (prof) prof->mark(ctx->stream);
   XtArgs a = args;
   a.t = t.get();
   launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  if (prof) prof->mark(ctx->stream);
   ctx->launches += 2;
 }
 
@@ -391,15 +436,107 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     ainv_.upload(inv.data(), inv.size(), s);
     rc_last_.alloc(std::max<int64_t>(1, fc_last));
     ec_last_.alloc(std::max<int64_t>(1, fc_last));
-  }
-  // workspaces: level 0 = outer FCG, level k >= 1 = inner solve configured by spec k-1
-  work_.push_back(std::make_unique<KrylovWork>(x->f(), keep0, solver.max_iters, solver.tol, s));
-  for (uint64_t k = 1; k < L; ++k) {
-    const rmg_level_spec& sp = specs_[k - 1].spec;
-    const int keep = static_cast<int>(std::max<uint64_t>(sp.coarse_truncation, 1));
-    work_.push_back(std::make_unique<KrylovWork>(level_matrix(k).f(), keep, sp.coarse_max_iters, sp.coarse_tol, s));
+    // workspaces: level 0 = outer FCG, level k >= 1 = inner solve configured by spec k-1
+    work_.push_back(std::make_unique<KrylovWork>(x->f(), keep0, solver.max_iters, solver.tol, s));
+    for (uint64_t k = 1; k < L; ++k) {
+      const rmg_level_spec& sp = specs_[k - 1].spec;
+      const int keep = static_cast<int>(std::max<uint64_t>(sp.coarse_truncation, 1));
+      work_.push_back(
+          std::make_unique<KrylovWork>(level_matrix(k).f(), keep, sp.coarse_max_iters, sp.coarse_tol, s));
+    }
+    build_dense_levels(inv);
   }
   ctx_->sync();
+}
+
+// Dense persistent inner solves (dense_level.cu) for every inner level that
+// has at most 4096 unknowns and whose own preconditioner is linear (direct
+// coarsest level below it) or absent (inner_cg).
+void Method::build_dense_levels(const std::vector<double>& ainv_host) {
+  const size_t L = coarse_.size();
+  dense_.resize(L + 1);
+  if (std::getenv("RMG_DISABLE_DENSE_INNER") != nullptr) return;
+  cudaStream_t s = ctx_->stream;
+  const unsigned threads = std::max(1u, std::thread::hardware_concurrency());
+  for (size_t k = 1; k < L; ++k) {
+    const int kind = specs_[k - 1].spec.coarse_kind;
+    const bool fcg = kind == RMG_COARSE_INNER_FCG;
+    const int64_t n = level_matrix(k).f();
+    if (n > 4096 || (fcg && k + 1 != L)) continue;
+    auto d = std::make_unique<DenseInner>();
+    d->fcg = fcg;
+    d->omega = omega_[k];
+    const std::vector<double> a = coarse_gram(level_matrix(k).host, level_beta(k));  // X_k^T X_k + beta_k I
+    d->A.upload(a.data(), a.size(), s);
+    if (fcg) {  // Q = (I - omega A_k) P A_{k+1}^{-1}
+      const Aggregation& agg = coarse_[k]->agg;
+      const int64_t nc = agg.n_coarse;
+      d->nc = static_cast<int>(nc);
+      std::vector<double> g(static_cast<size_t>(n) * nc), q(static_cast<size_t>(n) * nc);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t c = 0; c < nc; ++c) g[i * nc + c] = agg.weight[i] * ainv_host[agg.label[i] * nc + c];
+      std::vector<std::thread> pool;
+      const int64_t step = (n + threads - 1) / threads;
+      for (unsigned t = 0; t < threads; ++t) {
+        const int64_t lo = std::min<int64_t>(n, t * step), hi = std::min<int64_t>(n, lo + step);
+        pool.emplace_back([&, lo, hi] {
+          std::vector<double> acc(nc);
+          for (int64_t i = lo; i < hi; ++i) {
+            std::fill(acc.begin(), acc.end(), 0.0);
+            for (int64_t j = 0; j < n; ++j) {
+              const double aij = a[i * n + j];
+              if (aij == 0.0) continue;
+              const double* gj = &g[j * nc];
+              for (int64_t c = 0; c < nc; ++c) acc[c] += aij * gj[c];
+            }
+            for (int64_t c = 0; c < nc; ++c) q[i * nc + c] = g[i * nc + c] - d->omega * acc[c];
+          }
+        });
+      }
+      for (auto& th : pool) th.join();
+      d->Q.upload(q.data(), q.size(), s);
+    }
+    d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
+    d->pap_ring.alloc(kMaxKeep + 2);
+    d->partials.alloc(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride);
+    d->cg_shared.alloc(4);
+    dense_[k] = std::move(d);
+  }
+}
+
+uint64_t Method::run_dense(size_t k, const double* rhs) {
+  DenseInner& d = *dense_[k];
+  KrylovWork& w = *work_[k];
+  DenseKrylovArgs a;
+  a.n = static_cast<int>(level_matrix(k).f());
+  a.nc = d.nc;
+  a.fcg = d.fcg ? 1 : 0;
+  a.keep = w.keep;
+  a.max_iters = static_cast<int>(std::min<uint64_t>(w.max_iters, INT32_MAX));
+  a.tol = specs_[k - 1].spec.coarse_tol;
+  a.omega = d.omega;
+  a.A = d.A.get();
+  a.Q = d.Q.get();
+  if (d.fcg) {
+    const CoarseLevelDev& c = *coarse_[k];
+    a.mptr = c.mptr.get();
+    a.members = c.members.get();
+    a.weight = c.weight.get();
+  }
+  a.b = rhs;
+  a.x = w.x.get();
+  a.r = w.r.get();
+  a.p_ring = w.p_ring.get();
+  a.ap_ring = w.ap_ring.get();
+  a.pap_ring = d.pap_ring.get();
+  a.partials = d.partials.get();
+  a.cg_rz_shared = d.cg_shared.get();
+  a.cg_beta_shared = d.cg_shared.get() + 2;
+  a.hist = w.hist.get();
+  a.sc = w.sc.get();
+  launch_dense_krylov(d.plan, a, ctx_->stream);
+  ctx_->launches += 1;
+  return 0;
 }
 
 const std::vector<int64_t>& Method::labels(size_t k) const {
@@ -423,8 +560,11 @@ uint64_t Method::precond(size_t k, const double* r, double* z) {
     ctx_->launches += 2;
   } else {
     ctx_->launches += 1;
-    inner = specs_[k].spec.coarse_kind == RMG_COARSE_INNER_FCG ? run_fcg(k + 1, rc, false, nullptr)
-                                                                : run_cg(k + 1, rc, nullptr, false, nullptr);
+    if (dense_[k + 1])
+      inner = run_dense(k + 1, rc);
+    else
+      inner = specs_[k].spec.coarse_kind == RMG_COARSE_INNER_FCG ? run_fcg(k + 1, rc, false, nullptr)
+                                                                  : run_cg(k + 1, rc, nullptr, false, nullptr);
     ec = work_[k + 1]->x.get();
   }
   double* z1 = work_[k]->z1.get();
@@ -436,7 +576,7 @@ uint64_t Method::precond(size_t k, const double* r, double* z) {
   a.out = z;
   a.beta = level_beta(k);
   a.omega = omega_[k];
-  level_matrix(k).apply(z1, Epi::Rich, a);
+  level_matrix(k).apply(z1, Epi::Rich, a, prof(k));
   return inner;
 }
 
@@ -470,8 +610,15 @@ uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out
   KrylovScalars hs = ctx_->read(w.sc.get());
   if (hs.status == 3) throw InvalidArgument("fcg: non-finite rhs");
   std::vector<uint64_t> inner;
+  const bool nested = k + 1 < coarse_.size() + 0 && k + 1 < work_.size();
+  KrylovWork* iw = nested ? work_[k + 1].get() : nullptr;
+  KrylovScalars ihs{};
   while (!hs.done) {
-    const uint64_t in = precond(k, w.r.get(), w.z.get());
+    precond(k, w.r.get(), w.z.get());
+    if (iw) {
+      launch_copy_inner_count(iw->sc.get(), w.sc.get(), w.inner_hist.get(), s);
+      ctx_->launches += 1;
+    }
     launch_fcg_gs(w.z.get(), w.ap_ring.get(), w.p_ring.get(), n, w.sc.get(), w.vw, s);
     XtArgs a;
     a.v = w.p_ring.get();
@@ -480,17 +627,35 @@ uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out
     a.beta = level_beta(k);
     a.sc = w.sc.get();
     a.ring_stride = static_cast<int>(n);
-    m.apply_ring(w.p_ring.get(), static_cast<int>(n), w.sc.get(), Epi::Fcg, a);
+    m.apply_ring(w.p_ring.get(), static_cast<int>(n), w.sc.get(), Epi::Fcg, a, prof(k));
     launch_fcg_axpy(w.x.get(), w.r.get(), w.p_ring.get(), w.ap_ring.get(), n, w.sc.get(), w.hist.get(), w.vw, s);
     ctx_->launches += 3;
-    hs = ctx_->read(w.sc.get());
-    if (rec) inner.push_back(in);
+    if (iw) {
+      ctx_->read2(w.sc.get(), &hs, iw->sc.get(), &ihs);
+      if (ihs.status == 1 || ihs.status == 2)
+        throw RuntimeError(std::string(ihs.status == 1 ? "fcg: breakdown, <p, Ap> = 0" : "fcg: <p, Ap> <= 0") +
+                           " at iteration " + std::to_string(ihs.it) + " of the level-" + std::to_string(k + 1) +
+                           " inner solve; operator is not positive definite");
+      if (ihs.status == 3) throw InvalidArgument("fcg: non-finite rhs in the level-" + std::to_string(k + 1) + " inner solve");
+    } else {
+      hs = ctx_->read(w.sc.get());
+    }
+    if (profiling_) collect_profiles();
     if (hs.status == 1) throw RuntimeError("fcg: breakdown, <p, Ap> = 0 at iteration " + std::to_string(hs.it));
     if (hs.status == 2)
       throw RuntimeError("fcg: <p, Ap> < 0 at iteration " + std::to_string(hs.it) +
                          "; operator is not positive definite");
   }
-  if (rec) record(ctx_, w, hs, inner, t0, out);
+  if (rec) {
+    if (iw && hs.it > 0) {
+      inner.resize(static_cast<size_t>(hs.it));
+      RMG_CK(cudaMemcpyAsync(inner.data(), w.inner_hist.get(), inner.size() * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, s));
+    } else if (hs.it > 0) {
+      inner.assign(static_cast<size_t>(hs.it), 0);  // direct coarse solve: zero inner iterations
+    }
+    record(ctx_, w, hs, inner, t0, out);
+  }
   return static_cast<uint64_t>(hs.it);
 }
 
@@ -514,11 +679,12 @@ uint64_t Method::run_cg(size_t k, const double* rhs, const double* inv, bool rec
     a.out = ap;
     a.beta = level_beta(k);
     a.sc = w.sc.get();
-    m.apply(p, Epi::Cg, a);
+    m.apply(p, Epi::Cg, a, prof(k));
     launch_cg_axpy(w.x.get(), w.r.get(), w.z.get(), inv, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s);
     launch_cg_update_p(p, z, n, w.sc.get(), s);
     ctx_->launches += 2;
-    hs = ctx_->read(w.sc.get());
+ hs = ctx_->read(w.sc.get());
+    if (profiling_) collect_profiles();
     if (hs.status == 2)
       throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
                          "; operator is not positive definite");
@@ -539,6 +705,16 @@ SolveResult Method::solve_rhs(const double* rhs, double* w_out) {
   const int64_t n = fine_->f();
   if (n) RMG_CK(cudaMemcpyAsync(w_out, work_[0]->x.get(), n * 8, cudaMemcpyDeviceToDevice, ctx_->stream));
   return res;
+}
+
+void Method::set_profiling(bool on) {
+  profiling_ = on;
+  while (prof_.size() < static_cast<size_t>(n_levels())) prof_.push_back(std::make_unique<OpProfile>());
+  for (auto& p : prof_) p->reset();
+}
+
+void Method::collect_profiles() {
+  for (auto& p : prof_) p->collect();
 }
 
 void Method::precondition(const double* r, double* z) {

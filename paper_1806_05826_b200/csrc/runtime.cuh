@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "dense_level.cuh"
 #include "host_setup.hpp"
 #include "kernels.cuh"
 #include "ridgemg_b200.h"
@@ -75,6 +76,8 @@ struct Context {
   ~Context();
   void sync();
   KrylovScalars read(const KrylovScalars* dev);
+  // read two scalar blocks with one synchronization (outer + inner solver)
+  void read2(const KrylovScalars* a, KrylovScalars* ha, const KrylovScalars* b, KrylovScalars* hb);
 };
 
 // One orientation of a sparse matrix on the device.
@@ -94,6 +97,22 @@ struct DeviceSchedule {
   void build(const HostCsr& xt, cudaStream_t s);
 };
 
+// In-situ timing of one level's operator kernels (CUDA events on the
+// launching stream around K1 and K2 of every application).
+struct OpProfile {
+  std::vector<cudaEvent_t> pool;  // triples (before K1, between, after K2)
+  size_t used = 0;
+  uint64_t count = 0;
+  double ms_k1 = 0.0, ms_k2 = 0.0;
+  OpProfile() = default;
+  OpProfile(const OpProfile&) = delete;
+  OpProfile& operator=(const OpProfile&) = delete;
+  ~OpProfile();
+  void mark(cudaStream_t s);   // records the next event of the current triple
+  void collect();              // after a stream sync: accumulate finished triples
+  void reset();
+};
+
 // X (N x F) and X^T on the device, with the X^T schedule and an N-vector scratch.
 struct Matrix {
   Context* ctx = nullptr;
@@ -108,8 +127,9 @@ struct Matrix {
   int64_t f() const { return host.f; }
   int64_t nnz() const { return host.nnz(); }
   // t = X v then the X^T epilogue; v may live in a ring (sc != nullptr)
-  void apply(const double* v, Epi epi, const XtArgs& args);
-  void apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args);
+  void apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof = nullptr);
+  void apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args,
+                  OpProfile* prof = nullptr);
   void spmv(const double* v, double* y);
   void spmv_t(const double* u, double* y);
   double lambda_max(double tol, uint64_t max_iters, uint64_t seed, uint64_t* iters, bool* conv);
@@ -143,6 +163,15 @@ struct CoarseLevelDev {
   double beta = 0.0;
 };
 
+// Dense persistent inner solve of one coarse level (dense_level.cu).
+struct DenseInner {
+  DenseKrylovPlan plan;
+  bool fcg = true;
+  double omega = 0.0;
+  int nc = 0;
+  DBuf<double> A, Q, pap_ring, partials, cg_shared;
+};
+
 struct SolveResult {
   uint64_t iterations = 0;
   bool converged = false;
@@ -168,11 +197,17 @@ class Method {
   int kind() const { return kind_; }
   rmg_solver_config solver;
   double time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms);
+  void set_profiling(bool on);
+  const OpProfile& profile(size_t level) const { return *prof_.at(level); }
 
  private:
   uint64_t precond(size_t k, const double* r, double* z);
   uint64_t run_fcg(size_t k, const double* rhs, bool record, SolveResult* out);
   uint64_t run_cg(size_t k, const double* rhs, const double* inv_diag, bool record, SolveResult* out);
+  OpProfile* prof(size_t k) { return profiling_ ? prof_[k].get() : nullptr; }
+  void collect_profiles();
+  bool profiling_ = false;
+  std::vector<std::unique_ptr<OpProfile>> prof_;
   Context* ctx_;
   Matrix* fine_;
   double beta_;
@@ -181,6 +216,9 @@ class Method {
   std::vector<std::unique_ptr<CoarseLevelDev>> coarse_;
   std::vector<double> omega_;
   std::vector<std::unique_ptr<KrylovWork>> work_;  // per level 0..L-1
+  std::vector<std::unique_ptr<DenseInner>> dense_;  // per level (nullptr: host-sequenced path)
+  void build_dense_levels(const std::vector<double>& ainv_host);
+  uint64_t run_dense(size_t k, const double* rhs);
   DBuf<double> ainv_, rc_last_, ec_last_;
   DBuf<double> inv_diag_;
   std::vector<std::vector<int64_t>> labels_;

@@ -471,6 +471,15 @@ class PreparedMethod:
         _lib.check(self.lib.rmg_method_level_matrix(self.h, k, _ptr(rp), _ptr(ci), _ptr(v)))
         return FeatureMatrix(n, info["n_features"], rp, ci, v)
 
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.check(self.lib.rmg_method_set_profiling(self.h, int(on)))
+
+    def profile(self, level: int):
+        """(applications, ms in K1, ms in K2) accumulated by in-situ profiling."""
+        n, k1, k2 = C.c_uint64(), C.c_double(), C.c_double()
+        _lib.check(self.lib.rmg_method_profile(self.h, level, C.byref(n), C.byref(k1), C.byref(k2)))
+        return n.value, k1.value, k2.value
+
     def time_operator(self, level: int = 0, reps: int = 20, flush_l2: bool = True):
         t, k1, k2 = C.c_double(), C.c_double(), C.c_double()
         _lib.check(self.lib.rmg_method_time_operator(self.h, level, reps, int(flush_l2), C.byref(t), C.byref(k1),
