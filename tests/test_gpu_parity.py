@@ -284,3 +284,49 @@ def test_errors_and_edges(gpu):
     pm4 = R.PreparedMethod(m, 1e-3, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-14, 2)))
     w, rep = pm4.solve(np.ones(12))
     assert not rep.converged and rep.iterations == 2
+
+
+# ---------------------------------------------------------------- BASELINE cfg 2 (scaled and full)
+def _cfg2_spec(ks, labels=None):
+    levels = []
+    for i, k in enumerate(ks):
+        last = i == len(ks) - 1
+        if labels is None:
+            cl = R.ClusteringChoice(kind=R.KMEANS, target_size=k, seed=0, normalize_columns=True)
+        else:
+            cl = R.ClusteringChoice(kind=R.IMPORTED, labels=labels[i], n_clusters=k)
+        levels.append(R.LevelSpec(clustering=cl, solver=R.CoarseSolveChoice(
+            kind=R.DIRECT_CHOLESKY if last else R.INNER_FCG, tol=1e-6, max_iters=500)))
+    return R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=levels, solver=R.SolverConfig(1e-6, 1000))
+
+
+def _csr_sha(x):
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(x.row_offsets, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(x.column_indices, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(x.value_array(), np.float64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name,n,f,ks", [("cfg2_small", 10000, 2000, [200, 20]),
+                                         ("cfg2_full", 100000, 20000, [2000, 200])])
+def test_cfg2_multilevel(gpu, name, n, f, ks):
+    g = load_golden(name)
+    x = R.synth_sparse_zipf(n, f, 40.0, 1.1, False, 0)
+    assert _csr_sha(x) == str(g["sha256"])  # generator pinned
+    m = dm(x)
+    pm = R.PreparedMethod(m, 1.0, _cfg2_spec(ks))
+    for i in range(len(ks)):  # k-means on normalised columns, bit-exact per level
+        assert np.array_equal(pm.labels(i), g[f"labels{i}"].astype(np.int64))
+    w, rep = pm.solve(g["b"])
+    assert rep.converged
+    assert abs(rep.iterations - int(g["ml_iterations"])) <= 2
+    assert rel_diff(w, g["ml_w"]) <= W_TOL
+    assert len(rep.inner_iterations) == rep.iterations
+    gi = g["ml_inner"].astype(np.int64)
+    # inner solves (tol 1e-6) track the reference's within a couple of iterations
+    assert np.mean(np.abs(rep.inner_iterations[:50].astype(np.int64) - gi[:50])) <= 2.0
+    cg = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 5000)))
+    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= 2
+    assert rel_diff(cg.w, g["cg_w"]) <= W_TOL
