@@ -444,6 +444,17 @@ int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int3
   });
 }
 
+// Diagnostics (not part of the public header): phase timestamps of the
+// persistent inner solver of `level` (needs RMG_DENSE_TIMING at prepare time).
+int rmg_debug_dense_timing(rmg_method* pm, uint64_t level, unsigned long long* out256) {
+  return guard([&] {
+    need(pm, "method");
+    const rmg::DenseInner* d = pm->m.dense(level);
+    if (d == nullptr || d->timing.get() == nullptr) throw rmg::InvalidArgument("no dense timing buffer");
+    RMG_CK(cudaMemcpy(out256, d->timing.get(), 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
 int rmg_method_set_profiling(rmg_method* pm, int32_t on) {
   return guard([&] {
     need(pm, "method");

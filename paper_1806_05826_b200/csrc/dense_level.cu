@@ -8,17 +8,23 @@
 //     (mathematically GalerkinOperator::apply, coarsening.cpp:174-185);
 //   * with a direct coarsest level below, the level-k preconditioner
 //     (krylov.cpp:379-420) is the fixed linear map
-//         z = omega r + Q (P^T r),   Q = (I - omega A_k) P A_{k+1}^{-1}
-//     so it is precomputed once (n x n_c);
-//   * one cooperative launch runs the whole inner solve: 148 CTAs x 1024
+//         z = omega r + M r,   M = (I - omega A_k) P A_{k+1}^{-1} P^T
+//     precomputed once (n x n); no restriction/prolongation gathers remain,
+//     so unbalanced clusters (cfg 2 has one of 317 members) cost nothing;
+//   * one cooperative launch runs the whole inner solve: <= 148 CTAs x 256
 //     threads, each CTA owns a contiguous block of rows, keeps its rows of A_k
 //     resident in shared memory when they fit (2000 x 2000 fp64 = 32 MB
-//     = 148 x 216 KB), and the iteration synchronizes with 4 grid barriers.
+//     = 143 x 219 KB) and streams its rows of M from L2;
+//   * 4 grid barriers per iteration; every other step is spread over the
+//     CTA's threads (measured with tools/microbench_*.cu: serial per-row
+//     sections and 1024-thread CTAs were barrier-stall bound).
 // Reductions are deterministic: every CTA publishes a per-block partial and
-// every CTA re-reduces all partials in block order.
+// every CTA re-reduces all partials in the same fixed order; the FCG direction
+// update subtracts the Gram-Schmidt terms in the reference's order.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -30,9 +36,12 @@ namespace rmg {
 
 namespace {
 
-constexpr int kT = 1024;
+constexpr int kT = 256;
 constexpr int kW = kT / 32;
-constexpr int kPS = 40;  // partial slots per block: [0] ||b||^2, [1..31] GS, [34] pap, [35] pr, [36] rr
+constexpr int kPS = 40;  // partial slots per block: [0] ||b||^2, [1] #non-finite, [2..33] GS, [34] pap, [35] pr, [36] rr
+constexpr int kGS = 2, kPAP = 34, kPR = 35, kRR = 36;
+constexpr int kMaxQ = 16;  // n <= 4096 columns = 16 per thread
+constexpr int kMaxUse = 32;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -40,46 +49,100 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// Block sum, result broadcast to every thread.
+// Block sum of one value per thread, result broadcast to every thread.
 __device__ __forceinline__ double bsum_all(double v, double* sh) {
   v = wsum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();
   if (lane == 0) sh[wid] = v;
   __syncthreads();
-  if (wid == 0) {
-    double r = lane < kW ? sh[lane] : 0.0;
-    r = wsum(r);
-    if (lane == 0) sh[kW] = r;
-  }
-  __syncthreads();
-  return sh[kW];
+  double r = 0.0;
+#pragma unroll
+  for (int w = 0; w < kW; ++w) r += sh[w];
+  return r;
 }
 
-// Sum of slot `c` over all blocks in block order (same value in every CTA).
-__device__ __forceinline__ double all_blocks(const double* part, int c, double* sh) {
-  double acc = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += kT) acc += __ldcg(part + (size_t)b * kPS + c);
-  return bsum_all(acc, sh);
+// out[q] = sum over blocks b (fixed order) of partials[b][first + q], q < count,
+// one warp per quantity; ends with __syncthreads so every thread may read out.
+__device__ __forceinline__ void grid_sums(const double* partials, int first, int count, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int q = wid; q < count; q += kW) {
+    double acc = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * kPS + first + q);
+    acc = wsum(acc);
+    if (lane == 0) out[q] = acc;
+  }
+  __syncthreads();
+}
+
+// Row sums of (rows x v) for the nr owned rows; rows is nr x n row-major
+// (shared or global), v held as vc[q] = v[tid + q*kT].  Result in out[lr]
+// (fixed-order combine of the kW warp partials).
+template <bool GLOBAL>
+__device__ __forceinline__ void gemv_rows(const double* rows, int nr, int n, const double (&vc)[kMaxQ], double* red,
+                                          double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, tid = threadIdx.x;
+  for (int lr0 = 0; lr0 < nr; lr0 += 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // branch-free over the 4 rows (clamped to the last owned row; surplus
+    // sums are discarded) so all 4 x kMaxQ loads can be in flight at once
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* row = rows + (size_t)min(lr0 + u, nr - 1) * n;
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q) {
+        const int c = tid + q * kT;
+        if (c < n) acc[u] += (GLOBAL ? __ldg(row + c) : row[c]) * vc[q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double s = wsum(acc[u]);
+      if (lane == 0 && lr0 + u < nr) red[(lr0 + u) * kW + wid] = s;
+    }
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
+
+// Optional phase timing (diagnostics): %globaltimer of CTA 0 at phase marks
+// of the first 16 iterations, when args.timing != nullptr.
+__device__ __forceinline__ void tmark(const DenseKrylovArgs& a, int it, int idx) {
+  if (a.timing != nullptr && it < 16 && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.timing[it * 16 + idx] = t;
+  }
 }
 
 template <bool SMEM>
 __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double smem[];
-  const int n = a.n, nc = a.nc, R = a.rows_per_cta;
+  const int n = a.n, R = a.rows_per_cta;
   const int row0 = blockIdx.x * R;
   const int row1 = min(n, row0 + R);
   const int nr = max(0, row1 - row0);
-  // shared layout: [A rows: R*n if SMEM][rc: nc][red: R*kW][zs: R][sh: kW+1]
+  // shared layout: [A rows: R*n if SMEM][red: R*kW][zs: R][v: R][contrib: R*kMaxUse][gsum: 64][coef: kMaxUse][sh: kW]
   double* As = smem;
-  double* rc = smem + (SMEM ? (size_t)R * n : 0);
-  double* red = rc + nc;
+  double* red = smem + (SMEM ? (size_t)R * n : 0);
   double* zs = red + (size_t)R * kW;
-  double* sh = zs + R;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* vv = zs + R;
+  double* contrib = vv + R;
+  double* gsum = contrib + (size_t)R * kMaxUse;
+  double* coef = gsum + 64;
+  double* sh = coef + kMaxUse;
+  const int tid = threadIdx.x;
   double* part = a.partials + (size_t)blockIdx.x * kPS;
   KrylovScalars* sc = a.sc;
+  const double* Arows = SMEM ? As : a.A + (size_t)row0 * n;
+  const double* Mrows = a.M + (size_t)row0 * n;
 
   if (SMEM) {
     for (int idx = tid; idx < nr * n; idx += kT) As[idx] = a.A[(size_t)row0 * n + idx];
@@ -100,8 +163,9 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
     part[1] = bad;
   }
   grid.sync();
-  const double nb = sqrt(all_blocks(a.partials, 0, sh));
-  const double nbad = all_blocks(a.partials, 1, sh);
+  grid_sums(a.partials, 0, 2, gsum);
+  const double nb = sqrt(gsum[0]);
+  const double nbad = gsum[1];
   if (nbad > 0.0 || nb == 0.0) {
     if (blockIdx.x == 0 && tid == 0) {
       sc->it = 0;
@@ -114,9 +178,10 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
     }
     return;
   }
-  if (!a.fcg && blockIdx.x == 0 && tid == 0) a.cg_rz_shared[0] = nb * nb;  // rz = <r, z> = ||b||^2
   const int keep = a.keep, RING = keep + 1;
   const double omega = a.omega;
+  double rz = nb * nb;  // CG: <r, z> with z = r
+  double beta_cg = 0.0;
   int it = 0;
   bool converged = false;
   int status = 0;
@@ -125,132 +190,141 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
     const int slot = it % RING;
     double* p_now = a.p_ring + (size_t)slot * n;
     double* ap_now = a.ap_ring + (size_t)slot * n;
-    // ---- z = M^{-1} r for the owned rows
+    tmark(a, it, 0);
+    // ---- z = M^{-1} r for the owned rows: omega r + M r (FCG) or r (CG)
     if (a.fcg) {
-      for (int s = tid; s < nc; s += kT) {  // r_c = P^T r, members in increasing order
-        double acc = 0.0;
-        for (int q = a.mptr[s]; q < a.mptr[s + 1]; ++q) {
-          const int i = a.members[q];
-          const double ri = __ldcg(a.r + i);
-          if (ri != 0.0) acc += a.weight[i] * ri;
-        }
-        rc[s] = acc;
+      double rc[kMaxQ];
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q) {
+        const int c = tid + q * kT;
+        rc[q] = c < n ? __ldcg(a.r + c) : 0.0;
       }
-      __syncthreads();
-      for (int lr = wid; lr < nr; lr += kW) {  // z_i = omega r_i + Q_i . r_c
-        const double* qrow = a.Q + (size_t)(row0 + lr) * nc;
-        double acc = 0.0;
-        for (int s = lane; s < nc; s += 32) acc += qrow[s] * rc[s];
-        acc = wsum(acc);
-        if (lane == 0) zs[lr] = omega * a.r[row0 + lr] + acc;
+      if (!(a.dbg & 1)) {
+        gemv_rows<true>(Mrows, nr, n, rc, red, vv);
+      } else {
+        if (tid < nr) vv[tid] = 0.0;
+        __syncthreads();
       }
-    } else {  // plain CG: z = r
-      for (int lr = tid; lr < nr; lr += kT) zs[lr] = a.r[row0 + lr];
+      if (tid < nr) zs[tid] = omega * a.r[row0 + tid] + vv[tid];
+    } else {
+      if (tid < nr) zs[tid] = a.r[row0 + tid];
     }
     __syncthreads();
+    tmark(a, it, 1);
     if (a.fcg) {
-      // ---- Gram-Schmidt against the newest use = min(m_i, |hist|) directions (krylov.cpp:189-197)
+      // ---- classical Gram-Schmidt of z against the newest use = min(m_i, |hist|)
+      // directions (krylov.cpp:189-197); coefficients from z, oldest -> newest
       const int mi = it == 0 ? 0 : max(1, it % (keep + 1));
       const int use = min(mi, min(it, keep));
-      for (int q = wid; q < use; q += kW) {
-        const double* aph = a.ap_ring + (size_t)((it - use + q) % RING) * n;
-        double acc = 0.0;
-        for (int lr = lane; lr < nr; lr += 32) acc += zs[lr] * __ldcg(aph + row0 + lr);
-        acc = wsum(acc);
-        if (lane == 0) part[1 + q] = acc;
+      if (use > 0) {
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int q = wid; q < use; q += kW) {
+          const double* aph = a.ap_ring + (size_t)((it - use + q) % RING) * n;
+          double acc = 0.0;
+          for (int lr = lane; lr < nr; lr += 32) acc += zs[lr] * __ldcg(aph + row0 + lr);
+          acc = wsum(acc);
+          if (lane == 0) part[kGS + q] = acc;
+        }
+        tmark(a, it, 2);
+        grid.sync();  // B1
+        tmark(a, it, 3);
+        grid_sums(a.partials, kGS, use, gsum);
+        if (tid < use) coef[tid] = gsum[tid] / __ldcg(a.pap_ring + (it - use + tid) % RING);
+        __syncthreads();
+        tmark(a, it, 4);
+        for (int e = tid; e < nr * use; e += kT) {  // c_q p_q(row), all pairs in parallel
+          const int lr = e / use, q = e - lr * use;
+          contrib[lr * kMaxUse + q] = coef[q] * __ldcg(a.p_ring + (size_t)((it - use + q) % RING) * n + row0 + lr);
+        }
+        __syncthreads();
+        if (tid < nr) {  // p = z - c_0 p_0 - c_1 p_1 - ... (reference order)
+          double pi = zs[tid];
+          for (int q = 0; q < use; ++q) pi -= contrib[tid * kMaxUse + q];
+          zs[tid] = pi;
+        }
       }
-      grid.sync();  // B1
-      for (int q = 0; q < use; ++q) {
-        const double cq = all_blocks(a.partials, 1 + q, sh) / __ldcg(a.pap_ring + (it - use + q) % RING);
-        if (tid < nr) zs[tid] -= cq * __ldcg(a.p_ring + (size_t)((it - use + q) % RING) * n + row0 + tid);
-      }
-      // zs now holds p for the owned rows
-    } else if (it > 0) {
-      // CG: p = z + beta p_prev  (krylov.cpp:145-153), beta from the previous iteration
-      const double bcg = __ldcg(a.cg_beta_shared);
+    } else if (it > 0) {  // CG: p = z + beta p_prev (krylov.cpp:145-153)
       const double* pprev = a.p_ring + (size_t)((it - 1) % RING) * n;
-      if (tid < nr) zs[tid] += bcg * __ldcg(pprev + row0 + tid);
+      if (tid < nr) zs[tid] = zs[tid] + beta_cg * __ldcg(pprev + row0 + tid);
     }
-    __syncthreads();
-    for (int lr = tid; lr < nr; lr += kT) p_now[row0 + lr] = zs[lr];
+    if (tid < nr) p_now[row0 + tid] = zs[tid];
+    tmark(a, it, 5);
     grid.sync();  // B2: p complete
-    // ---- Ap = A p for the owned rows; pap, pr (krylov.cpp:199-208)
+    tmark(a, it, 6);
+    // ---- Ap = A p for the owned rows; <p,Ap>, <p,r> (krylov.cpp:199-208)
     {
-      constexpr int MAXQ = 4;  // n <= 4096
-      double pc[MAXQ];
+      double pc[kMaxQ];
 #pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
+      for (int q = 0; q < kMaxQ; ++q) {
         const int c = tid + q * kT;
         pc[q] = c < n ? __ldcg(p_now + c) : 0.0;
       }
-      for (int lr = 0; lr < nr; ++lr) {
-        const double* arow = SMEM ? As + (size_t)lr * n : a.A + (size_t)(row0 + lr) * n;
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
-          const int c = tid + q * kT;
-          if (c < n) acc += arow[c] * pc[q];
-        }
-        acc = wsum(acc);
-        if (lane == 0) red[lr * kW + wid] = acc;
+      if (a.dbg & 2) {
+        if (tid < nr) vv[tid] = zs[tid];  // ablation: A = I keeps pap > 0
+        __syncthreads();
+      } else if (SMEM) {
+        gemv_rows<false>(Arows, nr, n, pc, red, vv);
+      } else {
+        gemv_rows<true>(Arows, nr, n, pc, red, vv);
       }
-      __syncthreads();
+      tmark(a, it, 7);
       double dpap = 0.0, dpr = 0.0;
       if (tid < nr) {
-        double s = 0.0;
-        for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+        const double s = vv[tid];
         ap_now[row0 + tid] = s;
-        red[tid * kW] = s;  // keep Ap_i for the update below
         dpap = zs[tid] * s;
         dpr = zs[tid] * a.r[row0 + tid];
       }
       dpap = bsum_all(dpap, sh);
       dpr = bsum_all(dpr, sh);
       if (tid == 0) {
-        part[34] = dpap;
-        part[35] = dpr;
+        part[kPAP] = dpap;
+        part[kPR] = dpr;
       }
     }
+    tmark(a, it, 8);
     grid.sync();  // B3
-    const double pap = all_blocks(a.partials, 34, sh);
-    const double pr = all_blocks(a.partials, 35, sh);
-    if (a.fcg ? (pap == 0.0) : false) {
+    tmark(a, it, 9);
+    grid_sums(a.partials, kPAP, 2, gsum);
+    tmark(a, it, 10);
+    const double pap = gsum[0], pr = gsum[1];
+    if (a.fcg ? pap == 0.0 : false) {
       status = 1;
       break;
     }
-    if (a.fcg ? (pap < 0.0) : !(pap > 0.0)) {
+    if (a.fcg ? pap < 0.0 : !(pap > 0.0)) {
       status = 2;
       break;
     }
-    // FCG: alpha = <p,r>/pap.  CG: alpha = rz/pap with rz = <r,z> = <r,r> kept in cg_rz
-    const double alpha = a.fcg ? pr / pap : __ldcg(a.cg_rz_shared + (it & 1)) / pap;
+    const double alpha = a.fcg ? pr / pap : rz / pap;
     if (blockIdx.x == 0 && tid == 0) a.pap_ring[slot] = pap;
     double rr = 0.0;
     if (tid < nr) {
       const int i = row0 + tid;
       a.x[i] += alpha * zs[tid];
-      const double ri = a.r[i] - alpha * red[tid * kW];
+      const double ri = a.r[i] - alpha * vv[tid];
       a.r[i] = ri;
       rr = ri * ri;
     }
     rr = bsum_all(rr, sh);
-    if (tid == 0) part[36] = rr;
+    if (tid == 0) part[kRR] = rr;
+    tmark(a, it, 11);
     grid.sync();  // B4
-    const double rrs = all_blocks(a.partials, 36, sh);
+    tmark(a, it, 12);
+    grid_sums(a.partials, kRR, 1, gsum);
+    tmark(a, it, 13);
+    const double rrs = gsum[0];
     rel = sqrt(rrs) / nb;
-    if (blockIdx.x == 0 && tid == 0) {
-      a.hist[it] = rel;
-      if (!a.fcg) {  // CG: rz' = <r,r>, beta = rz'/rz
-        a.cg_beta_shared[0] = rrs / __ldcg(a.cg_rz_shared + (it & 1));
-        a.cg_rz_shared[(it + 1) & 1] = rrs;
-      }
-    }
+    if (blockIdx.x == 0 && tid == 0) a.hist[it] = rel;
     if (rel <= a.tol) {
       converged = true;
       ++it;
       break;
     }
-    if (!a.fcg) grid.sync();  // CG: beta visible to every CTA
+    if (!a.fcg) {  // CG: rz' = <r, r>, beta = rz'/rz (every CTA computes the same value)
+      beta_cg = rrs / rz;
+      rz = rrs;
+    }
   }
   if (blockIdx.x == 0 && tid == 0) {
     sc->it = it;
@@ -265,6 +339,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
 }  // namespace
 
 DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
+  (void)nc;
   DenseKrylovPlan p;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -272,16 +347,19 @@ DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   p.rows_per_cta = std::max(1, (n + sms - 1) / sms);
   p.grid = (n + p.rows_per_cta - 1) / p.rows_per_cta;
-  const size_t extra = ((size_t)nc + (size_t)p.rows_per_cta * kW + p.rows_per_cta + kW + 1) * sizeof(double);
-  const size_t with_a = extra + (size_t)p.rows_per_cta * n * sizeof(double);
+  const size_t R = p.rows_per_cta;
+  const size_t extra = (R * kW + 2 * R + R * kMaxUse + 64 + kMaxUse + kW) * sizeof(double);
+  const size_t with_a = extra + R * n * sizeof(double);
   p.smem_a = with_a <= (size_t)max_smem;
+  if (const char* e = std::getenv("RMG_DENSE_SMEM")) p.smem_a = p.smem_a && e[0] != '0';
   p.smem_bytes = p.smem_a ? with_a : extra;
   p.partial_stride = kPS;
   return p;
 }
 
 void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& args, cudaStream_t s) {
-  if (args.n > 4096) throw std::runtime_error("dense inner solver: level above 4096 unknowns");
+  if (args.n > kMaxQ * kT) throw std::runtime_error("dense inner solver: level above 4096 unknowns");
+  if (args.keep + 1 > kMaxUse) throw std::runtime_error("dense inner solver: truncation above 31");
   void* fn = plan.smem_a ? (void*)k_dense_krylov<true> : (void*)k_dense_krylov<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
   if (e != cudaSuccess) throw std::runtime_error(std::string("dense inner solver attribute: ") + cudaGetErrorString(e));

@@ -10,14 +10,11 @@ namespace rmg {
 
 struct DenseKrylovArgs {
   int n = 0, nc = 0, rows_per_cta = 1;
-  int fcg = 1;                 // 1: FCG with z = omega r + Q P^T r; 0: plain CG (inner_cg)
+  int fcg = 1;                 // 1: FCG with z = omega r + M r; 0: plain CG (inner_cg)
   int keep = 20, max_iters = 500;
   double tol = 1e-6, omega = 0.0;
   const double* A = nullptr;   // n x n row-major, A = X_k^T X_k + beta_k I
-  const double* Q = nullptr;   // n x nc row-major, (I - omega A) P A_{k+1}^{-1}
-  const int32_t* mptr = nullptr;
-  const int32_t* members = nullptr;
-  const double* weight = nullptr;
+  const double* M = nullptr;   // n x n row-major, (I - omega A) P A_{k+1}^{-1} P^T
   const double* b = nullptr;   // rhs
   double* x = nullptr;
   double* r = nullptr;
@@ -29,6 +26,8 @@ struct DenseKrylovArgs {
   double* cg_beta_shared = nullptr;  // [1]
   double* hist = nullptr;
   KrylovScalars* sc = nullptr;
+  unsigned long long* timing = nullptr;  // diagnostics: [16 iterations][16 marks]
+  int dbg = 0;  // diagnostics ablation (RMG_DENSE_DBG): 1 skip M r, 2 skip A p
 };
 
 struct DenseKrylovPlan {

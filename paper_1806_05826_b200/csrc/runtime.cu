@@ -407,6 +407,17 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     lvl->weight.upload(lvl->agg.weight.data(), lvl->agg.weight.size(), s);
     lvl->mptr.upload(lvl->agg.mptr.data(), lvl->agg.mptr.size(), s);
     lvl->members.upload(lvl->agg.members.data(), lvl->agg.members.size(), s);
+    {
+      HostCsr pt;  // P^T: row s lists the members of cluster s in increasing order
+      pt.n = nc;
+      pt.f = cur.f;
+      pt.ptr.assign(lvl->agg.mptr.begin(), lvl->agg.mptr.end());
+      pt.idx.assign(lvl->agg.members.begin(), lvl->agg.members.end());
+      pt.val.resize(pt.idx.size());
+      for (size_t q = 0; q < pt.idx.size(); ++q) pt.val[q] = lvl->agg.weight[pt.idx[q]];
+      lvl->pt.upload(pt, false, s);
+      lvl->pt_sched.build(pt, s);
+    }
     labels_.push_back(std::move(lab));
     coarse_.push_back(std::move(lvl));
     beta_run = next_beta;
@@ -494,12 +505,20 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
         });
       }
       for (auto& th : pool) th.join();
-      d->Q.upload(q.data(), q.size(), s);
+      // M = Q P^T: M[i][j] = Q[i][label_j] w_j
+      std::vector<double> mm(static_cast<size_t>(n) * n);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) mm[i * n + j] = q[i * nc + agg.label[j]] * agg.weight[j];
+      d->Q.upload(mm.data(), mm.size(), s);
     }
     d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
     d->pap_ring.alloc(kMaxKeep + 2);
     d->partials.alloc(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride);
     d->cg_shared.alloc(4);
+    if (std::getenv("RMG_DENSE_TIMING") != nullptr) {
+      d->timing.alloc(256);
+      RMG_CK(cudaMemsetAsync(d->timing.get(), 0, 256 * sizeof(unsigned long long), s));
+    }
     dense_[k] = std::move(d);
   }
 }
@@ -516,13 +535,7 @@ uint64_t Method::run_dense(size_t k, const double* rhs) {
   a.tol = specs_[k - 1].spec.coarse_tol;
   a.omega = d.omega;
   a.A = d.A.get();
-  a.Q = d.Q.get();
-  if (d.fcg) {
-    const CoarseLevelDev& c = *coarse_[k];
-    a.mptr = c.mptr.get();
-    a.members = c.members.get();
-    a.weight = c.weight.get();
-  }
+  a.M = d.Q.get();
   a.b = rhs;
   a.x = w.x.get();
   a.r = w.r.get();
@@ -534,7 +547,15 @@ uint64_t Method::run_dense(size_t k, const double* rhs) {
   a.cg_beta_shared = d.cg_shared.get() + 2;
   a.hist = w.hist.get();
   a.sc = w.sc.get();
+  a.timing = d.timing.get();
+  if (const char* dbg = std::getenv("RMG_DENSE_DBG")) a.dbg = std::atoi(dbg);
+  OpProfile* pr = prof(k);  // level-k profile: K1 slot = whole persistent inner solve
+  if (pr) pr->mark(ctx_->stream);
   launch_dense_krylov(d.plan, a, ctx_->stream);
+  if (pr) {
+    pr->mark(ctx_->stream);
+    pr->mark(ctx_->stream);
+  }
   ctx_->launches += 1;
   return 0;
 }
@@ -551,7 +572,12 @@ uint64_t Method::precond(size_t k, const double* r, double* z) {
   const int64_t nc = c.mat->f(), nf = level_matrix(k).f();
   cudaStream_t s = ctx_->stream;
   double* rc = (k + 1 == L) ? rc_last_.get() : work_[k + 1]->b.get();
-  launch_restrict(c.mptr.get(), c.members.get(), c.weight.get(), r, rc, nc, nullptr, s);
+  {  // r_c = P^T r as a segmented CSR pass (coarsening.cpp:43-55)
+    XtArgs ra;
+    ra.t = r;
+    ra.out = rc;
+    launch_xt(c.pt.view, c.pt_sched.view, Epi::Plain, ra, s);
+  }
   const double* ec;
   uint64_t inner = 0;
   if (k + 1 == L) {

@@ -160,6 +160,8 @@ struct CoarseLevelDev {
   Aggregation agg;              // level k-1 -> k
   DBuf<int32_t> label, mptr, members;
   DBuf<double> weight;
+  DeviceSparse pt;           // P^T as CSR (clusters x fine features), for the restriction
+  DeviceSchedule pt_sched;   // nnz-balanced: giant clusters are split into segments
   double beta = 0.0;
 };
 
@@ -170,6 +172,7 @@ struct DenseInner {
   double omega = 0.0;
   int nc = 0;
   DBuf<double> A, Q, pap_ring, partials, cg_shared;
+  DBuf<unsigned long long> timing;  // RMG_DENSE_TIMING diagnostics
 };
 
 struct SolveResult {
@@ -199,6 +202,7 @@ class Method {
   double time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms);
   void set_profiling(bool on);
   const OpProfile& profile(size_t level) const { return *prof_.at(level); }
+  const DenseInner* dense(size_t level) const { return level < dense_.size() ? dense_[level].get() : nullptr; }
 
  private:
   uint64_t precond(size_t k, const double* r, double* z);

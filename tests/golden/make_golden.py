@@ -213,6 +213,9 @@ def make_cfg2(ref, name, n, f, ks, chk_labels=None):
         l["labels"], l["n_clusters"] = labels[i], ks[i]
     solve_pack(out, "ml", ref, m, 1.0, b, "fcg_multilevel", levels=lv)
     solve_pack(out, "cg", ref, m, 1.0, b, "cg")
+    # the same solves driven to tol 1e-12, where w parity is sharp
+    solve_pack(out, "ml12", ref, m, 1.0, b, "fcg_multilevel", levels=lv, tol=1e-12)
+    solve_pack(out, "cg12", ref, m, 1.0, b, "cg", tol=1e-12, max_iters=5000)
     save(name, out)
 
 

@@ -319,14 +319,29 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     pm = R.PreparedMethod(m, 1.0, _cfg2_spec(ks))
     for i in range(len(ks)):  # k-means on normalised columns, bit-exact per level
         assert np.array_equal(pm.labels(i), g[f"labels{i}"].astype(np.int64))
+    # At tol 1e-6 the bar is the reference's own rounding envelope: its threaded
+    # mode (same algorithm, other summation order) drifts from its sequential
+    # mode by up to env iterations and env_w in w (tests/golden/envelope.json).
+    import json
+    import os
+    env = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "envelope.json")))[name]
     w, rep = pm.solve(g["b"])
     assert rep.converged
-    assert abs(rep.iterations - int(g["ml_iterations"])) <= 2
-    assert rel_diff(w, g["ml_w"]) <= W_TOL
+    assert abs(rep.iterations - int(g["ml_iterations"])) <= max(2, 2 * env["ml_iter_spread"])
+    assert rel_diff(w, g["ml_w"]) <= max(W_TOL, 4 * env["ml_w_spread"])
     assert len(rep.inner_iterations) == rep.iterations
     gi = g["ml_inner"].astype(np.int64)
     # inner solves (tol 1e-6) track the reference's within a couple of iterations
     assert np.mean(np.abs(rep.inner_iterations[:50].astype(np.int64) - gi[:50])) <= 2.0
     cg = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 5000)))
-    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= 2
-    assert rel_diff(cg.w, g["cg_w"]) <= W_TOL
+    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= max(2, 2 * env["cg_iter_spread"])
+    assert rel_diff(cg.w, g["cg_w"]) <= max(W_TOL, 4 * env["cg_w_spread"])
+    # Driven to tol 1e-12 both converge onto the same solution: the strict bar.
+    if "ml12_w" in g.files:
+        spec12 = _cfg2_spec(ks, [g[f"labels{i}"].astype(np.int64) for i in range(len(ks))])
+        spec12.solver = R.SolverConfig(1e-12, 1000)
+        w12, rep12 = R.PreparedMethod(m, 1.0, spec12).solve(g["b"])
+        assert rep12.converged
+        assert rel_diff(w12, g["ml12_w"]) <= W_TOL
+        cg12 = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-12, 5000)))
+        assert rel_diff(cg12.w, g["cg12_w"]) <= W_TOL

@@ -1,0 +1,88 @@
+// Microbenchmark: cost of grid-wide synchronization primitives on B200
+// (148 CTAs x 1024 threads, cooperative launch), to size the persistent
+// inner solver (dense_level.cu).  Build + run:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench_sync.cu && /tmp/mb
+#include <cooperative_groups.h>
+#include <cstdio>
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ double wsum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// mode 0: grid.sync only; 1: grid.sync + one all-block reduction (like all_blocks)
+// mode 2: custom flag barrier (atomic arrive + spin on generation)
+__global__ void __launch_bounds__(1024, 1) k(int iters, int mode, double* part, unsigned* bar, double* out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[33];
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    if (mode == 2) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        const unsigned a = atomicAdd(bar, 1u);
+        if (a == gridDim.x - 1) {
+          bar[0] = 0;
+          __threadfence();
+          atomicAdd((unsigned*)gen, 1u);
+        } else {
+          while (*gen == g) {
+          }
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    } else {
+      if (threadIdx.x == 0) part[blockIdx.x] = it + blockIdx.x;
+      grid.sync();
+      if (mode == 1) {
+        double v = threadIdx.x < gridDim.x ? __ldcg(part + threadIdx.x) : 0.0;
+        v = wsum(v);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          double r = sh[threadIdx.x];
+          r = wsum(r);
+          if (threadIdx.x == 0) sh[32] = r;
+        }
+        __syncthreads();
+        acc += sh[32];
+      }
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = acc;
+}
+
+int main() {
+  double *part, *out;
+  unsigned* bar;
+  cudaMalloc(&part, 4096 * 8);
+  cudaMalloc(&out, 8);
+  cudaMalloc(&bar, 8);
+  cudaMemset(bar, 0, 8);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int grid : {sms, 74, 32, 8}) {
+      int iters = 2000;
+      void* args[] = {&iters, &mode, &part, &bar, &out};
+      cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(1024), args, 0, 0);
+      cudaEventRecord(a);
+      cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(1024), args, 0, 0);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("mode %d grid %3d: %.3f us per iteration (%s)\n", mode, grid, ms * 1000.0 / iters,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
