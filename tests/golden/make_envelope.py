@@ -34,7 +34,7 @@ for name, n, f, ks in (("cfg2_small", 10000, 2000, [200, 20]), ("cfg2_full", 100
                coarse_tol=1e-6, coarse_max_iters=500) for i, k in enumerate(ks)]
     e = {"ml_iterations_seq": int(g["ml_iterations"]), "cg_iterations_seq": int(g["cg_iterations"]),
          "threads": {}}
-    for th in (3, 8):
+    for th in [int(t) for t in (sys.argv[1:] or ["2", "3", "4", "5", "6", "7", "8"])]:
         ref.set_num_threads(th)
         s = ref.solve(m, 1.0, g["b"], "fcg_multilevel", levels=lv, tol=1e-6, max_iters=1000)
         c = ref.solve(m, 1.0, g["b"], "cg", tol=1e-6, max_iters=5000)
