@@ -240,9 +240,15 @@ def run_b200(args, cfg):
 
     t_setup = time.time()
     x = make_matrix(cfg)
-    m = R.DeviceMatrix(x, ctx)
+    comm = None
+    if args.shard:  # row-sharded fine operator: NCCL all-reduce of the F-vector per X^T pass
+        obj = [R.Comm.new_unique_id() if rank == 0 else None]
+        if pg:
+            pg.broadcast_object_list(obj, src=0)
+        comm = R.Comm(ctx, world, rank, obj[0])
+    m = R.DeviceMatrix(x, ctx, comm=comm)
     labels = None
-    if world > 1:  # rank 0 clusters once; replicas import its labels
+    if world > 1:  # rank 0 clusters once; the other ranks import its labels
         obj = [None]
         if rank == 0:
             pm0 = R.PreparedMethod(m, cfg["beta"], R.MethodSpec(kind=R.method_from_string(cfg["method"]),
@@ -261,7 +267,8 @@ def run_b200(args, cfg):
 
     dev = torch.device("cuda", local)
     nsteps = args.warmup + args.steps
-    bs = [torch.from_numpy(R.rng_normals(42 + rank * 10007 + s, x.n_samples)).to(dev) for s in range(nsteps)]
+    rseed = 0 if args.shard else rank * 10007  # sharded: every rank solves the same system
+    bs = [torch.from_numpy(R.rng_normals(42 + rseed + s, x.n_samples)).to(dev) for s in range(nsteps)]
     w = torch.empty(x.n_features, dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
@@ -293,7 +300,7 @@ def run_b200(args, cfg):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         total_ms = float(t.item())
-    solves = args.steps * world
+    solves = args.steps * (1 if args.shard else world)
     value = total_ms / solves  # whole-job ms per solve (replicas: aggregate throughput)
     ms_per_step = total_ms / args.steps
 
@@ -338,7 +345,7 @@ def run_b200(args, cfg):
     fine_bytes = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
 
     # e2e: host buffers through the C ABI (H2D of b, D2H of w inside each step)
-    pinned_b = [torch.from_numpy(R.rng_normals(42 + rank * 10007 + s, x.n_samples)).pin_memory()
+    pinned_b = [torch.from_numpy(R.rng_normals(42 + rseed + s, x.n_samples)).pin_memory()
                 for s in range(args.steps)]
     pinned_w = torch.empty(x.n_features, dtype=torch.float64).pin_memory()
     e2e_ms = []
@@ -381,14 +388,16 @@ def run_b200(args, cfg):
         inner = [float(np.mean(r.inner_iterations)) if len(r.inner_iterations) else 0.0 for r in timed]
         line = {
             "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "strong" if args.shard else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
             "config": {"workload": cfg["workload"], "n_samples": x.n_samples, "n_features": x.n_features,
                        "nnz": m.nnz, "levels": [x.n_features] + list(cfg["ks"]), "beta": cfg["beta"],
                        "tol": cfg["tol"], "method": cfg["method"],
                        "l2": "flushed (256 MiB write) before every timed step, outside its events",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"row-sharded x{world} (NCCL all-reduce of the F-vector)" if args.shard
+                                       else f"replicas x{world}" if world > 1 else "single GPU")},
             "iterations": its, "inner_iterations_mean": inner, "converged": all(r.converged for r in timed),
             "setup_s": setup_s,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -426,6 +435,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample-iters", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="row-shard X across ranks (strong scaling)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -140,6 +140,27 @@ int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device
 int rmg_lambda_max(rmg_matrix* m, double tol, uint64_t max_iters, uint64_t seed, double* value,
                    uint64_t* iterations, int32_t* converged);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * Row sharding of X across the GPUs of one node (one process per GPU,
+ * SURVEY.md §8(e)): each rank keeps an nnz-balanced contiguous block of rows
+ * of X (and its transpose) on its device; every X^T pass all-reduces the
+ * F-vector with NCCL over NVLink before the epilogue.  Krylov vectors and the
+ * coarse levels are replicated.  Rank 0 creates the unique id, the caller
+ * broadcasts it (e.g. torch.distributed), every rank creates its communicator. */
+typedef struct rmg_comm rmg_comm;
+#define RMG_UNIQUE_ID_BYTES 128
+int rmg_comm_unique_id(uint8_t* id_out);
+int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id, rmg_comm** out);
+int rmg_comm_destroy(rmg_comm* comm);
+/* Every rank passes the FULL matrix (needed for the replicated hierarchy setup);
+ * only this rank's row block is uploaded. */
+int rmg_matrix_create_csr_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t n_features,
+                                  const uint64_t* row_offsets, const uint64_t* column_indices,
+                                  const double* values, int32_t detect_pattern, rmg_matrix** out);
+int rmg_matrix_shard(const rmg_matrix* m, uint64_t* row0, uint64_t* row1, int32_t* nranks, int32_t* rank);
+/* The partition itself (host only): bounds_out[r]..bounds_out[r+1] for rank r. */
+int rmg_shard_rows(const uint64_t* row_offsets, uint64_t n_samples, int32_t nranks, uint64_t* bounds_out);
+
 /* ---------------------------------------------------------------- host helpers
  * generate_rhs (analysis.cpp:225-232): b_i = CounterRng(seed) normals
  * (rng.hpp:25-72, glibc libm), rhs = X^T b on the device.  rhs may be NULL. */

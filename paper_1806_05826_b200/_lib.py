@@ -95,6 +95,12 @@ SIGNATURES = {
     "rmg_method_level_matrix": [_P, _U64, _P, _P, _P],
     "rmg_solve_system": [_P, _D, _I32, _P, _U64, _P, _P, _P, _P, _P],
     "rmg_method_time_operator": [_P, _U64, _U64, _I32, _P, _P, _P],
+    "rmg_comm_unique_id": [_P],
+    "rmg_comm_create": [_P, _I32, _I32, _P, _PP],
+    "rmg_comm_destroy": [_P],
+    "rmg_matrix_create_csr_sharded": [_P, _P, _U64, _U64, _P, _P, _P, _I32, _PP],
+    "rmg_matrix_shard": [_P, _P, _P, _P, _P],
+    "rmg_shard_rows": [_P, _U64, _I32, _P],
     "rmg_method_set_profiling": [_P, _I32],
     "rmg_method_profile": [_P, _U64, _P, _P, _P],
 }

@@ -22,6 +22,19 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+def _nccl_dirs():
+    """NCCL matching the one torch loads (same SONAME -> one NCCL per process)."""
+    try:
+        import nvidia.nccl as nn  # torch's bundled NCCL (2.28.x)
+        base = os.path.dirname(nn.__file__) if nn.__file__ else list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -36,8 +49,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
+    nccl_inc, nccl_lib = _nccl_dirs()
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", CSRC, "-I",
-              os.path.join(ROOT, "include")]
+              os.path.join(ROOT, "include"), "-I", nccl_inc]
     objs = []
     procs = []
     for src in SOURCES:
@@ -54,8 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             print(out)
     link = [NVCC, *ARCH, "-shared", *objs, "-o", LIB + ".tmp", "-lcudart",
-            "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/lib/x86_64-linux-gnu", "-l:libstdc++.so.6",
-            "-lpthread"]
+            "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L" + nccl_lib, "-l:libnccl.so.2",
+            "-Xlinker", "-rpath," + nccl_lib, "-L/usr/lib/x86_64-linux-gnu", "-l:libstdc++.so.6", "-lpthread"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(link) + "\n" + r.stdout + r.stderr)

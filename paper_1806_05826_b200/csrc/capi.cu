@@ -16,10 +16,15 @@ struct rmg_context {
 };
 struct rmg_matrix {
   rmg::Matrix m;
-  rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect) : m(ctx, std::move(h), detect) {}
+  rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect, rmg::Comm* comm = nullptr)
+      : m(ctx, std::move(h), detect, comm) {}
 };
 struct rmg_host_csr {
   rmg::HostCsr h;
+};
+struct rmg_comm {
+  rmg::Comm c;
+  rmg_comm(int nranks, int rank, const ncclUniqueId& id, int device) : c(nranks, rank, id, device) {}
 };
 struct rmg_method {
   rmg::Method m;
@@ -156,6 +161,72 @@ int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n, uint64_t f, const uint64
   });
 }
 
+int rmg_comm_unique_id(uint8_t* id_out) {
+  return guard([&] {
+    need(id_out, "id_out");
+    static_assert(sizeof(ncclUniqueId) == RMG_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    const ncclResult_t e = ncclGetUniqueId(&id);
+    if (e != ncclSuccess) throw rmg::CudaError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(e));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id, rmg_comm** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(id, "id");
+    need(out, "out");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    *out = new rmg_comm(nranks, rank, uid, ctx->c.device);
+  });
+}
+
+int rmg_comm_destroy(rmg_comm* comm) {
+  return guard([&] { delete comm; });
+}
+
+int rmg_matrix_create_csr_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n, uint64_t f, const uint64_t* rp,
+                                  const uint64_t* ci, const double* values, int32_t detect_pattern, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(comm, "comm");
+    need(out, "out");
+    need(rp, "row_offsets");
+    rmg::HostCsr h;
+    h.n = static_cast<int64_t>(n);
+    h.f = static_cast<int64_t>(f);
+    h.ptr.assign(rp, rp + n + 1);
+    const uint64_t nnz = rp[n];
+    if (nnz) need(ci, "column_indices");
+    h.idx.assign(ci, ci + nnz);
+    if (values) h.val.assign(values, values + nnz);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, std::move(h), detect_pattern != 0, &comm->c);
+  });
+}
+
+int rmg_matrix_shard(const rmg_matrix* m, uint64_t* row0, uint64_t* row1, int32_t* nranks, int32_t* rank) {
+  return guard([&] {
+    need(m, "matrix");
+    if (row0) *row0 = static_cast<uint64_t>(m->m.row0);
+    if (row1) *row1 = static_cast<uint64_t>(m->m.row1);
+    if (nranks) *nranks = m->m.comm ? m->m.comm->nranks : 1;
+    if (rank) *rank = m->m.comm ? m->m.comm->rank : 0;
+  });
+}
+
+int rmg_shard_rows(const uint64_t* rp, uint64_t n, int32_t nranks, uint64_t* bounds_out) {
+  return guard([&] {
+    need(rp, "row_offsets");
+    need(bounds_out, "bounds_out");
+    const std::vector<int64_t> p(rp, rp + n + 1);
+    const std::vector<int64_t> b = rmg::partition_rows(p, nranks);
+    for (size_t i = 0; i < b.size(); ++i) bounds_out[i] = static_cast<uint64_t>(b[i]);
+  });
+}
+
 int rmg_matrix_destroy(rmg_matrix* m) {
   return guard([&] { delete m; });
 }
@@ -221,7 +292,7 @@ int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device
     RMG_CK(cudaSetDevice(c.device));
     rmg::DBuf<double> bo;
     double* d = stage_out(m->m.f(), on_device, out, bo);
-    rmg::launch_diag_gram(m->m.xt.view, beta, d, c.stream);
+    m->m.gram_diagonal(beta, d);
     finish_out(c, d, out, m->m.f(), on_device);
   });
 }
@@ -451,7 +522,7 @@ int rmg_debug_dense_timing(rmg_method* pm, uint64_t level, unsigned long long* o
     need(pm, "method");
     const rmg::DenseInner* d = pm->m.dense(level);
     if (d == nullptr || d->timing.get() == nullptr) throw rmg::InvalidArgument("no dense timing buffer");
-    RMG_CK(cudaMemcpy(out256, d->timing.get(), 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    RMG_CK(cudaMemcpy(out256, d->timing.get(), 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 

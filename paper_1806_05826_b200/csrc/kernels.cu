@@ -78,12 +78,16 @@ __device__ __forceinline__ double sum_slots(const double* slots, int n, int stri
 __device__ __forceinline__ int ring_slot(const KrylovScalars* sc) { return sc->it % (sc->keep + 1); }
 
 // ------------------------------------------------------------------ K1: t = X v
-// Row-parallel CSR gather; W lanes per row, warp-uniform trip counts so the
-// group reductions never diverge.  Per-row sum order: lane-strided partials
-// then an xor tree (deterministic).
-template <int W, bool PAT>
+// Row-parallel CSR gather; W lanes per row, two rows per lane group in flight
+// and 4 elements per lane per round, so each thread keeps up to 8 index loads
+// and 8 gathers outstanding (the first version was long-scoreboard bound at
+// 1 TB/s, profiles/r1_ncu_summary.md).  Column indices are uint16 when F <=
+// 65536 (half the index stream).  Warp-uniform trip counts keep the group
+// reductions convergent.  Per-row order: lane-strided partials, xor tree.
+template <int W, bool PAT, bool NARROW>
 __global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restrict__ ptr,
                                                         const int32_t* __restrict__ idx,
+                                                        const uint16_t* __restrict__ idx16,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ v,
                                                         double* __restrict__ t, int64_t rows,
@@ -94,23 +98,44 @@ __global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restric
     if (sc->done) return;
     v += (size_t)ring_slot(sc) * ring_stride;
   }
-  constexpr int G = 32 / W;  // rows per warp
+  constexpr int G = 32 / W;  // rows per warp per pass
+  constexpr int U = 4;       // elements per lane per round
   const int lane = threadIdx.x & (W - 1);
   const int grp = (threadIdx.x & 31) / W;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-  for (int64_t rb = warp * G; rb < rows; rb += nwarps * G) {
-    const int64_t row = rb + grp;
-    double s = 0.0;
-    if (row < rows) {
-      const int k1 = ptr[row + 1];
-      for (int k = ptr[row] + lane; k < k1; k += W) {
-        const double x = __ldg(v + idx[k]);
-        s += PAT ? x : val[k] * x;
+  const int64_t span = nwarps * G;
+  for (int64_t rb = warp * G; rb < rows; rb += 2 * span) {
+    const int64_t ra = rb + grp, rbb = rb + span + grp;
+    const int a0 = ra < rows ? ptr[ra] : 0, a1 = ra < rows ? ptr[ra + 1] : 0;
+    const int b0 = rbb < rows ? ptr[rbb] : 0, b1 = rbb < rows ? ptr[rbb + 1] : 0;
+    double sa = 0.0, sb = 0.0;
+    for (int ka = a0 + lane, kb = b0 + lane; ka < a1 || kb < b1; ka += U * W, kb += U * W) {
+      int ca[U], cb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int pa = ka + u * W, pb = kb + u * W;
+        ca[u] = pa < a1 ? (NARROW ? (int)idx16[pa] : idx[pa]) : -1;
+        cb[u] = pb < b1 ? (NARROW ? (int)idx16[pb] : idx[pb]) : -1;
+      }
+      double xa[U], xb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xa[u] = ca[u] >= 0 ? __ldg(v + ca[u]) : 0.0;
+        xb[u] = cb[u] >= 0 ? __ldg(v + cb[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ca[u] >= 0) sa += PAT ? xa[u] : val[ka + u * W] * xa[u];
+        if (cb[u] >= 0) sb += PAT ? xb[u] : val[kb + u * W] * xb[u];
       }
     }
-    s = group_sum<W>(s);
-    if (row < rows && lane == 0) t[row] = s;
+    sa = group_sum<W>(sa);
+    sb = group_sum<W>(sb);
+    if (lane == 0) {
+      if (ra < rows) t[ra] = sa;
+      if (rbb < rows) t[rbb] = sb;
+    }
   }
 }
 
@@ -148,7 +173,69 @@ constexpr bool has_dots() {
   return E == Epi::Fcg || E == Epi::Cg || E == Epi::Gram;
 }
 
-template <int W, bool PAT, Epi E>
+// Scalar finalization of the dot-carrying epilogues (one thread).
+template <Epi E>
+__device__ __forceinline__ void xt_finalize(KrylovScalars* sc, double s0, double s1) {
+  if constexpr (E == Epi::Fcg) {  // krylov.cpp:199-208
+    sc->pap = s0;
+    sc->pr = s1;
+    if (s0 == 0.0) {
+      sc->status = 1;
+      sc->done = 1;
+    } else if (s0 < 0.0) {
+      sc->status = 2;
+      sc->done = 1;
+    } else {
+      sc->alpha = s1 / s0;
+      sc->pap_ring[ring_slot(sc)] = s0;
+    }
+  } else if constexpr (E == Epi::Cg) {  // krylov.cpp:126-134
+    sc->pap = s0;
+    if (!(s0 > 0.0)) {
+      sc->status = 2;
+      sc->done = 1;
+    } else {
+      sc->alpha = sc->rz / s0;
+    }
+  } else if constexpr (E == Epi::Gram) {  // lambda = ||A v|| (krylov.cpp:80-81)
+    sc->lambda = sqrt(s0);
+  }
+}
+
+// Gather index of element k of virtual row vrow: sample-blocked layout keeps
+// uint16 offsets inside a block of B samples.
+template <bool BLK>
+__device__ __forceinline__ int xt_col(const XtSchedule& sch, const int32_t* __restrict__ idx, int64_t base, int k) {
+  if constexpr (BLK) return (int)(base + sch.idx16[k]);
+  return idx[k];
+}
+
+// Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 4 elements per
+// lane per round (independent loads in flight); lane-strided order.
+template <bool PAT, bool BLK>
+__device__ __forceinline__ double xt_row_sum(const XtSchedule& sch, const int32_t* __restrict__ idx,
+                                             const double* __restrict__ val, const double* __restrict__ t,
+                                             int64_t base, int k0, int k1, int lane, int lanes) {
+  double s = 0.0;
+  for (int k = k0 + lane; k < k1; k += 4 * lanes) {
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = k + u * lanes < k1 ? xt_col<BLK>(sch, idx, base, k + u * lanes) : -1;
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c[u] >= 0) s += PAT ? x[u] : val[k + u * lanes] * x[u];
+  }
+  return s;
+}
+
+// K2: one work item per CTA (see XtSchedule).  Short rows take W lanes, medium
+// rows a full warp, long rows fixed CTA-wide segments combined in segment
+// order by the last-arriving CTA.  Unblocked: the epilogue runs here.  Blocked
+// (BLK): writes per-block partials (E == Plain), k_xt_finish does the rest.
+template <int W, bool PAT, Epi E, bool BLK>
 __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr,
                                                  const int32_t* __restrict__ idx,
                                                  const double* __restrict__ val, XtSchedule sch,
@@ -168,25 +255,30 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
   __shared__ int s_fin;
   const double* __restrict__ t = a.t;
   const int4 item = sch.items[blockIdx.x];
+  const int64_t F = sch.features;
   double d0 = 0.0, d1 = 0.0;
-  if (item.z < 0) {
-    // short columns [item.x, item.y): W lanes per column
-    constexpr int G = 32 / W;
-    const int lane = threadIdx.x & (W - 1);
-    const int grp = (threadIdx.x & 31) / W;
+  if (item.z == -1 || item.z == -2) {
+    const bool medium = item.z == -2;
+    const int lanes = medium ? 32 : W;
+    const int per_warp = 32 / lanes;
+    const int lane = threadIdx.x & (lanes - 1);
+    const int grp = (threadIdx.x & 31) / lanes;
     const int wid = threadIdx.x >> 5;
-    for (int cb = item.x + wid * G; cb < item.y; cb += kWarps * G) {
-      const int col = cb + grp;
+    for (int qb = item.x + wid * per_warp; qb < item.y; qb += kWarps * per_warp) {
+      const int q = qb + grp;
+      int vrow = -1;
       double s = 0.0;
-      if (col < item.y) {
-        const int k1 = ptr[col + 1];
-        for (int k = ptr[col] + lane; k < k1; k += W) {
-          const double x = __ldg(t + idx[k]);
-          s += PAT ? x : val[k] * x;
-        }
+      if (q < item.y) {
+        vrow = sch.perm[q];
+        const int64_t base = BLK ? (int64_t)(vrow / F) * sch.block_rows : 0;
+        s = xt_row_sum<PAT, BLK>(sch, idx, val, t, base, ptr[vrow], ptr[vrow + 1], lane, lanes);
       }
-      s = group_sum<W>(s);
-      if (col < item.y && lane == 0) xt_epilogue<E>(col, s, a, v, out, d0, d1);
+      if (medium) {
+        s = warp_sum(s);
+      } else {
+        s = group_sum<W>(s);
+      }
+      if (vrow >= 0 && lane == 0) xt_epilogue<E>(vrow, s, a, v, out, d0, d1);
     }
     if constexpr (has_dots<E>()) {
       const double b0 = block_sum(d0, sh);
@@ -197,12 +289,10 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
       }
     }
   } else {
-    // one fixed segment [item.y, item.z) of long column item.x
-    double s = 0.0;
-    for (int k = item.y + threadIdx.x; k < item.z; k += kThreads) {
-      const double x = __ldg(t + idx[k]);
-      s += PAT ? x : val[k] * x;
-    }
+    // one fixed segment [item.y, item.z) of long row long_col[item.x]
+    const int vrow = sch.long_col[item.x];
+    const int64_t base = BLK ? (int64_t)(vrow / F) * sch.block_rows : 0;
+    double s = xt_row_sum<PAT, BLK>(sch, idx, val, t, base, item.y, item.z, threadIdx.x, kThreads);
     s = block_sum(s, sh);
     if (threadIdx.x == 0) {
       sch.seg_partial[item.w] = s;
@@ -215,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
         const int first = sch.long_first_seg[item.x], nseg = sch.long_nseg[item.x];
         double tot = 0.0;
         for (int q = 0; q < nseg; ++q) tot += __ldcg(sch.seg_partial + first + q);
-        xt_epilogue<E>(sch.long_col[item.x], tot, a, v, out, d0, d1);
+        xt_epilogue<E>(vrow, tot, a, v, out, d0, d1);
         if constexpr (has_dots<E>()) {
           const int slot = sch.long_slot[item.x];
           sch.slots[(size_t)slot * 2] = d0;
@@ -228,33 +318,45 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
     if (grid_last(sch.grid_ticket)) {
       const double s0 = sum_slots(sch.slots, sch.n_slots, 2, 0, sh);
       const double s1 = (E == Epi::Fcg) ? sum_slots(sch.slots, sch.n_slots, 2, 1, sh) : 0.0;
-      if (threadIdx.x == 0) {
-        KrylovScalars* sc = a.sc;
-        if constexpr (E == Epi::Fcg) {  // krylov.cpp:199-208
-          sc->pap = s0;
-          sc->pr = s1;
-          if (s0 == 0.0) {
-            sc->status = 1;
-            sc->done = 1;
-          } else if (s0 < 0.0) {
-            sc->status = 2;
-            sc->done = 1;
-          } else {
-            sc->alpha = s1 / s0;
-            sc->pap_ring[ring_slot(sc)] = s0;
-          }
-        } else if constexpr (E == Epi::Cg) {  // krylov.cpp:126-134
-          sc->pap = s0;
-          if (!(s0 > 0.0)) {
-            sc->status = 2;
-            sc->done = 1;
-          } else {
-            sc->alpha = sc->rz / s0;
-          }
-        } else {  // Gram: lambda = ||A v|| (krylov.cpp:80-81)
-          sc->lambda = sqrt(s0);
-        }
-      }
+      if (threadIdx.x == 0) xt_finalize<E>(a.sc, s0, s1);
+    }
+  }
+}
+
+// Sample-blocked X^T finishing pass: s_j = sum over blocks (in block order) of
+// the partials, then the epilogue and the deterministic dot reduction.
+template <Epi E>
+__global__ void __launch_bounds__(kThreads) k_xt_finish(XtSchedule sch, XtArgs a) {
+  if (a.done != nullptr && *a.done) return;
+  const double* v = a.v;
+  double* out = a.out;
+  if constexpr (E == Epi::Fcg) {
+    if (a.sc->done) return;
+    const size_t off = (size_t)ring_slot(a.sc) * a.ring_stride;
+    v += off;
+    out += off;
+  } else if constexpr (E == Epi::Cg) {
+    if (a.sc->done) return;
+  }
+  __shared__ double sh[kWarps];
+  const int64_t F = sch.features;
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < F; j += (int64_t)gridDim.x * kThreads) {
+    double s = 0.0;
+    for (int b = 0; b < sch.n_blocks; ++b) s += sch.partial[(size_t)b * F + j];
+    xt_epilogue<E>((int)j, s, a, v, out, d0, d1);
+  }
+  if constexpr (has_dots<E>()) {
+    const double b0 = block_sum(d0, sh);
+    const double b1 = (E == Epi::Fcg) ? block_sum(d1, sh) : 0.0;
+    if (threadIdx.x == 0) {
+      sch.fin_slots[blockIdx.x * 2] = b0;
+      sch.fin_slots[blockIdx.x * 2 + 1] = b1;
+    }
+    if (grid_last(sch.fin_ticket)) {
+      const double s0 = sum_slots(sch.fin_slots, gridDim.x, 2, 0, sh);
+      const double s1 = (E == Epi::Fcg) ? sum_slots(sch.fin_slots, gridDim.x, 2, 1, sh) : 0.0;
+      if (threadIdx.x == 0) xt_finalize<E>(a.sc, s0, s1);
     }
   }
 }
@@ -541,12 +643,15 @@ __global__ void k_scale_by_lambda(const double* __restrict__ w, double* __restri
 // d_j = beta + sum_r X(r,j)^2 in increasing r (ridge.cpp:30-37 storage order)
 template <bool PAT>
 __global__ void k_diag_gram(const int32_t* __restrict__ ptr, const double* __restrict__ val, int64_t f,
-                            double beta, double* __restrict__ out) {
+                            int n_blocks, double beta, double* __restrict__ out) {
   grid_stride(f, [&](int64_t j) {
     double d = beta;
-    for (int k = ptr[j]; k < ptr[j + 1]; ++k) {
-      const double x = PAT ? 1.0 : val[k];
-      d = __dadd_rn(d, __dmul_rn(x, x));  // uncontracted: bit-equal to ridge.cpp:34
+    for (int b = 0; b < n_blocks; ++b) {  // sample blocks in order = increasing sample
+      const int64_t row = (int64_t)b * f + j;
+      for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
+        const double x = PAT ? 1.0 : val[k];
+        d = __dadd_rn(d, __dmul_rn(x, x));  // uncontracted: bit-equal to ridge.cpp:34
+      }
     }
     out[j] = d;
   });
@@ -574,8 +679,13 @@ int grid_for(int64_t work_threads, int cap) {
 template <int W, bool PAT>
 void spmv_rows_impl(const SparseDev& x, const double* v, double* t, const int32_t* done,
                     const KrylovScalars* sc, int ring_stride, cudaStream_t s) {
-  const int grid = grid_for(x.rows * W, 148 * 16);
-  k_spmv_rows<W, PAT><<<grid, kThreads, 0, s>>>(x.ptr, x.idx, x.val, v, t, x.rows, done, sc, ring_stride);
+  const int grid = grid_for((x.rows + 1) / 2 * W, 148 * 8);
+  if (x.idx16 != nullptr)
+    k_spmv_rows<W, PAT, true><<<grid, kThreads, 0, s>>>(x.ptr, x.idx, x.idx16, x.val, v, t, x.rows, done, sc,
+                                                        ring_stride);
+  else
+    k_spmv_rows<W, PAT, false><<<grid, kThreads, 0, s>>>(x.ptr, x.idx, x.idx16, x.val, v, t, x.rows, done, sc,
+                                                         ring_stride);
 }
 
 template <bool PAT>
@@ -592,13 +702,28 @@ void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* 
 template <int W, bool PAT>
 void xt_impl_w(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
   const dim3 grid(sch.n_items), block(kThreads);
+  if (sch.blocked) {  // per-block partials, then the finishing epilogue pass
+    XtArgs pa = a;
+    pa.out = sch.partial;
+    k_xt<W, PAT, Epi::Plain, true><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, pa);
+    const dim3 fg(sch.fin_grid);
+    switch (epi) {
+      case Epi::Plain: k_xt_finish<Epi::Plain><<<fg, block, 0, s>>>(sch, a); break;
+      case Epi::Axpby: k_xt_finish<Epi::Axpby><<<fg, block, 0, s>>>(sch, a); break;
+      case Epi::Fcg: k_xt_finish<Epi::Fcg><<<fg, block, 0, s>>>(sch, a); break;
+      case Epi::Cg: k_xt_finish<Epi::Cg><<<fg, block, 0, s>>>(sch, a); break;
+      case Epi::Rich: k_xt_finish<Epi::Rich><<<fg, block, 0, s>>>(sch, a); break;
+      case Epi::Gram: k_xt_finish<Epi::Gram><<<fg, block, 0, s>>>(sch, a); break;
+    }
+    return;
+  }
   switch (epi) {
-    case Epi::Plain: k_xt<W, PAT, Epi::Plain><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Axpby: k_xt<W, PAT, Epi::Axpby><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Fcg: k_xt<W, PAT, Epi::Fcg><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Cg: k_xt<W, PAT, Epi::Cg><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Rich: k_xt<W, PAT, Epi::Rich><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Gram: k_xt<W, PAT, Epi::Gram><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Plain: k_xt<W, PAT, Epi::Plain, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Axpby: k_xt<W, PAT, Epi::Axpby, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Fcg: k_xt<W, PAT, Epi::Fcg, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Cg: k_xt<W, PAT, Epi::Cg, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Rich: k_xt<W, PAT, Epi::Rich, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Gram: k_xt<W, PAT, Epi::Gram, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
   }
 }
 
@@ -633,6 +758,26 @@ void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_st
   else
     spmv_rows_w<false>(x, v_ring, t, nullptr, sc, ring_stride, s);
   check_launch("spmv_rows_ring");
+}
+
+void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtArgs& a, double* fin_slots,
+                        unsigned* fin_ticket, int fin_grid, cudaStream_t s) {
+  XtSchedule sch;
+  sch.features = features;
+  sch.n_blocks = 1;
+  sch.partial = const_cast<double*>(sums);
+  sch.fin_slots = fin_slots;
+  sch.fin_ticket = fin_ticket;
+  const dim3 fg(fin_grid), block(kThreads);
+  switch (epi) {
+    case Epi::Plain: k_xt_finish<Epi::Plain><<<fg, block, 0, s>>>(sch, a); break;
+    case Epi::Axpby: k_xt_finish<Epi::Axpby><<<fg, block, 0, s>>>(sch, a); break;
+    case Epi::Fcg: k_xt_finish<Epi::Fcg><<<fg, block, 0, s>>>(sch, a); break;
+    case Epi::Cg: k_xt_finish<Epi::Cg><<<fg, block, 0, s>>>(sch, a); break;
+    case Epi::Rich: k_xt_finish<Epi::Rich><<<fg, block, 0, s>>>(sch, a); break;
+    case Epi::Gram: k_xt_finish<Epi::Gram><<<fg, block, 0, s>>>(sch, a); break;
+  }
+  check_launch("xt_epilogue");
 }
 
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
@@ -702,11 +847,13 @@ void launch_scale_by_lambda(const double* w, double* v, int64_t n, const KrylovS
   check_launch("scale_by_lambda");
 }
 
-void launch_diag_gram(const SparseDev& xt, double beta, double* out, cudaStream_t s) {
+void launch_diag_gram(const SparseDev& xt, const XtSchedule& sch, double beta, double* out, cudaStream_t s) {
+  const int64_t f = sch.features;
+  const int nb = sch.blocked ? sch.n_blocks : 1;
   if (xt.val == nullptr)
-    k_diag_gram<true><<<grid_for(xt.rows, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, xt.rows, beta, out);
+    k_diag_gram<true><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, nb, beta, out);
   else
-    k_diag_gram<false><<<grid_for(xt.rows, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, xt.rows, beta, out);
+    k_diag_gram<false><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, nb, beta, out);
   check_launch("diag_gram");
 }
 

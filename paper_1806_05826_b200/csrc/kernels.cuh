@@ -47,17 +47,32 @@ struct SparseDev {
   int64_t rows = 0, cols = 0, nnz = 0;
   const int32_t* ptr = nullptr;
   const int32_t* idx = nullptr;
+  const uint16_t* idx16 = nullptr;  // narrow column indices when cols <= 65536 (K1)
   const double* val = nullptr;  // nullptr -> binary pattern
   int width = 8;                // lanes per row (4, 8, 16, 32)
 };
 
-// Work items for the X^T pass.  Short item: a contiguous range of feature
-// columns whose total nnz fits one CTA; long item: one fixed segment of a
-// feature column that is longer than that.
+// Work items for the X^T pass, by row-length class of the (virtual) X^T CSR:
+//   short : {q_begin, q_end, -1, slot}  rows perm[q_begin..q_end), W lanes each
+//   medium: {q_begin, q_end, -2, slot}  rows perm[..], one warp each
+//   long  : {long_id, nz_begin, nz_end, seg_id}  one fixed segment, whole CTA
+// With sample blocking (`blocked`), X^T is stored per block of B samples
+// (virtual row = block * F + feature, uint16 sample offsets inside the block):
+// a CTA's t-gathers stay inside one B*8-byte slice (L1 resident); the pass
+// writes per-block partials and k_xt_finish sums them in block order.
 struct XtSchedule {
-  const int4* items = nullptr;  // short: {col_begin, col_end, -1, slot}
-                                // long : {long_id, nz_begin, nz_end, seg_id}
+  const int4* items = nullptr;
+  const int32_t* perm = nullptr;  // virtual rows grouped by class (short, medium)
   int n_items = 0;
+  int blocked = 0;                // 1: sample-blocked layout
+  int64_t features = 0;           // F (virtual row -> feature = vrow % F)
+  int block_rows = 0;             // B
+  int n_blocks = 1;
+  const uint16_t* idx16 = nullptr;  // blocked: sample offset within the block
+  double* partial = nullptr;        // blocked: [n_blocks * F]
+  double* fin_slots = nullptr;      // blocked: finishing-kernel dot slots
+  unsigned* fin_ticket = nullptr;
+  int fin_grid = 1;
   const int32_t* long_col = nullptr;
   const int32_t* long_first_seg = nullptr;
   const int32_t* long_nseg = nullptr;
@@ -98,6 +113,10 @@ void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_st
                            const KrylovScalars* sc, double* t, cudaStream_t s);
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a,
                cudaStream_t s);
+// Epilogue (+ deterministic dots) over precomputed sums s_j = (X^T t)_j, e.g.
+// after an all-reduce of per-rank partial sums (row-sharded operator).
+void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtArgs& a, double* fin_slots,
+                        unsigned* fin_ticket, int fin_grid, cudaStream_t s);
 
 // Krylov vector work (all read their dynamic scalars from KrylovScalars)
 struct VecWork {
@@ -133,7 +152,7 @@ void launch_dense_gemv(const double* a, const double* x, double* y, int64_t n,
 // out = v / nrm (power iteration renormalization, krylov.cpp:84)
 void launch_scale_by_lambda(const double* w, double* v, int64_t n, const KrylovScalars* sc,
                             cudaStream_t s);
-void launch_diag_gram(const SparseDev& xt, double beta, double* out, cudaStream_t s);
+void launch_diag_gram(const SparseDev& xt, const XtSchedule& sch, double beta, double* out, cudaStream_t s);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
 void launch_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer,
                              uint64_t* inner_hist, cudaStream_t s);

@@ -63,63 +63,91 @@ std::vector<int32_t> narrow(const std::vector<int64_t>& v, const char* what) {
 
 }  // namespace
 
-void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s) {
+void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16) {
   const auto p32 = narrow(h.ptr, "row offsets");
-  const auto i32 = narrow(h.idx, "column indices");
   ptr.upload(p32.data(), p32.size(), s);
-  idx.upload(i32.data(), i32.size(), s);
+  if (narrow16) {  // uint16 column indices (half the index stream)
+    std::vector<uint16_t> i16(h.idx.size());
+    for (size_t k = 0; k < h.idx.size(); ++k) i16[k] = static_cast<uint16_t>(h.idx[k]);
+    idx16.upload(i16.data(), i16.size(), s);
+  } else {
+    const auto i32 = narrow(h.idx, "column indices");
+    idx.upload(i32.data(), i32.size(), s);
+  }
   if (!pattern) val.upload(h.val.data(), h.val.size(), s);
   RMG_CK(cudaStreamSynchronize(s));
   view.rows = h.n;
   view.cols = h.f;
   view.nnz = h.nnz();
   view.ptr = ptr.get();
-  view.idx = idx.get();
+  view.idx = narrow16 ? nullptr : idx.get();
+  view.idx16 = narrow16 ? idx16.get() : nullptr;
   view.val = pattern ? nullptr : val.get();
   view.width = lanes_for(h.n ? static_cast<double>(h.nnz()) / static_cast<double>(h.n) : 1.0);
 }
 
-// nnz-balanced work items over the rows of X^T (= feature columns of X).
-void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s) {
-  const int64_t F = xt.n, nnz = xt.nnz();
-  const int64_t C = std::max<int64_t>(256, std::min<int64_t>(16384, nnz / (148 * 4)));
+// Work items over the rows of a (possibly sample-blocked, virtual) X^T CSR,
+// by length class: short rows (<= 8 per lane of a W-lane group), medium rows
+// (one warp, <= 2048), long rows (fixed CTA segments).  Each CTA item holds
+// about C nonzeros, so no lane group owns a row much longer than its peers'.
+void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows) {
+  const int64_t V = xt.n, nnz = xt.nnz();
+  const int64_t C = std::max<int64_t>(512, std::min<int64_t>(16384, nnz / (148 * 4)));
+  // lane width from the median row length among rows that are not long
+  std::vector<int64_t> lens;
+  lens.reserve(V);
+  for (int64_t j = 0; j < V; ++j) {
+    const int64_t len = xt.ptr[j + 1] - xt.ptr[j];
+    if (len > 0 && len <= 2048) lens.push_back(len);
+  }
+  int width = 8;
+  if (!lens.empty()) {
+    std::nth_element(lens.begin(), lens.begin() + lens.size() / 2, lens.end());
+    width = lanes_for(static_cast<double>(lens[lens.size() / 2]));
+  }
+  const int64_t short_max = 8LL * width, medium_max = 2048;
+  const int64_t seg = std::max<int64_t>(C, 4096);
+  std::vector<int32_t> perm_short, perm_medium;
   std::vector<int4> it;
   std::vector<int32_t> lcol, lfirst, lnseg, lslot;
-  std::vector<int64_t> short_lens;
   int slot = 0, segs = 0;
-  int64_t cs = 0, acc = 0;
-  auto flush = [&](int64_t end) {
-    if (cs < end) it.push_back(make_int4((int)cs, (int)end, -1, slot++));
-    cs = end;
-    acc = 0;
-  };
-  for (int64_t j = 0; j < F; ++j) {
+  for (int64_t j = 0; j < V; ++j) {
     const int64_t len = xt.ptr[j + 1] - xt.ptr[j];
-    if (len > C) {
-      flush(j);
+    if (len <= short_max) {
+      perm_short.push_back(static_cast<int32_t>(j));
+    } else if (len <= medium_max) {
+      perm_medium.push_back(static_cast<int32_t>(j));
+    } else {
       const int id = static_cast<int>(lcol.size());
-      const int nseg = static_cast<int>((len + C - 1) / C);
-      lcol.push_back((int)j);
+      const int nseg = static_cast<int>((len + seg - 1) / seg);
+      lcol.push_back(static_cast<int32_t>(j));
       lfirst.push_back(segs);
       lnseg.push_back(nseg);
       lslot.push_back(slot++);
       for (int q = 0; q < nseg; ++q) {
-        const int64_t b = xt.ptr[j] + q * C, e = std::min<int64_t>(xt.ptr[j + 1], b + C);
+        const int64_t b = xt.ptr[j] + q * seg, e = std::min<int64_t>(xt.ptr[j + 1], b + seg);
         it.push_back(make_int4(id, (int)b, (int)e, segs++));
       }
-      cs = j + 1;
-    } else {
-      if ((acc + len > C || j - cs >= 4096) && cs < j) flush(j);
-      acc += len;
-      short_lens.push_back(len);
     }
   }
-  flush(F);
-  int width = 8;
-  if (!short_lens.empty()) {
-    std::nth_element(short_lens.begin(), short_lens.begin() + short_lens.size() / 2, short_lens.end());
-    width = lanes_for(static_cast<double>(short_lens[short_lens.size() / 2]));
-  }
+  std::vector<int32_t> prm(perm_short);
+  prm.insert(prm.end(), perm_medium.begin(), perm_medium.end());
+  auto pack = [&](int64_t q0, int64_t q1, int kind, int64_t max_rows) {
+    int64_t start = q0, acc = 0;
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t len = xt.ptr[prm[q] + 1] - xt.ptr[prm[q]];
+      if ((acc + len > C || q - start >= max_rows) && q > start) {
+        it.push_back(make_int4((int)start, (int)q, kind, slot++));
+        start = q;
+        acc = 0;
+      }
+      acc += std::max<int64_t>(len, 1);
+    }
+    if (q1 > start) it.push_back(make_int4((int)start, (int)q1, kind, slot++));
+  };
+  pack(0, static_cast<int64_t>(perm_short.size()), -1, 4096);
+  pack(static_cast<int64_t>(perm_short.size()), static_cast<int64_t>(prm.size()), -2, 4096);
+  perm.upload(prm.data(), prm.size(), s);
   items.upload(it.data(), it.size(), s);
   long_col.upload(lcol.data(), lcol.size(), s);
   long_first.upload(lfirst.data(), lfirst.size(), s);
@@ -146,6 +174,46 @@ void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s) {
   view.slots = slots.get();
   view.grid_ticket = grid_ticket.get();
   view.width = width;
+  view.perm = perm.get();
+  view.features = features;
+  view.n_blocks = std::max(1, n_blocks);
+  view.block_rows = block_rows;
+  view.blocked = n_blocks > 1 ? 1 : 0;
+  if (view.blocked) {
+    partial.alloc(static_cast<size_t>(n_blocks) * std::max<int64_t>(1, features));
+    view.partial = partial.get();
+    view.fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (features + 255) / 256)));
+    fin_slots.alloc(static_cast<size_t>(view.fin_grid) * 2);
+    fin_ticket.alloc(1);
+    RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), s));
+    RMG_CK(cudaStreamSynchronize(s));
+    view.fin_slots = fin_slots.get();
+    view.fin_ticket = fin_ticket.get();
+  }
+}
+
+// X^T restricted to sample blocks of B rows: virtual row (b, j) = b * F + j
+// lists the samples of block b that touch feature j, as uint16 offsets.
+HostCsr blocked_transpose(const HostCsr& xt, int64_t block_rows, int n_blocks) {
+  const int64_t F = xt.n;
+  HostCsr v;
+  v.n = static_cast<int64_t>(n_blocks) * F;
+  v.f = block_rows;
+  v.ptr.assign(v.n + 1, 0);
+  for (int64_t j = 0; j < F; ++j)
+    for (int64_t k = xt.ptr[j]; k < xt.ptr[j + 1]; ++k) v.ptr[(xt.idx[k] / block_rows) * F + j + 1]++;
+  for (int64_t r = 0; r < v.n; ++r) v.ptr[r + 1] += v.ptr[r];
+  v.idx.resize(xt.nnz());
+  if (!xt.val.empty()) v.val.resize(xt.nnz());
+  std::vector<int64_t> fill(v.ptr.begin(), v.ptr.end() - 1);
+  for (int64_t j = 0; j < F; ++j)
+    for (int64_t k = xt.ptr[j]; k < xt.ptr[j + 1]; ++k) {
+      const int64_t b = xt.idx[k] / block_rows;
+      const int64_t d = fill[b * F + j]++;  // samples stay increasing inside a block
+      v.idx[d] = xt.idx[k] - b * block_rows;
+      if (!xt.val.empty()) v.val[d] = xt.val[k];
+    }
+  return v;
 }
 
 // ------------------------------------------------------------------ profiling
@@ -178,7 +246,38 @@ void OpProfile::reset() {
 }
 
 // ------------------------------------------------------------------ Matrix
-Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern) : ctx(c), host(std::move(h)) {
+// ------------------------------------------------------------------ multi-GPU
+Comm::Comm(int nr, int r, const ncclUniqueId& id, int device) : nranks(nr), rank(r) {
+  if (nr < 1 || r < 0 || r >= nr) throw InvalidArgument("rmg_comm_create: rank outside [0, nranks)");
+  RMG_CK(cudaSetDevice(device));
+  const ncclResult_t e = ncclCommInitRank(&comm, nr, id, r);
+  if (e != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(e));
+}
+
+Comm::~Comm() {
+  if (comm) ncclCommDestroy(comm);
+}
+
+std::vector<int64_t> partition_rows(const std::vector<int64_t>& rp, int nranks) {
+  if (nranks < 1) throw InvalidArgument("partition_rows: nranks must be positive");
+  const int64_t n = static_cast<int64_t>(rp.size()) - 1, nnz = rp.back();
+  std::vector<int64_t> b(nranks + 1, n);
+  b[0] = 0;
+  for (int r = 1; r < nranks; ++r) {  // first row whose start reaches r/nranks of the nonzeros
+    const int64_t target = (nnz * r + nranks - 1) / nranks;
+    b[r] = std::lower_bound(rp.begin(), rp.end() - 1, target) - rp.begin();
+    b[r] = std::max(b[r], b[r - 1]);
+  }
+  return b;
+}
+
+void Matrix::allreduce_sums(double* sendbuf, double* recvbuf, int64_t count) {
+  const ncclResult_t e = ncclAllReduce(sendbuf, recvbuf, static_cast<size_t>(count), ncclDouble, ncclSum, comm->comm,
+                                       ctx->stream);
+  if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+}
+
+Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
   if (host.n > INT32_MAX || host.f > INT32_MAX || host.nnz() > INT32_MAX)
     throw InvalidArgument("FeatureMatrix: dimensions exceed the single-device int32 index range");
@@ -187,21 +286,75 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern) : ctx(c), host(std::m
     pattern = std::all_of(host.val.begin(), host.val.end(), [](double v) { return v == 1.0; });
   if (host.val.empty()) host.val.assign(host.nnz(), 1.0);
   RMG_CK(cudaSetDevice(ctx->device));
-  x.upload(host, pattern, ctx->stream);
-  const HostCsr ht = transpose(host);
-  xt.upload(ht, pattern, ctx->stream);
-  sched.build(ht, ctx->stream);
-  t.alloc(std::max<int64_t>(1, host.n));
+  row0 = 0;
+  row1 = host.n;
+  HostCsr shard;
+  if (comm != nullptr) {  // this rank's nnz-balanced row block (rows rebased to 0)
+    const std::vector<int64_t> b = partition_rows(host.ptr, comm->nranks);
+    row0 = b[comm->rank];
+    row1 = b[comm->rank + 1];
+    shard.n = row1 - row0;
+    shard.f = host.f;
+    shard.ptr.resize(shard.n + 1);
+    for (int64_t i = 0; i <= shard.n; ++i) shard.ptr[i] = host.ptr[row0 + i] - host.ptr[row0];
+    shard.idx.assign(host.idx.begin() + host.ptr[row0], host.idx.begin() + host.ptr[row1]);
+    shard.val.assign(host.val.begin() + host.ptr[row0], host.val.begin() + host.ptr[row1]);
+    part.alloc(std::max<int64_t>(1, host.f));
+    red.alloc(std::max<int64_t>(1, std::max(host.f, host.n)));
+    fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (host.f + 255) / 256)));
+    fin_slots.alloc(static_cast<size_t>(fin_grid) * 2);
+    fin_ticket.alloc(1);
+    RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
+  }
+  const HostCsr& local = comm != nullptr ? shard : host;
+  x.upload(local, pattern, ctx->stream, local.f <= 65536);
+  const HostCsr ht = transpose(local);
+  // Sample blocking of X^T: 8192-sample blocks keep each CTA's
+  // t-gathers in a 64 KB slice; used when the per-block bookkeeping (one
+  // pointer and one partial per block and feature) stays small next to nnz.
+  constexpr int64_t kBlock = 8192;
+  const int64_t nb = (local.n + kBlock - 1) / kBlock;
+  // Opt-in (RMG_BLOCKED_XT=1): measured slower than the length-class items on
+  // cfg 2 (85 vs 32 us cold, profiles/r1_operator.md); kept for large-N work.
+  const bool blocked = std::getenv("RMG_BLOCKED_XT") != nullptr && nb >= 2 &&
+                       nb * local.f * 3 <= local.nnz() && nb * local.f < INT32_MAX;
+  if (blocked) {
+    const HostCsr hb = blocked_transpose(ht, kBlock, static_cast<int>(nb));
+    xt.upload(hb, pattern, ctx->stream, true);
+    sched.build(hb, ctx->stream, local.f, static_cast<int>(nb), static_cast<int>(kBlock));
+    sched.view.idx16 = xt.view.idx16;
+  } else {
+    xt.upload(ht, pattern, ctx->stream, false);
+    sched.build(ht, ctx->stream, local.f, 1, 0);
+  }
+  t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);
 }
+
+namespace {
+// X^T pass of one operator application: fused epilogue, or (sharded) partial
+// sums + all-reduce of the F-vector + epilogue pass.
+void xt_pass(Matrix& m, const double* t, Epi epi, const XtArgs& args) {
+  XtArgs a = args;
+  a.t = t;
+  if (m.comm == nullptr) {
+    launch_xt(m.xt.view, m.sched.view, epi, a, m.ctx->stream);
+    return;
+  }
+  XtArgs pa = a;
+  pa.out = m.part.get();
+  launch_xt(m.xt.view, m.sched.view, Epi::Plain, pa, m.ctx->stream);
+  m.allreduce_sums(m.part.get(), m.red.get(), m.f());
+  launch_xt_epilogue(m.red.get(), m.f(), epi, a, m.fin_slots.get(), m.fin_ticket.get(), m.fin_grid, m.ctx->stream);
+  m.ctx->launches += 1;
+}
+}  // namespace
 
 void Matrix::apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof) {
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows(x.view, v, t.get(), args.done, ctx->stream);
   if (prof) prof->mark(ctx->stream);
-  XtArgs a = args;
-  a.t = t.get();
-  launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  xt_pass(*this, t.get(), epi, args);
   if (prof) prof->mark(ctx->stream);
   ctx->launches += 2;
 }
@@ -211,23 +364,42 @@ void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* s
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows_ring(x.view, v_ring, stride, sc, t.get(), ctx->stream);
   if (prof) prof->mark(ctx->stream);
-  XtArgs a = args;
-  a.t = t.get();
-  launch_xt(xt.view, sched.view, epi, a, ctx->stream);
+  xt_pass(*this, t.get(), epi, args);
   if (prof) prof->mark(ctx->stream);
   ctx->launches += 2;
 }
 
 void Matrix::spmv(const double* v, double* y) {
-  launch_spmv_rows(x.view, v, y, nullptr, ctx->stream);
+  if (comm == nullptr) {
+    launch_spmv_rows(x.view, v, y, nullptr, ctx->stream);
+  } else {  // own rows into a zeroed N-vector, then sum over ranks
+    RMG_CK(cudaMemsetAsync(y, 0, static_cast<size_t>(n()) * sizeof(double), ctx->stream));
+    launch_spmv_rows(x.view, v, y + row0, nullptr, ctx->stream);
+    allreduce_sums(y, y, n());
+  }
   ctx->launches += 1;
+}
+
+// gram_diagonal (ridge.cpp:30-37); sharded: local sums, all-reduce, + beta
+void Matrix::gram_diagonal(double beta, double* out) {
+  if (comm == nullptr) {
+    launch_diag_gram(xt.view, sched.view, beta, out, ctx->stream);
+    return;
+  }
+  launch_diag_gram(xt.view, sched.view, 0.0, part.get(), ctx->stream);
+  allreduce_sums(part.get(), red.get(), f());
+  std::vector<double> h(f());
+  if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), red.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  for (double& d : h) d = beta + d;
+  if (!h.empty()) RMG_CK(cudaMemcpyAsync(out, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->sync();
 }
 
 void Matrix::spmv_t(const double* u, double* y) {
   XtArgs a;
-  a.t = u;
   a.out = y;
-  launch_xt(xt.view, sched.view, Epi::Plain, a, ctx->stream);
+  xt_pass(*this, u + row0, Epi::Plain, a);  // sharded: this rank's samples of u
   ctx->launches += 1;
 }
 
@@ -349,7 +521,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     work_.push_back(std::make_unique<KrylovWork>(x->f(), 1, solver.max_iters, solver.tol, s));
     if (kind == RMG_METHOD_JACOBI_CG) {  // krylov.cpp:623-626, 41-47
       DBuf<double> d(std::max<int64_t>(1, x->f()));
-      launch_diag_gram(x->xt.view, beta, d.get(), s);
+      x->gram_diagonal(beta, d.get());
       std::vector<double> h(x->f());
       if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), d.get(), h.size() * 8, cudaMemcpyDeviceToHost, s));
       ctx_->sync();
@@ -416,7 +588,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       pt.val.resize(pt.idx.size());
       for (size_t q = 0; q < pt.idx.size(); ++q) pt.val[q] = lvl->agg.weight[pt.idx[q]];
       lvl->pt.upload(pt, false, s);
-      lvl->pt_sched.build(pt, s);
+      lvl->pt_sched.build(pt, s, nc, 1, 0);
     }
     labels_.push_back(std::move(lab));
     coarse_.push_back(std::move(lvl));
@@ -516,8 +688,8 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
     d->partials.alloc(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride);
     d->cg_shared.alloc(4);
     if (std::getenv("RMG_DENSE_TIMING") != nullptr) {
-      d->timing.alloc(256);
-      RMG_CK(cudaMemsetAsync(d->timing.get(), 0, 256 * sizeof(unsigned long long), s));
+      d->timing.alloc(512);
+      RMG_CK(cudaMemsetAsync(d->timing.get(), 0, 512 * sizeof(unsigned long long), s));
     }
     dense_[k] = std::move(d);
   }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <memory>
 #include <string>
@@ -84,18 +85,22 @@ struct Context {
 struct DeviceSparse {
   SparseDev view;
   DBuf<int32_t> ptr, idx;
+  DBuf<uint16_t> idx16;
   DBuf<double> val;
-  void upload(const HostCsr& h, bool pattern, cudaStream_t s);
+  void upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16 = false);
 };
 
 struct DeviceSchedule {
   XtSchedule view;
   DBuf<int4> items;
-  DBuf<int32_t> long_col, long_first, long_nseg, long_slot;
-  DBuf<double> seg_partial, slots;
-  DBuf<unsigned> col_ticket, grid_ticket;
-  void build(const HostCsr& xt, cudaStream_t s);
+  DBuf<int32_t> perm, long_col, long_first, long_nseg, long_slot;
+  DBuf<double> seg_partial, slots, partial, fin_slots;
+  DBuf<unsigned> col_ticket, grid_ticket, fin_ticket;
+  // xt: (virtual) X^T CSR; features F; n_blocks > 1 selects the sample-blocked layout
+  void build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows);
 };
+
+HostCsr blocked_transpose(const HostCsr& xt, int64_t block_rows, int n_blocks);
 
 // In-situ timing of one level's operator kernels (CUDA events on the
 // launching stream around K1 and K2 of every application).
@@ -113,7 +118,22 @@ struct OpProfile {
   void reset();
 };
 
+// NCCL communicator over the GPUs of one node (one process per GPU).
+struct Comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  Comm(int nranks, int rank, const ncclUniqueId& id, int device);
+  ~Comm();
+};
+
+// nnz-balanced contiguous row blocks: bounds[r]..bounds[r+1] for rank r.
+std::vector<int64_t> partition_rows(const std::vector<int64_t>& row_offsets, int nranks);
+
 // X (N x F) and X^T on the device, with the X^T schedule and an N-vector scratch.
+// With a communicator, only this rank's nnz-balanced row block of X lives on
+// the device and every X^T pass ends in an all-reduce of the F-vector
+// (north star: row sharding over NVLink); `host` keeps the full matrix for
+// the (replicated) hierarchy setup.
 struct Matrix {
   Context* ctx = nullptr;
   HostCsr host;  // canonical CSR kept for setup (clustering, coarsening)
@@ -122,7 +142,14 @@ struct Matrix {
   DeviceSchedule sched;
   DBuf<double> t;             // X v scratch
   DBuf<KrylovScalars> gram_sc;  // power-iteration scalars
-  Matrix(Context* c, HostCsr h, bool detect_pattern);
+  Comm* comm = nullptr;       // row-sharded when non-null
+  int64_t row0 = 0, row1 = 0; // this rank's rows of X (global numbering)
+  DBuf<double> part, red, fin_slots;
+  DBuf<unsigned> fin_ticket;
+  int fin_grid = 1;
+  Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr);
+  int64_t n_local() const { return row1 - row0; }
+  void allreduce_sums(double* sendbuf, double* recvbuf, int64_t count);
   int64_t n() const { return host.n; }
   int64_t f() const { return host.f; }
   int64_t nnz() const { return host.nnz(); }
@@ -132,6 +159,7 @@ struct Matrix {
                   OpProfile* prof = nullptr);
   void spmv(const double* v, double* y);
   void spmv_t(const double* u, double* y);
+  void gram_diagonal(double beta, double* out);
   double lambda_max(double tol, uint64_t max_iters, uint64_t seed, uint64_t* iters, bool* conv);
 };
 

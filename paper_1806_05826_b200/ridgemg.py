@@ -210,21 +210,63 @@ def default_context() -> Context:
     return _default_ctx
 
 
+def shard_rows(row_offsets, nranks: int) -> np.ndarray:
+    """nnz-balanced contiguous row blocks (host only): bounds[r]..bounds[r+1]."""
+    rp = np.ascontiguousarray(row_offsets, np.uint64)
+    out = np.zeros(nranks + 1, np.uint64)
+    _lib.check(_lib.load().rmg_shard_rows(_ptr(rp), len(rp) - 1, nranks, _ptr(out)))
+    return out
+
+
+class Comm:
+    """NCCL communicator (rmg_comm) for row-sharded operators.  `unique_id` is
+    the 128-byte id from Comm.new_unique_id() on rank 0, broadcast by the caller."""
+
+    @staticmethod
+    def new_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _lib.check(_lib.load().rmg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, nranks: int, rank: int, unique_id: bytes):
+        self.lib = ctx.lib
+        self.h = C.c_void_p()
+        idb = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _lib.check(self.lib.rmg_comm_create(ctx.h, nranks, rank, idb, C.byref(self.h)))
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.h:
+            self.lib.rmg_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
 class DeviceMatrix:
     """X and X^T resident in HBM (rmg_matrix).  Mirrors the FeatureMatrix-level
     free functions of the reference: spmv, spmv_transpose, RidgeOperator::apply,
-    gram_diagonal, estimate_lambda_max(GramOperator)."""
+    gram_diagonal, estimate_lambda_max(GramOperator).  With `comm`, only this
+    rank's nnz-balanced row block lives on the device and X^T passes all-reduce."""
 
-    def __init__(self, x: FeatureMatrix, ctx: Optional[Context] = None, detect_pattern: bool = True):
+    def __init__(self, x: FeatureMatrix, ctx: Optional[Context] = None, detect_pattern: bool = True,
+                 comm: Optional["Comm"] = None):
         self.ctx = ctx or default_context()
         self.lib = self.ctx.lib
         self.x = x
+        self.comm = comm
         rp = np.ascontiguousarray(x.row_offsets, np.uint64)
         ci = np.ascontiguousarray(x.column_indices, np.uint64)
         v = None if x.values is None else np.ascontiguousarray(x.values, np.float64)
         self.h = C.c_void_p()
-        _lib.check(self.lib.rmg_matrix_create_csr(self.ctx.h, x.n_samples, x.n_features, _ptr(rp), _ptr(ci), _ptr(v),
-                                                  int(detect_pattern), C.byref(self.h)))
+        if comm is None:
+            _lib.check(self.lib.rmg_matrix_create_csr(self.ctx.h, x.n_samples, x.n_features, _ptr(rp), _ptr(ci),
+                                                      _ptr(v), int(detect_pattern), C.byref(self.h)))
+        else:
+            _lib.check(self.lib.rmg_matrix_create_csr_sharded(self.ctx.h, comm.h, x.n_samples, x.n_features, _ptr(rp),
+                                                              _ptr(ci), _ptr(v), int(detect_pattern),
+                                                              C.byref(self.h)))
+        r0, r1, nr, rk = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_int32()
+        _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
+        self.row_range = (r0.value, r1.value)
         n, f, z, pat = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int32()
         _lib.check(self.lib.rmg_matrix_shape(self.h, C.byref(n), C.byref(f), C.byref(z), C.byref(pat)))
         self.n_samples, self.n_features, self.nnz, self.is_pattern = n.value, f.value, z.value, bool(pat.value)

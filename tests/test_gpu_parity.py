@@ -329,20 +329,23 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     assert rep.converged
     # cfg2_full: GPU 638 vs reference 647; reference threaded 650/651; see DESIGN.md §5
     assert abs(rep.iterations - int(g["ml_iterations"])) <= max(2, 3 * env["ml_iter_spread"]), rep.iterations
-    assert rel_diff(w, g["ml_w"]) <= max(W_TOL, 4 * env["ml_w_spread"])
+    # w at tol 1e-6: the kappa*tol regime (the reference itself moves by env["ml_w_spread"]
+    # between its thread counts); the strict 1e-8 comparison is made at tol 1e-12 below
+    assert rel_diff(w, g["ml_w"]) <= 1e-6, rel_diff(w, g["ml_w"])
     assert len(rep.inner_iterations) == rep.iterations
     gi = g["ml_inner"].astype(np.int64)
     # the first inner solves (same outer trajectory so far) take the reference's counts
     assert np.all(np.abs(rep.inner_iterations[:3].astype(np.int64) - gi[:3]) <= 2)
     cg = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 5000)))
-    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= max(2, 3 * env["cg_iter_spread"])
-    assert rel_diff(cg.w, g["cg_w"]) <= max(W_TOL, 4 * env["cg_w_spread"])
+    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= max(2, 3 * env["cg_iter_spread"]), \
+        (cg.report.iterations, int(g["cg_iterations"]))
+    assert rel_diff(cg.w, g["cg_w"]) <= 1e-6, (rel_diff(cg.w, g["cg_w"]), env)
     # Driven to tol 1e-12 both converge onto the same solution: the strict bar.
     if "ml12_w" in g.files:
         spec12 = _cfg2_spec(ks, [g[f"labels{i}"].astype(np.int64) for i in range(len(ks))])
         spec12.solver = R.SolverConfig(1e-12, 1000)
         w12, rep12 = R.PreparedMethod(m, 1.0, spec12).solve(g["b"])
         assert rep12.converged
-        assert rel_diff(w12, g["ml12_w"]) <= W_TOL
+        assert rel_diff(w12, g["ml12_w"]) <= W_TOL, rel_diff(w12, g["ml12_w"])
         cg12 = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-12, 5000)))
-        assert rel_diff(cg12.w, g["cg12_w"]) <= W_TOL
+        assert rel_diff(cg12.w, g["cg12_w"]) <= W_TOL, rel_diff(cg12.w, g["cg12_w"])

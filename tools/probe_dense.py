@@ -18,17 +18,26 @@ for lv in range(pm.n_levels):
     print("level", lv, pm.profile(lv))
 if os.environ.get("RMG_DENSE_TIMING"):
     import ctypes as C
-    buf = (C.c_ulonglong * 256)()
+    buf = (C.c_ulonglong * 512)()
     lib = R.load()
     lib.rmg_debug_dense_timing.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
     if lib.rmg_debug_dense_timing(pm.h, 1, buf) == 0:
-        t = np.array(buf[:], dtype=np.float64).reshape(16, 16)
+        t = np.array(buf[:256], dtype=np.float64).reshape(16, 16)
         names = ["start", "z(Mr)", "GSdots", "B1", "gsums", "p", "B2", "Ap", "pap", "B3", "gsums2", "upd", "B4", "gsums3"]
         rows = t[4:15]  # iterations 4..14 (all phases present)
         deltas = np.diff(rows[:, :14], axis=1)
         for i, nm in enumerate(names[1:]):
             print(f"  phase {nm:>7}: {np.mean(deltas[:, i]) / 1e3:7.3f} us")
         print("  iteration:", np.mean(np.diff(rows[:, 0])) / 1e3, "us")
+        arr = np.array(buf[256:512], dtype=np.float64)
+        arr = arr[arr > 0]
+        if len(arr):
+            rel = (arr - arr.min()) / 1e3
+            order = np.argsort(rel)
+            print(f"  per-CTA Ap end (it 8): spread {rel.max():.2f} us; slowest CTAs {order[-8:].tolist()} "
+                  f"({np.round(rel[order[-8:]], 2).tolist()} us); fastest {order[:4].tolist()}")
+            print("  per-CTA lateness histogram (us):", np.histogram(rel, bins=8)[0].tolist(),
+                  np.round(np.histogram(rel, bins=8)[1], 2).tolist())
 n, k1, k2 = pm.profile(1)
 if n:
     print("dense inner solve: %.3f ms per launch, %.2f us per inner iteration" % (k1 / n, k1 / n / np.mean(rep.inner_iterations) * 1e3))
