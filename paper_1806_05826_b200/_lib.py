@@ -116,10 +116,13 @@ def load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1806_05826_b200.build` "
                           "(the solve path has no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
+    override = os.environ.get("RMG_LIB_PATH")  # diagnostics: A/B another build of the library
+    lib = C.CDLL(override or LIB_PATH)
     lib.rmg_last_error.restype = C.c_char_p
     lib.rmg_last_error.argtypes = []
     for name, args in SIGNATURES.items():
+        if override and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int

@@ -38,7 +38,9 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
-constexpr int kPS = 40;  // partial slots per block: [0] ||b||^2, [1] #non-finite, [2..33] GS, [34] pap, [35] pr, [36] rr
+// partial slots per block: [0] ||b||^2, [1] #non-finite, [2..33] GS, [34] pap, [35] pr, [36] rr;
+// 64 doubles = 512 B per CTA so every CTA's slots start on their own L2 line group
+constexpr int kPS = 64;
 constexpr int kGS = 2, kPAP = 34, kPR = 35, kRR = 36;
 constexpr int kMaxQ = 16;  // n <= 4096 columns = 16 per thread
 constexpr int kMaxUse = 32;
@@ -62,13 +64,20 @@ __device__ __forceinline__ double bsum_all(double v, double* sh) {
   return r;
 }
 
-// out[q] = sum over blocks b (fixed order) of partials[b][first + q], q < count,
+// Cross-CTA partials are slot-major, partials[slot * stride + cta]: a reduced
+// quantity is one contiguous run of gridDim.x doubles (coalesced for the warp
+// that sums it); measured: the CTA-major layout (one line per CTA) put a
+// placement-dependent 25% on every inner iteration.
+__device__ __forceinline__ int slot_stride() { return (gridDim.x + 31) & ~31; }
+
+// out[q] = sum over blocks b (fixed order) of partials[first + q][b], q < count,
 // one warp per quantity; ends with __syncthreads so every thread may read out.
 __device__ __forceinline__ void grid_sums(const double* partials, int first, int count, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int q = wid; q < count; q += kW) {
     double acc = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + (size_t)b * kPS + first + q);
+    const double* row = partials + (size_t)(first + q) * slot_stride(); // slot-major: 143 contiguous doubles
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(row + b);
     acc = wsum(acc);
     if (lane == 0) out[q] = acc;
   }
@@ -139,7 +148,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   double* coef = gsum + 64;
   double* sh = coef + kMaxUse;
   const int tid = threadIdx.x;
-  double* part = a.partials + (size_t)blockIdx.x * kPS;
+  const int pstride = slot_stride();
+  auto part = [&](int slot) -> double& { return a.partials[(size_t)slot * pstride + blockIdx.x]; };
   KrylovScalars* sc = a.sc;
   const double* Arows = SMEM ? As : a.A + (size_t)row0 * n;
   const double* Mrows = a.M + (size_t)row0 * n;
@@ -159,8 +169,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   bb = bsum_all(bb, sh);
   bad = bsum_all(bad, sh);
   if (tid == 0) {
-    part[0] = bb;
-    part[1] = bad;
+    part(0) = bb;
+    part(1) = bad;
   }
   grid.sync();
   grid_sums(a.partials, 0, 2, gsum);
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
           double acc = 0.0;
           for (int lr = lane; lr < nr; lr += 32) acc += zs[lr] * __ldcg(aph + row0 + lr);
           acc = wsum(acc);
-          if (lane == 0) part[kGS + q] = acc;
+          if (lane == 0) part(kGS + q) = acc;
         }
         tmark(a, it, 2);
         grid.sync();  // B1
@@ -278,8 +288,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       dpap = bsum_all(dpap, sh);
       dpr = bsum_all(dpr, sh);
       if (tid == 0) {
-        part[kPAP] = dpap;
-        part[kPR] = dpr;
+        part(kPAP) = dpap;
+        part(kPR) = dpr;
       }
     }
     tmark(a, it, 8);
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       rr = ri * ri;
     }
     rr = bsum_all(rr, sh);
-    if (tid == 0) part[kRR] = rr;
+    if (tid == 0) part(kRR) = rr;
     tmark(a, it, 11);
     grid.sync();  // B4
     tmark(a, it, 12);
@@ -353,7 +363,7 @@ DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
   p.smem_a = with_a <= (size_t)max_smem;
   if (const char* e = std::getenv("RMG_DENSE_SMEM")) p.smem_a = p.smem_a && e[0] != '0';
   p.smem_bytes = p.smem_a ? with_a : extra;
-  p.partial_stride = kPS;
+  p.partial_stride = kPS * ((p.grid + 31) / 32 * 32) / std::max(1, p.grid);
   return p;
 }
 

@@ -685,7 +685,9 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
     }
     d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
     d->pap_ring.alloc(kMaxKeep + 2);
-    d->partials.alloc(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride);
+    // own 2 MB-granular allocation: the cross-CTA partials are read by every CTA
+    // after every grid barrier, so their placement is on the critical path
+    d->partials.alloc(std::max<size_t>(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride, 262144));
     d->cg_shared.alloc(4);
     if (std::getenv("RMG_DENSE_TIMING") != nullptr) {
       d->timing.alloc(512);

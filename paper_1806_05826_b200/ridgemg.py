@@ -265,8 +265,11 @@ class DeviceMatrix:
                                                               _ptr(ci), _ptr(v), int(detect_pattern),
                                                               C.byref(self.h)))
         r0, r1, nr, rk = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_int32()
-        _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
-        self.row_range = (r0.value, r1.value)
+        if hasattr(self.lib, "rmg_matrix_shard"):
+            _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
+            self.row_range = (r0.value, r1.value)
+        else:
+            self.row_range = (0, x.n_samples)
         n, f, z, pat = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int32()
         _lib.check(self.lib.rmg_matrix_shape(self.h, C.byref(n), C.byref(f), C.byref(z), C.byref(pat)))
         self.n_samples, self.n_features, self.nnz, self.is_pattern = n.value, f.value, z.value, bool(pat.value)
