@@ -180,6 +180,10 @@ int rmg_synth_dense_clustered(uint64_t n, uint64_t f, uint64_t groups, double no
  * seeded permutation, without replacement per row; values 1.0 or |N(0,1)| */
 int rmg_synth_sparse_zipf(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
                           uint64_t seed, rmg_host_csr** out, uint64_t* nnz);
+/* Same distribution with one RNG stream per row, generated by all host threads
+ * (large measurement shards, e.g. cfg5 per-GPU); not the reference's stream */
+int rmg_synth_sparse_zipf_rows(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
+                               uint64_t seed, rmg_host_csr** out, uint64_t* nnz);
 int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* row_offsets, uint64_t* column_indices, double* values);
 int rmg_host_csr_destroy(rmg_host_csr* h);
 

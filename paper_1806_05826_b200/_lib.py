@@ -82,6 +82,7 @@ SIGNATURES = {
     "rmg_rng_normals": [_U64, _U64, _P],
     "rmg_synth_dense_clustered": [_U64, _U64, _U64, _D, _U64, _PP, _P],
     "rmg_synth_sparse_zipf": [_U64, _U64, _D, _D, _I32, _U64, _PP, _P],
+    "rmg_synth_sparse_zipf_rows": [_U64, _U64, _D, _D, _I32, _U64, _PP, _P],
     "rmg_host_csr_export": [_P, _P, _P, _P],
     "rmg_host_csr_destroy": [_P],
     "rmg_method_prepare": [_P, _D, _I32, _P, _U64, _P, _PP],

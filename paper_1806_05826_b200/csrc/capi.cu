@@ -360,6 +360,17 @@ int rmg_synth_sparse_zipf(uint64_t n, uint64_t f, double mean_nnz, double zipf_s
   });
 }
 
+int rmg_synth_sparse_zipf_rows(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
+                               uint64_t seed, rmg_host_csr** out, uint64_t* nnz) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new rmg_host_csr{rmg::synth_sparse_zipf_rows(static_cast<int64_t>(n), static_cast<int64_t>(f),
+                                                           mean_nnz, zipf_s, abs_normal_values != 0, seed)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+  });
+}
+
 int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* rp, uint64_t* ci, double* v) {
   return guard([&] {
     need(h, "host csr");

@@ -460,20 +460,65 @@ HostCsr synth_dense_clustered(int64_t n, int64_t f, int64_t groups, double noise
   return m;
 }
 
+namespace {
+
+struct ZipfTable {
+  std::vector<int64_t> perm;
+  std::vector<double> cdf;
+  double total = 0.0;
+  ZipfTable(int64_t f, double zipf_s, CounterRng& rng) : perm(f), cdf(f) {
+    std::iota(perm.begin(), perm.end(), int64_t{0});
+    for (int64_t i = f; i > 1; --i) std::swap(perm[i - 1], perm[rng.next_index(i)]);
+    double run = 0.0;
+    for (int64_t k = 0; k < f; ++k) {
+      run += std::pow(static_cast<double>(k + 1), -zipf_s);
+      cdf[k] = run;
+    }
+    total = run;
+  }
+};
+
+// One row: k = max(1, Poisson(mean)) by inverse CDF (capped at F), then k
+// distinct columns by Zipf rank (without replacement), sorted by column.
+void zipf_row(CounterRng& rng, const ZipfTable& z, int64_t f, double mean_nnz, bool abs_normal_values,
+              std::vector<int64_t>& row, std::vector<double>& rv, std::vector<int64_t>& idx_out,
+              std::vector<double>& val_out) {
+  const double u = rng.next_double();
+  int64_t kk = 0;
+  double pk = std::exp(-mean_nnz), cum = pk;
+  while (u >= cum && kk < 20 * static_cast<int64_t>(mean_nnz) + 100) {
+    ++kk;
+    pk *= mean_nnz / static_cast<double>(kk);
+    cum += pk;
+  }
+  kk = std::min<int64_t>(std::max<int64_t>(kk, 1), f);
+  row.clear();
+  rv.clear();
+  while (static_cast<int64_t>(row.size()) < kk) {
+    const double t = rng.next_double() * z.total;
+    int64_t rank = std::upper_bound(z.cdf.begin(), z.cdf.end(), t) - z.cdf.begin();
+    if (rank >= f) rank = f - 1;
+    const int64_t col = z.perm[rank];
+    if (std::find(row.begin(), row.end(), col) != row.end()) continue;
+    row.push_back(col);
+    if (abs_normal_values) rv.push_back(std::fabs(rng.next_normal()));
+  }
+  std::vector<size_t> order(row.size());
+  std::iota(order.begin(), order.end(), size_t{0});
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return row[a] < row[b]; });
+  for (size_t q : order) {
+    idx_out.push_back(row[q]);
+    if (abs_normal_values) val_out.push_back(rv[q]);
+  }
+}
+
+}  // namespace
+
 HostCsr synth_sparse_zipf(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
                           uint64_t seed) {
   if (n <= 0 || f <= 0 || !(mean_nnz > 0.0)) throw InvalidArgument("synth_sparse_zipf: bad shape");
   CounterRng rng(seed);
-  std::vector<int64_t> perm(f);
-  std::iota(perm.begin(), perm.end(), int64_t{0});
-  for (int64_t i = f; i > 1; --i) std::swap(perm[i - 1], perm[rng.next_index(i)]);
-  std::vector<double> cdf(f);
-  double run = 0.0;
-  for (int64_t k = 0; k < f; ++k) {
-    run += std::pow(static_cast<double>(k + 1), -zipf_s);
-    cdf[k] = run;
-  }
-  const double total = run;
+  const ZipfTable z(f, zipf_s, rng);
   HostCsr m;
   m.n = n;
   m.f = f;
@@ -483,37 +528,61 @@ HostCsr synth_sparse_zipf(int64_t n, int64_t f, double mean_nnz, double zipf_s, 
   std::vector<int64_t> row;
   std::vector<double> rv;
   for (int64_t r = 0; r < n; ++r) {
-    // k_r = max(1, Poisson(mean_nnz)) by inverse CDF, capped at F
-    const double u = rng.next_double();
-    int64_t kk = 0;
-    double pk = std::exp(-mean_nnz), cum = pk;
-    while (u >= cum && kk < 20 * static_cast<int64_t>(mean_nnz) + 100) {
-      ++kk;
-      pk *= mean_nnz / static_cast<double>(kk);
-      cum += pk;
-    }
-    kk = std::min<int64_t>(std::max<int64_t>(kk, 1), f);
-    row.clear();
-    rv.clear();
-    while (static_cast<int64_t>(row.size()) < kk) {  // Zipf ranks without replacement
-      const double t = rng.next_double() * total;
-      int64_t rank = std::upper_bound(cdf.begin(), cdf.end(), t) - cdf.begin();
-      if (rank >= f) rank = f - 1;
-      const int64_t col = perm[rank];
-      if (std::find(row.begin(), row.end(), col) != row.end()) continue;
-      row.push_back(col);
-      if (abs_normal_values) rv.push_back(std::fabs(rng.next_normal()));
-    }
-    std::vector<size_t> order(row.size());
-    std::iota(order.begin(), order.end(), size_t{0});
-    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return row[a] < row[b]; });
     m.ptr[r] = m.nnz();
-    for (size_t q : order) {
-      m.idx.push_back(row[q]);
-      if (abs_normal_values) m.val.push_back(rv[q]);
-    }
+    zipf_row(rng, z, f, mean_nnz, abs_normal_values, row, rv, m.idx, m.val);
   }
   m.ptr[n] = m.nnz();
+  return m;
+}
+
+// Same distribution with one RNG stream per row (seeded from (seed, row)), so
+// rows are generated by all host threads: large measurement shards (cfg5).
+HostCsr synth_sparse_zipf_rows(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
+                               uint64_t seed) {
+  if (n <= 0 || f <= 0 || !(mean_nnz > 0.0)) throw InvalidArgument("synth_sparse_zipf: bad shape");
+  CounterRng table_rng(seed);
+  const ZipfTable z(f, zipf_s, table_rng);
+  const int64_t T = std::max<int64_t>(1, std::min<int64_t>(64, std::thread::hardware_concurrency()));
+  const int64_t chunk = (n + T - 1) / T;
+  std::vector<std::vector<int64_t>> idx(T), len(T);
+  std::vector<std::vector<double>> val(T);
+  std::vector<std::thread> pool;
+  for (int64_t t = 0; t < T; ++t) {
+    pool.emplace_back([&, t] {
+      std::vector<int64_t> row;
+      std::vector<double> rv;
+      const int64_t r0 = t * chunk, r1 = std::min(n, r0 + chunk);
+      if (r0 >= r1) return;
+      idx[t].reserve(static_cast<size_t>((r1 - r0) * mean_nnz * 1.05));
+      for (int64_t r = r0; r < r1; ++r) {
+        uint64_t h = seed ^ (static_cast<uint64_t>(r) + 1) * 0xD1B54A32D192ED03ull;
+        h = (h ^ (h >> 33)) * 0xFF51AFD7ED558CCDull;
+        CounterRng rng(h ^ (h >> 29));
+        const size_t before = idx[t].size();
+        zipf_row(rng, z, f, mean_nnz, abs_normal_values, row, rv, idx[t], val[t]);
+        len[t].push_back(static_cast<int64_t>(idx[t].size() - before));
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  HostCsr m;
+  m.n = n;
+  m.f = f;
+  m.ptr.assign(n + 1, 0);
+  size_t total = 0;
+  for (auto& v : idx) total += v.size();
+  m.idx.reserve(total);
+  if (abs_normal_values) m.val.reserve(total);
+  int64_t r = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    for (int64_t l : len[t]) {
+      m.ptr[r + 1] = m.ptr[r] + l;
+      ++r;
+    }
+    m.idx.insert(m.idx.end(), idx[t].begin(), idx[t].end());
+    if (abs_normal_values) m.val.insert(m.val.end(), val[t].begin(), val[t].end());
+    std::vector<int64_t>().swap(idx[t]);
+  }
   return m;
 }
 

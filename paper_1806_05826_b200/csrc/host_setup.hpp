@@ -86,5 +86,8 @@ std::vector<double> spd_inverse(const std::vector<double>& a, int64_t n, const s
 HostCsr synth_dense_clustered(int64_t n, int64_t f, int64_t groups, double noise, uint64_t seed);
 HostCsr synth_sparse_zipf(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
                           uint64_t seed);
+// Same distribution, one RNG stream per row (threaded): large measurement shards.
+HostCsr synth_sparse_zipf_rows(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
+                               uint64_t seed);
 
 }  // namespace rmg

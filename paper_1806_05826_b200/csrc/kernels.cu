@@ -7,8 +7,11 @@
 // tensor cores.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_set>
 
 #include "kernels.cuh"
 
@@ -77,6 +80,24 @@ __device__ __forceinline__ double sum_slots(const double* slots, int n, int stri
 
 __device__ __forceinline__ int ring_slot(const KrylovScalars* sc) { return sc->it % (sc->keep + 1); }
 
+// Streamed (read-once) index / value loads bypass L1 allocation so the L1
+// keeps the reused gather operand (v in K1, u in K2) instead of the stream.
+__device__ __forceinline__ int ld_stream(const int32_t* p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const uint16_t* p) {
+  unsigned short v;
+  asm("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(v) : "l"(p));
+  return (int)v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // ------------------------------------------------------------------ K1: t = X v
 // Row-parallel CSR gather; W lanes per row, two rows per lane group in flight
 // and 4 elements per lane per round, so each thread keeps up to 8 index loads
@@ -84,16 +105,36 @@ __device__ __forceinline__ int ring_slot(const KrylovScalars* sc) { return sc->i
 // 1 TB/s, profiles/r1_ncu_summary.md).  Column indices are uint16 when F <=
 // 65536 (half the index stream).  Warp-uniform trip counts keep the group
 // reductions convergent.  Per-row order: lane-strided partials, xor tree.
-template <int W, bool PAT, bool NARROW>
-__global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restrict__ ptr,
-                                                        const int32_t* __restrict__ idx,
-                                                        const uint16_t* __restrict__ idx16,
-                                                        const double* __restrict__ val,
-                                                        const double* __restrict__ v,
-                                                        double* __restrict__ t, int64_t rows,
-                                                        const int32_t* done,
-                                                        const KrylovScalars* sc, int ring_stride) {
+// Column relabeling for K1: when the matrix's columns are
+// renumbered by descending popularity, v is first gathered into that order
+// (vperm[j] = v[inv[j]]) so the hot columns' gathers share L1 lines.
+__global__ void __launch_bounds__(kThreads) k_vperm(const double* __restrict__ v_in, const int32_t* __restrict__ inv,
+                                                    double* __restrict__ vperm, int64_t cols, const int32_t* done,
+                                                    const KrylovScalars* sc, int ring_stride) {
   if (done != nullptr && *done) return;
+  const double* v = v_in;
+  if (sc != nullptr) {
+    if (sc->done) return;
+    v += (size_t)ring_slot(sc) * ring_stride;
+  }
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < cols; j += (int64_t)gridDim.x * kThreads)
+    vperm[j] = __ldg(v + inv[j]);
+}
+
+// Staging v in SMEM, and a CSR-Adaptive variant (block products in SMEM,
+// lane-per-row sums), were both tried in r1 and measured slower than this
+// kernel's L1 gathers (profiles/r1_operator.md).
+template <int W, bool PAT, bool NARROW, int NT = kThreads>
+__global__ void __launch_bounds__(NT) k_spmv_rows(const int32_t* __restrict__ ptr,
+                                                  const int32_t* __restrict__ idx,
+                                                  const uint16_t* __restrict__ idx16,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ v_in,
+                                                  double* __restrict__ t, int64_t rows,
+                                                  const int32_t* done,
+                                                  const KrylovScalars* sc, int ring_stride) {
+  if (done != nullptr && *done) return;
+  const double* v = v_in;
   if (sc != nullptr) {
     if (sc->done) return;
     v += (size_t)ring_slot(sc) * ring_stride;
@@ -102,21 +143,21 @@ __global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restric
   constexpr int U = 4;       // elements per lane per round
   const int lane = threadIdx.x & (W - 1);
   const int grp = (threadIdx.x & 31) / W;
-  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
   const int64_t span = nwarps * G;
   for (int64_t rb = warp * G; rb < rows; rb += 2 * span) {
     const int64_t ra = rb + grp, rbb = rb + span + grp;
-    const int a0 = ra < rows ? ptr[ra] : 0, a1 = ra < rows ? ptr[ra + 1] : 0;
-    const int b0 = rbb < rows ? ptr[rbb] : 0, b1 = rbb < rows ? ptr[rbb + 1] : 0;
+    const int a0 = ra < rows ? ld_stream(ptr + ra) : 0, a1 = ra < rows ? ld_stream(ptr + ra + 1) : 0;
+    const int b0 = rbb < rows ? ld_stream(ptr + rbb) : 0, b1 = rbb < rows ? ld_stream(ptr + rbb + 1) : 0;
     double sa = 0.0, sb = 0.0;
     for (int ka = a0 + lane, kb = b0 + lane; ka < a1 || kb < b1; ka += U * W, kb += U * W) {
       int ca[U], cb[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int pa = ka + u * W, pb = kb + u * W;
-        ca[u] = pa < a1 ? (NARROW ? (int)idx16[pa] : idx[pa]) : -1;
-        cb[u] = pb < b1 ? (NARROW ? (int)idx16[pb] : idx[pb]) : -1;
+        ca[u] = pa < a1 ? (NARROW ? ld_stream(idx16 + pa) : ld_stream(idx + pa)) : -1;
+        cb[u] = pb < b1 ? (NARROW ? ld_stream(idx16 + pb) : ld_stream(idx + pb)) : -1;
       }
       double xa[U], xb[U];
 #pragma unroll
@@ -126,8 +167,8 @@ __global__ void __launch_bounds__(kThreads) k_spmv_rows(const int32_t* __restric
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (ca[u] >= 0) sa += PAT ? xa[u] : val[ka + u * W] * xa[u];
-        if (cb[u] >= 0) sb += PAT ? xb[u] : val[kb + u * W] * xb[u];
+        if (ca[u] >= 0) sa += PAT ? xa[u] : ld_stream(val + ka + u * W) * xa[u];
+        if (cb[u] >= 0) sb += PAT ? xb[u] : ld_stream(val + kb + u * W) * xb[u];
       }
     }
     sa = group_sum<W>(sa);
@@ -206,8 +247,8 @@ __device__ __forceinline__ void xt_finalize(KrylovScalars* sc, double s0, double
 // uint16 offsets inside a block of B samples.
 template <bool BLK>
 __device__ __forceinline__ int xt_col(const XtSchedule& sch, const int32_t* __restrict__ idx, int64_t base, int k) {
-  if constexpr (BLK) return (int)(base + sch.idx16[k]);
-  return idx[k];
+  if constexpr (BLK) return (int)(base + ld_stream(sch.idx16 + k));
+  return ld_stream(idx + k);
 }
 
 // Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 4 elements per
@@ -226,7 +267,7 @@ __device__ __forceinline__ double xt_row_sum(const XtSchedule& sch, const int32_
     for (int u = 0; u < 4; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (c[u] >= 0) s += PAT ? x[u] : val[k + u * lanes] * x[u];
+      if (c[u] >= 0) s += PAT ? x[u] : ld_stream(val + k + u * lanes) * x[u];
   }
   return s;
 }
@@ -671,6 +712,16 @@ inline void check_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
 }
 
+// K1 / K2 keep almost no SMEM: ask for the largest L1 carveout (once per kernel).
+template <typename K>
+void prefer_l1(K kern) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> set;
+  std::lock_guard<std::mutex> lock(mu);
+  if (set.insert(reinterpret_cast<const void*>(kern)).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+}
+
 int grid_for(int64_t work_threads, int cap) {
   const int64_t g = (work_threads + kThreads - 1) / kThreads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
@@ -680,6 +731,8 @@ template <int W, bool PAT>
 void spmv_rows_impl(const SparseDev& x, const double* v, double* t, const int32_t* done,
                     const KrylovScalars* sc, int ring_stride, cudaStream_t s) {
   const int grid = grid_for((x.rows + 1) / 2 * W, 148 * 8);
+  prefer_l1(k_spmv_rows<W, PAT, true>);
+  prefer_l1(k_spmv_rows<W, PAT, false>);
   if (x.idx16 != nullptr)
     k_spmv_rows<W, PAT, true><<<grid, kThreads, 0, s>>>(x.ptr, x.idx, x.idx16, x.val, v, t, x.rows, done, sc,
                                                         ring_stride);
@@ -691,6 +744,13 @@ void spmv_rows_impl(const SparseDev& x, const double* v, double* t, const int32_
 template <bool PAT>
 void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* done, const KrylovScalars* sc,
                  int ring_stride, cudaStream_t s) {
+  if (x.col_inv != nullptr) {  // relabeled columns: v -> popularity order first
+    k_vperm<<<grid_for(x.cols, 148 * 4), kThreads, 0, s>>>(v, x.col_inv, x.vperm, x.cols, done, sc, ring_stride);
+    if (sc != nullptr) done = &sc->done;
+    v = x.vperm;
+    sc = nullptr;
+    ring_stride = 0;
+  }
   switch (x.width) {
     case 4: spmv_rows_impl<4, PAT>(x, v, t, done, sc, ring_stride, s); break;
     case 8: spmv_rows_impl<8, PAT>(x, v, t, done, sc, ring_stride, s); break;
@@ -717,13 +777,17 @@ void xt_impl_w(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs
     }
     return;
   }
+  auto go = [&](auto kern) {
+    prefer_l1(kern);
+    kern<<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a);
+  };
   switch (epi) {
-    case Epi::Plain: k_xt<W, PAT, Epi::Plain, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Axpby: k_xt<W, PAT, Epi::Axpby, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Fcg: k_xt<W, PAT, Epi::Fcg, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Cg: k_xt<W, PAT, Epi::Cg, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Rich: k_xt<W, PAT, Epi::Rich, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
-    case Epi::Gram: k_xt<W, PAT, Epi::Gram, false><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a); break;
+    case Epi::Plain: go(k_xt<W, PAT, Epi::Plain, false>); break;
+    case Epi::Axpby: go(k_xt<W, PAT, Epi::Axpby, false>); break;
+    case Epi::Fcg: go(k_xt<W, PAT, Epi::Fcg, false>); break;
+    case Epi::Cg: go(k_xt<W, PAT, Epi::Cg, false>); break;
+    case Epi::Rich: go(k_xt<W, PAT, Epi::Rich, false>); break;
+    case Epi::Gram: go(k_xt<W, PAT, Epi::Gram, false>); break;
   }
 }
 

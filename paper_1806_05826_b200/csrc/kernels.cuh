@@ -50,6 +50,8 @@ struct SparseDev {
   const uint16_t* idx16 = nullptr;  // narrow column indices when cols <= 65536 (K1)
   const double* val = nullptr;  // nullptr -> binary pattern
   int width = 8;                // lanes per row (4, 8, 16, 32)
+  const int32_t* col_inv = nullptr;  // relabeled columns: original column of label j (K1 v-permute)
+  double* vperm = nullptr;           // [cols] scratch: v in label order
 };
 
 // Work items for the X^T pass, by row-length class of the (virtual) X^T CSR:

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <thread>
 
 #include "runtime.cuh"
@@ -63,15 +64,36 @@ std::vector<int32_t> narrow(const std::vector<int64_t>& v, const char* what) {
 
 }  // namespace
 
-void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16) {
+void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16, bool relabel) {
   const auto p32 = narrow(h.ptr, "row offsets");
   ptr.upload(p32.data(), p32.size(), s);
+  // Relabel: label = rank of the column by descending nonzero count (ties by
+  // column).  Each row keeps its original element order, so every row sum
+  // adds the same terms in the same order as without relabeling.
+  std::vector<int32_t> label;
+  if (relabel) {
+    std::vector<int64_t> cnt(h.f, 0);
+    for (int64_t c : h.idx) ++cnt[c];
+    std::vector<int32_t> inv(h.f);
+    std::iota(inv.begin(), inv.end(), 0);
+    std::stable_sort(inv.begin(), inv.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+    label.resize(h.f);
+    for (int64_t j = 0; j < h.f; ++j) label[inv[j]] = static_cast<int32_t>(j);
+    col_inv.upload(inv.data(), inv.size(), s);
+    vperm.alloc(std::max<int64_t>(1, h.f));
+  }
+  auto col = [&](size_t k) -> int64_t { return relabel ? label[h.idx[k]] : h.idx[k]; };
   if (narrow16) {  // uint16 column indices (half the index stream)
     std::vector<uint16_t> i16(h.idx.size());
-    for (size_t k = 0; k < h.idx.size(); ++k) i16[k] = static_cast<uint16_t>(h.idx[k]);
+    for (size_t k = 0; k < h.idx.size(); ++k) i16[k] = static_cast<uint16_t>(col(k));
     idx16.upload(i16.data(), i16.size(), s);
   } else {
-    const auto i32 = narrow(h.idx, "column indices");
+    std::vector<int32_t> i32(h.idx.size());
+    for (size_t k = 0; k < h.idx.size(); ++k) {
+      const int64_t c = col(k);
+      if (c < 0 || c > INT32_MAX) throw InvalidArgument("column indices exceed the int32 device index range");
+      i32[k] = static_cast<int32_t>(c);
+    }
     idx.upload(i32.data(), i32.size(), s);
   }
   if (!pattern) val.upload(h.val.data(), h.val.size(), s);
@@ -84,6 +106,8 @@ void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool n
   view.idx16 = narrow16 ? idx16.get() : nullptr;
   view.val = pattern ? nullptr : val.get();
   view.width = lanes_for(h.n ? static_cast<double>(h.nnz()) / static_cast<double>(h.n) : 1.0);
+  view.col_inv = relabel ? col_inv.get() : nullptr;
+  view.vperm = relabel ? vperm.get() : nullptr;
 }
 
 // Work items over the rows of a (possibly sample-blocked, virtual) X^T CSR,
@@ -92,7 +116,8 @@ void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool n
 // about C nonzeros, so no lane group owns a row much longer than its peers'.
 void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows) {
   const int64_t V = xt.n, nnz = xt.nnz();
-  const int64_t C = std::max<int64_t>(512, std::min<int64_t>(16384, nnz / (148 * 4)));
+  // ~12 items per SM: the first schedule (4 per SM) ran 0.61 waves at 29 % occupancy
+  const int64_t C = std::max<int64_t>(512, std::min<int64_t>(16384, nnz / (148 * 12)));
   // lane width from the median row length among rows that are not long
   std::vector<int64_t> lens;
   lens.reserve(V);
@@ -307,7 +332,11 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), h
     RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
   }
   const HostCsr& local = comm != nullptr ? shard : host;
-  x.upload(local, pattern, ctx->stream, local.f <= 65536);
+  // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
+  // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
+  const char* rl = std::getenv("RMG_RELABEL");
+  const bool relabel = rl != nullptr ? std::string(rl) == "1" : local.f * 8 > 192 * 1024;
+  x.upload(local, pattern, ctx->stream, local.f <= 65536, relabel);
   const HostCsr ht = transpose(local);
   // Sample blocking of X^T: 8192-sample blocks keep each CTA's
   // t-gathers in a 64 KB slice; used when the per-block bookkeeping (one

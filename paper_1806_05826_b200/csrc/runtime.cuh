@@ -84,10 +84,11 @@ struct Context {
 // One orientation of a sparse matrix on the device.
 struct DeviceSparse {
   SparseDev view;
-  DBuf<int32_t> ptr, idx;
+  DBuf<int32_t> ptr, idx, col_inv;
   DBuf<uint16_t> idx16;
-  DBuf<double> val;
-  void upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16 = false);
+  DBuf<double> val, vperm;
+  // relabel: renumber columns by descending popularity (K1 gathers)
+  void upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16 = false, bool relabel = false);
 };
 
 struct DeviceSchedule {

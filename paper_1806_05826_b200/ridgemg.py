@@ -140,12 +140,12 @@ def _host_csr_to_matrix(h, n: int, f: int, nnz: int, pattern: bool) -> FeatureMa
     lib = _lib.load()
     rp = np.zeros(n + 1, np.uint64)
     ci = np.zeros(nnz, np.uint64)
-    v = np.zeros(nnz, np.float64)
+    v = None if pattern else np.zeros(nnz, np.float64)
     try:
-        _lib.check(lib.rmg_host_csr_export(h, _ptr(rp), _ptr(ci), _ptr(v)))
+        _lib.check(lib.rmg_host_csr_export(h, _ptr(rp), _ptr(ci), None if v is None else _ptr(v)))
     finally:
         lib.rmg_host_csr_destroy(h)
-    return FeatureMatrix(n, f, rp, ci, None if pattern else v)
+    return FeatureMatrix(n, f, rp, ci, v)
 
 
 def synth_dense_clustered(n: int, f: int, groups: int = 50, noise: float = 0.1, seed: int = 0) -> FeatureMatrix:
@@ -157,12 +157,13 @@ def synth_dense_clustered(n: int, f: int, groups: int = 50, noise: float = 0.1, 
 
 
 def synth_sparse_zipf(n: int, f: int, mean_nnz: float, zipf_s: float, abs_normal_values: bool = False,
-                      seed: int = 0) -> FeatureMatrix:
-    """BASELINE cfg 2/3/5 generator."""
+                      seed: int = 0, row_streams: bool = False) -> FeatureMatrix:
+    """BASELINE cfg 2/3/5 generator.  row_streams=True: same
+    distribution, one RNG stream per row, threaded (large measurement shards)."""
     lib = _lib.load()
     h, nnz = C.c_void_p(), C.c_uint64()
-    _lib.check(lib.rmg_synth_sparse_zipf(n, f, mean_nnz, zipf_s, int(abs_normal_values), seed, C.byref(h),
-                                         C.byref(nnz)))
+    fn = lib.rmg_synth_sparse_zipf_rows if row_streams else lib.rmg_synth_sparse_zipf
+    _lib.check(fn(n, f, mean_nnz, zipf_s, int(abs_normal_values), seed, C.byref(h), C.byref(nnz)))
     return _host_csr_to_matrix(h, n, f, nnz.value, not abs_normal_values)
 
 
