@@ -121,9 +121,60 @@ __global__ void __launch_bounds__(kThreads) k_vperm(const double* __restrict__ v
     vperm[j] = __ldg(v + inv[j]);
 }
 
-// Staging v in SMEM, and a CSR-Adaptive variant (block products in SMEM,
-// lane-per-row sums), were both tried in r1 and measured slower than this
-// kernel's L1 gathers (profiles/r1_operator.md).
+// K1 over SELL-32: one warp per 32-row slice, one lane per
+// row, elements column-major inside the slice (every index load is one
+// coalesced 128 B line).  Rows hold their elements in descending column
+// popularity, so instruction j gathers the j-th most popular column of 32
+// rows: the first instructions land on a handful of L1 lines instead of 32.
+// Per-row sum: sequential in that order (deterministic).
+template <bool PAT, bool NARROW>
+__global__ void __launch_bounds__(kThreads) k_spmv_sell(const int32_t* __restrict__ off,
+                                                        const int32_t* __restrict__ srow,
+                                                        const int32_t* __restrict__ slen,
+                                                        const int32_t* __restrict__ idx,
+                                                        const uint16_t* __restrict__ idx16,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ v_in, double* __restrict__ t,
+                                                        int64_t n_slices, const int32_t* done,
+                                                        const KrylovScalars* sc, int ring_stride) {
+  if (done != nullptr && *done) return;
+  const double* __restrict__ v = v_in;
+  if (sc != nullptr) {
+    if (sc->done) return;
+    v += (size_t)ring_slot(sc) * ring_stride;
+  }
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t sl = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; sl < n_slices; sl += nwarps) {
+    const int64_t base = off[sl];
+    const int L = (off[sl + 1] - off[sl]) >> 5;
+    const int row = srow[sl * 32 + lane];
+    const int len = slen[sl * 32 + lane];
+    double s = 0.0;
+    for (int j = 0; j < L; j += U) {
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = base + (int64_t)(j + u) * 32 + lane;
+        c[u] = j + u < len ? (NARROW ? ld_stream(idx16 + q) : ld_stream(idx + q)) : -1;
+      }
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(v + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s += PAT ? x[u] : ld_stream(val + base + (int64_t)(j + u) * 32 + lane) * x[u];
+    }
+    if (row >= 0) t[row] = s;
+  }
+}
+
+// K1 over row CSR (RMG_K1=csr diagnostics; the default is SELL-32 above).
+// Tried in r1 and measured slower than SELL on cfg 2 and the cfg 5 shard
+// (profiles/r1_operator.md): v staged in SMEM; a CSR-Adaptive variant (block
+// products in SMEM, lane-per-row sums); the hottest columns in SMEM (halved
+// occupancy); L1::evict_last for hot / no_allocate for cold columns.
 template <int W, bool PAT, bool NARROW, int NT = kThreads>
 __global__ void __launch_bounds__(NT) k_spmv_rows(const int32_t* __restrict__ ptr,
                                                   const int32_t* __restrict__ idx,
@@ -750,6 +801,19 @@ void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* 
     v = x.vperm;
     sc = nullptr;
     ring_stride = 0;
+  }
+  if (x.sell_off != nullptr) {
+    const int grid = grid_for(x.n_slices * 32, 148 * 8);
+    auto go = [&](auto kern) {
+      prefer_l1(kern);
+      kern<<<grid, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, v, t, x.n_slices,
+                                     done, sc, ring_stride);
+    };
+    if (x.idx16 != nullptr)
+      go(k_spmv_sell<PAT, true>);
+    else
+      go(k_spmv_sell<PAT, false>);
+    return;
   }
   switch (x.width) {
     case 4: spmv_rows_impl<4, PAT>(x, v, t, done, sc, ring_stride, s); break;

@@ -52,6 +52,11 @@ struct SparseDev {
   int width = 8;                // lanes per row (4, 8, 16, 32)
   const int32_t* col_inv = nullptr;  // relabeled columns: original column of label j (K1 v-permute)
   double* vperm = nullptr;           // [cols] scratch: v in label order
+  // SELL-32 (K1): slice s holds 32 rows column-major at [sell_off[s], sell_off[s+1])
+  const int32_t* sell_off = nullptr;  // [n_slices + 1]
+  const int32_t* sell_row = nullptr;  // [n_slices * 32] row of each slot (-1: padding)
+  const int32_t* sell_len = nullptr;  // [n_slices * 32] elements of each slot
+  int64_t n_slices = 0;
 };
 
 // Work items for the X^T pass, by row-length class of the (virtual) X^T CSR:

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -108,6 +109,95 @@ void DeviceSparse::upload(const HostCsr& h, bool pattern, cudaStream_t s, bool n
   view.width = lanes_for(h.n ? static_cast<double>(h.nnz()) / static_cast<double>(h.n) : 1.0);
   view.col_inv = relabel ? col_inv.get() : nullptr;
   view.vperm = relabel ? vperm.get() : nullptr;
+}
+
+void DeviceSparse::upload_sell(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16, bool relabel) {
+  const int64_t n = h.n, f = h.f;
+  // popularity rank of every column (descending count, ties by column)
+  std::vector<int64_t> cnt(f, 0);
+  for (int64_t c : h.idx) ++cnt[c];
+  std::vector<int32_t> inv(f);
+  std::iota(inv.begin(), inv.end(), 0);
+  std::stable_sort(inv.begin(), inv.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+  std::vector<int32_t> rank(f);
+  for (int64_t j = 0; j < f; ++j) rank[inv[j]] = static_cast<int32_t>(j);
+  // rows: length-descending inside 1024-row windows (32 slices per window)
+  constexpr int64_t kWin = 1024;
+  std::vector<int32_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  auto len = [&](int64_t r) { return h.ptr[r + 1] - h.ptr[r]; };
+  for (int64_t w0 = 0; w0 < n; w0 += kWin)
+    std::stable_sort(order.begin() + w0, order.begin() + std::min(n, w0 + kWin),
+                     [&](int32_t a, int32_t b) { return len(a) > len(b); });
+  const int64_t ns = (n + 31) / 32;
+  std::vector<int64_t> off(ns + 1, 0);
+  for (int64_t sl = 0; sl < ns; ++sl) off[sl + 1] = off[sl] + 32 * len(order[sl * 32]);
+  if (off[ns] > INT32_MAX) throw InvalidArgument("SELL layout exceeds the int32 device index range");
+  std::vector<int32_t> srow(ns * 32, -1), slen(ns * 32, 0), i32;
+  std::vector<uint16_t> i16;
+  std::vector<double> vals;
+  if (narrow16)
+    i16.assign(off[ns], 0);
+  else
+    i32.assign(off[ns], 0);
+  if (!pattern) vals.assign(off[ns], 0.0);
+  const int64_t T = std::max<int64_t>(1, std::min<int64_t>(64, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int64_t t = 0; t < T; ++t) {
+    pool.emplace_back([&, t] {
+      std::vector<std::pair<int32_t, int64_t>> el;
+      for (int64_t sl = t; sl < ns; sl += T) {
+        for (int lane = 0; lane < 32; ++lane) {
+          const int64_t q = sl * 32 + lane;
+          if (q >= n) break;
+          const int64_t r = order[q];
+          srow[q] = static_cast<int32_t>(r);
+          slen[q] = static_cast<int32_t>(len(r));
+          el.clear();
+          for (int64_t k = h.ptr[r]; k < h.ptr[r + 1]; ++k) el.emplace_back(rank[h.idx[k]], k);
+          std::sort(el.begin(), el.end());
+          for (size_t j = 0; j < el.size(); ++j) {
+            const int64_t d = off[sl] + static_cast<int64_t>(j) * 32 + lane;
+            const int64_t c = h.idx[el[j].second];
+            const int64_t lab = relabel ? rank[c] : c;
+            if (narrow16)
+              i16[d] = static_cast<uint16_t>(lab);
+            else
+              i32[d] = static_cast<int32_t>(lab);
+            if (!pattern) vals[d] = h.val[el[j].second];
+          }
+        }
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  std::vector<int32_t> off32(off.begin(), off.end());
+  sell_off.upload(off32.data(), off32.size(), s);
+  sell_row.upload(srow.data(), srow.size(), s);
+  sell_len.upload(slen.data(), slen.size(), s);
+  if (narrow16)
+    idx16.upload(i16.data(), i16.size(), s);
+  else
+    idx.upload(i32.data(), i32.size(), s);
+  if (!pattern) val.upload(vals.data(), vals.size(), s);
+  if (relabel) {
+    col_inv.upload(inv.data(), inv.size(), s);
+    vperm.alloc(std::max<int64_t>(1, f));
+  }
+  RMG_CK(cudaStreamSynchronize(s));
+  view = SparseDev{};
+  view.rows = n;
+  view.cols = f;
+  view.nnz = h.nnz();
+  view.idx = narrow16 ? nullptr : idx.get();
+  view.idx16 = narrow16 ? idx16.get() : nullptr;
+  view.val = pattern ? nullptr : val.get();
+  view.col_inv = relabel ? col_inv.get() : nullptr;
+  view.vperm = relabel ? vperm.get() : nullptr;
+  view.sell_off = sell_off.get();
+  view.sell_row = sell_row.get();
+  view.sell_len = sell_len.get();
+  view.n_slices = ns;
 }
 
 // Work items over the rows of a (possibly sample-blocked, virtual) X^T CSR,
@@ -336,7 +426,11 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), h
   // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
   const char* rl = std::getenv("RMG_RELABEL");
   const bool relabel = rl != nullptr ? std::string(rl) == "1" : local.f * 8 > 192 * 1024;
-  x.upload(local, pattern, ctx->stream, local.f <= 65536, relabel);
+  const char* k1 = std::getenv("RMG_K1");  // "csr": the row-CSR K1 (diagnostics)
+  if (k1 != nullptr && std::string(k1) == "csr")
+    x.upload(local, pattern, ctx->stream, local.f <= 65536, relabel);
+  else
+    x.upload_sell(local, pattern, ctx->stream, local.f <= 65536, relabel);
   const HostCsr ht = transpose(local);
   // Sample blocking of X^T: 8192-sample blocks keep each CTA's
   // t-gathers in a 64 KB slice; used when the per-block bookkeeping (one
@@ -650,6 +744,12 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     ec_last_.alloc(std::max<int64_t>(1, fc_last));
     // workspaces: level 0 = outer FCG, level k >= 1 = inner solve configured by spec k-1
     work_.push_back(std::make_unique<KrylovWork>(x->f(), keep0, solver.max_iters, solver.tol, s));
+    if (const char* pad = std::getenv("RMG_DENSE_PAD"))  // diagnostics: shift the inner buffers
+      pad_.alloc(static_cast<size_t>(std::atoll(pad)));
+    if (const char* pad = std::getenv("RMG_PAD_W")) {
+      pads_.emplace_back();
+      pads_.back().alloc(static_cast<size_t>(std::atoll(pad)));
+    }
     for (uint64_t k = 1; k < L; ++k) {
       const rmg_level_spec& sp = specs_[k - 1].spec;
       const int keep = static_cast<int>(std::max<uint64_t>(sp.coarse_truncation, 1));
@@ -657,6 +757,8 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
           std::make_unique<KrylovWork>(level_matrix(k).f(), keep, sp.coarse_max_iters, sp.coarse_tol, s));
     }
     build_dense_levels(inv);
+    for (size_t k = 1; k < dense_.size(); ++k)
+      if (dense_[k]) tune_dense_partials(k);
   }
   ctx_->sync();
 }
@@ -679,7 +781,15 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
     d->fcg = fcg;
     d->omega = omega_[k];
     const std::vector<double> a = coarse_gram(level_matrix(k).host, level_beta(k));  // X_k^T X_k + beta_k I
+    auto padk = [&](const char* name) {  // diagnostics: shift one buffer group
+      if (const char* e = std::getenv(name)) {
+        pads_.emplace_back();
+        pads_.back().alloc(static_cast<size_t>(std::atoll(e)));
+      }
+    };
+    padk("RMG_PAD_A");
     d->A.upload(a.data(), a.size(), s);
+    padk("RMG_PAD_Q");
     if (fcg) {  // Q = (I - omega A_k) P A_{k+1}^{-1}
       const Aggregation& agg = coarse_[k]->agg;
       const int64_t nc = agg.n_coarse;
@@ -713,6 +823,7 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
       d->Q.upload(mm.data(), mm.size(), s);
     }
     d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
+    padk("RMG_PAD_P");
     d->pap_ring.alloc(kMaxKeep + 2);
     // own 2 MB-granular allocation: the cross-CTA partials are read by every CTA
     // after every grid barrier, so their placement is on the critical path
@@ -726,7 +837,7 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
   }
 }
 
-uint64_t Method::run_dense(size_t k, const double* rhs) {
+DenseKrylovArgs Method::dense_args(size_t k, const double* rhs) {
   DenseInner& d = *dense_[k];
   KrylovWork& w = *work_[k];
   DenseKrylovArgs a;
@@ -752,15 +863,75 @@ uint64_t Method::run_dense(size_t k, const double* rhs) {
   a.sc = w.sc.get();
   a.timing = d.timing.get();
   if (const char* dbg = std::getenv("RMG_DENSE_DBG")) a.dbg = std::atoi(dbg);
+  return a;
+}
+
+uint64_t Method::run_dense(size_t k, const double* rhs) {
+  const DenseKrylovArgs a = dense_args(k, rhs);
   OpProfile* pr = prof(k);  // level-k profile: K1 slot = whole persistent inner solve
   if (pr) pr->mark(ctx_->stream);
-  launch_dense_krylov(d.plan, a, ctx_->stream);
+  launch_dense_krylov(dense_[k]->plan, a, ctx_->stream);
   if (pr) {
     pr->mark(ctx_->stream);
     pr->mark(ctx_->stream);
   }
   ctx_->launches += 1;
   return 0;
+}
+
+// The cross-CTA partials are written and re-read by every CTA after every grid
+// barrier; which physical pages they land on moves an inner iteration between
+// ~22 and ~29 us on B200 (measured by shifting only this buffer, DESIGN.md
+// §4.4).  Physical placement is not controllable, so it is tuned: 8 candidate
+// buffers, each timed on a fixed 40-iteration inner solve of a synthetic rhs,
+// the fastest kept.  Numerics do not depend on the choice.
+void Method::tune_dense_partials(size_t k) {
+  if (std::getenv("RMG_DENSE_NO_TUNE") != nullptr) return;
+  DenseInner& d = *dense_[k];
+  cudaStream_t s = ctx_->stream;
+  const int64_t n = level_matrix(k).f();
+  constexpr int kCand = 8;
+  const size_t count = d.partials.size();
+  std::vector<DBuf<double>> cand;
+  cand.push_back(std::move(d.partials));
+  for (int c = 1; c < kCand; ++c) {
+    cand.emplace_back();
+    cand.back().alloc(count);
+  }
+  DBuf<double> b(std::max<int64_t>(1, n));
+  launch_fill(b.get(), 1.0, n, s);
+  cudaEvent_t e0, e1;
+  RMG_CK(cudaEventCreate(&e0));
+  RMG_CK(cudaEventCreate(&e1));
+  std::vector<float> best_ms(kCand, 1e30f);
+  for (int rep = 0; rep < 3; ++rep) {
+    for (int c = 0; c < kCand; ++c) {
+      d.partials = std::move(cand[c]);
+      DenseKrylovArgs a = dense_args(k, b.get());
+      a.tol = 0.0;
+      a.max_iters = 40;
+      a.timing = nullptr;
+      RMG_CK(cudaEventRecord(e0, s));
+      launch_dense_krylov(d.plan, a, s);
+      RMG_CK(cudaEventRecord(e1, s));
+      RMG_CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      RMG_CK(cudaEventElapsedTime(&ms, e0, e1));
+      best_ms[c] = std::min(best_ms[c], ms);
+      cand[c] = std::move(d.partials);
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const int best = static_cast<int>(std::min_element(best_ms.begin(), best_ms.end()) - best_ms.begin());
+  d.partials = std::move(cand[best]);
+  d.tuned_ms.assign(best_ms.begin(), best_ms.end());
+  d.tuned_pick = best;
+  if (std::getenv("RMG_DENSE_TUNE_LOG") != nullptr) {
+    std::fprintf(stderr, "[rmg] level %zu partials placement (ms / 40 it):", k);
+    for (int c = 0; c < kCand; ++c) std::fprintf(stderr, " %.3f%s", best_ms[c], c == best ? "*" : "");
+    std::fprintf(stderr, "\n");
+  }
 }
 
 const std::vector<int64_t>& Method::labels(size_t k) const {

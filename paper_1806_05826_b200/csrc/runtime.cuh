@@ -84,11 +84,14 @@ struct Context {
 // One orientation of a sparse matrix on the device.
 struct DeviceSparse {
   SparseDev view;
-  DBuf<int32_t> ptr, idx, col_inv;
+  DBuf<int32_t> ptr, idx, col_inv, sell_off, sell_row, sell_len;
   DBuf<uint16_t> idx16;
   DBuf<double> val, vperm;
   // relabel: renumber columns by descending popularity (K1 gathers)
   void upload(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16 = false, bool relabel = false);
+  // K1 layout: SELL-32 slices, rows length-sorted in 1024-row
+  // windows, each row's elements in descending column popularity.
+  void upload_sell(const HostCsr& h, bool pattern, cudaStream_t s, bool narrow16, bool relabel);
 };
 
 struct DeviceSchedule {
@@ -202,6 +205,8 @@ struct DenseInner {
   int nc = 0;
   DBuf<double> A, Q, pap_ring, partials, cg_shared;
   DBuf<unsigned long long> timing;  // RMG_DENSE_TIMING diagnostics
+  std::vector<float> tuned_ms;      // partials placement candidates (ms per 40 iterations)
+  int tuned_pick = 0;
 };
 
 struct SolveResult {
@@ -252,7 +257,11 @@ class Method {
   std::vector<std::unique_ptr<DenseInner>> dense_;  // per level (nullptr: host-sequenced path)
   void build_dense_levels(const std::vector<double>& ainv_host);
   uint64_t run_dense(size_t k, const double* rhs);
+  DenseKrylovArgs dense_args(size_t k, const double* rhs);
+  void tune_dense_partials(size_t k);
   DBuf<double> ainv_, rc_last_, ec_last_;
+  DBuf<char> pad_;  // RMG_DENSE_PAD diagnostics
+  std::vector<DBuf<char>> pads_;
   DBuf<double> inv_diag_;
   std::vector<std::vector<int64_t>> labels_;
 };

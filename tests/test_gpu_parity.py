@@ -340,12 +340,21 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     assert abs(cg.report.iterations - int(g["cg_iterations"])) <= max(2, 3 * env["cg_iter_spread"]), \
         (cg.report.iterations, int(g["cg_iterations"]))
     assert rel_diff(cg.w, g["cg_w"]) <= 1e-6, (rel_diff(cg.w, g["cg_w"]), env)
-    # Driven to tol 1e-12 both converge onto the same solution: the strict bar.
+    # Driven to tol 1e-12: the strict bar.  The reference's CG converges there
+    # (cg12); its multilevel FCG converges on cfg2_small but stagnates near 1e-9
+    # on cfg2_full (inexact inner solves, ml12_converged = 0 in the golden) at a
+    # w 1.2e-9 from the CG solution, so there the GPU multilevel w is held to
+    # the CG solution at the same 1e-8 bar.
     if "ml12_w" in g.files:
         spec12 = _cfg2_spec(ks, [g[f"labels{i}"].astype(np.int64) for i in range(len(ks))])
         spec12.solver = R.SolverConfig(1e-12, 1000)
         w12, rep12 = R.PreparedMethod(m, 1.0, spec12).solve(g["b"])
-        assert rep12.converged
-        assert rel_diff(w12, g["ml12_w"]) <= W_TOL, rel_diff(w12, g["ml12_w"])
         cg12 = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-12, 5000)))
         assert rel_diff(cg12.w, g["cg12_w"]) <= W_TOL, rel_diff(cg12.w, g["cg12_w"])
+        if int(g["ml12_converged"]):
+            assert rep12.converged
+            assert rel_diff(w12, g["ml12_w"]) <= W_TOL, rel_diff(w12, g["ml12_w"])
+        else:
+            assert rel_diff(g["ml12_w"], g["cg12_w"]) <= W_TOL  # the reference's own gap
+            assert float(rep12.residual_history[-1]) <= 10 * float(g["ml12_hist"][-1])
+            assert rel_diff(w12, g["cg12_w"]) <= W_TOL, rel_diff(w12, g["cg12_w"])
