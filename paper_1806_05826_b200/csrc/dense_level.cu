@@ -8,9 +8,14 @@
 //     (mathematically GalerkinOperator::apply, coarsening.cpp:174-185);
 //   * with a direct coarsest level below, the level-k preconditioner
 //     (krylov.cpp:379-420) is the fixed linear map
-//         z = omega r + M r,   M = (I - omega A_k) P A_{k+1}^{-1} P^T
-//     precomputed once (n x n); no restriction/prolongation gathers remain,
-//     so unbalanced clusters (cfg 2 has one of 317 members) cost nothing;
+//         z = omega r + Q (P^T r),   Q = (I - omega A_k) P A_{k+1}^{-1}  (n x nc)
+//     with Q precomputed once.  The level's unknowns are held in next-level
+//     cluster order, so P^T r is a sum of per-CTA segment partials: each CTA
+//     scans its owned rows by cluster right after its r update (before the
+//     barrier that already ends the iteration) and every CTA gathers the
+//     ~grid + nc partials at the next z step.  Per iteration a CTA streams
+//     its n_c-wide rows of Q (22 KB on cfg 2) instead of n-wide rows of the
+//     dense M = Q P^T (224 KB; the fallback when nc exceeds the scratch);
 //   * one cooperative launch runs the whole inner solve: <= 148 CTAs x 256
 //     threads, each CTA owns a contiguous block of rows, keeps its rows of A_k
 //     resident in shared memory when they fit (2000 x 2000 fp64 = 32 MB
@@ -73,13 +78,32 @@ __device__ __forceinline__ int slot_stride() { return (gridDim.x + 31) & ~31; }
 // out[q] = sum over blocks b (fixed order) of partials[first + q][b], q < count,
 // one warp per quantity; ends with __syncthreads so every thread may read out.
 __device__ __forceinline__ void grid_sums(const double* partials, int first, int count, double* out) {
+  // All loads of a warp's (up to 4) quantities are issued before any add, so
+  // the sums cost one L2 round trip instead of one per quantity; per lane the
+  // order (b = lane, lane + 32, ...) and the warp tree are unchanged.
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int q = wid; q < count; q += kW) {
-    double acc = 0.0;
-    const double* row = partials + (size_t)(first + q) * slot_stride(); // slot-major: 143 contiguous doubles
-    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(row + b);
-    acc = wsum(acc);
-    if (lane == 0) out[q] = acc;
+  const int stride = slot_stride(), nb = gridDim.x;
+  for (int q0 = wid; q0 < count; q0 += 4 * kW) {
+    double x[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = q0 + j * kW;
+      const double* row = partials + (size_t)(first + q) * stride;  // slot-major: grid contiguous doubles
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = lane + 32 * u;
+        x[j][u] = (q < count && b < nb) ? __ldcg(row + b) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (lane + 32 * u < nb) acc += x[j][u];
+      acc = wsum(acc);
+      if (lane == 0 && q0 + j * kW < count) out[q0 + j * kW] = acc;
+    }
   }
   __syncthreads();
 }
@@ -109,6 +133,70 @@ __device__ __forceinline__ void gemv_rows(const double* rows, int nr, int n, con
       const double s = wsum(acc[u]);
       if (lane == 0 && lr0 + u < nr) red[(lr0 + u) * kW + wid] = s;
     }
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
+
+// Low-rank preconditioner: partial sums of w r over the owned rows, one per
+// (CTA, cluster) segment, by warp 0 (owned rows <= 28 = lanes).  Segmented
+// inclusive warp scan in cluster order; the segment's last lane stores it.
+// The per-lane layout (weight, head / end flags, segment slot) is constant for
+// the solve and computed once.
+struct SegLane {
+  double w = 0.0;
+  bool head = false, end = false;
+  int slot = -1;
+};
+
+__device__ __forceinline__ SegLane segment_layout(const DenseKrylovArgs& a, int row0, int nr) {
+  SegLane L;
+  const int lane = threadIdx.x & 31;
+  const bool own = lane < nr;
+  const int cl = own ? a.cid[row0 + lane] : -1;
+  const int prevc = __shfl_up_sync(0xffffffffu, cl, 1);
+  const int nextc = __shfl_down_sync(0xffffffffu, cl, 1);
+  L.head = own && (lane == 0 || prevc != cl);
+  L.end = own && (lane == nr - 1 || nextc != cl);
+  const unsigned heads = __ballot_sync(0xffffffffu, L.head);
+  L.slot = a.cta_seg0[blockIdx.x] + __popc(heads & ((2u << lane) - 1u)) - 1;
+  L.w = own ? a.wts[row0 + lane] : 0.0;
+  return L;
+}
+
+__device__ __forceinline__ void segment_partials(const DenseKrylovArgs& a, const SegLane& L, double ri) {
+  const int lane = threadIdx.x & 31;
+  double v = L.w * ri;
+  bool f = L.head;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, v, d);
+    const bool g = __shfl_up_sync(0xffffffffu, f, d);
+    if (lane >= d && !f) {
+      v += y;
+      f = g;
+    }
+  }
+  if (L.end) a.spart[L.slot] = v;
+}
+
+// Narrow GEMV for the low-rank preconditioner (nc <= kT columns, nr <= 28
+// rows): thread tid owns column tid; its rows' entries q[] are loaded by the
+// caller ahead of the cluster sums (one overlapped L2 round trip instead of
+// one per 4-row chunk).  Result in out[lr] (fixed-order warp combine).
+__device__ __forceinline__ void gemv_narrow(const double (&q)[28], int nr, double sv, double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, tid = threadIdx.x;
+#pragma unroll
+  for (int lr = 0; lr < 28; ++lr) {
+    if (lr >= nr) break;
+    const double s = wsum(q[lr] * sv);
+    if (lane == 0) red[lr * kW + wid] = s;
   }
   __syncthreads();
   if (tid < nr) {
@@ -152,7 +240,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   auto part = [&](int slot) -> double& { return a.partials[(size_t)slot * pstride + blockIdx.x]; };
   KrylovScalars* sc = a.sc;
   const double* Arows = SMEM ? As : a.A + (size_t)row0 * n;
-  const double* Mrows = a.M + (size_t)row0 * n;
+  const double* Mrows = a.M + (size_t)row0 * (a.lowrank ? a.nc : n);
+  auto orig = [&](int i) { return a.perm != nullptr ? a.perm[i] : i; };
 
   if (SMEM) {
     for (int idx = tid; idx < nr * n; idx += kT) As[idx] = a.A[(size_t)row0 * n + idx];
@@ -160,11 +249,16 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   // ---- begin: x = 0, r = b, ||b|| (krylov.cpp:164-176)
   double bb = 0.0, bad = 0.0;
   for (int i = row0 + tid; i < row1; i += kT) {
-    const double bi = a.b[i];
+    const double bi = a.b[orig(i)];
     a.x[i] = 0.0;
     a.r[i] = bi;
     bb += bi * bi;
     if (!isfinite(bi)) bad += 1.0;
+  }
+  SegLane seg;
+  if (a.lowrank && tid < 32) {
+    seg = segment_layout(a, row0, nr);
+    segment_partials(a, seg, tid < nr ? a.b[orig(row0 + tid)] : 0.0);
   }
   bb = bsum_all(bb, sh);
   bad = bsum_all(bad, sh);
@@ -186,6 +280,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       sc->nb = nb;
       if (nbad == 0.0) a.hist[0] = 0.0;
     }
+    if (a.x_out != a.x)
+      for (int i = row0 + tid; i < row1; i += kT) a.x_out[orig(i)] = 0.0;
     return;
   }
   const int keep = a.keep, RING = keep + 1;
@@ -203,17 +299,43 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
     tmark(a, it, 0);
     // ---- z = M^{-1} r for the owned rows: omega r + M r (FCG) or r (CG)
     if (a.fcg) {
-      double rc[kMaxQ];
-#pragma unroll
-      for (int q = 0; q < kMaxQ; ++q) {
-        const int c = tid + q * kT;
-        rc[q] = c < n ? __ldcg(a.r + c) : 0.0;
-      }
-      if (!(a.dbg & 1)) {
-        gemv_rows<true>(Mrows, nr, n, rc, red, vv);
-      } else {
+      if (a.dbg & 1) {
         if (tid < nr) vv[tid] = 0.0;
         __syncthreads();
+      } else if (a.lowrank) {  // S = P^T r from the segment partials, then Q S
+        if (a.nc <= kT) {
+          double q[28];  // this thread's column of the owned rows of Q, in flight first
+#pragma unroll
+          for (int lr = 0; lr < 28; ++lr)
+            q[lr] = (lr < nr && tid < a.nc) ? __ldg(Mrows + (size_t)lr * a.nc + tid) : 0.0;
+          for (int g = tid; g < a.n_segments; g += kT) contrib[g] = __ldcg(a.spart + g);  // one coalesced pass
+          __syncthreads();
+          double sum = 0.0;
+          if (tid < a.nc)
+            for (int g = __ldg(a.cseg + tid); g < __ldg(a.cseg + tid + 1); ++g) sum += contrib[g];
+          gemv_narrow(q, nr, sum, red, vv);
+        } else {
+          for (int g = tid; g < a.n_segments; g += kT) contrib[g] = __ldcg(a.spart + g);
+          __syncthreads();
+          double sv[kMaxQ];
+#pragma unroll
+          for (int q = 0; q < kMaxQ; ++q) {
+            const int c = tid + q * kT;
+            double sum = 0.0;
+            if (c < a.nc)
+              for (int g = __ldg(a.cseg + c); g < __ldg(a.cseg + c + 1); ++g) sum += contrib[g];
+            sv[q] = sum;
+          }
+          gemv_rows<true>(Mrows, nr, a.nc, sv, red, vv);
+        }
+      } else {
+        double rc[kMaxQ];
+#pragma unroll
+        for (int q = 0; q < kMaxQ; ++q) {
+          const int c = tid + q * kT;
+          rc[q] = c < n ? __ldcg(a.r + c) : 0.0;
+        }
+        gemv_rows<true>(Mrows, nr, n, rc, red, vv);
       }
       if (tid < nr) zs[tid] = omega * a.r[row0 + tid] + vv[tid];
     } else {
@@ -228,12 +350,19 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       const int use = min(mi, min(it, keep));
       if (use > 0) {
         const int lane = tid & 31, wid = tid >> 5;
-        for (int q = wid; q < use; q += kW) {
+        // nr <= 28 (n <= 4096 over >= 148 CTAs): one element per lane; the
+        // loads of a warp's (up to 4) directions are issued together
+        double y[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = wid + j * kW;
           const double* aph = a.ap_ring + (size_t)((it - use + q) % RING) * n;
-          double acc = 0.0;
-          for (int lr = lane; lr < nr; lr += 32) acc += zs[lr] * __ldcg(aph + row0 + lr);
-          acc = wsum(acc);
-          if (lane == 0) part(kGS + q) = acc;
+          y[j] = (q < use && lane < nr) ? zs[lane] * __ldcg(aph + row0 + lane) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double acc = wsum(y[j]);
+          if (lane == 0 && wid + j * kW < use) part(kGS + wid + j * kW) = acc;
         }
         tmark(a, it, 2);
         grid.sync();  // B1
@@ -308,14 +437,15 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
     }
     const double alpha = a.fcg ? pr / pap : rz / pap;
     if (blockIdx.x == 0 && tid == 0) a.pap_ring[slot] = pap;
-    double rr = 0.0;
+    double rr = 0.0, ri = 0.0;
     if (tid < nr) {
       const int i = row0 + tid;
       a.x[i] += alpha * zs[tid];
-      const double ri = a.r[i] - alpha * vv[tid];
+      ri = a.r[i] - alpha * vv[tid];
       a.r[i] = ri;
       rr = ri * ri;
     }
+    if (a.lowrank && tid < 32) segment_partials(a, seg, ri);
     rr = bsum_all(rr, sh);
     if (tid == 0) part(kRR) = rr;
     tmark(a, it, 11);
@@ -336,6 +466,8 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       rz = rrs;
     }
   }
+  if (a.x_out != a.x)  // solution back to the original order
+    for (int i = row0 + tid; i < row1; i += kT) a.x_out[orig(i)] = a.x[i];
   if (blockIdx.x == 0 && tid == 0) {
     sc->it = it;
     sc->status = status;
@@ -364,12 +496,17 @@ DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
   if (const char* e = std::getenv("RMG_DENSE_SMEM")) p.smem_a = p.smem_a && e[0] != '0';
   p.smem_bytes = p.smem_a ? with_a : extra;
   p.partial_stride = kPS * ((p.grid + 31) / 32 * 32) / std::max(1, p.grid);
+  p.max_clusters = p.rows_per_cta * kMaxUse;
   return p;
 }
 
 void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& args, cudaStream_t s) {
   if (args.n > kMaxQ * kT) throw std::runtime_error("dense inner solver: level above 4096 unknowns");
   if (args.keep + 1 > kMaxUse) throw std::runtime_error("dense inner solver: truncation above 31");
+  if (args.lowrank && args.n_segments > plan.max_clusters)
+    throw std::runtime_error("dense inner solver: more cluster segments than shared scratch");
+  if (plan.rows_per_cta > 32 || plan.grid > 256)  // one GS element per lane; grid_sums unroll
+    throw std::runtime_error("dense inner solver: too few SMs for this level");
   void* fn = plan.smem_a ? (void*)k_dense_krylov<true> : (void*)k_dense_krylov<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
   if (e != cudaSuccess) throw std::runtime_error(std::string("dense inner solver attribute: ") + cudaGetErrorString(e));

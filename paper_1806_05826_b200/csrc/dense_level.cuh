@@ -14,9 +14,21 @@ struct DenseKrylovArgs {
   int keep = 20, max_iters = 500;
   double tol = 1e-6, omega = 0.0;
   const double* A = nullptr;   // n x n row-major, A = X_k^T X_k + beta_k I
-  const double* M = nullptr;   // n x n row-major, (I - omega A) P A_{k+1}^{-1} P^T
-  const double* b = nullptr;   // rhs
-  double* x = nullptr;
+  const double* M = nullptr;   // dense: n x n row-major, (I - omega A) P A_{k+1}^{-1} P^T
+  // low-rank FCG preconditioner (lowrank = 1): M r = Q (P^T r) with M = Q (n x nc,
+  // row-major); unknowns held in next-level-cluster order (perm[i] = original
+  // index of position i) so P^T r is a sum of per-CTA segment partials.
+  int lowrank = 0;
+  const int32_t* perm = nullptr;
+  const int32_t* cid = nullptr;       // [n] cluster of position i (nondecreasing)
+  const double* wts = nullptr;        // [n] aggregation weight of position i
+  const int32_t* cta_seg0 = nullptr;  // [grid] first segment of each CTA
+  const int32_t* cseg = nullptr;      // [nc + 1] segments of cluster c: [cseg[c], cseg[c+1])
+  double* spart = nullptr;            // [n_segments] partial sums of w r
+  int n_segments = 0;
+  const double* b = nullptr;   // rhs (original order)
+  double* x = nullptr;         // solution (solver order)
+  double* x_out = nullptr;     // solution in the original order (== x when perm == nullptr)
   double* r = nullptr;
   double* p_ring = nullptr;
   double* ap_ring = nullptr;
@@ -34,6 +46,7 @@ struct DenseKrylovPlan {
   int grid = 1, rows_per_cta = 1, partial_stride = 40;
   bool smem_a = false;
   size_t smem_bytes = 0;
+  int max_clusters = 0;  // low-rank preconditioner: cluster segments the shared scratch holds
 };
 
 DenseKrylovPlan plan_dense_krylov(int n, int nc, int device);

@@ -787,13 +787,15 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
         pads_.back().alloc(static_cast<size_t>(std::atoll(e)));
       }
     };
+    d->nc = fcg ? static_cast<int>(coarse_[k]->agg.n_coarse) : 0;
+    d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
+    d->lowrank = fcg && d->nc <= d->plan.max_clusters && std::getenv("RMG_DENSE_FULL_M") == nullptr;
     padk("RMG_PAD_A");
-    d->A.upload(a.data(), a.size(), s);
-    padk("RMG_PAD_Q");
-    if (fcg) {  // Q = (I - omega A_k) P A_{k+1}^{-1}
+    if (!fcg) {
+      d->A.upload(a.data(), a.size(), s);
+    } else {  // Q = (I - omega A_k) P A_{k+1}^{-1}
       const Aggregation& agg = coarse_[k]->agg;
       const int64_t nc = agg.n_coarse;
-      d->nc = static_cast<int>(nc);
       std::vector<double> g(static_cast<size_t>(n) * nc), q(static_cast<size_t>(n) * nc);
       for (int64_t i = 0; i < n; ++i)
         for (int64_t c = 0; c < nc; ++c) g[i * nc + c] = agg.weight[i] * ainv_host[agg.label[i] * nc + c];
@@ -816,13 +818,59 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
         });
       }
       for (auto& th : pool) th.join();
-      // M = Q P^T: M[i][j] = Q[i][label_j] w_j
-      std::vector<double> mm(static_cast<size_t>(n) * n);
-      for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = 0; j < n; ++j) mm[i * n + j] = q[i * nc + agg.label[j]] * agg.weight[j];
-      d->Q.upload(mm.data(), mm.size(), s);
+      if (d->lowrank) {
+        // positions in cluster order; A and Q rows follow; segments of (CTA, cluster)
+        std::vector<int32_t> perm(n);
+        std::iota(perm.begin(), perm.end(), 0);
+        std::stable_sort(perm.begin(), perm.end(),
+                         [&](int32_t i, int32_t j) { return agg.label[i] < agg.label[j]; });
+        std::vector<int32_t> cid(n);
+        std::vector<double> wts(n), ap(static_cast<size_t>(n) * n), qp(static_cast<size_t>(n) * nc);
+        for (int64_t i = 0; i < n; ++i) {
+          cid[i] = static_cast<int32_t>(agg.label[perm[i]]);
+          wts[i] = agg.weight[perm[i]];
+          const size_t pi = static_cast<size_t>(perm[i]);
+          for (int64_t j = 0; j < n; ++j) ap[i * n + j] = a[pi * n + perm[j]];
+          std::copy(&q[pi * nc], &q[pi * nc] + nc, &qp[i * nc]);
+        }
+        const int R = d->plan.rows_per_cta, grid = d->plan.grid;
+        std::vector<int32_t> cta_seg0(grid), cseg(nc + 1, -1);
+        int32_t segs = 0;
+        for (int b = 0; b < grid; ++b) {
+          cta_seg0[b] = segs;
+          for (int64_t i = static_cast<int64_t>(b) * R; i < std::min<int64_t>(n, (b + 1) * R); ++i) {
+            if (i == static_cast<int64_t>(b) * R || cid[i] != cid[i - 1]) {
+              if (cseg[cid[i]] < 0) cseg[cid[i]] = segs;
+              ++segs;
+            }
+          }
+        }
+        cseg[nc] = segs;
+        for (int64_t c = nc - 1; c >= 0; --c)  // empty clusters: empty range
+          if (cseg[c] < 0) cseg[c] = cseg[c + 1];
+        d->n_segments = segs;
+        d->lowrank = segs <= d->plan.max_clusters;  // else the dense M fallback below
+        if (d->lowrank) {
+          d->A.upload(ap.data(), ap.size(), s);
+          d->Q.upload(qp.data(), qp.size(), s);
+          d->perm.upload(perm.data(), perm.size(), s);
+          d->cid.upload(cid.data(), cid.size(), s);
+          d->wts.upload(wts.data(), wts.size(), s);
+          d->cta_seg0.upload(cta_seg0.data(), cta_seg0.size(), s);
+          d->cseg.upload(cseg.data(), cseg.size(), s);
+          d->spart.alloc(std::max<int32_t>(1, segs));
+          d->xp.alloc(std::max<int64_t>(1, n));
+        }
+      }
+      if (!d->lowrank) {  // dense M = Q P^T: M[i][j] = Q[i][label_j] w_j
+        d->A.upload(a.data(), a.size(), s);
+        padk("RMG_PAD_Q");
+        std::vector<double> mm(static_cast<size_t>(n) * n);
+        for (int64_t i = 0; i < n; ++i)
+          for (int64_t j = 0; j < n; ++j) mm[i * n + j] = q[i * nc + agg.label[j]] * agg.weight[j];
+        d->Q.upload(mm.data(), mm.size(), s);
+      }
     }
-    d->plan = plan_dense_krylov(static_cast<int>(n), d->nc, ctx_->device);
     padk("RMG_PAD_P");
     d->pap_ring.alloc(kMaxKeep + 2);
     // own 2 MB-granular allocation: the cross-CTA partials are read by every CTA
@@ -852,6 +900,18 @@ DenseKrylovArgs Method::dense_args(size_t k, const double* rhs) {
   a.M = d.Q.get();
   a.b = rhs;
   a.x = w.x.get();
+  a.x_out = w.x.get();
+  if (d.lowrank) {
+    a.lowrank = 1;
+    a.n_segments = d.n_segments;
+    a.perm = d.perm.get();
+    a.cid = d.cid.get();
+    a.wts = d.wts.get();
+    a.cta_seg0 = d.cta_seg0.get();
+    a.cseg = d.cseg.get();
+    a.spart = d.spart.get();
+    a.x = d.xp.get();
+  }
   a.r = w.r.get();
   a.p_ring = w.p_ring.get();
   a.ap_ring = w.ap_ring.get();

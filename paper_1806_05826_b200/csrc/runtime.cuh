@@ -205,6 +205,11 @@ struct DenseInner {
   int nc = 0;
   DBuf<double> A, Q, pap_ring, partials, cg_shared;
   DBuf<unsigned long long> timing;  // RMG_DENSE_TIMING diagnostics
+  // low-rank preconditioner (dense_level.cu): unknowns in next-level cluster order
+  bool lowrank = false;
+  int n_segments = 0;
+  DBuf<int32_t> perm, cid, cta_seg0, cseg;
+  DBuf<double> wts, spart, xp;
   std::vector<float> tuned_ms;      // partials placement candidates (ms per 40 iterations)
   int tuned_pick = 0;
 };
