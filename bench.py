@@ -413,7 +413,7 @@ def run_b200(args, cfg):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_apply")
+            traffic = json.load(open(tpath)).get(args.config, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
