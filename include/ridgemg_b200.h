@@ -127,6 +127,11 @@ int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n_samples, uint64_t n_featu
 int rmg_matrix_destroy(rmg_matrix* m);
 int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n_samples, uint64_t* n_features,
                      uint64_t* nnz, int32_t* is_pattern);
+/* Diagnostics (no reference counterpart): layout of the hybrid X^T pass --
+ * hot features summed per sample block from SMEM; zeros when
+ * the matrix uses the plain segmented pass. */
+int rmg_matrix_hot_layout(const rmg_matrix* m, uint64_t* hot_features, uint64_t* sample_blocks,
+                          uint64_t* block_samples);
 
 /* y = X v            (sparse.hpp:61, sparse.cpp:127-144)   */
 int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "rmg_matrix_create_csr": [_P, _U64, _U64, _P, _P, _P, _I32, _PP],
     "rmg_matrix_destroy": [_P],
     "rmg_matrix_shape": [_P, _P, _P, _P, _P],
+    "rmg_matrix_hot_layout": [_P, _P, _P, _P],
     "rmg_spmv": [_P, _P, _P, _I32],
     "rmg_spmv_transpose": [_P, _P, _P, _I32],
     "rmg_ridge_apply": [_P, _D, _P, _P, _I32],

@@ -241,6 +241,17 @@ int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n, uint64_t* f, uint64_t* nn
   });
 }
 
+int rmg_matrix_hot_layout(const rmg_matrix* m, uint64_t* hot_features, uint64_t* sample_blocks,
+                          uint64_t* block_samples) {
+  return guard([&] {
+    need(m, "matrix");
+    const bool on = m->m.hot != nullptr;
+    if (hot_features) *hot_features = on ? static_cast<uint64_t>(m->m.hot->view.H) : 0;
+    if (sample_blocks) *sample_blocks = on ? static_cast<uint64_t>(m->m.hot->view.nblk) : 0;
+    if (block_samples) *block_samples = on ? static_cast<uint64_t>(m->m.hot->view.B) : 0;
+  });
+}
+
 int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");

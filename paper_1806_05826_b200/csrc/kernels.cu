@@ -231,6 +231,91 @@ __global__ void __launch_bounds__(NT) k_spmv_rows(const int32_t* __restrict__ pt
   }
 }
 
+// ------------------------------------------------------------------ K2 hot part (hybrid X^T pass)
+constexpr int kHotThreads = 1024;  // 2 CTAs x 32 warps per SM: latency hiding for SMEM gathers
+// One CTA per sample block b: t[b*B, b*B + B) is staged in SMEM (coalesced,
+// once), then every hot row (b, h) gathers from SMEM instead of moving a 32 B
+// L2 sector per nonzero.  Long rows (h < hA): a warp each; short rows: 8 lanes.
+template <bool PAT>
+__global__ void __launch_bounds__(kHotThreads) k_xt_hot(HotXtDev h, const double* __restrict__ t, const int32_t* done,
+                                                     const KrylovScalars* sc) {
+  if (done != nullptr && *done) return;
+  if (sc != nullptr && sc->done) return;
+  extern __shared__ double ts[];
+  const int b = blockIdx.x;
+  const int64_t s0 = (int64_t)b * h.B;
+  const int nb = (int)(h.N - s0 < (int64_t)h.B ? h.N - s0 : (int64_t)h.B);
+  for (int j = threadIdx.x; j < nb; j += kHotThreads) ts[j] = __ldcg(t + s0 + j);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t* __restrict__ p = h.ptr + (size_t)b * h.H;
+  double* __restrict__ out = h.partial + (size_t)b * h.H;
+  for (int r = wid; r < h.hA; r += kHotThreads / 32) {  // long rows: warp per row, 4 loads in flight per lane
+    const int k0 = p[r], k1 = p[r + 1];
+    double acc = 0.0;
+    for (int k = k0 + lane; k < k1; k += 128) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = k + 32 * u < k1 ? ld_stream(h.idx16 + k + 32 * u) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) acc += PAT ? ts[c[u]] : ld_stream(h.val + k + 32 * u) * ts[c[u]];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) out[r] = acc;
+  }
+  // short rows: 8 rows per warp, 4 lanes each, 4 index loads in flight per lane;
+  // the next round's row bounds are loaded while the current round runs
+  constexpr int G = 4, RPW = 32 / G, NW = kHotThreads / 32;
+  const int gl = lane & (G - 1), gw = lane / G;
+  const int step = NW * RPW;
+  int r = h.hA + wid * RPW + gw;
+  int nk0 = r < h.H ? p[r] : 0, nk1 = r < h.H ? p[r + 1] : 0;
+  for (int r0 = h.hA + wid * RPW; r0 < h.H; r0 += step) {  // warp-uniform trip count
+    const int k0 = nk0, k1 = nk1, rr = r;
+    r += step;
+    nk0 = r < h.H ? p[r] : 0;
+    nk1 = r < h.H ? p[r + 1] : 0;
+    double acc = 0.0;
+    for (int k = k0 + gl; k < k1; k += 4 * G) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = k + u * G < k1 ? ld_stream(h.idx16 + k + u * G) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) acc += PAT ? ts[c[u]] : ld_stream(h.val + k + u * G) * ts[c[u]];
+    }
+    acc = group_sum<G>(acc);
+    if (gl == 0 && rr < h.H) out[rr] = acc;
+  }
+}
+
+// Cross-block sums of the hot rows, fixed order: stage 1 sums chunk s of the
+// blocks for each h (coalesced over h), stage 2 adds the S chunk sums in order.
+__global__ void __launch_bounds__(kThreads) k_xt_hot_chunks(HotXtDev h, const int32_t* done, const KrylovScalars* sc) {
+  if (done != nullptr && *done) return;
+  if (sc != nullptr && sc->done) return;
+  const int r = blockIdx.x * kThreads + threadIdx.x;
+  if (r >= h.H) return;
+  const int per = (h.nblk + h.S - 1) / h.S;
+  const int b0 = blockIdx.y * per, b1 = min(h.nblk, b0 + per);
+  double acc = 0.0;
+#pragma unroll 8
+  for (int b = b0; b < b1; ++b) acc += __ldcg(h.partial + (size_t)b * h.H + r);
+  h.red2[(size_t)blockIdx.y * h.H + r] = acc;
+}
+
+__global__ void __launch_bounds__(kThreads) k_xt_hot_final(HotXtDev h, double* sums, const int32_t* done,
+                                                           const KrylovScalars* sc) {
+  if (done != nullptr && *done) return;
+  if (sc != nullptr && sc->done) return;
+  const int r = blockIdx.x * kThreads + threadIdx.x;
+  if (r >= h.H) return;
+  double acc = 0.0;
+  for (int q = 0; q < h.S; ++q) acc += h.red2[(size_t)q * h.H + r];
+  sums[h.feat[r]] = acc;
+}
+
 // ------------------------------------------------------------------ K2: X^T pass + epilogue
 template <Epi E>
 __device__ __forceinline__ void xt_epilogue(int col, double s, const XtArgs& a, const double* v,
@@ -773,6 +858,15 @@ void prefer_l1(K kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
 }
 
+template <typename K>
+void allow_smem(K kern, int bytes) {  // once per kernel
+  static std::mutex mu;
+  static std::unordered_set<const void*> set;
+  std::lock_guard<std::mutex> lock(mu);
+  if (set.insert(reinterpret_cast<const void*>(kern)).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 int grid_for(int64_t work_threads, int cap) {
   const int64_t g = (work_threads + kThreads - 1) / kThreads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
@@ -906,6 +1000,22 @@ void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtA
     case Epi::Gram: k_xt_finish<Epi::Gram><<<fg, block, 0, s>>>(sch, a); break;
   }
   check_launch("xt_epilogue");
+}
+
+void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
+                   cudaStream_t s) {
+  if (h.H == 0) return;
+  const size_t smem = static_cast<size_t>(h.B) * sizeof(double);
+  if (h.val == nullptr) {
+    allow_smem(k_xt_hot<true>, kHotBlockMax * 8);
+    k_xt_hot<true><<<h.nblk, kHotThreads, smem, s>>>(h, t, done, sc);
+  } else {
+    allow_smem(k_xt_hot<false>, kHotBlockMax * 8);
+    k_xt_hot<false><<<h.nblk, kHotThreads, smem, s>>>(h, t, done, sc);
+  }
+  k_xt_hot_chunks<<<dim3((h.H + kThreads - 1) / kThreads, h.S), kThreads, 0, s>>>(h, done, sc);
+  k_xt_hot_final<<<(h.H + kThreads - 1) / kThreads, kThreads, 0, s>>>(h, sums, done, sc);
+  check_launch("xt_hot");
 }
 
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {

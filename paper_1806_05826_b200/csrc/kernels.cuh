@@ -113,6 +113,21 @@ struct XtArgs {
   int ring_stride = 0;         // Fcg/Cg: v/out are ring bases, offset by (it % (keep+1)) * stride
 };
 
+// Hybrid X^T pass: the hot features (dense enough that a
+// sample block holds several of their nonzeros) are summed per sample block
+// from an SMEM copy of the block's slice of t; the rest uses the segmented K2.
+constexpr int kHotBlockMax = 13824;  // samples per block: 108 KB of t in SMEM, 2 CTAs per SM
+struct HotXtDev {
+  const int32_t* ptr = nullptr;     // [nblk * H + 1], row (b, h) = b * H + h
+  const uint16_t* idx16 = nullptr;  // sample offset inside block b
+  const double* val = nullptr;      // nullptr: binary pattern
+  const int32_t* feat = nullptr;    // [H] feature of hot row h
+  double* partial = nullptr;        // [nblk * H]
+  double* red2 = nullptr;           // [S * H]
+  int H = 0, hA = 0, nblk = 0, B = 0, S = 1;
+  int64_t N = 0;
+};
+
 // ---------------------------------------------------------------- launchers
 void launch_spmv_rows(const SparseDev& x, const double* v, double* t, const int32_t* done,
                       cudaStream_t s);
@@ -120,6 +135,9 @@ void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_st
                            const KrylovScalars* sc, double* t, cudaStream_t s);
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a,
                cudaStream_t s);
+// hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
+void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
+                   cudaStream_t s);
 // Epilogue (+ deterministic dots) over precomputed sums s_j = (X^T t)_j, e.g.
 // after an all-reduce of per-rank partial sums (row-sharded operator).
 void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtArgs& a, double* fin_slots,

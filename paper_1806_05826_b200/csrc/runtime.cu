@@ -204,7 +204,8 @@ void DeviceSparse::upload_sell(const HostCsr& h, bool pattern, cudaStream_t s, b
 // by length class: short rows (<= 8 per lane of a W-lane group), medium rows
 // (one warp, <= 2048), long rows (fixed CTA segments).  Each CTA item holds
 // about C nonzeros, so no lane group owns a row much longer than its peers'.
-void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows) {
+void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows,
+                           const std::vector<char>* skip) {
   const int64_t V = xt.n, nnz = xt.nnz();
   // ~12 items per SM: the first schedule (4 per SM) ran 0.61 waves at 29 % occupancy
   const int64_t C = std::max<int64_t>(512, std::min<int64_t>(16384, nnz / (148 * 12)));
@@ -213,7 +214,7 @@ void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, 
   lens.reserve(V);
   for (int64_t j = 0; j < V; ++j) {
     const int64_t len = xt.ptr[j + 1] - xt.ptr[j];
-    if (len > 0 && len <= 2048) lens.push_back(len);
+    if (len > 0 && len <= 2048 && !(skip && (*skip)[j])) lens.push_back(len);
   }
   int width = 8;
   if (!lens.empty()) {
@@ -227,6 +228,7 @@ void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, 
   std::vector<int32_t> lcol, lfirst, lnseg, lslot;
   int slot = 0, segs = 0;
   for (int64_t j = 0; j < V; ++j) {
+    if (skip && (*skip)[j]) continue;
     const int64_t len = xt.ptr[j + 1] - xt.ptr[j];
     if (len <= short_max) {
       perm_short.push_back(static_cast<int32_t>(j));
@@ -392,6 +394,99 @@ void Matrix::allreduce_sums(double* sendbuf, double* recvbuf, int64_t count) {
   if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
 }
 
+// Hybrid X^T pass.  Sample blocks: a multiple of 2 x 148
+// blocks of <= kHotBlockMax samples (two 108 KB t-slices per SM).  Hot features:
+// >= 4 nonzeros per block on average (the SMEM gathers then amortize the block
+// bookkeeping), most popular first, capped so the [block x hot] partials
+// (<= 64 MB) stay L2-resident.  Only when the samples span >= 296 blocks of
+// >= 4096 (smaller t-vectors are L2/L1-resident and gain nothing).
+void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
+  const char* env = std::getenv("RMG_XT_HOT");
+  const bool want = env != nullptr ? std::string(env) == "1" : n_samples >= 296LL * 4096;
+  if (!want || n_samples < 296) return;
+  const int64_t F = ht.n;
+  const int64_t unit = 296;
+  const int64_t nblk = unit * ((n_samples + unit * kHotBlockMax - 1) / (unit * kHotBlockMax));
+  const int64_t B = (n_samples + nblk - 1) / nblk;
+  std::vector<int32_t> order(F);
+  std::iota(order.begin(), order.end(), 0);
+  auto cnt = [&](int64_t f) { return ht.ptr[f + 1] - ht.ptr[f]; };
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt(a) > cnt(b); });
+  const int64_t cap = std::max<int64_t>(0, (96LL << 20) / (8 * nblk));
+  const char* hm = std::getenv("RMG_HOT_MIN");  // hot: >= this many nonzeros per block (mean)
+  const int64_t min_per_block = hm != nullptr ? std::max(1, std::atoi(hm)) : 4;
+  int64_t H = 0, hA = 0;
+  while (H < F && H < cap && cnt(order[H]) >= min_per_block * nblk) ++H;
+  while (hA < H && cnt(order[hA]) >= 64 * nblk) ++hA;
+  if (H == 0) return;
+  auto hx = std::make_unique<HotXt>();
+  std::vector<int32_t> feat(order.begin(), order.begin() + H);
+  // (block, hot row) counts, prefix, fill -- threads over hot rows
+  std::vector<int64_t> rp(static_cast<size_t>(nblk * H + 1), 0);
+  const int64_t T = std::max<int64_t>(1, std::min<int64_t>(64, std::thread::hardware_concurrency()));
+  auto par = [&](auto fn) {
+    std::vector<std::thread> pool;
+    for (int64_t t = 0; t < T; ++t) pool.emplace_back([&, t] {
+      for (int64_t h = t; h < H; h += T) fn(h);
+    });
+    for (auto& th : pool) th.join();
+  };
+  par([&](int64_t h) {
+    for (int64_t k = ht.ptr[feat[h]]; k < ht.ptr[feat[h] + 1]; ++k) ++rp[(ht.idx[k] / B) * H + h + 1];
+  });
+  for (size_t q = 0; q + 1 < rp.size(); ++q) rp[q + 1] += rp[q];
+  const int64_t hnnz = rp.back();
+  if (hnnz > INT32_MAX) return;
+  std::vector<uint16_t> i16(hnnz);
+  std::vector<double> v(pattern ? 0 : hnnz);
+  par([&](int64_t h) {
+    int64_t cur_b = -1, pos = 0;
+    for (int64_t k = ht.ptr[feat[h]]; k < ht.ptr[feat[h] + 1]; ++k) {  // samples ascending
+      const int64_t b = ht.idx[k] / B;
+      if (b != cur_b) {
+        cur_b = b;
+        pos = rp[b * H + h];
+      }
+      i16[pos] = static_cast<uint16_t>(ht.idx[k] - b * B);
+      if (!pattern) v[pos] = ht.val[k];
+      ++pos;
+    }
+  });
+  std::vector<int32_t> rp32(rp.begin(), rp.end());
+  cudaStream_t s = ctx->stream;
+  hx->ptr.upload(rp32.data(), rp32.size(), s);
+  hx->idx16.upload(i16.data(), i16.size(), s);
+  if (!pattern) hx->val.upload(v.data(), v.size(), s);
+  hx->feat.upload(feat.data(), feat.size(), s);
+  hx->view.S = static_cast<int>(std::min<int64_t>(8, nblk));
+  hx->partial.alloc(static_cast<size_t>(nblk * H));
+  hx->red2.alloc(static_cast<size_t>(hx->view.S * H));
+  std::vector<char> skip(F, 0);
+  for (int64_t h = 0; h < H; ++h) skip[feat[h]] = 1;
+  hx->cold.build(ht, s, F, 1, 0, &skip);
+  RMG_CK(cudaStreamSynchronize(s));
+  HotXtDev& d = hx->view;
+  d.ptr = hx->ptr.get();
+  d.idx16 = hx->idx16.get();
+  d.val = pattern ? nullptr : hx->val.get();
+  d.feat = hx->feat.get();
+  d.partial = hx->partial.get();
+  d.red2 = hx->red2.get();
+  d.H = static_cast<int>(H);
+  d.hA = static_cast<int>(hA);
+  d.nblk = static_cast<int>(nblk);
+  d.B = static_cast<int>(B);
+  d.N = n_samples;
+  hot = std::move(hx);
+  if (part.size() == 0) {  // sums + finishing epilogue, as in the sharded pass
+    part.alloc(std::max<int64_t>(1, F));
+    fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (F + 255) / 256)));
+    fin_slots.alloc(static_cast<size_t>(fin_grid) * 2);
+    fin_ticket.alloc(1);
+    RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), s));
+  }
+}
+
 Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
   if (host.n > INT32_MAX || host.f > INT32_MAX || host.nnz() > INT32_MAX)
@@ -449,6 +544,7 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), h
   } else {
     xt.upload(ht, pattern, ctx->stream, false);
     sched.build(ht, ctx->stream, local.f, 1, 0);
+    build_hot(ht, local.n);
   }
   t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);
@@ -460,15 +556,26 @@ namespace {
 void xt_pass(Matrix& m, const double* t, Epi epi, const XtArgs& args) {
   XtArgs a = args;
   a.t = t;
-  if (m.comm == nullptr) {
+  if (m.comm == nullptr && !m.hot) {
     launch_xt(m.xt.view, m.sched.view, epi, a, m.ctx->stream);
     return;
   }
   XtArgs pa = a;
   pa.out = m.part.get();
-  launch_xt(m.xt.view, m.sched.view, Epi::Plain, pa, m.ctx->stream);
-  m.allreduce_sums(m.part.get(), m.red.get(), m.f());
-  launch_xt_epilogue(m.red.get(), m.f(), epi, a, m.fin_slots.get(), m.fin_ticket.get(), m.fin_grid, m.ctx->stream);
+  if (m.hot) {  // hybrid: cold rows (segmented) + hot rows (sample-blocked), sums only
+    launch_xt(m.xt.view, m.hot->cold.view, Epi::Plain, pa, m.ctx->stream);
+    const KrylovScalars* sc = (epi == Epi::Fcg || epi == Epi::Cg) ? a.sc : nullptr;
+    launch_xt_hot(m.hot->view, t, a.done, sc, m.part.get(), m.ctx->stream);
+    m.ctx->launches += 3;
+  } else {
+    launch_xt(m.xt.view, m.sched.view, Epi::Plain, pa, m.ctx->stream);
+  }
+  const double* sums = m.part.get();
+  if (m.comm != nullptr) {
+    m.allreduce_sums(m.part.get(), m.red.get(), m.f());
+    sums = m.red.get();
+  }
+  launch_xt_epilogue(sums, m.f(), epi, a, m.fin_slots.get(), m.fin_ticket.get(), m.fin_grid, m.ctx->stream);
   m.ctx->launches += 1;
 }
 }  // namespace
@@ -1206,7 +1313,10 @@ double Method::time_operator(size_t level, uint64_t reps, bool flush, double* k1
     RMG_CK(cudaEventRecord(e0, s));
     launch_spmv_rows(m.x.view, v.get(), m.t.get(), nullptr, s);
     RMG_CK(cudaEventRecord(e1, s));
-    launch_xt(m.xt.view, m.sched.view, Epi::Axpby, a, s);
+    if (m.comm != nullptr)  // no collective inside a single-rank timing loop
+      launch_xt(m.xt.view, m.sched.view, Epi::Axpby, a, s);
+    else
+      xt_pass(m, m.t.get(), Epi::Axpby, a);
     RMG_CK(cudaEventRecord(e2, s));
     RMG_CK(cudaEventSynchronize(e2));
     float a1 = 0.f, a2 = 0.f;

@@ -100,8 +100,10 @@ struct DeviceSchedule {
   DBuf<int32_t> perm, long_col, long_first, long_nseg, long_slot;
   DBuf<double> seg_partial, slots, partial, fin_slots;
   DBuf<unsigned> col_ticket, grid_ticket, fin_ticket;
-  // xt: (virtual) X^T CSR; features F; n_blocks > 1 selects the sample-blocked layout
-  void build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows);
+  // xt: (virtual) X^T CSR; features F; n_blocks > 1 selects the sample-blocked layout;
+  // skip: rows left out of the schedule (the hot rows of the hybrid pass)
+  void build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows,
+             const std::vector<char>* skip = nullptr);
 };
 
 HostCsr blocked_transpose(const HostCsr& xt, int64_t block_rows, int n_blocks);
@@ -138,6 +140,15 @@ std::vector<int64_t> partition_rows(const std::vector<int64_t>& row_offsets, int
 // the device and every X^T pass ends in an all-reduce of the F-vector
 // (north star: row sharding over NVLink); `host` keeps the full matrix for
 // the (replicated) hierarchy setup.
+// Hybrid X^T pass: sample-blocked hot features + segmented cold rest.
+struct HotXt {
+  HotXtDev view;
+  DBuf<int32_t> ptr, feat;
+  DBuf<uint16_t> idx16;
+  DBuf<double> val, partial, red2;
+  DeviceSchedule cold;  // segmented schedule over the cold rows only
+};
+
 struct Matrix {
   Context* ctx = nullptr;
   HostCsr host;  // canonical CSR kept for setup (clustering, coarsening)
@@ -151,7 +162,9 @@ struct Matrix {
   DBuf<double> part, red, fin_slots;
   DBuf<unsigned> fin_ticket;
   int fin_grid = 1;
+  std::unique_ptr<HotXt> hot;  // hybrid X^T pass when N is large (nullptr otherwise)
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr);
+  void build_hot(const HostCsr& ht, int64_t n_samples);
   int64_t n_local() const { return row1 - row0; }
   void allreduce_sums(double* sendbuf, double* recvbuf, int64_t count);
   int64_t n() const { return host.n; }

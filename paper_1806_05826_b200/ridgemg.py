@@ -292,6 +292,12 @@ class DeviceMatrix:
             raise ValueError(f"length {a.shape[0] if a.ndim else 0}, expected {n}")
         return a
 
+    def hybrid_hot_features(self) -> int:
+        """Hot features of the hybrid X^T pass (0: plain segmented pass)."""
+        h = C.c_uint64()
+        _lib.check(self.lib.rmg_matrix_hot_layout(self.h, C.byref(h), None, None))
+        return int(h.value)
+
     def spmv(self, v) -> np.ndarray:
         v = self._vec(v, self.n_features)
         y = np.zeros(self.n_samples)

@@ -31,3 +31,10 @@ if name == "cfg2":
     t_got, t_want = m.spmv(w), o.spmv(om, w)
     print("K1 bit-exact vs oracle:", bool(np.array_equal(t_got, t_want)),
           "max abs diff", float(np.max(np.abs(t_got - t_want))))
+if name != "cfg2":
+    print("hybrid hot features:", m.hybrid_hot_features(), flush=True)
+    u = np.random.default_rng(1).standard_normal(x.n_samples)
+    got = m.spmv_transpose(u)
+    rows = np.repeat(np.arange(x.n_samples), np.diff(x.row_offsets.astype(np.int64)))
+    want = np.bincount(x.column_indices.astype(np.int64), weights=u[rows], minlength=x.n_features)
+    print("X^T u vs numpy: rel", np.linalg.norm(got - want) / np.linalg.norm(want))
