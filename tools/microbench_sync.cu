@@ -1,5 +1,5 @@
 // Microbenchmark: cost of grid-wide synchronization primitives on B200
-// (148 CTAs x 1024 threads, cooperative launch), to size the persistent
+// (148 / 143 CTAs x 256 threads, cooperative launch), to size the persistent
 // inner solver (dense_level.cu).  Build + run:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench_sync.cu && /tmp/mb
 #include <cooperative_groups.h>
@@ -13,12 +13,33 @@ __device__ __forceinline__ double wsum(double v) {
 
 // mode 0: grid.sync only; 1: grid.sync + one all-block reduction (like all_blocks)
 // mode 2: custom flag barrier (atomic arrive + spin on generation)
-__global__ void __launch_bounds__(1024, 1) k(int iters, int mode, double* part, unsigned* bar, double* out) {
+// mode 3: monotonic counter: red.release.gpu arrive, ld.acquire.gpu poll until
+//         (it + 1) * gridDim.x (no reset, no generation word)
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, unsigned* bar, double* out) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[33];
   double acc = 0.0;
   for (int it = 0; it < iters; ++it) {
-    if (mode == 2) {
+    if (mode == 3) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned target = (unsigned)(it + 1) * gridDim.x;
+        red_release_add(bar + 2, 1u);
+        while (ld_acquire(bar + 2) < target) {
+        }
+      }
+      __syncthreads();
+    } else if (mode == 2) {
       __syncthreads();
       if (threadIdx.x == 0) {
         volatile unsigned* gen = bar + 1;
@@ -62,20 +83,22 @@ int main() {
   unsigned* bar;
   cudaMalloc(&part, 4096 * 8);
   cudaMalloc(&out, 8);
-  cudaMalloc(&bar, 8);
-  cudaMemset(bar, 0, 8);
+  cudaMalloc(&bar, 16);
+  cudaMemset(bar, 0, 16);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 3; ++mode) {
-    for (int grid : {sms, 74, 32, 8}) {
+  for (int mode = 0; mode < 4; ++mode) {
+    for (int grid : {sms, 143, 74}) {
       int iters = 2000;
       void* args[] = {&iters, &mode, &part, &bar, &out};
-      cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(1024), args, 0, 0);
+      cudaMemset(bar, 0, 16);
+      cudaLaunchCooperativeKernel((void*)k<256>, dim3(grid), dim3(256), args, 0, 0);
+      cudaMemset(bar, 0, 16);
       cudaEventRecord(a);
-      cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(1024), args, 0, 0);
+      cudaLaunchCooperativeKernel((void*)k<256>, dim3(grid), dim3(256), args, 0, 0);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
