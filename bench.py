@@ -223,6 +223,54 @@ def run_reference_arm(args, cfg):
 
 
 # ---------------------------------------------------------------- B200 arm
+def dense_algorithmic_bytes(n, f, elem_bytes, sweeps=1):
+    """SURVEY.md §8(d), dense: B = S·N·F·s_val + 8(F + 2N + 2F); the dense path
+    is one fused sweep (S = 1)."""
+    return sweeps * n * f * elem_bytes + 8 * (f + 2 * n + 2 * f)
+
+
+def cfg4_shard_matrix(n=500_000, f=1024, seed=0):
+    """BASELINE cfg 4's per-GPU shard at 8 GPUs (500k of its 4M rows), fp32
+    storage: X = U diag(i^-1.5) V^T + 1e-3 N(0,1), V orthonormal (QR of a seeded
+    Gaussian), U = a seeded Gaussian / sqrt(4M) (columns orthonormal to O(1/sqrt(N)),
+    standing in for the rank-1024 orthonormal U of the full 4M rows).  Generated
+    on the GPU with torch (plumbing), returned as a host float32 array."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    v, _ = torch.linalg.qr(torch.randn(f, f, generator=g, device="cuda", dtype=torch.float64))
+    sig = torch.arange(1, f + 1, device="cuda", dtype=torch.float64) ** -1.5
+    w = (sig[:, None] * v.T).to(torch.float32)  # diag(sigma) V^T
+    out = torch.empty(n, f, dtype=torch.float32, device="cuda")
+    step = 65536
+    for r in range(0, n, step):
+        e = min(n, r + step)
+        u = torch.randn(e - r, f, generator=g, device="cuda", dtype=torch.float32) / (4_000_000 ** 0.5)
+        out[r:e] = u @ w + 1e-3 * torch.randn(e - r, f, generator=g, device="cuda", dtype=torch.float32)
+    return out.cpu().numpy()
+
+
+def dense_operator_roofline(peak):
+    """The dense path's operator on cfg 4's per-GPU shard at 8
+    GPUs: one fused sweep over 2 GB of fp32 X per apply, L2 flushed before each."""
+    import paper_1806_05826_b200 as R
+    t0 = time.time()
+    a = cfg4_shard_matrix()
+    m = R.DeviceMatrix.from_dense(a)
+    pm = R.PreparedMethod(m, 1e-4, R.MethodSpec(kind=R.CG))
+    setup = time.time() - t0
+    cold = pm.time_operator(0, 10, True)
+    warm = pm.time_operator(0, 10, False)
+    fb = dense_algorithmic_bytes(a.shape[0], a.shape[1], 4)
+    out = {"workload": "cfg4 per-GPU shard at 8 GPUs: N=500,000 x F=1024 dense, fp32 storage / fp64 arithmetic, "
+                       "X = U diag(i^-1.5) V^T + 1e-3 N(0,1), beta=1e-4",
+           "bound": "hbm", "kernel": "k_dense_ata (fused X^T X single sweep) + k_dense_finish",
+           "algorithmic_bytes_per_apply": fb, "ms_per_apply": cold[0], "achieved": fb / (cold[0] * 1e6),
+           "peak": peak, "unit": "GB/s", "frac": fb / (cold[0] * 1e6) / peak, "warm_ms": warm[0],
+           "setup_s": setup}
+    del pm, m, a
+    return out
+
+
 def shard_operator_roofline(peak):
     """The metric's HBM-bound operator figure: BASELINE cfg 5 (16M x 500k binary,
     Poisson(64) nnz/row, Zipf(1.05)) is row-sharded; one GPU's shard at 4 GPUs
@@ -402,12 +450,16 @@ def run_b200(args, cfg):
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
-    large_op = None
+    large_op = dense_op = None
     if rank == 0 and not args.no_large_operator:
         try:
             large_op = shard_operator_roofline(peak)
         except Exception as e:  # reported, never fatal
             large_op = {"failed": str(e)}
+        try:
+            dense_op = dense_operator_roofline(peak)
+        except Exception as e:
+            dense_op = {"failed": str(e)}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -449,6 +501,7 @@ def run_b200(args, cfg):
                                   "cold_k2_ms": cold[2], "in_situ_ms_per_apply":
                                       (prof[0]["ms_k1"] + prof[0]["ms_k2"]) / max(1, prof[0]["applications"])},
             "operator_roofline_cfg5_shard": large_op,
+            "operator_roofline_cfg4_shard": dense_op,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
                     "d2h_bytes_per_step": x.n_features * 8},

@@ -125,6 +125,15 @@ int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n_samples, uint64_t n_featu
                           const uint64_t* row_offsets, const uint64_t* column_indices,
                           const double* values, int32_t detect_pattern, rmg_matrix** out);
 int rmg_matrix_destroy(rmg_matrix* m);
+/* Dense X (north-star (1): row-major dense for dense inputs; no reference
+ * counterpart -- the reference stores every input as FeatureMatrix CSR, which a
+ * dense array becomes via csr_from_triplets, sparse.hpp:55-56).  data: host,
+ * row-major n x f with leading dimension ld elements, fp64 (fp32 = 0) or fp32
+ * storage (fp32 = 1; arithmetic stays fp64).  f <= 1024.  The operator is one
+ * fused sweep over X; setup sees the same values as CSR. */
+int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n_samples, uint64_t n_features, const void* data,
+                            uint64_t ld, int32_t fp32, rmg_matrix** out);
+int rmg_matrix_is_dense(const rmg_matrix* m, int32_t* dense, int32_t* fp32);
 int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n_samples, uint64_t* n_features,
                      uint64_t* nnz, int32_t* is_pattern);
 /* Diagnostics (no reference counterpart): layout of the hybrid X^T pass --
@@ -156,6 +165,10 @@ typedef struct rmg_comm rmg_comm;
 #define RMG_UNIQUE_ID_BYTES 128
 int rmg_comm_unique_id(uint8_t* id_out);
 int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id, rmg_comm** out);
+/* Dense X row-sharded over the communicator (north-star (e), cfg 4): each rank
+ * keeps its nnz-balanced (= row-balanced) block; see rmg_matrix_create_dense. */
+int rmg_matrix_create_dense_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t n_features,
+                                    const void* data, uint64_t ld, int32_t fp32, rmg_matrix** out);
 int rmg_comm_destroy(rmg_comm* comm);
 /* Every rank passes the FULL matrix (needed for the replicated hierarchy setup);
  * only this rank's row block is uploaded. */

@@ -74,6 +74,9 @@ SIGNATURES = {
     "rmg_matrix_destroy": [_P],
     "rmg_matrix_shape": [_P, _P, _P, _P, _P],
     "rmg_matrix_hot_layout": [_P, _P, _P, _P],
+    "rmg_matrix_create_dense": [_P, _U64, _U64, _P, _U64, _I32, _PP],
+    "rmg_matrix_create_dense_sharded": [_P, _P, _U64, _U64, _P, _U64, _I32, _PP],
+    "rmg_matrix_is_dense": [_P, _P, _P],
     "rmg_spmv": [_P, _P, _P, _I32],
     "rmg_spmv_transpose": [_P, _P, _P, _I32],
     "rmg_ridge_apply": [_P, _D, _P, _P, _I32],

@@ -6,6 +6,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
 
 #include "ridgemg_b200.h"
 #include "runtime.cuh"
@@ -16,8 +17,9 @@ struct rmg_context {
 };
 struct rmg_matrix {
   rmg::Matrix m;
-  rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect, rmg::Comm* comm = nullptr)
-      : m(ctx, std::move(h), detect, comm) {}
+  rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect, rmg::Comm* comm = nullptr,
+             const rmg::DenseInput* din = nullptr)
+      : m(ctx, std::move(h), detect, comm, din) {}
 };
 struct rmg_host_csr {
   rmg::HostCsr h;
@@ -161,6 +163,83 @@ int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n, uint64_t f, const uint64
   });
 }
 
+namespace {
+// Host CSR view of a dense row-major array (setup: clustering, coarsening);
+// exact zeros are not stored, fp32 values widen exactly.
+rmg::HostCsr dense_to_csr(uint64_t n, uint64_t f, const void* data, uint64_t ld, int32_t fp32) {
+  if (ld < f) throw rmg::InvalidArgument("dense X: leading dimension below the feature count");
+  auto at = [&](uint64_t i, uint64_t j) {
+    return fp32 ? static_cast<double>(static_cast<const float*>(data)[i * ld + j])
+                : static_cast<const double*>(data)[i * ld + j];
+  };
+  rmg::HostCsr h;
+  h.n = static_cast<int64_t>(n);
+  h.f = static_cast<int64_t>(f);
+  h.ptr.assign(n + 1, 0);
+  const uint64_t T = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  auto par = [&](auto fn) {  // contiguous row ranges per thread
+    std::vector<std::thread> pool;
+    for (uint64_t t = 0; t < T; ++t)
+      pool.emplace_back([&, t] { fn(n * t / T, n * (t + 1) / T); });
+    for (auto& th : pool) th.join();
+  };
+  par([&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      int64_t c = 0;
+      for (uint64_t j = 0; j < f; ++j) c += at(i, j) != 0.0;
+      h.ptr[i + 1] = c;
+    }
+  });
+  for (uint64_t i = 0; i < n; ++i) h.ptr[i + 1] += h.ptr[i];
+  h.idx.resize(h.ptr[n]);
+  h.val.resize(h.ptr[n]);
+  par([&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      int64_t q = h.ptr[i];
+      for (uint64_t j = 0; j < f; ++j) {
+        const double v = at(i, j);
+        if (v != 0.0) {
+          h.idx[q] = static_cast<int64_t>(j);
+          h.val[q++] = v;
+        }
+      }
+    }
+  });
+  return h;
+}
+}  // namespace
+
+int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n, uint64_t f, const void* data, uint64_t ld, int32_t fp32,
+                            rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (n * f) need(data, "data");
+    rmg::DenseInput din;
+    din.data = data;
+    din.fp32 = fp32 != 0;
+    din.ld = static_cast<int64_t>(ld);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, dense_to_csr(n, f, data, ld, fp32), false, nullptr, &din);
+  });
+}
+
+int rmg_matrix_create_dense_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n, uint64_t f, const void* data,
+                                    uint64_t ld, int32_t fp32, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(comm, "comm");
+    need(out, "out");
+    if (n * f) need(data, "data");
+    rmg::DenseInput din;
+    din.data = data;
+    din.fp32 = fp32 != 0;
+    din.ld = static_cast<int64_t>(ld);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, dense_to_csr(n, f, data, ld, fp32), false, &comm->c, &din);
+  });
+}
+
 int rmg_comm_unique_id(uint8_t* id_out) {
   return guard([&] {
     need(id_out, "id_out");
@@ -238,6 +317,14 @@ int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n, uint64_t* f, uint64_t* nn
     if (f) *f = m->m.f();
     if (nnz) *nnz = m->m.nnz();
     if (is_pattern) *is_pattern = m->m.pattern ? 1 : 0;
+  });
+}
+
+int rmg_matrix_is_dense(const rmg_matrix* m, int32_t* dense, int32_t* fp32) {
+  return guard([&] {
+    need(m, "matrix");
+    if (dense) *dense = m->m.dense ? 1 : 0;
+    if (fp32) *fp32 = m->m.dense ? m->m.dense->view.fp32 : 0;
   });
 }
 

@@ -553,6 +553,216 @@ __global__ void __launch_bounds__(kThreads) k_xt_finish(XtSchedule sch, XtArgs a
   }
 }
 
+// ------------------------------------------------------------------ dense X
+// One fused sweep: warp per row, lane l owns columns l + 32k.  MODE 0:
+// t = x.v (warp tree), acc += t x; MODE 1: t = u_i given (X^T u); MODE 2:
+// y_i = x.v only; MODE 3: acc += x^2 (Gram diagonal).  Warp partials are
+// combined in warp order per CTA and stored column-major [col][cta] for the
+// finishing kernel.  Row order per warp and every combine order are fixed.
+// TMA 1D bulk copies (no tensor map: a row tile is one contiguous range) into
+// a 3-stage SMEM ring, completion tracked by mbarriers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+constexpr int kDenseStages = 3;
+constexpr int kDenseTileBytes = 64 * 1024;
+
+// One fused sweep: the CTA streams tiles of consecutive rows (<= 64 KB) through
+// the SMEM ring; thread tid owns columns 4 tid .. 4 tid + 3 (v and the column
+// partials live in its registers).  MODE 0: t_r = x_r . v (thread products,
+// warp tree, then the kW warp sums in order), acc += t_r x_r; MODE 1: t_r =
+// u_r; MODE 2: y_r = t_r only; MODE 3: acc += x_r^2.  Rows are consumed in
+// increasing order per CTA; every combine order is fixed.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_dense_ata(DenseDev d, const double* v_in, const double* u, double* y,
+                                                           const int32_t* done, const KrylovScalars* sc,
+                                                           int ring_stride) {
+  if (done != nullptr && *done) return;
+  const double* v = v_in;
+  if (sc != nullptr) {
+    if (sc->done) return;
+    v += (size_t)ring_slot(sc) * ring_stride;
+  }
+  extern __shared__ __align__(128) unsigned char dsm_raw[];
+  __shared__ __align__(8) uint64_t bar[kDenseStages];
+  __shared__ double wdot[kWarps][16];
+  __shared__ double trow[16];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t row_bytes = d.ld * (int64_t)sizeof(T);
+  const int64_t tr_fit = kDenseTileBytes / row_bytes;
+  const int TR = (int)(tr_fit < 16 ? tr_fit : 16);  // rows per tile
+  const int64_t n_tiles = (d.rows + TR - 1) / TR;
+  const int c0 = 4 * tid;
+  const bool own = c0 < d.cols;
+  constexpr bool DOT = MODE == 0 || MODE == 2;
+  double vr[4] = {0.0, 0.0, 0.0, 0.0}, acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (DOT && own)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) vr[q] = c0 + q < d.cols ? __ldg(v + c0 + q) : 0.0;
+  const unsigned char* X = static_cast<const unsigned char*>(d.data);
+  auto tile_rows = [&](int64_t k) {
+    const int64_t left = d.rows - k * TR;
+    return (int)(left < TR ? left : TR);
+  };
+  auto issue = [&](int64_t k, int stage) {
+    tma_load_1d(dsm_raw + (size_t)stage * kDenseTileBytes, X + k * TR * row_bytes,
+                (uint32_t)(tile_rows(k) * row_bytes), &bar[stage]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kDenseStages; ++st) mbar_init(&bar[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t j = 0;  // local tile sequence
+  if (tid == 0)
+    for (int st = 0; st < kDenseStages; ++st) {
+      const int64_t k = blockIdx.x + (int64_t)st * gridDim.x;
+      if (k < n_tiles) issue(k, st);
+    }
+  for (int64_t k = blockIdx.x; k < n_tiles; k += gridDim.x, ++j) {
+    const int st = (int)(j % kDenseStages);
+    mbar_wait(&bar[st], (uint32_t)((j / kDenseStages) & 1));
+    const T* tile = reinterpret_cast<const T*>(dsm_raw + (size_t)st * kDenseTileBytes);
+    const int nr = tile_rows(k);
+    const int64_t r0 = k * TR;
+    // this thread's 4 columns of every tile row, vector loads (ld % 4 == 0, c0 % 4 == 0);
+    // columns past F are zero padding in the stored rows
+    double xs[16][4];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r < nr && own) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 q4 = *reinterpret_cast<const float4*>(tile + (size_t)r * d.ld + c0);
+          xs[r][0] = q4.x;
+          xs[r][1] = q4.y;
+          xs[r][2] = q4.z;
+          xs[r][3] = q4.w;
+        } else {
+          const double2 a2 = *reinterpret_cast<const double2*>(tile + (size_t)r * d.ld + c0);
+          const double2 b2 = *reinterpret_cast<const double2*>(tile + (size_t)r * d.ld + c0 + 2);
+          xs[r][0] = a2.x;
+          xs[r][1] = a2.y;
+          xs[r][2] = b2.x;
+          xs[r][3] = b2.y;
+        }
+      } else {
+        xs[r][0] = xs[r][1] = xs[r][2] = xs[r][3] = 0.0;
+      }
+    }
+    __syncthreads();  // every thread holds its slice of the tile: the stage is free
+    if (tid == 0 && k + (int64_t)kDenseStages * gridDim.x < n_tiles) issue(k + (int64_t)kDenseStages * gridDim.x, st);
+    if constexpr (DOT) {
+      double p[16];  // all 16 rows' warp trees interleave (rows past nr are zeros)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) p[r] = ((xs[r][0] * vr[0] + xs[r][1] * vr[1]) + xs[r][2] * vr[2]) + xs[r][3] * vr[3];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < 16; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
+      if (lane < 16) {
+        double mine = p[0];
+#pragma unroll
+        for (int r = 1; r < 16; ++r) mine = lane == r ? p[r] : mine;
+        wdot[wid][lane] = mine;
+      }
+      __syncthreads();
+      if (tid < nr) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) t += wdot[w][tid];
+        trow[tid] = t;
+        if (MODE == 2) y[r0 + tid] = t;
+      }
+      __syncthreads();
+    } else if constexpr (MODE == 1) {
+      if (tid < nr) trow[tid] = __ldg(u + r0 + tid);
+      __syncthreads();
+    }
+    if constexpr (MODE != 2) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {  // rows past nr hold zeros: adding them is exact
+        const double t = MODE == 3 ? 0.0 : (r < nr ? trow[r] : 0.0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += MODE == 3 ? xs[r][q] * xs[r][q] : t * xs[r][q];
+      }
+    }
+    if constexpr (DOT || MODE == 1) __syncthreads();  // trow / wdot reused by the next tile
+  }
+  if constexpr (MODE != 2) {
+    if (own)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c0 + q < d.cols) d.partial[(int64_t)(c0 + q) * d.n_cta + blockIdx.x] = acc[q];
+  }
+}
+
+// Per column: sum of the CTA partials (contiguous, warp per column, fixed
+// lane-strided order + warp tree), then the X^T epilogue and its dots.
+template <Epi E>
+__global__ void __launch_bounds__(kThreads) k_dense_finish(DenseDev d, XtArgs a) {
+  if (a.done != nullptr && *a.done) return;
+  const double* v = a.v;
+  double* out = a.out;
+  if constexpr (E == Epi::Fcg) {
+    if (a.sc->done) return;
+    const size_t off = (size_t)ring_slot(a.sc) * a.ring_stride;
+    v += off;
+    out += off;
+  } else if constexpr (E == Epi::Cg) {
+    if (a.sc->done) return;
+  }
+  __shared__ double sh[kWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * kWarps + wid; j < d.cols; j += (int64_t)gridDim.x * kWarps) {
+    const double* pj = d.partial + j * d.n_cta;
+    double sum = 0.0;
+    for (int b = lane; b < d.n_cta; b += 32) sum += __ldcg(pj + b);
+    sum = warp_sum(sum);
+    if (lane == 0) xt_epilogue<E>((int)j, sum, a, v, out, d0, d1);
+  }
+  if constexpr (has_dots<E>()) {
+    const double b0 = block_sum(d0, sh);
+    const double b1 = (E == Epi::Fcg) ? block_sum(d1, sh) : 0.0;
+    if (threadIdx.x == 0) {
+      d.fin_slots[blockIdx.x * 2] = b0;
+      d.fin_slots[blockIdx.x * 2 + 1] = b1;
+    }
+    if (grid_last(d.fin_ticket)) {
+      const double s0 = sum_slots(d.fin_slots, gridDim.x, 2, 0, sh);
+      const double s1 = (E == Epi::Fcg) ? sum_slots(d.fin_slots, gridDim.x, 2, 1, sh) : 0.0;
+      if (threadIdx.x == 0) xt_finalize<E>(a.sc, s0, s1);
+    }
+  }
+}
+
+__global__ void k_add_const(double* x, double c, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += c;
+}
+
+
 // ------------------------------------------------------------------ Krylov vector kernels
 template <class F>
 __device__ __forceinline__ void grid_stride(int64_t n, F&& f) {
@@ -1146,6 +1356,66 @@ void launch_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer, u
                              cudaStream_t s) {
   k_copy_inner_count<<<1, 1, 0, s>>>(inner, outer, inner_hist);
   check_launch("copy_inner_count");
+}
+
+
+namespace {
+template <int MODE>
+void dense_sweep(const DenseDev& d, const double* v, const double* u, double* y, const int32_t* done,
+                 const KrylovScalars* sc, int ring_stride, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(kDenseStages) * kDenseTileBytes;
+  const int grid = d.n_cta;
+  if (d.fp32) {
+    allow_smem(k_dense_ata<float, MODE>, kDenseStages * kDenseTileBytes);
+    k_dense_ata<float, MODE><<<grid, kThreads, smem, s>>>(d, v, u, y, done, sc, ring_stride);
+  } else {
+    allow_smem(k_dense_ata<double, MODE>, kDenseStages * kDenseTileBytes);
+    k_dense_ata<double, MODE><<<grid, kThreads, smem, s>>>(d, v, u, y, done, sc, ring_stride);
+  }
+}
+
+void dense_finish(const DenseDev& d, Epi epi, const XtArgs& a, cudaStream_t s) {
+  const dim3 g(d.fin_grid), b(kThreads);
+  switch (epi) {
+    case Epi::Plain: k_dense_finish<Epi::Plain><<<g, b, 0, s>>>(d, a); break;
+    case Epi::Axpby: k_dense_finish<Epi::Axpby><<<g, b, 0, s>>>(d, a); break;
+    case Epi::Fcg: k_dense_finish<Epi::Fcg><<<g, b, 0, s>>>(d, a); break;
+    case Epi::Cg: k_dense_finish<Epi::Cg><<<g, b, 0, s>>>(d, a); break;
+    case Epi::Rich: k_dense_finish<Epi::Rich><<<g, b, 0, s>>>(d, a); break;
+    case Epi::Gram: k_dense_finish<Epi::Gram><<<g, b, 0, s>>>(d, a); break;
+  }
+}
+}  // namespace
+
+void launch_dense_ata(const DenseDev& d, const double* v, int ring_stride, const KrylovScalars* sc, Epi epi,
+                      const XtArgs& a, cudaStream_t s) {
+  if (d.rows == 0 || d.cols == 0) return;
+  dense_sweep<0>(d, v, nullptr, nullptr, a.done, sc, ring_stride, s);
+  dense_finish(d, epi, a, s);
+  check_launch("dense_ata");
+}
+
+void launch_dense_spmv(const DenseDev& d, const double* v, double* y, cudaStream_t s) {
+  if (d.rows == 0) return;
+  dense_sweep<2>(d, v, nullptr, y, nullptr, nullptr, 0, s);
+  check_launch("dense_spmv");
+}
+
+void launch_dense_xt(const DenseDev& d, const double* u, Epi epi, const XtArgs& a, cudaStream_t s) {
+  if (d.cols == 0) return;
+  dense_sweep<1>(d, nullptr, u, nullptr, a.done, nullptr, 0, s);
+  dense_finish(d, epi, a, s);
+  check_launch("dense_xt");
+}
+
+void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t s) {
+  if (d.cols == 0) return;
+  dense_sweep<3>(d, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s);
+  XtArgs a;
+  a.out = out;
+  dense_finish(d, Epi::Plain, a, s);
+  k_add_const<<<grid_for(d.cols, 148), kThreads, 0, s>>>(out, beta, d.cols);
+  check_launch("dense_diag");
 }
 
 }  // namespace rmg

@@ -128,6 +128,21 @@ struct HotXtDev {
   int64_t N = 0;
 };
 
+// Dense X (row-major, fp64 or fp32 storage, fp64 arithmetic) for dense inputs
+// (DESIGN.md §4.6): the operator X^T X is one fused sweep over X.
+struct DenseDev {
+  const void* data = nullptr;
+  int fp32 = 0;            // 1: float storage
+  int64_t ld = 0;          // elements per stored row (>= cols)
+  int64_t rows = 0, cols = 0;
+  double* partial = nullptr;  // [cols x n_cta] column-major per-CTA partial sums
+  int n_cta = 0;
+  double* fin_slots = nullptr;
+  unsigned* fin_ticket = nullptr;
+  int fin_grid = 1;
+};
+constexpr int kDenseMaxCols = 1024;  // 32 register partials per lane
+
 // ---------------------------------------------------------------- launchers
 void launch_spmv_rows(const SparseDev& x, const double* v, double* t, const int32_t* done,
                       cudaStream_t s);
@@ -135,6 +150,13 @@ void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_st
                            const KrylovScalars* sc, double* t, cudaStream_t s);
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a,
                cudaStream_t s);
+// dense X: out = epilogue(X^T (X v)) in one sweep (v may live in a ring: sc != nullptr)
+void launch_dense_ata(const DenseDev& d, const double* v, int ring_stride, const KrylovScalars* sc, Epi epi,
+                      const XtArgs& a, cudaStream_t s);
+// dense X: y = X v (rows), out = X^T u (+ epilogue), out = beta + diag(X^T X)
+void launch_dense_spmv(const DenseDev& d, const double* v, double* y, cudaStream_t s);
+void launch_dense_xt(const DenseDev& d, const double* u, Epi epi, const XtArgs& a, cudaStream_t s);
+void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

@@ -487,7 +487,8 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   }
 }
 
-Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), host(std::move(h)), comm(cm) {
+Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din)
+    : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
   if (host.n > INT32_MAX || host.f > INT32_MAX || host.nnz() > INT32_MAX)
     throw InvalidArgument("FeatureMatrix: dimensions exceed the single-device int32 index range");
@@ -517,6 +518,43 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm) : ctx(c), h
     RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
   }
   const HostCsr& local = comm != nullptr ? shard : host;
+  if (din != nullptr) {  // dense X: one row-major device copy, fused single-sweep operator
+    if (host.f > kDenseMaxCols) throw InvalidArgument("dense X: more than 1024 features (use CSR)");
+    if (din->ld < host.f) throw InvalidArgument("dense X: leading dimension below the feature count");
+    pattern = false;
+    auto d = std::make_unique<DenseStore>();
+    const size_t esz = din->fp32 ? 4 : 8;
+    const int64_t nl = local.n;
+    // stored with ld = F rounded up to 4 elements (16 B aligned rows)
+    const int64_t ld = (host.f + 3) / 4 * 4;
+    std::vector<char> buf(static_cast<size_t>(nl) * ld * esz, 0);
+    const char* src = static_cast<const char*>(din->data) + static_cast<size_t>(row0) * din->ld * esz;
+    for (int64_t i = 0; i < nl; ++i)
+      std::memcpy(&buf[static_cast<size_t>(i) * ld * esz], src + static_cast<size_t>(i) * din->ld * esz,
+                  static_cast<size_t>(host.f) * esz);
+    d->data.upload(buf.data(), buf.size(), ctx->stream);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    d->view.n_cta = sms;
+    d->partial.alloc(static_cast<size_t>(std::max<int64_t>(1, host.f)) * sms);
+    d->view.fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, (host.f + 7) / 8)));
+    d->fin_slots.alloc(static_cast<size_t>(d->view.fin_grid) * 2);
+    d->fin_ticket.alloc(1);
+    RMG_CK(cudaMemsetAsync(d->fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
+    RMG_CK(cudaStreamSynchronize(ctx->stream));
+    d->view.data = d->data.get();
+    d->view.fp32 = din->fp32;
+    d->view.ld = ld;
+    d->view.rows = nl;
+    d->view.cols = host.f;
+    d->view.partial = d->partial.get();
+    d->view.fin_slots = d->fin_slots.get();
+    d->view.fin_ticket = d->fin_ticket.get();
+    dense = std::move(d);
+    t.alloc(std::max<int64_t>(1, local.n));
+    gram_sc.alloc(1);
+    return;
+  }
   // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
   // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
   const char* rl = std::getenv("RMG_RELABEL");
@@ -580,7 +618,32 @@ void xt_pass(Matrix& m, const double* t, Epi epi, const XtArgs& args) {
 }
 }  // namespace
 
+// Dense X: fused X^T (X v) sweep; sharded: plain sums, all-reduce, epilogue.
+static void dense_apply(Matrix& m, const double* v, int stride, const KrylovScalars* sc, Epi epi,
+                        const XtArgs& args) {
+  if (m.comm == nullptr) {
+    launch_dense_ata(m.dense->view, v, stride, sc, epi, args, m.ctx->stream);
+  } else {
+    XtArgs pa = args;
+    pa.out = m.part.get();
+    launch_dense_ata(m.dense->view, v, stride, sc, Epi::Plain, pa, m.ctx->stream);
+    m.allreduce_sums(m.part.get(), m.red.get(), m.f());
+    launch_xt_epilogue(m.red.get(), m.f(), epi, args, m.fin_slots.get(), m.fin_ticket.get(), m.fin_grid,
+                       m.ctx->stream);
+  }
+  m.ctx->launches += 2;
+}
+
 void Matrix::apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof) {
+  if (dense) {
+    if (prof) prof->mark(ctx->stream);
+    dense_apply(*this, v, 0, nullptr, epi, args);
+    if (prof) {
+      prof->mark(ctx->stream);
+      prof->mark(ctx->stream);
+    }
+    return;
+  }
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows(x.view, v, t.get(), args.done, ctx->stream);
   if (prof) prof->mark(ctx->stream);
@@ -591,6 +654,15 @@ void Matrix::apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof
 
 void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args,
                         OpProfile* prof) {
+  if (dense) {
+    if (prof) prof->mark(ctx->stream);
+    dense_apply(*this, v_ring, stride, sc, epi, args);
+    if (prof) {
+      prof->mark(ctx->stream);
+      prof->mark(ctx->stream);
+    }
+    return;
+  }
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows_ring(x.view, v_ring, stride, sc, t.get(), ctx->stream);
   if (prof) prof->mark(ctx->stream);
@@ -600,11 +672,17 @@ void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* s
 }
 
 void Matrix::spmv(const double* v, double* y) {
+  auto rows = [&](double* yy) {
+    if (dense)
+      launch_dense_spmv(dense->view, v, yy, ctx->stream);
+    else
+      launch_spmv_rows(x.view, v, yy, nullptr, ctx->stream);
+  };
   if (comm == nullptr) {
-    launch_spmv_rows(x.view, v, y, nullptr, ctx->stream);
+    rows(y);
   } else {  // own rows into a zeroed N-vector, then sum over ranks
     RMG_CK(cudaMemsetAsync(y, 0, static_cast<size_t>(n()) * sizeof(double), ctx->stream));
-    launch_spmv_rows(x.view, v, y + row0, nullptr, ctx->stream);
+    rows(y + row0);
     allreduce_sums(y, y, n());
   }
   ctx->launches += 1;
@@ -613,10 +691,16 @@ void Matrix::spmv(const double* v, double* y) {
 // gram_diagonal (ridge.cpp:30-37); sharded: local sums, all-reduce, + beta
 void Matrix::gram_diagonal(double beta, double* out) {
   if (comm == nullptr) {
-    launch_diag_gram(xt.view, sched.view, beta, out, ctx->stream);
+    if (dense)
+      launch_dense_diag(dense->view, beta, out, ctx->stream);
+    else
+      launch_diag_gram(xt.view, sched.view, beta, out, ctx->stream);
     return;
   }
-  launch_diag_gram(xt.view, sched.view, 0.0, part.get(), ctx->stream);
+  if (dense)
+    launch_dense_diag(dense->view, 0.0, part.get(), ctx->stream);
+  else
+    launch_diag_gram(xt.view, sched.view, 0.0, part.get(), ctx->stream);
   allreduce_sums(part.get(), red.get(), f());
   std::vector<double> h(f());
   if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), red.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -629,6 +713,19 @@ void Matrix::gram_diagonal(double beta, double* out) {
 void Matrix::spmv_t(const double* u, double* y) {
   XtArgs a;
   a.out = y;
+  if (dense) {
+    if (comm == nullptr) {
+      launch_dense_xt(dense->view, u, Epi::Plain, a, ctx->stream);
+    } else {
+      XtArgs pa = a;
+      pa.out = part.get();
+      launch_dense_xt(dense->view, u + row0, Epi::Plain, pa, ctx->stream);
+      allreduce_sums(part.get(), red.get(), f());
+      RMG_CK(cudaMemcpyAsync(y, red.get(), static_cast<size_t>(f()) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ctx->launches += 2;
+    return;
+  }
   xt_pass(*this, u + row0, Epi::Plain, a);  // sharded: this rank's samples of u
   ctx->launches += 1;
 }
@@ -1311,12 +1408,17 @@ double Method::time_operator(size_t level, uint64_t reps, bool flush, double* k1
   for (uint64_t r = 0; r < reps + 2; ++r) {  // 2 warm-ups
     if (flush) RMG_CK(cudaMemsetAsync(scratch.get(), static_cast<int>(r & 0xff), flush_bytes, s));
     RMG_CK(cudaEventRecord(e0, s));
-    launch_spmv_rows(m.x.view, v.get(), m.t.get(), nullptr, s);
-    RMG_CK(cudaEventRecord(e1, s));
-    if (m.comm != nullptr)  // no collective inside a single-rank timing loop
-      launch_xt(m.xt.view, m.sched.view, Epi::Axpby, a, s);
+    if (m.dense)  // fused single sweep: K1 slot = sweep + finish, K2 slot empty
+      m.apply(v.get(), Epi::Axpby, a);
     else
+      launch_spmv_rows(m.x.view, v.get(), m.t.get(), nullptr, s);
+    RMG_CK(cudaEventRecord(e1, s));
+    if (m.dense) {
+    } else if (m.comm != nullptr) {  // no collective inside a single-rank timing loop
+      launch_xt(m.xt.view, m.sched.view, Epi::Axpby, a, s);
+    } else {
       xt_pass(m, m.t.get(), Epi::Axpby, a);
+    }
     RMG_CK(cudaEventRecord(e2, s));
     RMG_CK(cudaEventSynchronize(e2));
     float a1 = 0.f, a2 = 0.f;

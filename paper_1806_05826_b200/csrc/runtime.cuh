@@ -149,6 +149,19 @@ struct HotXt {
   DeviceSchedule cold;  // segmented schedule over the cold rows only
 };
 
+// Dense X on the device: row-major, fp64 or fp32 storage.
+struct DenseInput {
+  const void* data = nullptr;  // host, row-major n x f, leading dimension ld
+  int fp32 = 0;
+  int64_t ld = 0;
+};
+struct DenseStore {
+  DenseDev view;
+  DBuf<char> data;
+  DBuf<double> partial, fin_slots;
+  DBuf<unsigned> fin_ticket;
+};
+
 struct Matrix {
   Context* ctx = nullptr;
   HostCsr host;  // canonical CSR kept for setup (clustering, coarsening)
@@ -163,7 +176,8 @@ struct Matrix {
   DBuf<unsigned> fin_ticket;
   int fin_grid = 1;
   std::unique_ptr<HotXt> hot;  // hybrid X^T pass when N is large (nullptr otherwise)
-  Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr);
+  std::unique_ptr<DenseStore> dense;  // dense inputs: X row-major on the device, no CSR copies
+  Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
   void build_hot(const HostCsr& ht, int64_t n_samples);
   int64_t n_local() const { return row1 - row0; }
   void allreduce_sums(double* sendbuf, double* recvbuf, int64_t count);

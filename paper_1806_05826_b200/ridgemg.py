@@ -265,6 +265,38 @@ class DeviceMatrix:
             _lib.check(self.lib.rmg_matrix_create_csr_sharded(self.ctx.h, comm.h, x.n_samples, x.n_features, _ptr(rp),
                                                               _ptr(ci), _ptr(v), int(detect_pattern),
                                                               C.byref(self.h)))
+        self._query()
+
+    @classmethod
+    def from_dense(cls, a, ctx: Optional[Context] = None, comm: Optional["Comm"] = None) -> "DeviceMatrix":
+        """Dense X (row-major, float64 or float32 storage; arithmetic stays fp64):
+        the operator is one fused sweep over X.  n_features <= 1024."""
+        a = np.asarray(a)
+        if a.ndim != 2:
+            raise ValueError("from_dense: a must be 2-D (samples x features)")
+        fp32 = a.dtype == np.float32
+        a = np.ascontiguousarray(a, np.float32 if fp32 else np.float64)
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.x = None
+        self.comm = comm
+        self.h = C.c_void_p()
+        n, f = a.shape
+        if comm is None:
+            _lib.check(self.lib.rmg_matrix_create_dense(self.ctx.h, n, f, _ptr(a), f, int(fp32), C.byref(self.h)))
+        else:
+            _lib.check(self.lib.rmg_matrix_create_dense_sharded(self.ctx.h, comm.h, n, f, _ptr(a), f, int(fp32),
+                                                                C.byref(self.h)))
+        self._query()
+        return self
+
+    def is_dense(self) -> bool:
+        d = C.c_int32()
+        _lib.check(self.lib.rmg_matrix_is_dense(self.h, C.byref(d), None))
+        return bool(d.value)
+
+    def _query(self):
         r0, r1, nr, rk = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_int32()
         if hasattr(self.lib, "rmg_matrix_shard"):
             _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
