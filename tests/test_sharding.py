@@ -142,3 +142,27 @@ def test_sharded_matrix_single_rank_nccl(gpu):
     assert np.linalg.norm(s1.w - s2.w) <= 1e-9 * np.linalg.norm(s2.w)
     ms.close()
     comm.close()
+
+
+@pytest.mark.gpu
+def test_dense_sharded_single_rank_nccl(gpu):
+    """Dense X row-sharded over NCCL (cfg 4's layout) on one rank equals the
+    unsharded dense operator and solve."""
+    a = np.random.default_rng(8).standard_normal((5000, 300)).astype(np.float32)
+    uid = R.Comm.new_unique_id()
+    comm = R.Comm(gpu, 1, 0, uid)
+    ms = R.DeviceMatrix.from_dense(a, gpu, comm=comm)
+    mu = R.DeviceMatrix.from_dense(a, gpu)
+    assert ms.is_dense() and ms.row_range == (0, 5000)
+    v = np.random.default_rng(3).standard_normal(300)
+    u = np.random.default_rng(4).standard_normal(5000)
+    for got, want in ((ms.ridge_apply(0.5, v), mu.ridge_apply(0.5, v)), (ms.spmv(v), mu.spmv(v)),
+                      (ms.spmv_transpose(u), mu.spmv_transpose(u)), (ms.gram_diagonal(0.5), mu.gram_diagonal(0.5))):
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+    bb = R.rng_normals(42, 5000)
+    spec = R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-10, 2000))
+    s1, s2 = R.solve_system(ms, 1e-2, bb, spec), R.solve_system(mu, 1e-2, bb, spec)
+    assert s1.report.converged and abs(s1.report.iterations - s2.report.iterations) <= 1
+    assert np.linalg.norm(s1.w - s2.w) <= 1e-9 * np.linalg.norm(s2.w)
+    ms.close()
+    comm.close()
