@@ -47,7 +47,8 @@ typedef enum {
   RMG_METHOD_CG = 0,
   RMG_METHOD_JACOBI_CG = 1,
   RMG_METHOD_FCG_TWOLEVEL = 2,
-  RMG_METHOD_FCG_MULTILEVEL = 3
+  RMG_METHOD_FCG_MULTILEVEL = 3,
+  RMG_METHOD_FGMRES_TWOLEVEL = 4 /* krylov.cpp:229-328 + :628-635, full (unrestarted) */
 } rmg_method_kind;
 
 /* krylov.hpp:135-146 ClusteringChoice::Kind (+ imported labels for parity runs) */

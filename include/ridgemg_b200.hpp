@@ -92,13 +92,14 @@ struct LevelSpec {
 
 // krylov.hpp:207-218
 enum class MethodKind { cg = RMG_METHOD_CG, jacobi_cg = RMG_METHOD_JACOBI_CG, fcg_twolevel = RMG_METHOD_FCG_TWOLEVEL,
-                        fcg_multilevel = RMG_METHOD_FCG_MULTILEVEL };
+                        fcg_multilevel = RMG_METHOD_FCG_MULTILEVEL, fgmres_twolevel = RMG_METHOD_FGMRES_TWOLEVEL };
 
 inline MethodKind method_from_string(const std::string& s) {  // krylov.cpp:574-581
   if (s == "cg") return MethodKind::cg;
   if (s == "jacobi_cg") return MethodKind::jacobi_cg;
   if (s == "fcg_twolevel") return MethodKind::fcg_twolevel;
   if (s == "fcg_multilevel") return MethodKind::fcg_multilevel;
+  if (s == "fgmres_twolevel") return MethodKind::fgmres_twolevel;
   throw std::invalid_argument("unknown method: '" + s + "'");
 }
 
@@ -248,7 +249,7 @@ class PreparedMethod {
     r.wall_time_s = rep.wall_time_s;
     const std::size_t nh = rep.iterations ? rep.iterations : (rep.converged ? 1 : 0);
     r.residual_history.assign(hist.begin(), hist.begin() + nh);
-    if (spec_.kind == MethodKind::fcg_twolevel || spec_.kind == MethodKind::fcg_multilevel)
+    if (spec_.kind != MethodKind::cg && spec_.kind != MethodKind::jacobi_cg)
       r.inner_iterations.assign(inner.begin(), inner.begin() + rep.iterations);
     return {std::move(w), std::move(r)};
   }

@@ -31,7 +31,7 @@ LIBS = {
 CLUSTER_LEADER_TOLERANCE, CLUSTER_LEADER_TARGET, CLUSTER_KMEANS = 0, 1, 2
 COARSE_DIRECT, COARSE_INNER_CG, COARSE_INNER_FCG = 0, 1, 2
 METHOD_CG, METHOD_JACOBI_CG, METHOD_FCG_TWOLEVEL, METHOD_FCG_MULTILEVEL = 0, 1, 2, 3
-METHODS = {"cg": 0, "jacobi_cg": 1, "fcg_twolevel": 2, "fcg_multilevel": 3}
+METHODS = {"cg": 0, "jacobi_cg": 1, "fcg_twolevel": 2, "fcg_multilevel": 3, "fgmres_twolevel": 4}
 
 
 class LevelSpec(C.Structure):

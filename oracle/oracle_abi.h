@@ -23,7 +23,7 @@ enum { OR_CLUSTER_LEADER_TOLERANCE = 0, OR_CLUSTER_LEADER_TARGET = 1, OR_CLUSTER
 enum { OR_COARSE_DIRECT = 0, OR_COARSE_INNER_CG = 1, OR_COARSE_INNER_FCG = 2 };
 /* krylov.hpp:207 MethodKind */
 enum { OR_METHOD_CG = 0, OR_METHOD_JACOBI_CG = 1, OR_METHOD_FCG_TWOLEVEL = 2,
-       OR_METHOD_FCG_MULTILEVEL = 3 };
+       OR_METHOD_FCG_MULTILEVEL = 3, OR_METHOD_FGMRES_TWOLEVEL = 4 };
 
 typedef struct {
   /* clustering (used when labels == NULL) */

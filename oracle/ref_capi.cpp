@@ -389,13 +389,14 @@ int ref_solve(void* h, double beta, int32_t method, const or_level_spec* levels,
       return;
     }
     std::vector<or_level_spec> specs(levels, levels + n_levels);
-    if (method == OR_METHOD_FCG_TWOLEVEL) {  // krylov.cpp:628-635
+    if (method == OR_METHOD_FCG_TWOLEVEL || method == OR_METHOD_FGMRES_TWOLEVEL) {  // krylov.cpp:628-635
       specs.resize(1);
       specs[0].coarse_kind = OR_COARSE_DIRECT;
     }
     auto hier = build_from_specs(x, beta, specs.data(), specs.size());
     const DenseVector rhs = spmv_transpose(x, bv);  // krylov.cpp:655
-    auto [sol, report] = fcg(*hier->fine_op, rhs, sc, *hier->preconds[0]);
+    auto [sol, report] = method == OR_METHOD_FGMRES_TWOLEVEL ? fgmres(*hier->fine_op, rhs, sc, *hier->preconds[0])
+                                                             : fcg(*hier->fine_op, rhs, sc, *hier->preconds[0]);
     std::memcpy(w, sol.data(), sol.size() * sizeof(double));
     fill_report(report, rep);
     if (rep) {

@@ -501,6 +501,81 @@ Vec fcg(const Op& a, const Vec& rhs, double tol, uint64_t max_iters, uint64_t tr
   return x;
 }
 
+// ---------------------------------------------------------------- FGMRES
+// krylov.cpp:229-328 — full (unrestarted) flexible GMRES, right-preconditioned:
+// modified Gram-Schmidt of w = A z_j against v_0..v_j, Givens rotations on the
+// Hessenberg column, residual estimate |g_{j+1}| / ||rhs||, back substitution,
+// x = sum_j y_j z_j.
+Vec fgmres(const Op& a, const Vec& rhs, double tol, uint64_t max_iters, const Precond& m, Report& rep) {
+  check_rhs(rhs, a.dim(), "fgmres");
+  const auto t0 = Clock::now();
+  const int64_t n = a.dim();
+  Vec x(n, 0.0);
+  const double nrhs = nrm(rhs.data(), n);
+  if (nrhs == 0.0) {
+    rep.converged = true;
+    rep.hist.push_back(0.0);
+    rep.wall = since(t0);
+    return x;
+  }
+  std::vector<Vec> basis, pre, hess;
+  Vec gc, gs, g;
+  basis.push_back(rhs);
+  for (double& v : basis[0]) v /= nrhs;
+  g.push_back(nrhs);
+  Vec z(n), w(n);
+  uint64_t k = 0;
+  for (uint64_t j = 0; j < max_iters; ++j) {
+    rep.inner.push_back(m.apply(basis[j].data(), z.data()));
+    pre.push_back(z);
+    a.apply(z.data(), w.data());
+    Vec h(j + 2, 0.0);
+    for (uint64_t i = 0; i <= j; ++i) {
+      h[i] = dotp(w.data(), basis[i].data(), n);
+      for (int64_t t = 0; t < n; ++t) w[t] -= h[i] * basis[i][t];
+    }
+    const double h_next = nrm(w.data(), n);
+    h[j + 1] = h_next;
+    for (uint64_t i = 0; i < j; ++i) {
+      const double tmp = gc[i] * h[i] + gs[i] * h[i + 1];
+      h[i + 1] = -gs[i] * h[i] + gc[i] * h[i + 1];
+      h[i] = tmp;
+    }
+    const double denom = std::hypot(h[j], h[j + 1]);
+    const double c = denom == 0.0 ? 1.0 : h[j] / denom;
+    const double sn = denom == 0.0 ? 0.0 : h[j + 1] / denom;
+    gc.push_back(c);
+    gs.push_back(sn);
+    h[j] = denom;
+    h[j + 1] = 0.0;
+    g.push_back(-sn * g[j]);
+    g[j] = c * g[j];
+    hess.push_back(std::move(h));
+    k = j + 1;
+    const double rel = std::abs(g[j + 1]) / nrhs;
+    rep.hist.push_back(rel);
+    rep.iterations = k;
+    if (rel <= tol || h_next == 0.0) {
+      rep.converged = true;
+      break;
+    }
+    basis.emplace_back(n);
+    for (int64_t t = 0; t < n; ++t) basis[j + 1][t] = w[t] / h_next;
+  }
+  Vec y(k, 0.0);
+  for (uint64_t i = k; i-- > 0;) {
+    double acc = g[i];
+    for (uint64_t jj = i + 1; jj < k; ++jj) acc -= hess[jj][i] * y[jj];
+    if (hess[i][i] == 0.0)
+      throw std::runtime_error("fgmres: rank-deficient Hessenberg system at column " + std::to_string(i));
+    y[i] = acc / hess[i][i];
+  }
+  for (uint64_t jj = 0; jj < k; ++jj)
+    for (int64_t t = 0; t < n; ++t) x[t] += y[jj] * pre[jj][t];
+  rep.wall = since(t0);
+  return x;
+}
+
 // ---------------------------------------------------------------- clustering
 using Labels = std::vector<int64_t>;
 
@@ -1090,13 +1165,16 @@ int orc_solve(void* h, double beta, int32_t method, const or_level_spec* levels,
       }
     } else {
       std::vector<or_level_spec> sp(levels, levels + n_levels);
-      if (method == OR_METHOD_FCG_TWOLEVEL) {
+      if (method == OR_METHOD_FCG_TWOLEVEL || method == OR_METHOD_FGMRES_TWOLEVEL) {  // krylov.cpp:628-635
         if (sp.empty()) throw std::invalid_argument("two-level method requires one level spec");
         sp.resize(1);
         sp[0].coarse_kind = OR_COARSE_DIRECT;
       }
       auto hier = build(x, beta, sp.data(), sp.size());
-      sol = fcg(hier->fine_op, rhs, cfg->tol, cfg->max_iters, cfg->truncation, *hier->pc[0], r);
+      if (method == OR_METHOD_FGMRES_TWOLEVEL)
+        sol = fgmres(hier->fine_op, rhs, cfg->tol, cfg->max_iters, *hier->pc[0], r);
+      else
+        sol = fcg(hier->fine_op, rhs, cfg->tol, cfg->max_iters, cfg->truncation, *hier->pc[0], r);
       if (rep) {
         rep->n_levels = sp.size() + 1;
         for (size_t k = 0; k < sp.size() && k < 8; ++k) rep->omega[k] = hier->omega[k];

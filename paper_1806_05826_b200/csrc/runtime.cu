@@ -9,6 +9,7 @@
 #include <thread>
 
 #include "runtime.cuh"
+#include "fgmres.cuh"
 
 namespace rmg {
 
@@ -837,7 +838,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
                const rmg_solver_config& sol)
     : solver(sol), ctx_(x->ctx), fine_(x), beta_(beta), kind_(kind) {
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
-  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_FCG_MULTILEVEL)
+  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_FGMRES_TWOLEVEL)
     throw InvalidArgument("unknown method kind " + std::to_string(kind));
   if (solver.max_iters > static_cast<uint64_t>(INT32_MAX)) throw InvalidArgument("max_iters too large");
   const int keep0 = static_cast<int>(std::max<uint64_t>(solver.truncation, 1));
@@ -863,9 +864,9 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
   }
 
   if (n_levels == 0 || levels == nullptr)
-    throw InvalidArgument(kind == RMG_METHOD_FCG_TWOLEVEL ? "two-level method requires one level spec"
-                                                          : "multilevel method requires level specs");
-  const uint64_t L = kind == RMG_METHOD_FCG_TWOLEVEL ? 1 : n_levels;
+    throw InvalidArgument(kind != RMG_METHOD_FCG_MULTILEVEL ? "two-level method requires one level spec"
+                                                            : "multilevel method requires level specs");
+  const uint64_t L = kind != RMG_METHOD_FCG_MULTILEVEL ? 1 : n_levels;
   if (L > RMG_MAX_LEVELS) throw InvalidArgument("too many levels");
   for (uint64_t k = 0; k < L; ++k) {
     LevelSpecHost ls;
@@ -878,7 +879,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     ls.spec.labels = nullptr;
     specs_.push_back(ls);
   }
-  if (kind == RMG_METHOD_FCG_TWOLEVEL) specs_[0].spec.coarse_kind = RMG_COARSE_DIRECT_CHOLESKY;  // krylov.cpp:632-634
+  if (kind != RMG_METHOD_FCG_MULTILEVEL) specs_[0].spec.coarse_kind = RMG_COARSE_DIRECT_CHOLESKY;  // krylov.cpp:632-634
   // krylov.cpp:495-505
   for (uint64_t k = 0; k + 1 < L; ++k)
     if (specs_[k].spec.coarse_kind == RMG_COARSE_DIRECT_CHOLESKY)
@@ -1323,6 +1324,110 @@ uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out
   return static_cast<uint64_t>(hs.it);
 }
 
+// fgmres (krylov.cpp:229-328), full flexible GMRES with the level-0 two-level
+// preconditioner.  Device: preconditioner, operator, the MGS sweep (one
+// cooperative launch per iteration, fgmres.cu), v_{j+1} = w / h_{j+1,j} and the
+// final x = sum y_j z_j.  Host: the reference's Givens rotations, residual
+// estimate and back substitution on the j + 2 Hessenberg entries per iteration.
+uint64_t Method::run_fgmres(const double* rhs, SolveResult* out) {
+  KrylovWork& w = *work_[0];
+  Matrix& m = level_matrix(0);
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  const auto t0 = Clock::now();
+  launch_krylov_begin(rhs, w.x.get(), w.r.get(), n, w.sc.get(), w.hist.get(), w.vw, s);  // x = 0, ||rhs||
+  ctx_->launches += 1;
+  const KrylovScalars hs0 = ctx_->read(w.sc.get());
+  if (hs0.status == 3) throw InvalidArgument("fgmres: non-finite rhs");
+  const double nrhs = hs0.nb;
+  out->inner.clear();
+  out->hist.clear();
+  out->iterations = 0;
+  out->converged = false;
+  if (nrhs == 0.0) {
+    out->converged = true;
+    out->hist.push_back(0.0);
+    out->final_rel = 0.0;
+    out->wall = secs(t0);
+    return 0;
+  }
+  const uint64_t maxit = solver.max_iters;
+  const size_t need_basis = static_cast<size_t>(maxit + 1) * std::max<int64_t>(1, n);
+  if (gm_basis_.size() < need_basis) {
+    gm_basis_.alloc(need_basis);
+    gm_z_.alloc(static_cast<size_t>(std::max<uint64_t>(1, maxit)) * std::max<int64_t>(1, n));
+    gm_h_.alloc(static_cast<size_t>(maxit + 2));
+    gm_part_.alloc(static_cast<size_t>(2 * mgs_grid(n)));
+  }
+  double* wv = w.r.get();  // w = A z_j, orthogonalized in place
+  // v_0 = rhs / ||rhs|| (KrylovScalars::nb on the device)
+  launch_div(gm_basis_.get(), rhs, &w.sc.get()->nb, n, s);
+  std::vector<std::vector<double>> hess;
+  std::vector<double> giv_c, giv_s, g{nrhs}, h;
+  uint64_t k = 0;
+  for (uint64_t j = 0; j < maxit; ++j) {
+    double* vj = gm_basis_.get() + static_cast<size_t>(j) * n;
+    double* zj = gm_z_.get() + static_cast<size_t>(j) * n;
+    out->inner.push_back(precond(0, vj, zj));
+    XtArgs a;
+    a.v = zj;
+    a.out = wv;
+    a.beta = level_beta(0);
+    m.apply(zj, Epi::Axpby, a, prof(0));
+    launch_mgs(wv, gm_basis_.get(), n, static_cast<int>(j), gm_h_.get(), gm_part_.get(), s);
+    ctx_->launches += 2;
+    h.assign(j + 2, 0.0);
+    RMG_CK(cudaMemcpyAsync(h.data(), gm_h_.get(), (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    ctx_->sync();
+    if (profiling_) collect_profiles();
+    const double h_next = h[j + 1];
+    for (uint64_t i = 0; i < j; ++i) {  // previously accumulated rotations
+      const double tmp = giv_c[i] * h[i] + giv_s[i] * h[i + 1];
+      h[i + 1] = -giv_s[i] * h[i] + giv_c[i] * h[i + 1];
+      h[i] = tmp;
+    }
+    const double denom = std::hypot(h[j], h[j + 1]);
+    const double c = denom == 0.0 ? 1.0 : h[j] / denom;
+    const double sn = denom == 0.0 ? 0.0 : h[j + 1] / denom;
+    giv_c.push_back(c);
+    giv_s.push_back(sn);
+    h[j] = denom;
+    h[j + 1] = 0.0;
+    g.push_back(-sn * g[j]);
+    g[j] = c * g[j];
+    hess.push_back(h);
+    k = j + 1;
+    const double rel = std::abs(g[j + 1]) / nrhs;
+    out->hist.push_back(rel);
+    out->iterations = k;
+    out->final_rel = rel;
+    if (rel <= solver.tol || h_next == 0.0) {  // converged, or happy breakdown
+      out->converged = true;
+      break;
+    }
+    launch_div(gm_basis_.get() + static_cast<size_t>(j + 1) * n, wv, gm_h_.get() + j + 1, n, s);
+    ctx_->launches += 1;
+  }
+  std::vector<double> y(k, 0.0);  // back substitution on the rotated triangle
+  for (uint64_t i = k; i-- > 0;) {
+    double acc = g[i];
+    for (uint64_t jj = i + 1; jj < k; ++jj) acc -= hess[jj][i] * y[jj];
+    const double diag = hess[i][i];
+    if (diag == 0.0)
+      throw RuntimeError("fgmres: rank-deficient Hessenberg system at column " + std::to_string(i));
+    y[i] = acc / diag;
+  }
+  if (k > 0) {
+    DBuf<double> yd(k);
+    yd.upload(y.data(), k, s);
+    launch_combine(w.x.get(), gm_z_.get(), yd.get(), static_cast<int>(k), n, s);
+    ctx_->launches += 1;
+    ctx_->sync();
+  }
+  out->wall = secs(t0);
+  return k;
+}
+
 // cg (krylov.cpp:94-157), optionally Jacobi-preconditioned
 uint64_t Method::run_cg(size_t k, const double* rhs, const double* inv, bool rec, SolveResult* out) {
   KrylovWork& w = *work_[k];
@@ -1364,6 +1469,8 @@ SolveResult Method::solve_rhs(const double* rhs, double* w_out) {
     run_cg(0, rhs, nullptr, true, &res);
   else if (kind_ == RMG_METHOD_JACOBI_CG)
     run_cg(0, rhs, inv_diag_.get(), true, &res);
+  else if (kind_ == RMG_METHOD_FGMRES_TWOLEVEL)
+    run_fgmres(rhs, &res);
   else
     run_fcg(0, rhs, true, &res);
   const int64_t n = fine_->f();

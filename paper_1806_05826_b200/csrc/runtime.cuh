@@ -289,6 +289,8 @@ class Method {
   std::vector<std::unique_ptr<DenseInner>> dense_;  // per level (nullptr: host-sequenced path)
   void build_dense_levels(const std::vector<double>& ainv_host);
   uint64_t run_dense(size_t k, const double* rhs);
+  uint64_t run_fgmres(const double* rhs, SolveResult* out);
+  DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);
   void tune_dense_partials(size_t k);
   DBuf<double> ainv_, rc_last_, ec_last_;

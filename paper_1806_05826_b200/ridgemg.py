@@ -18,8 +18,9 @@ import numpy as np
 from . import _lib
 
 # ---------------------------------------------------------------- enums (krylov.hpp)
-CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL = 0, 1, 2, 3
-METHOD_NAMES = {"cg": CG, "jacobi_cg": JACOBI_CG, "fcg_twolevel": FCG_TWOLEVEL, "fcg_multilevel": FCG_MULTILEVEL}
+CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL, FGMRES_TWOLEVEL = 0, 1, 2, 3, 4
+METHOD_NAMES = {"cg": CG, "jacobi_cg": JACOBI_CG, "fcg_twolevel": FCG_TWOLEVEL, "fcg_multilevel": FCG_MULTILEVEL,
+                "fgmres_twolevel": FGMRES_TWOLEVEL}
 LEADER_TOLERANCE, LEADER_TARGET, KMEANS, IMPORTED = 0, 1, 2, 100
 DIRECT_CHOLESKY, INNER_CG, INNER_FCG = 0, 1, 2
 
@@ -497,7 +498,7 @@ class PreparedMethod:
     def _finish(self, rep, hist, inner) -> SolveReport:
         it = rep.iterations
         nh = it if it else (1 if rep.converged else 0)
-        flexible = self.spec.kind in (FCG_TWOLEVEL, FCG_MULTILEVEL)
+        flexible = self.spec.kind in (FCG_TWOLEVEL, FCG_MULTILEVEL, FGMRES_TWOLEVEL)
         return SolveReport(iterations=it, residual_history=hist[:nh].copy(), converged=bool(rep.converged),
                            wall_time_s=rep.wall_time_s,
                            inner_iterations=inner[:it].copy() if flexible else np.zeros(0, np.uint64),

@@ -42,8 +42,9 @@ int main(int argc, char** argv) {
     } catch (const std::runtime_error& e) {
       std::printf("ok: %s\n", e.what());
     }
+    if (rb::method_from_string("fgmres_twolevel") != rb::MethodKind::fgmres_twolevel) return 1;
     try {
-      rb::method_from_string("fgmres_twolevel");
+      rb::method_from_string("gmres");
       return 1;
     } catch (const std::invalid_argument&) {
       std::printf("ok: unknown method rejected\n");
@@ -64,7 +65,7 @@ int main(int argc, char** argv) {
   rb::LevelSpec last;
   last.clustering.kind = rb::ClusteringChoice::Kind::kmeans;
   last.clustering.target_size = 5;
-  for (const char* name : {"cg", "jacobi_cg", "fcg_twolevel", "fcg_multilevel"}) {
+  for (const char* name : {"cg", "jacobi_cg", "fcg_twolevel", "fcg_multilevel", "fgmres_twolevel"}) {
     spec.kind = rb::method_from_string(name);
     spec.levels = spec.kind == rb::MethodKind::fcg_multilevel ? std::vector<rb::LevelSpec>{mid, last}
                                                               : std::vector<rb::LevelSpec>{mid};

@@ -32,4 +32,4 @@ def test_cpp_client_cpu_only(example):
 def test_cpp_client_solves(example):
     r = subprocess.run([example], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("converged=1") == 4
+    assert r.stdout.count("converged=1") == 5

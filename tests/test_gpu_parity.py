@@ -358,3 +358,44 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
             assert rel_diff(g["ml12_w"], g["cg12_w"]) <= W_TOL  # the reference's own gap
             assert float(rep12.residual_history[-1]) <= 10 * float(g["ml12_hist"][-1])
             assert rel_diff(w12, g["cg12_w"]) <= W_TOL, rel_diff(w12, g["cg12_w"])
+
+
+# ---------------------------------------------------------------- FGMRES
+@pytest.mark.parametrize("case", range(3))
+def test_fgmres_twolevel_matches_oracle(gpu, orc, case):
+    """fgmres_twolevel (krylov.cpp:229-328, 628-635): GPU MGS sweep + host
+    Givens against the oracle (pinned bit-exact to the reference build)."""
+    n, f, seed = [(300, 120, 5), (800, 300, 7), (2000, 500, 0)][case]
+    x = random_matrix(n, f, seed, 0.3) if case < 2 else R.synth_dense_clustered(2000, 500, 50, 0.1, 0)
+    m = dm(x)
+    om = to_checker(orc, x)
+    b = orc.normals(seed + 1, n)
+    k = [20, 40, 50][case]
+    sol = R.solve_system(m, 1e-2, b, R.MethodSpec(kind=R.FGMRES_TWOLEVEL, levels=[kmeans_level(k)],
+                                                  solver=R.SolverConfig(1e-10, 400)))
+    ref = orc.solve(om, 1e-2, b, "fgmres_twolevel", levels=[dict(target_size=k)], tol=1e-10, max_iters=400)
+    assert sol.report.converged == ref.converged
+    assert abs(sol.report.iterations - ref.iterations) <= 2, (sol.report.iterations, ref.iterations)
+    assert rel_diff(sol.w, ref.w) <= W_TOL, rel_diff(sol.w, ref.w)
+    assert len(sol.report.inner_iterations) == sol.report.iterations
+    assert np.all(sol.report.inner_iterations == 0)  # direct coarse solve
+
+
+def test_fgmres_edges(gpu, orc):
+    x = random_matrix(200, 60, 3, 0.4)
+    m = dm(x)
+    spec = R.MethodSpec(kind=R.FGMRES_TWOLEVEL, levels=[kmeans_level(10)], solver=R.SolverConfig(1e-12, 5))
+    pm = R.PreparedMethod(m, 0.1, spec)
+    w, rep = pm.solve(np.zeros(200))  # zero rhs: converged at 0 iterations, w = 0
+    assert rep.converged and rep.iterations == 0 and not np.any(w)
+    b = orc.normals(4, 200)
+    w, rep = pm.solve(b)  # max_iters cut-off: least-squares iterate, not converged
+    ref = orc.solve(to_checker(orc, x), 0.1, b, "fgmres_twolevel", levels=[dict(target_size=10)], tol=1e-12,
+                    max_iters=5)
+    assert not rep.converged and rep.iterations == 5 and rel_diff(w, ref.w) <= 1e-10
+    bad = b.copy()
+    bad[3] = np.nan
+    with pytest.raises(ValueError):
+        pm.solve(bad)
+    with pytest.raises(ValueError):  # two-level method requires one level spec
+        R.PreparedMethod(m, 0.1, R.MethodSpec(kind=R.FGMRES_TWOLEVEL))

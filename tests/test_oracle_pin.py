@@ -143,3 +143,23 @@ def test_oracle_equals_reference_build(orc, ref, seed):
     so = orc.solve(mo, 1e-3, b, "jacobi_cg", tol=1e-10, max_iters=500)
     sr = ref.solve(mr, 1e-3, b, "jacobi_cg", tol=1e-10, max_iters=500)
     assert so.iterations == sr.iterations and np.array_equal(so.w, sr.w)
+
+
+@pytest.mark.parametrize("seed", [5, 19])
+def test_fgmres_restatement_equals_reference_build(orc, ref, seed):
+    """fgmres (krylov.cpp:229-328) with the two-level preconditioner: the
+    sequential restatement reproduces the reference build bit for bit
+    (iterations, residual history, inner counts, w)."""
+    x = random_matrix(300, 120, seed, 0.3)
+    mo, mr = to_checker(orc, x), to_checker(ref, x)
+    b = ref.normals(seed, 300)
+    lv = [dict(clustering_kind=oracle.CLUSTER_KMEANS, target_size=20)]
+    so = orc.solve(mo, 0.1, b, "fgmres_twolevel", levels=lv, tol=1e-10, max_iters=200)
+    sr = ref.solve(mr, 0.1, b, "fgmres_twolevel", levels=lv, tol=1e-10, max_iters=200)
+    assert so.converged and so.iterations == sr.iterations
+    assert np.array_equal(so.residual_history, sr.residual_history)
+    assert np.array_equal(so.w, sr.w)
+    # the max_iters cut-off returns the least-squares iterate, not converged
+    so = orc.solve(mo, 0.1, b, "fgmres_twolevel", levels=lv, tol=1e-14, max_iters=5)
+    sr = ref.solve(mr, 0.1, b, "fgmres_twolevel", levels=lv, tol=1e-14, max_iters=5)
+    assert not so.converged and so.iterations == 5 and np.array_equal(so.w, sr.w)
