@@ -10,6 +10,7 @@
 
 #include "runtime.cuh"
 #include "fgmres.cuh"
+#include "kmeans_gpu.hpp"
 
 namespace rmg {
 
@@ -808,7 +809,7 @@ void KrylovWork::set_params(double tol, uint64_t max_iters_, int keep_m, cudaStr
 // ------------------------------------------------------------------ Method
 namespace {
 
-std::vector<int64_t> run_clustering(const HostCsr& cur, const LevelSpecHost& ls, int64_t* nc) {
+std::vector<int64_t> run_clustering(const HostCsr& cur, const LevelSpecHost& ls, int64_t* nc, cudaStream_t stream) {
   const rmg_level_spec& s = ls.spec;
   if (s.clustering_kind == RMG_CLUSTER_IMPORTED) {
     if (static_cast<int64_t>(ls.labels.size()) != cur.f)
@@ -823,9 +824,15 @@ std::vector<int64_t> run_clustering(const HostCsr& cur, const LevelSpecHost& ls,
   switch (s.clustering_kind) {
     case RMG_CLUSTER_LEADER_TOLERANCE: c = leader_follower(cols, s.tolerance); break;
     case RMG_CLUSTER_LEADER_TARGET: c = leader_follower_target(cols, static_cast<int64_t>(s.target_size)); break;
-    case RMG_CLUSTER_KMEANS:
-      c = kmeans(cols, static_cast<int64_t>(s.target_size), s.kmeans_max_iters, s.seed, threads);
+    case RMG_CLUSTER_KMEANS: {
+      const int64_t k = static_cast<int64_t>(s.target_size);
+      if (std::getenv("RMG_KMEANS_HOST") == nullptr && k >= 1 && k <= cols.n &&
+          kmeans_gpu_supported(src.n, src.f, k, src.nnz()))
+        c = kmeans_gpu(stream, cols, src, k, s.kmeans_max_iters, s.seed);  // bit-identical labels
+      else
+        c = kmeans(cols, k, s.kmeans_max_iters, s.seed, threads);
       break;
+    }
     default: throw InvalidArgument("unknown clustering kind " + std::to_string(s.clustering_kind));
   }
   *nc = c.n_clusters;
@@ -888,14 +895,24 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     throw InvalidArgument("build_hierarchy: the coarsest level must use direct_cholesky");
 
   // levels (krylov.cpp:512-530)
+  const bool slog = std::getenv("RMG_SETUP_LOG") != nullptr;  // setup phase timings on stderr
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tlog = [&](const char* what, uint64_t k, std::chrono::steady_clock::time_point t0) {
+    if (slog)
+      std::fprintf(stderr, "[rmg setup] level %llu %-12s %8.3f s\n", static_cast<unsigned long long>(k), what,
+                   std::chrono::duration<double>(tnow() - t0).count());
+  };
   double beta_run = beta;
   for (uint64_t k = 0; k < L; ++k) {
+    auto t0 = tnow();
     const HostCsr& cur = level_matrix(k).host;
     if (levels[k].clustering_kind == RMG_CLUSTER_IMPORTED)
       specs_[k].labels.assign(levels[k].labels, levels[k].labels + cur.f);
     const double next_beta = specs_[k].spec.has_beta_override ? specs_[k].spec.beta_override : beta_run;
     int64_t nc = 0;
-    std::vector<int64_t> lab = run_clustering(cur, specs_[k], &nc);
+    std::vector<int64_t> lab = run_clustering(cur, specs_[k], &nc, s);
+    tlog("clustering", k, t0);
+    t0 = tnow();
     if (nc >= cur.f)
       throw InvalidArgument("build_hierarchy: level " + std::to_string(k + 1) + " has " + std::to_string(nc) +
                             " clusters, not smaller than its fine level (" + std::to_string(cur.f) + " features)");
@@ -921,6 +938,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     labels_.push_back(std::move(lab));
     coarse_.push_back(std::move(lvl));
     beta_run = next_beta;
+    tlog("coarsen", k, t0);
   }
   const int64_t fc_last = coarse_.back()->mat->f();
   if (fc_last > 4096)  // kDirectSolveCap, krylov.hpp:170
@@ -936,11 +954,14 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     }
     uint64_t its;
     bool cv;
+    const auto t0 = tnow();
     const double lmax = level_matrix(k).lambda_max(1e-4, 200, 0x5eed + k, &its, &cv);
     omega_.push_back(2.0 / (level_beta(k) + lmax));
+    tlog("lambda_max", k, t0);
   }
   // coarsest dense solve (krylov.cpp:349-376), through A_c^{-1}
   {
+    auto t0 = tnow();
     const std::vector<double> ac = coarse_gram(coarse_.back()->mat->host, coarse_.back()->beta);
     const std::vector<double> inv =
         spd_inverse(ac, fc_last, "level " + std::to_string(L - 1) + " -> " + std::to_string(L));
@@ -961,9 +982,14 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       work_.push_back(
           std::make_unique<KrylovWork>(level_matrix(k).f(), keep, sp.coarse_max_iters, sp.coarse_tol, s));
     }
+    tlog("coarsest_inv", L, t0);
+    t0 = tnow();
     build_dense_levels(inv);
+    tlog("dense_levels", L, t0);
+    t0 = tnow();
     for (size_t k = 1; k < dense_.size(); ++k)
       if (dense_[k]) tune_dense_partials(k);
+    tlog("tune", L, t0);
   }
   ctx_->sync();
 }
