@@ -587,3 +587,93 @@ def solve_system(x: DeviceMatrix, beta: float, b, spec: MethodSpec) -> SystemSol
         return SystemSolution(w, rep, pm.coarse_size())
     finally:
         pm.close()
+
+
+# ---------------------------------------------------------------- bench harness (analysis.cpp:137-223)
+METHOD_STRINGS = {v: k for k, v in METHOD_NAMES.items()}
+
+
+def clustering_description(spec: "MethodSpec", coarse_size: int) -> str:
+    """describe_clustering (krylov.cpp:596-612); C++ ostream default formatting."""
+    if not spec.levels:
+        return ""
+    c = spec.levels[0].clustering
+    if c.kind == LEADER_TOLERANCE:
+        return f"lf(tol={c.tolerance:g},fc={coarse_size})"
+    if c.kind == LEADER_TARGET:
+        return f"lf(fc={coarse_size})"
+    if c.kind == KMEANS:
+        return f"km(k={coarse_size})"
+    return f"imported(fc={coarse_size})"
+
+
+@dataclass
+class BenchRow:
+    """analysis.hpp BenchRow: one (method, beta, tol) measurement."""
+    dataset: str
+    method: str
+    clustering: str = ""
+    f_c: int = 0
+    beta: float = 0.0
+    tol: float = 0.0
+    iterations: int = 0
+    wall_time_s: float = 0.0
+    speedup: float = 0.0
+
+
+def compare_methods(x: DeviceMatrix, dataset_name: str, beta_grid, tol_grid, methods, n_repeats: int = 1,
+                    rhs_seed: int = 42) -> list:
+    """compare_methods (analysis.cpp:137-198): for every (beta, tol), CG is always
+    measured (max_iters = max(20000, 4 F)) as the speed-up denominator; each method
+    is prepared once and solved n_repeats times for the rhs of generate_rhs(rhs_seed);
+    times are the solver's own wall_time_s (setup excluded), averaged."""
+    beta_grid, tol_grid, methods = list(beta_grid), list(tol_grid), list(methods)
+    if not beta_grid or not tol_grid:
+        raise ValueError("compare_methods: beta and tol grids must be non-empty")
+    if not methods:
+        raise ValueError("compare_methods: method list must be non-empty")
+    if n_repeats < 1:
+        raise ValueError("compare_methods: n_repeats must be >= 1")
+    b = generate_rhs(x, rhs_seed).b
+    rows = []
+    for beta in beta_grid:
+        for tol in tol_grid:
+            base = MethodSpec(kind=CG, solver=SolverConfig(tol, max(20000, x.n_features * 4)))
+            pcg = PreparedMethod(x, beta, base)
+            cg_time, cg_rep = 0.0, None
+            for _ in range(n_repeats):
+                _, cg_rep = pcg.solve(b)
+                cg_time += cg_rep.wall_time_s
+            cg_time /= n_repeats
+            pcg.close()
+            for m in methods:
+                spec = MethodSpec(kind=m.kind, levels=m.levels,
+                                  solver=SolverConfig(tol, m.solver.max_iters, m.solver.truncation))
+                row = BenchRow(dataset_name, METHOD_STRINGS[spec.kind], beta=beta, tol=tol)
+                if spec.kind == CG:
+                    row.iterations, row.wall_time_s, row.speedup = cg_rep.iterations, cg_time, 1.0
+                    rows.append(row)
+                    continue
+                pm = PreparedMethod(x, beta, spec)
+                t, rep = 0.0, None
+                for _ in range(n_repeats):
+                    _, rep = pm.solve(b)
+                    t += rep.wall_time_s
+                t /= n_repeats
+                row.clustering = clustering_description(spec, pm.coarse_size())
+                row.f_c = pm.coarse_size()
+                row.iterations = rep.iterations
+                row.wall_time_s = t
+                row.speedup = cg_time / t if t > 0.0 else 0.0
+                pm.close()
+                rows.append(row)
+    return rows
+
+
+def to_csv(rows) -> str:
+    """to_csv (analysis.cpp:200-212): the reference's header, ostream precision 12."""
+    out = ["dataset,method,clustering,f_c,beta,tol,iterations,wall_time_s,speedup"]
+    for r in rows:
+        out.append(f"{r.dataset},{r.method},{r.clustering},{r.f_c},{r.beta:.12g},{r.tol:.12g},{r.iterations},"
+                   f"{r.wall_time_s:.12g},{r.speedup:.12g}")
+    return "\n".join(out) + "\n"
