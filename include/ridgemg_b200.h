@@ -149,6 +149,12 @@ int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device);
 int rmg_spmv_transpose(rmg_matrix* m, const double* u, double* y, int32_t on_device);
 /* out = X^T X w + beta w   (RidgeOperator::apply, ridge.cpp:16-24) */
 int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, int32_t on_device);
+/* k right-hand sides at once (BASELINE cfg 3's block operator, no reference
+ * counterpart: the reference applies RidgeOperator once per vector):
+ * out = X^T (X V) + beta V with V, out row-major n_features x k, 1 <= k <= 64;
+ * column q equals rmg_ridge_apply of column q up to summation order.  Single-GPU
+ * CSR matrices. */
+int rmg_ridge_apply_block(rmg_matrix* m, double beta, const double* v, double* out, uint64_t k, int32_t on_device);
 /* d_j = beta + ||X(:,j)||^2 (gram_diagonal, ridge.cpp:30-37) */
 int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device);
 /* largest eigenvalue of X^T X by power iteration (estimate_lambda_max, krylov.cpp:62-92) */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "rmg_spmv": [_P, _P, _P, _I32],
     "rmg_spmv_transpose": [_P, _P, _P, _I32],
     "rmg_ridge_apply": [_P, _D, _P, _P, _I32],
+    "rmg_ridge_apply_block": [_P, _D, _P, _P, _U64, _I32],
     "rmg_gram_diagonal": [_P, _D, _P, _I32],
     "rmg_lambda_max": [_P, _D, _U64, _U64, _P, _P, _P],
     "rmg_generate_rhs": [_P, _U64, _P, _P],

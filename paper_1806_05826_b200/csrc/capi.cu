@@ -383,6 +383,20 @@ int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, in
   });
 }
 
+int rmg_ridge_apply_block(rmg_matrix* m, double beta, const double* v, double* out, uint64_t k, int32_t on_device) {
+  return guard([&] {
+    need(m, "matrix");
+    rmg::Context& c = *m->m.ctx;
+    RMG_CK(cudaSetDevice(c.device));
+    const size_t cnt = static_cast<size_t>(m->m.f()) * k;
+    rmg::DBuf<double> bi, bo;
+    const double* dv = stage_in(c, v, cnt, on_device, bi);
+    double* dout = stage_out(cnt, on_device, out, bo);
+    m->m.apply_block(dv, dout, beta, static_cast<int>(k));
+    finish_out(c, dout, out, cnt, on_device);
+  });
+}
+
 int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");

@@ -246,6 +246,131 @@ __global__ void __launch_bounds__(NT) k_spmv_rows(const int32_t* __restrict__ pt
   }
 }
 
+// ------------------------------------------------------------------ block operator (cfg 3)
+// Columns are processed in chunks of up to 16 (c0 .. c0 + kc) of row-major
+// blocks with leading dimension k.
+constexpr int kBlockCols = 16;
+
+__global__ void __launch_bounds__(kThreads) k_vperm_block(const double* __restrict__ v, const int32_t* __restrict__ inv,
+                                                          double* __restrict__ vp, int64_t cols, int k) {
+  const int64_t total = cols * k;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t j = e / k, q = e - j * k;
+    vp[e] = __ldg(v + (int64_t)inv[j] * k + q);
+  }
+}
+
+// T[row][c0 + q] = sum over the row's elements of x * V[col][c0 + q].  A
+// half-warp per row, lane q owning column q: every gathered row of V is one
+// coalesced access (2 lines per warp instruction), and each lane sums its
+// column in the row's element order (the single-vector K1's order).  A warp
+// walks its SELL slice two rows at a time; element loads run 4 ahead.
+template <bool PAT, bool NARROW>
+__global__ void __launch_bounds__(kThreads) k_spmm_sell(const int32_t* __restrict__ off,
+                                                        const int32_t* __restrict__ srow,
+                                                        const int32_t* __restrict__ slen,
+                                                        const int32_t* __restrict__ idx,
+                                                        const uint16_t* __restrict__ idx16,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ V, double* __restrict__ T,
+                                                        int64_t n_slices, int k, int c0, int kc) {
+  const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
+  const bool colq = q < kc;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t sl = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; sl < n_slices; sl += nwarps) {
+    const int64_t base = off[sl];
+    for (int p = 0; p < 16; ++p) {
+      const int slot = 2 * p + h;
+      const int row = srow[sl * 32 + slot];
+      const int len = slen[sl * 32 + slot];
+      const int lmax = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
+      double acc = 0.0;
+      for (int j = 0; j < lmax; j += 16) {
+        int c[16];
+        double x[16], vv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const bool ok = j + u < len;
+          const int64_t e = base + (int64_t)(j + u) * 32 + slot;
+          c[u] = ok ? (NARROW ? (int)idx16[e] : idx[e]) : -1;
+          x[u] = (ok && !PAT) ? val[e] : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) vv[u] = (c[u] >= 0 && colq) ? __ldg(V + (int64_t)c[u] * k + c0 + q) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (c[u] >= 0) acc += PAT ? vv[u] : x[u] * vv[u];
+      }
+      if (row >= 0 && colq) T[(int64_t)row * k + c0 + q] = acc;
+    }
+  }
+}
+
+// X^T pass over a block: a half-warp per unit of work, lane q owning column q,
+// elements in order.  Units: the rows with <= 4096 nonzeros (whole rows), then
+// the items of longer rows (segment partials for k_block_finish).
+template <bool PAT>
+__global__ void __launch_bounds__(kThreads) k_xt_block(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                                       const double* __restrict__ val, BlockXtSchedule bs,
+                                                       const double* __restrict__ T, const double* __restrict__ V,
+                                                       double* __restrict__ out, double beta, int k, int c0, int kc) {
+  const int lane = threadIdx.x & 31, q = lane & 15;
+  const bool colq = q < kc;
+  const int64_t unit = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 4;
+  const int64_t n_units = (int64_t)bs.n_short + bs.n_items;
+  if (unit >= n_units) return;
+  int row, e0, e1, seg;
+  if (unit < bs.n_short) {
+    row = bs.short_rows[unit];
+    e0 = ptr[row];
+    e1 = ptr[row + 1];
+    seg = -1;
+  } else {
+    const int4 it = bs.items[unit - bs.n_short];
+    row = it.x;
+    e0 = it.y;
+    e1 = it.z;
+    seg = it.w;
+  }
+  double acc = 0.0;
+  for (int e = e0; e < e1; e += 8) {
+    int smp[8];
+    double x[8], tv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = e + u < e1;
+      smp[u] = ok ? idx[e + u] : -1;
+      x[u] = (ok && !PAT) ? val[e + u] : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tv[u] = (smp[u] >= 0 && colq) ? __ldg(T + (int64_t)smp[u] * k + c0 + q) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (smp[u] >= 0) acc += PAT ? tv[u] : x[u] * tv[u];
+  }
+  if (!colq) return;
+  if (seg < 0)
+    out[(int64_t)row * k + c0 + q] = acc + beta * V[(int64_t)row * k + c0 + q];
+  else
+    bs.seg[(int64_t)seg * kBlockCols + q] = acc;
+}
+
+// rows split into several items: warp per row, lanes over the items
+// (lane-strided, fixed order) + warp tree, for each column
+__global__ void k_block_finish(BlockXtSchedule bs, const double* __restrict__ V, double* __restrict__ out,
+                               double beta, int k, int c0, int kc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= bs.n_multi) return;
+  const int4 m = bs.multi[w];
+  for (int q = 0; q < kc; ++q) {
+    double sum = 0.0;
+    for (int g = lane; g < m.z; g += 32) sum += bs.seg[(int64_t)(m.y + g) * kBlockCols + q];
+    sum = warp_sum(sum);
+    if (lane == 0) out[(int64_t)m.x * k + c0 + q] = sum + beta * V[(int64_t)m.x * k + c0 + q];
+  }
+}
+
 // ------------------------------------------------------------------ K2 hot part (hybrid X^T pass)
 constexpr int kHotThreads = 1024;  // 2 CTAs x 32 warps per SM: latency hiding for SMEM gathers
 // One CTA per sample block b: t[b*B, b*B + B) is staged in SMEM (coalesced,
@@ -1416,6 +1541,45 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
   dense_finish(d, Epi::Plain, a, s);
   k_add_const<<<grid_for(d.cols, 148), kThreads, 0, s>>>(out, beta, d.cols);
   check_launch("dense_diag");
+}
+
+
+void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule& bs, const double* v,
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
+  if (x.rows == 0 || x.cols == 0 || k <= 0) return;
+  if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
+  const double* vk = v;
+  if (x.col_inv != nullptr) {  // relabeled columns: V rows into label order
+    k_vperm_block<<<grid_for(x.cols * k, 148 * 8), kThreads, 0, s>>>(v, x.col_inv, vp, x.cols, k);
+    vk = vp;
+  }
+  const int g1 = grid_for(x.n_slices * 32, 148 * 8);
+  const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
+  const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
+  for (int c0 = 0; c0 < k; c0 += kBlockCols) {
+    const int kc = std::min(kBlockCols, k - c0);
+    if (x.val == nullptr) {
+      if (x.idx16 != nullptr)
+        k_spmm_sell<true, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
+                                                        t, x.n_slices, k, c0, kc);
+      else
+        k_spmm_sell<true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
+                                                         t, x.n_slices, k, c0, kc);
+      k_xt_block<true><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc);
+    } else {
+      if (x.idx16 != nullptr)
+        k_spmm_sell<false, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
+                                                         t, x.n_slices, k, c0, kc);
+      else
+        k_spmm_sell<false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val,
+                                                          vk, t, x.n_slices, k, c0, kc);
+      k_xt_block<false><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc);
+    }
+    if (bs.n_multi > 0)
+      k_block_finish<<<static_cast<int>((static_cast<int64_t>(bs.n_multi) * 32 + 255) / 256), 256, 0, s>>>(
+          bs, v, out, beta, k, c0, kc);
+  }
+  check_launch("ridge_block");
 }
 
 }  // namespace rmg

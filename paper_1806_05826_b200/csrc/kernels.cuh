@@ -143,6 +143,19 @@ struct DenseDev {
 };
 constexpr int kDenseMaxCols = 1024;  // 32 register partials per lane
 
+// Block operator (BASELINE cfg 3: k right-hand sides as one SpMM; DESIGN.md
+// §4.8): V, T and out are row-major blocks (F x k, N x k, F x k), so every
+// gathered row of V or T is k contiguous doubles (one 128 B line at k = 16).
+struct BlockXtSchedule {
+  const int32_t* short_rows = nullptr;  // rows of X^T with <= 4096 nonzeros: one unit each
+  int n_short = 0;
+  const int4* items = nullptr;          // (row, k0, k1, seg) items of longer rows
+  int n_items = 0;
+  const int4* multi = nullptr;          // (row, first_seg, n_seg, -) rows split into several items
+  int n_multi = 0;
+  double* seg = nullptr;                // [n_items x 16] segment partials (seg >= 0)
+};
+
 // ---------------------------------------------------------------- launchers
 void launch_spmv_rows(const SparseDev& x, const double* v, double* t, const int32_t* done,
                       cudaStream_t s);
@@ -157,6 +170,11 @@ void launch_dense_ata(const DenseDev& d, const double* v, int ring_stride, const
 void launch_dense_spmv(const DenseDev& d, const double* v, double* y, cudaStream_t s);
 void launch_dense_xt(const DenseDev& d, const double* u, Epi epi, const XtArgs& a, cudaStream_t s);
 void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t s);
+// out = X^T (X V) + beta V for a row-major F x k block (k <= 64); x: the K1
+// layout (SELL), xt: X^T CSR (int32 sample indices), t: N x k scratch, vp:
+// F x k scratch (relabeled columns).  Per column the arithmetic order is fixed.
+void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule& bs, const double* v,
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

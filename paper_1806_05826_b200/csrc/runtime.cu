@@ -489,6 +489,52 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   }
 }
 
+// Block operator schedule: rows of X^T with <= 512 nonzeros
+// are one unit each (a half-warp, elements in order); longer rows are split
+// into items of 512 whose partials are finished in item order.
+void Matrix::build_block_schedule(const HostCsr& ht) {
+  constexpr int64_t kItem = 512;  // a half-warp walks <= 512 elements (latency-bound chains)
+  std::vector<int32_t> sh;
+  std::vector<int4> it, mu;
+  int segs = 0;
+  for (int64_t r = 0; r < ht.n; ++r) {
+    const int64_t a = ht.ptr[r], e = ht.ptr[r + 1], len = e - a;
+    if (len <= kItem) {
+      sh.push_back(static_cast<int32_t>(r));
+    } else {
+      const int first = segs;
+      for (int64_t b = a; b < e; b += kItem)
+        it.push_back(make_int4(static_cast<int>(r), static_cast<int>(b), static_cast<int>(std::min(e, b + kItem)),
+                               segs++));
+      mu.push_back(make_int4(static_cast<int>(r), first, segs - first, 0));
+    }
+  }
+  cudaStream_t s = ctx->stream;
+  bshort.upload(sh.data(), sh.size(), s);
+  bitems.upload(it.data(), it.size(), s);
+  bmulti.upload(mu.data(), mu.size(), s);
+  bseg.alloc(static_cast<size_t>(std::max(1, segs)) * 16);
+  RMG_CK(cudaStreamSynchronize(s));
+  bview.short_rows = bshort.get();
+  bview.n_short = static_cast<int>(sh.size());
+  bview.items = bitems.get();
+  bview.n_items = static_cast<int>(it.size());
+  bview.multi = bmulti.get();
+  bview.n_multi = static_cast<int>(mu.size());
+  bview.seg = bseg.get();
+}
+
+void Matrix::apply_block(const double* v, double* out, double beta, int k) {
+  if (dense || comm != nullptr) throw InvalidArgument("block operator: single-GPU CSR matrices only");
+  if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
+  if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative");
+  const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
+  if (bt.size() < nt) bt.alloc(nt);
+  if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
+  launch_ridge_block(x.view, xt.view, bview, v, out, beta, k, bt.get(), bvp.get(), ctx->stream);
+  ctx->sync();
+}
+
 Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din)
     : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
@@ -585,6 +631,7 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
     xt.upload(ht, pattern, ctx->stream, false);
     sched.build(ht, ctx->stream, local.f, 1, 0);
     build_hot(ht, local.n);
+    build_block_schedule(ht);
   }
   t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);

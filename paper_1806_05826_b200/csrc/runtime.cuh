@@ -177,6 +177,14 @@ struct Matrix {
   int fin_grid = 1;
   std::unique_ptr<HotXt> hot;  // hybrid X^T pass when N is large (nullptr otherwise)
   std::unique_ptr<DenseStore> dense;  // dense inputs: X row-major on the device, no CSR copies
+  // block operator (cfg 3): schedule of the X^T pass over row-major F x k blocks
+  BlockXtSchedule bview;
+  DBuf<int32_t> bshort;
+  DBuf<int4> bitems, bmulti;
+  DBuf<double> bseg, bt, bvp;  // + scratch T (N x k) and permuted V (F x k), kept across calls
+  void build_block_schedule(const HostCsr& ht);
+  // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
+  void apply_block(const double* v, double* out, double beta, int k);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
   void build_hot(const HostCsr& ht, int64_t n_samples);
   int64_t n_local() const { return row1 - row0; }

@@ -325,6 +325,15 @@ class DeviceMatrix:
             raise ValueError(f"length {a.shape[0] if a.ndim else 0}, expected {n}")
         return a
 
+    def ridge_apply_block(self, beta: float, v) -> np.ndarray:
+        """X^T (X V) + beta V for V of shape (n_features, k), k <= 64 (cfg 3's block operator)."""
+        v = np.ascontiguousarray(v, np.float64)
+        if v.ndim != 2 or v.shape[0] != self.n_features:
+            raise ValueError("ridge_apply_block: V must be (n_features, k)")
+        out = np.zeros_like(v)
+        _lib.check(self.lib.rmg_ridge_apply_block(self.h, beta, _ptr(v), _ptr(out), v.shape[1], 0))
+        return out
+
     def hybrid_hot_features(self) -> int:
         """Hot features of the hybrid X^T pass (0: plain segmented pass)."""
         h = C.c_uint64()

@@ -1,0 +1,45 @@
+"""Block operator (BASELINE cfg 3's k right-hand sides as one SpMM; DESIGN.md
+§4.8): every column of X^T (X V) + beta V equals the single-vector operator
+(and the oracle) up to summation order."""
+import numpy as np
+import pytest
+
+import paper_1806_05826_b200 as R
+from helpers import rel_diff, to_checker
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("values", [False, True])
+@pytest.mark.parametrize("k", [1, 5, 16, 23, 40])
+def test_block_matches_columns(gpu, orc, values, k):
+    x = R.synth_sparse_zipf(6000, 900, 18.0, 1.1, values, 3)  # long Zipf rows: multi-item X^T rows
+    m = R.DeviceMatrix(x, R.default_context())
+    v = np.random.default_rng(k).standard_normal((x.n_features, k))
+    out = m.ridge_apply_block(0.7, v)
+    om = to_checker(orc, x)
+    for q in range(k):
+        want = orc.ridge_apply(om, 0.7, v[:, q].copy())
+        assert rel_diff(out[:, q], want) <= 1e-13, (q, rel_diff(out[:, q], want))
+
+
+def test_block_relabeled_wide(gpu, orc):
+    """F = 30000 > 24576: K1 runs on popularity-relabeled columns (V rows permuted)."""
+    x = R.synth_sparse_zipf(20000, 30000, 12.0, 1.05, True, 8)
+    m = R.DeviceMatrix(x, R.default_context())
+    v = np.random.default_rng(2).standard_normal((x.n_features, 16))
+    out = m.ridge_apply_block(0.0, v)
+    for q in (0, 7, 15):
+        assert rel_diff(out[:, q], m.ridge_apply(0.0, v[:, q].copy())) <= 1e-13
+
+
+def test_block_errors(gpu):
+    x = R.synth_sparse_zipf(500, 60, 5.0, 1.1, False, 1)
+    m = R.DeviceMatrix(x, R.default_context())
+    with pytest.raises(ValueError):
+        m.ridge_apply_block(0.1, np.zeros((60, 65)))
+    with pytest.raises(ValueError):
+        m.ridge_apply_block(-1.0, np.zeros((60, 4)))
+    d = R.DeviceMatrix.from_dense(np.ones((10, 4)))
+    with pytest.raises(ValueError):
+        d.ridge_apply_block(0.1, np.zeros((4, 2)))
