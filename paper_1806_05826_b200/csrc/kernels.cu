@@ -519,25 +519,16 @@ __device__ __forceinline__ void xt_finalize(KrylovScalars* sc, double s0, double
   }
 }
 
-// Gather index of element k of virtual row vrow: sample-blocked layout keeps
-// uint16 offsets inside a block of B samples.
-template <bool BLK>
-__device__ __forceinline__ int xt_col(const XtSchedule& sch, const int32_t* __restrict__ idx, int64_t base, int k) {
-  if constexpr (BLK) return (int)(base + ld_stream(sch.idx16 + k));
-  return ld_stream(idx + k);
-}
-
 // Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 4 elements per
 // lane per round (independent loads in flight); lane-strided order.
-template <bool PAT, bool BLK>
-__device__ __forceinline__ double xt_row_sum(const XtSchedule& sch, const int32_t* __restrict__ idx,
-                                             const double* __restrict__ val, const double* __restrict__ t,
-                                             int64_t base, int k0, int k1, int lane, int lanes) {
+template <bool PAT>
+__device__ __forceinline__ double xt_row_sum(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                             const double* __restrict__ t, int k0, int k1, int lane, int lanes) {
   double s = 0.0;
   for (int k = k0 + lane; k < k1; k += 4 * lanes) {
     int c[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) c[u] = k + u * lanes < k1 ? xt_col<BLK>(sch, idx, base, k + u * lanes) : -1;
+    for (int u = 0; u < 4; ++u) c[u] = k + u * lanes < k1 ? ld_stream(idx + k + u * lanes) : -1;
     double x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
@@ -550,9 +541,8 @@ __device__ __forceinline__ double xt_row_sum(const XtSchedule& sch, const int32_
 
 // K2: one work item per CTA (see XtSchedule).  Short rows take W lanes, medium
 // rows a full warp, long rows fixed CTA-wide segments combined in segment
-// order by the last-arriving CTA.  Unblocked: the epilogue runs here.  Blocked
-// (BLK): writes per-block partials (E == Plain), k_xt_finish does the rest.
-template <int W, bool PAT, Epi E, bool BLK>
+// order by the last-arriving CTA.  The epilogue runs here.
+template <int W, bool PAT, Epi E>
 __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr,
                                                  const int32_t* __restrict__ idx,
                                                  const double* __restrict__ val, XtSchedule sch,
@@ -587,8 +577,7 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
       double s = 0.0;
       if (q < item.y) {
         vrow = sch.perm[q];
-        const int64_t base = BLK ? (int64_t)(vrow / F) * sch.block_rows : 0;
-        s = xt_row_sum<PAT, BLK>(sch, idx, val, t, base, ptr[vrow], ptr[vrow + 1], lane, lanes);
+        s = xt_row_sum<PAT>(idx, val, t, ptr[vrow], ptr[vrow + 1], lane, lanes);
       }
       if (medium) {
         s = warp_sum(s);
@@ -608,8 +597,7 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
   } else {
     // one fixed segment [item.y, item.z) of long row long_col[item.x]
     const int vrow = sch.long_col[item.x];
-    const int64_t base = BLK ? (int64_t)(vrow / F) * sch.block_rows : 0;
-    double s = xt_row_sum<PAT, BLK>(sch, idx, val, t, base, item.y, item.z, threadIdx.x, kThreads);
+    double s = xt_row_sum<PAT>(idx, val, t, item.y, item.z, threadIdx.x, kThreads);
     s = block_sum(s, sh);
     if (threadIdx.x == 0) {
       sch.seg_partial[item.w] = s;
@@ -640,8 +628,8 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
   }
 }
 
-// Sample-blocked X^T finishing pass: s_j = sum over blocks (in block order) of
-// the partials, then the epilogue and the deterministic dot reduction.
+// Epilogue pass over precomputed sums s_j (sharded: after the all-reduce;
+// hybrid: hot + cold parts), with the deterministic dot reduction.
 template <Epi E>
 __global__ void __launch_bounds__(kThreads) k_xt_finish(XtSchedule sch, XtArgs a) {
   if (a.done != nullptr && *a.done) return;
@@ -659,9 +647,7 @@ __global__ void __launch_bounds__(kThreads) k_xt_finish(XtSchedule sch, XtArgs a
   const int64_t F = sch.features;
   double d0 = 0.0, d1 = 0.0;
   for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < F; j += (int64_t)gridDim.x * kThreads) {
-    double s = 0.0;
-    for (int b = 0; b < sch.n_blocks; ++b) s += sch.partial[(size_t)b * F + j];
-    xt_epilogue<E>((int)j, s, a, v, out, d0, d1);
+    xt_epilogue<E>((int)j, sch.partial[j], a, v, out, d0, d1);
   }
   if constexpr (has_dots<E>()) {
     const double b0 = block_sum(d0, sh);
@@ -1170,15 +1156,12 @@ __global__ void k_scale_by_lambda(const double* __restrict__ w, double* __restri
 // d_j = beta + sum_r X(r,j)^2 in increasing r (ridge.cpp:30-37 storage order)
 template <bool PAT>
 __global__ void k_diag_gram(const int32_t* __restrict__ ptr, const double* __restrict__ val, int64_t f,
-                            int n_blocks, double beta, double* __restrict__ out) {
+                            double beta, double* __restrict__ out) {
   grid_stride(f, [&](int64_t j) {
     double d = beta;
-    for (int b = 0; b < n_blocks; ++b) {  // sample blocks in order = increasing sample
-      const int64_t row = (int64_t)b * f + j;
-      for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
-        const double x = PAT ? 1.0 : val[k];
-        d = __dadd_rn(d, __dmul_rn(x, x));  // uncontracted: bit-equal to ridge.cpp:34
-      }
+    for (int k = ptr[j]; k < ptr[j + 1]; ++k) {
+      const double x = PAT ? 1.0 : val[k];
+      d = __dadd_rn(d, __dmul_rn(x, x));  // uncontracted: bit-equal to ridge.cpp:34
     }
     out[j] = d;
   });
@@ -1296,32 +1279,17 @@ void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* 
 template <int W, bool PAT>
 void xt_impl_w(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
   const dim3 grid(sch.n_items), block(kThreads);
-  if (sch.blocked) {  // per-block partials, then the finishing epilogue pass
-    XtArgs pa = a;
-    pa.out = sch.partial;
-    k_xt<W, PAT, Epi::Plain, true><<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, pa);
-    const dim3 fg(sch.fin_grid);
-    switch (epi) {
-      case Epi::Plain: k_xt_finish<Epi::Plain><<<fg, block, 0, s>>>(sch, a); break;
-      case Epi::Axpby: k_xt_finish<Epi::Axpby><<<fg, block, 0, s>>>(sch, a); break;
-      case Epi::Fcg: k_xt_finish<Epi::Fcg><<<fg, block, 0, s>>>(sch, a); break;
-      case Epi::Cg: k_xt_finish<Epi::Cg><<<fg, block, 0, s>>>(sch, a); break;
-      case Epi::Rich: k_xt_finish<Epi::Rich><<<fg, block, 0, s>>>(sch, a); break;
-      case Epi::Gram: k_xt_finish<Epi::Gram><<<fg, block, 0, s>>>(sch, a); break;
-    }
-    return;
-  }
   auto go = [&](auto kern) {
     prefer_l1(kern);
     kern<<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a);
   };
   switch (epi) {
-    case Epi::Plain: go(k_xt<W, PAT, Epi::Plain, false>); break;
-    case Epi::Axpby: go(k_xt<W, PAT, Epi::Axpby, false>); break;
-    case Epi::Fcg: go(k_xt<W, PAT, Epi::Fcg, false>); break;
-    case Epi::Cg: go(k_xt<W, PAT, Epi::Cg, false>); break;
-    case Epi::Rich: go(k_xt<W, PAT, Epi::Rich, false>); break;
-    case Epi::Gram: go(k_xt<W, PAT, Epi::Gram, false>); break;
+    case Epi::Plain: go(k_xt<W, PAT, Epi::Plain>); break;
+    case Epi::Axpby: go(k_xt<W, PAT, Epi::Axpby>); break;
+    case Epi::Fcg: go(k_xt<W, PAT, Epi::Fcg>); break;
+    case Epi::Cg: go(k_xt<W, PAT, Epi::Cg>); break;
+    case Epi::Rich: go(k_xt<W, PAT, Epi::Rich>); break;
+    case Epi::Gram: go(k_xt<W, PAT, Epi::Gram>); break;
   }
 }
 
@@ -1362,7 +1330,6 @@ void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtA
                         unsigned* fin_ticket, int fin_grid, cudaStream_t s) {
   XtSchedule sch;
   sch.features = features;
-  sch.n_blocks = 1;
   sch.partial = const_cast<double*>(sums);
   sch.fin_slots = fin_slots;
   sch.fin_ticket = fin_ticket;
@@ -1463,11 +1430,10 @@ void launch_scale_by_lambda(const double* w, double* v, int64_t n, const KrylovS
 
 void launch_diag_gram(const SparseDev& xt, const XtSchedule& sch, double beta, double* out, cudaStream_t s) {
   const int64_t f = sch.features;
-  const int nb = sch.blocked ? sch.n_blocks : 1;
   if (xt.val == nullptr)
-    k_diag_gram<true><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, nb, beta, out);
+    k_diag_gram<true><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, beta, out);
   else
-    k_diag_gram<false><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, nb, beta, out);
+    k_diag_gram<false><<<grid_for(f, 148 * 8), kThreads, 0, s>>>(xt.ptr, xt.val, f, beta, out);
   check_launch("diag_gram");
 }
 

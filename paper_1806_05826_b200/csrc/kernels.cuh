@@ -59,25 +59,18 @@ struct SparseDev {
   int64_t n_slices = 0;
 };
 
-// Work items for the X^T pass, by row-length class of the (virtual) X^T CSR:
+// Work items for the X^T pass, by row-length class of the X^T CSR:
 //   short : {q_begin, q_end, -1, slot}  rows perm[q_begin..q_end), W lanes each
 //   medium: {q_begin, q_end, -2, slot}  rows perm[..], one warp each
 //   long  : {long_id, nz_begin, nz_end, seg_id}  one fixed segment, whole CTA
-// With sample blocking (`blocked`), X^T is stored per block of B samples
-// (virtual row = block * F + feature, uint16 sample offsets inside the block):
-// a CTA's t-gathers stay inside one B*8-byte slice (L1 resident); the pass
-// writes per-block partials and k_xt_finish sums them in block order.
+// (The epilogue-only pass k_xt_finish reads precomputed sums from `partial`.)
 struct XtSchedule {
   const int4* items = nullptr;
-  const int32_t* perm = nullptr;  // virtual rows grouped by class (short, medium)
+  const int32_t* perm = nullptr;  // rows grouped by class (short, medium)
   int n_items = 0;
-  int blocked = 0;                // 1: sample-blocked layout
-  int64_t features = 0;           // F (virtual row -> feature = vrow % F)
-  int block_rows = 0;             // B
-  int n_blocks = 1;
-  const uint16_t* idx16 = nullptr;  // blocked: sample offset within the block
-  double* partial = nullptr;        // blocked: [n_blocks * F]
-  double* fin_slots = nullptr;      // blocked: finishing-kernel dot slots
+  int64_t features = 0;           // F
+  double* partial = nullptr;      // k_xt_finish: precomputed sums s_j
+  double* fin_slots = nullptr;    // k_xt_finish: dot slots
   unsigned* fin_ticket = nullptr;
   int fin_grid = 1;
   const int32_t* long_col = nullptr;

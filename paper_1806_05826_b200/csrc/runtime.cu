@@ -202,12 +202,11 @@ void DeviceSparse::upload_sell(const HostCsr& h, bool pattern, cudaStream_t s, b
   view.n_slices = ns;
 }
 
-// Work items over the rows of a (possibly sample-blocked, virtual) X^T CSR,
+// Work items over the rows of the X^T CSR,
 // by length class: short rows (<= 8 per lane of a W-lane group), medium rows
 // (one warp, <= 2048), long rows (fixed CTA segments).  Each CTA item holds
 // about C nonzeros, so no lane group owns a row much longer than its peers'.
-void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows,
-                           const std::vector<char>* skip) {
+void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, const std::vector<char>* skip) {
   const int64_t V = xt.n, nnz = xt.nnz();
   // ~12 items per SM: the first schedule (4 per SM) ran 0.61 waves at 29 % occupancy
   const int64_t C = std::max<int64_t>(512, std::min<int64_t>(16384, nnz / (148 * 12)));
@@ -295,44 +294,6 @@ void DeviceSchedule::build(const HostCsr& xt, cudaStream_t s, int64_t features, 
   view.width = width;
   view.perm = perm.get();
   view.features = features;
-  view.n_blocks = std::max(1, n_blocks);
-  view.block_rows = block_rows;
-  view.blocked = n_blocks > 1 ? 1 : 0;
-  if (view.blocked) {
-    partial.alloc(static_cast<size_t>(n_blocks) * std::max<int64_t>(1, features));
-    view.partial = partial.get();
-    view.fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (features + 255) / 256)));
-    fin_slots.alloc(static_cast<size_t>(view.fin_grid) * 2);
-    fin_ticket.alloc(1);
-    RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), s));
-    RMG_CK(cudaStreamSynchronize(s));
-    view.fin_slots = fin_slots.get();
-    view.fin_ticket = fin_ticket.get();
-  }
-}
-
-// X^T restricted to sample blocks of B rows: virtual row (b, j) = b * F + j
-// lists the samples of block b that touch feature j, as uint16 offsets.
-HostCsr blocked_transpose(const HostCsr& xt, int64_t block_rows, int n_blocks) {
-  const int64_t F = xt.n;
-  HostCsr v;
-  v.n = static_cast<int64_t>(n_blocks) * F;
-  v.f = block_rows;
-  v.ptr.assign(v.n + 1, 0);
-  for (int64_t j = 0; j < F; ++j)
-    for (int64_t k = xt.ptr[j]; k < xt.ptr[j + 1]; ++k) v.ptr[(xt.idx[k] / block_rows) * F + j + 1]++;
-  for (int64_t r = 0; r < v.n; ++r) v.ptr[r + 1] += v.ptr[r];
-  v.idx.resize(xt.nnz());
-  if (!xt.val.empty()) v.val.resize(xt.nnz());
-  std::vector<int64_t> fill(v.ptr.begin(), v.ptr.end() - 1);
-  for (int64_t j = 0; j < F; ++j)
-    for (int64_t k = xt.ptr[j]; k < xt.ptr[j + 1]; ++k) {
-      const int64_t b = xt.idx[k] / block_rows;
-      const int64_t d = fill[b * F + j]++;  // samples stay increasing inside a block
-      v.idx[d] = xt.idx[k] - b * block_rows;
-      if (!xt.val.empty()) v.val[d] = xt.val[k];
-    }
-  return v;
 }
 
 // ------------------------------------------------------------------ profiling
@@ -465,7 +426,7 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   hx->red2.alloc(static_cast<size_t>(hx->view.S * H));
   std::vector<char> skip(F, 0);
   for (int64_t h = 0; h < H; ++h) skip[feat[h]] = 1;
-  hx->cold.build(ht, s, F, 1, 0, &skip);
+  hx->cold.build(ht, s, F, &skip);
   RMG_CK(cudaStreamSynchronize(s));
   HotXtDev& d = hx->view;
   d.ptr = hx->ptr.get();
@@ -613,26 +574,10 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
   else
     x.upload_sell(local, pattern, ctx->stream, local.f <= 65536, relabel);
   const HostCsr ht = transpose(local);
-  // Sample blocking of X^T: 8192-sample blocks keep each CTA's
-  // t-gathers in a 64 KB slice; used when the per-block bookkeeping (one
-  // pointer and one partial per block and feature) stays small next to nnz.
-  constexpr int64_t kBlock = 8192;
-  const int64_t nb = (local.n + kBlock - 1) / kBlock;
-  // Opt-in (RMG_BLOCKED_XT=1): measured slower than the length-class items on
-  // cfg 2 (85 vs 32 us cold, profiles/r1_operator.md); kept for large-N work.
-  const bool blocked = std::getenv("RMG_BLOCKED_XT") != nullptr && nb >= 2 &&
-                       nb * local.f * 3 <= local.nnz() && nb * local.f < INT32_MAX;
-  if (blocked) {
-    const HostCsr hb = blocked_transpose(ht, kBlock, static_cast<int>(nb));
-    xt.upload(hb, pattern, ctx->stream, true);
-    sched.build(hb, ctx->stream, local.f, static_cast<int>(nb), static_cast<int>(kBlock));
-    sched.view.idx16 = xt.view.idx16;
-  } else {
-    xt.upload(ht, pattern, ctx->stream, false);
-    sched.build(ht, ctx->stream, local.f, 1, 0);
-    build_hot(ht, local.n);
-    build_block_schedule(ht);
-  }
+  xt.upload(ht, pattern, ctx->stream, false);
+  sched.build(ht, ctx->stream, local.f);
+  build_hot(ht, local.n);
+  build_block_schedule(ht);
   t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);
 }
@@ -980,7 +925,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       pt.val.resize(pt.idx.size());
       for (size_t q = 0; q < pt.idx.size(); ++q) pt.val[q] = lvl->agg.weight[pt.idx[q]];
       lvl->pt.upload(pt, false, s);
-      lvl->pt_sched.build(pt, s, nc, 1, 0);
+      lvl->pt_sched.build(pt, s, nc);
     }
     labels_.push_back(std::move(lab));
     coarse_.push_back(std::move(lvl));

@@ -98,15 +98,13 @@ struct DeviceSchedule {
   XtSchedule view;
   DBuf<int4> items;
   DBuf<int32_t> perm, long_col, long_first, long_nseg, long_slot;
-  DBuf<double> seg_partial, slots, partial, fin_slots;
-  DBuf<unsigned> col_ticket, grid_ticket, fin_ticket;
-  // xt: (virtual) X^T CSR; features F; n_blocks > 1 selects the sample-blocked layout;
-  // skip: rows left out of the schedule (the hot rows of the hybrid pass)
-  void build(const HostCsr& xt, cudaStream_t s, int64_t features, int n_blocks, int block_rows,
-             const std::vector<char>* skip = nullptr);
+  DBuf<double> seg_partial, slots;
+  DBuf<unsigned> col_ticket, grid_ticket;
+  // xt: X^T CSR; features F; skip: rows left out of the schedule (the hot
+  // rows of the hybrid pass)
+  void build(const HostCsr& xt, cudaStream_t s, int64_t features, const std::vector<char>* skip = nullptr);
 };
 
-HostCsr blocked_transpose(const HostCsr& xt, int64_t block_rows, int n_blocks);
 
 // In-situ timing of one level's operator kernels (CUDA events on the
 // launching stream around K1 and K2 of every application).
