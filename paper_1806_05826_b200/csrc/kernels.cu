@@ -933,19 +933,39 @@ __global__ void __launch_bounds__(kThreads) k_fcg_gs_dots(const double* __restri
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->use = 0;
     return;
   }
-  __shared__ double sh[kWarps];
+  __shared__ double sh[kWarps][32];
   const int R = keep + 1;
-  for (int q = 0; q < use; ++q) {
-    const double* aph = ap_ring + (size_t)((it - use + q) % R) * n;
-    double acc = 0.0;
-    grid_stride(n, [&](int64_t i) { acc += z[i] * aph[i]; });
-    const double s = block_sum(acc, sh);
-    if (threadIdx.x == 0) slots[(size_t)blockIdx.x * 32 + q] = s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // one pass: z[i] read once, all `use` dots accumulated in registers
+  double acc[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+  grid_stride(n, [&](int64_t i) {
+    const double zi = z[i];
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < use) acc[q] += zi * ap_ring[(size_t)((it - use + q) % R) * n + i];
+  });
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    if (q < use) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) sh[wid][q] = v;
+    }
   }
-  if (grid_last(ticket)) {
-    for (int q = 0; q < use; ++q) {
-      const double s = sum_slots(slots + q, gridDim.x, 32, 0, sh);
-      if (threadIdx.x == 0) sc->coeff[q] = s / sc->pap_ring[(it - use + q) % R];
+  __syncthreads();
+  if (threadIdx.x < use) {  // fixed warp order
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) v += sh[w][threadIdx.x];
+    slots[(size_t)blockIdx.x * 32 + threadIdx.x] = v;
+  }
+  if (grid_last(ticket)) {  // warp per coefficient, lanes over the CTAs (fixed order)
+    for (int q = wid; q < use; q += kWarps) {
+      double v = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(slots + (size_t)b * 32 + q);
+      v = warp_sum(v);
+      if (lane == 0) sc->coeff[q] = v / sc->pap_ring[(it - use + q) % R];
     }
     if (threadIdx.x == 0) sc->use = use;
   }
@@ -955,11 +975,14 @@ __global__ void __launch_bounds__(kThreads) k_fcg_gs_dots(const double* __restri
 __global__ void __launch_bounds__(kThreads) k_fcg_update_p(const double* __restrict__ z, double* p_ring, int64_t n,
                                                            const KrylovScalars* sc) {
   if (sc->done) return;
+  __shared__ double cf[32];
   const int it = sc->it, R = sc->keep + 1, use = sc->use;
+  if (threadIdx.x < use) cf[threadIdx.x] = sc->coeff[threadIdx.x];
+  __syncthreads();
   double* p = p_ring + (size_t)(it % R) * n;
   grid_stride(n, [&](int64_t i) {
     double pi = z[i];
-    for (int q = 0; q < use; ++q) pi -= sc->coeff[q] * p_ring[(size_t)((it - use + q) % R) * n + i];
+    for (int q = 0; q < use; ++q) pi -= cf[q] * p_ring[(size_t)((it - use + q) % R) * n + i];
     p[i] = pi;
   });
 }
