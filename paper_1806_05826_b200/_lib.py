@@ -92,6 +92,7 @@ SIGNATURES = {
     "rmg_host_csr_destroy": [_P],
     "rmg_method_prepare": [_P, _D, _I32, _P, _U64, _P, _PP],
     "rmg_method_destroy": [_P],
+    "rmg_method_set_beta": [_P, _D],
     "rmg_method_solve": [_P, _P, _P, _P, _I32],
     "rmg_method_solve_rhs": [_P, _P, _P, _P, _I32],
     "rmg_method_precondition": [_P, _P, _P, _I32],

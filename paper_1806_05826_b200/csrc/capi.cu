@@ -515,6 +515,13 @@ int rmg_method_prepare(rmg_matrix* m, double beta, int32_t kind, const rmg_level
   });
 }
 
+int rmg_method_set_beta(rmg_method* pm, double beta) {
+  return guard([&] {
+    need(pm, "method");
+    pm->m.set_beta(beta);
+  });
+}
+
 int rmg_method_destroy(rmg_method* pm) {
   return guard([&] { delete pm; });
 }

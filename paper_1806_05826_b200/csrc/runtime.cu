@@ -846,19 +846,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
 
   if (kind == RMG_METHOD_CG || kind == RMG_METHOD_JACOBI_CG) {
     work_.push_back(std::make_unique<KrylovWork>(x->f(), 1, solver.max_iters, solver.tol, s));
-    if (kind == RMG_METHOD_JACOBI_CG) {  // krylov.cpp:623-626, 41-47
-      DBuf<double> d(std::max<int64_t>(1, x->f()));
-      x->gram_diagonal(beta, d.get());
-      std::vector<double> h(x->f());
-      if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), d.get(), h.size() * 8, cudaMemcpyDeviceToHost, s));
-      ctx_->sync();
-      for (double& v : h) {
-        if (!(v > 0.0)) throw InvalidArgument("JacobiPreconditioner: diagonal must be positive");
-        v = 1.0 / v;
-      }
-      inv_diag_.upload(h.data(), h.size(), s);
-      ctx_->sync();
-    }
+    if (kind == RMG_METHOD_JACOBI_CG) jacobi_diag();  // krylov.cpp:623-626, 41-47
     return;
   }
 
@@ -942,12 +930,14 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       if (!(specs_[k].spec.omega_override > 0.0))
         throw InvalidArgument("TwoLevelPreconditioner: omega must be positive");
       omega_.push_back(specs_[k].spec.omega_override);
+      lambda_.push_back(0.0);
       continue;
     }
     uint64_t its;
     bool cv;
     const auto t0 = tnow();
     const double lmax = level_matrix(k).lambda_max(1e-4, 200, 0x5eed + k, &its, &cv);
+    lambda_.push_back(lmax);  // beta-independent: reused by set_beta
     omega_.push_back(2.0 / (level_beta(k) + lmax));
     tlog("lambda_max", k, t0);
   }
@@ -983,6 +973,56 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       if (dense_[k]) tune_dense_partials(k);
     tlog("tune", L, t0);
   }
+  ctx_->sync();
+}
+
+// JacobiPreconditioner (krylov.cpp:41-47): inverse of beta + diag(X^T X)
+void Method::jacobi_diag() {
+  cudaStream_t s = ctx_->stream;
+  DBuf<double> d(std::max<int64_t>(1, fine_->f()));
+  fine_->gram_diagonal(beta_, d.get());
+  std::vector<double> h(fine_->f());
+  if (!h.empty()) RMG_CK(cudaMemcpyAsync(h.data(), d.get(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+  ctx_->sync();
+  for (double& v : h) {
+    if (!(v > 0.0)) throw InvalidArgument("JacobiPreconditioner: diagonal must be positive");
+    v = 1.0 / v;
+  }
+  inv_diag_.upload(h.data(), h.size(), s);
+  ctx_->sync();
+}
+
+// A new regularization for the same hierarchy (BASELINE cfg 3's beta sweep):
+// clustering, P, X_c and lambda_max(X_k^T X_k) do not depend on beta, so only
+// the level betas (overrides kept), omega_k = 2 / (beta_k + lambda_k), the
+// coarsest inverse and the dense inner levels are rebuilt -- exactly what a
+// fresh prepare at this beta computes.
+void Method::set_beta(double beta) {
+  if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
+  RMG_CK(cudaSetDevice(ctx_->device));
+  beta_ = beta;
+  if (kind_ == RMG_METHOD_CG) return;
+  if (kind_ == RMG_METHOD_JACOBI_CG) {
+    jacobi_diag();
+    return;
+  }
+  const size_t L = coarse_.size();
+  double beta_run = beta;
+  for (size_t k = 0; k < L; ++k) {
+    const double next = specs_[k].spec.has_beta_override ? specs_[k].spec.beta_override : beta_run;
+    coarse_[k]->beta = next;
+    beta_run = next;
+  }
+  for (size_t k = 0; k < L; ++k)
+    if (!specs_[k].spec.has_omega_override) omega_[k] = 2.0 / (level_beta(k) + lambda_[k]);
+  const int64_t fc_last = coarse_.back()->mat->f();
+  const std::vector<double> ac = coarse_gram(coarse_.back()->mat->host, coarse_.back()->beta);
+  const std::vector<double> inv = spd_inverse(ac, fc_last, "level " + std::to_string(L - 1) + " -> " + std::to_string(L));
+  ainv_.upload(inv.data(), inv.size(), ctx_->stream);
+  dense_.clear();
+  build_dense_levels(inv);
+  for (size_t k = 1; k < dense_.size(); ++k)
+    if (dense_[k]) tune_dense_partials(k);
   ctx_->sync();
 }
 

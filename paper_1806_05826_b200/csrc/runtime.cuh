@@ -261,6 +261,8 @@ class Method {
   Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, uint64_t n_levels,
          const rmg_solver_config& solver);
   SolveResult solve_rhs(const double* rhs_dev, double* w_dev);
+  // rebuild the beta-dependent parts for a new regularization (same hierarchy)
+  void set_beta(double beta);
   void precondition(const double* r_dev, double* z_dev);
   int64_t n_levels() const { return static_cast<int64_t>(coarse_.size()) + 1; }
   int64_t coarse_size() const { return coarse_.empty() ? 0 : coarse_[0]->mat->f(); }
@@ -290,12 +292,13 @@ class Method {
   int kind_;
   std::vector<LevelSpecHost> specs_;
   std::vector<std::unique_ptr<CoarseLevelDev>> coarse_;
-  std::vector<double> omega_;
+  std::vector<double> omega_, lambda_;
   std::vector<std::unique_ptr<KrylovWork>> work_;  // per level 0..L-1
   std::vector<std::unique_ptr<DenseInner>> dense_;  // per level (nullptr: host-sequenced path)
   void build_dense_levels(const std::vector<double>& ainv_host);
   uint64_t run_dense(size_t k, const double* rhs);
   uint64_t run_fgmres(const double* rhs, SolveResult* out);
+  void jacobi_diag();
   DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);
   void tune_dense_partials(size_t k);

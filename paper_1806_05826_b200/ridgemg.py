@@ -492,6 +492,11 @@ class PreparedMethod:
         except Exception:
             pass
 
+    def set_beta(self, beta: float) -> None:
+        """A new regularization over the same hierarchy (cfg 3's beta sweep)."""
+        _lib.check(self.lib.rmg_method_set_beta(self.h, beta))
+        self.beta = beta
+
     def coarse_size(self) -> int:
         return self._coarse_size
 
