@@ -65,6 +65,8 @@ int guard(F&& f) {
   }
 }
 
+std::unique_lock<std::recursive_mutex> hold(rmg::Context* c) { return std::unique_lock<std::recursive_mutex>(c->mu); }
+
 void need(const void* p, const char* what) {
   if (p == nullptr) throw rmg::InvalidArgument(std::string(what) + " must not be NULL");
 }
@@ -130,6 +132,7 @@ int rmg_context_destroy(rmg_context* ctx) {
 int rmg_context_set_stream(rmg_context* ctx, void* stream) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     RMG_CK(cudaStreamSynchronize(ctx->c.stream));
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     ctx->c.own_stream = false;
@@ -140,6 +143,7 @@ int rmg_context_set_stream(rmg_context* ctx, void* stream) {
 int rmg_context_synchronize(rmg_context* ctx) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     ctx->c.sync();
   });
 }
@@ -148,6 +152,7 @@ int rmg_matrix_create_csr(rmg_context* ctx, uint64_t n, uint64_t f, const uint64
                           const double* values, int32_t detect_pattern, rmg_matrix** out) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     need(out, "out");
     need(rp, "row_offsets");
     rmg::HostCsr h;
@@ -213,6 +218,7 @@ int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n, uint64_t f, const void
                             rmg_matrix** out) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     need(out, "out");
     if (n * f) need(data, "data");
     rmg::DenseInput din;
@@ -228,6 +234,7 @@ int rmg_matrix_create_dense_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n
                                     uint64_t ld, int32_t fp32, rmg_matrix** out) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     need(comm, "comm");
     need(out, "out");
     if (n * f) need(data, "data");
@@ -254,6 +261,7 @@ int rmg_comm_unique_id(uint8_t* id_out) {
 int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id, rmg_comm** out) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     need(id, "id");
     need(out, "out");
     ncclUniqueId uid;
@@ -270,6 +278,7 @@ int rmg_matrix_create_csr_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n, 
                                   const uint64_t* ci, const double* values, int32_t detect_pattern, rmg_matrix** out) {
   return guard([&] {
     need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
     need(comm, "comm");
     need(out, "out");
     need(rp, "row_offsets");
@@ -307,7 +316,11 @@ int rmg_shard_rows(const uint64_t* rp, uint64_t n, int32_t nranks, uint64_t* bou
 }
 
 int rmg_matrix_destroy(rmg_matrix* m) {
-  return guard([&] { delete m; });
+  return guard([&] {
+    if (m == nullptr) return;
+    const auto lk_ = hold(m->m.ctx);
+    delete m;
+  });
 }
 
 int rmg_matrix_shape(const rmg_matrix* m, uint64_t* n, uint64_t* f, uint64_t* nnz, int32_t* is_pattern) {
@@ -342,6 +355,7 @@ int rmg_matrix_hot_layout(const rmg_matrix* m, uint64_t* hot_features, uint64_t*
 int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     rmg::Context& c = *m->m.ctx;
     RMG_CK(cudaSetDevice(c.device));
     rmg::DBuf<double> bi, bo;
@@ -355,6 +369,7 @@ int rmg_spmv(rmg_matrix* m, const double* v, double* y, int32_t on_device) {
 int rmg_spmv_transpose(rmg_matrix* m, const double* u, double* y, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     rmg::Context& c = *m->m.ctx;
     RMG_CK(cudaSetDevice(c.device));
     rmg::DBuf<double> bi, bo;
@@ -368,6 +383,7 @@ int rmg_spmv_transpose(rmg_matrix* m, const double* u, double* y, int32_t on_dev
 int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     if (beta < 0.0) throw rmg::InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
     rmg::Context& c = *m->m.ctx;
     RMG_CK(cudaSetDevice(c.device));
@@ -386,6 +402,7 @@ int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, in
 int rmg_ridge_apply_block(rmg_matrix* m, double beta, const double* v, double* out, uint64_t k, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     rmg::Context& c = *m->m.ctx;
     RMG_CK(cudaSetDevice(c.device));
     const size_t cnt = static_cast<size_t>(m->m.f()) * k;
@@ -400,6 +417,7 @@ int rmg_ridge_apply_block(rmg_matrix* m, double beta, const double* v, double* o
 int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     rmg::Context& c = *m->m.ctx;
     RMG_CK(cudaSetDevice(c.device));
     rmg::DBuf<double> bo;
@@ -413,6 +431,7 @@ int rmg_lambda_max(rmg_matrix* m, double tol, uint64_t max_iters, uint64_t seed,
                    int32_t* converged) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     need(value, "value");
     RMG_CK(cudaSetDevice(m->m.ctx->device));
     uint64_t it = 0;
@@ -434,6 +453,7 @@ int rmg_rng_normals(uint64_t seed, uint64_t n, double* out) {
 int rmg_generate_rhs(rmg_matrix* m, uint64_t seed, double* b_out, double* rhs_out) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     need(b_out, "b_out");
     rmg::CounterRng rng(seed);
     const int64_t n = m->m.n();
@@ -507,6 +527,7 @@ int rmg_method_prepare(rmg_matrix* m, double beta, int32_t kind, const rmg_level
                        const rmg_solver_config* solver, rmg_method** out) {
   return guard([&] {
     need(m, "matrix");
+    const auto lk_ = hold(m->m.ctx);
     need(out, "out");
     rmg_solver_config cfg{1e-6, 1000, 20};
     if (solver) cfg = *solver;
@@ -518,17 +539,23 @@ int rmg_method_prepare(rmg_matrix* m, double beta, int32_t kind, const rmg_level
 int rmg_method_set_beta(rmg_method* pm, double beta) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     pm->m.set_beta(beta);
   });
 }
 
 int rmg_method_destroy(rmg_method* pm) {
-  return guard([&] { delete pm; });
+  return guard([&] {
+    if (pm == nullptr) return;
+    const auto lk_ = hold(pm->m.fine()->ctx);
+    delete pm;
+  });
 }
 
 int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out, rmg_solve_report* report, int32_t on_device) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     need(rhs, "rhs");
     need(w_out, "w_out");
     rmg::Matrix& x = *pm->m.fine();
@@ -546,6 +573,7 @@ int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out, rmg_s
 int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_report* report, int32_t on_device) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     need(b, "b");
     need(w_out, "w_out");
     rmg::Matrix& x = *pm->m.fine();
@@ -565,6 +593,7 @@ int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_r
 int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     rmg::Matrix& x = *pm->m.fine();
     rmg::Context& c = *x.ctx;
     RMG_CK(cudaSetDevice(c.device));
@@ -587,6 +616,7 @@ int rmg_method_level(const rmg_method* pm, uint64_t level, uint64_t* n_features,
                      double* omega) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
     const rmg::Matrix& mk = pm->m.level_matrix(level);
     if (n_features) *n_features = mk.f();
@@ -599,6 +629,7 @@ int rmg_method_level(const rmg_method* pm, uint64_t level, uint64_t* n_features,
 int rmg_method_level_labels(const rmg_method* pm, uint64_t level, int64_t* labels_out) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     need(labels_out, "labels_out");
     const auto& l = pm->m.labels(level);
     std::memcpy(labels_out, l.data(), l.size() * sizeof(int64_t));
@@ -608,6 +639,7 @@ int rmg_method_level_labels(const rmg_method* pm, uint64_t level, int64_t* label
 int rmg_method_level_matrix(const rmg_method* pm, uint64_t level, uint64_t* rp, uint64_t* ci, double* v) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
     const rmg::HostCsr& h = pm->m.level_matrix(level).host;
     if (rp)
@@ -636,6 +668,7 @@ int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int3
                              double* ms_k1, double* ms_k2) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     double k1 = 0.0, k2 = 0.0;
     RMG_CK(cudaSetDevice(pm->m.fine()->ctx->device));
     const double t = pm->m.time_operator(level, reps, flush_l2 != 0, &k1, &k2);
@@ -650,6 +683,7 @@ int rmg_method_time_operator(rmg_method* pm, uint64_t level, uint64_t reps, int3
 int rmg_debug_dense_timing(rmg_method* pm, uint64_t level, unsigned long long* out256) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     const rmg::DenseInner* d = pm->m.dense(level);
     if (d == nullptr || d->timing.get() == nullptr) throw rmg::InvalidArgument("no dense timing buffer");
     RMG_CK(cudaMemcpy(out256, d->timing.get(), 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -659,6 +693,7 @@ int rmg_debug_dense_timing(rmg_method* pm, uint64_t level, unsigned long long* o
 int rmg_method_set_profiling(rmg_method* pm, int32_t on) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     pm->m.set_profiling(on != 0);
   });
 }
@@ -666,6 +701,7 @@ int rmg_method_set_profiling(rmg_method* pm, int32_t on) {
 int rmg_method_profile(const rmg_method* pm, uint64_t level, uint64_t* applications, double* ms_k1, double* ms_k2) {
   return guard([&] {
     need(pm, "method");
+    const auto lk_ = hold(pm->m.fine()->ctx);
     if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
     const rmg::OpProfile& p = pm->m.profile(level);
     if (applications) *applications = p.count;

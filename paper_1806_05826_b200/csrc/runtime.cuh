@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -68,6 +69,11 @@ class DBuf {
 };
 
 struct Context {
+  // every C-ABI call that touches this context holds it: workspaces (matrix
+  // scratch, method Krylov state) are per object and all device work is on one
+  // stream, so serializing calls costs no GPU parallelism (krylov.hpp:172-175:
+  // prepared methods accept concurrent solves)
+  std::recursive_mutex mu;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
