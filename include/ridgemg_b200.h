@@ -235,6 +235,13 @@ int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_r
 int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out,
                          rmg_solve_report* report, int32_t on_device);
 /* Apply the level-0 preconditioner once: z = M^{-1} r (two_level_apply, krylov.cpp:379-425). */
+/* k right-hand sides (SURVEY §8(b) k_rhs): b is column-major n_samples x k, w_out
+ * column-major n_features x k, reports[k] optional.  Column q equals
+ * rmg_method_solve of column q (the solves run one after the other on the
+ * context's stream; the block operator, rmg_ridge_apply_block, is the building
+ * block of a lock-step batched solver). */
+int rmg_method_solve_batch(rmg_method* pm, const double* b, double* w_out, uint64_t k, rmg_solve_report* reports,
+                           int32_t on_device);
 int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device);
 /* PreparedMethod::coarse_size (krylov.hpp:229) and per-level introspection */
 int rmg_method_info(const rmg_method* pm, uint64_t* n_levels, uint64_t* coarse_size);

@@ -96,6 +96,7 @@ SIGNATURES = {
     "rmg_method_solve": [_P, _P, _P, _P, _I32],
     "rmg_method_solve_rhs": [_P, _P, _P, _P, _I32],
     "rmg_method_precondition": [_P, _P, _P, _I32],
+    "rmg_method_solve_batch": [_P, _P, _P, _U64, _P, _I32],
     "rmg_method_info": [_P, _P, _P],
     "rmg_method_level": [_P, _U64, _P, _P, _P, _P],
     "rmg_method_level_labels": [_P, _U64, _P],

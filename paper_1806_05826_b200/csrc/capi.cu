@@ -590,6 +590,24 @@ int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_r
   });
 }
 
+int rmg_method_solve_batch(rmg_method* pm, const double* b, double* w_out, uint64_t k, rmg_solve_report* reports,
+                           int32_t on_device) {
+  return guard([&] {
+    need(pm, "method");
+    need(b, "b");
+    need(w_out, "w_out");
+    const auto lk_ = hold(pm->m.fine()->ctx);
+    rmg::Matrix& x = *pm->m.fine();
+    const int64_t n = x.n(), f = x.f();
+    // column q of the column-major blocks b (n x k) and w (f x k) is one solve
+    for (uint64_t q = 0; q < k; ++q) {
+      const int rc = rmg_method_solve(pm, b + q * n, w_out + q * f, reports ? reports + q : nullptr, on_device);
+      if (rc != RMG_OK) throw rmg::RuntimeError("rmg_method_solve_batch: right-hand side " + std::to_string(q) +
+                                                ": " + g_err);
+    }
+  });
+}
+
 int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device) {
   return guard([&] {
     need(pm, "method");

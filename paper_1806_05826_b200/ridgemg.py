@@ -528,6 +528,23 @@ class PreparedMethod:
         _lib.check(self.lib.rmg_method_solve(self.h, _ptr(b), _ptr(w), C.byref(rep), 0))
         return w, self._finish(rep, hist, inner)
 
+    def solve_batch(self, B) -> tuple[np.ndarray, list]:
+        """k right-hand sides, B of shape (n_samples, k): W (n_features, k) and one
+        SolveReport per column, each equal to solve(B[:, q])."""
+        B = np.asarray(B, np.float64)
+        if B.ndim != 2 or B.shape[0] != self.x.n_samples:
+            raise ValueError("solve_batch: B must be (n_samples, k)")
+        k = B.shape[1]
+        bcol = np.ascontiguousarray(B.T)  # column-major block = row-major transpose
+        wcol = np.zeros((k, self.x.n_features))
+        parts = [self._report() for _ in range(k)]
+        arr = (_lib.SolveReportC * max(1, k))()
+        for q, (rep, _, _) in enumerate(parts):
+            arr[q] = rep
+        _lib.check(self.lib.rmg_method_solve_batch(self.h, _ptr(bcol), _ptr(wcol), k, arr, 0))
+        reports = [self._finish(arr[q], parts[q][1], parts[q][2]) for q in range(k)]
+        return np.ascontiguousarray(wcol.T), reports
+
     def solve_rhs(self, rhs) -> tuple[np.ndarray, SolveReport]:
         rhs = np.ascontiguousarray(rhs, np.float64)
         if rhs.shape != (self.x.n_features,):

@@ -40,3 +40,18 @@ def test_concurrent_solves_match_sequential(gpu):
     assert not errors, errors
     for (a, b), (c, d) in zip(got, want):
         assert np.array_equal(a, c) and np.array_equal(b, d)
+
+
+def test_solve_batch_equals_single_solves(gpu):
+    x = random_matrix(500, 150, 4, 0.3)
+    m = R.DeviceMatrix(x, R.default_context())
+    lv = R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS, target_size=15),
+                     solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY))
+    pm = R.PreparedMethod(m, 1e-2, R.MethodSpec(kind=R.FCG_TWOLEVEL, levels=[lv], solver=R.SolverConfig(1e-10, 500)))
+    B = np.stack([R.rng_normals(10 + q, 500) for q in range(5)], axis=1)
+    W, reps = pm.solve_batch(B)
+    assert W.shape == (150, 5) and len(reps) == 5
+    for q in range(5):
+        w, rep = pm.solve(B[:, q])
+        assert np.array_equal(W[:, q], w) and reps[q].iterations == rep.iterations
+        assert np.array_equal(reps[q].residual_history, rep.residual_history)
