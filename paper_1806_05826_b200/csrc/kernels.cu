@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(NT) k_spmv_sell(const int32_t* __restrict__ of
     for (int i = threadIdx.x; i < n_hot; i += NT) vh[i] = __ldcg(v + i);
     __syncthreads();
   }
-  constexpr int U = 8;
+  constexpr int U = HOTV ? 16 : 8;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
   for (int64_t sl = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5; sl < n_slices; sl += nwarps) {
@@ -519,21 +519,22 @@ __device__ __forceinline__ void xt_finalize(KrylovScalars* sc, double s0, double
   }
 }
 
-// Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 4 elements per
+// Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 8 elements per
 // lane per round (independent loads in flight); lane-strided order.
 template <bool PAT>
 __device__ __forceinline__ double xt_row_sum(const int32_t* __restrict__ idx, const double* __restrict__ val,
                                              const double* __restrict__ t, int k0, int k1, int lane, int lanes) {
+  constexpr int U = 8;  // elements per lane per round (independent loads in flight)
   double s = 0.0;
-  for (int k = k0 + lane; k < k1; k += 4 * lanes) {
-    int c[4];
+  for (int k = k0 + lane; k < k1; k += U * lanes) {
+    int c[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) c[u] = k + u * lanes < k1 ? ld_stream(idx + k + u * lanes) : -1;
-    double x[4];
+    for (int u = 0; u < U; ++u) c[u] = k + u * lanes < k1 ? ld_stream(idx + k + u * lanes) : -1;
+    double x[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
+    for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (c[u] >= 0) s += PAT ? x[u] : ld_stream(val + k + u * lanes) * x[u];
   }
   return s;
