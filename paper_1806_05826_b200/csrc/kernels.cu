@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(NT) k_spmv_sell(const int32_t* __restrict__ of
     for (int i = threadIdx.x; i < n_hot; i += NT) vh[i] = __ldcg(v + i);
     __syncthreads();
   }
-  constexpr int U = HOTV ? 16 : 8;
+  constexpr int U = HOTV ? 16 : 8;  // HOTV (1 CTA of 1024 per SM): deeper lookahead measured 478 -> 417 us
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
   for (int64_t sl = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5; sl < n_slices; sl += nwarps) {
