@@ -5,6 +5,8 @@
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <atomic>
+#include <functional>
 #include <thread>
 
 namespace rmg {
@@ -128,6 +130,58 @@ double column_euclid(const HostCsr& xt, int64_t i, int64_t j) {
 
 }  // namespace
 
+// Persistent workers for loops issued many times in a row (k-means++ runs K
+// parallel passes): threads are created once, each pass is handed out in
+// dynamic chunks (Zipf-hot columns make static ranges uneven).  Which thread
+// computes an element never changes the element's value.
+class StepPool {
+ public:
+  explicit StepPool(unsigned threads) {
+    for (unsigned t = 1; t < threads; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~StepPool() {
+    stop_.store(true);
+    gen_.fetch_add(1);
+    for (auto& w : workers_) w.join();
+  }
+  template <class F>
+  void run(int64_t n, int64_t chunk, F&& body) {
+    body_ = [&](int64_t lo, int64_t hi) { body(lo, hi); };
+    n_ = n;
+    chunk_ = chunk;
+    next_.store(0);
+    pending_.store(static_cast<int>(workers_.size()));
+    gen_.fetch_add(1);
+    work();
+    while (pending_.load() != 0) std::this_thread::yield();
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const int64_t lo = next_.fetch_add(chunk_);
+      if (lo >= n_) return;
+      body_(lo, std::min(n_, lo + chunk_));
+    }
+  }
+  void loop() {
+    int64_t seen = 0;
+    for (;;) {
+      while (gen_.load() == seen) std::this_thread::yield();
+      seen = gen_.load();
+      if (stop_.load()) return;
+      work();
+      pending_.fetch_sub(1);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::function<void(int64_t, int64_t)> body_;
+  std::atomic<int64_t> gen_{0}, next_{0};
+  std::atomic<int> pending_{0};
+  std::atomic<bool> stop_{false};
+  int64_t n_ = 0, chunk_ = 1;
+};
+
 // clustering.cpp:189-255
 std::vector<int64_t> kmeanspp_seed(const HostCsr& xt, int64_t k, uint64_t seed, unsigned threads) {
   const int64_t f = xt.n;
@@ -137,9 +191,10 @@ std::vector<int64_t> kmeanspp_seed(const HostCsr& xt, int64_t k, uint64_t seed, 
   std::vector<char> used(f, 0);
   used[chosen[0]] = 1;
   std::vector<double> d2(f, std::numeric_limits<double>::infinity()), dist(f, 0.0);
+  StepPool pool(f >= 512 ? std::max(1u, threads) : 1u);
   while (static_cast<int64_t>(chosen.size()) < k) {
     const int64_t last = chosen.back();
-    parallel_ranges(f, threads, [&](int64_t lo, int64_t hi) {
+    pool.run(f, 64, [&](int64_t lo, int64_t hi) {
       for (int64_t j = lo; j < hi; ++j)
         if (!used[j]) dist[j] = column_euclid(xt, j, last);
     });
