@@ -109,21 +109,40 @@ void parallel_ranges(int64_t n, unsigned threads, F&& body) {
 }
 
 // Euclidean distance of two sparse columns over the merged supports in
-// increasing row order (distance.cpp:27-67).
+// increasing row order (distance.cpp:27-67).  A row in one support only adds
+// (x - 0)^2 = x^2 (exact operands), a shared row (x_i - x_j)^2, and (x - y)^2 ==
+// (y - x)^2 exactly, so the lists may swap roles: the longer one is walked in
+// runs between the shorter one's entries (binary search, then a branch-free
+// sum).  Same terms, same order, same rounding as the element-wise merge.
 double column_euclid(const HostCsr& xt, int64_t i, int64_t j) {
-  int64_t a = xt.ptr[i], b = xt.ptr[j];
-  const int64_t ae = xt.ptr[i + 1], be = xt.ptr[j + 1];
+  int64_t a = xt.ptr[i], ae = xt.ptr[i + 1], b = xt.ptr[j], be = xt.ptr[j + 1];
+  if (ae - a < be - b) {
+    std::swap(a, b);
+    std::swap(ae, be);
+  }
+  const int64_t* idx = xt.idx.data();
+  const double* val = xt.val.empty() ? nullptr : xt.val.data();
+  auto v = [&](int64_t q) { return val ? val[q] : 1.0; };
   double s = 0.0;
-  while (a < ae || b < be) {
-    double diff;
-    if (b >= be || (a < ae && xt.idx[a] < xt.idx[b])) {
-      diff = value_at(xt, a++) - 0.0;
-    } else if (a >= ae || xt.idx[b] < xt.idx[a]) {
-      diff = 0.0 - value_at(xt, b++);
-    } else {
-      diff = value_at(xt, a++) - value_at(xt, b++);
+  for (; b < be; ++b) {
+    const int64_t target = idx[b];
+    const int64_t p = std::lower_bound(idx + a, idx + ae, target) - idx;
+    for (; a < p; ++a) {
+      const double x = v(a);
+      s += x * x;
     }
-    s += diff * diff;
+    const double y = v(b);
+    if (a < ae && idx[a] == target) {
+      const double diff = v(a) - y;
+      s += diff * diff;
+      ++a;
+    } else {
+      s += y * y;
+    }
+  }
+  for (; a < ae; ++a) {
+    const double x = v(a);
+    s += x * x;
   }
   return std::sqrt(s);
 }
