@@ -45,8 +45,10 @@ constexpr int kT = 256;
 constexpr int kW = kT / 32;
 // partial slots per block: [0] ||b||^2, [1] #non-finite, [2..33] GS, [34] pap, [35] pr, [36] rr;
 // 64 doubles = 512 B per CTA so every CTA's slots start on their own L2 line group
-constexpr int kPS = 64;
+constexpr int kPS = 80;
 constexpr int kGS = 2, kPAP = 34, kPR = 35, kRR = 36;
+// two-barrier kernel: ||r||^2 and the Gram-Schmidt dots are one contiguous run
+constexpr int kRR2 = 40, kGS2 = 41;  // 41..71
 constexpr int kMaxQ = 16;  // n <= 4096 columns = 16 per thread
 constexpr int kMaxUse = 32;
 
@@ -170,7 +172,7 @@ __device__ __forceinline__ SegLane segment_layout(const DenseKrylovArgs& a, int 
   return L;
 }
 
-__device__ __forceinline__ void segment_partials(const DenseKrylovArgs& a, const SegLane& L, double ri) {
+__device__ __forceinline__ void segment_partials(const SegLane& L, double ri, double* dst) {
   const int lane = threadIdx.x & 31;
   double v = L.w * ri;
   bool f = L.head;
@@ -183,7 +185,7 @@ __device__ __forceinline__ void segment_partials(const DenseKrylovArgs& a, const
       f = g;
     }
   }
-  if (L.end) a.spart[L.slot] = v;
+  if (L.end) dst[L.slot] = v;
 }
 
 // Narrow GEMV for the low-rank preconditioner (nc <= kT columns, nr <= 28
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   SegLane seg;
   if (a.lowrank && tid < 32) {
     seg = segment_layout(a, row0, nr);
-    segment_partials(a, seg, tid < nr ? a.b[orig(row0 + tid)] : 0.0);
+    segment_partials(seg, tid < nr ? a.b[orig(row0 + tid)] : 0.0, a.spart);
   }
   bb = bsum_all(bb, sh);
   bad = bsum_all(bad, sh);
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
       a.r[i] = ri;
       rr = ri * ri;
     }
-    if (a.lowrank && tid < 32) segment_partials(a, seg, ri);
+    if (a.lowrank && tid < 32) segment_partials(seg, ri, a.spart);
     rr = bsum_all(rr, sh);
     if (tid == 0) part(kRR) = rr;
     tmark(a, it, 11);
@@ -478,6 +480,300 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
   }
 }
 
+// Two grid barriers per iteration, for the low-rank FCG
+// preconditioner and for plain CG.  Same iteration as k_dense_krylov
+// (krylov.cpp:164-220), regrouped around two exchanges:
+//   B1 publishes z (whole vector), ||r||^2 and the Gram-Schmidt dots <z, Ap_q>;
+//      then Ap = A z - sum_q c_q Ap_q (CG: A z + beta Ap_prev) from the own rows
+//      of the stored Ap history, so p never has to be exchanged, and
+//      p = z - sum_q c_q p_q in the reference's order;
+//   B3 publishes <p, Ap>, <p, r> and the segment partials of P^T Ap; after it
+//      every CTA has alpha, updates its rows of x and r, and forms
+//      P^T r_new = sum over segments of (P^T r_old - alpha P^T Ap) partials
+//      (both sets of partials are per-iteration, so nothing is carried over
+//      iterations and no recurrence drift builds up).
+// The convergence test of r_k (||r_k||^2 rides on B1 of iteration k) runs half
+// an iteration after the update; iteration counts, history and breakdown
+// exits are those of k_dense_krylov.  Own-row work (nr <= 28) is warp 0:
+// its reductions are warp sums.
+template <bool SMEM, int HM>  // HM >= truncation (history directions held per lane)
+__global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double smem[];
+  const int n = a.n, R = a.rows_per_cta;
+  const int row0 = blockIdx.x * R;
+  const int row1 = min(n, row0 + R);
+  const int nr = max(0, row1 - row0);
+  double* As = smem;  // same layout as k_dense_krylov
+  double* red = smem + (SMEM ? (size_t)R * n : 0);
+  double* zs = red + (size_t)R * kW;
+  double* vv = zs + R;
+  double* contrib = vv + R;
+  double* gsum = contrib + (size_t)R * kMaxUse;
+  double* coef = gsum + 64;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int pstride = slot_stride();
+  auto part = [&](int slot) -> double& { return a.partials[(size_t)slot * pstride + blockIdx.x]; };
+  KrylovScalars* sc = a.sc;
+  const double* Arows = SMEM ? As : a.A + (size_t)row0 * n;
+  const double* Qrows = a.M + (size_t)row0 * a.nc;
+  auto orig = [&](int i) { return a.perm != nullptr ? a.perm[i] : i; };
+  const bool own = wid == 0 && lane < nr;
+  const int i = row0 + lane;  // warp 0: lane lr holds row row0 + lr
+  const int nseg = a.n_segments;
+  // a.spart: [P^T r partials, even iterations | odd iterations | P^T Ap partials]
+  double* spart_ap = a.spart + 2 * nseg;
+
+  if (SMEM) {
+    for (int idx = tid; idx < nr * n; idx += kT) As[idx] = a.A[(size_t)row0 * n + idx];
+  }
+  // ---- begin: x = 0, r = b, ||b|| (krylov.cpp:164-176)
+  double ri = 0.0, xi = 0.0, pi = 0.0, api = 0.0;
+  SegLane seg;
+  if (wid == 0) {
+    ri = own ? a.b[orig(i)] : 0.0;
+    const double bb = wsum(ri * ri);
+    const double bad = wsum(own && !isfinite(ri) ? 1.0 : 0.0);
+    if (lane == 0) {
+      part(0) = bb;
+      part(1) = bad;
+    }
+    if (a.lowrank) {
+      seg = segment_layout(a, row0, nr);
+      segment_partials(seg, ri, a.spart);
+    }
+  }
+  int cs0 = 0, cs1 = 0;  // this thread's cluster segments (nc <= kT)
+  if (a.lowrank && a.nc <= kT && tid < a.nc) {
+    cs0 = __ldg(a.cseg + tid);
+    cs1 = __ldg(a.cseg + tid + 1);
+  }
+  grid.sync();
+  grid_sums(a.partials, 0, 2, gsum);
+  const double nb = sqrt(gsum[0]);
+  const double nbad = gsum[1];
+  if (nbad > 0.0 || nb == 0.0) {
+    if (blockIdx.x == 0 && tid == 0) {
+      sc->it = 0;
+      sc->status = nbad > 0.0 ? 3 : 0;
+      sc->converged = nbad > 0.0 ? 0 : 1;
+      sc->done = 1;
+      sc->rel = nbad > 0.0 ? 1.0 : 0.0;
+      sc->nb = nb;
+      if (nbad == 0.0) a.hist[0] = 0.0;
+    }
+    if (own) {
+      a.x_out[orig(i)] = 0.0;
+      if (a.x_out != a.x) a.x[i] = 0.0;
+    }
+    return;
+  }
+  const int keep = a.keep, RING = keep + 1;
+  const double omega = a.omega;
+  double rz = nb * nb;  // CG: <r, z> with z = r
+  double beta_cg = 0.0;
+  int iters = 0, status = 0;
+  bool converged = false;
+  double rel = 1.0;
+  for (int it = 0;; ++it) {
+    tmark(a, it, 0);
+    // ======== phase 1: alpha, x/r update (direction it-1), z_it
+    double q[28];
+    double sg[2] = {0.0, 0.0}, sa[2] = {0.0, 0.0};
+    if (a.lowrank) {
+      if (a.nc <= kT) {
+#pragma unroll
+        for (int lr = 0; lr < 28; ++lr)
+          q[lr] = (lr < nr && tid < a.nc) ? __ldg(Qrows + (size_t)lr * a.nc + tid) : 0.0;
+      }
+      const double* sp = a.spart + (it > 0 ? ((it - 1) & 1) * nseg : 0);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int g = tid + u * kT;
+        if (g < nseg) {
+          sg[u] = __ldcg(sp + g);
+          if (it > 0) sa[u] = __ldcg(spart_ap + g);
+        }
+      }
+    }
+    double alpha = 0.0;
+    if (it > 0) {
+      grid_sums(a.partials, kPAP, 2, gsum);
+      const double pap = gsum[0], pr = gsum[1];
+      if (a.fcg ? pap == 0.0 : false) {
+        status = 1;
+        iters = it - 1;
+        break;
+      }
+      if (a.fcg ? pap < 0.0 : !(pap > 0.0)) {
+        status = 2;
+        iters = it - 1;
+        break;
+      }
+      alpha = a.fcg ? pr / pap : rz / pap;
+      if (blockIdx.x == 0 && tid == 0) a.pap_ring[(it - 1) % RING] = pap;
+      if (own) {
+        xi += alpha * pi;
+        ri = ri - alpha * api;
+      }
+    }
+    tmark(a, it, 1);
+    double zi = ri;  // CG: z = r
+    if (a.lowrank) {  // z = omega r + Q (P^T r)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int g = tid + u * kT;
+        if (g < nseg) contrib[g] = it > 0 ? sg[u] - alpha * sa[u] : sg[u];
+      }
+      if (it > 0 && wid == 0) segment_partials(seg, own ? ri : 0.0, a.spart + (it & 1) * nseg);
+      __syncthreads();
+      if (a.nc <= kT) {
+        double sum = 0.0;
+        for (int g = cs0; g < cs1; ++g) sum += contrib[g];
+        gemv_narrow(q, nr, sum, red, vv);
+      } else {
+        double sv[kMaxQ];
+#pragma unroll
+        for (int qq = 0; qq < kMaxQ; ++qq) {
+          const int c = tid + qq * kT;
+          double sum = 0.0;
+          if (c < a.nc)
+            for (int g = __ldg(a.cseg + c); g < __ldg(a.cseg + c + 1); ++g) sum += contrib[g];
+          sv[qq] = sum;
+        }
+        gemv_rows<true>(Qrows, nr, a.nc, sv, red, vv);
+      }
+      if (own) zi = omega * ri + vv[lane];
+    }
+    tmark(a, it, 2);
+    // ---- publish z, ||r||^2, Gram-Schmidt dots <z, Ap_q> (krylov.cpp:189-197)
+    const int mi = it == 0 ? 0 : max(1, it % (keep + 1));
+    const int use = a.fcg ? min(mi, min(it, keep)) : 0;
+    if (wid == 0) {
+      if (own) {
+        a.zfull[i] = zi;
+        zs[lane] = zi;
+      }
+      const double rr = wsum(own ? ri * ri : 0.0);
+      if (lane == 0) part(kRR2) = rr;
+    }
+    if (use > 0) {
+      __syncthreads();
+      double y[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int qd = wid + j * kW;
+        const double* aph = a.ap_ring + (size_t)((it - use + qd) % RING) * n;
+        y[j] = (qd < use && lane < nr) ? zs[lane] * __ldcg(aph + row0 + lane) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double acc = wsum(y[j]);
+        if (lane == 0 && wid + j * kW < use) part(kGS2 + wid + j * kW) = acc;
+      }
+    }
+    tmark(a, it, 3);
+    grid.sync();  // B1
+    tmark(a, it, 4);
+    // ======== phase 2: convergence of r_it; direction it
+    double pc[kMaxQ];
+#pragma unroll
+    for (int qq = 0; qq < kMaxQ; ++qq) {
+      const int c = tid + qq * kT;
+      pc[qq] = c < n ? __ldcg(a.zfull + c) : 0.0;
+    }
+    double den = 1.0;
+    if (tid < use) den = __ldcg(a.pap_ring + (it - use + tid) % RING);
+    // own rows of the history: warp 0 loads the p_q, warp 1 the Ap_q
+    double h[HM];
+    {
+      const bool hw = wid < 2 && lane < nr;
+      const double* hb = wid == 0 ? a.p_ring : a.ap_ring;
+      const int nh = a.fcg ? use : (it > 0 ? 1 : 0);
+      int hs = (it - nh) % RING;
+#pragma unroll
+      for (int qd = 0; qd < HM; ++qd) {
+        h[qd] = (hw && qd < nh) ? __ldcg(hb + (size_t)hs * n + i) : 0.0;
+        hs = hs + 1 == RING ? 0 : hs + 1;
+      }
+    }
+    grid_sums(a.partials, kRR2, 1 + use, gsum);
+    tmark(a, it, 5);
+    const double rrs = gsum[0];
+    if (it > 0) {
+      rel = sqrt(rrs) / nb;
+      if (blockIdx.x == 0 && tid == 0) a.hist[it - 1] = rel;
+      if (rel <= a.tol) {
+        converged = true;
+        iters = it;
+        break;
+      }
+      if (!a.fcg) {  // CG: rz' = <r, r>, beta = rz'/rz
+        beta_cg = rrs / rz;
+        rz = rrs;
+      }
+    }
+    if (it >= a.max_iters) {
+      iters = it;
+      break;
+    }
+    if (tid < use) coef[tid] = gsum[1 + tid] / den;
+    // A z for the owned rows (ends with __syncthreads: coef and vv visible)
+    if (SMEM) {
+      gemv_rows<false>(Arows, nr, n, pc, red, vv);
+    } else {
+      gemv_rows<true>(Arows, nr, n, pc, red, vv);
+    }
+    tmark(a, it, 6);
+    if (wid < 2) {  // warp 0: p = z - c_0 p_0 - c_1 p_1 - ... (reference order); warp 1: Ap alike
+      double v = wid == 0 ? zi : (lane < nr ? vv[lane] : 0.0);
+      if (a.fcg) {
+#pragma unroll
+        for (int qd = 0; qd < HM; ++qd)
+          if (qd < use) v = v - __dmul_rn(coef[qd], h[qd]);
+      } else if (it > 0) {  // CG: p = z + beta p_prev (krylov.cpp:145-153)
+        v = v + beta_cg * h[0];
+      }
+      if (wid == 0) {
+        pi = own ? v : 0.0;
+      } else if (lane < nr) {
+        vv[lane] = v;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const int slot = it % RING;
+      api = own ? vv[lane] : 0.0;
+      if (own) {
+        a.p_ring[(size_t)slot * n + i] = pi;
+        a.ap_ring[(size_t)slot * n + i] = api;
+      }
+      const double dpap = wsum(pi * api);
+      const double dpr = wsum(pi * ri);
+      if (lane == 0) {
+        part(kPAP) = dpap;
+        part(kPR) = dpr;
+      }
+      if (a.lowrank) segment_partials(seg, api, spart_ap);
+    }
+    tmark(a, it, 7);
+    grid.sync();  // B3
+  }
+  if (own) {  // solution back to the original order
+    a.x_out[orig(i)] = xi;
+    if (a.x_out != a.x) a.x[i] = xi;
+    a.r[i] = ri;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    sc->it = iters;
+    sc->status = status;
+    sc->converged = converged ? 1 : 0;
+    sc->done = 1;
+    sc->rel = rel;
+    sc->nb = nb;
+  }
+}
+
 }  // namespace
 
 DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
@@ -500,6 +796,11 @@ DenseKrylovPlan plan_dense_krylov(int n, int nc, int device) {
   return p;
 }
 
+bool dense_two_barrier(const DenseKrylovArgs& a) {
+  static const bool off = std::getenv("RMG_DENSE_4B") != nullptr;
+  return !off && a.dbg == 0 && (a.fcg == 0 || (a.lowrank != 0 && a.n_segments <= 2 * kT)) && a.zfull != nullptr;
+}
+
 void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& args, cudaStream_t s) {
   if (args.n > kMaxQ * kT) throw std::runtime_error("dense inner solver: level above 4096 unknowns");
   if (args.keep + 1 > kMaxUse) throw std::runtime_error("dense inner solver: truncation above 31");
@@ -508,6 +809,12 @@ void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& arg
   if (plan.rows_per_cta > 32 || plan.grid > 256)  // one GS element per lane; grid_sums unroll
     throw std::runtime_error("dense inner solver: too few SMs for this level");
   void* fn = plan.smem_a ? (void*)k_dense_krylov<true> : (void*)k_dense_krylov<false>;
+  if (dense_two_barrier(args)) {
+    if (args.keep <= 20)
+      fn = plan.smem_a ? (void*)k_dense_krylov2<true, 20> : (void*)k_dense_krylov2<false, 20>;
+    else
+      fn = plan.smem_a ? (void*)k_dense_krylov2<true, kMaxUse - 1> : (void*)k_dense_krylov2<false, kMaxUse - 1>;
+  }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
   if (e != cudaSuccess) throw std::runtime_error(std::string("dense inner solver attribute: ") + cudaGetErrorString(e));
   DenseKrylovArgs a = args;

@@ -24,7 +24,8 @@ struct DenseKrylovArgs {
   const double* wts = nullptr;        // [n] aggregation weight of position i
   const int32_t* cta_seg0 = nullptr;  // [grid] first segment of each CTA
   const int32_t* cseg = nullptr;      // [nc + 1] segments of cluster c: [cseg[c], cseg[c+1])
-  double* spart = nullptr;            // [n_segments] partial sums of w r
+  double* spart = nullptr;            // [3 n_segments] partial sums of w r (2 parities), of w Ap
+  double* zfull = nullptr;            // [n] preconditioned residual (two-barrier kernel)
   int n_segments = 0;
   const double* b = nullptr;   // rhs (original order)
   double* x = nullptr;         // solution (solver order)
@@ -51,5 +52,7 @@ struct DenseKrylovPlan {
 
 DenseKrylovPlan plan_dense_krylov(int n, int nc, int device);
 void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& args, cudaStream_t s);
+// true when launch_dense_krylov runs the two-barrier kernel for these args
+bool dense_two_barrier(const DenseKrylovArgs& a);
 
 }  // namespace rmg

@@ -1121,7 +1121,7 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
           d->wts.upload(wts.data(), wts.size(), s);
           d->cta_seg0.upload(cta_seg0.data(), cta_seg0.size(), s);
           d->cseg.upload(cseg.data(), cseg.size(), s);
-          d->spart.alloc(std::max<int32_t>(1, segs));
+          d->spart.alloc(std::max<int32_t>(1, 3 * segs));
           d->xp.alloc(std::max<int64_t>(1, n));
         }
       }
@@ -1136,6 +1136,7 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
     }
     padk("RMG_PAD_P");
     d->pap_ring.alloc(kMaxKeep + 2);
+    d->zfull.alloc(std::max<int64_t>(1, n));
     // own 2 MB-granular allocation: the cross-CTA partials are read by every CTA
     // after every grid barrier, so their placement is on the critical path
     d->partials.alloc(std::max<size_t>(static_cast<size_t>(d->plan.grid) * d->plan.partial_stride, 262144));
@@ -1175,6 +1176,7 @@ DenseKrylovArgs Method::dense_args(size_t k, const double* rhs) {
     a.spart = d.spart.get();
     a.x = d.xp.get();
   }
+  a.zfull = d.zfull.get();
   a.r = w.r.get();
   a.p_ring = w.p_ring.get();
   a.ap_ring = w.ap_ring.get();

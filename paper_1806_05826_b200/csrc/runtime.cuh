@@ -248,7 +248,7 @@ struct DenseInner {
   bool lowrank = false;
   int n_segments = 0;
   DBuf<int32_t> perm, cid, cta_seg0, cseg;
-  DBuf<double> wts, spart, xp;
+  DBuf<double> wts, spart, xp, zfull;
   std::vector<float> tuned_ms;      // partials placement candidates (ms per 40 iterations)
   int tuned_pick = 0;
 };
