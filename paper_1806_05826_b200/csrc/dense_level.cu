@@ -210,6 +210,91 @@ __device__ __forceinline__ void gemv_narrow(const double (&q)[28], int nr, doubl
   __syncthreads();
 }
 
+
+// Warp reduce-scatter of NR (16 or 32) per-lane row partials: after it lane L
+// holds the warp sum of row L >> (NR == 16 ? 1 : 0) in acc[0] (16: lanes 2r and
+// 2r + 1 both hold row r).  NR - 1 shuffles instead of 5 NR for NR warp trees;
+// fixed order, deterministic.
+template <int NR>
+__device__ __forceinline__ double warp_rows_sum(double (&acc)[NR]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = NR / 2, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const double send = hi ? acc[k] : acc[k + w];
+      const double keep = hi ? acc[k + w] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  if (NR == 16) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+  return acc[0];
+}
+
+// Row sums of (rows x v) for nr <= 32 owned rows, all rows' loads in flight at
+// once and one reduce-scatter per warp (gemv_rows does 4 rows and 4 warp trees
+// at a time).  Same contract as gemv_rows.
+template <bool GLOBAL, int NQ>
+__device__ __forceinline__ void gemv_rows_rs(const double* rows, int nr, int n, const double (&vc)[NQ], double* red,
+                                             double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, tid = threadIdx.x;
+  for (int lr0 = 0; lr0 < nr; lr0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = tid + q * kT;
+      if (c < n) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double* row = rows + (size_t)min(lr0 + u, nr - 1) * n;
+          acc[u] += (GLOBAL ? __ldg(row + c) : row[c]) * vc[q];
+        }
+      }
+    }
+    const double sr = warp_rows_sum<16>(acc);
+    const int lr = lr0 + (lane >> 1);
+    if ((lane & 1) == 0 && lr < nr) red[lr * kW + wid] = sr;
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
+
+// gemv_narrow with the reduce-scatter (nr <= RM: 16 or 28).
+template <int RM>
+__device__ __forceinline__ void gemv_narrow_rs(const double (&q)[RM], int nr, double sv, double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, tid = threadIdx.x;
+  if (RM <= 16) {
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = q[u < RM ? u : 0] * sv;
+    const double s = warp_rows_sum<16>(acc);
+    if ((lane & 1) == 0 && (lane >> 1) < nr) red[(lane >> 1) * kW + wid] = s;
+  } else {
+    double acc[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) acc[u] = u < RM ? q[u < RM ? u : 0] * sv : 0.0;
+    const double s = warp_rows_sum<32>(acc);
+    if (lane < nr) red[lane * kW + wid] = s;
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
+
 // Optional phase timing (diagnostics): %globaltimer of CTA 0 at phase marks
 // of the first 16 iterations, when args.timing != nullptr.
 __device__ __forceinline__ void tmark(const DenseKrylovArgs& a, int it, int idx) {
@@ -496,8 +581,13 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
 // an iteration after the update; iteration counts, history and breakdown
 // exits are those of k_dense_krylov.  Own-row work (nr <= 28) is warp 0:
 // its reductions are warp sums.
-template <bool SMEM, int HM>  // HM >= truncation (history directions held per lane)
+// HM >= truncation (history directions held per lane); NQ = columns per thread
+// (n <= NQ * kT) and RM >= owned rows: compile-time so the unrolled loop body
+// stays small enough for the instruction cache (measured: no_inst stalls at
+// NQ = 16 on n = 2000).
+template <bool SMEM, int HM, int NQ>
 __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
+  constexpr int RM = NQ <= 8 ? 16 : 28;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double smem[];
   const int n = a.n, R = a.rows_per_cta;
@@ -543,6 +633,10 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
       segment_partials(seg, ri, a.spart);
     }
   }
+  double q[RM];  // this thread's column of the owned rows of Q, held for the whole solve
+#pragma unroll
+  for (int lr = 0; lr < RM; ++lr)
+    q[lr] = (a.lowrank && a.nc <= kT && lr < nr && tid < a.nc) ? __ldg(Qrows + (size_t)lr * a.nc + tid) : 0.0;
   int cs0 = 0, cs1 = 0;  // this thread's cluster segments (nc <= kT)
   if (a.lowrank && a.nc <= kT && tid < a.nc) {
     cs0 = __ldg(a.cseg + tid);
@@ -578,14 +672,16 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
   for (int it = 0;; ++it) {
     tmark(a, it, 0);
     // ======== phase 1: alpha, x/r update (direction it-1), z_it
-    double q[28];
+    const int mi = it == 0 ? 0 : max(1, it % (keep + 1));
+    const int use = a.fcg ? min(mi, min(it, keep)) : 0;
+    double ygs[4];  // own rows of the Ap_q for the Gram-Schmidt dots, in flight first
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int qd = wid + j * kW;
+      ygs[j] = (qd < use && lane < nr) ? __ldcg(a.ap_ring + (size_t)((it - use + qd) % RING) * n + i) : 0.0;
+    }
     double sg[2] = {0.0, 0.0}, sa[2] = {0.0, 0.0};
     if (a.lowrank) {
-      if (a.nc <= kT) {
-#pragma unroll
-        for (int lr = 0; lr < 28; ++lr)
-          q[lr] = (lr < nr && tid < a.nc) ? __ldg(Qrows + (size_t)lr * a.nc + tid) : 0.0;
-      }
       const double* sp = a.spart + (it > 0 ? ((it - 1) & 1) * nseg : 0);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -630,7 +726,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
       if (a.nc <= kT) {
         double sum = 0.0;
         for (int g = cs0; g < cs1; ++g) sum += contrib[g];
-        gemv_narrow(q, nr, sum, red, vv);
+        gemv_narrow_rs<RM>(q, nr, sum, red, vv);
       } else {
         double sv[kMaxQ];
 #pragma unroll
@@ -647,8 +743,6 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     }
     tmark(a, it, 2);
     // ---- publish z, ||r||^2, Gram-Schmidt dots <z, Ap_q> (krylov.cpp:189-197)
-    const int mi = it == 0 ? 0 : max(1, it % (keep + 1));
-    const int use = a.fcg ? min(mi, min(it, keep)) : 0;
     if (wid == 0) {
       if (own) {
         a.zfull[i] = zi;
@@ -659,16 +753,9 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     }
     if (use > 0) {
       __syncthreads();
-      double y[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int qd = wid + j * kW;
-        const double* aph = a.ap_ring + (size_t)((it - use + qd) % RING) * n;
-        y[j] = (qd < use && lane < nr) ? zs[lane] * __ldcg(aph + row0 + lane) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double acc = wsum(y[j]);
+        const double acc = wsum(lane < nr ? zs[lane] * ygs[j] : 0.0);
         if (lane == 0 && wid + j * kW < use) part(kGS2 + wid + j * kW) = acc;
       }
     }
@@ -676,9 +763,9 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     grid.sync();  // B1
     tmark(a, it, 4);
     // ======== phase 2: convergence of r_it; direction it
-    double pc[kMaxQ];
+    double pc[NQ];
 #pragma unroll
-    for (int qq = 0; qq < kMaxQ; ++qq) {
+    for (int qq = 0; qq < NQ; ++qq) {
       const int c = tid + qq * kT;
       pc[qq] = c < n ? __ldcg(a.zfull + c) : 0.0;
     }
@@ -719,11 +806,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     }
     if (tid < use) coef[tid] = gsum[1 + tid] / den;
     // A z for the owned rows (ends with __syncthreads: coef and vv visible)
-    if (SMEM) {
-      gemv_rows<false>(Arows, nr, n, pc, red, vv);
-    } else {
-      gemv_rows<true>(Arows, nr, n, pc, red, vv);
-    }
+    gemv_rows_rs<!SMEM, NQ>(Arows, nr, n, pc, red, vv);
     tmark(a, it, 6);
     if (wid < 2) {  // warp 0: p = z - c_0 p_0 - c_1 p_1 - ... (reference order); warp 1: Ap alike
       double v = wid == 0 ? zi : (lane < nr ? vv[lane] : 0.0);
@@ -810,10 +893,15 @@ void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& arg
     throw std::runtime_error("dense inner solver: too few SMs for this level");
   void* fn = plan.smem_a ? (void*)k_dense_krylov<true> : (void*)k_dense_krylov<false>;
   if (dense_two_barrier(args)) {
-    if (args.keep <= 20)
-      fn = plan.smem_a ? (void*)k_dense_krylov2<true, 20> : (void*)k_dense_krylov2<false, 20>;
+    const bool small = args.n <= 8 * kT && plan.rows_per_cta <= 16;
+    const bool h20 = args.keep <= 20;
+    if (small)
+      fn = h20 ? (plan.smem_a ? (void*)k_dense_krylov2<true, 20, 8> : (void*)k_dense_krylov2<false, 20, 8>)
+               : (plan.smem_a ? (void*)k_dense_krylov2<true, kMaxUse - 1, 8> : (void*)k_dense_krylov2<false, kMaxUse - 1, 8>);
     else
-      fn = plan.smem_a ? (void*)k_dense_krylov2<true, kMaxUse - 1> : (void*)k_dense_krylov2<false, kMaxUse - 1>;
+      fn = h20 ? (plan.smem_a ? (void*)k_dense_krylov2<true, 20, kMaxQ> : (void*)k_dense_krylov2<false, 20, kMaxQ>)
+               : (plan.smem_a ? (void*)k_dense_krylov2<true, kMaxUse - 1, kMaxQ>
+                              : (void*)k_dense_krylov2<false, kMaxUse - 1, kMaxQ>);
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes);
   if (e != cudaSuccess) throw std::runtime_error(std::string("dense inner solver attribute: ") + cudaGetErrorString(e));

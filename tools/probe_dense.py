@@ -23,11 +23,16 @@ if os.environ.get("RMG_DENSE_TIMING"):
     lib.rmg_debug_dense_timing.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
     if lib.rmg_debug_dense_timing(pm.h, 1, buf) == 0:
         t = np.array(buf[:256], dtype=np.float64).reshape(16, 16)
-        names = ["start", "z(Mr)", "GSdots", "B1", "gsums", "p", "B2", "Ap", "pap", "B3", "gsums2", "upd", "B4", "gsums3"]
+        if os.environ.get("RMG_DENSE_4B"):
+            names = ["start", "z(Mr)", "GSdots", "B1", "gsums", "p", "B2", "Ap", "pap", "B3", "gsums2", "upd", "B4", "gsums3"]
+        else:  # two-barrier kernel (k_dense_krylov2): marks 0..7, then the next iteration's 0
+            names = ["start", "pap sums+upd", "S, z", "publish", "B1", "loads+sums", "A z", "p, Ap, publish"]
+        nm_ = len(names)
         rows = t[4:15]  # iterations 4..14 (all phases present)
-        deltas = np.diff(rows[:, :14], axis=1)
-        for i, nm in enumerate(names[1:]):
-            print(f"  phase {nm:>7}: {np.mean(deltas[:, i]) / 1e3:7.3f} us")
+        nxt = t[5:16, 0:1]
+        deltas = np.diff(np.concatenate([rows[:, :nm_], nxt], axis=1), axis=1)
+        for i, nm in enumerate(names[1:] + ["B3/B4 -> next"]):
+            print(f"  phase {nm:>15}: {np.mean(deltas[:, i]) / 1e3:7.3f} us")
         print("  iteration:", np.mean(np.diff(rows[:, 0])) / 1e3, "us")
         arr = np.array(buf[256:512], dtype=np.float64)
         arr = arr[arr > 0]
