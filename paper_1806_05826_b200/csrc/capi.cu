@@ -2,6 +2,7 @@
 // point translates C++ exceptions into the status codes of the header and
 // keeps the message in a thread-local buffer (rmg_last_error).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -20,6 +21,7 @@ struct rmg_matrix {
   rmg_matrix(rmg::Context* ctx, rmg::HostCsr h, bool detect, rmg::Comm* comm = nullptr,
              const rmg::DenseInput* din = nullptr)
       : m(ctx, std::move(h), detect, comm, din) {}
+  rmg_matrix(rmg::Context* ctx, int64_t n, int64_t f, const rmg::DenseInput& din) : m(ctx, n, f, din) {}
 };
 struct rmg_host_csr {
   rmg::HostCsr h;
@@ -226,7 +228,10 @@ int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n, uint64_t f, const void
     din.fp32 = fp32 != 0;
     din.ld = static_cast<int64_t>(ld);
     RMG_CK(cudaSetDevice(ctx->c.device));
-    *out = new rmg_matrix(&ctx->c, dense_to_csr(n, f, data, ld, fp32), false, nullptr, &din);
+    if (std::getenv("RMG_DENSE_HOST_SETUP") != nullptr)  // diagnostics: setup from a host CSR view
+      *out = new rmg_matrix(&ctx->c, dense_to_csr(n, f, data, ld, fp32), false, nullptr, &din);
+    else  // no host CSR, hierarchy setup on the device
+      *out = new rmg_matrix(&ctx->c, static_cast<int64_t>(n), static_cast<int64_t>(f), din);
   });
 }
 
@@ -659,7 +664,28 @@ int rmg_method_level_matrix(const rmg_method* pm, uint64_t level, uint64_t* rp, 
     need(pm, "method");
     const auto lk_ = hold(pm->m.fine()->ctx);
     if (level >= static_cast<uint64_t>(pm->m.n_levels())) throw rmg::InvalidArgument("level index out of range");
-    const rmg::HostCsr& h = pm->m.level_matrix(level).host;
+    rmg::Matrix& mk = pm->m.level_matrix(level);
+    if (mk.device_setup()) {  // device-resident dense level: every stored entry, row-major (nnz = N x F)
+      const rmg::DenseDev& d = mk.dense->view;
+      std::vector<double> buf(static_cast<size_t>(d.rows) * d.ld);
+      if (d.fp32) {
+        std::vector<float> fb(buf.size());
+        if (!fb.empty()) RMG_CK(cudaMemcpy(fb.data(), d.data, fb.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < fb.size(); ++q) buf[q] = fb[q];
+      } else if (!buf.empty()) {
+        RMG_CK(cudaMemcpy(buf.data(), d.data, buf.size() * 8, cudaMemcpyDeviceToHost));
+      }
+      for (int64_t i = 0; i < d.rows; ++i) {
+        if (rp) rp[i] = static_cast<uint64_t>(i * d.cols);
+        for (int64_t j = 0; j < d.cols; ++j) {
+          if (ci) ci[i * d.cols + j] = static_cast<uint64_t>(j);
+          if (v) v[i * d.cols + j] = buf[i * d.ld + j];
+        }
+      }
+      if (rp) rp[d.rows] = static_cast<uint64_t>(d.rows * d.cols);
+      return;
+    }
+    const rmg::HostCsr& h = mk.host_csr();
     if (rp)
       for (int64_t i = 0; i <= h.n; ++i) rp[i] = static_cast<uint64_t>(h.ptr[i]);
     if (ci)

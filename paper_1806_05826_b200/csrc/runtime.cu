@@ -10,6 +10,7 @@
 
 #include "runtime.cuh"
 #include "fgmres.cuh"
+#include "dense_setup.hpp"
 #include "kmeans_gpu.hpp"
 
 namespace rmg {
@@ -496,6 +497,117 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k) {
   ctx->sync();
 }
 
+// Dense X kept on the device: rows padded to ld = F rounded up to 4 elements
+// (16 B aligned rows), the fused single-sweep operator's scratch.
+void Matrix::init_dense(DBuf<char>&& data, int fp32, int64_t ld, int64_t rows) {
+  if (host.f > kDenseMaxCols) throw InvalidArgument("dense X: more than 1024 features (use CSR)");
+  pattern = false;
+  auto d = std::make_unique<DenseStore>();
+  d->data = std::move(data);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  d->view.n_cta = sms;
+  d->partial.alloc(static_cast<size_t>(std::max<int64_t>(1, host.f)) * sms);
+  d->view.fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, (host.f + 7) / 8)));
+  d->fin_slots.alloc(static_cast<size_t>(d->view.fin_grid) * 2);
+  d->fin_ticket.alloc(1);
+  RMG_CK(cudaMemsetAsync(d->fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
+  RMG_CK(cudaStreamSynchronize(ctx->stream));
+  d->view.data = d->data.get();
+  d->view.fp32 = fp32;
+  d->view.ld = ld;
+  d->view.rows = rows;
+  d->view.cols = host.f;
+  d->view.partial = d->partial.get();
+  d->view.fin_slots = d->fin_slots.get();
+  d->view.fin_ticket = d->fin_ticket.get();
+  dense = std::move(d);
+  t.alloc(std::max<int64_t>(1, rows));
+  gram_sc.alloc(1);
+}
+
+void Matrix::init_dense_from_host(const void* data, int fp32, int64_t ld_in, int64_t rows) {
+  if (host.f > kDenseMaxCols) throw InvalidArgument("dense X: more than 1024 features (use CSR)");
+  const size_t esz = fp32 ? 4 : 8;
+  const int64_t ld = (host.f + 3) / 4 * 4;
+  DBuf<char> dev(std::max<size_t>(1, static_cast<size_t>(rows) * ld * esz));
+  // staged through a pinned buffer in row blocks (16 B aligned padded rows)
+  const int64_t block = std::max<int64_t>(1, (64ll << 20) / std::max<int64_t>(1, ld * esz));
+  char* stage = nullptr;
+  RMG_CK(cudaMallocHost(&stage, static_cast<size_t>(std::min(block, std::max<int64_t>(rows, 1))) * ld * esz));
+  try {
+    for (int64_t r0 = 0; r0 < rows; r0 += block) {
+      const int64_t nr = std::min(block, rows - r0);
+      RMG_CK(cudaStreamSynchronize(ctx->stream));  // the staging buffer is free again
+      std::memset(stage, 0, static_cast<size_t>(nr) * ld * esz);
+      for (int64_t i = 0; i < nr; ++i)
+        std::memcpy(stage + static_cast<size_t>(i) * ld * esz,
+                    static_cast<const char*>(data) + static_cast<size_t>(r0 + i) * ld_in * esz,
+                    static_cast<size_t>(host.f) * esz);
+      RMG_CK(cudaMemcpyAsync(dev.get() + static_cast<size_t>(r0) * ld * esz, stage, static_cast<size_t>(nr) * ld * esz,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    }
+    RMG_CK(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaFreeHost(stage);
+    throw;
+  }
+  cudaFreeHost(stage);
+  init_dense(std::move(dev), fp32, ld, rows);
+}
+
+// Dense X without a host CSR: setup runs on the device.
+Matrix::Matrix(Context* c, int64_t n, int64_t f, const DenseInput& din) : ctx(c) {
+  host.n = n;
+  host.f = f;
+  host_ok = false;
+  if (din.ld < f) throw InvalidArgument("dense X: leading dimension below the feature count");
+  RMG_CK(cudaSetDevice(ctx->device));
+  row0 = 0;
+  row1 = n;
+  init_dense_from_host(din.data, din.fp32, din.ld, n);
+}
+
+Matrix::Matrix(Context* c, int64_t n, int64_t f, DBuf<char>&& data, int fp32, int64_t ld) : ctx(c) {
+  host.n = n;
+  host.f = f;
+  host_ok = false;
+  RMG_CK(cudaSetDevice(ctx->device));
+  row0 = 0;
+  row1 = n;
+  init_dense(std::move(data), fp32, ld, n);
+}
+
+// The canonical CSR of a device-resident dense X (exact zeros not stored, as
+// dense_to_csr), built on first use by host-only setup (leader-follower).
+const HostCsr& Matrix::host_csr() {
+  if (host_ok) return host;
+  const DenseDev& v = dense->view;
+  const size_t esz = v.fp32 ? 4 : 8;
+  std::vector<char> buf(static_cast<size_t>(v.rows) * v.ld * esz);
+  if (!buf.empty())
+    RMG_CK(cudaMemcpyAsync(buf.data(), v.data, buf.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  RMG_CK(cudaStreamSynchronize(ctx->stream));
+  HostCsr h;
+  h.n = v.rows;
+  h.f = v.cols;
+  h.ptr.assign(h.n + 1, 0);
+  for (int64_t i = 0; i < h.n; ++i) {
+    for (int64_t j = 0; j < h.f; ++j) {
+      const double x = v.fp32 ? static_cast<double>(reinterpret_cast<const float*>(buf.data())[i * v.ld + j])
+                              : reinterpret_cast<const double*>(buf.data())[i * v.ld + j];
+      if (x != 0.0) {
+        h.idx.push_back(j);
+        h.val.push_back(x);
+      }
+    }
+    h.ptr[i + 1] = h.nnz();
+  }
+  host = std::move(h);
+  host_ok = true;
+  return host;
+}
+
 Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din)
     : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
@@ -528,40 +640,9 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
   }
   const HostCsr& local = comm != nullptr ? shard : host;
   if (din != nullptr) {  // dense X: one row-major device copy, fused single-sweep operator
-    if (host.f > kDenseMaxCols) throw InvalidArgument("dense X: more than 1024 features (use CSR)");
     if (din->ld < host.f) throw InvalidArgument("dense X: leading dimension below the feature count");
-    pattern = false;
-    auto d = std::make_unique<DenseStore>();
-    const size_t esz = din->fp32 ? 4 : 8;
-    const int64_t nl = local.n;
-    // stored with ld = F rounded up to 4 elements (16 B aligned rows)
-    const int64_t ld = (host.f + 3) / 4 * 4;
-    std::vector<char> buf(static_cast<size_t>(nl) * ld * esz, 0);
-    const char* src = static_cast<const char*>(din->data) + static_cast<size_t>(row0) * din->ld * esz;
-    for (int64_t i = 0; i < nl; ++i)
-      std::memcpy(&buf[static_cast<size_t>(i) * ld * esz], src + static_cast<size_t>(i) * din->ld * esz,
-                  static_cast<size_t>(host.f) * esz);
-    d->data.upload(buf.data(), buf.size(), ctx->stream);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    d->view.n_cta = sms;
-    d->partial.alloc(static_cast<size_t>(std::max<int64_t>(1, host.f)) * sms);
-    d->view.fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, (host.f + 7) / 8)));
-    d->fin_slots.alloc(static_cast<size_t>(d->view.fin_grid) * 2);
-    d->fin_ticket.alloc(1);
-    RMG_CK(cudaMemsetAsync(d->fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
-    RMG_CK(cudaStreamSynchronize(ctx->stream));
-    d->view.data = d->data.get();
-    d->view.fp32 = din->fp32;
-    d->view.ld = ld;
-    d->view.rows = nl;
-    d->view.cols = host.f;
-    d->view.partial = d->partial.get();
-    d->view.fin_slots = d->fin_slots.get();
-    d->view.fin_ticket = d->fin_ticket.get();
-    dense = std::move(d);
-    t.alloc(std::max<int64_t>(1, local.n));
-    gram_sc.alloc(1);
+    const char* src = static_cast<const char*>(din->data) + static_cast<size_t>(row0) * din->ld * (din->fp32 ? 4 : 8);
+    init_dense_from_host(src, din->fp32, din->ld, local.n);
     return;
   }
   // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
@@ -885,20 +966,49 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
   double beta_run = beta;
   for (uint64_t k = 0; k < L; ++k) {
     auto t0 = tnow();
-    const HostCsr& cur = level_matrix(k).host;
+    Matrix& curm = level_matrix(k);
+    const int64_t cur_f = curm.f();
+    // dense X without a host CSR: k-means, X_c = X P and the Gram matrices on
+    // the device, bit-identical to the host restatement
+    const bool dev = curm.device_setup();
     if (levels[k].clustering_kind == RMG_CLUSTER_IMPORTED)
-      specs_[k].labels.assign(levels[k].labels, levels[k].labels + cur.f);
+      specs_[k].labels.assign(levels[k].labels, levels[k].labels + cur_f);
     const double next_beta = specs_[k].spec.has_beta_override ? specs_[k].spec.beta_override : beta_run;
     int64_t nc = 0;
-    std::vector<int64_t> lab = run_clustering(cur, specs_[k], &nc, s);
+    std::vector<int64_t> lab;
+    const rmg_level_spec& cs = specs_[k].spec;
+    if (dev && cs.clustering_kind == RMG_CLUSTER_KMEANS) {
+      const int64_t k_c = static_cast<int64_t>(cs.target_size);
+      if (k_c < 1 || k_c > cur_f) throw InvalidArgument("kmeans: k outside [1, F]");
+      const int64_t ldx = (cur_f + 1) / 2 * 2;
+      DBuf<double> xc(static_cast<size_t>(std::max<int64_t>(1, curm.n())) * ldx);
+      dense_columns_f64(s, curm.dense->view, cs.normalize_columns != 0, xc.get(), ldx);
+      Clustering c = kmeans_dense_gpu(s, xc.get(), curm.n(), cur_f, ldx, k_c, cs.kmeans_max_iters, cs.seed);
+      nc = c.n_clusters;
+      lab = std::move(c.labels);
+    } else if (dev && cs.clustering_kind == RMG_CLUSTER_IMPORTED) {
+      if (static_cast<int64_t>(specs_[k].labels.size()) != cur_f)
+        throw InvalidArgument("imported labels: expected one label per feature of the level");
+      nc = static_cast<int64_t>(cs.n_clusters);
+      lab = specs_[k].labels;
+    } else {
+      lab = run_clustering(curm.host_csr(), specs_[k], &nc, s);
+    }
     tlog("clustering", k, t0);
     t0 = tnow();
-    if (nc >= cur.f)
+    if (nc >= cur_f)
       throw InvalidArgument("build_hierarchy: level " + std::to_string(k + 1) + " has " + std::to_string(nc) +
-                            " clusters, not smaller than its fine level (" + std::to_string(cur.f) + " features)");
+                            " clusters, not smaller than its fine level (" + std::to_string(cur_f) + " features)");
     auto lvl = std::make_unique<CoarseLevelDev>();
     lvl->agg = make_aggregation(lab, nc);
-    lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(cur, lvl->agg), true);
+    if (dev) {
+      const int64_t ldc = (nc + 3) / 4 * 4;
+      DBuf<char> xcd(std::max<size_t>(1, static_cast<size_t>(curm.n()) * ldc * sizeof(double)));
+      coarsen_dense_gpu(s, curm.dense->view, lvl->agg, reinterpret_cast<double*>(xcd.get()), ldc);
+      lvl->mat = std::make_unique<Matrix>(ctx_, curm.n(), nc, std::move(xcd), 0, ldc);
+    } else {
+      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(curm.host_csr(), lvl->agg), true);
+    }
     lvl->beta = next_beta;
     lvl->label.upload(lvl->agg.label.data(), lvl->agg.label.size(), s);
     lvl->weight.upload(lvl->agg.weight.data(), lvl->agg.weight.size(), s);
@@ -907,7 +1017,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     {
       HostCsr pt;  // P^T: row s lists the members of cluster s in increasing order
       pt.n = nc;
-      pt.f = cur.f;
+      pt.f = cur_f;
       pt.ptr.assign(lvl->agg.mptr.begin(), lvl->agg.mptr.end());
       pt.idx.assign(lvl->agg.members.begin(), lvl->agg.members.end());
       pt.val.resize(pt.idx.size());
@@ -944,7 +1054,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
   // coarsest dense solve (krylov.cpp:349-376), through A_c^{-1}
   {
     auto t0 = tnow();
-    const std::vector<double> ac = coarse_gram(coarse_.back()->mat->host, coarse_.back()->beta);
+    const std::vector<double> ac = level_gram(*coarse_.back()->mat, coarse_.back()->beta);
     const std::vector<double> inv =
         spd_inverse(ac, fc_last, "level " + std::to_string(L - 1) + " -> " + std::to_string(L));
     ainv_.upload(inv.data(), inv.size(), s);
@@ -974,6 +1084,18 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     tlog("tune", L, t0);
   }
   ctx_->sync();
+}
+
+// X_k^T X_k + beta I (coarse_gram, krylov.cpp:350-365): on the device for a
+// device-resident dense level (the beta-free sums cached: adding beta to the
+// diagonal after the sums is what coarse_gram does, so a beta sweep reuses them)
+std::vector<double> Method::level_gram(Matrix& m, double beta) {
+  if (!m.device_setup()) return coarse_gram(m.host_csr(), beta);
+  if (m.gram_cache.empty()) m.gram_cache = gram_dense_gpu(ctx_->stream, m.dense->view);
+  std::vector<double> a = m.gram_cache;
+  const int64_t n = m.f();
+  for (int64_t i = 0; i < n; ++i) a[i * n + i] += beta;
+  return a;
 }
 
 // JacobiPreconditioner (krylov.cpp:41-47): inverse of beta + diag(X^T X)
@@ -1016,7 +1138,7 @@ void Method::set_beta(double beta) {
   for (size_t k = 0; k < L; ++k)
     if (!specs_[k].spec.has_omega_override) omega_[k] = 2.0 / (level_beta(k) + lambda_[k]);
   const int64_t fc_last = coarse_.back()->mat->f();
-  const std::vector<double> ac = coarse_gram(coarse_.back()->mat->host, coarse_.back()->beta);
+  const std::vector<double> ac = level_gram(*coarse_.back()->mat, coarse_.back()->beta);
   const std::vector<double> inv = spd_inverse(ac, fc_last, "level " + std::to_string(L - 1) + " -> " + std::to_string(L));
   ainv_.upload(inv.data(), inv.size(), ctx_->stream);
   dense_.clear();
@@ -1043,7 +1165,7 @@ void Method::build_dense_levels(const std::vector<double>& ainv_host) {
     auto d = std::make_unique<DenseInner>();
     d->fcg = fcg;
     d->omega = omega_[k];
-    const std::vector<double> a = coarse_gram(level_matrix(k).host, level_beta(k));  // X_k^T X_k + beta_k I
+    const std::vector<double> a = level_gram(level_matrix(k), level_beta(k));  // X_k^T X_k + beta_k I
     auto padk = [&](const char* name) {  // diagnostics: shift one buffer group
       if (const char* e = std::getenv(name)) {
         pads_.emplace_back();

@@ -190,12 +190,22 @@ struct Matrix {
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
+  // dense X without a host CSR (setup on the device): from host
+  // rows, or from a device buffer already padded to ld (coarse levels)
+  Matrix(Context* c, int64_t n, int64_t f, const DenseInput& din);
+  Matrix(Context* c, int64_t n, int64_t f, DBuf<char>&& data, int fp32, int64_t ld);
+  bool host_ok = true;  // host holds the CSR view
+  const HostCsr& host_csr();  // built from the device copy on first use
+  bool device_setup() const { return dense != nullptr && comm == nullptr && !host_ok; }
+  std::vector<double> gram_cache;  // X^T X of a device-resident level (beta-independent)
+  void init_dense(DBuf<char>&& data, int fp32, int64_t ld, int64_t rows);
+  void init_dense_from_host(const void* data, int fp32, int64_t ld_in, int64_t rows);
   void build_hot(const HostCsr& ht, int64_t n_samples);
   int64_t n_local() const { return row1 - row0; }
   void allreduce_sums(double* sendbuf, double* recvbuf, int64_t count);
   int64_t n() const { return host.n; }
   int64_t f() const { return host.f; }
-  int64_t nnz() const { return host.nnz(); }
+  int64_t nnz() const { return host_ok ? host.nnz() : host.n * host.f; }
   // t = X v then the X^T epilogue; v may live in a ring (sc != nullptr)
   void apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof = nullptr);
   void apply_ring(const double* v_ring, int stride, const KrylovScalars* sc, Epi epi, const XtArgs& args,
@@ -305,6 +315,7 @@ class Method {
   uint64_t run_dense(size_t k, const double* rhs);
   uint64_t run_fgmres(const double* rhs, SolveResult* out);
   void jacobi_diag();
+  std::vector<double> level_gram(Matrix& m, double beta);
   DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);
   void tune_dense_partials(size_t k);
