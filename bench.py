@@ -40,6 +40,12 @@ CONFIGS = {
                  "beta=1; outer FCG(m=20) to rel. residual 1e-6",
         kind="zipf", n=100000, f=20000, mean=40.0, zipf=1.1, abs_values=False, seed=0, beta=1.0,
         ks=[2000, 200], normalize=True, method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg2_full"),
+    "cfg4": dict(
+        workload="cfg4: dense tall-skinny N=4,000,000 x F=1024, fp32 storage / fp64 arithmetic, X = U diag(i^-1.5) "
+                 "V^T + 1e-3 N(0,1); 3-level hierarchy k-means(unit-normalised columns, seed 0) 128/16 (setup on "
+                 "the device, DESIGN.md §4.9), inner FCG tol 1e-6; beta=1e-4; outer FCG(m=20) to rel. residual 1e-6",
+        kind="lowrank", n=4_000_000, f=1024, seed=0, beta=1e-4, ks=[128, 16], normalize=True,
+        method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg4_none", ref_rows=50_000),
     "cfg1": dict(
         workload="cfg1: dense clustered N=2000 x F=500 fp64 (row-major dense path); 2-level k-means 50; beta=1e-2; "
                  "FCG(m=20) to rel. residual 1e-6",
@@ -57,8 +63,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
+class DenseX:
+    """A dense synthetic X (cfg 4): shape plus the row-major array (fp32 storage)."""
+
+    def __init__(self, a):
+        self.a = a
+        self.n_samples, self.n_features = a.shape
+
+    def dense(self):
+        return self.a
+
+    def row_sample(self, rows):
+        """CSR of the first `rows` samples (fp32 values widened exactly): the
+        bounded CPU-baseline workload (the reference's CSR of all 4M rows is 65 GB)."""
+        import paper_1806_05826_b200 as R
+        return R.from_dense(self.a[:rows].astype(np.float64))
+
+
 def make_matrix(cfg):
     import paper_1806_05826_b200 as R
+    if cfg["kind"] == "lowrank":
+        return DenseX(cfg4_shard_matrix(n=cfg["n"], f=cfg["f"], seed=cfg["seed"]))
     if cfg["kind"] == "zipf":
         return R.synth_sparse_zipf(cfg["n"], cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"])
     return R.synth_dense_clustered(cfg["n"], cfg["f"], cfg["groups"], cfg["noise"], cfg["seed"])
@@ -178,12 +203,29 @@ def reference_solve_sample(cfg, x, labels, threads, sample_iters, rhs_seed=42):
     return s.wall_time_s / max(1, s.iterations), kind, s.iterations
 
 
+def lowrank_sample_labels(cfg):
+    """cfg 4's CPU sample imports round-robin clusters of the configured sizes: the
+    reference's per-iteration cost on dense X does not depend on which features
+    share a cluster (its k-means on 1024 x 50k would dominate the sample)."""
+    labels, f = [], cfg["f"]
+    for k in cfg["ks"]:
+        labels.append(np.arange(f, dtype=np.int64) % k)
+        f = k
+    return labels
+
+
 def run_reference_arm(args, cfg):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
     x = make_matrix(cfg)
-    labels = load_golden_labels(cfg)
+    scale, iters_fixed = 1.0, None
+    if cfg["kind"] == "lowrank":  # bounded sample: the first ref_rows samples, solved to tolerance
+        scale = x.n_samples / cfg["ref_rows"]
+        x = x.row_sample(cfg["ref_rows"])
+        labels = lowrank_sample_labels(cfg)
+    else:
+        labels = load_golden_labels(cfg)
     if labels is None:
         import oracle
         o = oracle.Checker("oracle")
@@ -204,14 +246,19 @@ def run_reference_arm(args, cfg):
             full_iters = int(gz[key])
     per_iter = []
     t0 = time.time()
+    sample_iters = args.ref_sample_iters if cfg["kind"] != "lowrank" else cfg["max_iters"]
     for step in range(args.warmup + args.steps):
-        sec, kind, ran = reference_solve_sample(cfg, x, labels, threads, args.ref_sample_iters, 42 + step)
+        sec, kind, ran = reference_solve_sample(cfg, x, labels, threads, sample_iters, 42 + step)
         if step >= args.warmup:
             per_iter.append(sec)
     iters = full_iters or ran
-    value = statistics.mean(per_iter) * iters * 1e3
-    sample = (f"{args.ref_sample_iters} outer FCG iterations per step (setup untimed, the reference's own "
+    value = statistics.mean(per_iter) * iters * scale * 1e3
+    sample = (f"{sample_iters} outer FCG iterations per step (setup untimed, the reference's own "
               f"krylov.cpp timer), extrapolated x {iters} iterations")
+    if cfg["kind"] == "lowrank":
+        sample = (f"the first {cfg['ref_rows']} of {int(scale * cfg['ref_rows'])} samples as CSR, solved to "
+                  f"tolerance ({iters} iterations, reference timer), x {scale:.0f} rows (cost linear in N); "
+                  f"round-robin labels of the same cluster counts")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
@@ -319,7 +366,7 @@ def run_b200(args, cfg):
         if pg:
             pg.broadcast_object_list(obj, src=0)
         comm = R.Comm(ctx, world, rank, obj[0])
-    if cfg["kind"] == "dense":  # dense inputs take the fused single-sweep dense path
+    if cfg["kind"] in ("dense", "lowrank"):  # dense inputs: fused single-sweep dense path
         m = R.DeviceMatrix.from_dense(x.dense(), ctx, comm=comm)
     else:
         m = R.DeviceMatrix(x, ctx, comm=comm)
@@ -409,6 +456,10 @@ def run_b200(args, cfg):
         bytes_per_launch = inner_mean * 8 * (nk * nk + nk * nnext + 48 * nk)
         kernel_name = (f"k_dense_krylov: persistent level-{dom['level']} inner FCG (n={nk}, "
                        f"{inner_mean:.1f} iterations/launch), in-situ events")
+    elif m.is_dense():  # dense levels: one fused sweep (fine: its storage; device-built coarse levels: fp64)
+        esz = x.dense().itemsize if dom["level"] == 0 else 8
+        bytes_per_launch = dense_algorithmic_bytes(x.n_samples, dom["n_features"], esz)
+        kernel_name = f"level-{dom['level']} dense operator (k_dense_ata fused X^T X sweep + finish), in-situ events"
     else:
         pattern = m.is_pattern if dom["level"] == 0 else False
         bytes_per_launch = algorithmic_bytes(x.n_samples, dom["n_features"], dom["nnz"], pattern)
@@ -420,7 +471,12 @@ def run_b200(args, cfg):
     # cold / warm fine-operator timing (dedicated loop, L2 flushed or not)
     cold = pm.time_operator(0, 20, True)
     warm = pm.time_operator(0, 20, False)
-    fine_bytes = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
+    if m.is_dense():
+        fine_bytes = dense_algorithmic_bytes(x.n_samples, x.n_features, x.dense().itemsize)
+        op_kernel = "k_dense_ata (fused X^T X single sweep, 1D TMA tiles) + k_dense_finish"
+    else:
+        fine_bytes = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
+        op_kernel = "K1 (X v, SELL-32) + K2 (X^T pass, segmented)"
 
     # e2e: host buffers through the C ABI (H2D of b, D2H of w inside each step)
     pinned_b = [torch.from_numpy(R.rng_normals(42 + rseed + s, x.n_samples)).pin_memory()
@@ -445,11 +501,20 @@ def run_b200(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sec, kind, ran = reference_solve_sample(cfg, x, labels, 1, args.ref_sample_iters)
             iters = statistics.mean(r.iterations for r in timed)
-            cpu = {"value": sec * iters * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
-                   "sample": f"{ran} outer FCG iterations of the same solve (reference timer, setup untimed), "
-                             f"x {iters:.1f} iterations/solve"}
+            if cfg["kind"] == "lowrank":  # reference CSR of all rows would be 65 GB: a row sample, scaled
+                rows = cfg["ref_rows"]
+                sec, kind, ran = reference_solve_sample(cfg, x.row_sample(rows), lowrank_sample_labels(cfg), 1,
+                                                        cfg["max_iters"])
+                cpu = {"value": sec * ran * (x.n_samples / rows) * 1e3, "unit": "ms/solve", "cores": 1,
+                       "kind": kind,
+                       "sample": f"the first {rows} samples as CSR solved to tolerance ({ran} iterations, reference "
+                                 f"timer), x {x.n_samples / rows:.0f} (cost linear in N); round-robin labels"}
+            else:
+                sec, kind, ran = reference_solve_sample(cfg, x, labels, 1, args.ref_sample_iters)
+                cpu = {"value": sec * iters * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
+                       "sample": f"{ran} outer FCG iterations of the same solve (reference timer, setup untimed), "
+                                 f"x {iters:.1f} iterations/solve"}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -496,7 +561,7 @@ def run_b200(args, cfg):
                          "share_of_step": (dom['ms_k1'] + dom['ms_k2']) / (prof_step_ms or 1.0)},
             "operator_profile": prof,
             # the metric's second half: X^T X operator, fine level, L2 flushed before every apply
-            "operator_roofline": {"bound": "hbm", "kernel": "K1 (X v, SELL-32) + K2 (X^T pass, segmented)",
+            "operator_roofline": {"bound": "hbm", "kernel": op_kernel,
                                   "algorithmic_bytes_per_apply": fine_bytes, "ms_per_apply": cold[0],
                                   "achieved": fine_bytes / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
                                   "frac": fine_bytes / (cold[0] * 1e6) / peak, "warm_ms": warm[0],
