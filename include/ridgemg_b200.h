@@ -42,7 +42,7 @@ typedef struct rmg_context rmg_context;
 typedef struct rmg_matrix rmg_matrix;
 typedef struct rmg_method rmg_method;
 
-/* krylov.hpp:207 MethodKind (fgmres_twolevel is out of scope) */
+/* krylov.hpp:207 MethodKind */
 typedef enum {
   RMG_METHOD_CG = 0,
   RMG_METHOD_JACOBI_CG = 1,
@@ -56,6 +56,10 @@ typedef enum {
   RMG_CLUSTER_LEADER_TOLERANCE = 0,
   RMG_CLUSTER_LEADER_TARGET = 1,
   RMG_CLUSTER_KMEANS = 2,
+  /* extension for levels too large for the reference's k-means (BASELINE cfg 3 / 5,
+   * SURVEY App. A.8): the reference k-means on a sign sketch of the columns
+   * (d = sketch_dim <= 32 rows).  Not the reference's clustering. */
+  RMG_CLUSTER_KMEANS_SKETCH = 3,
   RMG_CLUSTER_IMPORTED = 100
 } rmg_clustering_kind;
 
@@ -92,6 +96,7 @@ typedef struct {
   double beta_override;
   int32_t has_omega_override; /* parity runs: import the oracle's omega_k */
   double omega_override;
+  uint64_t sketch_dim;        /* RMG_CLUSTER_KMEANS_SKETCH: rows of the sketch (0: 32) */
 } rmg_level_spec;
 
 /* krylov.hpp:25-31 SolveReport; history arrays are caller buffers (may be NULL). */
@@ -131,7 +136,9 @@ int rmg_matrix_destroy(rmg_matrix* m);
  * dense array becomes via csr_from_triplets, sparse.hpp:55-56).  data: host,
  * row-major n x f with leading dimension ld elements, fp64 (fp32 = 0) or fp32
  * storage (fp32 = 1; arithmetic stays fp64).  f <= 1024.  The operator is one
- * fused sweep over X; setup sees the same values as CSR. */
+ * fused sweep over X.  No host CSR is kept: the hierarchy setup
+ * (k-means, X_c = X P, coarse Gram) runs on the device with the same arithmetic as
+ * the CSR path; the sharded variant keeps the host CSR setup. */
 int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n_samples, uint64_t n_features, const void* data,
                             uint64_t ld, int32_t fp32, rmg_matrix** out);
 int rmg_matrix_is_dense(const rmg_matrix* m, int32_t* dense, int32_t* fp32);

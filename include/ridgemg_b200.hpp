@@ -59,7 +59,8 @@ struct SolveReport {
 // krylov.hpp:135-146 (+ imported labels for parity runs)
 struct ClusteringChoice {
   enum class Kind { leader_tolerance = RMG_CLUSTER_LEADER_TOLERANCE, leader_target = RMG_CLUSTER_LEADER_TARGET,
-                    kmeans = RMG_CLUSTER_KMEANS, imported = RMG_CLUSTER_IMPORTED };
+                    kmeans = RMG_CLUSTER_KMEANS, kmeans_sketch = RMG_CLUSTER_KMEANS_SKETCH,
+                    imported = RMG_CLUSTER_IMPORTED };
   Kind kind = Kind::leader_tolerance;
   double tolerance = 1.0;
   std::size_t target_size = 0;
@@ -68,6 +69,7 @@ struct ClusteringChoice {
   bool normalize_columns = false;
   std::vector<std::int64_t> labels;  // kind == imported
   std::size_t n_clusters = 0;
+  std::size_t sketch_dim = 32;  // kind == kmeans_sketch (extension)
 };
 
 // krylov.hpp:154-160
@@ -200,6 +202,7 @@ inline std::vector<rmg_level_spec> to_c(const std::vector<LevelSpec>& levels) {
     s.normalize_columns = l.clustering.normalize_columns ? 1 : 0;
     s.labels = l.clustering.labels.empty() ? nullptr : l.clustering.labels.data();
     s.n_clusters = l.clustering.n_clusters;
+    s.sketch_dim = l.clustering.sketch_dim;
     s.coarse_kind = static_cast<int32_t>(l.solver.kind);
     s.coarse_tol = l.solver.tol;
     s.coarse_max_iters = l.solver.max_iters;

@@ -36,6 +36,7 @@ class LevelSpecC(C.Structure):
         ("beta_override", C.c_double),
         ("has_omega_override", C.c_int32),
         ("omega_override", C.c_double),
+        ("sketch_dim", C.c_uint64),
     ]
 
 

@@ -294,7 +294,85 @@ void cluster_rows(cudaStream_t s, const void* x, bool fp32, int64_t ld, int64_t 
 
 int64_t even(int64_t v) { return (v + 1) / 2 * 2; }
 
+// sign of the sketch entry G[r][c]: splitmix64 of a counter, top bit
+__device__ __forceinline__ bool sketch_negative(uint64_t seed, int64_t r, int c, int d) {
+  uint64_t z = (seed ^ 0xC0FFEE5CE7C4ull) + static_cast<uint64_t>(r * d + c + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (z >> 63) != 0;
+}
+
+// warp per feature j (a row of X^T), lane c < d: S[c][j] = sum over the feature's
+// nonzeros (increasing sample order) of +-x (x / norm_j when normalising)
+__global__ void k_sketch_sparse(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                const double* __restrict__ val, int64_t f, const double* __restrict__ norm, int d,
+                                uint64_t seed, double* __restrict__ S, int64_t ldS) {
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int c = threadIdx.x & 31;
+  if (j >= f || c >= d) return;
+  const double nj = norm != nullptr ? norm[j] : 1.0;
+  double acc = 0.0;
+  for (int32_t q = ptr[j]; q < ptr[j + 1]; ++q) {
+    double x = val != nullptr ? val[q] : 1.0;
+    if (norm != nullptr) x = __ddiv_rn(x, nj);
+    acc = __dadd_rn(acc, sketch_negative(seed, idx[q], c, d) ? -x : x);
+  }
+  S[c * ldS + j] = acc;
+}
+
+// G (n x d, row-major) of +-1 for the dense sketch
+__global__ void k_sketch_signs(int64_t n, int d, uint64_t seed, double* g) {
+  const int64_t total = n * d;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    g[q] = sketch_negative(seed, q / d, static_cast<int>(q % d), d) ? -1.0 : 1.0;
+}
+
+// S[c][j] = st[j][c]
+__global__ void k_transpose_st(const double* st, int64_t f, int d, double* S, int64_t ldS) {
+  const int64_t total = f * d;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    S[(q % d) * ldS + q / d] = st[q];
+}
+
 }  // namespace
+
+void sketch_sparse_gpu(cudaStream_t s, const SparseDev& xt, const double* norm, int d, uint64_t seed, double* S,
+                       int64_t ldS) {
+  if (d < 1 || d > 32) throw InvalidArgument("kmeans_sketch: sketch dimension outside [1, 32]");
+  const int64_t f = xt.rows;
+  if (f > 0) {
+    k_sketch_sparse<<<static_cast<unsigned>((f * 32 + kT - 1) / kT), kT, 0, s>>>(xt.ptr, xt.idx, xt.val, f, norm, d,
+                                                                                   seed, S, ldS);
+    RMG_CK(cudaGetLastError());
+  }
+  RMG_CK(cudaStreamSynchronize(s));
+}
+
+void sketch_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t f, int64_t ld, int d, uint64_t seed,
+                      double* S, int64_t ldS) {
+  if (d < 1 || d > 32) throw InvalidArgument("kmeans_sketch: sketch dimension outside [1, 32]");
+  const int64_t ldg = even(d);
+  DBuf<double> g(static_cast<size_t>(std::max<int64_t>(1, n)) * ldg), st(static_cast<size_t>(std::max<int64_t>(1, f)) * d);
+  RMG_CK(cudaMemsetAsync(g.get(), 0, g.size() * sizeof(double), s));
+  if (ldg == d) {
+    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g.get());
+  } else {  // odd d: fill a d-wide scratch, then pad rows to even width
+    DBuf<double> g0(static_cast<size_t>(std::max<int64_t>(1, n)) * d);
+    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g0.get());
+    RMG_CK(cudaMemcpy2DAsync(g.get(), ldg * sizeof(double), g0.get(), d * sizeof(double), d * sizeof(double), n,
+                             cudaMemcpyDeviceToDevice, s));
+    RMG_CK(cudaStreamSynchronize(s));
+  }
+  RMG_CK(cudaGetLastError());
+  // st[j][c] = sum_r xc[r][j] * G[r][c], rows in order (products by +-1 are exact)
+  pair_chain<1>(s, xc, ld, f, g.get(), ldg, d, n, nullptr, st.get(), d);
+  k_transpose_st<<<grid_for(f * d), kT, 0, s>>>(st.get(), f, d, S, ldS);
+  RMG_CK(cudaGetLastError());
+  RMG_CK(cudaStreamSynchronize(s));
+}
 
 void dense_columns_f64(cudaStream_t s, const DenseDev& x, bool normalize, double* out, int64_t ldo) {
   DBuf<double> norm;

@@ -36,4 +36,15 @@ void coarsen_dense_gpu(cudaStream_t s, const DenseDev& x, const Aggregation& agg
 // the products summed over rows in increasing order.  x must be fp64.
 std::vector<double> gram_dense_gpu(cudaStream_t s, const DenseDev& x);
 
+// Sketched clustering (RMG_CLUSTER_KMEANS_SKETCH): the columns of a
+// level are projected to d <= 32 dimensions, S = G^T X (d x F, row-major, leading
+// dimension ldS), G[r][c] = -1 or +1 from sketch_negative(seed, r, c, d) below, the
+// columns of X unit-normalised first when norm != nullptr (x / norm_j, norms as
+// normalized_columns).  Each S entry sums over the column's nonzeros in increasing
+// row order.  The reference's k-means (kmeans_dense_gpu) then runs on S.
+void sketch_sparse_gpu(cudaStream_t s, const SparseDev& xt, const double* norm, int d, uint64_t seed, double* S,
+                       int64_t ldS);
+void sketch_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t f, int64_t ld, int d, uint64_t seed,
+                      double* S, int64_t ldS);
+
 }  // namespace rmg

@@ -986,6 +986,8 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       Clustering c = kmeans_dense_gpu(s, xc.get(), curm.n(), cur_f, ldx, k_c, cs.kmeans_max_iters, cs.seed);
       nc = c.n_clusters;
       lab = std::move(c.labels);
+    } else if (cs.clustering_kind == RMG_CLUSTER_KMEANS_SKETCH) {
+      lab = sketch_clustering(curm, cs, &nc);
     } else if (dev && cs.clustering_kind == RMG_CLUSTER_IMPORTED) {
       if (static_cast<int64_t>(specs_[k].labels.size()) != cur_f)
         throw InvalidArgument("imported labels: expected one label per feature of the level");
@@ -1084,6 +1086,44 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     tlog("tune", L, t0);
   }
   ctx_->sync();
+}
+
+// RMG_CLUSTER_KMEANS_SKETCH: the reference's k-means
+// (kmeans_dense_gpu, bit-identical arithmetic) on S = G^T X, G an N x d sign
+// matrix, the columns of X unit-normalised first when asked.
+std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc) {
+  if (m.comm != nullptr) throw InvalidArgument("kmeans_sketch: unsharded matrices only");
+  const int64_t f = m.f(), n = m.n();
+  const int64_t k = static_cast<int64_t>(cs.target_size);
+  if (k < 1 || k > f) throw InvalidArgument("kmeans: k outside [1, F]");
+  const int d = cs.sketch_dim == 0 ? 32 : static_cast<int>(std::min<uint64_t>(cs.sketch_dim, 1u << 30));
+  if (d < 1 || d > 32) throw InvalidArgument("kmeans_sketch: sketch dimension outside [1, 32]");
+  cudaStream_t s = ctx_->stream;
+  const int64_t ldS = (f + 1) / 2 * 2;
+  DBuf<double> S(static_cast<size_t>(d) * ldS);
+  RMG_CK(cudaMemsetAsync(S.get(), 0, S.size() * sizeof(double), s));
+  if (m.dense) {
+    const int64_t ldx = (f + 1) / 2 * 2;
+    DBuf<double> xc(static_cast<size_t>(std::max<int64_t>(1, n)) * ldx);
+    dense_columns_f64(s, m.dense->view, cs.normalize_columns != 0, xc.get(), ldx);
+    sketch_dense_gpu(s, xc.get(), n, f, ldx, d, cs.seed, S.get(), ldS);
+  } else {
+    DBuf<double> nrm;
+    if (cs.normalize_columns) {  // normalized_columns (host_setup.cpp:79-90): row order per column
+      const HostCsr& h = m.host_csr();
+      std::vector<double> v(f, 0.0);
+      for (int64_t q = 0; q < h.nnz(); ++q) {
+        const double x = h.val.empty() ? 1.0 : h.val[q];
+        v[h.idx[q]] += x * x;
+      }
+      for (double& e : v) e = std::sqrt(e);
+      nrm.upload(v.data(), v.size(), s);
+    }
+    sketch_sparse_gpu(s, m.xt.view, nrm.get(), d, cs.seed, S.get(), ldS);
+  }
+  Clustering c = kmeans_dense_gpu(s, S.get(), d, f, ldS, k, cs.kmeans_max_iters, cs.seed);
+  *nc = c.n_clusters;
+  return std::move(c.labels);
 }
 
 // X_k^T X_k + beta I (coarse_gram, krylov.cpp:350-365): on the device for a

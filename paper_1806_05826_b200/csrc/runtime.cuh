@@ -316,6 +316,7 @@ class Method {
   uint64_t run_fgmres(const double* rhs, SolveResult* out);
   void jacobi_diag();
   std::vector<double> level_gram(Matrix& m, double beta);
+  std::vector<int64_t> sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc);
   DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);
   void tune_dense_partials(size_t k);

@@ -21,7 +21,7 @@ from . import _lib
 CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL, FGMRES_TWOLEVEL = 0, 1, 2, 3, 4
 METHOD_NAMES = {"cg": CG, "jacobi_cg": JACOBI_CG, "fcg_twolevel": FCG_TWOLEVEL, "fcg_multilevel": FCG_MULTILEVEL,
                 "fgmres_twolevel": FGMRES_TWOLEVEL}
-LEADER_TOLERANCE, LEADER_TARGET, KMEANS, IMPORTED = 0, 1, 2, 100
+LEADER_TOLERANCE, LEADER_TARGET, KMEANS, KMEANS_SKETCH, IMPORTED = 0, 1, 2, 3, 100
 DIRECT_CHOLESKY, INNER_CG, INNER_FCG = 0, 1, 2
 
 
@@ -401,6 +401,7 @@ class ClusteringChoice:
     normalize_columns: bool = False  # BASELINE cfg 2 extension
     labels: Optional[np.ndarray] = None  # IMPORTED
     n_clusters: int = 0
+    sketch_dim: int = 32  # KMEANS_SKETCH
 
 
 @dataclass
@@ -448,6 +449,7 @@ def _level_array(levels: Sequence[LevelSpec]):
         s.seed = c.seed
         s.kmeans_max_iters = c.kmeans_max_iters
         s.normalize_columns = int(c.normalize_columns)
+        s.sketch_dim = c.sketch_dim
         if c.kind == IMPORTED:
             if c.labels is None:
                 raise ValueError("imported clustering without labels")
@@ -635,6 +637,8 @@ def clustering_description(spec: "MethodSpec", coarse_size: int) -> str:
         return f"lf(fc={coarse_size})"
     if c.kind == KMEANS:
         return f"km(k={coarse_size})"
+    if c.kind == KMEANS_SKETCH:  # extension
+        return f"kms(d={c.sketch_dim},k={coarse_size})"
     return f"imported(fc={coarse_size})"
 
 

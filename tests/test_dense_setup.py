@@ -110,3 +110,54 @@ def test_dense_device_setup_equals_host_setup(gpu):
     wh, rh = ph.solve(b)
     assert abs(rd.iterations - rh.iterations) <= 1
     assert rel_diff(wd, wh) <= 1e-9
+
+
+@pytest.mark.parametrize("method", ["jacobi_cg", "fcg_twolevel", "fgmres_twolevel", "fcg_multilevel"])
+def test_dense_device_levels_set_beta_and_methods(gpu, orc, method):
+    """Every method kind on a device-resident dense hierarchy; a beta sweep over it
+    (cached X_k^T X_k) equals a fresh prepare bit for bit."""
+    a = matrix_with_structure(900, 96, 21, fp32=True)
+    m = R.DeviceMatrix.from_dense(a)
+    ks = [24, 6] if method == "fcg_multilevel" else [24] if method != "jacobi_cg" else []
+    levels = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS, target_size=k, normalize_columns=True),
+                          solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == len(ks) - 1 else R.INNER_FCG))
+              for i, k in enumerate(ks)]
+    spec = R.MethodSpec(kind=R.method_from_string(method), levels=levels, solver=R.SolverConfig(1e-10, 2000))
+    b = np.random.default_rng(2).standard_normal(900)
+    pm = R.PreparedMethod(m, 1e-3, spec)
+    om = to_checker(orc, R.from_dense(a.astype(np.float64)))
+    for beta in (1e-2, 1.0):
+        pm.set_beta(beta)
+        w1, r1 = pm.solve(b)
+        fresh = R.PreparedMethod(m, beta, spec)
+        w2, r2 = fresh.solve(b)
+        assert r1.iterations == r2.iterations and np.array_equal(w1, w2), (method, beta)
+        olv = [dict(clustering_kind=oracle.CLUSTER_KMEANS, target_size=k, normalize_columns=True,
+                    coarse_kind=oracle.COARSE_DIRECT if i == len(ks) - 1 else oracle.COARSE_INNER_FCG)
+               for i, k in enumerate(ks)]
+        ref = orc.solve(om, beta, b, method, levels=olv, tol=1e-10, max_iters=2000)
+        assert abs(r1.iterations - ref.iterations) <= 2, (method, beta, r1.iterations, ref.iterations)
+        assert rel_diff(w1, ref.w) <= 1e-8
+        fresh.close()
+
+
+def test_dense_device_leader_follower_and_imported(gpu, orc):
+    """Clusterings without a device kernel (leader-follower) build the host CSR on
+    first use; imported labels skip clustering; both match the oracle."""
+    a = matrix_with_structure(400, 60, 8)
+    om = to_checker(orc, R.from_dense(a))
+    m = R.DeviceMatrix.from_dense(a)
+    want, nc, _, _ = orc.leader_follower_target(om, 12)
+    lv = R.LevelSpec(clustering=R.ClusteringChoice(kind=R.LEADER_TARGET, target_size=12),
+                     solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY))
+    pm = R.PreparedMethod(m, 1e-2, R.MethodSpec(kind=R.FCG_TWOLEVEL, levels=[lv]))
+    assert np.array_equal(pm.labels(0), want)
+    lab = np.arange(60, dtype=np.int64) % 7
+    lv = R.LevelSpec(clustering=R.ClusteringChoice(kind=R.IMPORTED, labels=lab, n_clusters=7),
+                     solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY))
+    pm = R.PreparedMethod(m, 1e-2, R.MethodSpec(kind=R.FCG_TWOLEVEL, levels=[lv], solver=R.SolverConfig(1e-10, 500)))
+    b = np.random.default_rng(0).standard_normal(400)
+    w, rep = pm.solve(b)
+    ref = orc.solve(om, 1e-2, b, "fcg_twolevel", levels=[dict(labels=lab, n_clusters=7)], tol=1e-10, max_iters=500)
+    assert np.array_equal(pm.labels(0), lab)
+    assert abs(rep.iterations - ref.iterations) <= 2 and rel_diff(w, ref.w) <= 1e-8
