@@ -185,6 +185,92 @@ __global__ void __launch_bounds__(NT) k_spmv_sell(const int32_t* __restrict__ of
   }
 }
 
+// Software-pipelined SELL K1: the index batch of round j + 1 (or the first
+// batch of the warp's next slice, whose header is also fetched a slice ahead)
+// is in flight while round j's gathers are, so a round costs one memory
+// latency instead of two (index load, then the dependent gather).  Same
+// elements, same per-row order, same sums as k_spmv_sell.
+template <bool PAT, bool NARROW, bool HOTV, int NT, int U>
+__global__ void __launch_bounds__(NT) k_spmv_sell_pipe(const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ srow,
+                                                       const int32_t* __restrict__ slen,
+                                                       const int32_t* __restrict__ idx,
+                                                       const uint16_t* __restrict__ idx16,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ v_in, double* __restrict__ t,
+                                                       int64_t n_slices, const int32_t* done,
+                                                       const KrylovScalars* sc, int ring_stride, int n_hot = 0) {
+  if (done != nullptr && *done) return;
+  const double* __restrict__ v = v_in;
+  if (sc != nullptr) {
+    if (sc->done) return;
+    v += (size_t)ring_slot(sc) * ring_stride;
+  }
+  extern __shared__ double vh[];
+  if constexpr (HOTV) {
+    for (int i = threadIdx.x; i < n_hot; i += NT) vh[i] = __ldcg(v + i);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * NT) >> 5;
+  int64_t sl = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
+  if (sl >= n_slices) return;
+  auto load_idx = [&](int (&c)[U], int64_t base, int j, int len) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = base + (int64_t)(j + u) * 32 + lane;
+      c[u] = j + u < len ? (NARROW ? ld_stream(idx16 + q) : ld_stream(idx + q)) : -1;
+    }
+  };
+  int64_t base = off[sl];
+  int L = (off[sl + 1] - base) >> 5;
+  int row = srow[sl * 32 + lane];
+  int len = slen[sl * 32 + lane];
+  int cn[U];
+  load_idx(cn, base, 0, len);
+  for (;;) {
+    const int64_t nsl = sl + nwarps;
+    const bool more = nsl < n_slices;
+    int64_t nbase = 0;
+    int nL = 0, nrow = -1, nlen = 0;
+    if (more) {  // next slice's header, a slice ahead
+      nbase = off[nsl];
+      nL = (off[nsl + 1] - nbase) >> 5;
+      nrow = srow[nsl * 32 + lane];
+      nlen = slen[nsl * 32 + lane];
+    }
+    double s = 0.0;
+    for (int j = 0; j < L; j += U) {
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = cn[u];
+      if (j + U < L)
+        load_idx(cn, base, j + U, len);
+      else if (more)
+        load_idx(cn, nbase, 0, nlen);
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (HOTV)
+          x[u] = c[u] < 0 ? 0.0 : (c[u] < n_hot ? vh[c[u]] : ld_stream(v + c[u]));
+        else
+          x[u] = c[u] >= 0 ? __ldg(v + c[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s += PAT ? x[u] : ld_stream(val + base + (int64_t)(j + u) * 32 + lane) * x[u];
+    }
+    if (L == 0 && more) load_idx(cn, nbase, 0, nlen);
+    if (row >= 0) t[row] = s;
+    if (!more) break;
+    sl = nsl;
+    base = nbase;
+    L = nL;
+    row = nrow;
+    len = nlen;
+  }
+}
+
 // K1 over row CSR (RMG_K1=csr diagnostics; the default is SELL-32 above).
 // Tried in r1 and measured slower than SELL on cfg 2 and the cfg 5 shard
 // (profiles/r1_operator.md): v staged in SMEM; a CSR-Adaptive variant (block
@@ -1273,10 +1359,25 @@ void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* 
       kern<<<grid, NT, static_cast<size_t>(n_hot) * 8, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val,
                                                             v, t, x.n_slices, done, sc, ring_stride, n_hot);
     };
-    if (x.idx16 != nullptr)
-      go(k_spmv_sell<PAT, true, true, NT>);
-    else
-      go(k_spmv_sell<PAT, false, true, NT>);
+    // default: the pipelined kernel, 12 elements per round (cfg 5 shard K1 416 -> 378 us;
+    // RMG_K1_PIPE=0 selects k_spmv_sell, 8 the 8-element variant: 391 us)
+    static const int pipe = std::getenv("RMG_K1_PIPE") ? std::atoi(std::getenv("RMG_K1_PIPE")) : 12;
+    if (pipe == 8) {
+      if (x.idx16 != nullptr)
+        go(k_spmv_sell_pipe<PAT, true, true, NT, 8>);
+      else
+        go(k_spmv_sell_pipe<PAT, false, true, NT, 8>);
+    } else if (pipe == 12) {
+      if (x.idx16 != nullptr)
+        go(k_spmv_sell_pipe<PAT, true, true, NT, 12>);
+      else
+        go(k_spmv_sell_pipe<PAT, false, true, NT, 12>);
+    } else {
+      if (x.idx16 != nullptr)
+        go(k_spmv_sell<PAT, true, true, NT>);
+      else
+        go(k_spmv_sell<PAT, false, true, NT>);
+    }
     return;
   }
   if (x.sell_off != nullptr) {
@@ -1286,10 +1387,20 @@ void spmv_rows_w(const SparseDev& x, const double* v, double* t, const int32_t* 
       kern<<<grid, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, v, t, x.n_slices,
                                      done, sc, ring_stride, 0);
     };
-    if (x.idx16 != nullptr)
-      go(k_spmv_sell<PAT, true>);
-    else
-      go(k_spmv_sell<PAT, false>);
+    // RMG_K1_PIPE=8: the pipelined kernel (60 registers: half the occupancy; cfg 2 cold
+    // 19.0 -> 18.3 us, warm 15.9 -> 18.2 us), so the plain kernel stays the default here
+    static const int pipe = std::getenv("RMG_K1_PIPE") ? std::atoi(std::getenv("RMG_K1_PIPE")) : 0;
+    if (pipe == 8) {
+      if (x.idx16 != nullptr)
+        go(k_spmv_sell_pipe<PAT, true, false, kThreads, 8>);
+      else
+        go(k_spmv_sell_pipe<PAT, false, false, kThreads, 8>);
+    } else {
+      if (x.idx16 != nullptr)
+        go(k_spmv_sell<PAT, true>);
+      else
+        go(k_spmv_sell<PAT, false>);
+    }
     return;
   }
   switch (x.width) {
