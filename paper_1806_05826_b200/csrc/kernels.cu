@@ -607,7 +607,7 @@ __device__ __forceinline__ void xt_finalize(KrylovScalars* sc, double s0, double
 
 // Sum of one X^T row (elements [k0, k1)) with `lanes` lanes, 8 elements per
 // lane per round (independent loads in flight); lane-strided order.
-template <bool PAT>
+template <bool PAT, bool NA = false>
 __device__ __forceinline__ double xt_row_sum(const int32_t* __restrict__ idx, const double* __restrict__ val,
                                              const double* __restrict__ t, int k0, int k1, int lane, int lanes) {
   constexpr int U = 8;  // elements per lane per round (independent loads in flight)
@@ -618,7 +618,7 @@ __device__ __forceinline__ double xt_row_sum(const int32_t* __restrict__ idx, co
     for (int u = 0; u < U; ++u) c[u] = k + u * lanes < k1 ? ld_stream(idx + k + u * lanes) : -1;
     double x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? __ldg(t + c[u]) : 0.0;
+    for (int u = 0; u < U; ++u) x[u] = c[u] >= 0 ? (NA ? ld_stream(t + c[u]) : __ldg(t + c[u])) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (c[u] >= 0) s += PAT ? x[u] : ld_stream(val + k + u * lanes) * x[u];
@@ -629,7 +629,7 @@ __device__ __forceinline__ double xt_row_sum(const int32_t* __restrict__ idx, co
 // K2: one work item per CTA (see XtSchedule).  Short rows take W lanes, medium
 // rows a full warp, long rows fixed CTA-wide segments combined in segment
 // order by the last-arriving CTA.  The epilogue runs here.
-template <int W, bool PAT, Epi E>
+template <int W, bool PAT, Epi E, bool NA = false>
 __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr,
                                                  const int32_t* __restrict__ idx,
                                                  const double* __restrict__ val, XtSchedule sch,
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
       double s = 0.0;
       if (q < item.y) {
         vrow = sch.perm[q];
-        s = xt_row_sum<PAT>(idx, val, t, ptr[vrow], ptr[vrow + 1], lane, lanes);
+        s = xt_row_sum<PAT, NA>(idx, val, t, ptr[vrow], ptr[vrow + 1], lane, lanes);
       }
       if (medium) {
         s = warp_sum(s);
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
   } else {
     // one fixed segment [item.y, item.z) of long row long_col[item.x]
     const int vrow = sch.long_col[item.x];
-    double s = xt_row_sum<PAT>(idx, val, t, item.y, item.z, threadIdx.x, kThreads);
+    double s = xt_row_sum<PAT, NA>(idx, val, t, item.y, item.z, threadIdx.x, kThreads);
     s = block_sum(s, sh);
     if (threadIdx.x == 0) {
       sch.seg_partial[item.w] = s;
@@ -1419,7 +1419,12 @@ void xt_impl_w(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs
     kern<<<grid, block, 0, s>>>(xt.ptr, xt.idx, xt.val, sch, a);
   };
   switch (epi) {
-    case Epi::Plain: go(k_xt<W, PAT, Epi::Plain>); break;
+    case Epi::Plain:
+      if (sch.stream_t)
+        go(k_xt<W, PAT, Epi::Plain, true>);
+      else
+        go(k_xt<W, PAT, Epi::Plain>);
+      break;
     case Epi::Axpby: go(k_xt<W, PAT, Epi::Axpby>); break;
     case Epi::Fcg: go(k_xt<W, PAT, Epi::Fcg>); break;
     case Epi::Cg: go(k_xt<W, PAT, Epi::Cg>); break;

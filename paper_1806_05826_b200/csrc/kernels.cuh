@@ -83,6 +83,7 @@ struct XtSchedule {
   double* slots = nullptr;        // [n_slots * 2]
   unsigned* grid_ticket = nullptr;
   int width = 8;                  // lanes per short column
+  int stream_t = 0;               // gathers of t bypass L1 (large N, no reuse: the hybrid cold pass)
 };
 
 // Epilogue of the X^T pass, s_j = sum_r X(r,j) t_r:

@@ -428,6 +428,9 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   std::vector<char> skip(F, 0);
   for (int64_t h = 0; h < H; ++h) skip[feat[h]] = 1;
   hx->cold.build(ht, s, F, &skip);
+  // RMG_XT_COLD_NA=1: the cold features' t gathers bypass L1 (measured slower on the
+  // cfg 5 shard, 586 vs 555 us: the L1 still catches some reuse)
+  hx->cold.view.stream_t = std::getenv("RMG_XT_COLD_NA") != nullptr ? 1 : 0;
   RMG_CK(cudaStreamSynchronize(s));
   HotXtDev& d = hx->view;
   d.ptr = hx->ptr.get();
