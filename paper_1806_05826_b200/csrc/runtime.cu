@@ -679,9 +679,26 @@ void xt_pass(Matrix& m, const double* t, Epi epi, const XtArgs& args) {
   XtArgs pa = a;
   pa.out = m.part.get();
   if (m.hot) {  // hybrid: cold rows (segmented) + hot rows (sample-blocked), sums only
-    launch_xt(m.xt.view, m.hot->cold.view, Epi::Plain, pa, m.ctx->stream);
+    static const bool serial = std::getenv("RMG_XT_SERIAL") != nullptr;
+    HotXt& h = *m.hot;
+    cudaStream_t cs = m.ctx->stream;
+    if (!serial && h.side == nullptr) {
+      RMG_CK(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
+      RMG_CK(cudaEventCreateWithFlags(&h.fork, cudaEventDisableTiming));
+      RMG_CK(cudaEventCreateWithFlags(&h.join, cudaEventDisableTiming));
+    }
+    if (!serial) {  // fork: the cold pass on the side stream
+      RMG_CK(cudaEventRecord(h.fork, m.ctx->stream));
+      RMG_CK(cudaStreamWaitEvent(h.side, h.fork, 0));
+      cs = h.side;
+    }
+    launch_xt(m.xt.view, h.cold.view, Epi::Plain, pa, cs);
     const KrylovScalars* sc = (epi == Epi::Fcg || epi == Epi::Cg) ? a.sc : nullptr;
-    launch_xt_hot(m.hot->view, t, a.done, sc, m.part.get(), m.ctx->stream);
+    launch_xt_hot(h.view, t, a.done, sc, m.part.get(), m.ctx->stream);
+    if (!serial) {  // join before the epilogue reads both parts
+      RMG_CK(cudaEventRecord(h.join, h.side));
+      RMG_CK(cudaStreamWaitEvent(m.ctx->stream, h.join, 0));
+    }
     m.ctx->launches += 3;
   } else {
     launch_xt(m.xt.view, m.sched.view, Epi::Plain, pa, m.ctx->stream);

@@ -151,6 +151,15 @@ struct HotXt {
   DBuf<uint16_t> idx16;
   DBuf<double> val, partial, red2;
   DeviceSchedule cold;  // segmented schedule over the cold rows only
+  // the cold pass runs on a side stream, concurrently with the hot pass
+  // (RMG_XT_SERIAL=1: one stream)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~HotXt() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
+  }
 };
 
 // Dense X on the device: row-major, fp64 or fp32 storage.
