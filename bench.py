@@ -318,6 +318,51 @@ def dense_operator_roofline(peak):
     return out
 
 
+def cfg4_full_summary(peak):
+    """BASELINE cfg 4 at full scale on this GPU (4M x 1024 fp32 = 16.4 GB): the
+    dense fused operator's roofline (L2 flushed is moot at 16 GB) and the
+    multilevel solve (hierarchy built on the device), device-timed
+    with CUDA events on the library's stream.  `bench.py --config cfg4` is the
+    full bench line for this config (profiles/r1_bench_cfg4.json)."""
+    import torch
+    import paper_1806_05826_b200 as R
+    cfg = CONFIGS["cfg4"]
+    t0 = time.time()
+    a = cfg4_shard_matrix(n=cfg["n"], f=cfg["f"], seed=cfg["seed"])
+    stream = torch.cuda.current_stream()
+    ctx = R.Context(torch.cuda.current_device())
+    ctx.set_stream(stream.cuda_stream)  # the events below bracket the library's own launches
+    m = R.DeviceMatrix.from_dense(a, ctx)
+    del a
+    pm = R.PreparedMethod(m, cfg["beta"], R.MethodSpec(kind=R.method_from_string(cfg["method"]),
+                                                        levels=level_specs(cfg),
+                                                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"])))
+    setup = time.time() - t0
+    op = pm.time_operator(0, 10, False)
+    fb = dense_algorithmic_bytes(cfg["n"], cfg["f"], 4)
+    b = torch.from_numpy(R.rng_normals(42, cfg["n"])).cuda()
+    w = torch.empty(cfg["f"], dtype=torch.float64, device="cuda")
+    ms, its = [], []
+    for s in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        rep = pm.solve_device(b.data_ptr(), w.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if s > 0:
+            ms.append(e0.elapsed_time(e1))
+            its.append(rep.iterations)
+    out = {"workload": cfg["workload"], "setup_s": setup, "ms_per_solve": statistics.mean(ms), "iterations": its,
+           "operator": {"bound": "hbm", "kernel": "k_dense_ata (fused X^T X single sweep) + k_dense_finish",
+                        "algorithmic_bytes_per_apply": fb, "ms_per_apply": op[0], "achieved": fb / (op[0] * 1e6),
+                        "peak": peak, "unit": "GB/s", "frac": fb / (op[0] * 1e6) / peak}}
+    pm.close()
+    m.close()
+    ctx.close()
+    return out
+
+
 def shard_operator_roofline(peak):
     """The metric's HBM-bound operator figure: BASELINE cfg 5 (16M x 500k binary,
     Poisson(64) nnz/row, Zipf(1.05)) is row-sharded; one GPU's shard at 4 GPUs
@@ -518,7 +563,7 @@ def run_b200(args, cfg):
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
-    large_op = dense_op = None
+    large_op = dense_op = cfg4_full = None
     if rank == 0 and not args.no_large_operator:
         try:
             large_op = shard_operator_roofline(peak)
@@ -528,6 +573,11 @@ def run_b200(args, cfg):
             dense_op = dense_operator_roofline(peak)
         except Exception as e:
             dense_op = {"failed": str(e)}
+        if args.config != "cfg4":
+            try:
+                cfg4_full = cfg4_full_summary(peak)
+            except Exception as e:
+                cfg4_full = {"failed": str(e)}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -570,6 +620,7 @@ def run_b200(args, cfg):
                                       (prof[0]["ms_k1"] + prof[0]["ms_k2"]) / max(1, prof[0]["applications"])},
             "operator_roofline_cfg5_shard": large_op,
             "operator_roofline_cfg4_shard": dense_op,
+            "cfg4_full_scale": cfg4_full,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
                     "d2h_bytes_per_step": x.n_features * 8},
