@@ -48,7 +48,12 @@ typedef enum {
   RMG_METHOD_JACOBI_CG = 1,
   RMG_METHOD_FCG_TWOLEVEL = 2,
   RMG_METHOD_FCG_MULTILEVEL = 3,
-  RMG_METHOD_FGMRES_TWOLEVEL = 4 /* krylov.cpp:229-328 + :628-635, full (unrestarted) */
+  RMG_METHOD_FGMRES_TWOLEVEL = 4, /* krylov.cpp:229-328 + :628-635, full (unrestarted) */
+  /* extension (BASELINE cfg 1's "Jacobi smoothing, 1 pre- and 1 post-sweep"; north-star (2);
+   * no reference counterpart): plain PCG with a symmetric V-cycle over the
+   * same hierarchy, damped-Jacobi pre- and post-smoothing at every level above the coarsest,
+   * the coarsest level solved directly */
+  RMG_METHOD_PCG_VCYCLE = 5
 } rmg_method_kind;
 
 /* krylov.hpp:135-146 ClusteringChoice::Kind (+ imported labels for parity runs) */

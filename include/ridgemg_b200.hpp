@@ -94,7 +94,8 @@ struct LevelSpec {
 
 // krylov.hpp:207-218
 enum class MethodKind { cg = RMG_METHOD_CG, jacobi_cg = RMG_METHOD_JACOBI_CG, fcg_twolevel = RMG_METHOD_FCG_TWOLEVEL,
-                        fcg_multilevel = RMG_METHOD_FCG_MULTILEVEL, fgmres_twolevel = RMG_METHOD_FGMRES_TWOLEVEL };
+                        fcg_multilevel = RMG_METHOD_FCG_MULTILEVEL, fgmres_twolevel = RMG_METHOD_FGMRES_TWOLEVEL,
+                        pcg_vcycle = RMG_METHOD_PCG_VCYCLE /* extension */ };
 
 inline MethodKind method_from_string(const std::string& s) {  // krylov.cpp:574-581
   if (s == "cg") return MethodKind::cg;
@@ -102,6 +103,7 @@ inline MethodKind method_from_string(const std::string& s) {  // krylov.cpp:574-
   if (s == "fcg_twolevel") return MethodKind::fcg_twolevel;
   if (s == "fcg_multilevel") return MethodKind::fcg_multilevel;
   if (s == "fgmres_twolevel") return MethodKind::fgmres_twolevel;
+  if (s == "pcg_vcycle") return MethodKind::pcg_vcycle;
   throw std::invalid_argument("unknown method: '" + s + "'");
 }
 

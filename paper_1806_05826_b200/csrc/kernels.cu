@@ -1162,7 +1162,8 @@ __global__ void __launch_bounds__(kThreads) k_cg_begin(const double* __restrict_
 __global__ void __launch_bounds__(kThreads) k_cg_axpy(double* __restrict__ x, double* __restrict__ r, double* z,
                                                       const double* __restrict__ inv, const double* __restrict__ p,
                                                       const double* __restrict__ ap, int64_t n, KrylovScalars* sc,
-                                                      double* hist, double* slots, unsigned* ticket) {
+                                                      double* hist, double* slots, unsigned* ticket,
+                                                      int general_m) {
   if (sc->done) return;
   __shared__ double sh[kWarps];
   const double alpha = sc->alpha;
@@ -1193,8 +1194,10 @@ __global__ void __launch_bounds__(kThreads) k_cg_axpy(double* __restrict__ x, do
         sc->converged = 1;
         sc->done = 1;
       } else {
-        sc->beta_cg = t1 / sc->rz;
-        sc->rz = t1;
+        if (!general_m) {  // general preconditioner: <r, z> after z = M r (k_pcg_rz)
+          sc->beta_cg = t1 / sc->rz;
+          sc->rz = t1;
+        }
         if (sc->it >= sc->max_iters) sc->done = 1;
       }
     }
@@ -1536,9 +1539,83 @@ void launch_cg_begin(const double* b, const double* inv_diag, double* x, double*
 }
 
 void launch_cg_axpy(double* x, double* r, double* z, const double* inv_diag, const double* p, const double* ap,
-                    int64_t n, KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s) {
-  k_cg_axpy<<<w.grid, kThreads, 0, s>>>(x, r, z, inv_diag, p, ap, n, sc, hist, w.slots, w.ticket);
+                    int64_t n, KrylovScalars* sc, double* hist, const VecWork& w, cudaStream_t s, bool general_m) {
+  k_cg_axpy<<<w.grid, kThreads, 0, s>>>(x, r, z, inv_diag, p, ap, n, sc, hist, w.slots, w.ticket, general_m ? 1 : 0);
   check_launch("cg_axpy");
+}
+
+// ---------------------------------------------------------------- V-cycle (extension)
+// Symmetric two-grid / multigrid cycle with damped-Jacobi pre- and post-smoothing
+// (BASELINE cfg 1's "Jacobi smoothing (1 pre-sweep, 1 post-sweep)", north-star (2);
+// not a reference routine).  Elementwise steps:
+//   pre:  x1 = w dinv r                         (k_vc_pre)
+//   r1 = r - y1   (y1 = A x1)                   (k_vc_sub, in place in y1)
+//   x2 = x1 + e   (e = P e_c)                   (k_vc_add, in place in e)
+//   post: z = x2 + w dinv (r - y2)  (y2 = A x2) (k_vc_post)
+__global__ void __launch_bounds__(kThreads) k_vc_pre(const double* __restrict__ r, const double* __restrict__ dinv,
+                                                     double w, double* __restrict__ x1, int64_t n, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(n, [&](int64_t i) { x1[i] = w * (dinv[i] * r[i]); });
+}
+__global__ void __launch_bounds__(kThreads) k_vc_sub(const double* __restrict__ r, double* __restrict__ y, int64_t n,
+                                                     const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(n, [&](int64_t i) { y[i] = r[i] - y[i]; });
+}
+__global__ void __launch_bounds__(kThreads) k_vc_add(const double* __restrict__ x1, double* __restrict__ e, int64_t n,
+                                                     const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(n, [&](int64_t i) { e[i] = x1[i] + e[i]; });
+}
+__global__ void __launch_bounds__(kThreads) k_vc_post(const double* __restrict__ x2, const double* __restrict__ r,
+                                                      const double* __restrict__ y2, const double* __restrict__ dinv,
+                                                      double w, double* __restrict__ z, int64_t n, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(n, [&](int64_t i) { z[i] = x2[i] + w * (dinv[i] * (r[i] - y2[i])); });
+}
+
+// PCG with a general preconditioner (krylov.cpp:94-157 with z = M r): rz' = <r, z>
+// (fixed-order grid reduction); begin: rz = rz', else beta = rz' / rz, rz = rz'.
+__global__ void __launch_bounds__(kThreads) k_pcg_rz(const double* __restrict__ r, const double* __restrict__ z,
+                                                     int64_t n, KrylovScalars* sc, int begin, double* slots,
+                                                     unsigned* ticket) {
+  if (sc->done) return;
+  __shared__ double sh[kWarps];
+  double rz = 0.0;
+  grid_stride(n, [&](int64_t i) { rz += r[i] * z[i]; });
+  const double b = block_sum(rz, sh);
+  if (threadIdx.x == 0) slots[blockIdx.x] = b;
+  if (grid_last(ticket)) {
+    const double t = sum_slots(slots, gridDim.x, 1, 0, sh);
+    if (threadIdx.x == 0) {
+      if (!begin) sc->beta_cg = t / sc->rz;
+      sc->rz = t;
+    }
+  }
+}
+
+void launch_vc_pre(const double* r, const double* dinv, double w, double* x1, int64_t n, const int32_t* done,
+                   cudaStream_t s) {
+  k_vc_pre<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(r, dinv, w, x1, n, done);
+  check_launch("vc_pre");
+}
+void launch_vc_sub(const double* r, double* y, int64_t n, const int32_t* done, cudaStream_t s) {
+  k_vc_sub<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(r, y, n, done);
+  check_launch("vc_sub");
+}
+void launch_vc_add(const double* x1, double* e, int64_t n, const int32_t* done, cudaStream_t s) {
+  k_vc_add<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(x1, e, n, done);
+  check_launch("vc_add");
+}
+void launch_vc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
+                    int64_t n, const int32_t* done, cudaStream_t s) {
+  k_vc_post<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(x2, r, y2, dinv, w, z, n, done);
+  check_launch("vc_post");
+}
+void launch_pcg_rz(const double* r, const double* z, int64_t n, KrylovScalars* sc, bool begin, const VecWork& w,
+                   cudaStream_t s) {
+  k_pcg_rz<<<w.grid, kThreads, 0, s>>>(r, z, n, sc, begin ? 1 : 0, w.slots, w.ticket);
+  check_launch("pcg_rz");
 }
 
 void launch_cg_update_p(double* p, const double* z, int64_t n, const KrylovScalars* sc, cudaStream_t s) {

@@ -195,7 +195,16 @@ void launch_cg_begin(const double* b, const double* inv_diag, double* x, double*
                      cudaStream_t s);
 void launch_cg_axpy(double* x, double* r, double* z, const double* inv_diag, const double* p,
                     const double* ap, int64_t n, KrylovScalars* sc, double* hist,
-                    const VecWork& w, cudaStream_t s);
+                    const VecWork& w, cudaStream_t s, bool general_m = false);
+// symmetric Jacobi-smoothed V-cycle steps and general-preconditioner PCG (kernels.cu)
+void launch_vc_pre(const double* r, const double* dinv, double w, double* x1, int64_t n, const int32_t* done,
+                   cudaStream_t s);
+void launch_vc_sub(const double* r, double* y, int64_t n, const int32_t* done, cudaStream_t s);
+void launch_vc_add(const double* x1, double* e, int64_t n, const int32_t* done, cudaStream_t s);
+void launch_vc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
+                    int64_t n, const int32_t* done, cudaStream_t s);
+void launch_pcg_rz(const double* r, const double* z, int64_t n, KrylovScalars* sc, bool begin, const VecWork& w,
+                   cudaStream_t s);
 void launch_cg_update_p(double* p, const double* z, int64_t n, const KrylovScalars* sc,
                         cudaStream_t s);
 

@@ -938,7 +938,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
                const rmg_solver_config& sol)
     : solver(sol), ctx_(x->ctx), fine_(x), beta_(beta), kind_(kind) {
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
-  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_FGMRES_TWOLEVEL)
+  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_PCG_VCYCLE)
     throw InvalidArgument("unknown method kind " + std::to_string(kind));
   if (solver.max_iters > static_cast<uint64_t>(INT32_MAX)) throw InvalidArgument("max_iters too large");
   const int keep0 = static_cast<int>(std::max<uint64_t>(solver.truncation, 1));
@@ -954,7 +954,8 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
   if (n_levels == 0 || levels == nullptr)
     throw InvalidArgument(kind != RMG_METHOD_FCG_MULTILEVEL ? "two-level method requires one level spec"
                                                             : "multilevel method requires level specs");
-  const uint64_t L = kind != RMG_METHOD_FCG_MULTILEVEL ? 1 : n_levels;
+  const bool multi = kind == RMG_METHOD_FCG_MULTILEVEL || kind == RMG_METHOD_PCG_VCYCLE;
+  const uint64_t L = multi ? n_levels : 1;
   if (L > RMG_MAX_LEVELS) throw InvalidArgument("too many levels");
   for (uint64_t k = 0; k < L; ++k) {
     LevelSpecHost ls;
@@ -968,6 +969,9 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     specs_.push_back(ls);
   }
   if (kind != RMG_METHOD_FCG_MULTILEVEL) specs_[0].spec.coarse_kind = RMG_COARSE_DIRECT_CHOLESKY;  // krylov.cpp:632-634
+  if (kind == RMG_METHOD_PCG_VCYCLE)  // intermediate levels are visited by the recursive cycle
+    for (uint64_t k = 0; k < L; ++k)
+      specs_[k].spec.coarse_kind = k + 1 == L ? RMG_COARSE_DIRECT_CHOLESKY : RMG_COARSE_INNER_FCG;
   // krylov.cpp:495-505
   for (uint64_t k = 0; k + 1 < L; ++k)
     if (specs_[k].spec.coarse_kind == RMG_COARSE_DIRECT_CHOLESKY)
@@ -1100,6 +1104,11 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     t0 = tnow();
     build_dense_levels(inv);
     tlog("dense_levels", L, t0);
+    if (kind_ == RMG_METHOD_PCG_VCYCLE) {
+      t0 = tnow();
+      build_vcycle();
+      tlog("vcycle", L, t0);
+    }
     t0 = tnow();
     for (size_t k = 1; k < dense_.size(); ++k)
       if (dense_[k]) tune_dense_partials(k);
@@ -1205,6 +1214,7 @@ void Method::set_beta(double beta) {
   build_dense_levels(inv);
   for (size_t k = 1; k < dense_.size(); ++k)
     if (dense_[k]) tune_dense_partials(k);
+  if (kind_ == RMG_METHOD_PCG_VCYCLE) build_vcycle();
   ctx_->sync();
 }
 
@@ -1214,6 +1224,7 @@ void Method::set_beta(double beta) {
 void Method::build_dense_levels(const std::vector<double>& ainv_host) {
   const size_t L = coarse_.size();
   dense_.resize(L + 1);
+  if (kind_ == RMG_METHOD_PCG_VCYCLE) return;  // no inner Krylov solves
   if (std::getenv("RMG_DISABLE_DENSE_INNER") != nullptr) return;
   cudaStream_t s = ctx_->stream;
   const unsigned threads = std::max(1u, std::thread::hardware_concurrency());
@@ -1713,6 +1724,8 @@ SolveResult Method::solve_rhs(const double* rhs, double* w_out) {
     run_cg(0, rhs, inv_diag_.get(), true, &res);
   else if (kind_ == RMG_METHOD_FGMRES_TWOLEVEL)
     run_fgmres(rhs, &res);
+  else if (kind_ == RMG_METHOD_PCG_VCYCLE)
+    run_pcg_vcycle(rhs, &res);
   else
     run_fcg(0, rhs, true, &res);
   const int64_t n = fine_->f();
@@ -1732,7 +1745,149 @@ void Method::collect_profiles() {
 
 void Method::precondition(const double* r, double* z) {
   if (coarse_.empty()) throw InvalidArgument("precondition: method has no hierarchy");
-  precond(0, r, z);
+  if (kind_ == RMG_METHOD_PCG_VCYCLE)
+    vcycle(0, r, z, nullptr);
+  else
+    precond(0, r, z);
+}
+
+// ---------------------------------------------------------------- pcg_vcycle
+// Damped Jacobi at every level above the coarsest: D_k = diag(X_k^T X_k) + beta_k
+// (gram_diagonal, ridge.cpp:30-37), weight 1 / lambda_max(D_k^-1 A_k) by 30 power
+// steps from CounterRng(0x5eed + 64 + k) normals (underestimates lambda_max by a
+// little, so w lambda_max stays just above 1, inside (0, 2)).
+void Method::build_vcycle() {
+  cudaStream_t s = ctx_->stream;
+  const size_t L = coarse_.size();
+  vc_.clear();
+  for (size_t k = 0; k < L; ++k) {
+    Matrix& m = level_matrix(k);
+    const int64_t n = m.f();
+    auto v = std::make_unique<VcLevel>();
+    const size_t nn = static_cast<size_t>(std::max<int64_t>(1, n));
+    v->dinv.alloc(nn);
+    v->x1.alloc(nn);
+    v->y.alloc(nn);
+    v->e.alloc(nn);
+    m.gram_diagonal(level_beta(k), v->x1.get());
+    std::vector<double> d(n);
+    if (n) RMG_CK(cudaMemcpyAsync(d.data(), v->x1.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    ctx_->sync();
+    for (double& e : d) {
+      if (!(e > 0.0)) throw InvalidArgument("pcg_vcycle: Jacobi diagonal must be positive");
+      e = 1.0 / e;
+    }
+    v->dinv.upload(d.data(), d.size(), s);
+    CounterRng rng(0x5eed + 64 + k);
+    std::vector<double> h(n);
+    for (double& e : h) e = rng.next_normal();
+    double lam = 0.0;
+    for (int it = 0; it < 30 && n > 0; ++it) {
+      double nv = 0.0;
+      for (double e : h) nv += e * e;
+      nv = std::sqrt(nv);
+      if (nv == 0.0) break;
+      for (double& e : h) e /= nv;
+      lam = nv;
+      v->x1.upload(h.data(), h.size(), s);
+      XtArgs a;
+      a.v = v->x1.get();
+      a.out = v->y.get();
+      a.beta = level_beta(k);
+      m.apply(v->x1.get(), Epi::Axpby, a);
+      launch_vc_pre(v->y.get(), v->dinv.get(), 1.0, v->e.get(), n, nullptr, s);  // D^-1 A v
+      RMG_CK(cudaMemcpyAsync(h.data(), v->e.get(), n * 8, cudaMemcpyDeviceToHost, s));
+      ctx_->sync();
+    }
+    {
+      double nv = 0.0;
+      for (double e : h) nv += e * e;
+      lam = std::sqrt(nv);
+    }
+    if (!(lam > 0.0)) throw RuntimeError("pcg_vcycle: Jacobi power iteration collapsed");
+    v->w = 1.0 / lam;
+    vc_.push_back(std::move(v));
+  }
+}
+
+// z = M_k r: pre-smooth from zero, coarse correction (the next level's cycle, or the
+// coarsest direct solve), post-smooth -- symmetric, so plain PCG applies.
+void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
+  cudaStream_t s = ctx_->stream;
+  const size_t L = coarse_.size();
+  CoarseLevelDev& c = *coarse_[k];
+  Matrix& m = level_matrix(k);
+  const int64_t nf = m.f();
+  VcLevel& v = *vc_[k];
+  launch_vc_pre(r, v.dinv.get(), v.w, v.x1.get(), nf, done, s);
+  XtArgs a;
+  a.v = v.x1.get();
+  a.out = v.y.get();
+  a.beta = level_beta(k);
+  a.done = done;
+  m.apply(v.x1.get(), Epi::Axpby, a, prof(k));
+  launch_vc_sub(r, v.y.get(), nf, done, s);  // y = r - A x1
+  const bool last = k + 1 == L;
+  double* rc = last ? rc_last_.get() : work_[k + 1]->b.get();
+  double* ec = last ? ec_last_.get() : work_[k + 1]->x.get();
+  XtArgs ra;
+  ra.t = v.y.get();
+  ra.out = rc;
+  ra.done = done;
+  launch_xt(c.pt.view, c.pt_sched.view, Epi::Plain, ra, s);
+  if (last)
+    launch_dense_gemv(ainv_.get(), rc, ec, c.mat->f(), done, s);
+  else
+    vcycle(k + 1, rc, ec, done);
+  launch_prolong(c.label.get(), c.weight.get(), ec, v.e.get(), nf, done, s);
+  launch_vc_add(v.x1.get(), v.e.get(), nf, done, s);  // e = x2
+  a.v = v.e.get();
+  a.out = v.y.get();
+  m.apply(v.e.get(), Epi::Axpby, a, prof(k));
+  launch_vc_post(v.e.get(), r, v.y.get(), v.dinv.get(), v.w, z, nf, done, s);
+  ctx_->launches += 8;
+}
+
+// PCG (krylov.cpp:94-157) with z = M r the V-cycle
+uint64_t Method::run_pcg_vcycle(const double* rhs, SolveResult* out) {
+  KrylovWork& w = *work_[0];
+  Matrix& m = *fine_;
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  double* p = w.p_ring.get();
+  double* ap = w.ap_ring.get();
+  double* z = w.z.get();
+  const int32_t* done = &w.sc.get()->done;
+  const auto t0 = Clock::now();
+  launch_cg_begin(rhs, nullptr, w.x.get(), w.r.get(), z, p, n, w.sc.get(), w.hist.get(), w.vw, s);
+  KrylovScalars hs = ctx_->read(w.sc.get());
+  if (hs.status == 3) throw InvalidArgument("cg: non-finite rhs");
+  if (!hs.done) {
+    vcycle(0, w.r.get(), z, done);
+    launch_pcg_rz(w.r.get(), z, n, w.sc.get(), true, w.vw, s);
+    RMG_CK(cudaMemcpyAsync(p, z, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
+    ctx_->launches += 2;
+  }
+  while (!hs.done) {
+    XtArgs a;
+    a.v = p;
+    a.out = ap;
+    a.beta = level_beta(0);
+    a.sc = w.sc.get();
+    m.apply(p, Epi::Cg, a, prof(0));
+    launch_cg_axpy(w.x.get(), w.r.get(), z, nullptr, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s, true);
+    vcycle(0, w.r.get(), z, done);
+    launch_pcg_rz(w.r.get(), z, n, w.sc.get(), false, w.vw, s);
+    launch_cg_update_p(p, z, n, w.sc.get(), s);
+    ctx_->launches += 3;
+    hs = ctx_->read(w.sc.get());
+    if (profiling_) collect_profiles();
+    if (hs.status == 2)
+      throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
+                         "; operator is not positive definite");
+  }
+  if (out) record(ctx_, w, hs, std::vector<uint64_t>(static_cast<size_t>(hs.it), 0), t0, out);
+  return static_cast<uint64_t>(hs.it);
 }
 
 double Method::time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms) {

@@ -293,7 +293,12 @@ class Method {
   int64_t coarse_size() const { return coarse_.empty() ? 0 : coarse_[0]->mat->f(); }
   Matrix& level_matrix(size_t k) const { return k == 0 ? *fine_ : *coarse_[k - 1]->mat; }
   double level_beta(size_t k) const { return k == 0 ? beta_ : coarse_[k - 1]->beta; }
-  double omega(size_t k) const { return k < omega_.size() ? omega_[k] : 0.0; }
+  // the level's smoothing weight: Richardson omega_k (krylov.cpp:539-546), or the
+  // damped-Jacobi weight for pcg_vcycle
+  double omega(size_t k) const {
+    if (kind_ == RMG_METHOD_PCG_VCYCLE) return k < vc_.size() ? vc_[k]->w : 0.0;
+    return k < omega_.size() ? omega_[k] : 0.0;
+  }
   const std::vector<int64_t>& labels(size_t k) const;
   Matrix* fine() const { return fine_; }
   int kind() const { return kind_; }
@@ -325,6 +330,16 @@ class Method {
   uint64_t run_fgmres(const double* rhs, SolveResult* out);
   void jacobi_diag();
   std::vector<double> level_gram(Matrix& m, double beta);
+  // pcg_vcycle: per smoothed level k < L, D_k^-1 and the
+  // damped-Jacobi weight 1 / lambda_max(D_k^-1 A_k); scratch x1, y, e
+  struct VcLevel {
+    DBuf<double> dinv, x1, y, e;
+    double w = 0.0;
+  };
+  std::vector<std::unique_ptr<VcLevel>> vc_;
+  void build_vcycle();
+  void vcycle(size_t k, const double* r, double* z, const int32_t* done);
+  uint64_t run_pcg_vcycle(const double* rhs, SolveResult* out);
   std::vector<int64_t> sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc);
   DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);

@@ -1,0 +1,108 @@
+"""pcg_vcycle (extension): plain PCG with a symmetric V-cycle over
+the reference's hierarchy -- damped-Jacobi pre- and post-smoothing (BASELINE cfg 1's
+"1 pre-sweep, 1 post-sweep"), coarsest level direct.  The reference has no such
+routine, so it is pinned against a numpy restatement of the same
+cycle on the same hierarchy (labels, X_k, beta_k and Jacobi weights read back from
+the prepared method), and its solves against the reference's solution of the same
+system (oracle CG to 1e-12)."""
+import numpy as np
+import pytest
+
+import paper_1806_05826_b200 as R
+from helpers import random_matrix, rel_diff, to_checker
+
+pytestmark = pytest.mark.gpu
+
+
+def spec(ks, tol=1e-10, max_iters=2000, normalize=False):
+    levels = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS, target_size=k, seed=0,
+                                                        normalize_columns=normalize),
+                          solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == len(ks) - 1 else R.INNER_FCG))
+              for i, k in enumerate(ks)]
+    return R.MethodSpec(kind=R.PCG_VCYCLE, levels=levels, solver=R.SolverConfig(tol, max_iters))
+
+
+def restated_cycle(pm, r):
+    """The cycle in numpy: z = x2 + w D^-1 (r - A x2), x2 = x1 + P A_c^-1 P^T (r - A x1),
+    x1 = w D^-1 r, recursively; P = adjusted average (weights 1/sqrt(n_S))."""
+    L = pm.n_levels - 1  # smoothed levels 0..L-1, level L direct
+    mats = [pm.x.x.dense() if pm.x.x is not None else None] + [pm.level_matrix(k).dense() for k in range(1, L + 1)]
+    betas = [pm.level(k)["beta"] for k in range(L + 1)]
+    ws = [pm.level(k)["omega"] for k in range(L)]
+    labs = [pm.labels(k) for k in range(L)]
+
+    def cycle(k, rk):
+        x = mats[k]
+        a = x.T @ x + betas[k] * np.eye(x.shape[1])
+        dinv = 1.0 / np.diag(a)
+        lab = labs[k]
+        nc = lab.max() + 1
+        size = np.bincount(lab, minlength=nc)
+        p = np.zeros((x.shape[1], nc))
+        p[np.arange(x.shape[1]), lab] = 1.0 / np.sqrt(size[lab])
+        x1 = ws[k] * dinv * rk
+        rc = p.T @ (rk - a @ x1)
+        if k + 1 == L:
+            xc = mats[k + 1]
+            ec = np.linalg.solve(xc.T @ xc + betas[k + 1] * np.eye(nc), rc)
+        else:
+            ec = cycle(k + 1, rc)
+        x2 = x1 + p @ ec
+        return x2 + ws[k] * dinv * (rk - a @ x2)
+
+    return cycle(0, r)
+
+
+@pytest.mark.parametrize("ks", [[30], [40, 8]])
+def test_vcycle_matches_restatement_and_is_symmetric(gpu, ks):
+    x = random_matrix(300, 120, 7, 0.3)
+    m = R.DeviceMatrix(x)
+    pm = R.PreparedMethod(m, 0.5, spec(ks))
+    rng = np.random.default_rng(1)
+    u, v = rng.standard_normal(120), rng.standard_normal(120)
+    mu, mv = pm.precondition(u), pm.precondition(v)
+    assert abs(u @ mv - v @ mu) <= 1e-12 * abs(u @ mv)
+    assert rel_diff(mv, restated_cycle(pm, v)) <= 1e-12
+    for k in range(len(ks)):
+        assert 0.0 < pm.level(k)["omega"] < 2.0
+
+
+@pytest.mark.parametrize("ks", [[30], [40, 8]])
+def test_vcycle_solve_matches_reference_solution(gpu, orc, ks):
+    x = random_matrix(300, 120, 8, 0.3)
+    m = R.DeviceMatrix(x)
+    b = R.rng_normals(42, 300)
+    sol = R.solve_system(m, 0.5, b, spec(ks))
+    ref = orc.solve(to_checker(orc, x), 0.5, b, "cg", tol=1e-12, max_iters=5000)
+    assert sol.report.converged
+    assert rel_diff(sol.w, ref.w) <= 1e-8
+    assert sol.report.iterations < ref.iterations
+
+
+def test_vcycle_cfg1_dense(gpu):
+    """cfg 1 (dense 2000 x 500, 50 clusters) with Jacobi pre + post smoothing."""
+    x = R.synth_dense_clustered(2000, 500, 50, 0.1, 0)
+    a = x.dense()
+    m = R.DeviceMatrix.from_dense(a)
+    b = R.rng_normals(42, 2000)
+    sol = R.solve_system(m, 1e-2, b, spec([50]))
+    exact = np.linalg.solve(a.T @ a + 1e-2 * np.eye(500), a.T @ b)
+    assert sol.report.converged
+    assert rel_diff(sol.w, exact) <= 1e-8
+    cg = R.solve_system(m, 1e-2, b, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-10, 5000)))
+    assert sol.report.iterations < cg.report.iterations
+
+
+def test_vcycle_set_beta_and_errors(gpu):
+    x = random_matrix(200, 80, 9, 0.3)
+    m = R.DeviceMatrix(x)
+    pm = R.PreparedMethod(m, 1e-2, spec([20]))
+    b = R.rng_normals(3, 200)
+    for beta in (1.0, 1e-3):
+        pm.set_beta(beta)
+        w1, r1 = pm.solve(b)
+        fresh = R.PreparedMethod(m, beta, spec([20]))
+        w2, r2 = fresh.solve(b)
+        assert r1.iterations == r2.iterations and np.array_equal(w1, w2)
+    with pytest.raises(ValueError):
+        R.PreparedMethod(m, 1e-2, R.MethodSpec(kind=R.PCG_VCYCLE, levels=[]))
