@@ -542,6 +542,35 @@ def run_b200(args, cfg):
         e2e_total = float(t.item())
     e2e_value = e2e_total / solves
 
+    # extension: the same systems through pcg_vcycle -- plain PCG with a
+    # symmetric Jacobi-smoothed V-cycle over the same hierarchy (BASELINE cfg 1's
+    # "1 pre-, 1 post-sweep"); not the reference's algorithm, so not the headline
+    vcycle = None
+    if rank == 0:
+        try:
+            pv = R.PreparedMethod(m, cfg["beta"], R.MethodSpec(kind=R.PCG_VCYCLE, levels=level_specs(cfg, labels),
+                                                                solver=R.SolverConfig(cfg["tol"], cfg["max_iters"])))
+            wv = torch.empty_like(w)
+            pv.solve_device(bs[0].data_ptr(), wv.data_ptr())
+            vms, vits = [], []
+            for s in range(args.steps):
+                flush.random_(0, 255)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                rep = pv.solve_device(bs[args.warmup + s].data_ptr(), wv.data_ptr())
+                e1.record(stream)
+                torch.cuda.synchronize()
+                vms.append(e0.elapsed_time(e1))
+                vits.append(rep.iterations)
+            pm.solve_device(bs[args.warmup + args.steps - 1].data_ptr(), w.data_ptr())
+            torch.cuda.synchronize()
+            vcycle = {"method": "pcg_vcycle (extension: PCG + symmetric V-cycle, damped-Jacobi pre/post smoothing)",
+                      "ms_per_solve": statistics.mean(vms), "iterations": vits,
+                      "rel_diff_w_vs_headline_method": float(torch.linalg.norm(wv - w) / torch.linalg.norm(w))}
+            pv.close()
+        except Exception as e:  # reported, never fatal
+            vcycle = {"failed": str(e)}
+
     # CPU baseline: the reference on this host, rank 0 at N=1 only, bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -621,6 +650,7 @@ def run_b200(args, cfg):
             "operator_roofline_cfg5_shard": large_op,
             "operator_roofline_cfg4_shard": dense_op,
             "cfg4_full_scale": cfg4_full,
+            "pcg_vcycle": vcycle,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
                     "d2h_bytes_per_step": x.n_features * 8},

@@ -13,6 +13,7 @@ import paper_1806_05826_b200 as R
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 f = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
 ks = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [10_000, 1_000, 100]
+method = sys.argv[4] if len(sys.argv) > 4 else "fcg_multilevel"
 t = time.time()
 x = R.synth_sparse_zipf(n, f, 50.0, 1.1, True, 0, row_streams=True)
 print(f"generate {time.time() - t:.1f} s, nnz {x.nnz}", flush=True)
@@ -27,11 +28,13 @@ for i, k in enumerate(ks):
                               solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if last else R.INNER_FCG,
                                                          tol=1e-6, max_iters=500)))
 t = time.time()
-pm = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=levels, solver=R.SolverConfig(1e-6, 1000)))
+pm = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.method_from_string(method), levels=levels,
+                                            solver=R.SolverConfig(1e-6, 1000)))
 print(f"prepare {time.time() - t:.1f} s; levels", [pm.level(i)["n_features"] for i in range(pm.n_levels)], flush=True)
 for beta in (1.0, 10.0, 1e-1, 1e-2, 1e-3):
     pm.set_beta(beta)
     b = R.rng_normals(42, n)
+    pm.solve(b)  # warm
     t = time.time()
     w, r = pm.solve(b)
     inner = r.inner_iterations
