@@ -17,6 +17,7 @@
 // Every product / difference / sum the host rounds separately is a separate
 // __dmul_rn / __dsub_rn / __dadd_rn here (no FMA contraction).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <limits>
 #include <stdexcept>
@@ -135,7 +136,28 @@ void col_chain(cudaStream_t s, const void* x, bool fp32, int64_t ld, int64_t n, 
 // OP 0 (Lloyd, clustering.cpp:281-291 / host_setup.cpp:283-290):
 //      acc = init[b];  acc += (x - p)^2 - p^2   (x = A[r][a], p = B[r][b])
 // OP 1 (Gram, coarse_gram): acc = 0;  acc += A[r][a] * B[r][b]
+// OP 2: OP 0 with the assignment's scan fused: per feature a, the tile's 32
+//      prototypes reduce to the first minimum of max(acc, 0) (NaN never wins),
+//      written as one (value, index) pair per (feature, prototype tile) --
+//      F x K/32 pairs instead of the F x K distances (cfg 5: 12.5 GB, not 200 GB)
 constexpr int kPcRows = 64, kPcStages = 4;
+
+struct ArgMin {
+  double v;
+  long long s;
+};
+
+// first minimum in prototype order: strictly smaller value, or equal value and
+// a smaller index (the reference's strict-< scan, clustering.cpp:292-302)
+__device__ __forceinline__ ArgMin argmin_combine(ArgMin a, ArgMin b) {
+  if (b.v < a.v || (b.v == a.v && b.s < a.s)) return b;
+  return a;
+}
+
+__device__ __forceinline__ double lloyd_sq(double acc) {
+  if (isnan(acc)) return INFINITY;  // std::max(NaN, 0) is NaN, never < best: like +inf here
+  return acc < 0.0 ? 0.0 : acc;     // std::max(acc, 0.0)
+}
 
 template <int OP>
 __global__ void __launch_bounds__(kT) k_pair_chain(const double* A, int64_t lda, int64_t na, const double* B,
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(kT) k_pair_chain(const double* A, int64_t lda,
   for (int i = 0; i < kPcStages - 1; ++i) stage(i);
   const int64_t b = b0 + lane;
   double acc0 = 0.0, acc1 = 0.0;
-  if (OP == 0 && b < nb) acc0 = acc1 = init[b];
+  if ((OP == 0 || OP == 2) && b < nb) acc0 = acc1 = init[b];
   for (int64_t ch = 0; ch < nchunks; ++ch) {
     stage(ch + kPcStages - 1);
     cp_async_wait<kPcStages - 1>();
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(kT) k_pair_chain(const double* A, int64_t lda,
 #pragma unroll 4
     for (int r = 0; r < rows; ++r) {
       const double x0 = sa[r * 16 + wid], x1 = sa[r * 16 + wid + 8], p = sb[r * 32 + lane];
-      if (OP == 0) {
+      if (OP == 0 || OP == 2) {
         const double pp = __dmul_rn(p, p);
         const double d0 = __dsub_rn(x0, p), d1 = __dsub_rn(x1, p);
         acc0 = __dadd_rn(acc0, __dsub_rn(__dmul_rn(d0, d0), pp));
@@ -193,10 +215,42 @@ __global__ void __launch_bounds__(kT) k_pair_chain(const double* A, int64_t lda,
     }
     __syncthreads();
   }
-  if (b < nb) {
+  if constexpr (OP == 2) {
+    ArgMin m0{b < nb ? lloyd_sq(acc0) : INFINITY, b < nb ? (long long)b : LLONG_MAX};
+    ArgMin m1{b < nb ? lloyd_sq(acc1) : INFINITY, b < nb ? (long long)b : LLONG_MAX};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMin t0{__shfl_xor_sync(0xffffffffu, m0.v, o), __shfl_xor_sync(0xffffffffu, m0.s, o)};
+      ArgMin t1{__shfl_xor_sync(0xffffffffu, m1.v, o), __shfl_xor_sync(0xffffffffu, m1.s, o)};
+      m0 = argmin_combine(m0, t0);
+      m1 = argmin_combine(m1, t1);
+    }
+    ArgMin* tiles = reinterpret_cast<ArgMin*>(out);  // [na][gridDim.y]
+    if (lane == 0) {
+      if (a0 + wid < na) tiles[(a0 + wid) * gridDim.y + blockIdx.y] = m0;
+      if (a0 + wid + 8 < na) tiles[(a0 + wid + 8) * gridDim.y + blockIdx.y] = m1;
+    }
+  } else if (b < nb) {
     if (a0 + wid < na) out[(a0 + wid) * ldo + b] = acc0;
     if (a0 + wid + 8 < na) out[(a0 + wid + 8) * ldo + b] = acc1;
   }
+}
+
+// per feature: the tiles' minima in prototype order, strict < from (inf, 0)
+__global__ void k_argmin_tiles(const ArgMin* tiles, int ny, int64_t f, int32_t* member, double* own) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= f) return;
+  int64_t best = 0;
+  double best_sq = INFINITY;
+  for (int y = 0; y < ny; ++y) {
+    const ArgMin t = tiles[j * ny + y];
+    if (t.v < best_sq) {
+      best_sq = t.v;
+      best = t.s;
+    }
+  }
+  member[j] = static_cast<int32_t>(best);
+  own[j] = best_sq;
 }
 
 template <int OP>
@@ -233,25 +287,6 @@ __global__ void k_copy_col(const double* src, int64_t lds, int64_t j, int64_t n,
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x)
     dst[r * ldd + s] = src[r * lds + j];
-}
-
-// Lloyd assignment per feature: the strict-< scan over max(acc, 0) in prototype
-// order (host_setup.cpp:292-302)
-__global__ void k_argmin(const double* dist, int64_t ldd, int64_t f, int64_t k, int32_t* member, double* own) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= f) return;
-  int64_t best = 0;
-  double best_sq = INFINITY;
-  for (int64_t s = 0; s < k; ++s) {
-    const double a = dist[j * ldd + s];
-    const double sq = a < 0.0 ? 0.0 : a;  // std::max(acc, 0.0)
-    if (sq < best_sq) {
-      best_sq = sq;
-      best = s;
-    }
-  }
-  member[j] = static_cast<int32_t>(best);
-  own[j] = best_sq;
 }
 
 // out[r][c] = (sum over members m of c, increasing: x[r][m] (* w[m])) (* scale[c]);
@@ -389,7 +424,9 @@ Clustering kmeans_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t
                             uint64_t max_iters, uint64_t seed) {
   if (k <= 0 || k > f) throw InvalidArgument("kmeans: k outside [1, F]");
   const int64_t ldk = even(k);
-  DBuf<double> proto(static_cast<size_t>(std::max<int64_t>(1, n)) * ldk), psq(ldk), dist(static_cast<size_t>(f) * ldk),
+  const int64_t ny = (k + 31) / 32;  // prototype tiles of the fused assignment
+  DBuf<ArgMin> tiles(static_cast<size_t>(f) * ny);
+  DBuf<double> proto(static_cast<size_t>(std::max<int64_t>(1, n)) * ldk), psq(ldk), dist(static_cast<size_t>(f)),
       own_d(f), colv(std::max<int64_t>(1, n)), inv_d(k);
   DBuf<int32_t> member_d(f), mptr_d(k + 1), members_d(f);
   RMG_CK(cudaMemsetAsync(proto.get(), 0, proto.size() * sizeof(double), s));
@@ -405,13 +442,19 @@ Clustering kmeans_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t
     chosen.push_back(static_cast<int64_t>(rng.next_index(f)));
     std::vector<char> used(f, 0);
     used[chosen[0]] = 1;
-    std::vector<double> d2(f, std::numeric_limits<double>::infinity()), dh(f, 0.0);
+    std::vector<double> d2(f, std::numeric_limits<double>::infinity());
+    double* dh = nullptr;  // pinned: one D2H of F distances per seeding step
+    RMG_CK(cudaMallocHost(&dh, static_cast<size_t>(f) * sizeof(double)));
+    struct PinnedFree {
+      double* p;
+      ~PinnedFree() { cudaFreeHost(p); }
+    } dh_free{dh};
     while (static_cast<int64_t>(chosen.size()) < k) {
       const int64_t last = chosen.back();
       k_copy_col<<<grid_for(n), kT, 0, s>>>(xc, ld, last, n, colv.get(), 1, 0);
       RMG_CK(cudaGetLastError());
       col_chain<1>(s, xc, false, ld, n, f, colv.get(), dist.get(), true);
-      RMG_CK(cudaMemcpyAsync(dh.data(), dist.get(), f * sizeof(double), cudaMemcpyDeviceToHost, s));
+      RMG_CK(cudaMemcpyAsync(dh, dist.get(), f * sizeof(double), cudaMemcpyDeviceToHost, s));
       RMG_CK(cudaStreamSynchronize(s));
       double total = 0.0;
       for (int64_t j = 0; j < f; ++j) {
@@ -458,8 +501,9 @@ Clustering kmeans_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t
   std::vector<int32_t> mptr(k + 1), members(f);
   for (uint64_t iter = 0; iter < std::max<uint64_t>(max_iters, 1); ++iter) {
     col_chain<0>(s, proto.get(), false, ldk, n, k, nullptr, psq.get(), false);
-    pair_chain<0>(s, xc, ld, f, proto.get(), ldk, k, n, psq.get(), dist.get(), ldk);
-    k_argmin<<<static_cast<unsigned>((f + kT - 1) / kT), kT, 0, s>>>(dist.get(), ldk, f, k, member_d.get(), own_d.get());
+    pair_chain<2>(s, xc, ld, f, proto.get(), ldk, k, n, psq.get(), reinterpret_cast<double*>(tiles.get()), 0);
+    k_argmin_tiles<<<static_cast<unsigned>((f + kT - 1) / kT), kT, 0, s>>>(tiles.get(), static_cast<int>(ny), f,
+                                                                           member_d.get(), own_d.get());
     RMG_CK(cudaGetLastError());
     RMG_CK(cudaMemcpyAsync(mh.data(), member_d.get(), f * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RMG_CK(cudaMemcpyAsync(own.data(), own_d.get(), f * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -427,26 +427,60 @@ HostCsr coarsen(const HostCsr& x, const Aggregation& p) {
   c.n = x.n;
   c.f = p.n_coarse;
   c.ptr.assign(x.n + 1, 0);
-  std::vector<double> acc(p.n_coarse, 0.0);
-  std::vector<int64_t> stamp(p.n_coarse, -1), hit;
-  for (int64_t r = 0; r < x.n; ++r) {
-    hit.clear();
-    for (int64_t k = x.ptr[r]; k < x.ptr[r + 1]; ++k) {
-      const int64_t i = x.idx[k];
-      const int32_t s = p.label[i];
-      if (stamp[s] != r) {
-        stamp[s] = r;
-        hit.push_back(s);
+  // rows are independent: contiguous row ranges per thread, concatenated in order
+  // (each row exactly as the sequential loop builds it, coarsening.cpp:112-148)
+  const unsigned T = x.nnz() < (1 << 20) ? 1u : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  struct Part {
+    std::vector<int64_t> idx;
+    std::vector<double> val;
+  };
+  std::vector<Part> parts(T);
+  auto body = [&](unsigned t) {
+    const int64_t r0 = x.n * t / T, r1 = x.n * (t + 1) / T;
+    Part& out = parts[t];
+    std::vector<double> acc(p.n_coarse, 0.0);
+    std::vector<int64_t> stamp(p.n_coarse, -1), hit;
+    for (int64_t r = r0; r < r1; ++r) {
+      hit.clear();
+      for (int64_t k = x.ptr[r]; k < x.ptr[r + 1]; ++k) {
+        const int64_t i = x.idx[k];
+        const int32_t s = p.label[i];
+        if (stamp[s] != r) {
+          stamp[s] = r;
+          hit.push_back(s);
+        }
+        acc[s] += value_at(x, k) * p.weight[i];
       }
-      acc[s] += value_at(x, k) * p.weight[i];
+      std::sort(hit.begin(), hit.end());
+      for (int64_t s : hit) {
+        out.idx.push_back(s);
+        out.val.push_back(acc[s]);
+        acc[s] = 0.0;
+      }
+      c.ptr[r + 1] = static_cast<int64_t>(hit.size());
     }
-    std::sort(hit.begin(), hit.end());
-    for (int64_t s : hit) {
-      c.idx.push_back(s);
-      c.val.push_back(acc[s]);
-      acc[s] = 0.0;
+  };
+  if (T == 1) {
+    body(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t) pool.emplace_back(body, t);
+    for (auto& th : pool) th.join();
+  }
+  for (int64_t r = 0; r < x.n; ++r) c.ptr[r + 1] += c.ptr[r];
+  c.idx.resize(c.ptr[x.n]);
+  c.val.resize(c.ptr[x.n]);
+  {
+    std::vector<std::thread> pool;
+    int64_t off = 0;
+    for (unsigned t = 0; t < T; ++t) {
+      pool.emplace_back([&, t, off] {
+        std::copy(parts[t].idx.begin(), parts[t].idx.end(), c.idx.begin() + off);
+        std::copy(parts[t].val.begin(), parts[t].val.end(), c.val.begin() + off);
+      });
+      off += static_cast<int64_t>(parts[t].idx.size());
     }
-    c.ptr[r + 1] = c.nnz();
+    for (auto& th : pool) th.join();
   }
   return c;
 }
