@@ -55,6 +55,13 @@ CONFIGS = {
         kind="zipf", n=1_000_000, f=100_000, mean=50.0, zipf=1.1, abs_values=True, seed=0, beta=1.0,
         ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
         golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32),
+    "cfg5": dict(
+        workload="cfg5: binary CSR N=16,000,000 x F=500,000 (1.02e9 nonzeros), nnz/row max(1,Poisson(64)), Zipf(1.05) "
+                 "columns, on ONE GPU; 4-level hierarchy 50000/5000/500 by sketched k-means (d=32, unit-normalised "
+                 "columns, DESIGN.md §4.10); beta=0.5; solver pcg_vcycle (DESIGN.md §4.11) to rel. residual 1e-6",
+        kind="zipf", n=16_000_000, f=500_000, mean=64.0, zipf=1.05, abs_values=False, seed=0, beta=0.5,
+        ks=[50_000, 5_000, 500], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
+        golden="cfg5_none", betas=[0.5], n_rhs=4, sketch=32),
     "cfg1": dict(
         workload="cfg1: dense clustered N=2000 x F=500 fp64 (row-major dense path); 2-level k-means 50; beta=1e-2; "
                  "FCG(m=20) to rel. residual 1e-6",
@@ -229,6 +236,10 @@ def lowrank_sample_labels(cfg):
     return labels
 
 
+def ref_cg_beta(cfg):
+    return 1.0 if 1.0 in cfg["betas"] else cfg["betas"][0]
+
+
 def run_reference_cfg3(args, cfg):
     """cfg 3's reference arm: the reference's plain cg on the same system (beta = 1),
     all host threads -- once to convergence for its iteration count, then bounded
@@ -237,17 +248,26 @@ def run_reference_cfg3(args, cfg):
     world = dist_setup()[0]
     x = make_matrix(cfg)
     threads = os.cpu_count() or 1
-    c = dict(cfg, ks=[], method="cg", beta=1.0)
+    cb = ref_cg_beta(cfg)
+    c = dict(cfg, ks=[], method="cg", beta=cb)
     t0 = time.time()
-    _, kind, iters = reference_solve_sample(c, x, [], threads, 20000)
+    iters = None
+    if cfg["n"] > 4_000_000:  # cfg 5: thousands of CG iterations at ~seconds each -- use the GPU run's count
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", f"r1_bench_{args.config}.json")))
+            iters = int(prof["cg_iterations"])
+        except Exception:
+            iters = None
+    if iters is None:
+        _, kind, iters = reference_solve_sample(c, x, [], threads, 20000)
     per = []
     for step in range(args.warmup + args.steps):
         sec, kind, _ = reference_solve_sample(c, x, [], threads, 10, 42 + step)
         if step >= args.warmup:
             per.append(sec)
     value = statistics.mean(per) * iters * 1e3
-    sample = (f"reference cg (beta=1), {iters} iterations to 1e-6 (one full run), then 10-iteration samples per "
-              f"step x {iters}; not the headline's algorithm (pcg_vcycle), the reference's fastest here")
+    sample = (f"reference cg (beta={cb:g}), {iters} iterations to 1e-6, 10-iteration samples per step x {iters}; "
+              f"not the headline's algorithm (pcg_vcycle), the reference's fastest here")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
@@ -789,34 +809,38 @@ def run_cfg3(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
         tb.append(e0.elapsed_time(e1))
-    fb = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, False)
+    fb = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
     # CPU baseline: the reference's own solver on this system within minutes -- its plain
     # cg (its multilevel FCG needs > 1000 outer iterations x ~400 inner level-1 solves here,
     # DESIGN.md §4.10), 3 iterations timed, x the GPU's CG iteration count for beta = 1
     cpu = None
-    if not args.no_cpu_baseline:
+    cb = ref_cg_beta(cfg)
+    cg_iters = None
+    try:  # the GPU's plain-CG iteration count on this system (the reference arm's extrapolation)
+        pc = R.PreparedMethod(m, cb, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(cfg["tol"], 50000)))
+        cg_iters = pc.solve_device(bs[0].data_ptr(), w.data_ptr()).iterations
+        pc.close()
+    except Exception:
+        cg_iters = None
+    if not args.no_cpu_baseline and cg_iters:
         try:
-            pm.set_beta(1.0)
-            pc = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(cfg["tol"], 20000)))
-            cg_rep = pc.solve_device(bs[0].data_ptr(), w.data_ptr())
-            pc.close()
-            sec, kind, ran = reference_solve_sample(dict(cfg, ks=[], method="cg", beta=1.0), x, [], 1, 3)
-            cpu = {"value": sec * cg_rep.iterations * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
-                   "sample": f"reference cg on the same system (beta=1), {ran} iterations timed x "
-                             f"{cg_rep.iterations} CG iterations (GPU count); different algorithm from the headline"}
+            sec, kind, ran = reference_solve_sample(dict(cfg, ks=[], method="cg", beta=cb), x, [], 1, 3)
+            cpu = {"value": sec * cg_iters * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
+                   "sample": f"reference cg on the same system (beta={cb:g}), {ran} iterations timed x "
+                             f"{cg_iters} CG iterations (GPU count); different algorithm from the headline"}
         except Exception as e:
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded CounterRng generator with BASELINE cfg 3 shapes (DESIGN.md §6)",
+        "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
         "config": {"workload": cfg["workload"], "n_samples": x.n_samples, "n_features": x.n_features, "nnz": m.nnz,
                    "levels": [x.n_features] + list(cfg["ks"]), "betas": cfg["betas"], "n_rhs": nb,
                    "tol": cfg["tol"], "method": cfg["method"], "parallelism": "single GPU",
-                   "l2": "inputs (600 MB of X) larger than L2"},
+                   "l2": "inputs (X: >= 600 MB) larger than L2"},
         "iterations": [r[0].iterations for r in res], "converged": all(r[0].converged for r in res),
-        "setup_s": setup_s,
+        "setup_s": setup_s, "cg_iterations": cg_iters,
         "roofline": {"bound": "hbm", "kernel": "level-0 operator K1 + K2 (cold L2)", "algorithmic_bytes_per_launch": fb,
                      "ms_per_launch": cold[0], "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
                      "frac": fb / (cold[0] * 1e6) / peak, "traffic": None, "peak_kind": peak_kind},
@@ -847,7 +871,7 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
-    elif args.config == "cfg3":
+    elif args.config in ("cfg3", "cfg5"):
         run_cfg3(args, cfg)
     else:
         run_b200(args, cfg)
