@@ -61,7 +61,7 @@ CONFIGS = {
                  "columns, DESIGN.md §4.10); beta=0.5; solver pcg_vcycle (DESIGN.md §4.11) to rel. residual 1e-6",
         kind="zipf", n=16_000_000, f=500_000, mean=64.0, zipf=1.05, abs_values=False, seed=0, beta=0.5,
         ks=[50_000, 5_000, 500], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
-        golden="cfg5_none", betas=[0.5], n_rhs=4, sketch=32),
+        golden="cfg5_none", betas=[0.5], n_rhs=1, sketch=32),
     "cfg1": dict(
         workload="cfg1: dense clustered N=2000 x F=500 fp64 (row-major dense path); 2-level k-means 50; beta=1e-2; "
                  "FCG(m=20) to rel. residual 1e-6",
@@ -780,7 +780,30 @@ def run_cfg3(args, cfg):
         for i in range(args.steps):
             res.append(go(args.warmup + i, True))
     ms = [r[1] for r in res]
-    value = statistics.mean(ms)
+    single_ms = statistics.mean(ms)
+    value, batched = single_ms, None
+    if nb > 1 and cfg["method"] == "pcg_vcycle":
+        # the config's "k right-hand sides solved as a batched block operator": one
+        # rmg_method_solve_batch call per beta solves all nb columns in lock step
+        # (DESIGN.md §4.12); a step = one beta's batch, value = ms per right-hand side
+        bcm = torch.stack(bs, 0).contiguous()  # column-major n x nb block
+        wcm = torch.empty(nb, x.n_features, dtype=torch.float64, device=dev)
+        bms = []
+        for i in range(args.warmup + args.steps):
+            beta = cfg["betas"][i % len(cfg["betas"])]
+            if cur[0] != beta:
+                pm.set_beta(beta)
+                cur[0] = beta
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            R.ridgemg._lib.check(pm.lib.rmg_method_solve_batch(pm.h, bcm.data_ptr(), wcm.data_ptr(), nb, None, 1))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                bms.append(e0.elapsed_time(e1))
+        value = statistics.mean(bms) / nb
+        batched = {"k": nb, "ms_per_batch": statistics.mean(bms), "ms_per_rhs": value,
+                   "unbatched_ms_per_rhs": single_ms}
     # e2e through the C ABI with host buffers (pinned b, w)
     pb = [torch.from_numpy(R.rng_normals(42 + k, x.n_samples)).pin_memory() for k in range(nb)]
     pw = torch.empty(x.n_features, dtype=torch.float64).pin_memory()
@@ -846,6 +869,7 @@ def run_cfg3(args, cfg):
                      "frac": fb / (cold[0] * 1e6) / peak, "traffic": None, "peak_kind": peak_kind},
         "block_operator": {"k": nb, "ms_per_block": statistics.median(tb), "ms_per_rhs": statistics.median(tb) / nb,
                            "ms_single_apply": cold[0]},
+        "batched_solve": batched,
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.mean(e2e), "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
                 "d2h_bytes_per_step": x.n_features * 8},

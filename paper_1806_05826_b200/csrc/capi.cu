@@ -604,6 +604,19 @@ int rmg_method_solve_batch(rmg_method* pm, const double* b, double* w_out, uint6
     const auto lk_ = hold(pm->m.fine()->ctx);
     rmg::Matrix& x = *pm->m.fine();
     const int64_t n = x.n(), f = x.f();
+    if (k > 1 && k <= 64 && pm->m.block_capable() && std::getenv("RMG_BATCH_SEQ") == nullptr) {
+      // pcg_vcycle: the k columns in lock step over the block operator
+      rmg::Context& c = *x.ctx;
+      RMG_CK(cudaSetDevice(c.device));
+      const uint64_t l0 = c.launches;
+      rmg::DBuf<double> bi, bo;
+      const double* db = stage_in(c, b, static_cast<size_t>(n) * k, on_device, bi);
+      double* dw = stage_out(static_cast<size_t>(f) * k, on_device, w_out, bo);
+      const std::vector<rmg::SolveResult> rs = pm->m.solve_block(db, dw, static_cast<int>(k));
+      finish_out(c, dw, w_out, static_cast<size_t>(f) * k, on_device);
+      for (uint64_t q = 0; q < k; ++q) fill_report(rs[q], (c.launches - l0) / k, reports ? reports + q : nullptr);
+      return;
+    }
     // column q of the column-major blocks b (n x k) and w (f x k) is one solve
     for (uint64_t q = 0; q < k; ++q) {
       const int rc = rmg_method_solve(pm, b + q * n, w_out + q * f, reports ? reports + q : nullptr, on_device);

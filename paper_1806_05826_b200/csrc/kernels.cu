@@ -1594,6 +1594,257 @@ __global__ void __launch_bounds__(kThreads) k_pcg_rz(const double* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- batched pcg_vcycle
+// k right-hand sides in lock step (BASELINE cfg 3's "16 right-hand sides solved as a
+// batched block operator"): every block is row-major n x k, so each row of a
+// block is k contiguous doubles (the block operator's layout).
+// Per column the arithmetic is the single-RHS pcg_vcycle's; reductions are
+// per-column fixed-order (CTA row ranges, then CTAs in order).
+__global__ void __launch_bounds__(kThreads) k_bdot_partial(const double* __restrict__ a, const double* __restrict__ b,
+                                                           int64_t n, int k, double* __restrict__ partial) {
+  __shared__ double red[kThreads];
+  const int rl_n = kThreads / k, t = threadIdx.x, rl = t / k, c = t % k;
+  const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = (n < r0 + rows_per ? n : r0 + rows_per);
+  double acc = 0.0;
+  if (rl < rl_n)
+    for (int64_t i = r0 + rl; i < r1; i += rl_n) acc += a[i * k + c] * b[i * k + c];
+  red[t] = acc;
+  __syncthreads();
+  if (t < k) {
+    double s = 0.0;
+    for (int q = 0; q < rl_n; ++q) s += red[q * k + t];
+    partial[(size_t)blockIdx.x * k + t] = s;
+  }
+}
+
+__global__ void k_bdot_final(const double* __restrict__ partial, int g, int k, double* __restrict__ out) {
+  const int c = threadIdx.x;
+  if (c >= k) return;
+  double s = 0.0;
+  for (int b = 0; b < g; ++b) s += partial[(size_t)b * k + c];
+  out[c] = s;
+}
+
+// begin: nb = ||rhs||, non-finite check, rz = <r, z>
+__global__ void k_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, const double* nonfinite, int k,
+                             double* hist) {
+  const int c = threadIdx.x;
+  if (c >= k) return;
+  BlockScalars& s = sc[c];
+  s.nb = sqrt(rr[c]);
+  s.rz = rz[c];
+  s.it = 0;
+  s.converged = 0;
+  s.status = nonfinite[c] > 0.0 ? 3 : 0;
+  s.done = s.status != 0 ? 1 : 0;
+  s.rel = 1.0;
+  if (s.status == 0 && s.nb == 0.0) {
+    s.converged = 1;
+    s.done = 1;
+    s.rel = 0.0;
+    hist[c] = 0.0;
+  }
+}
+
+// alpha = rz / <p, Ap>; <p, Ap> must be > 0 (krylov.cpp:128-132)
+__global__ void k_bpcg_alpha(BlockScalars* sc, const double* pap, int k) {
+  const int c = threadIdx.x;
+  if (c >= k || sc[c].done) return;
+  BlockScalars& s = sc[c];
+  s.pap = pap[c];
+  if (!(s.pap > 0.0)) {
+    s.status = 2;
+    s.done = 1;
+    s.alpha = 0.0;
+    return;
+  }
+  s.alpha = s.rz / s.pap;
+}
+
+__global__ void __launch_bounds__(kThreads) k_bupdate_xr(double* __restrict__ x, double* __restrict__ r,
+                                                         const double* __restrict__ p, const double* __restrict__ ap,
+                                                         const BlockScalars* sc, int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) {
+    const int c = (int)(q % k);
+    if (sc[c].done) return;
+    const double a = sc[c].alpha;
+    x[q] += a * p[q];
+    r[q] = r[q] - a * ap[q];
+  });
+}
+
+// ||r|| / ||rhs||, history, stop test (krylov.cpp:136-143)
+__global__ void k_bpcg_conv(BlockScalars* sc, const double* rr, int k, double* hist) {
+  const int c = threadIdx.x;
+  if (c >= k || sc[c].done) return;
+  BlockScalars& s = sc[c];
+  const double rel = sqrt(rr[c]) / s.nb;
+  hist[(size_t)s.it * k + c] = rel;
+  s.rel = rel;
+  s.it += 1;
+  if (rel <= s.tol) {
+    s.converged = 1;
+    s.done = 1;
+  } else if (s.it >= s.max_iters) {
+    s.done = 1;
+  }
+}
+
+__global__ void k_bpcg_beta(BlockScalars* sc, const double* rz, int k) {
+  const int c = threadIdx.x;
+  if (c >= k || sc[c].done) return;
+  sc[c].beta = rz[c] / sc[c].rz;
+  sc[c].rz = rz[c];
+}
+
+// p = z + beta p for running columns; finished columns' p is zeroed (their Ap = 0)
+__global__ void __launch_bounds__(kThreads) k_bupdate_p(double* __restrict__ p, const double* __restrict__ z,
+                                                        const BlockScalars* sc, int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) {
+    const int c = (int)(q % k);
+    p[q] = sc[c].done ? 0.0 : z[q] + sc[c].beta * p[q];
+  });
+}
+
+// V-cycle blocks (rows scaled by the level's Jacobi diagonal)
+__global__ void __launch_bounds__(kThreads) k_bvc_pre(const double* __restrict__ r, const double* __restrict__ dinv,
+                                                      double w, double* __restrict__ x1, int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) { x1[q] = w * (dinv[q / k] * r[q]); });
+}
+__global__ void __launch_bounds__(kThreads) k_bvc_post(const double* __restrict__ x2, const double* __restrict__ r,
+                                                       const double* __restrict__ y2, const double* __restrict__ dinv,
+                                                       double w, double* __restrict__ z, int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) { z[q] = x2[q] + w * (dinv[q / k] * (r[q] - y2[q])); });
+}
+__global__ void __launch_bounds__(kThreads) k_bsub(const double* __restrict__ r, double* __restrict__ y, int64_t nk) {
+  grid_stride(nk, [&](int64_t q) { y[q] = r[q] - y[q]; });
+}
+__global__ void __launch_bounds__(kThreads) k_badd(const double* __restrict__ x1, double* __restrict__ e, int64_t nk) {
+  grid_stride(nk, [&](int64_t q) { e[q] = x1[q] + e[q]; });
+}
+// rc[s][c] = sum over the members i of s (increasing) of w_i y[i][c]
+__global__ void __launch_bounds__(kThreads) k_brestrict(const int32_t* __restrict__ mptr,
+                                                        const int32_t* __restrict__ members,
+                                                        const double* __restrict__ weight,
+                                                        const double* __restrict__ y, double* __restrict__ rc,
+                                                        int64_t nc, int k) {
+  grid_stride(nc * k, [&](int64_t q) {
+    const int64_t s = q / k;
+    const int c = (int)(q % k);
+    double acc = 0.0;
+    for (int e = mptr[s]; e < mptr[s + 1]; ++e) {
+      const int i = members[e];
+      acc += weight[i] * y[(int64_t)i * k + c];
+    }
+    rc[q] = acc;
+  });
+}
+// e[i][c] = w_i ec[label_i][c]
+__global__ void __launch_bounds__(kThreads) k_bprolong(const int32_t* __restrict__ label,
+                                                       const double* __restrict__ weight,
+                                                       const double* __restrict__ ec, double* __restrict__ e,
+                                                       int64_t nf, int k) {
+  grid_stride(nf * k, [&](int64_t q) {
+    const int64_t i = q / k;
+    e[q] = weight[i] * ec[(int64_t)label[i] * k + q % k];
+  });
+}
+// ec = A_c^-1 rc for k columns (row-major nc x nc inverse)
+__global__ void __launch_bounds__(kThreads) k_bgemm_inv(const double* __restrict__ ainv, const double* __restrict__ rc,
+                                                        double* __restrict__ ec, int64_t nc, int k) {
+  grid_stride(nc * k, [&](int64_t q) {
+    const int64_t i = q / k;
+    const int c = (int)(q % k);
+    const double* row = ainv + i * nc;
+    double acc = 0.0;
+    for (int64_t j = 0; j < nc; ++j) acc += row[j] * rc[j * k + c];
+    ec[q] = acc;
+  });
+}
+// column-major (n x k) <-> row-major (n x k)
+__global__ void __launch_bounds__(kThreads) k_bcol2row(const double* __restrict__ cm, double* __restrict__ rm,
+                                                       int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) { rm[q] = cm[(q % k) * n + q / k]; });
+}
+__global__ void __launch_bounds__(kThreads) k_brow2col(const double* __restrict__ rm, double* __restrict__ cm,
+                                                       int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) { cm[(q % k) * n + q / k] = rm[q]; });
+}
+__global__ void __launch_bounds__(kThreads) k_bnonfinite(const double* __restrict__ r, int64_t n, int k,
+                                                         double* __restrict__ bad) {
+  // one CTA per column: count of non-finite entries (order irrelevant: integers)
+  const int c = blockIdx.x;
+  __shared__ double sh[kWarps];
+  double cnt = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cnt += isfinite(r[i * k + c]) ? 0.0 : 1.0;
+  cnt = block_sum(cnt, sh);
+  if (threadIdx.x == 0) bad[c] = cnt;
+}
+
+void launch_bdots(const double* a, const double* b, int64_t n, int k, double* partial, int g, double* out,
+                  cudaStream_t s) {
+  k_bdot_partial<<<g, kThreads, 0, s>>>(a, b, n, k, partial);
+  k_bdot_final<<<1, 64, 0, s>>>(partial, g, k, out);
+  check_launch("bdots");
+}
+void launch_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, const double* bad, int k, double* hist,
+                       cudaStream_t s) {
+  k_bpcg_begin<<<1, 64, 0, s>>>(sc, rr, rz, bad, k, hist);
+  check_launch("bpcg_begin");
+}
+void launch_bpcg_alpha(BlockScalars* sc, const double* pap, int k, cudaStream_t s) {
+  k_bpcg_alpha<<<1, 64, 0, s>>>(sc, pap, k);
+}
+void launch_bupdate_xr(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
+                       int k, cudaStream_t s) {
+  k_bupdate_xr<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(x, r, p, ap, sc, n, k);
+}
+void launch_bpcg_conv(BlockScalars* sc, const double* rr, int k, double* hist, cudaStream_t s) {
+  k_bpcg_conv<<<1, 64, 0, s>>>(sc, rr, k, hist);
+}
+void launch_bpcg_beta(BlockScalars* sc, const double* rz, int k, cudaStream_t s) {
+  k_bpcg_beta<<<1, 64, 0, s>>>(sc, rz, k);
+}
+void launch_bupdate_p(double* p, const double* z, const BlockScalars* sc, int64_t n, int k, cudaStream_t s) {
+  k_bupdate_p<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(p, z, sc, n, k);
+  check_launch("bpcg_update");
+}
+void launch_bvc_pre(const double* r, const double* dinv, double w, double* x1, int64_t n, int k, cudaStream_t s) {
+  k_bvc_pre<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(r, dinv, w, x1, n, k);
+}
+void launch_bvc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
+                     int64_t n, int k, cudaStream_t s) {
+  k_bvc_post<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(x2, r, y2, dinv, w, z, n, k);
+}
+void launch_bsub(const double* r, double* y, int64_t nk, cudaStream_t s) {
+  k_bsub<<<grid_for(nk, 148 * 8), kThreads, 0, s>>>(r, y, nk);
+}
+void launch_badd(const double* x1, double* e, int64_t nk, cudaStream_t s) {
+  k_badd<<<grid_for(nk, 148 * 8), kThreads, 0, s>>>(x1, e, nk);
+}
+void launch_brestrict(const int32_t* mptr, const int32_t* members, const double* weight, const double* y, double* rc,
+                      int64_t nc, int k, cudaStream_t s) {
+  k_brestrict<<<grid_for(nc * k, 148 * 8), kThreads, 0, s>>>(mptr, members, weight, y, rc, nc, k);
+}
+void launch_bprolong(const int32_t* label, const double* weight, const double* ec, double* e, int64_t nf, int k,
+                     cudaStream_t s) {
+  k_bprolong<<<grid_for(nf * k, 148 * 8), kThreads, 0, s>>>(label, weight, ec, e, nf, k);
+}
+void launch_bgemm_inv(const double* ainv, const double* rc, double* ec, int64_t nc, int k, cudaStream_t s) {
+  k_bgemm_inv<<<grid_for(nc * k, 148 * 8), kThreads, 0, s>>>(ainv, rc, ec, nc, k);
+}
+void launch_bcol2row(const double* cm, double* rm, int64_t n, int k, cudaStream_t s) {
+  k_bcol2row<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(cm, rm, n, k);
+}
+void launch_brow2col(const double* rm, double* cm, int64_t n, int k, cudaStream_t s) {
+  k_brow2col<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(rm, cm, n, k);
+}
+void launch_bnonfinite(const double* r, int64_t n, int k, double* bad, cudaStream_t s) {
+  k_bnonfinite<<<k, kThreads, 0, s>>>(r, n, k, bad);
+  check_launch("bnonfinite");
+}
+
 void launch_vc_pre(const double* r, const double* dinv, double w, double* x1, int64_t n, const int32_t* done,
                    cudaStream_t s) {
   k_vc_pre<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(r, dinv, w, x1, n, done);

@@ -203,6 +203,34 @@ void launch_vc_sub(const double* r, double* y, int64_t n, const int32_t* done, c
 void launch_vc_add(const double* x1, double* e, int64_t n, const int32_t* done, cudaStream_t s);
 void launch_vc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
                     int64_t n, const int32_t* done, cudaStream_t s);
+// batched pcg_vcycle (k right-hand sides in lock step; row-major n x k blocks)
+struct BlockScalars {
+  double nb, rz, alpha, beta, rel, pap, tol;
+  int32_t it, max_iters, done, converged, status, pad;
+};
+void launch_bdots(const double* a, const double* b, int64_t n, int k, double* partial, int g, double* out,
+                  cudaStream_t s);
+void launch_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, const double* bad, int k, double* hist,
+                       cudaStream_t s);
+void launch_bpcg_alpha(BlockScalars* sc, const double* pap, int k, cudaStream_t s);
+void launch_bupdate_xr(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
+                       int k, cudaStream_t s);
+void launch_bpcg_conv(BlockScalars* sc, const double* rr, int k, double* hist, cudaStream_t s);
+void launch_bpcg_beta(BlockScalars* sc, const double* rz, int k, cudaStream_t s);
+void launch_bupdate_p(double* p, const double* z, const BlockScalars* sc, int64_t n, int k, cudaStream_t s);
+void launch_bvc_pre(const double* r, const double* dinv, double w, double* x1, int64_t n, int k, cudaStream_t s);
+void launch_bvc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
+                     int64_t n, int k, cudaStream_t s);
+void launch_bsub(const double* r, double* y, int64_t nk, cudaStream_t s);
+void launch_badd(const double* x1, double* e, int64_t nk, cudaStream_t s);
+void launch_brestrict(const int32_t* mptr, const int32_t* members, const double* weight, const double* y, double* rc,
+                      int64_t nc, int k, cudaStream_t s);
+void launch_bprolong(const int32_t* label, const double* weight, const double* ec, double* e, int64_t nf, int k,
+                     cudaStream_t s);
+void launch_bgemm_inv(const double* ainv, const double* rc, double* ec, int64_t nc, int k, cudaStream_t s);
+void launch_bcol2row(const double* cm, double* rm, int64_t n, int k, cudaStream_t s);
+void launch_brow2col(const double* rm, double* cm, int64_t n, int k, cudaStream_t s);
+void launch_bnonfinite(const double* r, int64_t n, int k, double* bad, cudaStream_t s);
 void launch_pcg_rz(const double* r, const double* z, int64_t n, KrylovScalars* sc, bool begin, const VecWork& w,
                    cudaStream_t s);
 void launch_cg_update_p(double* p, const double* z, int64_t n, const KrylovScalars* sc,

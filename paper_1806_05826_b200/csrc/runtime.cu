@@ -489,7 +489,7 @@ void Matrix::build_block_schedule(const HostCsr& ht) {
   bview.seg = bseg.get();
 }
 
-void Matrix::apply_block(const double* v, double* out, double beta, int k) {
+void Matrix::apply_block(const double* v, double* out, double beta, int k, bool sync) {
   if (dense || comm != nullptr) throw InvalidArgument("block operator: single-GPU CSR matrices only");
   if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative");
@@ -497,7 +497,7 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k) {
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
   launch_ridge_block(x.view, xt.view, bview, v, out, beta, k, bt.get(), bvp.get(), ctx->stream);
-  ctx->sync();
+  if (sync) ctx->sync();
 }
 
 // Dense X kept on the device: rows padded to ld = F rounded up to 4 elements
@@ -1846,6 +1846,141 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
   m.apply(v.e.get(), Epi::Axpby, a, prof(k));
   launch_vc_post(v.e.get(), r, v.y.get(), v.dinv.get(), v.w, z, nf, done, s);
   ctx_->launches += 8;
+}
+
+bool Method::block_capable() const {
+  if (kind_ != RMG_METHOD_PCG_VCYCLE || coarse_.empty()) return false;
+  for (size_t k = 0; k < coarse_.size(); ++k) {
+    const Matrix& m = level_matrix(k);
+    if (m.dense != nullptr || m.comm != nullptr) return false;
+  }
+  return true;
+}
+
+// the V-cycle of vcycle() on k columns at once (row-major blocks; every operator
+// application is one block operator call)
+void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
+  cudaStream_t s = ctx_->stream;
+  const size_t L = coarse_.size();
+  CoarseLevelDev& c = *coarse_[lv];
+  Matrix& m = level_matrix(lv);
+  const int64_t nf = m.f(), nc = c.mat->f();
+  VcLevel& v = *vc_[lv];
+  while (bl_.size() <= lv) bl_.push_back(std::make_unique<BlockLevel>());
+  BlockLevel& b = *bl_[lv];
+  const size_t nfk = static_cast<size_t>(std::max<int64_t>(1, nf)) * k, nck = static_cast<size_t>(std::max<int64_t>(1, nc)) * k;
+  if (b.x1.size() < nfk) {
+    b.x1.alloc(nfk);
+    b.y.alloc(nfk);
+    b.e.alloc(nfk);
+  }
+  if (b.rc.size() < nck) {
+    b.rc.alloc(nck);
+    b.ec.alloc(nck);
+  }
+  launch_bvc_pre(r, v.dinv.get(), v.w, b.x1.get(), nf, k, s);
+  m.apply_block(b.x1.get(), b.y.get(), level_beta(lv), k, false);
+  launch_bsub(r, b.y.get(), nf * k, s);
+  launch_brestrict(c.mptr.get(), c.members.get(), c.weight.get(), b.y.get(), b.rc.get(), nc, k, s);
+  if (lv + 1 == L)
+    launch_bgemm_inv(ainv_.get(), b.rc.get(), b.ec.get(), nc, k, s);
+  else
+    bvcycle(lv + 1, b.rc.get(), b.ec.get(), k);
+  launch_bprolong(c.label.get(), c.weight.get(), b.ec.get(), b.e.get(), nf, k, s);
+  launch_badd(b.x1.get(), b.e.get(), nf * k, s);
+  m.apply_block(b.e.get(), b.y.get(), level_beta(lv), k, false);
+  launch_bvc_post(b.e.get(), r, b.y.get(), v.dinv.get(), v.w, z, nf, k, s);
+  ctx_->launches += 10;
+}
+
+std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, int k) {
+  if (!block_capable()) throw InvalidArgument("solve_block: pcg_vcycle over single-GPU CSR levels only");
+  if (k < 1 || k > 64) throw InvalidArgument("solve_block: k must be in [1, 64]");
+  RMG_CK(cudaSetDevice(ctx_->device));
+  cudaStream_t s = ctx_->stream;
+  Matrix& m = *fine_;
+  const int64_t n = m.f(), N = m.n();
+  const uint64_t maxit = std::max<uint64_t>(solver.max_iters, 1);
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (n + 255) / 256)));
+  BlockWork& w = bw_;
+  const size_t nk = static_cast<size_t>(std::max<int64_t>(1, n)) * k;
+  if (w.k != k || w.x.size() < nk) {
+    w.x.alloc(nk);
+    w.r.alloc(nk);
+    w.z.alloc(nk);
+    w.p.alloc(nk);
+    w.ap.alloc(nk);
+    w.rhs_cm.alloc(nk);
+    w.partial.alloc(static_cast<size_t>(g) * 64);
+    w.dots.alloc(4 * 64);
+    w.sc.alloc(64);
+    w.k = k;
+  }
+  if (w.hist.size() < (maxit + 1) * k) w.hist.alloc((maxit + 1) * k);
+  double *rr = w.dots.get(), *rz = rr + 64, *pap = rr + 128, *bad = rr + 192;
+  const auto t0 = Clock::now();
+  for (int q = 0; q < k; ++q) m.spmv_t(b_cm + static_cast<size_t>(q) * N, w.rhs_cm.get() + static_cast<size_t>(q) * n);
+  launch_bcol2row(w.rhs_cm.get(), w.r.get(), n, k, s);
+  RMG_CK(cudaMemsetAsync(w.x.get(), 0, nk * sizeof(double), s));
+  std::vector<BlockScalars> hs(k);
+  for (auto& e : hs) {
+    std::memset(&e, 0, sizeof(e));
+    e.tol = solver.tol;
+    e.max_iters = static_cast<int32_t>(std::min<uint64_t>(maxit, INT32_MAX));
+  }
+  RMG_CK(cudaMemcpyAsync(w.sc.get(), hs.data(), k * sizeof(BlockScalars), cudaMemcpyHostToDevice, s));
+  launch_bnonfinite(w.r.get(), n, k, bad, s);
+  launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, s);
+  bvcycle(0, w.r.get(), w.z.get(), k);
+  launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, s);
+  launch_bpcg_begin(w.sc.get(), rr, rz, bad, k, w.hist.get(), s);
+  RMG_CK(cudaMemcpyAsync(w.p.get(), w.z.get(), nk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  const double beta0 = level_beta(0);
+  for (;;) {
+    RMG_CK(cudaMemcpyAsync(hs.data(), w.sc.get(), k * sizeof(BlockScalars), cudaMemcpyDeviceToHost, s));
+    ctx_->sync();
+    bool all = true;
+    for (int c = 0; c < k; ++c) {
+      if (hs[c].status == 3) throw InvalidArgument("cg: non-finite rhs (right-hand side " + std::to_string(c) + ")");
+      if (hs[c].status == 2)
+        throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs[c].pap) + " at iteration " + std::to_string(hs[c].it) +
+                           " of right-hand side " + std::to_string(c) + "; operator is not positive definite");
+      all = all && hs[c].done;
+    }
+    if (all) break;
+    m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);
+    launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, s);
+    launch_bpcg_alpha(w.sc.get(), pap, k, s);
+    launch_bupdate_xr(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, s);
+    launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, s);
+    launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), s);
+    bvcycle(0, w.r.get(), w.z.get(), k);
+    launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, s);
+    launch_bpcg_beta(w.sc.get(), rz, k, s);
+    launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, s);
+    ctx_->launches += 12;
+  }
+  const double wall = secs(t0);
+  launch_brow2col(w.x.get(), w_cm, n, k, s);
+  int32_t itmax = 0;
+  for (const auto& e : hs) itmax = std::max(itmax, e.it);
+  std::vector<double> hist(static_cast<size_t>(itmax + 1) * k);
+  if (!hist.empty())
+    RMG_CK(cudaMemcpyAsync(hist.data(), w.hist.get(), hist.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx_->sync();
+  std::vector<SolveResult> out(k);
+  for (int c = 0; c < k; ++c) {
+    SolveResult& r = out[c];
+    r.wall = wall;
+    r.iterations = static_cast<uint64_t>(hs[c].it);
+    r.converged = hs[c].converged != 0;
+    r.final_rel = hs[c].rel;
+    const size_t nh = hs[c].it == 0 && hs[c].converged ? 1 : static_cast<size_t>(hs[c].it);
+    r.hist.resize(nh);
+    for (size_t i = 0; i < nh; ++i) r.hist[i] = hist[i * k + c];
+    r.inner.assign(static_cast<size_t>(hs[c].it), 0);
+  }
+  return out;
 }
 
 // PCG (krylov.cpp:94-157) with z = M r the V-cycle

@@ -197,7 +197,7 @@ struct Matrix {
   DBuf<double> bseg, bt, bvp;  // + scratch T (N x k) and permuted V (F x k), kept across calls
   void build_block_schedule(const HostCsr& ht);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
-  void apply_block(const double* v, double* out, double beta, int k);
+  void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
   // dense X without a host CSR (setup on the device): from host
   // rows, or from a device buffer already padded to ld (coarse levels)
@@ -340,6 +340,25 @@ class Method {
   void build_vcycle();
   void vcycle(size_t k, const double* r, double* z, const int32_t* done);
   uint64_t run_pcg_vcycle(const double* rhs, SolveResult* out);
+  // batched pcg_vcycle: k right-hand sides in lock step over the block operator
+  struct BlockLevel {
+    DBuf<double> x1, y, e, rc, ec;
+  };
+  std::vector<std::unique_ptr<BlockLevel>> bl_;
+  struct BlockWork {
+    int k = 0;
+    DBuf<double> x, r, z, p, ap, rhs_cm, partial, dots, hist;
+    DBuf<BlockScalars> sc;
+  } bw_;
+  void bvcycle(size_t lv, const double* r, double* z, int k);
+
+ public:
+  // pcg_vcycle over single-GPU CSR levels: solve_batch runs the k columns in lock step
+  bool block_capable() const;
+  // b_cm: column-major n_samples x k (device), w_cm: column-major F x k (device)
+  std::vector<SolveResult> solve_block(const double* b_cm, double* w_cm, int k);
+
+ private:
   std::vector<int64_t> sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc);
   DBuf<double> gm_basis_, gm_z_, gm_h_, gm_part_;  // FGMRES: basis, preconditioned basis, Hessenberg column
   DenseKrylovArgs dense_args(size_t k, const double* rhs);
