@@ -166,3 +166,25 @@ def test_dense_sharded_single_rank_nccl(gpu):
     assert np.linalg.norm(s1.w - s2.w) <= 1e-9 * np.linalg.norm(s2.w)
     ms.close()
     comm.close()
+
+
+@pytest.mark.gpu
+def test_sharded_pcg_vcycle_single_rank_nccl(gpu):
+    """pcg_vcycle on the row-sharded operator: the fine-level
+    applications go through the all-reduce path, the coarse levels are replicated;
+    equal to the unsharded solve."""
+    x = R.synth_sparse_zipf(8000, 900, 25.0, 1.1, True, 5)
+    uid = R.Comm.new_unique_id()
+    comm = R.Comm(gpu, 1, 0, uid)
+    ms = R.DeviceMatrix(x, gpu, comm=comm)
+    mu = R.DeviceMatrix(x, gpu)
+    levels = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS, target_size=90),
+                          solver=R.CoarseSolveChoice(kind=R.INNER_FCG)),
+              R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS, target_size=12))]
+    spec = R.MethodSpec(kind=R.PCG_VCYCLE, levels=levels, solver=R.SolverConfig(1e-10, 2000))
+    bb = R.rng_normals(7, x.n_samples)
+    s1, s2 = R.solve_system(ms, 0.5, bb, spec), R.solve_system(mu, 0.5, bb, spec)
+    assert s1.report.converged and abs(s1.report.iterations - s2.report.iterations) <= 1
+    assert np.linalg.norm(s1.w - s2.w) <= 1e-9 * np.linalg.norm(s2.w)
+    ms.close()
+    comm.close()
