@@ -567,7 +567,10 @@ def run_b200(args, cfg):
         inner_mean = float(np.mean([np.mean(r.inner_iterations) for r in prof_reports if len(r.inner_iterations)]))
         bytes_per_launch = inner_mean * 8 * (nk * nk + nk * nnext + 48 * nk)
         kernel_name = (f"k_dense_krylov: persistent level-{dom['level']} inner FCG (n={nk}, "
-                       f"{inner_mean:.1f} iterations/launch), in-situ events")
+                       f"{inner_mean:.1f} iterations/launch), in-situ events; the bytes are A_k read from shared "
+                       f"memory and Q plus the Krylov vectors from L2 every inner iteration (DRAM: A_k once per "
+                       f"launch); the kernel is bound by its two grid-wide exchanges per iteration, not by DRAM "
+                       f"(DESIGN.md §4.4, profiles/r1b_dense2.md)")
     elif m.is_dense():  # dense levels: one fused sweep (fine: its storage; device-built coarse levels: fp64)
         esz = x.dense().itemsize if dom["level"] == 0 else 8
         bytes_per_launch = dense_algorithmic_bytes(x.n_samples, dom["n_features"], esz)
