@@ -416,6 +416,39 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
       ++pos;
     }
   });
+  // Long rows (warp per row: lanes read 32 consecutive entries, two half-warp
+  // phases of 16 eight-byte SMEM loads): order each (block, row) segment in rounds
+  // of one entry per bank pair (sample index mod 16), so a half-warp's 16 gathers of
+  // the t-slice hit 16 distinct bank pairs instead of colliding at random.  The sum
+  // order changes (still fixed: deterministic).  RMG_HOT_BANKS=0 keeps sample order.
+  if (std::getenv("RMG_HOT_BANKS") == nullptr || std::string(std::getenv("RMG_HOT_BANKS")) != "0") {
+    par([&](int64_t h) {
+      if (h >= hA) return;
+      std::vector<uint16_t> bi[16];
+      std::vector<double> bv[16];
+      for (int64_t b = 0; b < nblk; ++b) {
+        const int64_t q0 = rp[b * H + h], q1 = rp[b * H + h + 1];
+        for (int k = 0; k < 16; ++k) {
+          bi[k].clear();
+          bv[k].clear();
+        }
+        for (int64_t q = q0; q < q1; ++q) {
+          bi[i16[q] & 15].push_back(i16[q]);
+          if (!pattern) bv[i16[q] & 15].push_back(v[q]);
+        }
+        size_t pos[16] = {0};
+        int64_t q = q0;
+        while (q < q1)
+          for (int k = 0; k < 16; ++k)
+            if (pos[k] < bi[k].size()) {
+              i16[q] = bi[k][pos[k]];
+              if (!pattern) v[q] = bv[k][pos[k]];
+              ++pos[k];
+              ++q;
+            }
+      }
+    });
+  }
   std::vector<int32_t> rp32(rp.begin(), rp.end());
   cudaStream_t s = ctx->stream;
   hx->ptr.upload(rp32.data(), rp32.size(), s);
