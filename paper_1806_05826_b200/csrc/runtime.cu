@@ -1792,6 +1792,7 @@ void Method::precondition(const double* r, double* z) {
 void Method::build_vcycle() {
   cudaStream_t s = ctx_->stream;
   const size_t L = coarse_.size();
+  vc_graph_.reset();  // its kernels point at the buffers rebuilt here
   vc_.clear();
   for (size_t k = 0; k < L; ++k) {
     Matrix& m = level_matrix(k);
@@ -2016,6 +2017,83 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   return out;
 }
 
+namespace {
+__global__ void k_set_while(cudaGraphConditionalHandle h, const int32_t* done) {
+  cudaGraphSetConditional(h, *done ? 0u : 1u);
+}
+}  // namespace
+
+// one PCG iteration with the V-cycle (the launch sequence the graph captures)
+void Method::pcg_vcycle_iteration() {
+  KrylovWork& w = *work_[0];
+  Matrix& m = *fine_;
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  double* p = w.p_ring.get();
+  double* ap = w.ap_ring.get();
+  double* z = w.z.get();
+  const int32_t* done = &w.sc.get()->done;
+  XtArgs a;
+  a.v = p;
+  a.out = ap;
+  a.beta = level_beta(0);
+  a.sc = w.sc.get();
+  a.done = done;
+  m.apply(p, Epi::Cg, a, prof(0));
+  launch_cg_axpy(w.x.get(), w.r.get(), z, nullptr, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s, true);
+  vcycle(0, w.r.get(), z, done);
+  launch_pcg_rz(w.r.get(), z, n, w.sc.get(), false, w.vw, s);
+  launch_cg_update_p(p, z, n, w.sc.get(), s);
+  ctx_->launches += 3;
+}
+
+// The while-node graph (CUDA 12.4+ conditional nodes).  Built once per hierarchy /
+// beta (the buffers it points at are fixed); false when the runtime refuses it.
+bool Method::build_vcycle_graph() {
+  if (std::getenv("RMG_NO_GRAPH") != nullptr) return false;
+  for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
+    if (level_matrix(k).comm != nullptr) return false;
+  auto gl = std::make_unique<GraphLoop>();
+  cudaStream_t s = ctx_->stream;
+  if (cudaGraphCreate(&gl->g, 0) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, gl->g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return false;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, gl->g, nullptr, 0, &cp) != cudaSuccess) return false;
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const uint64_t l0 = ctx_->launches;
+  bool ok = true;
+  try {
+    pcg_vcycle_iteration();
+    k_set_while<<<1, 1, 0, s>>>(h, &work_[0]->sc.get()->done);
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &captured);
+  if (!ok || ec != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  gl->launches_per_iter = ctx_->launches - l0 + 1;
+  ctx_->launches = l0;
+  if (cudaGraphInstantiate(&gl->exec, gl->g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  vc_graph_ = std::move(gl);
+  return true;
+}
+
 // PCG (krylov.cpp:94-157) with z = M r the V-cycle
 uint64_t Method::run_pcg_vcycle(const double* rhs, SolveResult* out) {
   KrylovWork& w = *work_[0];
@@ -2036,18 +2114,17 @@ uint64_t Method::run_pcg_vcycle(const double* rhs, SolveResult* out) {
     RMG_CK(cudaMemcpyAsync(p, z, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
     ctx_->launches += 2;
   }
+  if (!hs.done && !profiling_ && (vc_graph_ || build_vcycle_graph())) {
+    // the whole iteration loop on the device: one graph launch
+    RMG_CK(cudaGraphLaunch(vc_graph_->exec, s));
+    hs = ctx_->read(w.sc.get());
+    ctx_->launches += vc_graph_->launches_per_iter * static_cast<uint64_t>(std::max(1, hs.it));
+    if (hs.status == 2)
+      throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
+                         "; operator is not positive definite");
+  }
   while (!hs.done) {
-    XtArgs a;
-    a.v = p;
-    a.out = ap;
-    a.beta = level_beta(0);
-    a.sc = w.sc.get();
-    m.apply(p, Epi::Cg, a, prof(0));
-    launch_cg_axpy(w.x.get(), w.r.get(), z, nullptr, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s, true);
-    vcycle(0, w.r.get(), z, done);
-    launch_pcg_rz(w.r.get(), z, n, w.sc.get(), false, w.vw, s);
-    launch_cg_update_p(p, z, n, w.sc.get(), s);
-    ctx_->launches += 3;
+    pcg_vcycle_iteration();
     hs = ctx_->read(w.sc.get());
     if (profiling_) collect_profiles();
     if (hs.status == 2)

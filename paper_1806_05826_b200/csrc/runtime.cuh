@@ -338,6 +338,21 @@ class Method {
   };
   std::vector<std::unique_ptr<VcLevel>> vc_;
   void build_vcycle();
+  // pcg_vcycle's iteration as a CUDA graph inside a device-side while loop (a
+  // conditional node whose condition a kernel sets from the solver's done flag):
+  // one graph launch per solve, no host round trip per iteration
+  struct GraphLoop {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches_per_iter = 0;
+    ~GraphLoop() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (g) cudaGraphDestroy(g);
+    }
+  };
+  std::unique_ptr<GraphLoop> vc_graph_;
+  void pcg_vcycle_iteration();
+  bool build_vcycle_graph();
   void vcycle(size_t k, const double* r, double* z, const int32_t* done);
   uint64_t run_pcg_vcycle(const double* rhs, SolveResult* out);
   // batched pcg_vcycle: k right-hand sides in lock step over the block operator
