@@ -1287,6 +1287,10 @@ __global__ void k_fill(double* p, double v, int64_t n) {
 __global__ void k_copy_inner_count(const KrylovScalars* inner, KrylovScalars* outer, uint64_t* hist) {
   if (outer->done) return;
   hist[outer->it] = (uint64_t)inner->it;
+  if (inner->status >= 1 && inner->status <= 3) {  // inner breakdown / bad rhs ends the outer solve too
+    outer->status = 100 + inner->status;            // (the host turns it into the inner solve's error)
+    outer->done = 1;
+  }
 }
 
 inline void check_launch(const char* what) {

@@ -15,6 +15,16 @@
 
 namespace rmg {
 
+namespace {
+// graph while-loops (pcg_vcycle, outer FCG): continue while the solver is not done
+__global__ void k_set_while(cudaGraphConditionalHandle h, const int32_t* done) {
+  cudaGraphSetConditional(h, *done ? 0u : 1u);
+}
+void launch_set_while(cudaGraphConditionalHandle h, const int32_t* done, cudaStream_t s) {
+  k_set_while<<<1, 1, 0, s>>>(h, done);
+}
+}  // namespace
+
 // ------------------------------------------------------------------ Context
 Context::Context(int dev) : device(dev) {
   int n = 0;
@@ -1224,6 +1234,8 @@ void Method::jacobi_diag() {
 void Method::set_beta(double beta) {
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
   RMG_CK(cudaSetDevice(ctx_->device));
+  fcg_graph_.reset();  // the graphs point at the coarse buffers rebuilt below
+  vc_graph_.reset();
   beta_ = beta;
   if (kind_ == RMG_METHOD_CG) return;
   if (kind_ == RMG_METHOD_JACOBI_CG) {
@@ -1549,6 +1561,78 @@ void record(Context* ctx, KrylovWork& w, const KrylovScalars& hs, const std::vec
 }
 }  // namespace
 
+// one outer FCG iteration at level k (krylov.cpp:185-220): the launch sequence the
+// graph loop captures
+void Method::fcg_iteration(size_t k) {
+  KrylovWork& w = *work_[k];
+  Matrix& m = level_matrix(k);
+  const int64_t n = m.f();
+  cudaStream_t s = ctx_->stream;
+  const bool nested = k + 1 < coarse_.size() + 0 && k + 1 < work_.size();
+  KrylovWork* iw = nested ? work_[k + 1].get() : nullptr;
+  precond(k, w.r.get(), w.z.get());
+  if (iw) {
+    launch_copy_inner_count(iw->sc.get(), w.sc.get(), w.inner_hist.get(), s);
+    ctx_->launches += 1;
+  }
+  launch_fcg_gs(w.z.get(), w.ap_ring.get(), w.p_ring.get(), n, w.sc.get(), w.vw, s);
+  XtArgs a;
+  a.v = w.p_ring.get();
+  a.r = w.r.get();
+  a.out = w.ap_ring.get();
+  a.beta = level_beta(k);
+  a.sc = w.sc.get();
+  a.ring_stride = static_cast<int>(n);
+  m.apply_ring(w.p_ring.get(), static_cast<int>(n), w.sc.get(), Epi::Fcg, a, prof(k));
+  launch_fcg_axpy(w.x.get(), w.r.get(), w.p_ring.get(), w.ap_ring.get(), n, w.sc.get(), w.hist.get(), w.vw, s);
+  ctx_->launches += 3;
+}
+
+bool Method::build_fcg_graph() {
+  if (std::getenv("RMG_NO_GRAPH") != nullptr) return false;
+  for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
+    if (level_matrix(k).comm != nullptr) return false;
+  auto gl = std::make_unique<GraphLoop>();
+  cudaStream_t s = ctx_->stream;
+  if (cudaGraphCreate(&gl->g, 0) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, gl->g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return false;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, gl->g, nullptr, 0, &cp) != cudaSuccess) return false;
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const uint64_t l0 = ctx_->launches;
+  bool ok = true;
+  try {
+    fcg_iteration(0);
+    launch_set_while(h, &work_[0]->sc.get()->done, s);
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &captured);
+  if (!ok || ec != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  gl->launches_per_iter = ctx_->launches - l0 + 1;
+  ctx_->launches = l0;
+  if (cudaGraphInstantiate(&gl->exec, gl->g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  fcg_graph_ = std::move(gl);
+  return true;
+}
+
 // fcg (krylov.cpp:159-227) at level k with the level-k preconditioner
 uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out) {
   KrylovWork& w = *work_[k];
@@ -1564,23 +1648,30 @@ uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out
   const bool nested = k + 1 < coarse_.size() + 0 && k + 1 < work_.size();
   KrylovWork* iw = nested ? work_[k + 1].get() : nullptr;
   KrylovScalars ihs{};
-  while (!hs.done) {
-    precond(k, w.r.get(), w.z.get());
-    if (iw) {
-      launch_copy_inner_count(iw->sc.get(), w.sc.get(), w.inner_hist.get(), s);
-      ctx_->launches += 1;
+  // outer loop on the device (one CUDA graph launch) when every inner level runs
+  // without the host: the persistent dense solver or the direct coarsest solve
+  const bool graphable = k == 0 && !profiling_ && (!nested || (dense_.size() > 1 && dense_[1] != nullptr));
+  if (!hs.done && graphable && (fcg_graph_ || build_fcg_graph())) {
+    RMG_CK(cudaGraphLaunch(fcg_graph_->exec, s));
+    if (iw)
+      ctx_->read2(w.sc.get(), &hs, iw->sc.get(), &ihs);
+    else
+      hs = ctx_->read(w.sc.get());
+    ctx_->launches += fcg_graph_->launches_per_iter * static_cast<uint64_t>(std::max(1, hs.it));
+    if (hs.status >= 101 && hs.status <= 103) {
+      const int st = hs.status - 100;
+      if (st == 3) throw InvalidArgument("fcg: non-finite rhs in the level-" + std::to_string(k + 1) + " inner solve");
+      throw RuntimeError(std::string(st == 1 ? "fcg: breakdown, <p, Ap> = 0" : "fcg: <p, Ap> <= 0") +
+                         " at iteration " + std::to_string(ihs.it) + " of the level-" + std::to_string(k + 1) +
+                         " inner solve; operator is not positive definite");
     }
-    launch_fcg_gs(w.z.get(), w.ap_ring.get(), w.p_ring.get(), n, w.sc.get(), w.vw, s);
-    XtArgs a;
-    a.v = w.p_ring.get();
-    a.r = w.r.get();
-    a.out = w.ap_ring.get();
-    a.beta = level_beta(k);
-    a.sc = w.sc.get();
-    a.ring_stride = static_cast<int>(n);
-    m.apply_ring(w.p_ring.get(), static_cast<int>(n), w.sc.get(), Epi::Fcg, a, prof(k));
-    launch_fcg_axpy(w.x.get(), w.r.get(), w.p_ring.get(), w.ap_ring.get(), n, w.sc.get(), w.hist.get(), w.vw, s);
-    ctx_->launches += 3;
+    if (hs.status == 1) throw RuntimeError("fcg: breakdown, <p, Ap> = 0 at iteration " + std::to_string(hs.it));
+    if (hs.status == 2)
+      throw RuntimeError("fcg: <p, Ap> < 0 at iteration " + std::to_string(hs.it) +
+                         "; operator is not positive definite");
+  }
+  while (!hs.done) {
+    fcg_iteration(k);
     if (iw) {
       ctx_->read2(w.sc.get(), &hs, iw->sc.get(), &ihs);
       if (ihs.status == 1 || ihs.status == 2)
@@ -2017,12 +2108,6 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   return out;
 }
 
-namespace {
-__global__ void k_set_while(cudaGraphConditionalHandle h, const int32_t* done) {
-  cudaGraphSetConditional(h, *done ? 0u : 1u);
-}
-}  // namespace
-
 // one PCG iteration with the V-cycle (the launch sequence the graph captures)
 void Method::pcg_vcycle_iteration() {
   KrylovWork& w = *work_[0];
@@ -2074,7 +2159,7 @@ bool Method::build_vcycle_graph() {
   bool ok = true;
   try {
     pcg_vcycle_iteration();
-    k_set_while<<<1, 1, 0, s>>>(h, &work_[0]->sc.get()->done);
+    launch_set_while(h, &work_[0]->sc.get()->done, s);
   } catch (...) {
     ok = false;
   }

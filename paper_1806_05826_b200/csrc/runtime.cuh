@@ -351,6 +351,9 @@ class Method {
     }
   };
   std::unique_ptr<GraphLoop> vc_graph_;
+  std::unique_ptr<GraphLoop> fcg_graph_;  // the outer FCG loop when no inner level needs the host
+  void fcg_iteration(size_t k);
+  bool build_fcg_graph();
   void pcg_vcycle_iteration();
   bool build_vcycle_graph();
   void vcycle(size_t k, const double* r, double* z, const int32_t* done);
