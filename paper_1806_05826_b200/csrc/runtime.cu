@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <thread>
 
@@ -24,6 +25,55 @@ void launch_set_while(cudaGraphConditionalHandle h, const int32_t* done, cudaStr
   k_set_while<<<1, 1, 0, s>>>(h, done);
 }
 }  // namespace
+
+// A graph holding one while node whose body is `body()` (captured on the
+// context's private capture stream, with ctx->stream pointing at it meanwhile)
+// followed by the kernel that re-evaluates the condition from `done`.
+bool capture_while_graph(Context* ctx, const int32_t* done, const std::function<void()>& body, cudaGraph_t* g_out,
+                         cudaGraphExec_t* exec_out, uint64_t* launches_out) {
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
+  auto fail = [&] {
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    return false;
+  };
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail();
+  cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+  if (ctx->capture_stream == nullptr &&
+      cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail();
+  const cudaStream_t orig = ctx->stream;
+  if (cudaStreamBeginCaptureToGraph(ctx->capture_stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+      cudaSuccess)
+    return fail();
+  ctx->stream = ctx->capture_stream;
+  const uint64_t l0 = ctx->launches;
+  bool ok = true;
+  try {
+    body();
+    launch_set_while(h, done, ctx->stream);
+  } catch (...) {
+    ok = false;
+  }
+  ctx->stream = orig;
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(ctx->capture_stream, &captured);
+  if (!ok || ec != cudaSuccess || cudaGetLastError() != cudaSuccess) return fail();
+  *launches_out = ctx->launches - l0 + 1;
+  ctx->launches = l0;
+  if (cudaGraphInstantiate(exec_out, g, 0) != cudaSuccess) return fail();
+  *g_out = g;
+  return true;
+}
 
 // ------------------------------------------------------------------ Context
 Context::Context(int dev) : device(dev) {
@@ -46,6 +96,7 @@ void Context::read2(const KrylovScalars* a, KrylovScalars* ha, const KrylovScala
 
 Context::~Context() {
   if (pinned_sc) cudaFreeHost(pinned_sc);
+  if (capture_stream) cudaStreamDestroy(capture_stream);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -1593,42 +1644,9 @@ bool Method::build_fcg_graph() {
   for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
     if (level_matrix(k).comm != nullptr) return false;
   auto gl = std::make_unique<GraphLoop>();
-  cudaStream_t s = ctx_->stream;
-  if (cudaGraphCreate(&gl->g, 0) != cudaSuccess) return false;
-  cudaGraphConditionalHandle h;
-  if (cudaGraphConditionalHandleCreate(&h, gl->g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return false;
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  if (cudaGraphAddNode(&node, gl->g, nullptr, 0, &cp) != cudaSuccess) return false;
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
-    cudaGetLastError();
+  if (!capture_while_graph(ctx_, &work_[0]->sc.get()->done, [&] { fcg_iteration(0); }, &gl->g, &gl->exec,
+                           &gl->launches_per_iter))
     return false;
-  }
-  const uint64_t l0 = ctx_->launches;
-  bool ok = true;
-  try {
-    fcg_iteration(0);
-    launch_set_while(h, &work_[0]->sc.get()->done, s);
-  } catch (...) {
-    ok = false;
-  }
-  cudaGraph_t captured = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(s, &captured);
-  if (!ok || ec != cudaSuccess || cudaGetLastError() != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  gl->launches_per_iter = ctx_->launches - l0 + 1;
-  ctx_->launches = l0;
-  if (cudaGraphInstantiate(&gl->exec, gl->g, 0) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
   fcg_graph_ = std::move(gl);
   return true;
 }
@@ -2139,42 +2157,9 @@ bool Method::build_vcycle_graph() {
   for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
     if (level_matrix(k).comm != nullptr) return false;
   auto gl = std::make_unique<GraphLoop>();
-  cudaStream_t s = ctx_->stream;
-  if (cudaGraphCreate(&gl->g, 0) != cudaSuccess) return false;
-  cudaGraphConditionalHandle h;
-  if (cudaGraphConditionalHandleCreate(&h, gl->g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return false;
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  if (cudaGraphAddNode(&node, gl->g, nullptr, 0, &cp) != cudaSuccess) return false;
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
-    cudaGetLastError();
+  if (!capture_while_graph(ctx_, &work_[0]->sc.get()->done, [&] { pcg_vcycle_iteration(); }, &gl->g, &gl->exec,
+                           &gl->launches_per_iter))
     return false;
-  }
-  const uint64_t l0 = ctx_->launches;
-  bool ok = true;
-  try {
-    pcg_vcycle_iteration();
-    launch_set_while(h, &work_[0]->sc.get()->done, s);
-  } catch (...) {
-    ok = false;
-  }
-  cudaGraph_t captured = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(s, &captured);
-  if (!ok || ec != cudaSuccess || cudaGetLastError() != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  gl->launches_per_iter = ctx_->launches - l0 + 1;
-  ctx_->launches = l0;
-  if (cudaGraphInstantiate(&gl->exec, gl->g, 0) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
   vc_graph_ = std::move(gl);
   return true;
 }

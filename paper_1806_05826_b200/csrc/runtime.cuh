@@ -79,6 +79,9 @@ struct Context {
   bool own_stream = false;
   KrylovScalars* pinned_sc = nullptr;  // host mirror for per-iteration readback
   uint64_t launches = 0;               // kernels issued (diagnostics)
+  // graphs are captured on this private stream (the caller's stream may be the
+  // legacy default stream, which cannot capture) and launched on `stream`
+  cudaStream_t capture_stream = nullptr;
   explicit Context(int dev);
   ~Context();
   void sync();
