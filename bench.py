@@ -775,8 +775,12 @@ def run_cfg3(args, cfg):
         torch.cuda.synchronize()
         return rep, e0.elapsed_time(e1)
 
+    trace = (lambda *a: print("[trace]", *a, file=sys.stderr, flush=True)) if os.environ.get("RMG_BENCH_TRACE") else (
+        lambda *a: None)
+    trace("setup", setup_s)
     for i in range(args.warmup):
         go(i, False)
+        trace("warm", i)
     torch.cuda.synchronize()
     res = []
     with ClockSampler(local) as clocks:
@@ -792,6 +796,7 @@ def run_cfg3(args, cfg):
         bcm = torch.stack(bs, 0).contiguous()  # column-major n x nb block
         wcm = torch.empty(nb, x.n_features, dtype=torch.float64, device=dev)
         bms = []
+        trace("single done")
         for i in range(args.warmup + args.steps):
             beta = cfg["betas"][i % len(cfg["betas"])]
             if cur[0] != beta:
@@ -804,6 +809,7 @@ def run_cfg3(args, cfg):
             torch.cuda.synchronize()
             if i >= args.warmup:
                 bms.append(e0.elapsed_time(e1))
+            trace("batch", i)
         value = statistics.mean(bms) / nb
         batched = {"k": nb, "ms_per_batch": statistics.mean(bms), "ms_per_rhs": value,
                    "unbatched_ms_per_rhs": single_ms}
@@ -820,6 +826,7 @@ def run_cfg3(args, cfg):
             tt = time.perf_counter()
             R.ridgemg._lib.check(pm.lib.rmg_method_solve_batch(pm.h, hb.data_ptr(), hw.data_ptr(), nb, None, 0))
             be2e.append((time.perf_counter() - tt) * 1e3 / nb)
+            trace("e2e batch", i)
         batched["e2e_ms_per_rhs"] = statistics.mean(be2e)
     # e2e through the C ABI with host buffers (pinned b, w)
     pb = [torch.from_numpy(R.rng_normals(42 + k, x.n_samples)).pin_memory() for k in range(nb)]
@@ -853,6 +860,7 @@ def run_cfg3(args, cfg):
     # CPU baseline: the reference's own solver on this system within minutes -- its plain
     # cg (its multilevel FCG needs > 1000 outer iterations x ~400 inner level-1 solves here,
     # DESIGN.md §4.10), 3 iterations timed, x the GPU's CG iteration count for beta = 1
+    trace("operator timings done")
     cpu = None
     cb = ref_cg_beta(cfg)
     cg_iters = None

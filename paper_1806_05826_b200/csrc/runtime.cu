@@ -18,11 +18,20 @@ namespace rmg {
 
 namespace {
 // graph while-loops (pcg_vcycle, outer FCG): continue while the solver is not done
-__global__ void k_set_while(cudaGraphConditionalHandle h, const int32_t* done) {
-  cudaGraphSetConditional(h, *done ? 0u : 1u);
+// (a guard counter bounds every device-side loop at `limit` passes: if a done flag
+// were never raised the host loop takes over instead of the GPU spinning forever)
+__global__ void k_set_while(cudaGraphConditionalHandle h, const int32_t* done, unsigned long long* passes,
+                            unsigned long long limit) {
+  const unsigned long long c = ++*passes;
+  cudaGraphSetConditional(h, (*done || c >= limit) ? 0u : 1u);
 }
-void launch_set_while(cudaGraphConditionalHandle h, const int32_t* done, cudaStream_t s) {
-  k_set_while<<<1, 1, 0, s>>>(h, done);
+// batched solves: continue while any column runs
+__global__ void k_set_while_any(cudaGraphConditionalHandle h, const BlockScalars* sc, int k,
+                                unsigned long long* passes, unsigned long long limit) {
+  unsigned run = 0;
+  for (int c = 0; c < k; ++c) run |= sc[c].done ? 0u : 1u;
+  const unsigned long long c = ++*passes;
+  cudaGraphSetConditional(h, (run != 0u && c < limit) ? 1u : 0u);
 }
 }  // namespace
 
@@ -30,7 +39,8 @@ void launch_set_while(cudaGraphConditionalHandle h, const int32_t* done, cudaStr
 // context's private capture stream, with ctx->stream pointing at it meanwhile)
 // followed by the kernel that re-evaluates the condition from `done`.
 bool capture_while_graph(Context* ctx, const int32_t* done, const std::function<void()>& body, cudaGraph_t* g_out,
-                         cudaGraphExec_t* exec_out, uint64_t* launches_out) {
+                         cudaGraphExec_t* exec_out, uint64_t* launches_out, unsigned long long* passes,
+                         unsigned long long limit, const BlockScalars* block_sc = nullptr, int block_k = 0) {
   cudaGraph_t g = nullptr;
   if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
   auto fail = [&] {
@@ -60,7 +70,10 @@ bool capture_while_graph(Context* ctx, const int32_t* done, const std::function<
   bool ok = true;
   try {
     body();
-    launch_set_while(h, done, ctx->stream);
+    if (block_sc != nullptr)
+      k_set_while_any<<<1, 1, 0, ctx->stream>>>(h, block_sc, block_k, passes, limit);
+    else
+      k_set_while<<<1, 1, 0, ctx->stream>>>(h, done, passes, limit);
   } catch (...) {
     ok = false;
   }
@@ -1287,6 +1300,9 @@ void Method::set_beta(double beta) {
   RMG_CK(cudaSetDevice(ctx_->device));
   fcg_graph_.reset();  // the graphs point at the coarse buffers rebuilt below
   vc_graph_.reset();
+  bw_graph_.reset();
+  cg_graph_[0].reset();  // beta is a kernel argument of every captured apply
+  cg_graph_[1].reset();
   beta_ = beta;
   if (kind_ == RMG_METHOD_CG) return;
   if (kind_ == RMG_METHOD_JACOBI_CG) {
@@ -1644,8 +1660,9 @@ bool Method::build_fcg_graph() {
   for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
     if (level_matrix(k).comm != nullptr) return false;
   auto gl = std::make_unique<GraphLoop>();
+  gl->passes.alloc(1);
   if (!capture_while_graph(ctx_, &work_[0]->sc.get()->done, [&] { fcg_iteration(0); }, &gl->g, &gl->exec,
-                           &gl->launches_per_iter))
+                           &gl->launches_per_iter, gl->passes.get(), solver.max_iters + 2))
     return false;
   fcg_graph_ = std::move(gl);
   return true;
@@ -1670,6 +1687,7 @@ uint64_t Method::run_fcg(size_t k, const double* rhs, bool rec, SolveResult* out
   // without the host: the persistent dense solver or the direct coarsest solve
   const bool graphable = k == 0 && !profiling_ && (!nested || (dense_.size() > 1 && dense_[1] != nullptr));
   if (!hs.done && graphable && (fcg_graph_ || build_fcg_graph())) {
+    RMG_CK(cudaMemsetAsync(fcg_graph_->passes.get(), 0, sizeof(unsigned long long), s));
     RMG_CK(cudaGraphLaunch(fcg_graph_->exec, s));
     if (iw)
       ctx_->read2(w.sc.get(), &hs, iw->sc.get(), &ihs);
@@ -1837,17 +1855,44 @@ uint64_t Method::run_cg(size_t k, const double* rhs, const double* inv, bool rec
   ctx_->launches += 1;
   KrylovScalars hs = ctx_->read(w.sc.get());
   if (hs.status == 3) throw InvalidArgument("cg: non-finite rhs");
-  while (!hs.done) {
+  auto iteration = [&] {
+    cudaStream_t cs = ctx_->stream;  // the capture stream while a graph is recorded
     XtArgs a;
     a.v = p;
     a.out = ap;
     a.beta = level_beta(k);
     a.sc = w.sc.get();
+    a.done = &w.sc.get()->done;
     m.apply(p, Epi::Cg, a, prof(k));
-    launch_cg_axpy(w.x.get(), w.r.get(), w.z.get(), inv, p, ap, n, w.sc.get(), w.hist.get(), w.vw, s);
-    launch_cg_update_p(p, z, n, w.sc.get(), s);
+    launch_cg_axpy(w.x.get(), w.r.get(), w.z.get(), inv, p, ap, n, w.sc.get(), w.hist.get(), w.vw, cs);
+    launch_cg_update_p(p, z, n, w.sc.get(), cs);
     ctx_->launches += 2;
- hs = ctx_->read(w.sc.get());
+  };
+  // level 0 (cg, jacobi_cg): the loop as a CUDA graph (§4.13)
+  if (!hs.done && k == 0 && !profiling_ && std::getenv("RMG_NO_GRAPH") == nullptr && m.comm == nullptr) {
+    GraphLoop* gl = inv ? cg_graph_[1].get() : cg_graph_[0].get();
+    if (gl == nullptr) {
+      auto g = std::make_unique<GraphLoop>();
+      g->passes.alloc(1);
+      if (capture_while_graph(ctx_, &w.sc.get()->done, iteration, &g->g, &g->exec, &g->launches_per_iter,
+                              g->passes.get(), w.max_iters + 2)) {
+        gl = g.get();
+        cg_graph_[inv ? 1 : 0] = std::move(g);
+      }
+    }
+    if (gl != nullptr) {
+      RMG_CK(cudaMemsetAsync(gl->passes.get(), 0, sizeof(unsigned long long), s));
+      RMG_CK(cudaGraphLaunch(gl->exec, s));
+      hs = ctx_->read(w.sc.get());
+      ctx_->launches += gl->launches_per_iter * static_cast<uint64_t>(std::max(1, hs.it));
+      if (hs.status == 2)
+        throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
+                           "; operator is not positive definite");
+    }
+  }
+  while (!hs.done) {
+    iteration();
+    hs = ctx_->read(w.sc.get());
     if (profiling_) collect_profiles();
     if (hs.status == 2)
       throw RuntimeError("cg: <p, Ap> = " + std::to_string(hs.pap) + " at iteration " + std::to_string(hs.it) +
@@ -2079,6 +2124,38 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   launch_bpcg_begin(w.sc.get(), rr, rz, bad, k, w.hist.get(), s);
   RMG_CK(cudaMemcpyAsync(w.p.get(), w.z.get(), nk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const double beta0 = level_beta(0);
+  auto iteration = [&] {
+    cudaStream_t cs = ctx_->stream;  // the capture stream while a graph is recorded
+    m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);
+    launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, cs);
+    launch_bpcg_alpha(w.sc.get(), pap, k, cs);
+    launch_bupdate_xr(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, cs);
+    launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, cs);
+    launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), cs);
+    bvcycle(0, w.r.get(), w.z.get(), k);
+    launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
+    launch_bpcg_beta(w.sc.get(), rz, k, cs);
+    launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, cs);
+    ctx_->launches += 12;
+  };
+  // the lock-step loop as a CUDA graph (§4.13): runs while any column runs
+  if (std::getenv("RMG_NO_GRAPH") == nullptr) {
+    if (!bw_graph_ || bw_graph_k_ != k) {
+      bw_graph_.reset();
+      auto gl = std::make_unique<GraphLoop>();
+      gl->passes.alloc(1);
+      if (capture_while_graph(ctx_, nullptr, iteration, &gl->g, &gl->exec, &gl->launches_per_iter, gl->passes.get(),
+                              maxit + 2, w.sc.get(), k)) {
+        bw_graph_ = std::move(gl);
+        bw_graph_k_ = k;
+      }
+    }
+    if (bw_graph_) {
+      RMG_CK(cudaMemsetAsync(bw_graph_->passes.get(), 0, sizeof(unsigned long long), s));
+      RMG_CK(cudaGraphLaunch(bw_graph_->exec, s));
+      ctx_->launches += bw_graph_->launches_per_iter;
+    }
+  }
   for (;;) {
     RMG_CK(cudaMemcpyAsync(hs.data(), w.sc.get(), k * sizeof(BlockScalars), cudaMemcpyDeviceToHost, s));
     ctx_->sync();
@@ -2091,17 +2168,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
       all = all && hs[c].done;
     }
     if (all) break;
-    m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);
-    launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, s);
-    launch_bpcg_alpha(w.sc.get(), pap, k, s);
-    launch_bupdate_xr(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, s);
-    launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, s);
-    launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), s);
-    bvcycle(0, w.r.get(), w.z.get(), k);
-    launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, s);
-    launch_bpcg_beta(w.sc.get(), rz, k, s);
-    launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, s);
-    ctx_->launches += 12;
+    iteration();
   }
   const double wall = secs(t0);
   launch_brow2col(w.x.get(), w_cm, n, k, s);
@@ -2157,8 +2224,9 @@ bool Method::build_vcycle_graph() {
   for (size_t k = 0; k < coarse_.size(); ++k)  // NCCL collectives stay outside graphs here
     if (level_matrix(k).comm != nullptr) return false;
   auto gl = std::make_unique<GraphLoop>();
+  gl->passes.alloc(1);
   if (!capture_while_graph(ctx_, &work_[0]->sc.get()->done, [&] { pcg_vcycle_iteration(); }, &gl->g, &gl->exec,
-                           &gl->launches_per_iter))
+                           &gl->launches_per_iter, gl->passes.get(), solver.max_iters + 2))
     return false;
   vc_graph_ = std::move(gl);
   return true;
@@ -2186,6 +2254,7 @@ uint64_t Method::run_pcg_vcycle(const double* rhs, SolveResult* out) {
   }
   if (!hs.done && !profiling_ && (vc_graph_ || build_vcycle_graph())) {
     // the whole iteration loop on the device: one graph launch
+    RMG_CK(cudaMemsetAsync(vc_graph_->passes.get(), 0, sizeof(unsigned long long), s));
     RMG_CK(cudaGraphLaunch(vc_graph_->exec, s));
     hs = ctx_->read(w.sc.get());
     ctx_->launches += vc_graph_->launches_per_iter * static_cast<uint64_t>(std::max(1, hs.it));

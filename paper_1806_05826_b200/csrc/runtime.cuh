@@ -348,6 +348,7 @@ class Method {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t exec = nullptr;
     uint64_t launches_per_iter = 0;
+    DBuf<unsigned long long> passes;  // loop guard (reset before each launch)
     ~GraphLoop() {
       if (exec) cudaGraphExecDestroy(exec);
       if (g) cudaGraphDestroy(g);
@@ -355,6 +356,9 @@ class Method {
   };
   std::unique_ptr<GraphLoop> vc_graph_;
   std::unique_ptr<GraphLoop> fcg_graph_;  // the outer FCG loop when no inner level needs the host
+  std::unique_ptr<GraphLoop> cg_graph_[2];  // level-0 cg, jacobi_cg
+  std::unique_ptr<GraphLoop> bw_graph_;     // batched pcg_vcycle (k columns)
+  int bw_graph_k_ = 0;
   void fcg_iteration(size_t k);
   bool build_fcg_graph();
   void pcg_vcycle_iteration();
