@@ -346,6 +346,29 @@ __global__ void __launch_bounds__(kThreads) k_vperm_block(const double* __restri
   }
 }
 
+// Volatile loads keep their program order among themselves: a batch of them
+// issues back to back (nvcc otherwise interleaves each gather with its use).
+__device__ __forceinline__ int ldv_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldv_u16(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return (int)v;
+}
+__device__ __forceinline__ double ldv_f64_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldv_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // T[row][c0 + q] = sum over the row's elements of x * V[col][c0 + q].  A
 // half-warp per row, lane q owning column q: every gathered row of V is one
 // coalesced access (2 lines per warp instruction), and each lane sums its
@@ -371,21 +394,31 @@ __global__ void __launch_bounds__(kThreads) k_spmm_sell(const int32_t* __restric
       const int len = slen[sl * 32 + slot];
       const int lmax = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
       double acc = 0.0;
+      // lane q of the half-warp loads element j + q's index (and value) once;
+      // shuffles hand the 16 indices to every lane, whose 16 row gathers are
+      // then independent (the per-element broadcast loads compiled to one
+      // dependent index -> gather pair at a time)
+      const int qq = colq ? q : 0;
+      const int src0 = lane & 16;
       for (int j = 0; j < lmax; j += 16) {
+        const bool okq = j + q < len;
+        const int64_t eq = okq ? base + (int64_t)(j + q) * 32 + slot : base + slot;
+        const int ciq = okq ? (NARROW ? (int)ld_stream(idx16 + eq) : ld_stream(idx + eq)) : -1;
+        const double xq = PAT ? 1.0 : ld_stream(val + eq);
         int c[16];
         double x[16], vv[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          const bool ok = j + u < len;
-          const int64_t e = base + (int64_t)(j + u) * 32 + slot;
-          c[u] = ok ? (NARROW ? (int)idx16[e] : idx[e]) : -1;
-          x[u] = (ok && !PAT) ? val[e] : 1.0;
+          c[u] = __shfl_sync(0xffffffffu, ciq, src0 | u);
+          x[u] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xq, src0 | u);
         }
 #pragma unroll
-        for (int u = 0; u < 16; ++u) vv[u] = (c[u] >= 0 && colq) ? __ldg(V + (int64_t)c[u] * k + c0 + q) : 0.0;
+        for (int u = 0; u < 16; ++u) vv[u] = __ldg(V + (int64_t)(c[u] < 0 ? 0 : c[u]) * k + c0 + qq);
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (c[u] >= 0) acc += PAT ? vv[u] : x[u] * vv[u];
+        for (int u = 0; u < 16; ++u) {
+          const double add = acc + (PAT ? vv[u] : x[u] * vv[u]);
+          acc = c[u] >= 0 ? add : acc;
+        }
       }
       if (row >= 0 && colq) T[(int64_t)row * k + c0 + q] = acc;
     }
@@ -418,6 +451,8 @@ __global__ void __launch_bounds__(kThreads) k_xt_block(const int32_t* __restrict
     e1 = it.z;
     seg = it.w;
   }
+  // (the shuffle-broadcast batching of k_spmm_sell measured slower here: the two
+  // half-warps' Zipf-skewed row lengths would have to share one trip count)
   double acc = 0.0;
   for (int e = e0; e < e1; e += 8) {
     int smp[8];

@@ -30,8 +30,25 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_release(double* p, double v) {
+  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int NT>
-__global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, double* vec, double* out, int n) {
+__global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, double* vec, double* out, int n, unsigned* flags) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[33];
   const int tid = threadIdx.x, lane = tid & 31, nb = gridDim.x;
@@ -39,7 +56,69 @@ __global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, do
   double acc = 0.0;
   for (int it = 0; it < iters; ++it) {
     const int cur = it % 3, nxt = (it + 1) % 3;
-    if (mode == 0 || mode == 2) {
+    if (mode >= 4) {
+      // 4: sentinel, st.release publish (re-arm issued one exchange earlier), ld.acquire polls
+      // 5: sentinel, relaxed everything, no fences (ordering lower bound, not a valid protocol)
+      // 6: per-CTA flags: data, st.release flag; one warp polls 143 flags (ld.acquire), then loads
+      if (mode == 6) {
+        if (tid == 0) {
+          part[blockIdx.x] = it + blockIdx.x;
+          st_release_u32(flags + blockIdx.x, it + 1);
+        }
+        if (tid < 32) {
+          for (int b = lane; b < nb; b += 32)
+            while (ld_acquire_u32(flags + b) < (unsigned)(it + 1)) {
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {
+          double v = 0.0;
+          for (int b = lane; b < nb; b += 32) v += __ldcg(part + b);
+          v = wsum(v);
+          if (tid == 0) sh[0] = v;
+        }
+      } else {
+        double* P = part;
+        const int m = nb;
+        if (tid == 0) {
+          // re-arm own slot of the next buffer (read last two exchanges ago), ordered
+          // before this publish by its release
+          st_relaxed(P + (size_t)nxt * m + blockIdx.x, __longlong_as_double(kSentinel));
+          if (mode == 4) st_release(P + (size_t)cur * m + blockIdx.x, it + blockIdx.x);
+          else st_relaxed(P + (size_t)cur * m + blockIdx.x, it + blockIdx.x);
+        }
+        const double* src = P + (size_t)cur * m;
+        if (tid < 32) {
+          double x[5];
+          unsigned pending = 0;
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            x[u] = 0.0;
+            if (lane + 32 * u < nb) pending |= 1u << u;
+          }
+          while (pending) {
+#pragma unroll
+            for (int u = 0; u < 5; ++u)
+              if (pending & (1u << u)) {
+                const unsigned long long bits =
+                    mode == 4 ? ld_acquire64(src + lane + 32 * u) : ld_relaxed(src + lane + 32 * u);
+                if (bits != kSentinel) {
+                  x[u] = __longlong_as_double(bits);
+                  pending &= ~(1u << u);
+                }
+              }
+          }
+          double v = 0.0;
+#pragma unroll
+          for (int u = 0; u < 5; ++u) v += x[u];
+          v = wsum(v);
+          if (tid == 0) sh[0] = v;
+        }
+      }
+      __syncthreads();
+      acc += sh[0];
+      __syncthreads();
+    } else if (mode == 0 || mode == 2) {
       if (mode == 0) {
         if (tid == 0) part[blockIdx.x] = it + blockIdx.x;
       } else {
@@ -155,12 +234,15 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const char* names[] = {"grid.sync + 143 partials", "sentinel slots, 143 partials", "grid.sync + 2000-vector",
-                         "sentinel slots, 2000-vector"};
-  for (int mode = 0; mode < 4; ++mode) {
+                         "sentinel slots, 2000-vector", "sentinel, st.release/ld.acquire", "sentinel, no ordering",
+                         "per-CTA release flags"};
+  unsigned* flags;
+  cudaMalloc(&flags, 4096 * 4);
+  for (int mode = 0; mode < 7; ++mode) {
     for (int grid : {143, sms}) {
       int iters = 4000;
       int nn = n;
-      void* args[] = {&iters, &mode, &part, &vec, &out, &nn};
+      void* args[] = {&iters, &mode, &part, &vec, &out, &nn, &flags};
       for (int rep = 0; rep < 2; ++rep) {
         // all slots start armed (sentinel) for the sentinel modes
         unsigned long long s = kSentinel;
@@ -168,6 +250,7 @@ int main() {
         for (auto& x : h) x = s;
         cudaMemcpy(part, h, sizeof(h), cudaMemcpyHostToDevice);
         cudaMemcpy(vec, h, sizeof(h), cudaMemcpyHostToDevice);
+        cudaMemset(flags, 0, 4096 * 4);
         cudaEventRecord(a);
         cudaLaunchCooperativeKernel((void*)k<256>, dim3(grid), dim3(256), args, 0, 0);
         cudaEventRecord(b);
