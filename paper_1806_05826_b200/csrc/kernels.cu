@@ -375,7 +375,7 @@ __device__ __forceinline__ double ldv_f64(const double* p) {
 // column in the row's element order (the single-vector K1's order).  A warp
 // walks its SELL slice two rows at a time; element loads run 4 ahead.
 template <bool PAT, bool NARROW>
-__global__ void __launch_bounds__(kThreads) k_spmm_sell(const int32_t* __restrict__ off,
+__global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __restrict__ off,
                                                         const int32_t* __restrict__ srow,
                                                         const int32_t* __restrict__ slen,
                                                         const int32_t* __restrict__ idx,
