@@ -111,10 +111,41 @@ __global__ void __launch_bounds__(kT) k_col_chain(const void* x, int64_t ld, int
   if (tid < 32 && c0 + lane < cols) out[c0 + lane] = take_sqrt ? sqrt(acc) : acc;
 }
 
+// Few rows (a sketch: n <= 256): one thread per column walks the rows itself --
+// the same ordered chain, without the staging ring (whose 100 KB of shared memory
+// per CTA made every k-means++ step of a 500 k-column sketch 50+ waves).
+template <int OP, bool FP32>
+__global__ void __launch_bounds__(kT) k_small_chain(const void* x, int64_t ld, int64_t n, int64_t cols,
+                                                    const double* c, double* out, int take_sqrt) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (j >= cols) return;
+  double acc = 0.0;
+  for (int64_t r = 0; r < n; ++r) {
+    const double v = FP32 ? static_cast<double>(static_cast<const float*>(x)[r * ld + j])
+                          : static_cast<const double*>(x)[r * ld + j];
+    if (OP == 0) {
+      acc = __dadd_rn(acc, __dmul_rn(v, v));
+    } else {
+      const double d = __dsub_rn(v, c[r]);
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+  }
+  out[j] = take_sqrt ? sqrt(acc) : acc;
+}
+
 template <int OP>
 void col_chain(cudaStream_t s, const void* x, bool fp32, int64_t ld, int64_t n, int64_t cols, const double* c,
                double* out, bool take_sqrt) {
   if (cols <= 0) return;
+  if (n <= 256) {
+    const dim3 g(static_cast<unsigned>((cols + kT - 1) / kT));
+    if (fp32)
+      k_small_chain<OP, true><<<g, kT, 0, s>>>(x, ld, n, cols, c, out, take_sqrt ? 1 : 0);
+    else
+      k_small_chain<OP, false><<<g, kT, 0, s>>>(x, ld, n, cols, c, out, take_sqrt ? 1 : 0);
+    RMG_CK(cudaGetLastError());
+    return;
+  }
   const size_t smem = static_cast<size_t>(kCcStages) * kCcRows * 32 * (fp32 ? 4 : 8) +
                       static_cast<size_t>(kCcStages) * kCcRows * sizeof(double);
   const dim3 grid(static_cast<unsigned>((cols + 31) / 32));
