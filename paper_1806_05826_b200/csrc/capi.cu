@@ -222,7 +222,7 @@ int rmg_matrix_create_dense(rmg_context* ctx, uint64_t n, uint64_t f, const void
     need(ctx, "ctx");
     const auto lk_ = hold(&ctx->c);
     need(out, "out");
-    if (n * f) need(data, "data");
+    if (n != 0 && f != 0) need(data, "data");
     rmg::DenseInput din;
     din.data = data;
     din.fp32 = fp32 != 0;
@@ -242,7 +242,7 @@ int rmg_matrix_create_dense_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n
     const auto lk_ = hold(&ctx->c);
     need(comm, "comm");
     need(out, "out");
-    if (n * f) need(data, "data");
+    if (n != 0 && f != 0) need(data, "data");
     rmg::DenseInput din;
     din.data = data;
     din.fp32 = fp32 != 0;

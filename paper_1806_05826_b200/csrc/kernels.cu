@@ -684,7 +684,6 @@ __global__ void __launch_bounds__(kThreads) k_xt(const int32_t* __restrict__ ptr
   __shared__ int s_fin;
   const double* __restrict__ t = a.t;
   const int4 item = sch.items[blockIdx.x];
-  const int64_t F = sch.features;
   double d0 = 0.0, d1 = 0.0;
   if (item.z == -1 || item.z == -2) {
     const bool medium = item.z == -2;
