@@ -450,7 +450,11 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   std::iota(order.begin(), order.end(), 0);
   auto cnt = [&](int64_t f) { return ht.ptr[f + 1] - ht.ptr[f]; };
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt(a) > cnt(b); });
-  const int64_t cap = std::max<int64_t>(0, (96LL << 20) / (8 * nblk));
+  // [block x hot] partials budget (RMG_HOT_CAP_MB; default 256 MB: at cfg 5 full scale
+  // (1184 sample blocks) 96 MB capped the hot set at 10 k features, K2 3256 -> 3078 us)
+  const char* capmb = std::getenv("RMG_HOT_CAP_MB");
+  const int64_t cap_bytes = (capmb != nullptr ? std::max(1LL, std::atoll(capmb)) : 256LL) << 20;
+  const int64_t cap = std::max<int64_t>(0, cap_bytes / (8 * nblk));
   const char* hm = std::getenv("RMG_HOT_MIN");  // hot: >= this many nonzeros per block (mean)
   const int64_t min_per_block = hm != nullptr ? std::max(1, std::atoi(hm)) : 4;
   int64_t H = 0, hA = 0;

@@ -16,6 +16,8 @@ elif name == "cfg4shard":  # cfg4 per-GPU shard at 8 GPUs: 500k of its 4M rows, 
     dense = bench.cfg4_shard_matrix()
     import types
     x = types.SimpleNamespace(n_samples=dense.shape[0], n_features=dense.shape[1])
+elif name == "cfg5full":  # cfg5 on one GPU: all 16M rows
+    x = R.synth_sparse_zipf(16_000_000, 500_000, 64.0, 1.05, False, 0, row_streams=True)
 else:  # cfg5 per-GPU shard at 4 GPUs: 4M of its 16M rows
     x = R.synth_sparse_zipf(4_000_000, 500_000, 64.0, 1.05, False, 0, row_streams=True)
 t1 = time.time()
@@ -68,7 +70,7 @@ if name == "cfg4shard":
     got = m.spmv_transpose(u)
     want = dense.astype(np.float64).T @ u
     print("X^T u vs numpy: rel", np.linalg.norm(got - want) / np.linalg.norm(want))
-elif name not in ("cfg2", "cfg3"):
+elif name not in ("cfg2", "cfg3", "cfg5full"):
     print("hybrid hot features:", m.hybrid_hot_features(), flush=True)
     u = np.random.default_rng(1).standard_normal(x.n_samples)
     got = m.spmv_transpose(u)
