@@ -1553,6 +1553,27 @@ void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, cons
   check_launch("xt_hot");
 }
 
+// out[f] = sum over chunks c (in order) of part[c][f], for the listed (cold) features
+__global__ void __launch_bounds__(kThreads) k_chunk_combine(const double* __restrict__ part, int nchunks, int64_t F,
+                                                            const int32_t* __restrict__ list, int64_t nlist,
+                                                            double* __restrict__ out, const int32_t* done,
+                                                            const KrylovScalars* sc) {
+  if (done != nullptr && *done) return;
+  if (sc != nullptr && sc->done) return;
+  grid_stride(nlist, [&](int64_t q) {
+    const int64_t f = list[q];
+    double acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) acc += part[(int64_t)c * F + f];
+    out[f] = acc;
+  });
+}
+
+void launch_chunk_combine(const double* part, int nchunks, int64_t F, const int32_t* list, int64_t nlist, double* out,
+                          const int32_t* done, const KrylovScalars* sc, cudaStream_t s) {
+  k_chunk_combine<<<grid_for(nlist, 148 * 4), kThreads, 0, s>>>(part, nchunks, F, list, nlist, out, done, sc);
+  check_launch("chunk_combine");
+}
+
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a, cudaStream_t s) {
   if (sch.n_items == 0) return;
   if (xt.val == nullptr)

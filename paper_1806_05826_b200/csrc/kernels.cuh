@@ -157,6 +157,8 @@ void launch_spmv_rows_ring(const SparseDev& x, const double* v_ring, int ring_st
                            const KrylovScalars* sc, double* t, cudaStream_t s);
 void launch_xt(const SparseDev& xt, const XtSchedule& sch, Epi epi, const XtArgs& a,
                cudaStream_t s);
+void launch_chunk_combine(const double* part, int nchunks, int64_t F, const int32_t* list, int64_t nlist, double* out,
+                          const int32_t* done, const KrylovScalars* sc, cudaStream_t s);
 // dense X: out = epilogue(X^T (X v)) in one sweep (v may live in a ring: sc != nullptr)
 void launch_dense_ata(const DenseDev& d, const double* v, int ring_stride, const KrylovScalars* sc, Epi epi,
                       const XtArgs& a, cudaStream_t s);

@@ -539,6 +539,55 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   std::vector<char> skip(F, 0);
   for (int64_t h = 0; h < H; ++h) skip[feat[h]] = 1;
   hx->cold.build(ht, s, F, &skip);
+  // t (N doubles) beyond ~64 MB no longer stays in the L2 between the cold gathers:
+  // split the cold rows by sample chunk of 2 M (16 MB of t) -- RMG_XT_CHUNK=0/1 forces
+  {
+    const char* ce = std::getenv("RMG_XT_CHUNK");
+    const bool chunked = ce != nullptr ? std::string(ce) == "1" : n_samples > 8000000;
+    if (chunked) {
+      const int64_t S = std::getenv("RMG_XT_CHUNK_ROWS") ? std::atoll(std::getenv("RMG_XT_CHUNK_ROWS")) : 2000000;
+      const int64_t C = (n_samples + S - 1) / S;
+      std::vector<int32_t> cold;
+      for (int64_t f = 0; f < F; ++f)
+        if (!skip[f] && ht.ptr[f + 1] > ht.ptr[f]) cold.push_back(static_cast<int32_t>(f));
+      hx->n_cold = static_cast<int64_t>(cold.size());
+      hx->cold_list.upload(cold.data(), cold.size(), s);
+      hx->chunk_part.alloc(static_cast<size_t>(C) * std::max<int64_t>(1, F));
+      RMG_CK(cudaMemsetAsync(hx->chunk_part.get(), 0, hx->chunk_part.size() * sizeof(double), s));
+      hx->chunk_x.resize(C);
+      hx->chunk_sched.resize(C);
+      for (int64_t c = 0; c < C; ++c) {
+        HostCsr cc;  // rows = features (cold only), samples of chunk c, increasing
+        cc.n = F;
+        cc.f = ht.f;
+        cc.ptr.assign(F + 1, 0);
+        for (int64_t f = 0; f < F; ++f) {
+          int64_t cnt = 0;
+          if (!skip[f]) {
+            const int64_t* b = ht.idx.data() + ht.ptr[f];
+            const int64_t* e = ht.idx.data() + ht.ptr[f + 1];
+            cnt = std::lower_bound(b, e, (c + 1) * S) - std::lower_bound(b, e, c * S);
+          }
+          cc.ptr[f + 1] = cc.ptr[f] + cnt;
+        }
+        cc.idx.resize(cc.ptr[F]);
+        if (!pattern) cc.val.resize(cc.ptr[F]);
+        for (int64_t f = 0; f < F; ++f) {
+          if (skip[f]) continue;
+          const int64_t* b = ht.idx.data() + ht.ptr[f];
+          const int64_t* e = ht.idx.data() + ht.ptr[f + 1];
+          const int64_t k0 = std::lower_bound(b, e, c * S) - ht.idx.data();
+          const int64_t k1 = std::lower_bound(b, e, (c + 1) * S) - ht.idx.data();
+          std::copy(ht.idx.begin() + k0, ht.idx.begin() + k1, cc.idx.begin() + cc.ptr[f]);
+          if (!pattern) std::copy(ht.val.begin() + k0, ht.val.begin() + k1, cc.val.begin() + cc.ptr[f]);
+        }
+        hx->chunk_x[c].upload(cc, pattern, s, false);
+        std::vector<char> empty(F, 0);
+        for (int64_t f = 0; f < F; ++f) empty[f] = cc.ptr[f + 1] == cc.ptr[f] ? 1 : 0;
+        hx->chunk_sched[c].build(cc, s, F, &empty);
+      }
+    }
+  }
   // RMG_XT_COLD_NA=1: the cold features' t gathers bypass L1 (measured slower on the
   // cfg 5 shard, 586 vs 555 us: the L1 still catches some reuse)
   hx->cold.view.stream_t = std::getenv("RMG_XT_COLD_NA") != nullptr ? 1 : 0;
@@ -803,7 +852,19 @@ void xt_pass(Matrix& m, const double* t, Epi epi, const XtArgs& args) {
       RMG_CK(cudaStreamWaitEvent(h.side, h.fork, 0));
       cs = h.side;
     }
-    launch_xt(m.xt.view, h.cold.view, Epi::Plain, pa, cs);
+    if (h.chunk_x.empty()) {
+      launch_xt(m.xt.view, h.cold.view, Epi::Plain, pa, cs);
+    } else {  // sample-chunked cold pass: partials per chunk, combined in chunk order
+      const int64_t F = m.f();
+      for (size_t c = 0; c < h.chunk_x.size(); ++c) {
+        XtArgs ca = pa;
+        ca.out = h.chunk_part.get() + c * F;
+        launch_xt(h.chunk_x[c].view, h.chunk_sched[c].view, Epi::Plain, ca, cs);
+      }
+      const KrylovScalars* csc = (epi == Epi::Fcg || epi == Epi::Cg) ? a.sc : nullptr;
+      launch_chunk_combine(h.chunk_part.get(), static_cast<int>(h.chunk_x.size()), F, h.cold_list.get(), h.n_cold,
+                           m.part.get(), a.done, csc, cs);
+    }
     const KrylovScalars* sc = (epi == Epi::Fcg || epi == Epi::Cg) ? a.sc : nullptr;
     launch_xt_hot(h.view, t, a.done, sc, m.part.get(), m.ctx->stream);
     if (!serial) {  // join before the epilogue reads both parts

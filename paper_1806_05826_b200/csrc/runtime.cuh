@@ -154,6 +154,13 @@ struct HotXt {
   DBuf<uint16_t> idx16;
   DBuf<double> val, partial, red2;
   DeviceSchedule cold;  // segmented schedule over the cold rows only
+  // when t outgrows the L2 (N > 8 M): the cold rows split by sample chunk, one
+  // pass per chunk over its L2-resident t slice, partials combined in chunk order
+  std::vector<DeviceSparse> chunk_x;
+  std::vector<DeviceSchedule> chunk_sched;
+  DBuf<double> chunk_part;  // [chunks][F]
+  DBuf<int32_t> cold_list;  // the cold features (combine targets)
+  int64_t n_cold = 0;
   // the cold pass runs on a side stream, concurrently with the hot pass
   // (RMG_XT_SERIAL=1: one stream)
   cudaStream_t side = nullptr;

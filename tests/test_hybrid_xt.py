@@ -17,11 +17,17 @@ from helpers import rel_diff, to_checker
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def hybrid(monkeypatch):
+@pytest.fixture(params=["unchunked", "chunked"])
+def hybrid(monkeypatch, request):
+    """Both cold-pass layouts: one segmented pass, and the sample-chunked passes
+    (the default above 8 M samples) forced with chunks of 3000 samples."""
     monkeypatch.setenv("RMG_XT_HOT", "1")
+    if request.param == "chunked":
+        monkeypatch.setenv("RMG_XT_CHUNK", "1")
+        monkeypatch.setenv("RMG_XT_CHUNK_ROWS", "3000")
     yield
-    monkeypatch.delenv("RMG_XT_HOT", raising=False)
+    for k in ("RMG_XT_HOT", "RMG_XT_CHUNK", "RMG_XT_CHUNK_ROWS"):
+        monkeypatch.delenv(k, raising=False)
 
 
 def zipf(n, f, mean, s, values, seed):
