@@ -57,6 +57,91 @@ __global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, un
         __threadfence();
       }
       __syncthreads();
+    } else if (mode == 9 || mode == 10) {
+      // 9: one 128 B line per CTA's partial; 10: partials written with st.global (L1
+      // write-through) but read after the barrier with ld.acquire.gpu
+      const int stride = mode == 9 ? 16 : 1;
+      if (threadIdx.x == 0) part[(size_t)blockIdx.x * stride] = it + blockIdx.x;
+      grid.sync();
+      double v = 0.0;
+      if (threadIdx.x < gridDim.x) {
+        if (mode == 9) {
+          v = __ldcg(part + (size_t)threadIdx.x * stride);
+        } else {
+          asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(part + threadIdx.x) : "memory");
+        }
+      }
+      v = wsum(v);
+      if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double r = threadIdx.x < (NT / 32) ? sh[threadIdx.x] : 0.0;
+        r = wsum(r);
+        if (threadIdx.x == 0) sh[32] = r;
+      }
+      __syncthreads();
+      acc += sh[32];
+    } else if (mode == 12 || mode == 13) {
+      // 12: the monotonic-counter barrier (tight spin, no backoff) + the constant block
+      // reduction of mode 11; 13: the same with every warp's lane 0 polling (no
+      // __syncthreads release inside the CTA)
+      __syncthreads();
+      const unsigned target = (unsigned)(it + 1) * gridDim.x;
+      if (threadIdx.x == 0) red_release_add(bar + 2, 1u);
+      if (mode == 12) {
+        if (threadIdx.x == 0)
+          while (ld_acquire(bar + 2) < target) {
+          }
+        __syncthreads();
+      } else {
+        if ((threadIdx.x & 31) == 0)
+          while (ld_acquire(bar + 2) < target) {
+          }
+        __syncwarp();
+      }
+      double v = threadIdx.x < gridDim.x ? (double)threadIdx.x : 0.0;
+      v = wsum(v);
+      if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double r = threadIdx.x < (NT / 32) ? sh[threadIdx.x] : 0.0;
+        r = wsum(r);
+        if (threadIdx.x == 0) sh[32] = r;
+      }
+      __syncthreads();
+      acc += sh[32];
+    } else if (mode == 11) {
+      // grid.sync + block reduction of a constant (no global load): the reduction's own cost
+      grid.sync();
+      double v = threadIdx.x < gridDim.x ? (double)threadIdx.x : 0.0;
+      v = wsum(v);
+      if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double r = threadIdx.x < (NT / 32) ? sh[threadIdx.x] : 0.0;
+        r = wsum(r);
+        if (threadIdx.x == 0) sh[32] = r;
+      }
+      __syncthreads();
+      acc += sh[32];
+    } else if (mode >= 4) {
+      // mode 4 + log2(R): grid.sync + one all-block reduction read from R replicas of
+      // the partials (CTA b reads replica b % R): fewer readers per L2 line
+      const int R = 1 << (mode - 4);
+      if (threadIdx.x < R) part[(size_t)threadIdx.x * 512 + blockIdx.x] = it + blockIdx.x;
+      grid.sync();
+      const double* src = part + (size_t)(blockIdx.x % R) * 512;
+      double v = threadIdx.x < gridDim.x ? __ldcg(src + threadIdx.x) : 0.0;
+      v = wsum(v);
+      if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double r = threadIdx.x < (NT / 32) ? sh[threadIdx.x] : 0.0;
+        r = wsum(r);
+        if (threadIdx.x == 0) sh[32] = r;
+      }
+      __syncthreads();
+      acc += sh[32];
     } else {
       if (threadIdx.x == 0) part[blockIdx.x] = it + blockIdx.x;
       grid.sync();
@@ -81,7 +166,7 @@ __global__ void __launch_bounds__(NT, 1) k(int iters, int mode, double* part, un
 int main() {
   double *part, *out;
   unsigned* bar;
-  cudaMalloc(&part, 4096 * 8);
+  cudaMalloc(&part, 16 * 512 * 8);
   cudaMalloc(&out, 8);
   cudaMalloc(&bar, 16);
   cudaMemset(bar, 0, 16);
@@ -90,7 +175,7 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 14; ++mode) {
     for (int grid : {sms, 143, 74}) {
       int iters = 2000;
       void* args[] = {&iters, &mode, &part, &bar, &out};
