@@ -1585,7 +1585,8 @@ void Method::tune_dense_partials(size_t k) {
   DenseInner& d = *dense_[k];
   cudaStream_t s = ctx_->stream;
   const int64_t n = level_matrix(k).f();
-  constexpr int kCand = 8;
+  const char* tn = std::getenv("RMG_DENSE_TUNE_N");  // candidate buffers (default 8)
+  const int kCand = tn != nullptr ? std::max(1, std::min(64, std::atoi(tn))) : 8;
   const size_t count = d.partials.size();
   std::vector<DBuf<double>> cand;
   cand.push_back(std::move(d.partials));
