@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __rest
 // elements in order.  Units: the rows with <= 4096 nonzeros (whole rows), then
 // the items of longer rows (segment partials for k_block_finish).
 template <bool PAT>
-__global__ void __launch_bounds__(kThreads) k_xt_block(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(kThreads, 5) k_xt_block(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                        const double* __restrict__ val, BlockXtSchedule bs,
                                                        const double* __restrict__ T, const double* __restrict__ V,
                                                        double* __restrict__ out, double beta, int k, int c0, int kc) {
