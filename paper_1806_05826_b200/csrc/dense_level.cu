@@ -268,6 +268,45 @@ __device__ __forceinline__ void gemv_rows_rs(const double* rows, int nr, int n, 
   __syncthreads();
 }
 
+// gemv_rows_rs with column pairs (n even): thread tid owns columns 2 tid + 2 kT p
+// and the next one, read as one 16-byte load (half the load instructions); the
+// pairs' products are added in column order.
+template <bool GLOBAL, int NP>
+__device__ __forceinline__ void gemv_rows_rs2(const double* rows, int nr, int n, const double (&vc)[2 * NP],
+                                              double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, tid = threadIdx.x;
+  for (int lr0 = 0; lr0 < nr; lr0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int c = 2 * tid + p * 2 * kT;
+      if (c < n) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double* row = rows + (size_t)min(lr0 + u, nr - 1) * n;
+          const double2 x = GLOBAL ? __ldg(reinterpret_cast<const double2*>(row + c))
+                                   : *reinterpret_cast<const double2*>(row + c);
+          acc[u] += x.x * vc[2 * p];
+          acc[u] += x.y * vc[2 * p + 1];
+        }
+      }
+    }
+    const double sr = warp_rows_sum<16>(acc);
+    const int lr = lr0 + (lane >> 1);
+    if ((lane & 1) == 0 && lr < nr) red[lr * kW + wid] = sr;
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) s += red[tid * kW + w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
+
 // gemv_narrow with the reduce-scatter (nr <= RM: 16 or 28).
 template <int RM>
 __device__ __forceinline__ void gemv_narrow_rs(const double (&q)[RM], int nr, double sv, double* red, double* out) {
@@ -585,7 +624,7 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
 // (n <= NQ * kT) and RM >= owned rows: compile-time so the unrolled loop body
 // stays small enough for the instruction cache (measured: no_inst stalls at
 // NQ = 16 on n = 2000).
-template <bool SMEM, int HM, int NQ>
+template <bool SMEM, int HM, int NQ, bool PAIR = false>
 __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
   constexpr int RM = NQ <= 8 ? 16 : 28;
   cg::grid_group grid = cg::this_grid();
@@ -764,10 +803,20 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     tmark(a, it, 4);
     // ======== phase 2: convergence of r_it; direction it
     double pc[NQ];
+    if constexpr (PAIR) {  // columns 2 tid + 2 kT p and the next (gemv_rows_rs2)
 #pragma unroll
-    for (int qq = 0; qq < NQ; ++qq) {
-      const int c = tid + qq * kT;
-      pc[qq] = c < n ? __ldcg(a.zfull + c) : 0.0;
+      for (int p2 = 0; p2 < NQ / 2; ++p2) {
+        const int c = 2 * tid + p2 * 2 * kT;
+        const double2 zz = c < n ? __ldcg(reinterpret_cast<const double2*>(a.zfull + c)) : make_double2(0.0, 0.0);
+        pc[2 * p2] = zz.x;
+        pc[2 * p2 + 1] = zz.y;
+      }
+    } else {
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        const int c = tid + qq * kT;
+        pc[qq] = c < n ? __ldcg(a.zfull + c) : 0.0;
+      }
     }
     double den = 1.0;
     if (tid < use) den = __ldcg(a.pap_ring + (it - use + tid) % RING);
@@ -806,7 +855,10 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov2(DenseKrylovArgs a) {
     }
     if (tid < use) coef[tid] = gsum[1 + tid] / den;
     // A z for the owned rows (ends with __syncthreads: coef and vv visible)
-    gemv_rows_rs<!SMEM, NQ>(Arows, nr, n, pc, red, vv);
+    if constexpr (PAIR)
+      gemv_rows_rs2<!SMEM, NQ / 2>(Arows, nr, n, pc, red, vv);
+    else
+      gemv_rows_rs<!SMEM, NQ>(Arows, nr, n, pc, red, vv);
     tmark(a, it, 6);
     if (wid < 2) {  // warp 0: p = z - c_0 p_0 - c_1 p_1 - ... (reference order); warp 1: Ap alike
       double v = wid == 0 ? zi : (lane < nr ? vv[lane] : 0.0);
@@ -895,7 +947,11 @@ void launch_dense_krylov(const DenseKrylovPlan& plan, const DenseKrylovArgs& arg
   if (dense_two_barrier(args)) {
     const bool small = args.n <= 8 * kT && plan.rows_per_cta <= 16;
     const bool h20 = args.keep <= 20;
-    if (small)
+    static const bool no_pair = std::getenv("RMG_DENSE_NO_PAIR") != nullptr;
+    const bool pair = !no_pair && args.n % 2 == 0 && plan.smem_a && h20;
+    if (pair)
+      fn = small ? (void*)k_dense_krylov2<true, 20, 8, true> : (void*)k_dense_krylov2<true, 20, kMaxQ, true>;
+    else if (small)
       fn = h20 ? (plan.smem_a ? (void*)k_dense_krylov2<true, 20, 8> : (void*)k_dense_krylov2<false, 20, 8>)
                : (plan.smem_a ? (void*)k_dense_krylov2<true, kMaxUse - 1, 8> : (void*)k_dense_krylov2<false, kMaxUse - 1, 8>);
     else
