@@ -131,7 +131,7 @@ class Checker:
             build(kind)
         self.kind = kind
         self.lib = C.CDLL(path)
-        for name in ("matrix_from_csr", "coarsen") + (("read_matrix_market", "matrix_from_triplets") if kind == "ref" else ()):
+        for name in ("matrix_from_csr", "coarsen", "synth_sparse_zipf", "synth_dense_clustered") + (("read_matrix_market", "matrix_from_triplets") if kind == "ref" else ()):
             getattr(self.lib, self.prefix + name).restype = C.c_void_p
         self.lib[self.prefix + "last_error"].restype = C.c_char_p
 
@@ -154,6 +154,19 @@ class Checker:
         ci = np.ascontiguousarray(column_indices, np.uint64)
         v = None if values is None else np.ascontiguousarray(values, np.float64)
         h = self._fn("matrix_from_csr")(C.c_uint64(n), C.c_uint64(f), C.c_uint64(len(ci)), _p(rp), _p(ci), _p(v))
+        return Matrix(self, h)
+
+    def synth_sparse_zipf(self, n, f, mean_nnz, zipf_s, abs_normal_values, seed, row_streams=False) -> Matrix:
+        """BASELINE cfg 2/3/5 generator (oracle/synth.hpp) on this checker's CounterRng."""
+        h = self._fn("synth_sparse_zipf")(C.c_uint64(n), C.c_uint64(f), C.c_double(mean_nnz), C.c_double(zipf_s),
+                                          C.c_int32(int(abs_normal_values)), C.c_uint64(seed),
+                                          C.c_int32(int(row_streams)))
+        return Matrix(self, h)
+
+    def synth_dense_clustered(self, n, f, groups, noise, seed) -> Matrix:
+        """BASELINE cfg 1 generator (oracle/synth.hpp)."""
+        h = self._fn("synth_dense_clustered")(C.c_uint64(n), C.c_uint64(f), C.c_uint64(groups), C.c_double(noise),
+                                              C.c_uint64(seed))
         return Matrix(self, h)
 
     def read_matrix_market(self, path: str) -> Matrix:

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "oracle_abi.h"
+#include "synth.hpp"
 #include "ridgemg/krylov.hpp"
 #include "ridgemg/matrix_market.hpp"
 #include "ridgemg/rng.hpp"
@@ -227,6 +228,32 @@ void* ref_read_matrix_market(const char* path) {
   FeatureMatrix* out = nullptr;
   const int rc = guard([&] { out = new FeatureMatrix(read_matrix_market(std::filesystem::path(path))); });
   return rc == 0 ? out : nullptr;
+}
+
+// BASELINE synthetic inputs (oracle/synth.hpp) drawn from the reference's own
+// CounterRng (rng.hpp:25-72): the reference arm builds its X without the
+// product library.  The CSR is filled directly (csr_from_triplets would need
+// ~3x the memory at cfg 3 / cfg 5 scale).
+void* ref_synth_sparse_zipf(uint64_t n, uint64_t f, double mean, double s, int32_t values, uint64_t seed,
+                            int32_t row_streams) {
+  auto g = oracle_synth::sparse_zipf<CounterRng>(static_cast<int64_t>(n), static_cast<int64_t>(f), mean, s,
+                                                 values != 0, seed, row_streams != 0);
+  auto* m = new FeatureMatrix;
+  m->n_samples = n;
+  m->n_features = f;
+  m->row_offsets = std::move(g.ptr);
+  m->column_indices.assign(g.idx.begin(), g.idx.end());
+  std::vector<uint64_t>().swap(g.idx);
+  if (values)
+    m->values = std::move(g.val);
+  else
+    m->values.assign(m->column_indices.size(), 1.0);
+  return m;
+}
+void* ref_synth_dense_clustered(uint64_t n, uint64_t f, uint64_t groups, double noise, uint64_t seed) {
+  auto g = oracle_synth::dense_clustered<CounterRng>(static_cast<int64_t>(n), static_cast<int64_t>(f),
+                                                     static_cast<int64_t>(groups), noise, seed);
+  return ref_matrix_from_csr(n, f, g.idx.size(), g.ptr.data(), g.idx.data(), g.val.data());
 }
 
 void ref_matrix_free(void* h) { delete M(h); }

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "oracle_abi.h"
+#include "synth.hpp"
 
 namespace {
 
@@ -66,6 +67,10 @@ struct Rng {
     const auto v = static_cast<uint64_t>(unit() * static_cast<double>(n));
     return v >= n ? n - 1 : v;
   }
+  // the reference's method names (rng.hpp:36-69), for oracle/synth.hpp
+  double next_double() { return unit(); }
+  double next_normal() { return normal(); }
+  uint64_t next_index(uint64_t n) { return index(n); }
 };
 
 // ---------------------------------------------------------------- CSR
@@ -1004,6 +1009,18 @@ void* orc_matrix_from_csr(uint64_t n, uint64_t f, uint64_t nnz, const uint64_t* 
   else
     m->val.assign(nnz, 1.0);
   return m;
+}
+// BASELINE synthetic inputs (oracle/synth.hpp) as a checker matrix
+void* orc_synth_sparse_zipf(uint64_t n, uint64_t f, double mean, double s, int32_t values, uint64_t seed,
+                            int32_t row_streams) {
+  auto g = oracle_synth::sparse_zipf<Rng>(static_cast<int64_t>(n), static_cast<int64_t>(f), mean, s, values != 0,
+                                          seed, row_streams != 0);
+  return orc_matrix_from_csr(n, f, g.idx.size(), g.ptr.data(), g.idx.data(), values ? g.val.data() : nullptr);
+}
+void* orc_synth_dense_clustered(uint64_t n, uint64_t f, uint64_t groups, double noise, uint64_t seed) {
+  auto g = oracle_synth::dense_clustered<Rng>(static_cast<int64_t>(n), static_cast<int64_t>(f),
+                                              static_cast<int64_t>(groups), noise, seed);
+  return orc_matrix_from_csr(n, f, g.idx.size(), g.ptr.data(), g.idx.data(), g.val.data());
 }
 void orc_matrix_free(void* h) { delete H(h); }
 int orc_matrix_shape(void* h, uint64_t* n, uint64_t* f, uint64_t* nnz) {

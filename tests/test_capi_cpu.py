@@ -122,3 +122,25 @@ def test_null_arguments_are_invalid():
     assert lib.rmg_rng_normals(1, 5, None) == _lib.RMG_ERR_INVALID_ARGUMENT
     major, minor = C.c_int32(), C.c_int32()
     assert lib.rmg_version(C.byref(major), C.byref(minor)) == 0
+
+
+def _msha(m):
+    rp, ci, v = m.export()
+    h = hashlib.sha256()
+    h.update(rp.tobytes())
+    h.update(ci.tobytes())
+    h.update(v.tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("kind", ["oracle", "ref"])
+def test_checker_generators_match_product(kind, request):
+    """The reference arm builds its inputs with the checkers' own generator
+    (oracle/synth.hpp on the reference's CounterRng): same bytes as the product's."""
+    chk = request.getfixturevalue("orc" if kind == "oracle" else "ref")
+    assert _msha(chk.synth_dense_clustered(2000, 500, 50, 0.1, 0)) == str(load_golden("cfg1")["sha256"])
+    assert _msha(chk.synth_sparse_zipf(10000, 2000, 40.0, 1.1, False, 0)) == str(load_golden("cfg2_small")["sha256"])
+    for args in ((3000, 700, 25.0, 1.05, True, 3), (2000, 50, 60.0, 1.1, False, 9)):
+        for rows in (False, True):
+            assert _msha(chk.synth_sparse_zipf(*args, row_streams=rows)) == _sha(
+                R.synth_sparse_zipf(*args, row_streams=rows)), (args, rows)
