@@ -1,19 +1,23 @@
 #!/usr/bin/env python
 """Benchmark of the ridgemg_b200 solve path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
 
-One step = one preconditioned Krylov solve of (X^T X + beta I) w = X^T b to
-relative residual 1e-6 for a fresh right-hand side b (seeded N(0,1)), with X,
-the hierarchy and b already resident in HBM; the step runs from b on the
-device to w on the device (rhs = X^T b formation included).  Default workload
-is BASELINE configs[1] (cfg2).  L2 is flushed (256 MiB write) before every
-timed step, outside the step's event pair.  Multi-GPU (torchrun): independent
-replicas, one per rank, max-over-ranks device time.
+Default workload: BASELINE configs[2] = cfg 3, the largest single-GPU config: a
+regularisation sweep (5 betas) over one fixed 4-level hierarchy with 16
+right-hand sides solved as a batched block operator.  One step = one beta's
+batch of 16 solves to relative residual 1e-6, X, the hierarchy and B already
+resident in HBM (rhs = X^T b formation included); value = device ms per
+right-hand side.  `e2e` = the same batched call from pinned host buffers.
+Multi-GPU (torchrun): the (beta, batch) units are dealt round-robin to the
+ranks, max-over-ranks device time.  `--config cfg2 | cfg4 | cfg1 | cfg5` run the
+other BASELINE configs (cfg 2: the reference's own multilevel FCG, bit-exact
+labels; `--shard`: the row-sharded operator over NCCL).
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
-CPU implementation (oracle/_ref, the unmodified reference sources) on the
-same config with all host threads, on bounded samples.
+CPU implementation (oracle/_ref: the unmodified reference sources) with all
+host threads on the same config, its input built by the reference's own
+CounterRng (oracle/synth.hpp; SHA-256 in `config`), never by this repo's library.
 """
 from __future__ import annotations
 
@@ -48,20 +52,21 @@ CONFIGS = {
         method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg4_none", ref_rows=50_000),
     "cfg3": dict(
         workload="cfg3: sparse CSR N=1,000,000 x F=100,000, nnz/row max(1,Poisson(50)), Zipf(1.1) columns, "
-                 "values |N(0,1)| fp64; 4-level hierarchy 10000/1000/100 by sketched k-means (d=32, unit-normalised "
-                 "columns; the reference's k-means is infeasible here, DESIGN.md §4.10) fixed across a beta sweep "
-                 "{1e-3,1e-2,1e-1,1,10} x 16 right-hand sides; solver pcg_vcycle (PCG + symmetric Jacobi-smoothed "
-                 "V-cycle, DESIGN.md §4.11) to rel. residual 1e-6",
+                 "values |N(0,1)| fp64 (generator oracle/synth.hpp = the product's, one CounterRng stream per row, "
+                 "seed 0); regularisation sweep beta in {1e-3,1e-2,1e-1,1,10} over one fixed 4-level hierarchy "
+                 "10000/1000/100 (sketched k-means on unit-normalised columns, DESIGN.md §4.10); 16 right-hand "
+                 "sides b_k = normals(42+k) solved as one batched block operator per beta; rel. residual 1e-6",
         kind="zipf", n=1_000_000, f=100_000, mean=50.0, zipf=1.1, abs_values=True, seed=0, beta=1.0,
         ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
-        golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32),
+        golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32, ref_method="jacobi_cg",
+        ref_fixture="cfg3_ref.json"),
     "cfg5": dict(
         workload="cfg5: binary CSR N=16,000,000 x F=500,000 (1.02e9 nonzeros), nnz/row max(1,Poisson(64)), Zipf(1.05) "
                  "columns, on ONE GPU; 4-level hierarchy 50000/5000/500 by sketched k-means (d=32, unit-normalised "
                  "columns, DESIGN.md §4.10); beta=0.5; solver pcg_vcycle (DESIGN.md §4.11) to rel. residual 1e-6",
         kind="zipf", n=16_000_000, f=500_000, mean=64.0, zipf=1.05, abs_values=False, seed=0, beta=0.5,
         ks=[50_000, 5_000, 500], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
-        golden="cfg5_none", betas=[0.5], n_rhs=1, sketch=32),
+        golden="cfg5_none", betas=[0.5], n_rhs=1, sketch=32, ref_method="jacobi_cg"),
     "cfg1": dict(
         workload="cfg1: dense clustered N=2000 x F=500 fp64 (row-major dense path); 2-level k-means 50; beta=1e-2; "
                  "FCG(m=20) to rel. residual 1e-6",
@@ -106,6 +111,33 @@ def make_matrix(cfg):
     if cfg["kind"] == "zipf":
         return R.synth_sparse_zipf(cfg["n"], cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"])
     return R.synth_dense_clustered(cfg["n"], cfg["f"], cfg["groups"], cfg["noise"], cfg["seed"])
+
+
+class CheckerCsr:
+    """A CSR exported from a CPU checker (FeatureMatrix-like: the reference arm's input)."""
+
+    def __init__(self, n, f, rp, ci, v):
+        self.n_samples, self.n_features = n, f
+        self.row_offsets, self.column_indices, self.values = rp, ci, v
+
+    def value_array(self):
+        return self.values
+
+
+def make_reference_matrix(cfg):
+    """The reference arm's input, built by the checker's own generator (oracle/synth.hpp on
+    the reference's CounterRng) -- never by the product library."""
+    if cfg["kind"] == "lowrank":
+        return DenseX(cfg4_shard_matrix(n=cfg["n"], f=cfg["f"], seed=cfg["seed"]))
+    import oracle
+    chk = oracle.Checker("ref" if oracle.available("ref") else "oracle")
+    if cfg["kind"] == "zipf":
+        m = chk.synth_sparse_zipf(cfg["n"], cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"],
+                                  row_streams=bool(cfg.get("sketch")))
+    else:
+        m = chk.synth_dense_clustered(cfg["n"], cfg["f"], cfg["groups"], cfg["noise"], cfg["seed"])
+    rp, ci, v = m.export()
+    return CheckerCsr(cfg["n"], cfg["f"], rp, ci, v)
 
 
 def level_specs(cfg, labels=None):
@@ -236,56 +268,89 @@ def lowrank_sample_labels(cfg):
     return labels
 
 
-def ref_cg_beta(cfg):
-    return 1.0 if 1.0 in cfg["betas"] else cfg["betas"][0]
+def csr_sha(rp, ci, v):
+    """SHA-256 of a CSR as the checkers export it (uint64 offsets / indices, fp64 values)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(rp, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(ci, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(v, np.float64).tobytes())
+    return h.hexdigest()
 
 
-def run_reference_cfg3(args, cfg):
-    """cfg 3's reference arm: the reference's plain cg on the same system (beta = 1),
-    all host threads -- once to convergence for its iteration count, then bounded
-    10-iteration samples per step.  The reference cannot build cfg 3's hierarchy
-    (k-means with K = 10 000 over 1 M rows) nor finish its multilevel FCG here."""
+def sweep_config(cfg, nnz, sha):
+    """The config keys both arms print for a beta-sweep workload (same_config)."""
+    nb = cfg["n_rhs"]
+    return {"workload": cfg["workload"], "n_samples": cfg["n"], "n_features": cfg["f"], "nnz": int(nnz),
+            "x_sha256": sha, "betas": cfg["betas"], "n_rhs": nb, "rhs_seeds": f"42..{42 + nb - 1}",
+            "tol": cfg["tol"], "levels": [cfg["f"]] + list(cfg["ks"]),
+            "l2": "inputs larger than L2 (X >= 600 MB; no flush needed)"}
+
+
+def ref_fixture(cfg):
+    path = os.path.join(ROOT, "tests", "golden", cfg.get("ref_fixture", "none"))
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
+def ref_method_text(cfg):
+    return (f"reference {cfg['ref_method']} (krylov.cpp:94-157 + JacobiPreconditioner :41-47): the reference's "
+            f"fastest method on this system -- its fcg_multilevel needs > 1000 outer iterations here and its k-means "
+            f"cannot build the hierarchy (DESIGN.md §4.10, §6)")
+
+
+def run_reference_sweep(args, cfg):
+    """The reference arm of a beta-sweep config (cfg 3): the reference's own
+    sources (oracle/_ref) on all host threads, input built by the reference's
+    own CounterRng (oracle/synth.hpp, SHA-256 printed), every step one COMPLETE
+    solve -- b = normals(42 + step mod 16), beta = betas[step mod 5], the
+    reference timer (krylov.cpp:651-668, setup and rhs formation untimed)."""
+    import oracle
     world = dist_setup()[0]
-    x = make_matrix(cfg)
-    threads = os.cpu_count() or 1
-    cb = ref_cg_beta(cfg)
-    c = dict(cfg, ks=[], method="cg", beta=cb)
     t0 = time.time()
-    iters = None
-    if cfg["n"] > 4_000_000:  # cfg 5: thousands of CG iterations at ~seconds each -- use the GPU run's count
-        try:
-            prof = json.load(open(os.path.join(ROOT, "profiles", f"r1_bench_{args.config}.json")))
-            iters = int(prof["cg_iterations"])
-        except Exception:
-            iters = None
-    if iters is None:
-        _, kind, iters = reference_solve_sample(c, x, [], threads, 20000)
-    per = []
+    kind = "reference" if oracle.available("ref") else "port"
+    chk = oracle.Checker("ref" if kind == "reference" else "oracle")
+    threads = os.cpu_count() or 1
+    chk.set_num_threads(threads)
+    m = chk.synth_sparse_zipf(cfg["n"], cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"],
+                              row_streams=True)
+    sha = csr_sha(*m.export())
+    t_gen = time.time() - t0
+    per, its = [], []
+    nb, betas = cfg["n_rhs"], cfg["betas"]
     for step in range(args.warmup + args.steps):
-        sec, kind, _ = reference_solve_sample(c, x, [], threads, 10, 42 + step)
+        beta = betas[step % len(betas)]
+        b = chk.normals(42 + step % nb, cfg["n"])
+        s = chk.solve(m, beta, b, cfg["ref_method"], tol=cfg["tol"], max_iters=400_000)
         if step >= args.warmup:
-            per.append(sec)
-    value = statistics.mean(per) * iters * 1e3
-    sample = (f"reference cg (beta={cb:g}), {iters} iterations to 1e-6, 10-iteration samples per step x {iters}; "
-              f"not the headline's algorithm (pcg_vcycle), the reference's fastest here")
+            per.append(s.wall_time_s * 1e3)
+            its.append(int(s.iterations))
+    value = statistics.mean(per)
+    sample = (f"complete {cfg['ref_method']} solves, one per step (beta = betas[step mod 5], b = normals(42 + step "
+              f"mod 16)), reference timer, {threads} host threads; no extrapolation")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "parallelism": "host threads"},
+        "config": sweep_config(cfg, m.nnz, sha),
+        "algorithm": ref_method_text(cfg), "execution": f"host threads x{threads}",
+        "iterations": its,
+        "same_algorithm": {"method": cfg["ref_method"], "reference_ms_per_solve": value},
         "cpu_baseline": {"value": value, "unit": "ms/solve", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "ms/solve", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": time.time() - t0}), flush=True)
+        "input_generation_s": t_gen, "wall_s": time.time() - t0}), flush=True)
 
 
 def run_reference_arm(args, cfg):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    if cfg.get("sketch"):  # cfg 3: the reference's cg (its multilevel FCG cannot finish here)
-        run_reference_cfg3(args, cfg)
+    if cfg.get("sketch"):  # cfg 3 / 5: complete solves of the reference's fastest method
+        run_reference_sweep(args, cfg)
         return
-    x = make_matrix(cfg)
+    x = make_reference_matrix(cfg)
     scale, iters_fixed = 1.0, None
     if cfg["kind"] == "lowrank":  # bounded sample: the first ref_rows samples, solved to tolerance
         scale = x.n_samples / cfg["ref_rows"]
@@ -737,179 +802,218 @@ def run_b200(args, cfg):
         pg.destroy_process_group()
 
 
-def run_cfg3(args, cfg):
-    """BASELINE cfg 3: a beta sweep over one fixed hierarchy with 16 right-hand sides.
-    A step is one solve of one (beta, b) pair, pairs taken in sweep order (beta
-    changes via set_beta between steps, outside the events: it rebuilds only the
-    beta-dependent coarse factors, §4.8).  value = device ms per solve."""
+def timed_batches(pm, stream, bcm, wcm, nb, betas, schedule, cur):
+    """Batched solves (one rmg_method_solve_batch per step), beta changed between steps
+    outside the events; returns per-step device ms and the reports."""
     import torch
-    import paper_1806_05826_b200 as R
-    world, rank, local = dist_setup()
-    if rank != 0:
-        return
-    torch.cuda.set_device(local)
-    ctx = R.Context(local)
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
-    t0 = time.time()
-    x = make_matrix(cfg)
-    m = R.DeviceMatrix(x, ctx)
-    spec = R.MethodSpec(kind=R.method_from_string(cfg["method"]), levels=level_specs(cfg),
-                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"]))
-    pm = R.PreparedMethod(m, cfg["betas"][0], spec)
-    setup_s = time.time() - t0
-    dev = torch.device("cuda", local)
-    nb = cfg["n_rhs"]
-    bs = [torch.from_numpy(R.rng_normals(42 + k, x.n_samples)).to(dev) for k in range(nb)]
-    w = torch.empty(x.n_features, dtype=torch.float64, device=dev)
-    pairs = [(beta, k) for beta in cfg["betas"] for k in range(nb)]
-    cur = [None]
-
-    def go(i, timed):
-        beta, k = pairs[i % len(pairs)]
+    ms, reps = [], []
+    for bi in schedule:
+        beta = betas[bi]
         if cur[0] != beta:
             pm.set_beta(beta)
             cur[0] = beta
-        if not timed:
-            return pm.solve_device(bs[k].data_ptr(), w.data_ptr()), None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rep = pm.solve_device(bs[k].data_ptr(), w.data_ptr())
+        rs = pm.solve_batch_device(bcm.data_ptr(), wcm.data_ptr(), nb, True)
         e1.record(stream)
         torch.cuda.synchronize()
-        return rep, e0.elapsed_time(e1)
+        ms.append(e0.elapsed_time(e1))
+        reps.append(rs)
+    return ms, reps
 
+
+def block_bytes(n, f, nnz, pattern, k):
+    """SURVEY.md §8(d) for k right-hand sides: the index / value streams of both sweeps
+    once, the vector term (v, beta v, t written + read, out) k times."""
+    s_val = 0 if pattern else 8
+    return 2 * nnz * (4 + s_val) + 4 * (n + 1) + 4 * (f + 1) + 8 * (f + 2 * n + 2 * f) * k
+
+
+def run_sweep(args, cfg):
+    """BASELINE cfg 3: a beta sweep over one fixed hierarchy with 16 right-hand sides
+    solved as a batched block operator.  A step = one beta's batch (one
+    rmg_method_solve_batch of the 16 columns), betas in sweep order (set_beta between
+    steps, outside the events: it rebuilds only the beta-dependent coarse factors).
+    value = device ms per right-hand side.  N > 1 ranks: the (beta, batch) steps are
+    independent units, dealt round-robin to the ranks (no collective on the data
+    path); value = max-over-ranks time / all solves."""
+    import torch
+    import paper_1806_05826_b200 as R
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    ctx = R.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
     trace = (lambda *a: print("[trace]", *a, file=sys.stderr, flush=True)) if os.environ.get("RMG_BENCH_TRACE") else (
         lambda *a: None)
+    t0 = time.time()
+    x = make_matrix(cfg)
+    sha = csr_sha(x.row_offsets, x.column_indices, x.value_array()) if rank == 0 else None
+    m = R.DeviceMatrix(x, ctx)
+    betas, nb = cfg["betas"], cfg["n_rhs"]
+    spec = R.MethodSpec(kind=R.method_from_string(cfg["method"]), levels=level_specs(cfg),
+                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"]))
+    pm = R.PreparedMethod(m, betas[0], spec)
+    cur = [betas[0]]
+    setup_s = time.time() - t0
     trace("setup", setup_s)
-    for i in range(args.warmup):
-        go(i, False)
-        trace("warm", i)
+    dev = torch.device("cuda", local)
+    bcm = torch.stack([torch.from_numpy(R.rng_normals(42 + k, x.n_samples)) for k in range(nb)], 0).to(dev)
+    bcm = bcm.contiguous()  # column-major n x nb block (column k = b_k)
+    wcm = torch.empty(nb, x.n_features, dtype=torch.float64, device=dev)
+    sched = lambda i: (i * world + rank) % len(betas)  # noqa: E731  round-robin units over ranks
+    timed_batches(pm, stream, bcm, wcm, nb, betas, [sched(i) for i in range(args.warmup)], cur)
     torch.cuda.synchronize()
-    res = []
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            res.append(go(args.warmup + i, True))
-    ms = [r[1] for r in res]
-    single_ms = statistics.mean(ms)
-    value, batched = single_ms, None
-    if nb > 1 and cfg["method"] == "pcg_vcycle":
-        # the config's "k right-hand sides solved as a batched block operator": one
-        # rmg_method_solve_batch call per beta solves all nb columns in lock step
-        # (DESIGN.md §4.12); a step = one beta's batch, value = ms per right-hand side
-        bcm = torch.stack(bs, 0).contiguous()  # column-major n x nb block
-        wcm = torch.empty(nb, x.n_features, dtype=torch.float64, device=dev)
-        bms = []
-        trace("single done")
-        for i in range(args.warmup + args.steps):
-            beta = cfg["betas"][i % len(cfg["betas"])]
-            if cur[0] != beta:
-                pm.set_beta(beta)
-                cur[0] = beta
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            R.ridgemg._lib.check(pm.lib.rmg_method_solve_batch(pm.h, bcm.data_ptr(), wcm.data_ptr(), nb, None, 1))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if i >= args.warmup:
-                bms.append(e0.elapsed_time(e1))
-            trace("batch", i)
-        value = statistics.mean(bms) / nb
-        batched = {"k": nb, "ms_per_batch": statistics.mean(bms), "ms_per_rhs": value,
-                   "unbatched_ms_per_rhs": single_ms}
-        # e2e: the same batched call with host buffers (pinned B in, W out)
-        hb = bcm.cpu().pin_memory()
-        hw = torch.empty(nb, x.n_features, dtype=torch.float64).pin_memory()
-        be2e = []
-        for i in range(args.steps):
-            beta = cfg["betas"][(args.warmup + i) % len(cfg["betas"])]
-            if cur[0] != beta:
-                pm.set_beta(beta)
-                cur[0] = beta
-            torch.cuda.synchronize()
-            tt = time.perf_counter()
-            R.ridgemg._lib.check(pm.lib.rmg_method_solve_batch(pm.h, hb.data_ptr(), hw.data_ptr(), nb, None, 0))
-            be2e.append((time.perf_counter() - tt) * 1e3 / nb)
-            trace("e2e batch", i)
-        batched["e2e_ms_per_rhs"] = statistics.mean(be2e)
-    # e2e through the C ABI with host buffers (pinned b, w)
-    pb = [torch.from_numpy(R.rng_normals(42 + k, x.n_samples)).pin_memory() for k in range(nb)]
-    pw = torch.empty(x.n_features, dtype=torch.float64).pin_memory()
+        ms, reps = timed_batches(pm, stream, bcm, wcm, nb, betas,
+                                 [sched(args.warmup + i) for i in range(args.steps)], cur)
+    total = sum(ms)
+    if pg:
+        pg.barrier()
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total = float(t.item())
+    value = total / (args.steps * nb * world)
+    trace("timed", value)
+
+    # e2e: the same batched call with host buffers (pinned B in, W out, copies inside)
+    hb = bcm.cpu().pin_memory()
+    hw = torch.empty(nb, x.n_features, dtype=torch.float64).pin_memory()
     e2e = []
     for i in range(args.steps):
-        beta, k = pairs[(args.warmup + i) % len(pairs)]
+        beta = betas[sched(args.warmup + i)]
         if cur[0] != beta:
             pm.set_beta(beta)
             cur[0] = beta
         torch.cuda.synchronize()
         tt = time.perf_counter()
-        R.ridgemg._lib.check(pm.lib.rmg_method_solve(pm.h, R.ridgemg._ptr(pb[k].numpy()), R.ridgemg._ptr(pw.numpy()),
-                                                     None, 0))
+        pm.solve_batch_device(hb.data_ptr(), hw.data_ptr(), nb, False)
         e2e.append((time.perf_counter() - tt) * 1e3)
-    # the 16-RHS block operator (SpMM) against 16 single applications
+    e2e_total = sum(e2e)
+    if pg:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = e2e_total / (args.steps * nb * world)
+    trace("e2e", e2e_value)
+    if rank != 0:
+        pm.close()
+        m.close()
+        pg.barrier()
+        pg.destroy_process_group()
+        return
+
+    # the dominant kernel: the fine-level block operator (k_spmm_sell + k_xt_block), 3
+    # applications per lock-step PCG iteration (one outside, two inside the V-cycle)
     peak, peak_kind = peaks()
-    cold = pm.time_operator(0, 10, True)
     vb = torch.randn(x.n_features, nb, dtype=torch.float64, device=dev)
     ob = torch.empty_like(vb)
-    torch.cuda.synchronize()
     tb = []
-    for _ in range(6):
+    for i in range(12):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         R.ridgemg._lib.check(m.lib.rmg_ridge_apply_block(m.h, 1.0, vb.data_ptr(), ob.data_ptr(), nb, 1))
         e1.record(stream)
         torch.cuda.synchronize()
-        tb.append(e0.elapsed_time(e1))
+        if i >= 2:
+            tb.append(e0.elapsed_time(e1))
+    t_block = statistics.mean(tb)
+    bb = block_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern, nb)
+    max_its = [max(r.iterations for r in rs) for rs in reps]
+    fine_applies = sum(3 * it + 2 for it in max_its) if cfg["method"] == "pcg_vcycle" else sum(it + 1 for it in max_its)
+    cold = pm.time_operator(0, 10, True)
     fb = algorithmic_bytes(x.n_samples, x.n_features, m.nnz, m.is_pattern)
-    # CPU baseline: the reference's own solver on this system within minutes -- its plain
-    # cg (its multilevel FCG needs > 1000 outer iterations x ~400 inner level-1 solves here,
-    # DESIGN.md §4.10), 3 iterations timed, x the GPU's CG iteration count for beta = 1
-    trace("operator timings done")
-    cpu = None
-    cb = ref_cg_beta(cfg)
-    cg_iters = None
-    try:  # the GPU's plain-CG iteration count on this system (the reference arm's extrapolation)
-        pc = R.PreparedMethod(m, cb, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(cfg["tol"], 50000)))
-        cg_iters = pc.solve_device(bs[0].data_ptr(), w.data_ptr()).iterations
-        pc.close()
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get(
+            "dram_bytes_per_launch")
     except Exception:
-        cg_iters = None
-    if not args.no_cpu_baseline and cg_iters:
+        traffic = None
+
+    # same algorithm as the reference arm: the reference's fastest method, batched here
+    fx = ref_fixture(cfg)
+    same = None
+    try:
+        pj = R.PreparedMethod(m, betas[0], R.MethodSpec(kind=R.method_from_string(cfg["ref_method"]),
+                                                        solver=R.SolverConfig(cfg["tol"], 400_000)))
+        jc = [betas[0]]
+        timed_batches(pj, stream, bcm, wcm, nb, betas, [0], jc)
+        jms, jreps = timed_batches(pj, stream, bcm, wcm, nb, betas, list(range(len(betas))), jc)
+        wj = wcm.clone()
+        ref_its = fx.get(f"{cfg['ref_method']}/threads1/tol{cfg['tol']:g}", {})
+        same = {"method": cfg["ref_method"], "gpu": "batched block operator, 16 columns in lock step",
+                "gpu_ms_per_solve": statistics.mean(jms) / nb,
+                "gpu_ms_per_solve_by_beta": {f"{b:g}": t / nb for b, t in zip(betas, jms)},
+                "gpu_iterations_b42_by_beta": {f"{b:g}": rs[0].iterations for b, rs in zip(betas, jreps)},
+                "reference_iterations_b42_by_beta": {k: v["iterations"] for k, v in ref_its.items()},
+                "reference_fixture": "tests/golden/cfg3_ref.json (oracle/_ref, threads = 1)"}
+        pj.close()
+        del wj
+    except Exception as e:  # reported, never fatal
+        same = {"failed": str(e)}
+
+    # CPU baseline: the reference (oracle/_ref) on ONE host thread, complete solves
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
         try:
-            sec, kind, ran = reference_solve_sample(dict(cfg, ks=[], method="cg", beta=cb), x, [], 1, 3)
-            cpu = {"value": sec * cg_iters * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
-                   "sample": f"reference cg on the same system (beta={cb:g}), {ran} iterations timed x "
-                             f"{cg_iters} CG iterations (GPU count); different algorithm from the headline"}
+            import oracle
+            kind = "reference" if oracle.available("ref") else "port"
+            chk = oracle.Checker("ref" if kind == "reference" else "oracle")
+            chk.set_num_threads(1)
+            om = chk.matrix(x.n_samples, x.n_features, x.row_offsets, x.column_indices, x.value_array())
+            bsel = [betas[-1], betas[len(betas) // 2]]
+            secs = [chk.solve(om, bt, chk.normals(42, x.n_samples), cfg["ref_method"], tol=cfg["tol"],
+                              max_iters=400_000).wall_time_s for bt in bsel]
+            cpu = {"value": statistics.mean(secs) * 1e3, "unit": "ms/solve", "cores": 1, "kind": kind,
+                   "sample": f"complete {cfg['ref_method']} solves at beta {[f'{b:g}' for b in bsel]} (b = "
+                             f"normals(42)), the reference's own timer, 1 host thread; no extrapolation"}
+            del om
         except Exception as e:
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    its = [[r.iterations for r in rs] for rs in reps]
     print(json.dumps({
-        "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": batched["ms_per_batch"] if batched else value,
-        "higher_is_better": False, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
-        "config": {"workload": cfg["workload"], "n_samples": x.n_samples, "n_features": x.n_features, "nnz": m.nnz,
-                   "levels": [x.n_features] + list(cfg["ks"]), "betas": cfg["betas"], "n_rhs": nb,
-                   "tol": cfg["tol"], "method": cfg["method"], "parallelism": "single GPU",
-                   "l2": "inputs (X: >= 600 MB) larger than L2"},
-        "iterations": [r[0].iterations for r in res], "converged": all(r[0].converged for r in res),
-        "setup_s": setup_s, "cg_iterations": cg_iters,
-        "roofline": {"bound": "hbm", "kernel": "level-0 operator K1 + K2 (cold L2)", "algorithmic_bytes_per_launch": fb,
-                     "ms_per_launch": cold[0], "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
-                     "frac": fb / (cold[0] * 1e6) / peak, "traffic": None, "peak_kind": peak_kind},
-        "block_operator": {"k": nb, "ms_per_block": statistics.median(tb), "ms_per_rhs": statistics.median(tb) / nb,
-                           "ms_single_apply": cold[0]},
-        "batched_solve": batched,
+        "config": sweep_config(cfg, m.nnz, sha),
+        "algorithm": (f"{cfg['method']}: PCG (krylov.cpp:94-157) preconditioned by a symmetric V-cycle over the "
+                      f"config's 4-level hierarchy (damped-Jacobi pre/post smoothing; dense G_k for levels 1-2, "
+                      f"DESIGN.md §4.11, §4.14), 16 columns in lock step over the block operator"),
+        "execution": (f"{world} GPUs, independent (beta, batch) units round-robin" if world > 1 else "single GPU"),
+        "iterations_per_step": its, "converged": all(r.converged for rs in reps for r in rs),
+        "betas_per_step": [betas[sched(args.warmup + i)] for i in range(args.steps)],
+        "setup_s": setup_s,
+        "roofline": {"bound": "hbm", "kernel": "level-0 block operator X^T (X V) + beta V, k = 16 (k_spmm_sell + "
+                                              "k_xt_block + k_block_finish), CUDA events on the library stream",
+                     "achieved": bb / (t_block * 1e6), "peak": peak, "unit": "GB/s", "frac": bb / (t_block * 1e6) / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bb, "ms_per_launch": t_block,
+                     "peak_kind": peak_kind, "share_of_step": fine_applies * t_block / total},
+        "operator_roofline": {"bound": "hbm", "kernel": "K1 (X v, SELL-32) + K2 (X^T pass), one RHS, L2 flushed",
+                              "algorithmic_bytes_per_apply": fb, "ms_per_apply": cold[0],
+                              "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
+                              "frac": fb / (cold[0] * 1e6) / peak},
+        "same_algorithm": same,
         "cpu_baseline": cpu,
-        "e2e": ({"value": batched["e2e_ms_per_rhs"], "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8 * nb,
-                 "d2h_bytes_per_step": x.n_features * 8 * nb, "note": "one batched call of nb right-hand sides per step"}
-                if batched else
-                {"value": statistics.mean(e2e), "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8,
-                 "d2h_bytes_per_step": x.n_features * 8}),
-        "gpu_launches": int(sum(r[0].kernel_launches for r in res)),
+        "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8 * nb,
+                "d2h_bytes_per_step": x.n_features * 8 * nb,
+                "note": "one batched call of 16 right-hand sides per step from pinned host memory"},
+        "gpu_launches": int(sum(sum(r.kernel_launches for r in rs) for rs in reps)),
         "clocks": clocks.summary()}), flush=True)
     pm.close()
     m.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
 
 
 def main():
@@ -917,7 +1021,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample-iters", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -929,7 +1033,7 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     elif args.config in ("cfg3", "cfg5"):
-        run_cfg3(args, cfg)
+        run_sweep(args, cfg)
     else:
         run_b200(args, cfg)
 

@@ -1,0 +1,206 @@
+// Dense Gram matrices of coarse levels: assembly and application (dense_gram.cuh).
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#include "dense_gram.cuh"
+
+namespace rmg {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+inline void check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// One warp per feature i (row of G) and column tile [c0, c0 + width): the
+// warp walks the rows r of X^T row i in increasing order; for each, its lanes
+// take the row's nonzeros (distinct columns, so no two lanes touch the same
+// accumulator) and add x_ri * x_rj into the warp's shared-memory tile.  Every
+// entry therefore sums its products in increasing row order, each product and
+// sum rounded separately -- coarse_gram's (and krylov.cpp:350-365's) order.
+__global__ void k_gram_rows(const int32_t* __restrict__ xptr, const int32_t* __restrict__ xidx,
+                            const double* __restrict__ xval, const int32_t* __restrict__ tptr,
+                            const int32_t* __restrict__ tidx, const double* __restrict__ tval, int64_t n, int64_t c0,
+                            int width, double* __restrict__ G, int64_t ldg) {
+  extern __shared__ double acc_all[];
+  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* acc = acc_all + static_cast<size_t>(warp) * width;
+  const int64_t c1 = c0 + width;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * warps + warp; i < n; i += static_cast<int64_t>(gridDim.x) * warps) {
+    for (int q = lane; q < width; q += 32) acc[q] = 0.0;
+    __syncwarp();
+    const int32_t b = tptr[i], e = tptr[i + 1];
+    for (int32_t base = b; base < e; base += 32) {
+      const int m = min(32, e - base);
+      int32_t rb = 0, re = 0;
+      double vp = 0.0;
+      if (lane < m) {
+        const int32_t r = tidx[base + lane];
+        vp = tval != nullptr ? tval[base + lane] : 1.0;
+        rb = xptr[r];
+        re = xptr[r + 1];
+      }
+      for (int t = 0; t < m; ++t) {
+        const double v = __shfl_sync(kFull, vp, t);
+        const int32_t s0 = __shfl_sync(kFull, rb, t), s1 = __shfl_sync(kFull, re, t);
+        for (int32_t q = s0 + lane; q < s1; q += 32) {
+          const int32_t j = xidx[q];
+          if (j >= c0 && j < c1) {
+            const double xv = xval != nullptr ? xval[q] : 1.0;
+            acc[j - c0] = __dadd_rn(acc[j - c0], __dmul_rn(v, xv));
+          }
+        }
+        __syncwarp();
+      }
+    }
+    double* out = G + i * ldg + c0;
+    for (int q = lane; q < width; q += 32) out[q] = acc[q];
+    __syncwarp();
+  }
+}
+
+// y = G x + beta x: one warp per row, G streamed once (evict-first loads), x
+// from L1/L2.  Fixed per-lane order and butterfly: deterministic.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_gram_gemv(const double* __restrict__ G, int64_t ldg,
+                                                   const double* __restrict__ x, double beta, double* __restrict__ y,
+                                                   int64_t n, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + warp; i < n; i += static_cast<int64_t>(gridDim.x) * 8) {
+    const double* g = G + i * ldg;
+    double a0 = 0.0, a1 = 0.0;
+    if (VEC) {
+      const int64_t n2 = n & ~int64_t{1};
+#pragma unroll 4
+      for (int64_t j = 2 * lane; j < n2; j += 64) {
+        const double2 gv = __ldcs(reinterpret_cast<const double2*>(g + j));
+        const double2 xv = __ldg(reinterpret_cast<const double2*>(x + j));
+        a0 = fma(gv.x, xv.x, a0);
+        a1 = fma(gv.y, xv.y, a1);
+      }
+      if ((n & 1) && lane == 0) a0 = fma(__ldcs(g + n - 1), x[n - 1], a0);
+    } else {
+#pragma unroll 4
+      for (int64_t j = lane; j < n; j += 32) a0 = fma(__ldcs(g + j), __ldg(x + j), a0);
+    }
+    double a = a0 + a1;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) a += __shfl_xor_sync(kFull, a, off);
+    if (lane == 0) y[i] = a + beta * x[i];
+  }
+}
+
+// Y = G V + beta V for one 16-column chunk [col0, col0 + kc) of row-major
+// n x ldv blocks.  A CTA owns 16 rows of G (4 per warp); V's rows are staged
+// in shared memory 256 at a time (column-major, padded: conflict-free), and
+// lane l accumulates the j = l (mod 32) terms of its warp's 4 x 16 outputs;
+// a warp reduce-scatter leaves lane l with outputs 2l, 2l + 1.
+constexpr int kGemmRows = 4, kGemmWarps = 4, kGemmJ = 256, kGemmK = 16, kVsLd = kGemmJ + 1;
+
+__global__ void __launch_bounds__(kGemmWarps * 32, 2)
+    k_gram_gemm(const double* __restrict__ G, int64_t ldg, const double* __restrict__ V, int ldv, int col0, int kc,
+                double beta, double* __restrict__ Y, int64_t n) {
+  __shared__ double vs[kGemmK * kVsLd];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kGemmWarps + warp) * kGemmRows;
+  const double* grow[kGemmRows];
+#pragma unroll
+  for (int r = 0; r < kGemmRows; ++r) grow[r] = G + min(row0 + r, n - 1) * ldg;
+  double acc[kGemmRows * kGemmK];
+#pragma unroll
+  for (int e = 0; e < kGemmRows * kGemmK; ++e) acc[e] = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += kGemmJ) {
+    const int jn = static_cast<int>(n - j0 < kGemmJ ? n - j0 : int64_t{kGemmJ});
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGemmJ * kGemmK; e += blockDim.x) {
+      const int jj = e / kGemmK, q = e % kGemmK;
+      vs[q * kVsLd + jj] = (jj < jn && q < kc) ? V[(j0 + jj) * ldv + col0 + q] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = 0; t < kGemmJ / 32; ++t) {
+      const int jj = lane + 32 * t;
+      double g[kGemmRows];
+#pragma unroll
+      for (int r = 0; r < kGemmRows; ++r) g[r] = jj < jn ? __ldcs(grow[r] + j0 + jj) : 0.0;
+#pragma unroll
+      for (int q = 0; q < kGemmK; ++q) {
+        const double v = vs[q * kVsLd + jj];
+#pragma unroll
+        for (int r = 0; r < kGemmRows; ++r) acc[r * kGemmK + q] = fma(g[r], v, acc[r * kGemmK + q]);
+      }
+    }
+  }
+  // reduce-scatter over the warp: stage `off` halves the live values
+#pragma unroll
+  for (int off = 16, cnt = kGemmRows * kGemmK / 2; off >= 1; off >>= 1, cnt >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int e = 0; e < cnt; ++e) {
+      const double send = upper ? acc[e] : acc[e + cnt];
+      const double keep = upper ? acc[e + cnt] : acc[e];
+      acc[e] = keep + __shfl_xor_sync(kFull, send, off);
+    }
+  }
+  // lane l now holds flattened outputs 2l and 2l + 1 (row l / 8, columns 2(l % 8) + {0, 1})
+  const int r = lane >> 3, q = (2 * lane) & (kGemmK - 1);
+  const int64_t row = row0 + r;
+  if (row < n) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (q + u < kc) {
+        const int64_t o = row * ldv + col0 + q + u;
+        Y[o] = acc[u] + beta * V[o];
+      }
+  }
+}
+
+}  // namespace
+
+void sparse_gram_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval,
+                     const int32_t* tptr, const int32_t* tidx, const double* tval, int64_t n, double* G,
+                     int64_t ldg) {
+  if (n <= 0) return;
+  const int tile = static_cast<int>(std::min<int64_t>(n, 6144));
+  const int warps = std::max(1, std::min(16, (200 * 1024) / (tile * 8)));
+  const size_t smem = static_cast<size_t>(warps) * tile * sizeof(double);
+  cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const int64_t blocks_needed = (n + warps - 1) / warps;
+  const int grid = static_cast<int>(std::min<int64_t>(blocks_needed, 148 * std::max(1, 16 / warps)));
+  for (int64_t c0 = 0; c0 < n; c0 += tile) {
+    const int width = static_cast<int>(std::min<int64_t>(tile, n - c0));
+    k_gram_rows<<<grid, warps * 32, smem, s>>>(xptr, xidx, xval, tptr, tidx, tval, n, c0, width, G, ldg);
+    check("gram_rows");
+  }
+}
+
+void launch_gram_gemv(const double* G, int64_t ldg, const double* x, double beta, double* y, int64_t n,
+                      const int32_t* done, cudaStream_t s) {
+  if (n <= 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 7) / 8, 148 * 8));
+  const bool vec = (ldg % 2 == 0) && (reinterpret_cast<uintptr_t>(G) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  if (vec)
+    k_gram_gemv<true><<<grid, 256, 0, s>>>(G, ldg, x, beta, y, n, done);
+  else
+    k_gram_gemv<false><<<grid, 256, 0, s>>>(G, ldg, x, beta, y, n, done);
+  check("gram_gemv");
+}
+
+void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
+                      cudaStream_t s) {
+  if (n <= 0 || k <= 0) return;
+  const int rows = kGemmRows * kGemmWarps;
+  const int grid = static_cast<int>((n + rows - 1) / rows);
+  for (int c0 = 0; c0 < k; c0 += kGemmK) {
+    const int kc = std::min(kGemmK, k - c0);
+    k_gram_gemm<<<grid, kGemmWarps * 32, 0, s>>>(G, ldg, V, k, c0, kc, beta, Y, n);
+    check("gram_gemm");
+  }
+}
+
+}  // namespace rmg

@@ -1,0 +1,37 @@
+// Dense Gram matrices of coarse levels.
+//
+// A coarse level X_k (N rows, n_k features) enters the solve only through
+// A_k = X_k^T X_k + beta_k I.  When n_k^2 doubles are fewer bytes than one
+// sweep pair over X_k (cfg 3: n_1 = 10 000 -> 800 MB against 1.15 GB of
+// X_c1 per application), the V-cycle applies the dense G_k = X_k^T X_k
+// instead: a GEMV (one RHS) or a skinny GEMM (k RHS) streaming G_k once.
+//
+// G_k is assembled on the device from the CSR of X_k and of X_k^T with the
+// reference coarse Gram's arithmetic (krylov.cpp:350-365): entry (i, j) is
+// the sum over the rows r holding both features, in increasing r, of the
+// separately rounded products x_ri * x_rj -- bit-identical to the host
+// restatement coarse_gram (host_setup.cpp), which also uses it for the
+// coarsest Cholesky and the dense inner levels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rmg {
+
+// G (n x n, row-major, leading dimension ldg) = X^T X, no beta.
+//   X   : row CSR (xptr[N+1], xidx, xval or nullptr for a binary pattern)
+//   X^T : feature CSR (tptr[n+1], tidx = rows ascending, tval or nullptr)
+void sparse_gram_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval,
+                     const int32_t* tptr, const int32_t* tidx, const double* tval, int64_t n, double* G,
+                     int64_t ldg);
+
+// y = G x + beta x (one right-hand side); no-op when *done != 0.
+void launch_gram_gemv(const double* G, int64_t ldg, const double* x, double beta, double* y, int64_t n,
+                      const int32_t* done, cudaStream_t s);
+
+// Y = G V + beta V for row-major n x k blocks V, Y (leading dimension k), k <= 64.
+void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
+                      cudaStream_t s);
+
+}  // namespace rmg

@@ -14,6 +14,7 @@
 #include <unordered_set>
 
 #include "kernels.cuh"
+#include "spmm_tma.cuh"
 
 namespace rmg {
 
@@ -382,11 +383,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __rest
                                                         const uint16_t* __restrict__ idx16,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ V, double* __restrict__ T,
-                                                        int64_t n_slices, int k, int c0, int kc) {
+                                                        int64_t slice0, int64_t n_slices, int k, int c0, int kc) {
   const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
   const bool colq = q < kc;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-  for (int64_t sl = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; sl < n_slices; sl += nwarps) {
+  for (int64_t sl = slice0 + (((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5); sl < slice0 + n_slices;
+       sl += nwarps) {
     const int64_t base = off[sl];
     for (int p = 0; p < 16; ++p) {
       const int slot = 2 * p + h;
@@ -400,11 +402,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __rest
       // dependent index -> gather pair at a time)
       const int qq = colq ? q : 0;
       const int src0 = lane & 16;
-      for (int j = 0; j < lmax; j += 16) {
+      // the next batch's index / value loads are issued before this batch's
+      // gathers, so a batch costs one memory latency instead of two
+      auto load = [&](int j, int& ci, double& xv) {
         const bool okq = j + q < len;
         const int64_t eq = okq ? base + (int64_t)(j + q) * 32 + slot : base + slot;
-        const int ciq = okq ? (NARROW ? (int)ld_stream(idx16 + eq) : ld_stream(idx + eq)) : -1;
-        const double xq = PAT ? 1.0 : ld_stream(val + eq);
+        ci = okq ? (NARROW ? (int)ld_stream(idx16 + eq) : ld_stream(idx + eq)) : -1;
+        xv = PAT ? 1.0 : ld_stream(val + eq);
+      };
+      int ci_next;
+      double x_next;
+      load(0, ci_next, x_next);
+      for (int j = 0; j < lmax; j += 16) {
+        const int ciq = ci_next;
+        const double xq = x_next;
+        if (j + 16 < lmax) load(j + 16, ci_next, x_next);
         int c[16];
         double x[16], vv[16];
 #pragma unroll
@@ -426,60 +438,79 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __rest
 }
 
 // X^T pass over a block: a half-warp per unit of work, lane q owning column q,
-// elements in order.  Units: the rows with <= 4096 nonzeros (whole rows), then
-// the items of longer rows (segment partials for k_block_finish).
+// elements in order.  Units: the rows with <= 512 nonzeros in the sample chunk
+// (whole rows, sorted by length so the two half-warps of a warp share a trip
+// count), then the items of longer rows (segment partials for k_block_finish).
+// Lane q loads element e + q of each 16-element batch once and shuffles hand
+// the indices to every lane (16 independent T-row gathers); the next batch's
+// loads are issued before this batch's gathers.
 template <bool PAT>
-__global__ void __launch_bounds__(kThreads, 5) k_xt_block(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(kThreads, 3) k_xt_block(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                        const double* __restrict__ val, BlockXtSchedule bs,
                                                        const double* __restrict__ T, const double* __restrict__ V,
-                                                       double* __restrict__ out, double beta, int k, int c0, int kc) {
-  const int lane = threadIdx.x & 31, q = lane & 15;
+                                                       double* __restrict__ out, double beta, int k, int c0, int kc,
+                                                       int first, int last) {
+  const int lane = threadIdx.x & 31, q = lane & 15, src0 = lane & 16;
   const bool colq = q < kc;
   const int64_t unit = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 4;
   const int64_t n_units = (int64_t)bs.n_short + bs.n_items;
-  if (unit >= n_units) return;
-  int row, e0, e1, seg;
-  if (unit < bs.n_short) {
+  if (((unit >> 1) << 1) >= n_units) return;  // both half-warps out of range: the whole warp
+  const bool valid = unit < n_units;
+  int row = 0, e0 = 0, e1 = 0, seg = -1;
+  if (valid && unit < bs.n_short) {
     row = bs.short_rows[unit];
-    e0 = ptr[row];
-    e1 = ptr[row + 1];
-    seg = -1;
-  } else {
+    e0 = bs.e_begin[row];
+    e1 = bs.e_end[row];
+  } else if (valid) {
     const int4 it = bs.items[unit - bs.n_short];
     row = it.x;
     e0 = it.y;
     e1 = it.z;
     seg = it.w;
   }
-  // (the shuffle-broadcast batching of k_spmm_sell measured slower here: the two
-  // half-warps' Zipf-skewed row lengths would have to share one trip count)
+  const int len = e1 - e0;
+  const int lmax = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
+  auto load = [&](int j, int& ci, double& xv) {
+    const bool ok = j + q < len;
+    ci = ok ? ld_stream(idx + e0 + j + q) : -1;
+    xv = (PAT || !ok) ? 1.0 : ld_stream(val + e0 + j + q);
+  };
+  int ci_next;
+  double x_next;
+  load(0, ci_next, x_next);
   double acc = 0.0;
-  for (int e = e0; e < e1; e += 8) {
-    int smp[8];
-    double x[8], tv[8];
+  for (int j = 0; j < lmax; j += 16) {
+    const int ci = ci_next;
+    const double xv = x_next;
+    if (j + 16 < lmax) load(j + 16, ci_next, x_next);
+    int c[16];
+    double x[16], tv[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool ok = e + u < e1;
-      smp[u] = ok ? idx[e + u] : -1;
-      x[u] = (ok && !PAT) ? val[e + u] : 1.0;
+    for (int u = 0; u < 16; ++u) {
+      c[u] = __shfl_sync(0xffffffffu, ci, src0 | u);
+      x[u] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xv, src0 | u);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) tv[u] = (smp[u] >= 0 && colq) ? __ldg(T + (int64_t)smp[u] * k + c0 + q) : 0.0;
+    for (int u = 0; u < 16; ++u) tv[u] = (c[u] >= 0 && colq) ? __ldg(T + (int64_t)c[u] * k + c0 + q) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (smp[u] >= 0) acc += PAT ? tv[u] : x[u] * tv[u];
+    for (int u = 0; u < 16; ++u)
+      if (c[u] >= 0) acc += PAT ? tv[u] : x[u] * tv[u];
   }
-  if (!colq) return;
-  if (seg < 0)
-    out[(int64_t)row * k + c0 + q] = acc + beta * V[(int64_t)row * k + c0 + q];
-  else
+  if (!colq || !valid) return;
+  if (seg < 0) {  // chunks accumulate in chunk order; the last one adds beta V
+    const int64_t o = (int64_t)row * k + c0 + q;
+    double r = first ? acc : out[o] + acc;
+    if (last) r = r + beta * V[o];
+    out[o] = r;
+  } else {
     bs.seg[(int64_t)seg * kBlockCols + q] = acc;
+  }
 }
 
 // rows split into several items: warp per row, lanes over the items
 // (lane-strided, fixed order) + warp tree, for each column
 __global__ void k_block_finish(BlockXtSchedule bs, const double* __restrict__ V, double* __restrict__ out,
-                               double beta, int k, int c0, int kc) {
+                               double beta, int k, int c0, int kc, int first, int last) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= bs.n_multi) return;
@@ -488,7 +519,12 @@ __global__ void k_block_finish(BlockXtSchedule bs, const double* __restrict__ V,
     double sum = 0.0;
     for (int g = lane; g < m.z; g += 32) sum += bs.seg[(int64_t)(m.y + g) * kBlockCols + q];
     sum = warp_sum(sum);
-    if (lane == 0) out[(int64_t)m.x * k + c0 + q] = sum + beta * V[(int64_t)m.x * k + c0 + q];
+    if (lane == 0) {
+      const int64_t o = (int64_t)m.x * k + c0 + q;
+      double r = first ? sum : out[o] + sum;
+      if (last) r = r + beta * V[o];
+      out[o] = r;
+    }
   }
 }
 
@@ -2048,40 +2084,68 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
 }
 
 
-void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule& bs, const double* v,
-                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
+void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
+                        const double* v, double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
   if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
+  // TMA gather passes (spmm_tma.cu) when V and T rows are 16-byte aligned
+  if (n_chunks > 0 && chunks[0].tk1.units != nullptr && tma_spmm_ok(v, k) && tma_spmm_ok(t, k)) {
+    for (int c0 = 0; c0 < k; c0 += kBlockCols) {
+      const int kc = std::min(kBlockCols, k - c0);
+      for (int c = 0; c < n_chunks; ++c) {
+        const BlockXtSchedule& bs = chunks[c];
+        const int first = c == 0, last = c + 1 == n_chunks;
+        launch_spmm_tma_rows(bs.tk1, v, x.cols, k, c0, kc, t, s);
+        launch_spmm_tma_xt(bs.tk2, t, x.rows, k, c0, kc, out, v, beta, bs.seg, first, last, s);
+        if (bs.n_multi > 0)
+          k_block_finish<<<static_cast<int>((static_cast<int64_t>(bs.n_multi) * 32 + 255) / 256), 256, 0, s>>>(
+              bs, v, out, beta, k, c0, kc, first, last);
+      }
+    }
+    check_launch("ridge_block_tma");
+    return;
+  }
   const double* vk = v;
   if (x.col_inv != nullptr) {  // relabeled columns: V rows into label order
     k_vperm_block<<<grid_for(x.cols * k, 148 * 8), kThreads, 0, s>>>(v, x.col_inv, vp, x.cols, k);
     vk = vp;
   }
-  const int g1 = grid_for(x.n_slices * 32, 148 * 8);
-  const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
-  const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
   for (int c0 = 0; c0 < k; c0 += kBlockCols) {
     const int kc = std::min(kBlockCols, k - c0);
-    if (x.val == nullptr) {
-      if (x.idx16 != nullptr)
-        k_spmm_sell<true, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
-                                                        t, x.n_slices, k, c0, kc);
-      else
-        k_spmm_sell<true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
-                                                         t, x.n_slices, k, c0, kc);
-      k_xt_block<true><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc);
-    } else {
-      if (x.idx16 != nullptr)
-        k_spmm_sell<false, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
-                                                         t, x.n_slices, k, c0, kc);
-      else
-        k_spmm_sell<false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val,
-                                                          vk, t, x.n_slices, k, c0, kc);
-      k_xt_block<false><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc);
+    for (int c = 0; c < n_chunks; ++c) {
+      const BlockXtSchedule& bs = chunks[c];
+      const int first = c == 0, last = c + 1 == n_chunks;
+      const int g1 = grid_for(bs.n_slices * 32, 148 * 8);
+      const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
+      const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
+      if (bs.n_slices > 0) {
+        if (x.val == nullptr) {
+          if (x.idx16 != nullptr)
+            k_spmm_sell<true, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val,
+                                                            vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+          else
+            k_spmm_sell<true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
+                                                             x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+        } else {
+          if (x.idx16 != nullptr)
+            k_spmm_sell<false, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
+                                                             x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+          else
+            k_spmm_sell<false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
+                                                              x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+        }
+      }
+      if (units > 0) {
+        if (xt.val == nullptr)
+          k_xt_block<true><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc, first, last);
+        else
+          k_xt_block<false><<<g2, kThreads, 0, s>>>(xt.ptr, xt.idx, xt.val, bs, t, v, out, beta, k, c0, kc, first,
+                                                    last);
+      }
+      if (bs.n_multi > 0)
+        k_block_finish<<<static_cast<int>((static_cast<int64_t>(bs.n_multi) * 32 + 255) / 256), 256, 0, s>>>(
+            bs, v, out, beta, k, c0, kc, first, last);
     }
-    if (bs.n_multi > 0)
-      k_block_finish<<<static_cast<int>((static_cast<int64_t>(bs.n_multi) * 32 + 255) / 256), 256, 0, s>>>(
-          bs, v, out, beta, k, c0, kc);
   }
   check_launch("ridge_block");
 }

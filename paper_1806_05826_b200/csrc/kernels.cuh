@@ -140,14 +140,32 @@ constexpr int kDenseMaxCols = 1024;  // 32 register partials per lane
 // Block operator (BASELINE cfg 3: k right-hand sides as one SpMM; DESIGN.md
 // §4.8): V, T and out are row-major blocks (F x k, N x k, F x k), so every
 // gathered row of V or T is k contiguous doubles (one 128 B line at k = 16).
+// A unit of work of the TMA gather passes (spmm_tma.cuh): (row of Y, first
+// entry, one past the last entry, segment slot or -1).  Units are whole CSR
+// rows, or <= 512-entry items of long rows whose segment partials
+// k_block_finish combines.
+struct TmaSpmm {
+  const int4* units = nullptr;
+  int n_units = 0;
+  const int32_t* idx = nullptr;  // column (K1) / sample (X^T pass) indices
+  const double* val = nullptr;   // nullptr: binary pattern
+};
+
+// The samples are split into chunks whose T slice (rows x 16 columns) stays in
+// L2: per chunk, K1 writes its T rows, then the X^T pass over
+// the same samples gathers them back from L2 and accumulates into out.
 struct BlockXtSchedule {
-  const int32_t* short_rows = nullptr;  // rows of X^T with <= 4096 nonzeros: one unit each
+  const int32_t* short_rows = nullptr;  // rows of X^T with <= 512 nonzeros in the chunk: one unit each
   int n_short = 0;
   const int4* items = nullptr;          // (row, k0, k1, seg) items of longer rows
   int n_items = 0;
   const int4* multi = nullptr;          // (row, first_seg, n_seg, -) rows split into several items
   int n_multi = 0;
   double* seg = nullptr;                // [n_items x 16] segment partials (seg >= 0)
+  const int32_t* e_begin = nullptr;     // per X^T row: first entry whose sample lies in the chunk
+  const int32_t* e_end = nullptr;       // per X^T row: one past its last entry in the chunk
+  int64_t slice0 = 0, n_slices = 0;     // K1: the SELL slices holding the chunk's samples
+  TmaSpmm tk1, tk2;                     // the same chunk as TMA gather units (K1 rows, X^T units)
 };
 
 // ---------------------------------------------------------------- launchers
@@ -169,8 +187,8 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
 // out = X^T (X V) + beta V for a row-major F x k block (k <= 64); x: the K1
 // layout (SELL), xt: X^T CSR (int32 sample indices), t: N x k scratch, vp:
 // F x k scratch (relabeled columns).  Per column the arithmetic order is fixed.
-void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule& bs, const double* v,
-                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
+void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
+                        const double* v, double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

@@ -10,6 +10,8 @@
 #include <thread>
 
 #include "runtime.cuh"
+#include "dense_gram.cuh"
+#include "spmm_tma.cuh"
 #include "fgmres.cuh"
 #include "dense_setup.hpp"
 #include "kmeans_gpu.hpp"
@@ -617,36 +619,101 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
 // Block operator schedule: rows of X^T with <= 512 nonzeros
 // are one unit each (a half-warp, elements in order); longer rows are split
 // into items of 512 whose partials are finished in item order.
-void Matrix::build_block_schedule(const HostCsr& ht) {
+void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   constexpr int64_t kItem = 512;  // a half-warp walks <= 512 elements (latency-bound chains)
-  std::vector<int32_t> sh;
-  std::vector<int4> it, mu;
-  int segs = 0;
-  for (int64_t r = 0; r < ht.n; ++r) {
-    const int64_t a = ht.ptr[r], e = ht.ptr[r + 1], len = e - a;
-    if (len <= kItem) {
-      sh.push_back(static_cast<int32_t>(r));
-    } else {
-      const int first = segs;
-      for (int64_t b = a; b < e; b += kItem)
-        it.push_back(make_int4(static_cast<int>(r), static_cast<int>(b), static_cast<int>(std::min(e, b + kItem)),
-                               segs++));
-      mu.push_back(make_int4(static_cast<int>(r), first, segs - first, 0));
+  // sample chunks: T's chunk slice (rows x 16 columns x 8 B) <= 64 MB stays in L2
+  // between K1 writing and the X^T pass reading it; chunks are whole 1024-row
+  // SELL windows (RMG_BLOCK_CHUNK_ROWS overrides the row count)
+  const int64_t n = ht.f, F = ht.n;
+  int64_t rmax = (int64_t{64} << 20) / (16 * 8);
+  if (const char* e = std::getenv("RMG_BLOCK_CHUNK_ROWS")) rmax = std::max<int64_t>(1, std::atoll(e));
+  const int64_t nch0 = std::max<int64_t>(1, (n + rmax - 1) / rmax);
+  int64_t rows = ((n + nch0 - 1) / nch0 + 1023) / 1024 * 1024;
+  rows = std::max<int64_t>(rows, 1024);
+  const int nch = static_cast<int>(std::max<int64_t>(1, (n + rows - 1) / rows));
+  bchunk_rows = rows;
+  // per X^T row j and chunk boundary c: the first entry with sample >= c * rows
+  std::vector<int32_t> bounds(static_cast<size_t>(nch + 1) * F);
+  for (int64_t j = 0; j < F; ++j) {
+    int64_t q = ht.ptr[j];
+    for (int c = 0; c <= nch; ++c) {
+      const int64_t lim = std::min<int64_t>(n, static_cast<int64_t>(c) * rows);
+      while (q < ht.ptr[j + 1] && ht.idx[q] < lim) ++q;
+      bounds[static_cast<size_t>(c) * F + j] = static_cast<int32_t>(c == nch ? ht.ptr[j + 1] : q);
     }
   }
   cudaStream_t s = ctx->stream;
-  bshort.upload(sh.data(), sh.size(), s);
-  bitems.upload(it.data(), it.size(), s);
-  bmulti.upload(mu.data(), mu.size(), s);
-  bseg.alloc(static_cast<size_t>(std::max(1, segs)) * 16);
-  RMG_CK(cudaStreamSynchronize(s));
-  bview.short_rows = bshort.get();
-  bview.n_short = static_cast<int>(sh.size());
-  bview.items = bitems.get();
-  bview.n_items = static_cast<int>(it.size());
-  bview.multi = bmulti.get();
-  bview.n_multi = static_cast<int>(mu.size());
-  bview.seg = bseg.get();
+  bbounds.upload(bounds.data(), bounds.size(), s);
+  const bool tma = tma_spmm_enabled();
+  if (tma) {  // X's row CSR for the TMA K1 (column order: the reference's summation order per row)
+    const std::vector<int32_t> i32 = narrow(xr.idx, "column indices");
+    bx_idx.upload(i32.data(), i32.size(), s);
+    if (!pattern) bx_val.upload(xr.val.data(), xr.val.size(), s);
+    RMG_CK(cudaStreamSynchronize(s));
+  }
+  bchunk_bufs.clear();
+  bchunk_bufs.resize(nch);
+  bviews.assign(nch, BlockXtSchedule{});
+  int max_segs = 1;
+  for (int c = 0; c < nch; ++c) {
+    std::vector<int32_t> sh;
+    std::vector<int4> it, mu;
+    int segs = 0;
+    for (int64_t r = 0; r < F; ++r) {
+      const int64_t a = bounds[static_cast<size_t>(c) * F + r], e = bounds[static_cast<size_t>(c + 1) * F + r];
+      if (e - a <= kItem) {
+        sh.push_back(static_cast<int32_t>(r));
+      } else {
+        const int first = segs;
+        for (int64_t b = a; b < e; b += kItem)
+          it.push_back(make_int4(static_cast<int>(r), static_cast<int>(b), static_cast<int>(std::min(e, b + kItem)),
+                                 segs++));
+        mu.push_back(make_int4(static_cast<int>(r), first, segs - first, 0));
+      }
+    }
+    max_segs = std::max(max_segs, segs);
+    // longest first: the two half-warps of a warp get rows of similar length
+    std::stable_sort(sh.begin(), sh.end(), [&](int32_t a, int32_t b) {
+      const size_t oa = static_cast<size_t>(c) * F, ob = static_cast<size_t>(c + 1) * F;
+      return bounds[ob + a] - bounds[oa + a] > bounds[ob + b] - bounds[oa + b];
+    });
+    BlockChunkBufs& cb = bchunk_bufs[c];
+    cb.sh.upload(sh.data(), sh.size(), s);
+    cb.it.upload(it.data(), it.size(), s);
+    cb.mu.upload(mu.data(), mu.size(), s);
+    const int64_t r0 = static_cast<int64_t>(c) * rows, r1 = std::min(n, r0 + rows);
+    std::vector<int4> u1, u2;  // TMA units: longest first (round-robin warps stay balanced)
+    for (int64_t r = tma ? r0 : r1; r < r1; ++r)
+      u1.push_back(make_int4(static_cast<int>(r), static_cast<int>(xr.ptr[r]), static_cast<int>(xr.ptr[r + 1]), -1));
+    std::stable_sort(u1.begin(), u1.end(), [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
+    for (int32_t r : sh) {
+      if (!tma) break;
+      u2.push_back(make_int4(r, bounds[static_cast<size_t>(c) * F + r], bounds[static_cast<size_t>(c + 1) * F + r], -1));
+    }
+    std::vector<int4> itl(tma ? it : std::vector<int4>{});
+    std::stable_sort(itl.begin(), itl.end(), [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
+    u2.insert(u2.begin(), itl.begin(), itl.end());
+    cb.u1.upload(u1.data(), u1.size(), s);
+    cb.u2.upload(u2.data(), u2.size(), s);
+    BlockXtSchedule& v = bviews[c];
+    v.short_rows = cb.sh.get();
+    v.n_short = static_cast<int>(sh.size());
+    v.items = cb.it.get();
+    v.n_items = static_cast<int>(it.size());
+    v.multi = cb.mu.get();
+    v.n_multi = static_cast<int>(mu.size());
+    v.e_begin = bbounds.get() + static_cast<size_t>(c) * F;
+    v.e_end = bbounds.get() + static_cast<size_t>(c + 1) * F;
+    if (tma) {
+      v.tk1 = TmaSpmm{cb.u1.get(), static_cast<int>(u1.size()), bx_idx.get(), pattern ? nullptr : bx_val.get()};
+      v.tk2 = TmaSpmm{cb.u2.get(), static_cast<int>(u2.size()), xt.view.idx, pattern ? nullptr : xt.view.val};
+    }
+    v.slice0 = r0 / 32;
+    v.n_slices = (r1 + 31) / 32 - r0 / 32;
+    RMG_CK(cudaStreamSynchronize(s));  // host vectors above go out of scope
+  }
+  bseg.alloc(static_cast<size_t>(max_segs) * 16);
+  for (auto& v : bviews) v.seg = bseg.get();
 }
 
 void Matrix::apply_block(const double* v, double* out, double beta, int k, bool sync) {
@@ -656,7 +723,8 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
-  launch_ridge_block(x.view, xt.view, bview, v, out, beta, k, bt.get(), bvp.get(), ctx->stream);
+  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), v, out, beta, k, bt.get(),
+                     bvp.get(), ctx->stream);
   if (sync) ctx->sync();
 }
 
@@ -821,7 +889,7 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
   xt.upload(ht, pattern, ctx->stream, false);
   sched.build(ht, ctx->stream, local.f);
   build_hot(ht, local.n);
-  build_block_schedule(ht);
+  build_block_schedule(local, ht);
   t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);
 }
@@ -1331,12 +1399,79 @@ std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& 
 // device-resident dense level (the beta-free sums cached: adding beta to the
 // diagonal after the sums is what coarse_gram does, so a beta sweep reuses them)
 std::vector<double> Method::level_gram(Matrix& m, double beta) {
-  if (!m.device_setup()) return coarse_gram(m.host_csr(), beta);
-  if (m.gram_cache.empty()) m.gram_cache = gram_dense_gpu(ctx_->stream, m.dense->view);
-  std::vector<double> a = m.gram_cache;
   const int64_t n = m.f();
-  for (int64_t i = 0; i < n; ++i) a[i * n + i] += beta;
+  if (m.gram_cache.empty()) {
+    if (m.device_setup()) {
+      m.gram_cache = gram_dense_gpu(ctx_->stream, m.dense->view);
+    } else if (m.comm != nullptr || m.dense != nullptr || std::getenv("RMG_HOST_GRAM") != nullptr) {
+      return coarse_gram(m.host_csr(), beta);
+    } else {  // sparse level: the same sums on the device (dense_gram.cu), bit-identical
+      DBuf<double> g(static_cast<size_t>(std::max<int64_t>(1, n)) * std::max<int64_t>(1, n));
+      device_gram(m, g.get(), n);
+      m.gram_cache.resize(static_cast<size_t>(n) * n);
+      if (n) RMG_CK(cudaMemcpyAsync(m.gram_cache.data(), g.get(), m.gram_cache.size() * 8, cudaMemcpyDeviceToHost,
+                                    ctx_->stream));
+      ctx_->sync();
+    }
+  }
+  std::vector<double> a = m.gram_cache;
+  for (int64_t i = 0; i < n; ++i) a[i * n + i] += beta;  // after the sums, as coarse_gram does
   return a;
+}
+
+// G = X^T X of a sparse level on the device: X's row CSR is staged for the
+// assembly (the resident K1 copy is SELL-32, possibly relabeled) and X^T is the
+// resident feature CSR.  Dense levels: gram_dense_gpu (dense_setup.cu).
+void Method::device_gram(Matrix& m, double* G, int64_t ld) {
+  cudaStream_t s = ctx_->stream;
+  const int64_t n = m.f();
+  if (m.dense != nullptr) {
+    if (m.gram_cache.empty()) m.gram_cache = gram_dense_gpu(s, m.dense->view);
+    for (int64_t i = 0; i < n; ++i)
+      RMG_CK(cudaMemcpyAsync(G + i * ld, m.gram_cache.data() + i * n, n * 8, cudaMemcpyHostToDevice, s));
+    ctx_->sync();
+    return;
+  }
+  const HostCsr& h = m.host_csr();
+  DBuf<int32_t> xp, xi;
+  DBuf<double> xv;
+  {
+    const std::vector<int32_t> p32 = narrow(h.ptr, "row offsets"), i32 = narrow(h.idx, "column indices");
+    xp.upload(p32.data(), p32.size(), s);
+    xi.upload(i32.data(), i32.size(), s);
+    if (!m.pattern) xv.upload(h.val.data(), h.val.size(), s);
+    sparse_gram_gpu(s, xp.get(), xi.get(), m.pattern ? nullptr : xv.get(), m.xt.view.ptr, m.xt.view.idx,
+                    m.pattern ? nullptr : m.xt.view.val, n, G, ld);
+    ctx_->sync();  // the staged CSR is released on return
+  }
+}
+
+// pcg_vcycle: dense G_k for the levels where streaming n_k^2 doubles once costs
+// fewer bytes than the X_k sweep pair (X_k, then X_k^T) it replaces, and that
+// fit comfortably in free HBM (RMG_VC_DENSE=0 keeps the sweeps).
+void Method::build_dense_grams() {
+  dg_built_ = true;
+  dg_.clear();
+  dg_.resize(coarse_.size());
+  const char* e = std::getenv("RMG_VC_DENSE");
+  if (e != nullptr && std::string(e) == "0") return;
+  for (size_t k = 1; k < coarse_.size(); ++k) {
+    Matrix& m = level_matrix(k);
+    if (m.comm != nullptr) continue;
+    const int64_t n = m.f();
+    const double dense_bytes = 8.0 * static_cast<double>(n) * static_cast<double>(n);
+    const double sweep_bytes = m.dense != nullptr ? static_cast<double>(m.n()) * n * 8.0
+                                                  : 2.0 * static_cast<double>(m.nnz()) * (m.pattern ? 4.0 : 12.0);
+    size_t free_b = 0, total_b = 0;
+    RMG_CK(cudaMemGetInfo(&free_b, &total_b));
+    if (!(dense_bytes < sweep_bytes) || dense_bytes > 0.4 * static_cast<double>(free_b)) continue;
+    auto d = std::make_unique<DenseGram>();
+    d->n = n;
+    d->ld = (n + 1) / 2 * 2;
+    d->G.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * d->ld);
+    device_gram(m, d->G.get(), d->ld);
+    dg_[k] = std::move(d);
+  }
 }
 
 // JacobiPreconditioner (krylov.cpp:41-47): inverse of beta + diag(X^T X)
@@ -2014,6 +2149,7 @@ void Method::build_vcycle() {
   const size_t L = coarse_.size();
   vc_graph_.reset();  // its kernels point at the buffers rebuilt here
   vc_.clear();
+  if (!dg_built_) build_dense_grams();  // beta-free: built once, kept across set_beta
   for (size_t k = 0; k < L; ++k) {
     Matrix& m = level_matrix(k);
     const int64_t n = m.f();
@@ -2048,7 +2184,10 @@ void Method::build_vcycle() {
       a.v = v->x1.get();
       a.out = v->y.get();
       a.beta = level_beta(k);
-      m.apply(v->x1.get(), Epi::Axpby, a);
+      if (const DenseGram* dg = dgram(k))
+        launch_gram_gemv(dg->G.get(), dg->ld, v->x1.get(), level_beta(k), v->y.get(), n, nullptr, s);
+      else
+        m.apply(v->x1.get(), Epi::Axpby, a);
       launch_vc_pre(v->y.get(), v->dinv.get(), 1.0, v->e.get(), n, nullptr, s);  // D^-1 A v
       RMG_CK(cudaMemcpyAsync(h.data(), v->e.get(), n * 8, cudaMemcpyDeviceToHost, s));
       ctx_->sync();
@@ -2079,7 +2218,11 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
   a.out = v.y.get();
   a.beta = level_beta(k);
   a.done = done;
-  m.apply(v.x1.get(), Epi::Axpby, a, prof(k));
+  const DenseGram* dg = dgram(k);
+  if (dg != nullptr)
+    launch_gram_gemv(dg->G.get(), dg->ld, v.x1.get(), level_beta(k), v.y.get(), nf, done, s);
+  else
+    m.apply(v.x1.get(), Epi::Axpby, a, prof(k));
   launch_vc_sub(r, v.y.get(), nf, done, s);  // y = r - A x1
   const bool last = k + 1 == L;
   double* rc = last ? rc_last_.get() : work_[k + 1]->b.get();
@@ -2097,18 +2240,37 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
   launch_vc_add(v.x1.get(), v.e.get(), nf, done, s);  // e = x2
   a.v = v.e.get();
   a.out = v.y.get();
-  m.apply(v.e.get(), Epi::Axpby, a, prof(k));
+  if (dg != nullptr)
+    launch_gram_gemv(dg->G.get(), dg->ld, v.e.get(), level_beta(k), v.y.get(), nf, done, s);
+  else
+    m.apply(v.e.get(), Epi::Axpby, a, prof(k));
   launch_vc_post(v.e.get(), r, v.y.get(), v.dinv.get(), v.w, z, nf, done, s);
   ctx_->launches += 8;
 }
 
 bool Method::block_capable() const {
+  if (fine_->dense != nullptr || fine_->comm != nullptr) return false;
+  if (kind_ == RMG_METHOD_CG || kind_ == RMG_METHOD_JACOBI_CG) return true;
   if (kind_ != RMG_METHOD_PCG_VCYCLE || coarse_.empty()) return false;
-  for (size_t k = 0; k < coarse_.size(); ++k) {
+  for (size_t k = 1; k < coarse_.size(); ++k) {
+    if (dgram(k) != nullptr) continue;
     const Matrix& m = level_matrix(k);
     if (m.dense != nullptr || m.comm != nullptr) return false;
   }
   return true;
+}
+
+void Method::bprecond(const double* r, double* z, int k) {
+  cudaStream_t s = ctx_->stream;  // the capture stream while a graph is recorded
+  const int64_t n = fine_->f();
+  if (kind_ == RMG_METHOD_PCG_VCYCLE) {
+    bvcycle(0, r, z, k);
+  } else if (kind_ == RMG_METHOD_JACOBI_CG) {  // z = r * (1/d) (krylov.cpp:41-47)
+    launch_bvc_pre(r, inv_diag_.get(), 1.0, z, n, k, s);
+    ctx_->launches += 1;
+  } else {  // IdentityPreconditioner (krylov.cpp:34-39)
+    RMG_CK(cudaMemcpyAsync(z, r, static_cast<size_t>(n) * k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
 }
 
 // the V-cycle of vcycle() on k columns at once (row-major blocks; every operator
@@ -2132,8 +2294,15 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
     b.rc.alloc(nck);
     b.ec.alloc(nck);
   }
+  const DenseGram* dg = dgram(lv);
+  auto apply = [&](const double* in, double* out) {
+    if (dg != nullptr)
+      launch_gram_gemm(dg->G.get(), dg->ld, in, level_beta(lv), out, nf, k, s);
+    else
+      m.apply_block(in, out, level_beta(lv), k, false);
+  };
   launch_bvc_pre(r, v.dinv.get(), v.w, b.x1.get(), nf, k, s);
-  m.apply_block(b.x1.get(), b.y.get(), level_beta(lv), k, false);
+  apply(b.x1.get(), b.y.get());
   launch_bsub(r, b.y.get(), nf * k, s);
   launch_brestrict(c.mptr.get(), c.members.get(), c.weight.get(), b.y.get(), b.rc.get(), nc, k, s);
   if (lv + 1 == L)
@@ -2142,13 +2311,14 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
     bvcycle(lv + 1, b.rc.get(), b.ec.get(), k);
   launch_bprolong(c.label.get(), c.weight.get(), b.ec.get(), b.e.get(), nf, k, s);
   launch_badd(b.x1.get(), b.e.get(), nf * k, s);
-  m.apply_block(b.e.get(), b.y.get(), level_beta(lv), k, false);
+  apply(b.e.get(), b.y.get());
   launch_bvc_post(b.e.get(), r, b.y.get(), v.dinv.get(), v.w, z, nf, k, s);
   ctx_->launches += 10;
 }
 
 std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, int k) {
-  if (!block_capable()) throw InvalidArgument("solve_block: pcg_vcycle over single-GPU CSR levels only");
+  if (!block_capable())
+    throw InvalidArgument("solve_block: cg, jacobi_cg or pcg_vcycle over a single-GPU CSR matrix only");
   if (k < 1 || k > 64) throw InvalidArgument("solve_block: k must be in [1, 64]");
   RMG_CK(cudaSetDevice(ctx_->device));
   cudaStream_t s = ctx_->stream;
@@ -2185,7 +2355,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   RMG_CK(cudaMemcpyAsync(w.sc.get(), hs.data(), k * sizeof(BlockScalars), cudaMemcpyHostToDevice, s));
   launch_bnonfinite(w.r.get(), n, k, bad, s);
   launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, s);
-  bvcycle(0, w.r.get(), w.z.get(), k);
+  bprecond(w.r.get(), w.z.get(), k);
   launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, s);
   launch_bpcg_begin(w.sc.get(), rr, rz, bad, k, w.hist.get(), s);
   RMG_CK(cudaMemcpyAsync(w.p.get(), w.z.get(), nk * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -2198,13 +2368,14 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
     launch_bupdate_xr(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, cs);
     launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, cs);
     launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), cs);
-    bvcycle(0, w.r.get(), w.z.get(), k);
+    bprecond(w.r.get(), w.z.get(), k);
     launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
     launch_bpcg_beta(w.sc.get(), rz, k, cs);
     launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, cs);
     ctx_->launches += 12;
   };
   // the lock-step loop as a CUDA graph (§4.13): runs while any column runs
+  bool graph_used = false;
   if (std::getenv("RMG_NO_GRAPH") == nullptr) {
     if (!bw_graph_ || bw_graph_k_ != k) {
       bw_graph_.reset();
@@ -2219,7 +2390,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
     if (bw_graph_) {
       RMG_CK(cudaMemsetAsync(bw_graph_->passes.get(), 0, sizeof(unsigned long long), s));
       RMG_CK(cudaGraphLaunch(bw_graph_->exec, s));
-      ctx_->launches += bw_graph_->launches_per_iter;
+      graph_used = true;
     }
   }
   for (;;) {
@@ -2240,6 +2411,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   launch_brow2col(w.x.get(), w_cm, n, k, s);
   int32_t itmax = 0;
   for (const auto& e : hs) itmax = std::max(itmax, e.it);
+  if (graph_used) ctx_->launches += bw_graph_->launches_per_iter * static_cast<uint64_t>(std::max(1, itmax));
   std::vector<double> hist(static_cast<size_t>(itmax + 1) * k);
   if (!hist.empty())
     RMG_CK(cudaMemcpyAsync(hist.data(), w.hist.get(), hist.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

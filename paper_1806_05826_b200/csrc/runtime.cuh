@@ -201,11 +201,19 @@ struct Matrix {
   std::unique_ptr<HotXt> hot;  // hybrid X^T pass when N is large (nullptr otherwise)
   std::unique_ptr<DenseStore> dense;  // dense inputs: X row-major on the device, no CSR copies
   // block operator (cfg 3): schedule of the X^T pass over row-major F x k blocks
-  BlockXtSchedule bview;
-  DBuf<int32_t> bshort;
-  DBuf<int4> bitems, bmulti;
+  // one schedule per sample chunk: its X^T entry ranges, units and segments
+  struct BlockChunkBufs {
+    DBuf<int32_t> sh;
+    DBuf<int4> it, mu, u1, u2;  // + the TMA passes' units (K1 rows, X^T rows and items)
+  };
+  DBuf<int32_t> bx_idx;        // X as a row CSR for the TMA K1 (entries in column order)
+  DBuf<double> bx_val;
+  std::vector<BlockChunkBufs> bchunk_bufs;
+  std::vector<BlockXtSchedule> bviews;
+  DBuf<int32_t> bbounds;       // (chunks + 1) x F entry offsets into X^T
+  int64_t bchunk_rows = 0;
   DBuf<double> bseg, bt, bvp;  // + scratch T (N x k) and permuted V (F x k), kept across calls
-  void build_block_schedule(const HostCsr& ht);
+  void build_block_schedule(const HostCsr& x, const HostCsr& ht);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
@@ -383,6 +391,20 @@ class Method {
     DBuf<BlockScalars> sc;
   } bw_;
   void bvcycle(size_t lv, const double* r, double* z, int k);
+  // z = M r for k columns: the V-cycle, Jacobi (z = D^-1 r) or identity (cg)
+  void bprecond(const double* r, double* z, int k);
+  // pcg_vcycle: dense G_k = X_k^T X_k per level k >= 1 where n_k^2 doubles are
+  // fewer bytes than an X_k sweep pair; nullptr: sweep X_k
+  struct DenseGram {
+    DBuf<double> G;
+    int64_t n = 0, ld = 0;
+  };
+  std::vector<std::unique_ptr<DenseGram>> dg_;
+  bool dg_built_ = false;
+  void build_dense_grams();
+  const DenseGram* dgram(size_t k) const { return k < dg_.size() ? dg_[k].get() : nullptr; }
+  // G = X^T X of a level on the device (bit-identical to coarse_gram's sums)
+  void device_gram(Matrix& m, double* G, int64_t ld);
 
  public:
   // pcg_vcycle over single-GPU CSR levels: solve_batch runs the k columns in lock step

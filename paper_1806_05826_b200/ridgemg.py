@@ -548,6 +548,17 @@ class PreparedMethod:
         reports = [self._finish(arr[q], parts[q][1], parts[q][2]) for q in range(k)]
         return np.ascontiguousarray(wcol.T), reports
 
+    def solve_batch_device(self, b_ptr: int, w_ptr: int, k: int, on_device: bool = True) -> list:
+        """rmg_method_solve_batch on raw pointers: column-major b (n_samples x k) and
+        w (n_features x k) in device memory (on_device) or host memory."""
+        parts = [self._report() for _ in range(k)]
+        arr = (_lib.SolveReportC * max(1, k))()
+        for q, (rep, _, _) in enumerate(parts):
+            arr[q] = rep
+        _lib.check(self.lib.rmg_method_solve_batch(self.h, C.c_void_p(b_ptr), C.c_void_p(w_ptr), k, arr,
+                                                   int(on_device)))
+        return [self._finish(arr[q], parts[q][1], parts[q][2]) for q in range(k)]
+
     def solve_rhs(self, rhs) -> tuple[np.ndarray, SolveReport]:
         rhs = np.ascontiguousarray(rhs, np.float64)
         if rhs.shape != (self.x.n_features,):
