@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -125,8 +126,30 @@ void mul_t(const Csr& m, const double* u, double* y) {
   }
 }
 
+// Rounding-envelope diagnostics (never set by the tests' pinned
+// runs): ORC_DOT_TREE=1 sums dot products pairwise in blocks of 256 (the GPU's
+// order class), ORC_OMEGA_ULP=k moves every omega_k by k ulps, ORC_COARSE_INV=1
+// applies the coarsest level through its explicit inverse (the GPU's choice).
+int env_int(const char* name) {
+  const char* e = std::getenv(name);
+  return e == nullptr ? 0 : std::atoi(e);
+}
+
 // sparse.cpp:184-191
 double dotp(const double* a, const double* b, int64_t n) {
+  static const bool tree = env_int("ORC_DOT_TREE") != 0;
+  if (tree) {
+    double total = 0.0;
+    for (int64_t b0 = 0; b0 < n; b0 += 256) {
+      double part[256];
+      const int64_t m = std::min<int64_t>(256, n - b0);
+      for (int64_t i = 0; i < m; ++i) part[i] = a[b0 + i] * b[b0 + i];
+      for (int64_t w = 1; w < m; w *= 2)
+        for (int64_t i = 0; i + w < m; i += 2 * w) part[i] += part[i + w];
+      total += part[0];
+    }
+    return total;
+  }
   double s = 0.0;
   for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
@@ -288,7 +311,29 @@ struct Chol {
       }
     }
   }
+  Vec inv;  // ORC_COARSE_INV: explicit inverse (columns by the triangular solves below)
+  void make_inverse() {
+    inv.assign(n * n, 0.0);
+    Vec e(n), col(n);
+    for (int64_t j = 0; j < n; ++j) {
+      std::fill(e.begin(), e.end(), 0.0);
+      e[j] = 1.0;
+      solve_tri(e.data(), col.data());
+      for (int64_t i = 0; i < n; ++i) inv[i * n + j] = col[i];
+    }
+  }
   void solve(const double* b, double* x) const {
+    if (!inv.empty()) {
+      for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t j = 0; j < n; ++j) s += inv[i * n + j] * b[j];
+        x[i] = s;
+      }
+      return;
+    }
+    solve_tri(b, x);
+  }
+  void solve_tri(const double* b, double* x) const {
     Vec y(n);
     for (int64_t i = 0; i < n; ++i) {
       double s = b[i];
@@ -412,6 +457,7 @@ struct TwoLevel final : Precond {
           ac[xc.idx[a] * fc + xc.idx[b]] += xc.val[a] * xc.val[b];
     for (int64_t i = 0; i < fc; ++i) ac[i * fc + i] += coarse->beta;
     chol.factor(ac, fc);
+    if (env_int("ORC_COARSE_INV") != 0) chol.make_inverse();
   }
 
   uint64_t apply(const double* r, double* z) const override {
@@ -938,7 +984,10 @@ std::unique_ptr<Hierarchy> build(const Csr& x, double beta, const or_level_spec*
     bool cv;
     const double lmax = lambda_max(gram, 1e-4, 200, 0x5eed + k, &it, &cv);
     const double b = k == 0 ? beta : h->lv[k - 1]->beta;
-    h->omega.push_back(2.0 / (b + lmax));
+    double om = 2.0 / (b + lmax);
+    for (int u = env_int("ORC_OMEGA_ULP"), i = 0; i < std::abs(u); ++i)
+      om = std::nextafter(om, u > 0 ? 2.0 * om : 0.0);
+    h->omega.push_back(om);
   }
   h->pc.resize(n);
   for (size_t k = n; k-- > 0;) {
