@@ -26,6 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "oracle": (os.path.join(HERE, "_build", "libridgemg_oracle.so"), "orc_"),
     "ref": (os.path.join(HERE, "_ref", "libridgemg_ref.so"), "ref_"),
+    # rounding-envelope diagnostics only (FMA-contracted restatement, tests/golden/make_envelope.py)
+    "oracle_fma": (os.path.join(HERE, "_build", "libridgemg_oracle_fma.so"), "orc_"),
 }
 
 CLUSTER_LEADER_TOLERANCE, CLUSTER_LEADER_TARGET, CLUSTER_KMEANS = 0, 1, 2
@@ -78,7 +80,7 @@ class OracleError(RuntimeError):
 
 def build(kind: str = "oracle") -> str:
     """Compile a checker library with oracle/Makefile; returns its path."""
-    target = {"oracle": "oracle", "ref": "ref"}[kind]
+    target = {"oracle": "oracle", "ref": "ref", "oracle_fma": "oracle_fma"}[kind]
     subprocess.run(["make", "-s", "-C", HERE, target], check=True)
     return LIBS[kind][0]
 

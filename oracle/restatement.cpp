@@ -107,6 +107,11 @@ Csc transpose_of(const Csr& m) {
   return c;
 }
 
+int env_int(const char* name) {
+  const char* e = std::getenv(name);
+  return e == nullptr ? 0 : std::atoi(e);
+}
+
 // sparse.cpp:103-112 — per row, sequential in stored (increasing column) order
 void mul(const Csr& m, const double* v, double* y) {
   for (int64_t r = 0; r < m.n; ++r) {
@@ -118,6 +123,23 @@ void mul(const Csr& m, const double* v, double* y) {
 
 // sparse.cpp:152-158,114-123 — zero fill, then scatter rows in order, skipping u_r == 0
 void mul_t(const Csr& m, const double* u, double* y) {
+  // ORC_XT_SEG=s (envelope diagnostics): every column summed in row segments of s
+  // rows, the segment sums added in order (the GPU's segmented X^T pass class)
+  static const int64_t seg = env_int("ORC_XT_SEG");
+  if (seg > 0 && m.n > seg) {
+    std::fill(y, y + m.f, 0.0);
+    Vec part(m.f);
+    for (int64_t r0 = 0; r0 < m.n; r0 += seg) {
+      std::fill(part.begin(), part.end(), 0.0);
+      for (int64_t r = r0; r < std::min(m.n, r0 + seg); ++r) {
+        const double ur = u[r];
+        if (ur == 0.0) continue;
+        for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) part[m.idx[k]] += m.val[k] * ur;
+      }
+      for (int64_t j = 0; j < m.f; ++j) y[j] += part[j];
+    }
+    return;
+  }
   std::fill(y, y + m.f, 0.0);
   for (int64_t r = 0; r < m.n; ++r) {
     const double ur = u[r];
@@ -130,14 +152,17 @@ void mul_t(const Csr& m, const double* u, double* y) {
 // runs): ORC_DOT_TREE=1 sums dot products pairwise in blocks of 256 (the GPU's
 // order class), ORC_OMEGA_ULP=k moves every omega_k by k ulps, ORC_COARSE_INV=1
 // applies the coarsest level through its explicit inverse (the GPU's choice).
-int env_int(const char* name) {
-  const char* e = std::getenv(name);
-  return e == nullptr ? 0 : std::atoi(e);
-}
 
 // sparse.cpp:184-191
 double dotp(const double* a, const double* b, int64_t n) {
-  static const bool tree = env_int("ORC_DOT_TREE") != 0;
+  static const int tree = env_int("ORC_DOT_TREE");
+  if (tree == 2) {  // fully pairwise (the GPU's grid reduction is of this accuracy class)
+    std::vector<double> part(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) part[i] = a[i] * b[i];
+    for (int64_t w = 1; w < n; w *= 2)
+      for (int64_t i = 0; i + w < n; i += 2 * w) part[i] += part[i + w];
+    return n > 0 ? part[0] : 0.0;
+  }
   if (tree) {
     double total = 0.0;
     for (int64_t b0 = 0; b0 < n; b0 += 256) {

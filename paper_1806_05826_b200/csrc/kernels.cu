@@ -375,19 +375,31 @@ __device__ __forceinline__ double ldv_f64(const double* p) {
 // coalesced access (2 lines per warp instruction), and each lane sums its
 // column in the row's element order (the single-vector K1's order).  A warp
 // walks its SELL slice two rows at a time; element loads run 4 ahead.
-template <bool PAT, bool NARROW>
-__global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __restrict__ off,
+// HOT: the n_hot most popular labels' V rows (relabeled columns: labels in
+// descending popularity, ~2/3 of the gathers on cfg 3) are staged once per
+// persistent CTA in shared memory; only the rest is gathered from L1 / L2.
+template <bool PAT, bool NARROW, bool HOT>
+__global__ void __launch_bounds__(HOT ? 512 : kThreads, HOT ? 1 : 3) k_spmm_sell(const int32_t* __restrict__ off,
                                                         const int32_t* __restrict__ srow,
                                                         const int32_t* __restrict__ slen,
                                                         const int32_t* __restrict__ idx,
                                                         const uint16_t* __restrict__ idx16,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ V, double* __restrict__ T,
-                                                        int64_t slice0, int64_t n_slices, int k, int c0, int kc) {
+                                                        int64_t slice0, int64_t n_slices, int k, int c0, int kc,
+                                                        int n_hot) {
+  extern __shared__ double vs[];
   const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
   const bool colq = q < kc;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-  for (int64_t sl = slice0 + (((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5); sl < slice0 + n_slices;
+  if (HOT) {
+    for (int e = threadIdx.x; e < n_hot * 16; e += blockDim.x) {
+      const int r = e >> 4, cq = e & 15;
+      vs[e] = cq < kc ? __ldg(V + (int64_t)r * k + c0 + cq) : 0.0;
+    }
+    __syncthreads();
+  }
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = slice0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); sl < slice0 + n_slices;
        sl += nwarps) {
     const int64_t base = off[sl];
     for (int p = 0; p < 16; ++p) {
@@ -425,7 +437,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmm_sell(const int32_t* __rest
           x[u] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xq, src0 | u);
         }
 #pragma unroll
-        for (int u = 0; u < 16; ++u) vv[u] = __ldg(V + (int64_t)(c[u] < 0 ? 0 : c[u]) * k + c0 + qq);
+        for (int u = 0; u < 16; ++u)
+          vv[u] = (HOT && c[u] < n_hot) ? vs[(c[u] < 0 ? 0 : c[u]) * 16 + qq]
+                                        : __ldg(V + (int64_t)(c[u] < 0 ? 0 : c[u]) * k + c0 + qq);
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const double add = acc + (PAT ? vv[u] : x[u] * vv[u]);
@@ -2084,6 +2098,29 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
 }
 
 
+// RMG_BLOCK_HOT: V rows kept in shared memory by the K1 pass (0 disables)
+int64_t block_hot_rows() {
+  static int64_t rows = -1;
+  if (rows < 0) {
+    const char* e = std::getenv("RMG_BLOCK_HOT");
+    rows = e != nullptr ? std::max<int64_t>(0, std::atoll(e)) : 0;  // measured slower on cfg 3
+    rows = std::min<int64_t>(rows, 1700);  // <= 212 KB of shared memory
+  }
+  return rows;
+}
+
+template <bool PAT, bool NARROW>
+void spmm_hot(int grid, size_t smem, cudaStream_t s, const SparseDev& x, const double* vk, double* t,
+              const BlockXtSchedule& bs, int k, int c0, int kc, int n_hot) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmm_sell<PAT, NARROW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1700 * 128);
+    attr = true;
+  }
+  k_spmm_sell<PAT, NARROW, true><<<grid, 512, smem, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
+                                                         t, bs.slice0, bs.n_slices, k, c0, kc, n_hot);
+}
+
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
                         const double* v, double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
@@ -2119,20 +2156,41 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
       const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
       if (bs.n_slices > 0) {
-        if (x.val == nullptr) {
+        // hot V rows in shared memory when the columns are relabeled by popularity
+        const int n_hot = x.col_inv != nullptr ? static_cast<int>(std::min<int64_t>(x.cols, block_hot_rows())) : 0;
+        const size_t hsm = static_cast<size_t>(n_hot) * 16 * sizeof(double);
+        if (n_hot > 0) {
+          int sms = 148;
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+          const int gh = static_cast<int>(std::min<int64_t>(sms, (bs.n_slices + 15) / 16));
+          if (x.val == nullptr) {
+            if (x.idx16 != nullptr)
+              spmm_hot<true, true>(gh, hsm, s, x, vk, t, bs, k, c0, kc, n_hot);
+            else
+              spmm_hot<true, false>(gh, hsm, s, x, vk, t, bs, k, c0, kc, n_hot);
+          } else {
+            if (x.idx16 != nullptr)
+              spmm_hot<false, true>(gh, hsm, s, x, vk, t, bs, k, c0, kc, n_hot);
+            else
+              spmm_hot<false, false>(gh, hsm, s, x, vk, t, bs, k, c0, kc, n_hot);
+          }
+        } else if (x.val == nullptr) {
           if (x.idx16 != nullptr)
-            k_spmm_sell<true, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val,
-                                                            vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+            k_spmm_sell<true, true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
+                                                                   x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc, 0);
           else
-            k_spmm_sell<true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
-                                                             x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+            k_spmm_sell<true, false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
+                                                                    x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
+                                                                    c0, kc, 0);
         } else {
           if (x.idx16 != nullptr)
-            k_spmm_sell<false, true><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
-                                                             x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+            k_spmm_sell<false, true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
+                                                                    x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
+                                                                    c0, kc, 0);
           else
-            k_spmm_sell<false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
-                                                              x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc);
+            k_spmm_sell<false, false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
+                                                                     x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
+                                                                     c0, kc, 0);
         }
       }
       if (units > 0) {
