@@ -189,8 +189,28 @@ int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_
 int rmg_matrix_create_dense_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t n_features,
                                     const void* data, uint64_t ld, int32_t fp32, rmg_matrix** out);
 int rmg_comm_destroy(rmg_comm* comm);
-/* Every rank passes the FULL matrix (needed for the replicated hierarchy setup);
- * only this rank's row block is uploaded. */
+/* A host-staged communicator: every all-reduce copies the vector to pinned host
+ * memory, calls fn(user, buf, count) -- which must replace buf by the sum over
+ * all ranks, in rank order, and return 0 -- and copies it back.  For several
+ * ranks on ONE device (NCCL refuses duplicate devices): tests and single-GPU
+ * rehearsals of the sharded path (e.g. fn = a gloo all-reduce). */
+typedef int (*rmg_host_allreduce_fn)(void* user, double* buf, uint64_t count);
+int rmg_comm_create_host(rmg_context* ctx, int32_t nranks, int32_t rank, rmg_host_allreduce_fn fn, void* user,
+                         rmg_comm** out);
+/* Per-rank input (no rank needs the whole matrix): this rank's contiguous block of
+ * rows [row0, row0 + n_local) of an n_samples x n_features X, row offsets rebased
+ * to 0 (n_local + 1 entries).  Blocks must tile [0, n_samples) in rank order.
+ * Hierarchy setup on such a matrix is sharded too: coarse levels X_k = X P are
+ * coarsened row-locally (X_k keeps the same row blocks), their Gram matrices and
+ * Jacobi diagonals are all-reduced, and clustering must be kmeans_sketch (the
+ * sketch S = G^T X is all-reduced) or imported labels. */
+int rmg_matrix_create_csr_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t row0,
+                               uint64_t n_local, uint64_t n_features, const uint64_t* row_offsets,
+                               const uint64_t* column_indices, const double* values, int32_t detect_pattern,
+                               rmg_matrix** out);
+/* Replicated-setup variant: every rank passes the FULL matrix (the hierarchy is then
+ * built unsharded on every rank); only this rank's nnz-balanced row block is
+ * uploaded. */
 int rmg_matrix_create_csr_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t n_features,
                                   const uint64_t* row_offsets, const uint64_t* column_indices,
                                   const double* values, int32_t detect_pattern, rmg_matrix** out);
@@ -221,6 +241,11 @@ int rmg_synth_sparse_zipf(uint64_t n, uint64_t f, double mean_nnz, double zipf_s
  * (large measurement shards, e.g. cfg5 per-GPU); not the reference's stream */
 int rmg_synth_sparse_zipf_rows(uint64_t n, uint64_t f, double mean_nnz, double zipf_s, int32_t abs_normal_values,
                                uint64_t seed, rmg_host_csr** out, uint64_t* nnz);
+/* Rows [row0, row1) of the matrix rmg_synth_sparse_zipf_rows generates (the same
+ * bytes): per-rank generation of a row-sharded input. */
+int rmg_synth_sparse_zipf_row_range(uint64_t n, uint64_t f, double mean_nnz, double zipf_s,
+                                    int32_t abs_normal_values, uint64_t seed, uint64_t row0, uint64_t row1,
+                                    rmg_host_csr** out, uint64_t* nnz);
 int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* row_offsets, uint64_t* column_indices, double* values);
 int rmg_host_csr_destroy(rmg_host_csr* h);
 

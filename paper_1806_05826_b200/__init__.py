@@ -12,6 +12,7 @@ from .ridgemg import (  # noqa: F401
     LEADER_TARGET, LEADER_TOLERANCE, ClusteringChoice, CoarseSolveChoice, Comm, Context, DeviceMatrix, FeatureMatrix,
     LevelSpec, MethodSpec, PreparedMethod, RhsSample, SolveReport, SolverConfig, SystemSolution, csr_from_triplets,
     default_context, from_dense, generate_rhs, method_from_string, read_matrix_market, rng_normals, shard_rows,
-    solve_system, synth_dense_clustered, synth_sparse_zipf, BenchRow, compare_methods, to_csv, clustering_description)
+    solve_system, synth_dense_clustered, synth_sparse_zipf, synth_sparse_zipf_row_range, BenchRow, compare_methods,
+    to_csv, clustering_description)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

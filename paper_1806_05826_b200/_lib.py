@@ -107,6 +107,9 @@ SIGNATURES = {
     "rmg_comm_unique_id": [_P],
     "rmg_comm_create": [_P, _I32, _I32, _P, _PP],
     "rmg_comm_destroy": [_P],
+    "rmg_comm_create_host": [_P, _I32, _I32, _P, _P, _PP],
+    "rmg_matrix_create_csr_rows": [_P, _P, _U64, _U64, _U64, _U64, _P, _P, _P, _I32, _PP],
+    "rmg_synth_sparse_zipf_row_range": [_U64, _U64, _D, _D, _I32, _U64, _U64, _U64, _PP, _P],
     "rmg_matrix_create_csr_sharded": [_P, _P, _U64, _U64, _P, _P, _P, _I32, _PP],
     "rmg_matrix_shard": [_P, _P, _P, _P, _P],
     "rmg_shard_rows": [_P, _U64, _I32, _P],

@@ -22,6 +22,8 @@ struct rmg_matrix {
              const rmg::DenseInput* din = nullptr)
       : m(ctx, std::move(h), detect, comm, din) {}
   rmg_matrix(rmg::Context* ctx, int64_t n, int64_t f, const rmg::DenseInput& din) : m(ctx, n, f, din) {}
+  rmg_matrix(rmg::Context* ctx, rmg::HostCsr local, int64_t n_global, int64_t row0, bool detect, rmg::Comm* comm)
+      : m(ctx, std::move(local), n_global, row0, detect, comm) {}
 };
 struct rmg_host_csr {
   rmg::HostCsr h;
@@ -29,6 +31,7 @@ struct rmg_host_csr {
 struct rmg_comm {
   rmg::Comm c;
   rmg_comm(int nranks, int rank, const ncclUniqueId& id, int device) : c(nranks, rank, id, device) {}
+  rmg_comm(int nranks, int rank, rmg_host_allreduce_fn fn, void* user) : c(nranks, rank, fn, user) {}
 };
 struct rmg_method {
   rmg::Method m;
@@ -275,8 +278,41 @@ int rmg_comm_create(rmg_context* ctx, int32_t nranks, int32_t rank, const uint8_
   });
 }
 
+int rmg_comm_create_host(rmg_context* ctx, int32_t nranks, int32_t rank, rmg_host_allreduce_fn fn, void* user,
+                         rmg_comm** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    *out = new rmg_comm(nranks, rank, fn, user);
+  });
+}
+
 int rmg_comm_destroy(rmg_comm* comm) {
   return guard([&] { delete comm; });
+}
+
+int rmg_matrix_create_csr_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n, uint64_t row0, uint64_t n_local,
+                               uint64_t f, const uint64_t* rp, const uint64_t* ci, const double* values,
+                               int32_t detect_pattern, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
+    need(comm, "comm");
+    need(out, "out");
+    need(rp, "row_offsets");
+    if (rp[0] != 0) throw rmg::InvalidArgument("rmg_matrix_create_csr_rows: row offsets must be rebased to 0");
+    rmg::HostCsr h;
+    h.n = static_cast<int64_t>(n_local);
+    h.f = static_cast<int64_t>(f);
+    h.ptr.assign(rp, rp + n_local + 1);
+    const uint64_t nnz = rp[n_local];
+    if (nnz) need(ci, "column_indices");
+    h.idx.assign(ci, ci + nnz);
+    if (values) h.val.assign(values, values + nnz);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, std::move(h), static_cast<int64_t>(n), static_cast<int64_t>(row0),
+                          detect_pattern != 0, &comm->c);
+  });
 }
 
 int rmg_matrix_create_csr_sharded(rmg_context* ctx, rmg_comm* comm, uint64_t n, uint64_t f, const uint64_t* rp,
@@ -503,6 +539,19 @@ int rmg_synth_sparse_zipf_rows(uint64_t n, uint64_t f, double mean_nnz, double z
     need(out, "out");
     auto* h = new rmg_host_csr{rmg::synth_sparse_zipf_rows(static_cast<int64_t>(n), static_cast<int64_t>(f),
                                                            mean_nnz, zipf_s, abs_normal_values != 0, seed)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+  });
+}
+
+int rmg_synth_sparse_zipf_row_range(uint64_t n, uint64_t f, double mean_nnz, double zipf_s,
+                                    int32_t abs_normal_values, uint64_t seed, uint64_t row0, uint64_t row1,
+                                    rmg_host_csr** out, uint64_t* nnz) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new rmg_host_csr{rmg::synth_sparse_zipf_rows(static_cast<int64_t>(n), static_cast<int64_t>(f), mean_nnz,
+                                                           zipf_s, abs_normal_values != 0, seed,
+                                                           static_cast<int64_t>(row0), static_cast<int64_t>(row1))};
     *out = h;
     if (nnz) *nnz = h->h.nnz();
   });

@@ -373,7 +373,7 @@ __device__ __forceinline__ bool sketch_negative(uint64_t seed, int64_t r, int c,
 // nonzeros (increasing sample order) of +-x (x / norm_j when normalising)
 __global__ void k_sketch_sparse(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                 const double* __restrict__ val, int64_t f, const double* __restrict__ norm, int d,
-                                uint64_t seed, double* __restrict__ S, int64_t ldS) {
+                                uint64_t seed, double* __restrict__ S, int64_t ldS, int64_t row0) {
   const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int c = threadIdx.x & 31;
   if (j >= f || c >= d) return;
@@ -382,7 +382,7 @@ __global__ void k_sketch_sparse(const int32_t* __restrict__ ptr, const int32_t* 
   for (int32_t q = ptr[j]; q < ptr[j + 1]; ++q) {
     double x = val != nullptr ? val[q] : 1.0;
     if (norm != nullptr) x = __ddiv_rn(x, nj);
-    acc = __dadd_rn(acc, sketch_negative(seed, idx[q], c, d) ? -x : x);
+    acc = __dadd_rn(acc, sketch_negative(seed, row0 + idx[q], c, d) ? -x : x);
   }
   S[c * ldS + j] = acc;
 }
@@ -406,12 +406,12 @@ __global__ void k_transpose_st(const double* st, int64_t f, int d, double* S, in
 }  // namespace
 
 void sketch_sparse_gpu(cudaStream_t s, const SparseDev& xt, const double* norm, int d, uint64_t seed, double* S,
-                       int64_t ldS) {
+                       int64_t ldS, int64_t row0) {
   if (d < 1 || d > 32) throw InvalidArgument("kmeans_sketch: sketch dimension outside [1, 32]");
   const int64_t f = xt.rows;
   if (f > 0) {
     k_sketch_sparse<<<static_cast<unsigned>((f * 32 + kT - 1) / kT), kT, 0, s>>>(xt.ptr, xt.idx, xt.val, f, norm, d,
-                                                                                   seed, S, ldS);
+                                                                                   seed, S, ldS, row0);
     RMG_CK(cudaGetLastError());
   }
   RMG_CK(cudaStreamSynchronize(s));

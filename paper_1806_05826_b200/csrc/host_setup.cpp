@@ -645,9 +645,12 @@ HostCsr synth_sparse_zipf(int64_t n, int64_t f, double mean_nnz, double zipf_s, 
 
 // Same distribution with one RNG stream per row (seeded from (seed, row)), so
 // rows are generated by all host threads: large measurement shards (cfg5).
-HostCsr synth_sparse_zipf_rows(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
-                               uint64_t seed) {
-  if (n <= 0 || f <= 0 || !(mean_nnz > 0.0)) throw InvalidArgument("synth_sparse_zipf: bad shape");
+HostCsr synth_sparse_zipf_rows(int64_t n_total, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
+                               uint64_t seed, int64_t row0, int64_t row1) {
+  if (row1 < 0) row1 = n_total;
+  if (n_total <= 0 || f <= 0 || !(mean_nnz > 0.0)) throw InvalidArgument("synth_sparse_zipf: bad shape");
+  if (row0 < 0 || row1 > n_total || row0 > row1) throw InvalidArgument("synth_sparse_zipf: row range outside [0, n)");
+  const int64_t n = row1 - row0;  // rows [row0, row1) of the n_total-row matrix
   CounterRng table_rng(seed);
   const ZipfTable z(f, zipf_s, table_rng);
   const int64_t T = std::max<int64_t>(1, std::min<int64_t>(64, std::thread::hardware_concurrency()));
@@ -662,7 +665,7 @@ HostCsr synth_sparse_zipf_rows(int64_t n, int64_t f, double mean_nnz, double zip
       const int64_t r0 = t * chunk, r1 = std::min(n, r0 + chunk);
       if (r0 >= r1) return;
       idx[t].reserve(static_cast<size_t>((r1 - r0) * mean_nnz * 1.05));
-      for (int64_t r = r0; r < r1; ++r) {
+      for (int64_t r = r0 + row0; r < r1 + row0; ++r) {  // global row numbers seed the streams
         uint64_t h = seed ^ (static_cast<uint64_t>(r) + 1) * 0xD1B54A32D192ED03ull;
         h = (h ^ (h >> 33)) * 0xFF51AFD7ED558CCDull;
         CounterRng rng(h ^ (h >> 29));

@@ -87,7 +87,8 @@ HostCsr synth_dense_clustered(int64_t n, int64_t f, int64_t groups, double noise
 HostCsr synth_sparse_zipf(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
                           uint64_t seed);
 // Same distribution, one RNG stream per row (threaded): large measurement shards.
+// rows [row0, row1) only (row1 < 0: all): per-rank generation of a row-sharded input
 HostCsr synth_sparse_zipf_rows(int64_t n, int64_t f, double mean_nnz, double zipf_s, bool abs_normal_values,
-                               uint64_t seed);
+                               uint64_t seed, int64_t row0 = 0, int64_t row1 = -1);
 
 }  // namespace rmg

@@ -411,8 +411,36 @@ Comm::Comm(int nr, int r, const ncclUniqueId& id, int device) : nranks(nr), rank
   if (e != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(e));
 }
 
+Comm::Comm(int nr, int r, HostAllreduceFn fn, void* user) : nranks(nr), rank(r), host_fn(fn), host_user(user) {
+  if (nr < 1 || r < 0 || r >= nr) throw InvalidArgument("rmg_comm_create: rank outside [0, nranks)");
+  if (fn == nullptr) throw InvalidArgument("rmg_comm_create_host: null all-reduce function");
+}
+
 Comm::~Comm() {
   if (comm) ncclCommDestroy(comm);
+  if (pinned) cudaFreeHost(pinned);
+}
+
+void Comm::allreduce(const double* send, double* recv, int64_t count, cudaStream_t s) {
+  if (count <= 0) return;
+  if (host_fn == nullptr) {
+    const ncclResult_t e =
+        ncclAllReduce(send, recv, static_cast<size_t>(count), ncclDouble, ncclSum, comm, s);
+    if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+    return;
+  }
+  if (pinned_n < static_cast<size_t>(count)) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    RMG_CK(cudaMallocHost(&pinned, static_cast<size_t>(count) * sizeof(double)));
+    pinned_n = static_cast<size_t>(count);
+  }
+  RMG_CK(cudaMemcpyAsync(pinned, send, static_cast<size_t>(count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RMG_CK(cudaStreamSynchronize(s));
+  if (host_fn(host_user, pinned, static_cast<uint64_t>(count)) != 0)
+    throw RuntimeError("host all-reduce callback failed");
+  RMG_CK(cudaMemcpyAsync(recv, pinned, static_cast<size_t>(count) * sizeof(double), cudaMemcpyHostToDevice, s));
+  RMG_CK(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next call
 }
 
 std::vector<int64_t> partition_rows(const std::vector<int64_t>& rp, int nranks) {
@@ -429,9 +457,7 @@ std::vector<int64_t> partition_rows(const std::vector<int64_t>& rp, int nranks) 
 }
 
 void Matrix::allreduce_sums(double* sendbuf, double* recvbuf, int64_t count) {
-  const ncclResult_t e = ncclAllReduce(sendbuf, recvbuf, static_cast<size_t>(count), ncclDouble, ncclSum, comm->comm,
-                                       ctx->stream);
-  if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+  comm->allreduce(sendbuf, recvbuf, count, ctx->stream);
 }
 
 // Hybrid X^T pass.  Sample blocks: a multiple of 2 x 148
@@ -842,8 +868,6 @@ const HostCsr& Matrix::host_csr() {
 Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din)
     : ctx(c), host(std::move(h)), comm(cm) {
   validate_csr(host);
-  if (host.n > INT32_MAX || host.f > INT32_MAX || host.nnz() > INT32_MAX)
-    throw InvalidArgument("FeatureMatrix: dimensions exceed the single-device int32 index range");
   pattern = host.val.empty();
   if (!pattern && detect_pattern)
     pattern = std::all_of(host.val.begin(), host.val.end(), [](double v) { return v == 1.0; });
@@ -862,20 +886,51 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
     for (int64_t i = 0; i <= shard.n; ++i) shard.ptr[i] = host.ptr[row0 + i] - host.ptr[row0];
     shard.idx.assign(host.idx.begin() + host.ptr[row0], host.idx.begin() + host.ptr[row1]);
     shard.val.assign(host.val.begin() + host.ptr[row0], host.val.begin() + host.ptr[row1]);
-    part.alloc(std::max<int64_t>(1, host.f));
-    red.alloc(std::max<int64_t>(1, std::max(host.f, host.n)));
-    fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (host.f + 255) / 256)));
-    fin_slots.alloc(static_cast<size_t>(fin_grid) * 2);
-    fin_ticket.alloc(1);
-    RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
   }
   const HostCsr& local = comm != nullptr ? shard : host;
   if (din != nullptr) {  // dense X: one row-major device copy, fused single-sweep operator
     if (din->ld < host.f) throw InvalidArgument("dense X: leading dimension below the feature count");
+    if (comm != nullptr) alloc_comm_buffers();
     const char* src = static_cast<const char*>(din->data) + static_cast<size_t>(row0) * din->ld * (din->fp32 ? 4 : 8);
     init_dense_from_host(src, din->fp32, din->ld, local.n);
     return;
   }
+  init_sparse(local);
+}
+
+Matrix::Matrix(Context* c, HostCsr local, int64_t n_glob, int64_t r0, bool detect_pattern, Comm* cm)
+    : ctx(c), host(std::move(local)), comm(cm) {
+  validate_csr(host);
+  if (comm == nullptr) throw InvalidArgument("rmg_matrix_create_csr_rows: needs a communicator");
+  if (r0 < 0 || n_glob < 0 || r0 + host.n > n_glob)
+    throw InvalidArgument("rmg_matrix_create_csr_rows: rows [row0, row0 + n_local) outside [0, n_samples)");
+  n_global = n_glob;
+  rows_only = true;
+  row0 = r0;
+  row1 = r0 + host.n;
+  pattern = host.val.empty();
+  if (!pattern && detect_pattern)
+    pattern = std::all_of(host.val.begin(), host.val.end(), [](double v) { return v == 1.0; });
+  if (host.val.empty()) host.val.assign(host.nnz(), 1.0);
+  RMG_CK(cudaSetDevice(ctx->device));
+  init_sparse(host);
+}
+
+void Matrix::alloc_comm_buffers() {
+  part.alloc(std::max<int64_t>(1, host.f));
+  red.alloc(std::max<int64_t>(1, std::max(host.f, n())));
+  fin_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (host.f + 255) / 256)));
+  fin_slots.alloc(static_cast<size_t>(fin_grid) * 2);
+  fin_ticket.alloc(1);
+  RMG_CK(cudaMemsetAsync(fin_ticket.get(), 0, sizeof(unsigned), ctx->stream));
+}
+
+// the device copies of this rank's rows (the whole matrix when unsharded)
+void Matrix::init_sparse(const HostCsr& local) {
+  // the device index range is int32: checked on the rows this device holds
+  if (local.n > INT32_MAX || local.f > INT32_MAX || local.nnz() > INT32_MAX)
+    throw InvalidArgument("FeatureMatrix: dimensions exceed the single-device int32 index range");
+  if (comm != nullptr) alloc_comm_buffers();
   // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
   // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
   const char* rl = std::getenv("RMG_RELABEL");
@@ -1252,11 +1307,18 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       lab = std::move(c.labels);
     } else if (cs.clustering_kind == RMG_CLUSTER_KMEANS_SKETCH) {
       lab = sketch_clustering(curm, cs, &nc);
-    } else if (dev && cs.clustering_kind == RMG_CLUSTER_IMPORTED) {
+    } else if ((dev || curm.rows_only) && cs.clustering_kind == RMG_CLUSTER_IMPORTED) {
       if (static_cast<int64_t>(specs_[k].labels.size()) != cur_f)
         throw InvalidArgument("imported labels: expected one label per feature of the level");
       nc = static_cast<int64_t>(cs.n_clusters);
+      if (nc < 1 || nc > cur_f) throw InvalidArgument("imported labels: n_clusters outside [1, F]");
+      for (int64_t v : specs_[k].labels)
+        if (v < 0 || v >= nc) throw InvalidArgument("imported labels: label outside [0, n_clusters)");
       lab = specs_[k].labels;
+    } else if (curm.rows_only) {  // every rank holds only its rows: no exact column clustering
+      throw InvalidArgument(
+          "build_hierarchy: a row-sharded matrix (rmg_matrix_create_csr_rows) needs kmeans_sketch or imported "
+          "labels; exact k-means / leader-follower need every row of a column on one device");
     } else {
       lab = run_clustering(curm.host_csr(), specs_[k], &nc, s);
     }
@@ -1272,6 +1334,9 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       DBuf<char> xcd(std::max<size_t>(1, static_cast<size_t>(curm.n()) * ldc * sizeof(double)));
       coarsen_dense_gpu(s, curm.dense->view, lvl->agg, reinterpret_cast<double*>(xcd.get()), ldc);
       lvl->mat = std::make_unique<Matrix>(ctx_, curm.n(), nc, std::move(xcd), 0, ldc);
+    } else if (curm.rows_only) {  // X_k = X P is row-local: every rank coarsens its own rows
+      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(curm.host_csr(), lvl->agg), curm.n_global, curm.row0, true,
+                                          curm.comm);
     } else {
       lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(curm.host_csr(), lvl->agg), true);
     }
@@ -1361,7 +1426,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
 // (kmeans_dense_gpu, bit-identical arithmetic) on S = G^T X, G an N x d sign
 // matrix, the columns of X unit-normalised first when asked.
 std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc) {
-  if (m.comm != nullptr) throw InvalidArgument("kmeans_sketch: unsharded matrices only");
+  if (m.comm != nullptr && m.dense != nullptr) throw InvalidArgument("kmeans_sketch: sharded dense matrices unsupported");
   const int64_t f = m.f(), n = m.n();
   const int64_t k = static_cast<int64_t>(cs.target_size);
   if (k < 1 || k > f) throw InvalidArgument("kmeans: k outside [1, F]");
@@ -1378,17 +1443,19 @@ std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& 
     sketch_dense_gpu(s, xc.get(), n, f, ldx, d, cs.seed, S.get(), ldS);
   } else {
     DBuf<double> nrm;
-    if (cs.normalize_columns) {  // normalized_columns (host_setup.cpp:79-90): row order per column
-      const HostCsr& h = m.host_csr();
-      std::vector<double> v(f, 0.0);
-      for (int64_t q = 0; q < h.nnz(); ++q) {
-        const double x = h.val.empty() ? 1.0 : h.val[q];
-        v[h.idx[q]] += x * x;
-      }
+    if (cs.normalize_columns) {  // normalized_columns (host_setup.cpp:79-90): sum of squares per column
+      // in row order = gram_diagonal(0) (ridge.cpp:30-37, same order); sharded: summed over ranks
+      nrm.alloc(std::max<int64_t>(1, f));
+      m.gram_diagonal(0.0, nrm.get());
+      std::vector<double> v(f);
+      if (f) RMG_CK(cudaMemcpyAsync(v.data(), nrm.get(), f * 8, cudaMemcpyDeviceToHost, s));
+      ctx_->sync();
       for (double& e : v) e = std::sqrt(e);
       nrm.upload(v.data(), v.size(), s);
     }
-    sketch_sparse_gpu(s, m.xt.view, nrm.get(), d, cs.seed, S.get(), ldS);
+    // S over this device's rows (global row numbers seed the signs); sharded: summed over ranks
+    sketch_sparse_gpu(s, m.xt.view, nrm.get(), d, cs.seed, S.get(), ldS, m.row0);
+    if (m.comm != nullptr) m.allreduce_sums(S.get(), S.get(), static_cast<int64_t>(d) * ldS);
   }
   Clustering c = kmeans_dense_gpu(s, S.get(), d, f, ldS, k, cs.kmeans_max_iters, cs.seed);
   *nc = c.n_clusters;
@@ -1403,11 +1470,14 @@ std::vector<double> Method::level_gram(Matrix& m, double beta) {
   if (m.gram_cache.empty()) {
     if (m.device_setup()) {
       m.gram_cache = gram_dense_gpu(ctx_->stream, m.dense->view);
-    } else if (m.comm != nullptr || m.dense != nullptr || std::getenv("RMG_HOST_GRAM") != nullptr) {
+    } else if ((m.comm != nullptr && !m.rows_only) || m.dense != nullptr ||
+               (std::getenv("RMG_HOST_GRAM") != nullptr && m.comm == nullptr)) {
       return coarse_gram(m.host_csr(), beta);
-    } else {  // sparse level: the same sums on the device (dense_gram.cu), bit-identical
+    } else {  // sparse level: the same sums on the device (dense_gram.cu), bit-identical;
+              // row-sharded: every rank's rows, then summed over the ranks
       DBuf<double> g(static_cast<size_t>(std::max<int64_t>(1, n)) * std::max<int64_t>(1, n));
       device_gram(m, g.get(), n);
+      if (m.comm != nullptr) m.allreduce_sums(g.get(), g.get(), n * n);
       m.gram_cache.resize(static_cast<size_t>(n) * n);
       if (n) RMG_CK(cudaMemcpyAsync(m.gram_cache.data(), g.get(), m.gram_cache.size() * 8, cudaMemcpyDeviceToHost,
                                     ctx_->stream));
@@ -1432,6 +1502,8 @@ void Method::device_gram(Matrix& m, double* G, int64_t ld) {
     ctx_->sync();
     return;
   }
+  if (m.comm != nullptr && !m.rows_only)
+    throw InvalidArgument("device Gram: replicated-setup sharded matrices keep the host Gram");
   const HostCsr& h = m.host_csr();
   DBuf<int32_t> xp, xi;
   DBuf<double> xv;
@@ -1457,7 +1529,7 @@ void Method::build_dense_grams() {
   if (e != nullptr && std::string(e) == "0") return;
   for (size_t k = 1; k < coarse_.size(); ++k) {
     Matrix& m = level_matrix(k);
-    if (m.comm != nullptr) continue;
+    if (m.comm != nullptr && !m.rows_only) continue;
     const int64_t n = m.f();
     const double dense_bytes = 8.0 * static_cast<double>(n) * static_cast<double>(n);
     const double sweep_bytes = m.dense != nullptr ? static_cast<double>(m.n()) * n * 8.0
@@ -1470,6 +1542,7 @@ void Method::build_dense_grams() {
     d->ld = (n + 1) / 2 * 2;
     d->G.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * d->ld);
     device_gram(m, d->G.get(), d->ld);
+    if (m.comm != nullptr) m.allreduce_sums(d->G.get(), d->G.get(), n * d->ld);  // replicated G_k
     dg_[k] = std::move(d);
   }
 }

@@ -132,11 +132,23 @@ struct OpProfile {
 };
 
 // NCCL communicator over the GPUs of one node (one process per GPU).
+// Sums over ranks: NCCL over NVLink, or host-staged (several ranks on one device,
+// where NCCL refuses duplicate devices): the vector is copied to pinned host
+// memory, `host_fn` replaces it by the sum over the ranks, and it is copied back.
+typedef int (*HostAllreduceFn)(void* user, double* buf, uint64_t count);
 struct Comm {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  HostAllreduceFn host_fn = nullptr;
+  void* host_user = nullptr;
+  double* pinned = nullptr;
+  size_t pinned_n = 0;
   Comm(int nranks, int rank, const ncclUniqueId& id, int device);
+  Comm(int nranks, int rank, HostAllreduceFn fn, void* user);
   ~Comm();
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  void allreduce(const double* send, double* recv, int64_t count, cudaStream_t s);
 };
 
 // nnz-balanced contiguous row blocks: bounds[r]..bounds[r+1] for rank r.
@@ -217,6 +229,13 @@ struct Matrix {
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
+  // per-rank input: `local` holds rows [row0, row0 + local.n) of an n_global-row X
+  // (row offsets rebased); every setup step on it is sharded (rmg_matrix_create_csr_rows)
+  Matrix(Context* c, HostCsr local, int64_t n_global, int64_t row0, bool detect_pattern, Comm* comm);
+  int64_t n_global = -1;
+  bool rows_only = false;  // host holds only this rank's rows
+  void init_sparse(const HostCsr& local);
+  void alloc_comm_buffers();
   // dense X without a host CSR (setup on the device): from host
   // rows, or from a device buffer already padded to ld (coarse levels)
   Matrix(Context* c, int64_t n, int64_t f, const DenseInput& din);
@@ -230,7 +249,7 @@ struct Matrix {
   void build_hot(const HostCsr& ht, int64_t n_samples);
   int64_t n_local() const { return row1 - row0; }
   void allreduce_sums(double* sendbuf, double* recvbuf, int64_t count);
-  int64_t n() const { return host.n; }
+  int64_t n() const { return n_global >= 0 ? n_global : host.n; }
   int64_t f() const { return host.f; }
   int64_t nnz() const { return host_ok ? host.nnz() : host.n * host.f; }
   // t = X v then the X^T epilogue; v may live in a ring (sc != nullptr)

@@ -169,6 +169,17 @@ def synth_sparse_zipf(n: int, f: int, mean_nnz: float, zipf_s: float, abs_normal
     return _host_csr_to_matrix(h, n, f, nnz.value, not abs_normal_values)
 
 
+def synth_sparse_zipf_row_range(n: int, f: int, mean_nnz: float, zipf_s: float, abs_normal_values: bool, seed: int,
+                                row0: int, row1: int) -> FeatureMatrix:
+    """Rows [row0, row1) of synth_sparse_zipf(..., row_streams=True) (same bytes), as a
+    (row1 - row0)-row matrix: per-rank generation of a row-sharded input."""
+    lib = _lib.load()
+    h, nnz = C.c_void_p(), C.c_uint64()
+    _lib.check(lib.rmg_synth_sparse_zipf_row_range(n, f, mean_nnz, zipf_s, int(abs_normal_values), seed, row0, row1,
+                                                   C.byref(h), C.byref(nnz)))
+    return _host_csr_to_matrix(h, row1 - row0, f, nnz.value, not abs_normal_values)
+
+
 def rng_normals(seed: int, n: int) -> np.ndarray:
     out = np.zeros(n)
     _lib.check(_lib.load().rmg_rng_normals(seed, n, _ptr(out)))
@@ -238,10 +249,35 @@ class Comm:
         _lib.check(self.lib.rmg_comm_create(ctx.h, nranks, rank, idb, C.byref(self.h)))
         self.nranks, self.rank = nranks, rank
 
+    @classmethod
+    def host_staged(cls, ctx: Context, nranks: int, rank: int, allreduce) -> "Comm":
+        """A host-staged communicator (rmg_comm_create_host): `allreduce(buf)` gets a
+        float64 numpy view of the staged vector and must replace it in place by the
+        sum over all ranks (e.g. a gloo all-reduce).  Several ranks may share one GPU."""
+        self = cls.__new__(cls)
+        self.lib = ctx.lib
+        self.h = C.c_void_p()
+
+        def fn(user, buf, count):
+            try:
+                allreduce(np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double)), shape=(count,)))
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                return 1
+
+        self._cb = _HOST_ALLREDUCE(fn)  # kept alive with the communicator
+        _lib.check(self.lib.rmg_comm_create_host(ctx.h, nranks, rank, C.cast(self._cb, C.c_void_p), None,
+                                                 C.byref(self.h)))
+        self.nranks, self.rank = nranks, rank
+        return self
+
     def close(self):
         if self.h:
             self.lib.rmg_comm_destroy(self.h)
             self.h = C.c_void_p()
+
+
+_HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
 
 
 class DeviceMatrix:
@@ -268,6 +304,26 @@ class DeviceMatrix:
                                                               _ptr(ci), _ptr(v), int(detect_pattern),
                                                               C.byref(self.h)))
         self._query()
+
+    @classmethod
+    def from_rows(cls, x_local: FeatureMatrix, n_samples: int, row0: int, comm: "Comm",
+                  ctx: Optional[Context] = None, detect_pattern: bool = True) -> "DeviceMatrix":
+        """Per-rank input (rmg_matrix_create_csr_rows): this rank's rows [row0, row0 +
+        x_local.n_samples) of an n_samples-row X; the hierarchy setup on it is sharded."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.x = x_local
+        self.comm = comm
+        rp = np.ascontiguousarray(x_local.row_offsets, np.uint64)
+        ci = np.ascontiguousarray(x_local.column_indices, np.uint64)
+        v = None if x_local.values is None else np.ascontiguousarray(x_local.values, np.float64)
+        self.h = C.c_void_p()
+        _lib.check(self.lib.rmg_matrix_create_csr_rows(self.ctx.h, comm.h, n_samples, row0, x_local.n_samples,
+                                                       x_local.n_features, _ptr(rp), _ptr(ci), _ptr(v),
+                                                       int(detect_pattern), C.byref(self.h)))
+        self._query()
+        return self
 
     @classmethod
     def from_dense(cls, a, ctx: Optional[Context] = None, comm: Optional["Comm"] = None) -> "DeviceMatrix":
