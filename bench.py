@@ -1016,6 +1016,108 @@ def run_sweep(args, cfg):
         pg.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """`--shard` on a sparse sweep config (cfg 3 / cfg 5): X row-sharded over the ranks
+    with per-rank input -- each rank generates and holds only its rows
+    (synth_sparse_zipf_row_range, rmg_matrix_create_csr_rows) -- and the hierarchy
+    set up sharded (sketch S, coarse Grams, Jacobi diagonals all-reduced over NCCL,
+    X_k = X P coarsened row-locally).  A step = one single-RHS solve (beta and b
+    cycling through the sweep); every X^T pass all-reduces the F-vector.  Strong
+    scaling: the total work per step is fixed; value = max-over-ranks ms per solve."""
+    import torch
+    import paper_1806_05826_b200 as R
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    ctx = R.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    obj = [R.Comm.new_unique_id() if rank == 0 else None]
+    if pg:
+        pg.broadcast_object_list(obj, src=0)
+    comm = R.Comm(ctx, world, rank, obj[0])
+    t0 = time.time()
+    n = cfg["n"]
+    r0, r1 = rank * n // world, (rank + 1) * n // world
+    xl = R.synth_sparse_zipf_row_range(n, cfg["f"], cfg["mean"], cfg["zipf"], cfg["abs_values"], cfg["seed"], r0, r1)
+    m = R.DeviceMatrix.from_rows(xl, n, r0, comm, ctx)
+    nnz_local = m.nnz
+    del xl
+    betas, nb = cfg["betas"], cfg["n_rhs"]
+    spec = R.MethodSpec(kind=R.method_from_string(cfg["method"]), levels=level_specs(cfg),
+                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"]))
+    pm = R.PreparedMethod(m, betas[0], spec)
+    cur = betas[0]
+    setup_s = time.time() - t0
+    dev = torch.device("cuda", local)
+    bs = [torch.from_numpy(R.rng_normals(42 + k, n)).to(dev) for k in range(min(nb, 4))]
+    w = torch.empty(cfg["f"], dtype=torch.float64, device=dev)
+    units = [(b_i, k) for b_i in range(len(betas)) for k in range(len(bs))]
+
+    def step(i):
+        nonlocal cur
+        bi, k = units[i % len(units)]
+        if cur != betas[bi]:
+            pm.set_beta(betas[bi])
+            cur = betas[bi]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = pm.solve_device(bs[k].data_ptr(), w.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), rep
+
+    for i in range(args.warmup):
+        step(i)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        res = [step(args.warmup + i) for i in range(args.steps)]
+    total = sum(r[0] for r in res)
+    if pg:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total = float(t.item())
+        z = torch.tensor([float(nnz_local)], dtype=torch.float64, device=dev)
+        pg.all_reduce(z)
+        nnz_total = int(z.item())
+    else:
+        nnz_total = nnz_local
+    value = total / args.steps
+    cold = pm.time_operator(0, 10, True)  # this rank's shard, no collective inside the loop
+    if rank == 0:
+        peak, peak_kind = peaks()
+        fb = algorithmic_bytes(r1 - r0, cfg["f"], nnz_local, m.is_pattern)
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes, generated per rank",
+            "config": {"workload": cfg["workload"], "n_samples": n, "n_features": cfg["f"], "nnz": nnz_total,
+                       "levels": [cfg["f"]] + list(cfg["ks"]), "betas": betas, "tol": cfg["tol"],
+                       "parallelism": f"row-sharded x{world} (per-rank input; NCCL all-reduce of the F-vector)"},
+            "algorithm": f"{cfg['method']} over the sharded hierarchy (DESIGN.md §7)",
+            "iterations": [r[1].iterations for r in res], "converged": all(r[1].converged for r in res),
+            "setup_s": setup_s,
+            "roofline": {"bound": "hbm", "kernel": "rank-0 shard operator K1 + K2 (cold L2), no collective",
+                         "algorithmic_bytes_per_launch": fb, "ms_per_launch": cold[0],
+                         "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
+                         "frac": fb / (cold[0] * 1e6) / peak, "traffic": None, "peak_kind": peak_kind},
+            "e2e": None, "gpu_launches": int(sum(r[1].kernel_launches for r in res)),
+            "clocks": clocks.summary()}), flush=True)
+    pm.close()
+    m.close()
+    comm.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1032,6 +1134,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+    elif args.config in ("cfg3", "cfg5") and args.shard:
+        run_sharded(args, cfg)
     elif args.config in ("cfg3", "cfg5"):
         run_sweep(args, cfg)
     else:
