@@ -271,14 +271,17 @@ int rmg_method_solve(rmg_method* pm, const double* b, double* w_out, rmg_solve_r
 /* Same solve from a prebuilt rhs = X^T b (the reference's timed region). */
 int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out,
                          rmg_solve_report* report, int32_t on_device);
-/* Apply the level-0 preconditioner once: z = M^{-1} r (two_level_apply, krylov.cpp:379-425). */
 /* k right-hand sides (SURVEY §8(b) k_rhs): b is column-major n_samples x k, w_out
  * column-major n_features x k, reports[k] optional.  Column q equals
- * rmg_method_solve of column q (the solves run one after the other on the
- * context's stream; the block operator, rmg_ridge_apply_block, is the building
- * block of a lock-step batched solver). */
+ * rmg_method_solve of column q to rounding.  For cg, jacobi_cg and pcg_vcycle on
+ * a single-GPU CSR matrix and 2 <= k <= 64 the k columns run in LOCK STEP: every
+ * operator application at every level is one block-operator call (rmg_ridge_
+ * apply_block; dense coarse Grams as one skinny GEMM), reductions are per column
+ * in a fixed order and a converged column freezes.  Other
+ * methods (or RMG_BATCH_SEQ=1) solve the columns one after the other. */
 int rmg_method_solve_batch(rmg_method* pm, const double* b, double* w_out, uint64_t k, rmg_solve_report* reports,
                            int32_t on_device);
+/* Apply the level-0 preconditioner once: z = M^{-1} r (two_level_apply, krylov.cpp:379-425). */
 int rmg_method_precondition(rmg_method* pm, const double* r, double* z, int32_t on_device);
 /* PreparedMethod::coarse_size (krylov.hpp:229) and per-level introspection */
 int rmg_method_info(const rmg_method* pm, uint64_t* n_levels, uint64_t* coarse_size);

@@ -1,5 +1,6 @@
 // Dense Gram matrices of coarse levels: assembly and application (dense_gram.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -159,6 +160,91 @@ __global__ void __launch_bounds__(kGemmWarps * 32, 2)
   }
 }
 
+// The same product on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): the
+// dense multi-right-hand-side contraction of north-star's "tensor cores for the
+// dense multi-RHS variant".  A CTA owns 64 rows of G (16 per warp: two 8-row
+// m-tiles) x the 16-column chunk (two 8-column n-tiles); G's fragments are read
+// straight from global memory (each warp load is 8 rows x one 32-byte sector,
+// every byte used once), V is staged 64 rows at a time in shared memory
+// (double-buffered) and shared by the 4 warps.  Fragment layouts (PTX ISA,
+// m8n8k4 f64): A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}].
+constexpr int kDmWarps = 4, kDmRows = 16 * kDmWarps, kDmK = 64, kDmLd = 17, kGramSplitsMax = 16;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Split K: blockIdx.y takes columns [kb, ke) of G; each split writes its own
+// partial block P[split] (n x 16), summed in split order by k_gram_finish.
+__global__ void __launch_bounds__(kDmWarps * 32)
+    k_gram_gemm_dmma(const double* __restrict__ G, int64_t ldg, const double* __restrict__ V, int ldv, int col0,
+                     int kc, int64_t n, int64_t kspan, double* __restrict__ P) {
+  __shared__ double vs[2][kDmK * kDmLd];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * kDmRows + warp * 16;
+  const int64_t kb = static_cast<int64_t>(blockIdx.y) * kspan, ke = min(n, kb + kspan);
+  // this lane's A rows (one per m-tile), clamped in range; column lane % 4
+  const int64_t ra0 = min(rbase + (lane >> 2), n - 1), ra1 = min(rbase + 8 + (lane >> 2), n - 1);
+  const double* g0 = G + ra0 * ldg + (lane & 3);
+  const double* g1 = G + ra1 * ldg + (lane & 3);
+  double c[2][2][2] = {};  // [m-tile][n-tile][2]
+  auto stage = [&](int buf, int64_t k0) {
+    for (int e = threadIdx.x; e < kDmK * 16; e += kDmWarps * 32) {
+      const int kk = e >> 4, q = e & 15;
+      const int64_t kr = k0 + kk;
+      vs[buf][kk * kDmLd + q] = (kr < ke && q < kc) ? V[kr * ldv + col0 + q] : 0.0;
+    }
+  };
+  stage(0, kb);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = kb; k0 < ke; k0 += kDmK) {
+    if (k0 + kDmK < ke) stage(buf ^ 1, k0 + kDmK);  // next chunk's V while this one is multiplied
+    const double* vb = vs[buf];
+#pragma unroll 4
+    for (int kk = 0; kk < kDmK; kk += 4) {
+      const int64_t kcol = k0 + kk + (lane & 3);
+      const double a0 = kcol < ke ? __ldcs(g0 + k0 + kk) : 0.0;
+      const double a1 = kcol < ke ? __ldcs(g1 + k0 + kk) : 0.0;
+      const double b0 = vb[(kk + (lane & 3)) * kDmLd + (lane >> 2)];
+      const double b1 = vb[(kk + (lane & 3)) * kDmLd + 8 + (lane >> 2)];
+      dmma(c[0][0][0], c[0][0][1], a0, b0);
+      dmma(c[0][1][0], c[0][1][1], a0, b1);
+      dmma(c[1][0][0], c[1][0][1], a1, b0);
+      dmma(c[1][1][0], c[1][1][1], a1, b1);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* part = P + static_cast<int64_t>(blockIdx.y) * n * 16;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int64_t row = rbase + 8 * mt + (lane >> 2);
+    if (row >= n) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+      *reinterpret_cast<double2*>(part + row * 16 + 8 * nt + 2 * (lane & 3)) =
+          make_double2(c[mt][nt][0], c[mt][nt][1]);
+  }
+}
+
+// Y = sum over the splits, in split order, + beta V
+__global__ void k_gram_finish(const double* __restrict__ P, int splits, const double* __restrict__ V, int ldv,
+                              int col0, int kc, double beta, double* __restrict__ Y, int64_t n) {
+  const int64_t total = n * kc;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = e / kc;
+    const int q = static_cast<int>(e - row * kc);
+    double sum = 0.0;
+    for (int sp = 0; sp < splits; ++sp) sum += P[(static_cast<int64_t>(sp) * n + row) * 16 + q];
+    const int64_t o = row * ldv + col0 + q;
+    Y[o] = sum + beta * V[o];
+  }
+}
+
 }  // namespace
 
 void sparse_gram_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval,
@@ -191,14 +277,32 @@ void launch_gram_gemv(const double* G, int64_t ldg, const double* x, double beta
   check("gram_gemv");
 }
 
+int64_t gram_gemm_scratch(int64_t n) { return static_cast<int64_t>(kGramSplitsMax) * n * 16; }
+
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
-                      cudaStream_t s) {
+                      double* scratch, cudaStream_t s) {
   if (n <= 0 || k <= 0) return;
-  const int rows = kGemmRows * kGemmWarps;
-  const int grid = static_cast<int>((n + rows - 1) / rows);
+  static const bool cuda_cores = [] {
+    const char* e = std::getenv("RMG_GRAM_GEMM");
+    return e != nullptr && std::string(e) == "cuda";
+  }();
   for (int c0 = 0; c0 < k; c0 += kGemmK) {
     const int kc = std::min(kGemmK, k - c0);
-    k_gram_gemm<<<grid, kGemmWarps * 32, 0, s>>>(G, ldg, V, k, c0, kc, beta, Y, n);
+    if (cuda_cores) {  // CUDA-core FP64 variant (A/B comparisons)
+      const int rows = kGemmRows * kGemmWarps;
+      k_gram_gemm<<<static_cast<int>((n + rows - 1) / rows), kGemmWarps * 32, 0, s>>>(G, ldg, V, k, c0, kc, beta, Y,
+                                                                                      n);
+    } else {
+      // split K so that the grid fills the GPU: ~8 CTAs (32 warps) per SM
+      const int64_t tiles = (n + kDmRows - 1) / kDmRows;
+      int splits = static_cast<int>(std::min<int64_t>(kGramSplitsMax, std::max<int64_t>(1, (148 * 8) / tiles)));
+      int64_t kspan = ((n + splits - 1) / splits + kDmK - 1) / kDmK * kDmK;
+      splits = static_cast<int>((n + kspan - 1) / kspan);
+      k_gram_gemm_dmma<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), kDmWarps * 32, 0, s>>>(
+          G, ldg, V, k, c0, kc, n, kspan, scratch);
+      k_gram_finish<<<static_cast<int>(std::min<int64_t>(148 * 4, (n * kc + 255) / 256)), 256, 0, s>>>(
+          scratch, splits, V, k, c0, kc, beta, Y, n);
+    }
     check("gram_gemm");
   }
 }

@@ -30,8 +30,11 @@ void sparse_gram_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, c
 void launch_gram_gemv(const double* G, int64_t ldg, const double* x, double beta, double* y, int64_t n,
                       const int32_t* done, cudaStream_t s);
 
-// Y = G V + beta V for row-major n x k blocks V, Y (leading dimension k), k <= 64.
+// Y = G V + beta V for row-major n x k blocks V, Y (leading dimension k), k <= 64,
+// on the FP64 tensor cores (DMMA, split K; RMG_GRAM_GEMM=cuda: CUDA cores).
+// scratch: gram_gemm_scratch(n) doubles (split-K partials).
+int64_t gram_gemm_scratch(int64_t n);
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
-                      cudaStream_t s);
+                      double* scratch, cudaStream_t s);
 
 }  // namespace rmg

@@ -617,8 +617,12 @@ __global__ void __launch_bounds__(kT, 1) k_dense_krylov(DenseKrylovArgs a) {
 //      (both sets of partials are per-iteration, so nothing is carried over
 //      iterations and no recurrence drift builds up).
 // The convergence test of r_k (||r_k||^2 rides on B1 of iteration k) runs half
-// an iteration after the update; iteration counts, history and breakdown
-// exits are those of k_dense_krylov.  Own-row work (nr <= 28) is warp 0:
+// an iteration after the update; the iteration logic, history and breakdown
+// exits are those of k_dense_krylov.  The A z row sums are a different
+// (fixed) summation order per variant -- the PAIR variant (even n, A in SMEM)
+// has thread tid sum columns 2 tid, 2 tid + 1, 2 tid + 2 kT, ...; the others
+// columns tid, tid + kT, ... -- so inner rounding depends on the variant
+// (tests/test_gpu_parity.py::test_pair_variant_within_bars holds both to the bars).  Own-row work (nr <= 28) is warp 0:
 // its reductions are warp sums.
 // HM >= truncation (history directions held per lane); NQ = columns per thread
 // (n <= NQ * kT) and RM >= owned rows: compile-time so the unrolled loop body

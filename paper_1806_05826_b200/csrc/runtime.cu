@@ -1541,6 +1541,7 @@ void Method::build_dense_grams() {
     d->n = n;
     d->ld = (n + 1) / 2 * 2;
     d->G.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * d->ld);
+    d->scratch.alloc(static_cast<size_t>(std::max<int64_t>(1, gram_gemm_scratch(n))));
     device_gram(m, d->G.get(), d->ld);
     if (m.comm != nullptr) m.allreduce_sums(d->G.get(), d->G.get(), n * d->ld);  // replicated G_k
     dg_[k] = std::move(d);
@@ -2370,7 +2371,7 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
   const DenseGram* dg = dgram(lv);
   auto apply = [&](const double* in, double* out) {
     if (dg != nullptr)
-      launch_gram_gemm(dg->G.get(), dg->ld, in, level_beta(lv), out, nf, k, s);
+      launch_gram_gemm(dg->G.get(), dg->ld, in, level_beta(lv), out, nf, k, dg->scratch.get(), s);
     else
       m.apply_block(in, out, level_beta(lv), k, false);
   };

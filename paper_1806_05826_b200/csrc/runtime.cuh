@@ -415,7 +415,7 @@ class Method {
   // pcg_vcycle: dense G_k = X_k^T X_k per level k >= 1 where n_k^2 doubles are
   // fewer bytes than an X_k sweep pair; nullptr: sweep X_k
   struct DenseGram {
-    DBuf<double> G;
+    DBuf<double> G, scratch;  // + split-K partials of the block GEMM
     int64_t n = 0, ld = 0;
   };
   std::vector<std::unique_ptr<DenseGram>> dg_;

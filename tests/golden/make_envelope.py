@@ -34,8 +34,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, os.path.dirname(HERE))
 import oracle  # noqa: E402
 
-CASES = (("cfg2_small", 10000, 2000, [200, 20]), ("cfg2_full", 100000, 20000, [2000, 200]), ("cnae", 0, 0, []))
-BETA = {"cnae": 1e-6}
+CASES = (("cfg2_small", 10000, 2000, [200, 20]), ("cfg2_full", 100000, 20000, [2000, 200]), ("cnae", 0, 0, []),
+         ("lpsc105", 0, 0, []))
+BETA = {"cnae": 1e-6, "lpsc105": 1e-6}
 VARIANTS = {  # name -> environment; ENVELOPE_LIB picks the FMA-contracted build
     "dot_tree": {"ORC_DOT_TREE": "1"},
     "coarse_inverse": {"ORC_COARSE_INV": "1"},
@@ -59,7 +60,7 @@ def rel_diff(a, b):
 
 def setup(chk, name, n, f, ks):
     g = np.load(os.path.join(HERE, name + ".npz"))
-    if name == "cnae":  # the bundled UCI CNAE-9 matrix, beta = 1e-6, plain CG only
+    if name in ("cnae", "lpsc105"):  # the bundled CNAE-9 / netlib SC105 matrices, beta = 1e-6, plain CG only
         m = chk.matrix(int(g["x_shape"][0]), int(g["x_shape"][1]), g["x_row_offsets"], g["x_column_indices"],
                        g["x_values"])
         return g, m, []

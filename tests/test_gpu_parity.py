@@ -137,9 +137,10 @@ def test_lpsc105_cg_66(gpu):
     assert int(g["cg_iterations"]) == 66
     assert abs(sol.report.iterations - 66) <= 2
     # kappa(A) ~ 1e7 at beta = 1e-6: two CG trajectories that differ only in
-    # reduction rounding agree to ~3e-8 at tol 1e-6 (the reference's own
-    # threaded mode differs from its sequential mode the same way) ...
-    assert rel_diff(sol.w, g["cg_w"]) <= 1e-6
+    # reduction rounding agree to ~7e-8 at tol 1e-6 -- the reference's own
+    # threaded runs differ from its sequential run by up to envelope cg_w_spread ...
+    env = _envelope("lpsc105")
+    assert rel_diff(sol.w, g["cg_w"]) <= env["cg_w_spread"], (rel_diff(sol.w, g["cg_w"]), env["cg_w_spread"])
     assert sol.coarse_size == 0
     # ... and to the 1e-8 bar once both are driven to tol 1e-12 (SURVEY App. B protocol)
     ref_tight = R.solve_system(m, 1e-6, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-12, 20000)))
@@ -165,7 +166,8 @@ def test_lpsc105_leader_follower_52(gpu):
     """LF closest to 56 yields 52 clusters.  Its coarse system (beta = 1e-6) is so
     ill-conditioned that the iteration count depends on the Cholesky rounding:
     reference+Eigen recorded 43 (proj/test_output.txt:41), reference+our LLT
-    shim 37 (golden).  The GPU uses an explicit inverse; we bound it loosely."""
+    shim 37 (golden); the shim build with 4, 7 or 8 threads gives 40.  The GPU
+    (explicit inverse of the same Cholesky factor) is held to +-2 of the golden."""
     g = load_golden("lpsc105")
     m = dm(golden_matrix(g))
     lv = R.LevelSpec(clustering=R.ClusteringChoice(kind=R.LEADER_TARGET, target_size=56))
@@ -173,7 +175,7 @@ def test_lpsc105_leader_follower_52(gpu):
     assert pm.coarse_size() == 52
     assert np.array_equal(pm.labels(0), g["lf56_labels"])
     w, rep = pm.solve(g["b"])
-    assert rep.converged and rep.iterations <= 60
+    assert rep.converged and abs(rep.iterations - int(g["lf56_iterations"])) <= 2, rep.iterations
 
 
 def test_cnae_duplicate_merging(gpu):
@@ -187,12 +189,16 @@ def test_cnae_duplicate_merging(gpu):
     assert rep.converged and rep.iterations == 1
     # Unpreconditioned CG needs 656 iterations on an 856-dimensional, beta = 1e-6
     # system: far past the point where finite-precision CG loses orthogonality,
-    # so the count follows the reduction rounding (the sequential-order oracle
-    # reproduces 656 exactly; tree-ordered GPU dots land within a few percent).
+    # so the count follows the summation accuracy.  The bar is the measured
+    # envelope of the same algorithm (tests/golden/envelope.json "cnae": the
+    # reference's threads, and the restatement with pairwise dots / segmented
+    # X^T sums / FMA updates -- the GPU's accuracy class -- which gives 640-657).
+    env = _envelope("cnae")
     cg = R.solve_system(m, 1e-6, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 20000)))
     assert cg.report.converged
-    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= 0.03 * int(g["cg_iterations"])
-    assert rel_diff(cg.w, g["cg_w"]) <= 1e-5
+    lo, hi = env["cg_iterations_range"]
+    assert lo <= cg.report.iterations <= hi, (cg.report.iterations, env["cg_iterations_range"])
+    assert rel_diff(cg.w, g["cg_w"]) <= env["cg_w_spread"], (rel_diff(cg.w, g["cg_w"]), env["cg_w_spread"])
 
 
 def test_cfg1_two_level(gpu):
@@ -300,6 +306,12 @@ def _cfg2_spec(ks, labels=None):
     return R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=levels, solver=R.SolverConfig(1e-6, 1000))
 
 
+def _envelope(name):
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "envelope.json")))[name]
+
+
 def _csr_sha(x):
     import hashlib
     h = hashlib.sha256()
@@ -319,27 +331,26 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     pm = R.PreparedMethod(m, 1.0, _cfg2_spec(ks))
     for i in range(len(ks)):  # k-means on normalised columns, bit-exact per level
         assert np.array_equal(pm.labels(i), g[f"labels{i}"].astype(np.int64))
-    # At tol 1e-6 the bar is the reference's own rounding envelope: its threaded
-    # mode (same algorithm, other summation order) drifts from its sequential
-    # mode by up to env iterations and env_w in w (tests/golden/envelope.json).
-    import json
-    import os
-    env = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "envelope.json")))[name]
+    # At tol 1e-6 the bar is the measured rounding envelope of the reference's
+    # algorithm (tests/golden/envelope.json): its own threaded runs (2-8 threads) and
+    # the restatement under the GPU's arithmetic choices (pairwise dots, segmented
+    # X^T sums, FMA updates, explicit coarse inverse, omega +-1 ulp).
+    env = _envelope(name)
     w, rep = pm.solve(g["b"])
     assert rep.converged
-    # cfg2_full: GPU 638 vs reference 647; reference threaded 650/651; see DESIGN.md §5
-    assert abs(rep.iterations - int(g["ml_iterations"])) <= max(2, 3 * env["ml_iter_spread"]), rep.iterations
-    # w at tol 1e-6: the kappa*tol regime (the reference itself moves by env["ml_w_spread"]
-    # between its thread counts); the strict 1e-8 comparison is made at tol 1e-12 below
-    assert rel_diff(w, g["ml_w"]) <= 1e-6, rel_diff(w, g["ml_w"])
+    lo, hi = env["ml_iterations_range"]
+    assert lo <= rep.iterations <= hi, (rep.iterations, env["ml_iterations_range"])
+    # w at tol 1e-6: within the envelope's w spread; the strict 1e-8 comparison is
+    # made at tol 1e-12 below
+    assert rel_diff(w, g["ml_w"]) <= env["ml_w_spread"], (rel_diff(w, g["ml_w"]), env["ml_w_spread"])
     assert len(rep.inner_iterations) == rep.iterations
     gi = g["ml_inner"].astype(np.int64)
     # the first inner solves (same outer trajectory so far) take the reference's counts
     assert np.all(np.abs(rep.inner_iterations[:3].astype(np.int64) - gi[:3]) <= 2)
     cg = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 5000)))
-    assert abs(cg.report.iterations - int(g["cg_iterations"])) <= max(2, 3 * env["cg_iter_spread"]), \
-        (cg.report.iterations, int(g["cg_iterations"]))
-    assert rel_diff(cg.w, g["cg_w"]) <= 1e-6, (rel_diff(cg.w, g["cg_w"]), env)
+    lo, hi = env["cg_iterations_range"]
+    assert lo <= cg.report.iterations <= hi, (cg.report.iterations, env["cg_iterations_range"])
+    assert rel_diff(cg.w, g["cg_w"]) <= env["cg_w_spread"], (rel_diff(cg.w, g["cg_w"]), env["cg_w_spread"])
     # Driven to tol 1e-12: the strict bar.  The reference's CG converges there
     # (cg12); its multilevel FCG converges on cfg2_small but stagnates near 1e-9
     # on cfg2_full (inexact inner solves, ml12_converged = 0 in the golden) at a
@@ -399,3 +410,33 @@ def test_fgmres_edges(gpu, orc):
         pm.solve(bad)
     with pytest.raises(ValueError):  # two-level method requires one level spec
         R.PreparedMethod(m, 0.1, R.MethodSpec(kind=R.FGMRES_TWOLEVEL))
+
+
+def test_pair_variant_within_bars(gpu):
+    """The persistent inner solver's PAIR variant (even n, A in SMEM: A z summed over
+    column pairs) and the plain variant (RMG_DENSE_NO_PAIR=1, read once per process,
+    so in a subprocess) are both held to the cfg2_small bars: iterations in the
+    envelope, w within its spread."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, sys, numpy as np; sys.path.insert(0, 'tests');"
+        "import paper_1806_05826_b200 as R; from helpers import load_golden, rel_diff;"
+        "g = load_golden('cfg2_small'); x = R.synth_sparse_zipf(10000, 2000, 40.0, 1.1, False, 0);"
+        "lv = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.IMPORTED, labels=g[f'labels{i}'].astype(np.int64),"
+        " n_clusters=k), solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == 1 else R.INNER_FCG,"
+        " tol=1e-6, max_iters=500)) for i, k in enumerate([200, 20])];"
+        "pm = R.PreparedMethod(R.DeviceMatrix(x), 1.0, R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=lv,"
+        " solver=R.SolverConfig(1e-6, 1000)));"
+        "w, rep = pm.solve(g['b']); print(json.dumps([rep.iterations, rel_diff(w, g['ml_w'])]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = _envelope("cfg2_small")
+    lo, hi = env["ml_iterations_range"]
+    for extra in ({}, {"RMG_DENSE_NO_PAIR": "1"}):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **extra},
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        its, err = json.loads(out.stdout.strip().splitlines()[-1])
+        assert lo <= its <= hi and err <= env["ml_w_spread"], (extra, its, err, env)
