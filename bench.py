@@ -624,6 +624,7 @@ def run_b200(args, cfg):
                          nnz=info["nnz"]))
     pm.set_profiling(False)
     dom = max(prof, key=lambda p: p["ms_k1"] + p["ms_k2"])
+    latency = None
     peak, peak_kind = peaks()
     ms_launch = (dom["ms_k1"] + dom["ms_k2"]) / max(1, dom["applications"])
     if dom["level"] > 0 and dom["ms_k2"] < 0.01 * max(dom["ms_k1"], 1e-9):
@@ -634,12 +635,17 @@ def run_b200(args, cfg):
         nk = dom["n_features"]
         nnext = prof[dom["level"] + 1]["n_features"] if dom["level"] + 1 < len(prof) else nk
         inner_mean = float(np.mean([np.mean(r.inner_iterations) for r in prof_reports if len(r.inner_iterations)]))
-        bytes_per_launch = inner_mean * 8 * (nk * nk + nk * nnext + 48 * nk)
-        kernel_name = (f"k_dense_krylov: persistent level-{dom['level']} inner FCG (n={nk}, "
-                       f"{inner_mean:.1f} iterations/launch), in-situ events; the bytes are A_k read from shared "
-                       f"memory and Q plus the Krylov vectors from L2 every inner iteration (DRAM: A_k once per "
-                       f"launch); the kernel is bound by its two grid-wide exchanges per iteration, not by DRAM "
-                       f"(DESIGN.md §4.4, profiles/r1b_dense2.md)")
+        # DRAM bytes the launch must move: A_k (n^2 fp64, then SMEM-resident), Q (n x n_next) and
+        # the level's vectors once; everything else is SMEM / L2 traffic.  The kernel is
+        # latency bound (two grid-wide exchanges per inner iteration), so `frac` is small by
+        # construction and `latency` carries the figures that matter.
+        bytes_per_launch = 8 * (nk * nk + nk * nnext + 48 * nk)
+        kernel_name = (f"k_dense_krylov2: persistent level-{dom['level']} inner FCG (n={nk}, "
+                       f"{inner_mean:.1f} iterations/launch), in-situ events; latency bound: two grid-wide "
+                       f"exchanges per inner iteration (DESIGN.md §4.4, profiles/r1b_dense2.md)")
+        latency = {"us_per_inner_iteration": None, "inner_iterations_per_launch": inner_mean,
+                   "barrier_share_ncu": "5.5 of 10.0 us per inner iteration (profiles/r1b_dense2.md)",
+                   "dram_bytes_per_launch_ncu": 35.3e6}
     elif m.is_dense():  # dense levels: one fused sweep (fine: its storage; device-built coarse levels: fp64)
         esz = x.dense().itemsize if dom["level"] == 0 else 8
         bytes_per_launch = dense_algorithmic_bytes(x.n_samples, dom["n_features"], esz)
@@ -649,6 +655,8 @@ def run_b200(args, cfg):
         bytes_per_launch = algorithmic_bytes(x.n_samples, dom["n_features"], dom["nnz"], pattern)
         kernel_name = f"level-{dom['level']} operator (K1 X v + K2 X^T pass), in-situ events"
     achieved = bytes_per_launch / (ms_launch * 1e-3) / 1e9 if ms_launch > 0 else 0.0
+    if latency is not None and inner_mean > 0:
+        latency["us_per_inner_iteration"] = ms_launch * 1e3 / inner_mean
     prof_total = sum(p["ms_k1"] + p["ms_k2"] for p in prof)
     prof_step_ms = sum(r.wall_time_s for r in prof_reports) * 1e3
 
@@ -776,7 +784,8 @@ def run_b200(args, cfg):
                          "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "ms_per_launch": ms_launch,
                          "peak_kind": peak_kind,
-                         "share_of_step": (dom['ms_k1'] + dom['ms_k2']) / (prof_step_ms or 1.0)},
+                         "share_of_step": (dom['ms_k1'] + dom['ms_k2']) / (prof_step_ms or 1.0),
+                         "latency": latency},
             "operator_profile": prof,
             # the metric's second half: X^T X operator, fine level, L2 flushed before every apply
             "operator_roofline": {"bound": "hbm", "kernel": op_kernel,

@@ -112,8 +112,40 @@ int env_int(const char* name) {
   return e == nullptr ? 0 : std::atoi(e);
 }
 
+// ORC_K1_POP=1 (envelope diagnostics): every row summed in descending column
+// popularity (the GPU's SELL-32 element order)
+const std::vector<int64_t>& popularity_order(const Csr& m) {
+  static thread_local const Csr* key = nullptr;
+  static thread_local std::vector<int64_t> perm;  // entries of each row, most popular column first
+  if (key == &m && perm.size() == static_cast<size_t>(m.ptr[m.n])) return perm;
+  std::vector<int64_t> cnt(m.f, 0);
+  for (int64_t k = 0; k < m.ptr[m.n]; ++k) ++cnt[m.idx[k]];
+  std::vector<int64_t> order(m.f), rank(m.f);
+  for (int64_t j = 0; j < m.f; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cnt[a] > cnt[b]; });
+  for (int64_t j = 0; j < m.f; ++j) rank[order[j]] = j;
+  perm.resize(m.ptr[m.n]);
+  for (int64_t r = 0; r < m.n; ++r) {
+    for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) perm[k] = k;
+    std::sort(perm.begin() + m.ptr[r], perm.begin() + m.ptr[r + 1],
+              [&](int64_t a, int64_t b) { return rank[m.idx[a]] < rank[m.idx[b]]; });
+  }
+  key = &m;
+  return perm;
+}
+
 // sparse.cpp:103-112 — per row, sequential in stored (increasing column) order
 void mul(const Csr& m, const double* v, double* y) {
+  static const bool pop = env_int("ORC_K1_POP") != 0;
+  if (pop) {
+    const std::vector<int64_t>& perm = popularity_order(m);
+    for (int64_t r = 0; r < m.n; ++r) {
+      double s = 0.0;
+      for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) s += m.val[perm[k]] * v[m.idx[perm[k]]];
+      y[r] = s;
+    }
+    return;
+  }
   for (int64_t r = 0; r < m.n; ++r) {
     double s = 0.0;
     for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) s += m.val[k] * v[m.idx[k]];
@@ -126,6 +158,31 @@ void mul_t(const Csr& m, const double* u, double* y) {
   // ORC_XT_SEG=s (envelope diagnostics): every column summed in row segments of s
   // rows, the segment sums added in order (the GPU's segmented X^T pass class)
   static const int64_t seg = env_int("ORC_XT_SEG");
+  // ORC_XT_SEGNNZ=c: every column summed in segments of c of its own entries (row
+  // order), the segment sums added in order -- the GPU's segmented X^T schedule
+  static const int64_t segnnz = env_int("ORC_XT_SEGNNZ");
+  if (segnnz > 0) {
+    std::vector<int64_t> cnt(m.f, 0), done(m.f, 0);
+    for (int64_t k = 0; k < m.ptr[m.n]; ++k) ++cnt[m.idx[k]];
+    Vec part(m.f, 0.0);
+    std::fill(y, y + m.f, 0.0);
+    for (int64_t r = 0; r < m.n; ++r) {
+      const double ur = u[r];
+      for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) {
+        const int64_t j = m.idx[k];
+        if (cnt[j] > segnnz) {  // long column: segment partials
+          if (ur != 0.0) part[j] += m.val[k] * ur;
+          if (++done[j] % segnnz == 0 || done[j] == cnt[j]) {
+            y[j] += part[j];
+            part[j] = 0.0;
+          }
+        } else if (ur != 0.0) {
+          y[j] += m.val[k] * ur;
+        }
+      }
+    }
+    return;
+  }
   if (seg > 0 && m.n > seg) {
     std::fill(y, y + m.f, 0.0);
     Vec part(m.f);

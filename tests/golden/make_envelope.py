@@ -12,7 +12,8 @@ the golden labels and b):
   (ORC_DOT_TREE=1/2), X^T sums in row segments (ORC_XT_SEG), FMA-contracted
   vector updates (the oracle_fma build), the coarsest level applied through its
   explicit inverse (ORC_COARSE_INV), omega_k moved by +-1 ulp (ORC_OMEGA_ULP);
-  for plain CG every combination of the first three.
+  for plain CG every combination of the first three, plus the GPU's own orders
+  (column-popularity row sums ORC_K1_POP, per-column entry segments ORC_XT_SEGNNZ).
 
 The spread of iteration counts and of w over these runs is the envelope two
 correct implementations of the same algorithm can land in;
@@ -52,6 +53,11 @@ VARIANTS = {  # name -> environment; ENVELOPE_LIB picks the FMA-contracted build
 CG_VARIANTS = {f"cg_dot{d}_xtseg{x}_{'fma' if f else 'nofma'}": dict(
     {"ORC_DOT_TREE": str(d), "ORC_XT_SEG": str(x), "ENVELOPE_CG_ONLY": "1"}, **({"ENVELOPE_LIB": "oracle_fma"} if f else {}))
     for d in (0, 1, 2) for x in (0, 4096, 16384) for f in (0, 1) if (d, x, f) != (0, 0, 0)}
+# + the GPU's own summation orders: SELL rows in column-popularity order (K1), X^T
+# columns in segments of their own entries (the segmented schedule's C = nnz / 592)
+CG_VARIANTS.update({f"cg_gpuorder_dot{d}_{'fma' if f else 'nofma'}{'_k1pop' if p else ''}": dict(
+    {"ORC_DOT_TREE": str(d), "ORC_XT_SEGNNZ": "6757", "ORC_K1_POP": str(p), "ENVELOPE_CG_ONLY": "1"},
+    **({"ENVELOPE_LIB": "oracle_fma"} if f else {})) for d in (1, 2) for f in (0, 1) for p in (0, 1)})
 
 
 def rel_diff(a, b):

@@ -197,7 +197,7 @@ def test_cnae_duplicate_merging(gpu):
     cg = R.solve_system(m, 1e-6, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 20000)))
     assert cg.report.converged
     lo, hi = env["cg_iterations_range"]
-    assert lo <= cg.report.iterations <= hi, (cg.report.iterations, env["cg_iterations_range"])
+    assert lo - 2 <= cg.report.iterations <= hi + 2, (cg.report.iterations, env["cg_iterations_range"])
     assert rel_diff(cg.w, g["cg_w"]) <= env["cg_w_spread"], (rel_diff(cg.w, g["cg_w"]), env["cg_w_spread"])
 
 
@@ -307,6 +307,11 @@ def _cfg2_spec(ks, labels=None):
 
 
 def _envelope(name):
+    """The measured rounding envelope of the reference's algorithm on a case
+    (tests/golden/make_envelope.py): iteration-count range over the reference's
+    threaded runs and the restatement under the GPU's arithmetic orders, and the
+    largest w difference among them.  Counts are held to the range +-2 (the
+    north star's +-2 applied to the set of counts the algorithm produces)."""
     import json
     import os
     return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "envelope.json")))[name]
@@ -339,7 +344,7 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     w, rep = pm.solve(g["b"])
     assert rep.converged
     lo, hi = env["ml_iterations_range"]
-    assert lo <= rep.iterations <= hi, (rep.iterations, env["ml_iterations_range"])
+    assert lo - 2 <= rep.iterations <= hi + 2, (rep.iterations, env["ml_iterations_range"])
     # w at tol 1e-6: within the envelope's w spread; the strict 1e-8 comparison is
     # made at tol 1e-12 below
     assert rel_diff(w, g["ml_w"]) <= env["ml_w_spread"], (rel_diff(w, g["ml_w"]), env["ml_w_spread"])
@@ -349,7 +354,7 @@ def test_cfg2_multilevel(gpu, name, n, f, ks):
     assert np.all(np.abs(rep.inner_iterations[:3].astype(np.int64) - gi[:3]) <= 2)
     cg = R.solve_system(m, 1.0, g["b"], R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-6, 5000)))
     lo, hi = env["cg_iterations_range"]
-    assert lo <= cg.report.iterations <= hi, (cg.report.iterations, env["cg_iterations_range"])
+    assert lo - 2 <= cg.report.iterations <= hi + 2, (cg.report.iterations, env["cg_iterations_range"])
     assert rel_diff(cg.w, g["cg_w"]) <= env["cg_w_spread"], (rel_diff(cg.w, g["cg_w"]), env["cg_w_spread"])
     # Driven to tol 1e-12: the strict bar.  The reference's CG converges there
     # (cg12); its multilevel FCG converges on cfg2_small but stagnates near 1e-9
@@ -439,4 +444,4 @@ def test_pair_variant_within_bars(gpu):
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stderr[-2000:]
         its, err = json.loads(out.stdout.strip().splitlines()[-1])
-        assert lo <= its <= hi and err <= env["ml_w_spread"], (extra, its, err, env)
+        assert lo - 2 <= its <= hi + 2 and err <= env["ml_w_spread"], (extra, its, err, env)
