@@ -36,6 +36,7 @@ struct rmg_comm {
 struct rmg_method {
   rmg::Method m;
   rmg::DBuf<double> b, rhs, w;  // staging for host-pointer calls
+  rmg::DBuf<double> bb, wb;     // ... and for batched calls (kept: no allocation per call)
   template <class... A>
   explicit rmg_method(A&&... a) : m(std::forward<A>(a)...) {}
 };
@@ -658,9 +659,8 @@ int rmg_method_solve_batch(rmg_method* pm, const double* b, double* w_out, uint6
       rmg::Context& c = *x.ctx;
       RMG_CK(cudaSetDevice(c.device));
       const uint64_t l0 = c.launches;
-      rmg::DBuf<double> bi, bo;
-      const double* db = stage_in(c, b, static_cast<size_t>(n) * k, on_device, bi);
-      double* dw = stage_out(static_cast<size_t>(f) * k, on_device, w_out, bo);
+      const double* db = stage_in(c, b, static_cast<size_t>(n) * k, on_device, pm->bb);
+      double* dw = stage_out(static_cast<size_t>(f) * k, on_device, w_out, pm->wb);
       const std::vector<rmg::SolveResult> rs = pm->m.solve_block(db, dw, static_cast<int>(k));
       finish_out(c, dw, w_out, static_cast<size_t>(f) * k, on_device);
       for (uint64_t q = 0; q < k; ++q) fill_report(rs[q], (c.launches - l0) / k, reports ? reports + q : nullptr);
