@@ -317,3 +317,53 @@ class Checker:
                         residual_history=hist[:it].copy(),
                         inner_iterations=inner[:it].copy() if mk >= 2 else np.zeros(0, np.uint64),
                         omega=list(rep.omega[: max(0, nl - 1)]), level_sizes=list(rep.level_sizes[:nl]))
+
+
+# ---------------------------------------------------------------- bench harness
+def describe_clustering(level: dict, coarse_size: int) -> str:
+    """describe_clustering (krylov.cpp:596-612) for a checker level dict."""
+    kind = level.get("clustering_kind", CLUSTER_KMEANS)
+    if level.get("labels") is not None:
+        return f"imported(fc={coarse_size})"
+    if kind == CLUSTER_LEADER_TOLERANCE:
+        return f"lf(tol={level.get('tolerance', 1.0):g},fc={coarse_size})"
+    if kind == CLUSTER_LEADER_TARGET:
+        return f"lf(fc={coarse_size})"
+    return f"km(k={coarse_size})"
+
+
+def compare_methods(chk: Checker, m: Matrix, dataset: str, beta_grid, tol_grid, methods, n_repeats=1,
+                    rhs_seed=42):
+    """analysis.cpp:137-211 on a checker: for every (beta, tol) the plain-CG baseline
+    (max_iters = max(20000, 4F)) and every method of `methods` -- (name, levels)
+    pairs with checker level dicts -- solved for generate_rhs(x, rhs_seed).b, wall
+    time averaged over n_repeats (the solver's own timer); rows as dicts in the
+    reference's CSV schema (dataset, method, clustering, f_c, beta, tol, iterations,
+    wall_time_s, speedup)."""
+    if not beta_grid or not tol_grid:
+        raise ValueError("compare_methods: beta and tol grids must be non-empty")
+    if not methods:
+        raise ValueError("compare_methods: method list must be non-empty")
+    b, _ = chk.generate_rhs(m, rhs_seed)
+    rows = []
+    for beta in beta_grid:
+        for tol in tol_grid:
+            cg_t, cg = 0.0, None
+            for _ in range(n_repeats):
+                cg = chk.solve(m, beta, b, "cg", tol=tol, max_iters=max(20000, 4 * m.n_features))
+                cg_t += cg.wall_time_s
+            cg_t /= n_repeats
+            for name, levels in methods:
+                row = dict(dataset=dataset, method=name, clustering="", f_c=0, beta=beta, tol=tol)
+                if name == "cg":
+                    rows.append(dict(row, iterations=cg.iterations, wall_time_s=cg_t, speedup=1.0))
+                    continue
+                t, s = 0.0, None
+                for _ in range(n_repeats):
+                    s = chk.solve(m, beta, b, name, levels=levels, tol=tol)
+                    t += s.wall_time_s
+                t /= n_repeats
+                fc = int(s.level_sizes[1]) if len(s.level_sizes) > 1 else 0
+                rows.append(dict(row, clustering=describe_clustering(levels[0], fc) if levels else "", f_c=fc,
+                                 iterations=s.iterations, wall_time_s=t, speedup=cg_t / t if t > 0 else 0.0))
+    return rows

@@ -245,7 +245,80 @@ __global__ void k_gram_finish(const double* __restrict__ P, int splits, const do
   }
 }
 
+// Warp per row; the row's (label, product) pairs staged in shared memory (rows
+// longer than kCoarsenStage are read from global memory instead).  Lane e is the
+// first occurrence of its label -> it sums that label's products in element
+// (= fine column) order and writes at the label's rank among the row's labels.
+constexpr int kCoarsenWarps = 8, kCoarsenStage = 256;
+
+__global__ void __launch_bounds__(kCoarsenWarps * 32)
+    k_coarsen_rows(const int32_t* __restrict__ xptr, const int32_t* __restrict__ xidx, const double* __restrict__ xval,
+                   int64_t n, const int32_t* __restrict__ label, const double* __restrict__ weight,
+                   int32_t* __restrict__ count, int32_t* __restrict__ cidx, double* __restrict__ cval) {
+  __shared__ int32_t sl_all[kCoarsenWarps][kCoarsenStage];
+  __shared__ double sp_all[kCoarsenWarps][kCoarsenStage];
+  __shared__ unsigned char sf_all[kCoarsenWarps][kCoarsenStage];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* sl = sl_all[warp];
+  double* sp = sp_all[warp];
+  unsigned char* sf = sf_all[warp];
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * kCoarsenWarps + warp; r < n;
+       r += static_cast<int64_t>(gridDim.x) * kCoarsenWarps) {
+    const int32_t b = xptr[r], len = xptr[r + 1] - b;
+    const bool staged = len <= kCoarsenStage;
+    auto lab = [&](int e) { return staged ? sl[e] : label[xidx[b + e]]; };
+    auto prod = [&](int e) {
+      if (staged) return sp[e];
+      const int32_t i = xidx[b + e];
+      return __dmul_rn(xval != nullptr ? xval[b + e] : 1.0, weight[i]);
+    };
+    auto is_first = [&](int e) {  // no earlier entry of the row has e's label
+      const int32_t t = lab(e);
+      for (int u = 0; u < e; ++u)
+        if (lab(u) == t) return false;
+      return true;
+    };
+    if (staged) {
+      for (int e = lane; e < len; e += 32) {
+        const int32_t i = xidx[b + e];
+        sl[e] = label[i];
+        sp[e] = __dmul_rn(xval != nullptr ? xval[b + e] : 1.0, weight[i]);
+      }
+      __syncwarp();
+      for (int e = lane; e < len; e += 32) sf[e] = is_first(e) ? 1 : 0;
+    }
+    __syncwarp();
+    int distinct = 0;
+    for (int e = lane; e < len; e += 32) {
+      const int32_t s = lab(e);
+      if (!(staged ? sf[e] != 0 : is_first(e))) continue;
+      ++distinct;
+      double acc = __dadd_rn(0.0, prod(e));  // the dense accumulator starts at 0.0
+      int rank = 0;  // distinct labels of the row below s
+      for (int q = 0; q < len; ++q) {
+        const int32_t t = lab(q);
+        if (q > e && t == s) acc = __dadd_rn(acc, prod(q));
+        if (t < s && (staged ? sf[q] != 0 : is_first(q))) ++rank;
+      }
+      cidx[b + rank] = s;
+      cval[b + rank] = acc;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) distinct += __shfl_xor_sync(kFull, distinct, off);
+    if (lane == 0) count[r] = distinct;
+    __syncwarp();
+  }
+}
+
 }  // namespace
+
+void coarsen_rows_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval, int64_t n,
+                      const int32_t* label, const double* weight, int32_t* count, int32_t* cidx, double* cval) {
+  if (n <= 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>((n + kCoarsenWarps - 1) / kCoarsenWarps, 148 * 16));
+  k_coarsen_rows<<<grid, kCoarsenWarps * 32, 0, s>>>(xptr, xidx, xval, n, label, weight, count, cidx, cval);
+  check("coarsen_rows");
+}
 
 void sparse_gram_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval,
                      const int32_t* tptr, const int32_t* tidx, const double* tval, int64_t n, double* G,

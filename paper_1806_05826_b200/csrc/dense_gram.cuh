@@ -37,4 +37,13 @@ int64_t gram_gemm_scratch(int64_t n);
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
                       double* scratch, cudaStream_t s);
 
+// X_c = X P on the device (coarsening.cpp:112-148), bit-identical to the host
+// restatement: per row, the products x_ri * w_i (separately rounded) of each
+// coarse column summed from 0.0 in increasing fine-column order, the row's coarse
+// columns ascending, explicit zeros from exact cancellation kept.  Row r's entries
+// land at [xptr[r], xptr[r] + count[r]) of cidx / cval (a row of X_c has at most
+// as many entries as the same row of X).
+void coarsen_rows_gpu(cudaStream_t s, const int32_t* xptr, const int32_t* xidx, const double* xval, int64_t n,
+                      const int32_t* label, const double* weight, int32_t* count, int32_t* cidx, double* cval);
+
 }  // namespace rmg

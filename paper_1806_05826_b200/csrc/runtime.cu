@@ -1335,10 +1335,10 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       coarsen_dense_gpu(s, curm.dense->view, lvl->agg, reinterpret_cast<double*>(xcd.get()), ldc);
       lvl->mat = std::make_unique<Matrix>(ctx_, curm.n(), nc, std::move(xcd), 0, ldc);
     } else if (curm.rows_only) {  // X_k = X P is row-local: every rank coarsens its own rows
-      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(curm.host_csr(), lvl->agg), curm.n_global, curm.row0, true,
+      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), curm.n_global, curm.row0, true,
                                           curm.comm);
     } else {
-      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen(curm.host_csr(), lvl->agg), true);
+      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), true);
     }
     lvl->beta = next_beta;
     lvl->label.upload(lvl->agg.label.data(), lvl->agg.label.size(), s);
@@ -1516,6 +1516,69 @@ void Method::device_gram(Matrix& m, double* G, int64_t ld) {
                     m.pattern ? nullptr : m.xt.view.val, n, G, ld);
     ctx_->sync();  // the staged CSR is released on return
   }
+}
+
+// X_c = X P of a sparse level (coarsening.cpp:112-148) on the device, bit-identical
+// to the host restatement `coarsen` (RMG_HOST_COARSEN=1 keeps the host loop).
+HostCsr Method::coarsen_level(Matrix& m, const Aggregation& agg) {
+  const HostCsr& h = m.host_csr();
+  if (std::getenv("RMG_HOST_COARSEN") != nullptr || (m.comm != nullptr && !m.rows_only) || h.nnz() == 0)
+    return coarsen(h, agg);
+  if (agg.n_fine != h.f) throw InvalidArgument("coarsen: prolongation does not match the matrix features");
+  cudaStream_t s = ctx_->stream;
+  const int64_t n = h.n, nnz = h.nnz();
+  DBuf<int32_t> xp, xi, lab, cnt, ci;
+  DBuf<double> xv, wt, cv;
+  {
+    const std::vector<int32_t> p32 = narrow(h.ptr, "row offsets"), i32 = narrow(h.idx, "column indices");
+    xp.upload(p32.data(), p32.size(), s);
+    xi.upload(i32.data(), i32.size(), s);
+  }
+  if (!m.pattern) xv.upload(h.val.data(), h.val.size(), s);
+  lab.upload(agg.label.data(), agg.label.size(), s);
+  wt.upload(agg.weight.data(), agg.weight.size(), s);
+  cnt.alloc(std::max<int64_t>(1, n));
+  ci.alloc(std::max<int64_t>(1, nnz));
+  cv.alloc(std::max<int64_t>(1, nnz));
+  const bool slog = std::getenv("RMG_SETUP_LOG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  if (slog) ctx_->sync();
+  auto t1 = std::chrono::steady_clock::now();
+  coarsen_rows_gpu(s, xp.get(), xi.get(), m.pattern ? nullptr : xv.get(), n, lab.get(), wt.get(), cnt.get(), ci.get(),
+                   cv.get());
+  if (slog) {
+    ctx_->sync();
+    std::fprintf(stderr, "[rmg setup]   coarsen kernel %.3f s\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count());
+  }
+  (void)t0;
+  std::vector<int32_t> hc(n), hi(nnz);
+  std::vector<double> hv(nnz);
+  RMG_CK(cudaMemcpyAsync(hc.data(), cnt.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  RMG_CK(cudaMemcpyAsync(hi.data(), ci.get(), nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  RMG_CK(cudaMemcpyAsync(hv.data(), cv.get(), nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx_->sync();
+  HostCsr c;
+  c.n = n;
+  c.f = agg.n_coarse;
+  c.ptr.assign(n + 1, 0);
+  for (int64_t r = 0; r < n; ++r) c.ptr[r + 1] = c.ptr[r] + hc[r];
+  c.idx.resize(c.ptr[n]);
+  c.val.resize(c.ptr[n]);
+  // row r's entries were written at its fine offsets: compact (threaded over rows)
+  const unsigned T = nnz < (1 << 20) ? 1u : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  auto body = [&](unsigned t) {
+    for (int64_t r = n * t / T; r < n * (t + 1) / T; ++r)
+      for (int64_t q = 0; q < hc[r]; ++q) {
+        c.idx[c.ptr[r] + q] = hi[h.ptr[r] + q];
+        c.val[c.ptr[r] + q] = hv[h.ptr[r] + q];
+      }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(body, t);
+  body(0);
+  for (auto& th : pool) th.join();
+  return c;
 }
 
 // pcg_vcycle: dense G_k for the levels where streaming n_k^2 doubles once costs

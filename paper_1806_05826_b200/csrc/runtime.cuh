@@ -424,6 +424,8 @@ class Method {
   const DenseGram* dgram(size_t k) const { return k < dg_.size() ? dg_[k].get() : nullptr; }
   // G = X^T X of a level on the device (bit-identical to coarse_gram's sums)
   void device_gram(Matrix& m, double* G, int64_t ld);
+  // X_c = X P of a sparse level on the device (bit-identical to coarsen)
+  HostCsr coarsen_level(Matrix& m, const Aggregation& agg);
 
  public:
   // pcg_vcycle over single-GPU CSR levels: solve_batch runs the k columns in lock step

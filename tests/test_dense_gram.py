@@ -116,3 +116,54 @@ def test_batched_cg_equals_single_and_reference(gpu, ref, method):
         for q in range(3):
             s = ref.solve(om, 0.1, B[:, q], method, tol=1e-6, max_iters=20000)
             assert abs(reps6[q].iterations - s.iterations) <= 2, (q, reps6[q].iterations, s.iterations)
+
+
+def _level_arrays(pm, k):
+    x = pm.level_matrix(k)
+    return x.row_offsets.copy(), x.column_indices.copy(), x.values.copy()
+
+
+@pytest.mark.parametrize("case", ["zipf_values", "zipf_pattern", "signed_cancel"])
+def test_device_coarsen_bit_identical_to_host(gpu, case):
+    """X_c = X P on the device (k_coarsen_rows) equals the host restatement of
+    coarsening.cpp:112-148 bit for bit: same coarse columns (ascending), same values
+    (products summed from 0.0 in fine-column order), explicit zeros from exact
+    cancellation kept."""
+    if case == "signed_cancel":
+        # features 2j and 2j + 1 share a cluster with weight 1/sqrt(2); rows hold +v / -v pairs
+        rng = np.random.default_rng(3)
+        n, f = 400, 60
+        rows, cols, vals = [], [], []
+        for r in range(n):
+            for j in rng.choice(f // 2, 5, replace=False):
+                v = float(rng.standard_normal())
+                rows += [r, r]
+                cols += [2 * j, 2 * j + 1]
+                vals += [v, -v if r % 3 == 0 else 0.5 * v]
+        x = R.csr_from_triplets(n, f, rows, cols, vals)
+        labels = [np.arange(f) // 2, np.arange(f // 2) // 5]
+        ks = [f // 2, f // 10]
+        lv = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.IMPORTED, labels=labels[i], n_clusters=k),
+                          solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == 1 else R.INNER_FCG))
+              for i, k in enumerate(ks)]
+    else:
+        x = R.synth_sparse_zipf(4000, 600, 20.0, 1.1, case == "zipf_values", 4)
+        lv = levels([70, 9])
+    m = R.DeviceMatrix(x)
+    spec = R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=lv, solver=R.SolverConfig(1e-10, 500))
+
+    def run():
+        pm = R.PreparedMethod(m, 0.5, spec)
+        out = [_level_arrays(pm, k) for k in (1, 2)]
+        w, rep = pm.solve(R.rng_normals(42, x.n_samples))
+        pm.close()
+        return out, w, rep
+
+    dev, w_dev, r_dev = run()
+    host, w_host, r_host = with_env("RMG_HOST_COARSEN", "1", run)
+    for (a, b) in zip(dev, host):
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
+    if case == "signed_cancel":
+        assert np.any(dev[0][2] == 0.0)  # the cancelled entries are stored
+    assert r_dev.iterations == r_host.iterations and np.array_equal(w_dev, w_host)
