@@ -521,6 +521,113 @@ __global__ void __launch_bounds__(kThreads, 3) k_xt_block(const int32_t* __restr
   }
 }
 
+// Hot features: one CTA per sample block b stages T[bR .. bR + R) (16 columns) in
+// shared memory once; a group of 4 lanes per hot feature sums its entries of the
+// block in row order, lane g owning columns 4g .. 4g + 3 (two 16-byte shared
+// loads per entry), entries loaded 8 at a time (broadcast within the group).
+constexpr int kHotBlkThreads = 1024;
+
+template <bool PAT>
+__global__ void __launch_bounds__(kHotBlkThreads, 1) k_xt_hotblk(BlockHot hb, const double* __restrict__ T, int k,
+                                                                int c0, int kc, int64_t N) {
+  extern __shared__ double ts[];
+  const int b = blockIdx.x;
+  const int64_t s0 = (int64_t)b * hb.R;
+  const int nb = (int)(N - s0 < (int64_t)hb.R ? N - s0 : (int64_t)hb.R);
+  // row r's 16-byte chunk c (of 8) lives at chunk c ^ (r & 7): the 8 groups of a
+  // warp read 8 different rows, and the swizzle spreads them over the banks
+  for (int e = threadIdx.x; e < nb * 16; e += kHotBlkThreads) {
+    const int r = e >> 4, q = e & 15;
+    ts[r * 16 + ((((q >> 1) ^ r) & 7) << 1) + (q & 1)] = q < kc ? __ldcg(T + (s0 + r) * k + c0 + q) : 0.0;
+  }
+  __syncthreads();
+  const int g = threadIdx.x & 3;
+  const int32_t* __restrict__ p = hb.ptr + (size_t)b * (hb.H + 1);
+  const double2* __restrict__ ts2 = reinterpret_cast<const double2*>(ts);
+  // the HL longest features: a warp each, 8 sub-groups taking every 8th entry (8
+  // independent chains), the sub-group partials reduced by a fixed shuffle tree
+  const int lane = threadIdx.x & 31, sub = lane >> 2;
+  for (int h = threadIdx.x >> 5; h < hb.HL; h += kHotBlkThreads / 32) {
+    const int e0 = p[h], e1 = p[h + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int e = e0 + sub; e < e1; e += 8) {
+      const int r = hb.row[e];
+      const double x = PAT ? 1.0 : hb.val[e];
+      const double2 lo = ts2[r * 8 + ((2 * g) ^ (r & 7))], hi = ts2[r * 8 + ((2 * g + 1) ^ (r & 7))];
+      a0 = PAT ? a0 + lo.x : fma(x, lo.x, a0);
+      a1 = PAT ? a1 + lo.y : fma(x, lo.y, a1);
+      a2 = PAT ? a2 + hi.x : fma(x, hi.x, a2);
+      a3 = PAT ? a3 + hi.y : fma(x, hi.y, a3);
+    }
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+    }
+    if (sub == 0) {
+      double2* out = reinterpret_cast<double2*>(hb.part + ((size_t)b * hb.H + h) * 16 + 4 * g);
+      out[0] = make_double2(a0, a1);
+      out[1] = make_double2(a2, a3);
+    }
+  }
+  for (int h = hb.HL + (threadIdx.x >> 2); h < hb.H; h += kHotBlkThreads / 4) {
+    const int e0 = p[h], e1 = p[h + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int e = e0;
+    for (; e + 8 <= e1; e += 8) {
+      int r[8];
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        r[u] = hb.row[e + u];
+        x[u] = PAT ? 1.0 : hb.val[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2 lo = ts2[r[u] * 8 + ((2 * g) ^ (r[u] & 7))], hi = ts2[r[u] * 8 + ((2 * g + 1) ^ (r[u] & 7))];
+        a0 = PAT ? a0 + lo.x : fma(x[u], lo.x, a0);
+        a1 = PAT ? a1 + lo.y : fma(x[u], lo.y, a1);
+        a2 = PAT ? a2 + hi.x : fma(x[u], hi.x, a2);
+        a3 = PAT ? a3 + hi.y : fma(x[u], hi.y, a3);
+      }
+    }
+    for (; e < e1; ++e) {
+      const int r = hb.row[e];
+      const double x = PAT ? 1.0 : hb.val[e];
+      const double2 lo = ts2[r * 8 + ((2 * g) ^ (r & 7))], hi = ts2[r * 8 + ((2 * g + 1) ^ (r & 7))];
+      a0 = PAT ? a0 + lo.x : fma(x, lo.x, a0);
+      a1 = PAT ? a1 + lo.y : fma(x, lo.y, a1);
+      a2 = PAT ? a2 + hi.x : fma(x, hi.x, a2);
+      a3 = PAT ? a3 + hi.y : fma(x, hi.y, a3);
+    }
+    double2* out = reinterpret_cast<double2*>(hb.part + ((size_t)b * hb.H + h) * 16 + 4 * g);
+    out[0] = make_double2(a0, a1);
+    out[1] = make_double2(a2, a3);
+  }
+}
+
+// out[feat[h]] = sum over the blocks + beta V: a CTA per hot feature, thread
+// (s, q) sums the blocks b = s (mod 8) in order, the 8 sub-sums added in s order.
+__global__ void __launch_bounds__(128) k_hot_fold(BlockHot hb, const double* __restrict__ V, double* __restrict__ out,
+                                                  double beta, int k, int c0, int kc) {
+  __shared__ double sh[8][16];
+  const int h = blockIdx.x, q = threadIdx.x & 15, sub = threadIdx.x >> 4;
+  double sum = 0.0;
+#pragma unroll 4
+  for (int b = sub; b < hb.nblk; b += 8) sum += __ldcg(hb.part + ((size_t)b * hb.H + h) * 16 + q);
+  sh[sub][q] = sum;
+  __syncthreads();
+  if (sub == 0 && q < kc) {
+    double tot = sh[0][q];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) tot += sh[u][q];
+    const int64_t o = (int64_t)hb.feat[h] * k + c0 + q;
+    out[o] = tot + beta * V[o];
+  }
+}
+
 // rows split into several items: warp per row, lanes over the items
 // (lane-strided, fixed order) + warp tree, for each column
 __global__ void k_block_finish(BlockXtSchedule bs, const double* __restrict__ V, double* __restrict__ out,
@@ -2122,7 +2229,8 @@ void spmm_hot(int grid, size_t smem, cudaStream_t s, const SparseDev& x, const d
 }
 
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const double* v, double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
+                        const BlockHot& hot, const double* v, double* out, double beta, int k, double* t, double* vp,
+                        cudaStream_t s) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
   if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
   // TMA gather passes (spmm_tma.cu) when V and T rows are 16-byte aligned
@@ -2203,6 +2311,20 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       if (bs.n_multi > 0)
         k_block_finish<<<static_cast<int>((static_cast<int64_t>(bs.n_multi) * 32 + 255) / 256), 256, 0, s>>>(
             bs, v, out, beta, k, c0, kc, first, last);
+    }
+    if (hot.H > 0) {  // hot features: from shared-memory T blocks, then folded
+      const size_t smem = static_cast<size_t>(hot.R) * 16 * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_xt_hotblk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        cudaFuncSetAttribute(k_xt_hotblk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        attr = true;
+      }
+      if (hot.val == nullptr)
+        k_xt_hotblk<true><<<hot.nblk, kHotBlkThreads, smem, s>>>(hot, t, k, c0, kc, x.rows);
+      else
+        k_xt_hotblk<false><<<hot.nblk, kHotBlkThreads, smem, s>>>(hot, t, k, c0, kc, x.rows);
+      k_hot_fold<<<hot.H, 128, 0, s>>>(hot, v, out, beta, k, c0, kc);
     }
   }
   check_launch("ridge_block");

@@ -187,8 +187,22 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
 // out = X^T (X V) + beta V for a row-major F x k block (k <= 64); x: the K1
 // layout (SELL), xt: X^T CSR (int32 sample indices), t: N x k scratch, vp:
 // F x k scratch (relabeled columns).  Per column the arithmetic order is fixed.
+// Hot features of the block X^T pass: summed per sample block of R
+// rows from a shared-memory copy of the block's T rows, one 16-double partial per
+// (block, hot feature), folded in block order; the cold features keep the chunked
+// gather pass.
+struct BlockHot {
+  int H = 0, R = 0, nblk = 0;
+  int HL = 0;                      // the first HL (longest) hot features: a warp each
+  const int32_t* ptr = nullptr;    // [nblk][H + 1] entry offsets
+  const uint16_t* row = nullptr;   // row within the block
+  const double* val = nullptr;     // nullptr: binary pattern
+  const int32_t* feat = nullptr;   // [H] the hot features (most popular first)
+  double* part = nullptr;          // [nblk][H][16]
+};
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const double* v, double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
+                        const BlockHot& hot, const double* v, double* out, double beta, int k, double* t, double* vp,
+                        cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

@@ -671,6 +671,75 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   cudaStream_t s = ctx->stream;
   bbounds.upload(bounds.data(), bounds.size(), s);
   const bool tma = tma_spmm_enabled();
+  // hot features: >= hot_min entries per sample block of R rows on
+  // average, most popular first; they leave the chunked gather pass
+  std::vector<char> is_hot(F, 0);
+  bhot = BlockHot{};
+  {
+    const char* e = std::getenv("RMG_BLOCK_HOTXT");  // "0": off; a number: the per-block minimum
+    const double hot_min = e != nullptr ? std::atof(e) : 4.0;  // measured: 4 (2.11 ms) < 8 < 2 < off (2.27 ms)
+    constexpr int64_t R = 1536;  // 1536 rows x 16 doubles = 192 KB of shared memory
+    const int64_t nblk = (n + R - 1) / R;
+    std::vector<int32_t> feat;
+    if (!tma && hot_min > 0.0 && nblk >= 2) {
+      std::vector<int64_t> order(F);
+      std::iota(order.begin(), order.end(), int64_t{0});
+      auto cnt = [&](int64_t j) { return ht.ptr[j + 1] - ht.ptr[j]; };
+      std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cnt(a) > cnt(b); });
+      for (int64_t j : order) {
+        if (static_cast<double>(cnt(j)) < hot_min * static_cast<double>(nblk) || feat.size() >= 4096) break;
+        feat.push_back(static_cast<int32_t>(j));
+      }
+    }
+    const int64_t H = static_cast<int64_t>(feat.size());
+    if (H > 0) {
+      std::vector<int32_t> ptr(static_cast<size_t>(nblk) * (H + 1), 0);
+      for (int64_t h = 0; h < H; ++h)
+        for (int64_t q = ht.ptr[feat[h]]; q < ht.ptr[feat[h] + 1]; ++q)
+          ++ptr[static_cast<size_t>(ht.idx[q] / R) * (H + 1) + h + 1];
+      int64_t run = 0;  // block-major, then feature: offsets into one entry array
+      for (int64_t b = 0; b < nblk; ++b)
+        for (int64_t h = 0; h <= H; ++h) {
+          const size_t o = static_cast<size_t>(b) * (H + 1) + h;
+          const int64_t c = h < H ? ptr[o + 1] : 0;
+          ptr[o] = static_cast<int32_t>(run);
+          run += c;
+          if (run > INT32_MAX) throw InvalidArgument("block operator: hot entries exceed the int32 range");
+        }
+      for (int64_t b = 0; b < nblk; ++b) ptr[static_cast<size_t>(b) * (H + 1) + H] =
+          b + 1 < nblk ? ptr[static_cast<size_t>(b + 1) * (H + 1)] : static_cast<int32_t>(run);
+      std::vector<uint16_t> hrow(run);
+      std::vector<double> hval(pattern ? 0 : run);
+      std::vector<int32_t> cur(ptr);
+      for (int64_t h = 0; h < H; ++h)
+        for (int64_t q = ht.ptr[feat[h]]; q < ht.ptr[feat[h] + 1]; ++q) {
+          const int64_t smp = ht.idx[q], b = smp / R;
+          const int32_t at = cur[static_cast<size_t>(b) * (H + 1) + h]++;
+          hrow[at] = static_cast<uint16_t>(smp - b * R);
+          if (!pattern) hval[at] = ht.val[q];
+        }
+      for (int32_t j : feat) is_hot[j] = 1;
+      bh_ptr.upload(ptr.data(), ptr.size(), s);
+      bh_feat.upload(feat.data(), feat.size(), s);
+      bh_row.upload(hrow.data(), hrow.size(), s);
+      if (!pattern) bh_val.upload(hval.data(), hval.size(), s);
+      bh_part.alloc(static_cast<size_t>(nblk) * H * 16);
+      RMG_CK(cudaStreamSynchronize(s));
+      bhot.H = static_cast<int>(H);
+      const char* el = std::getenv("RMG_BLOCK_HOTXT_LONG");  // entries per block for a warp of its own
+      const int64_t long_min = el != nullptr ? std::max<int64_t>(1, std::atoll(el)) : 32;
+      int64_t hl = 0;
+      while (hl < H && ht.ptr[feat[hl] + 1] - ht.ptr[feat[hl]] >= long_min * nblk) ++hl;
+      bhot.HL = static_cast<int>(hl);
+      bhot.R = static_cast<int>(R);
+      bhot.nblk = static_cast<int>(nblk);
+      bhot.ptr = bh_ptr.get();
+      bhot.row = bh_row.get();
+      bhot.val = pattern ? nullptr : bh_val.get();
+      bhot.feat = bh_feat.get();
+      bhot.part = bh_part.get();
+    }
+  }
   if (tma) {  // X's row CSR for the TMA K1 (column order: the reference's summation order per row)
     const std::vector<int32_t> i32 = narrow(xr.idx, "column indices");
     bx_idx.upload(i32.data(), i32.size(), s);
@@ -686,6 +755,7 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
     std::vector<int4> it, mu;
     int segs = 0;
     for (int64_t r = 0; r < F; ++r) {
+      if (is_hot[r]) continue;  // summed by the hot pass
       const int64_t a = bounds[static_cast<size_t>(c) * F + r], e = bounds[static_cast<size_t>(c + 1) * F + r];
       if (e - a <= kItem) {
         sh.push_back(static_cast<int32_t>(r));
@@ -749,7 +819,7 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
-  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), v, out, beta, k, bt.get(),
+  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, v, out, beta, k, bt.get(),
                      bvp.get(), ctx->stream);
   if (sync) ctx->sync();
 }

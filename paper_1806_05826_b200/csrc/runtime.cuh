@@ -220,6 +220,10 @@ struct Matrix {
   };
   DBuf<int32_t> bx_idx;        // X as a row CSR for the TMA K1 (entries in column order)
   DBuf<double> bx_val;
+  BlockHot bhot;               // hot features of the block X^T pass (H = 0: none)
+  DBuf<int32_t> bh_ptr, bh_feat;
+  DBuf<uint16_t> bh_row;
+  DBuf<double> bh_val, bh_part;
   std::vector<BlockChunkBufs> bchunk_bufs;
   std::vector<BlockXtSchedule> bviews;
   DBuf<int32_t> bbounds;       // (chunks + 1) x F entry offsets into X^T
