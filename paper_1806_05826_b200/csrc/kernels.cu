@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(HOT ? 512 : kThreads, HOT ? 1 : 3) k_spmm_sell
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ V, double* __restrict__ T,
                                                         int64_t slice0, int64_t n_slices, int k, int c0, int kc,
-                                                        int n_hot) {
+                                                        int n_hot, int acc_in) {
   extern __shared__ double vs[];
   const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
   const bool colq = q < kc;
@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(HOT ? 512 : kThreads, HOT ? 1 : 3) k_spmm_sell
           acc = c[u] >= 0 ? add : acc;
         }
       }
-      if (row >= 0 && colq) T[(int64_t)row * k + c0 + q] = acc;
+      if (row >= 0 && colq) {  // acc_in: the hot entries' sum is already in T (k_spmm_hot)
+        const int64_t o = (int64_t)row * k + c0 + q;
+        T[o] = acc_in ? T[o] + acc : acc;
+      }
     }
   }
 }
@@ -518,6 +521,60 @@ __global__ void __launch_bounds__(kThreads, 3) k_xt_block(const int32_t* __restr
     out[o] = r;
   } else {
     bs.seg[(int64_t)seg * kBlockCols + q] = acc;
+  }
+}
+
+// Hot part of K1: the H1 most popular labels' V rows (label order = vperm's) staged
+// once per persistent CTA (16-byte chunks XOR-swizzled by label); a group of 4 lanes
+// per row sums the row's hot entries (popularity order), lane g owning columns
+// 4g .. 4g + 3, and writes T; the cold SELL pass then adds the rest.
+template <bool PAT>
+__global__ void __launch_bounds__(1024, 1) k_spmm_hot(BlockHotK1 h1, const double* __restrict__ Vp, int k, int c0,
+                                                     int kc, int64_t r0, int64_t r1, double* __restrict__ T) {
+  extern __shared__ double vs[];
+  for (int e = threadIdx.x; e < h1.H1 * 16; e += blockDim.x) {
+    const int r = e >> 4, q = e & 15;
+    vs[r * 16 + ((((q >> 1) ^ r) & 7) << 1) + (q & 1)] = q < kc ? __ldg(Vp + (int64_t)r * k + c0 + q) : 0.0;
+  }
+  __syncthreads();
+  const double2* __restrict__ vs2 = reinterpret_cast<const double2*>(vs);
+  const int g = threadIdx.x & 3;
+  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x >> 2);
+  for (int64_t r = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2); r < r1; r += ngroups) {
+    const int e0 = h1.ptr[r], e1 = h1.ptr[r + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int e = e0;
+    for (; e + 8 <= e1; e += 8) {
+      int l[8];
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        l[u] = h1.lab[e + u];
+        x[u] = PAT ? 1.0 : h1.val[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2 lo = vs2[l[u] * 8 + ((2 * g) ^ (l[u] & 7))], hi = vs2[l[u] * 8 + ((2 * g + 1) ^ (l[u] & 7))];
+        a0 = PAT ? a0 + lo.x : fma(x[u], lo.x, a0);
+        a1 = PAT ? a1 + lo.y : fma(x[u], lo.y, a1);
+        a2 = PAT ? a2 + hi.x : fma(x[u], hi.x, a2);
+        a3 = PAT ? a3 + hi.y : fma(x[u], hi.y, a3);
+      }
+    }
+    for (; e < e1; ++e) {
+      const int l = h1.lab[e];
+      const double x = PAT ? 1.0 : h1.val[e];
+      const double2 lo = vs2[l * 8 + ((2 * g) ^ (l & 7))], hi = vs2[l * 8 + ((2 * g + 1) ^ (l & 7))];
+      a0 = PAT ? a0 + lo.x : fma(x, lo.x, a0);
+      a1 = PAT ? a1 + lo.y : fma(x, lo.y, a1);
+      a2 = PAT ? a2 + hi.x : fma(x, hi.x, a2);
+      a3 = PAT ? a3 + hi.y : fma(x, hi.y, a3);
+    }
+    double* out = T + r * k + c0 + 4 * g;
+    const double a[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (4 * g + u < kc) out[u] = a[u];
   }
 }
 
@@ -2225,12 +2282,12 @@ void spmm_hot(int grid, size_t smem, cudaStream_t s, const SparseDev& x, const d
     attr = true;
   }
   k_spmm_sell<PAT, NARROW, true><<<grid, 512, smem, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16, x.val, vk,
-                                                         t, bs.slice0, bs.n_slices, k, c0, kc, n_hot);
+                                                         t, bs.slice0, bs.n_slices, k, c0, kc, n_hot, 0);
 }
 
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const BlockHot& hot, const double* v, double* out, double beta, int k, double* t, double* vp,
-                        cudaStream_t s) {
+                        const BlockHot& hot, const BlockHotK1& hot1, const double* v, double* out, double beta, int k,
+                        double* t, double* vp, cudaStream_t s) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
   if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
   // TMA gather passes (spmm_tma.cu) when V and T rows are 16-byte aligned
@@ -2263,7 +2320,44 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       const int g1 = grid_for(bs.n_slices * 32, 148 * 8);
       const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
       const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
-      if (bs.n_slices > 0) {
+      if (bs.n_slices > 0 && hot1.H1 > 0 && x.col_inv != nullptr) {
+        // K1 split: hot labels from shared memory (T written), cold SELL pass adds
+        const int64_t r0 = bs.slice0 * 32, r1 = std::min<int64_t>(x.rows, (bs.slice0 + bs.n_slices) * 32);
+        static bool attr1 = false;
+        if (!attr1) {
+          cudaFuncSetAttribute(k_spmm_hot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+          cudaFuncSetAttribute(k_spmm_hot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+          attr1 = true;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const size_t hsm = static_cast<size_t>(hot1.H1) * 16 * sizeof(double);
+        if (hot1.val == nullptr)
+          k_spmm_hot<true><<<sms, 1024, hsm, s>>>(hot1, vk, k, c0, kc, r0, r1, t);
+        else
+          k_spmm_hot<false><<<sms, 1024, hsm, s>>>(hot1, vk, k, c0, kc, r0, r1, t);
+        const SparseDev& xc = hot1.cold;
+        const int gc = grid_for(bs.n_slices * 32, 148 * 8);
+        if (xc.val == nullptr) {
+          if (xc.idx16 != nullptr)
+            k_spmm_sell<true, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                   xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                   c0, kc, 0, 1);
+          else
+            k_spmm_sell<true, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                    xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                    c0, kc, 0, 1);
+        } else {
+          if (xc.idx16 != nullptr)
+            k_spmm_sell<false, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                    xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                    c0, kc, 0, 1);
+          else
+            k_spmm_sell<false, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                     xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices,
+                                                                     k, c0, kc, 0, 1);
+        }
+      } else if (bs.n_slices > 0) {
         // hot V rows in shared memory when the columns are relabeled by popularity
         const int n_hot = x.col_inv != nullptr ? static_cast<int>(std::min<int64_t>(x.cols, block_hot_rows())) : 0;
         const size_t hsm = static_cast<size_t>(n_hot) * 16 * sizeof(double);
@@ -2285,20 +2379,20 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
         } else if (x.val == nullptr) {
           if (x.idx16 != nullptr)
             k_spmm_sell<true, true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx, x.idx16,
-                                                                   x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc, 0);
+                                                                   x.val, vk, t, bs.slice0, bs.n_slices, k, c0, kc, 0, 0);
           else
             k_spmm_sell<true, false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
                                                                     x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
-                                                                    c0, kc, 0);
+                                                                    c0, kc, 0, 0);
         } else {
           if (x.idx16 != nullptr)
             k_spmm_sell<false, true, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
                                                                     x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
-                                                                    c0, kc, 0);
+                                                                    c0, kc, 0, 0);
           else
             k_spmm_sell<false, false, false><<<g1, kThreads, 0, s>>>(x.sell_off, x.sell_row, x.sell_len, x.idx,
                                                                      x.idx16, x.val, vk, t, bs.slice0, bs.n_slices, k,
-                                                                     c0, kc, 0);
+                                                                     c0, kc, 0, 0);
         }
       }
       if (units > 0) {

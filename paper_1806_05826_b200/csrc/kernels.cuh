@@ -200,9 +200,20 @@ struct BlockHot {
   const int32_t* feat = nullptr;   // [H] the hot features (most popular first)
   double* part = nullptr;          // [nblk][H][16]
 };
+// K1 split the same way: the H1 most popular labels' V rows staged in
+// shared memory per persistent CTA and summed per row from a row-major CSR of the
+// hot entries; the cold entries form a second SELL-32 layout (original columns)
+// whose pass adds onto T.
+struct BlockHotK1 {
+  int H1 = 0;
+  const int32_t* ptr = nullptr;    // [N + 1] hot entries of each row
+  const uint16_t* lab = nullptr;   // popularity label (< H1)
+  const double* val = nullptr;     // nullptr: binary pattern
+  SparseDev cold;                  // the remaining entries, SELL-32, original column indices
+};
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const BlockHot& hot, const double* v, double* out, double beta, int k, double* t, double* vp,
-                        cudaStream_t s);
+                        const BlockHot& hot, const BlockHotK1& hot1, const double* v, double* out, double beta, int k,
+                        double* t, double* vp, cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

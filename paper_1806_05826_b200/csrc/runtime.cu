@@ -671,6 +671,59 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   cudaStream_t s = ctx->stream;
   bbounds.upload(bounds.data(), bounds.size(), s);
   const bool tma = tma_spmm_enabled();
+  // K1's hot labels: the H1 most popular columns (the relabeled SELL's
+  // labels 0 .. H1-1) from shared memory, the rest in a second SELL layout
+  bhot1 = BlockHotK1{};
+  {
+    const char* e1 = std::getenv("RMG_BLOCK_HOTK1");  // rows of V kept in shared memory (0: off)
+    const int64_t h1 = std::min<int64_t>(xr.f, e1 != nullptr ? std::max<int64_t>(0, std::atoll(e1)) : 1400);
+    if (!tma && h1 > 0 && x.view.col_inv != nullptr && h1 <= 1600) {
+      std::vector<int64_t> cnt(xr.f, 0);  // the SELL's popularity ranks (same sort as upload_sell)
+      for (int64_t c : xr.idx) ++cnt[c];
+      std::vector<int32_t> inv(xr.f), rank(xr.f);
+      std::iota(inv.begin(), inv.end(), 0);
+      std::stable_sort(inv.begin(), inv.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+      for (int64_t j = 0; j < xr.f; ++j) rank[inv[j]] = static_cast<int32_t>(j);
+      std::vector<int32_t> hptr(xr.n + 1, 0);
+      std::vector<uint16_t> hlab;
+      std::vector<double> hval;
+      HostCsr cold;
+      cold.n = xr.n;
+      cold.f = xr.f;
+      cold.ptr.assign(xr.n + 1, 0);
+      std::vector<std::pair<int32_t, int64_t>> row;
+      for (int64_t r = 0; r < xr.n; ++r) {
+        row.clear();
+        for (int64_t q = xr.ptr[r]; q < xr.ptr[r + 1]; ++q) {
+          if (rank[xr.idx[q]] < h1) {
+            row.emplace_back(rank[xr.idx[q]], q);
+          } else {
+            cold.idx.push_back(xr.idx[q]);
+            cold.val.push_back(xr.val.empty() ? 1.0 : xr.val[q]);
+          }
+        }
+        std::sort(row.begin(), row.end());  // popularity order, as the SELL rows
+        for (const auto& pq : row) {
+          hlab.push_back(static_cast<uint16_t>(pq.first));
+          if (!pattern) hval.push_back(xr.val[pq.second]);
+        }
+        hptr[r + 1] = static_cast<int32_t>(hlab.size());
+        cold.ptr[r + 1] = static_cast<int64_t>(cold.idx.size());
+      }
+      if (hlab.size() < static_cast<size_t>(INT32_MAX)) {
+        bh1_ptr.upload(hptr.data(), hptr.size(), s);
+        bh1_lab.upload(hlab.data(), hlab.size(), s);
+        if (!pattern) bh1_val.upload(hval.data(), hval.size(), s);
+        bh1_cold.upload_sell(cold, pattern, s, cold.f <= 65536, false);
+        RMG_CK(cudaStreamSynchronize(s));
+        bhot1.H1 = static_cast<int>(h1);
+        bhot1.ptr = bh1_ptr.get();
+        bhot1.lab = bh1_lab.get();
+        bhot1.val = pattern ? nullptr : bh1_val.get();
+        bhot1.cold = bh1_cold.view;
+      }
+    }
+  }
   // hot features: >= hot_min entries per sample block of R rows on
   // average, most popular first; they leave the chunked gather pass
   std::vector<char> is_hot(F, 0);
@@ -819,7 +872,8 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
-  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, v, out, beta, k, bt.get(),
+  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, v, out, beta, k,
+                     bt.get(),
                      bvp.get(), ctx->stream);
   if (sync) ctx->sync();
 }

@@ -221,6 +221,11 @@ struct Matrix {
   DBuf<int32_t> bx_idx;        // X as a row CSR for the TMA K1 (entries in column order)
   DBuf<double> bx_val;
   BlockHot bhot;               // hot features of the block X^T pass (H = 0: none)
+  BlockHotK1 bhot1;            // hot labels of the block K1 (H1 = 0: none)
+  DBuf<int32_t> bh1_ptr;
+  DBuf<uint16_t> bh1_lab;
+  DBuf<double> bh1_val;
+  DeviceSparse bh1_cold;
   DBuf<int32_t> bh_ptr, bh_feat;
   DBuf<uint16_t> bh_row;
   DBuf<double> bh_val, bh_part;

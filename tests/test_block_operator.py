@@ -23,14 +23,19 @@ def test_block_matches_columns(gpu, orc, values, k):
         assert rel_diff(out[:, q], want) <= 1e-13, (q, rel_diff(out[:, q], want))
 
 
-def test_block_relabeled_wide(gpu, orc):
-    """F = 30000 > 24576: K1 runs on popularity-relabeled columns (V rows permuted)."""
-    x = R.synth_sparse_zipf(20000, 30000, 12.0, 1.05, True, 8)
+@pytest.mark.parametrize("values", [True, False])
+@pytest.mark.parametrize("k", [5, 16, 23])
+def test_block_relabeled_wide(gpu, orc, values, k):
+    """F = 30000 > 24576: K1 runs on popularity-relabeled columns (V rows permuted);
+    its 1400 most popular labels come from shared memory (k_spmm_hot), the rest from
+    the cold SELL pass, and the hot X^T features from shared-memory T blocks."""
+    x = R.synth_sparse_zipf(20000, 30000, 12.0, 1.05, values, 8)
     m = R.DeviceMatrix(x, R.default_context())
-    v = np.random.default_rng(2).standard_normal((x.n_features, 16))
-    out = m.ridge_apply_block(0.0, v)
-    for q in (0, 7, 15):
-        assert rel_diff(out[:, q], m.ridge_apply(0.0, v[:, q].copy())) <= 1e-13
+    v = np.random.default_rng(2).standard_normal((x.n_features, k))
+    out = m.ridge_apply_block(0.3, v)
+    om = to_checker(orc, x)
+    for q in sorted({0, k // 2, k - 1}):
+        assert rel_diff(out[:, q], orc.ridge_apply(om, 0.3, v[:, q].copy())) <= 1e-13
 
 
 def test_block_errors(gpu):
