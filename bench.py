@@ -46,7 +46,7 @@ CONFIGS = {
         ks=[2000, 200], normalize=True, method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg2_full"),
     "cfg4": dict(
         workload="cfg4: dense tall-skinny N=4,000,000 x F=1024, fp32 storage / fp64 arithmetic, X = U diag(i^-1.5) "
-                 "V^T + 1e-3 N(0,1); 3-level hierarchy k-means(unit-normalised columns, seed 0) 128/16 (setup on "
+                 "V^T + 1e-3 N(0,1), U and V orthonormal (CholeskyQR / QR of seeded Gaussians); 3-level hierarchy k-means(unit-normalised columns, seed 0) 128/16 (setup on "
                  "the device, DESIGN.md §4.9), inner FCG tol 1e-6; beta=1e-4; outer FCG(m=20) to rel. residual 1e-6",
         kind="lowrank", n=4_000_000, f=1024, seed=0, beta=1e-4, ks=[128, 16], normalize=True,
         method="fcg_multilevel", tol=1e-6, max_iters=1000, golden="cfg4_none", ref_rows=50_000),
@@ -408,23 +408,38 @@ def dense_algorithmic_bytes(n, f, elem_bytes, sweeps=1):
     return sweeps * n * f * elem_bytes + 8 * (f + 2 * n + 2 * f)
 
 
-def cfg4_shard_matrix(n=500_000, f=1024, seed=0):
-    """BASELINE cfg 4's per-GPU shard at 8 GPUs (500k of its 4M rows), fp32
-    storage: X = U diag(i^-1.5) V^T + 1e-3 N(0,1), V orthonormal (QR of a seeded
-    Gaussian), U = a seeded Gaussian / sqrt(4M) (columns orthonormal to O(1/sqrt(N)),
-    standing in for the rank-1024 orthonormal U of the full 4M rows).  Generated
-    on the GPU with torch (plumbing), returned as a host float32 array."""
+def cfg4_shard_matrix(n=500_000, f=1024, seed=0, n_total=4_000_000):
+    """BASELINE cfg 4 (fp32 storage): X = U diag(i^-1.5) V^T + 1e-3 N(0,1) with U the
+    n_total x 1024 orthonormal factor of a seeded Gaussian and V = Q of a seeded
+    1024^2 Gaussian; returns the first n rows (n = 500 k: one GPU's shard at 8 GPUs;
+    n = n_total: the whole matrix).  U by CholeskyQR over all n_total rows: G = A^T A
+    summed over row chunks, U = A L^-T (a 4 M x 1024 Gaussian has condition number
+    ~1.03, so one pass is orthonormal to ~1e-15).  Seeded torch generators on the GPU
+    (one per 64 k-row chunk, so every chunk is reproducible); returned as host float32."""
     import torch
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    v, _ = torch.linalg.qr(torch.randn(f, f, generator=g, device="cuda", dtype=torch.float64))
-    sig = torch.arange(1, f + 1, device="cuda", dtype=torch.float64) ** -1.5
-    w = (sig[:, None] * v.T).to(torch.float32)  # diag(sigma) V^T
-    out = torch.empty(n, f, dtype=torch.float32, device="cuda")
     step = 65536
+    dev = "cuda"
+
+    def gen(tag, r):
+        return torch.Generator(device=dev).manual_seed((seed * 1_000_003 + tag) * 100_003 + r // step)
+
+    def a_chunk(r):
+        return torch.randn(min(step, n_total - r), f, generator=gen(1, r), device=dev, dtype=torch.float64)
+
+    v, _ = torch.linalg.qr(torch.randn(f, f, generator=gen(0, 0), device=dev, dtype=torch.float64))
+    sig = torch.arange(1, f + 1, device=dev, dtype=torch.float64) ** -1.5
+    w = sig[:, None] * v.T  # diag(sigma) V^T
+    g = torch.zeros(f, f, device=dev, dtype=torch.float64)
+    for r in range(0, n_total, step):
+        a = a_chunk(r)
+        g += a.T @ a
+    lower = torch.linalg.cholesky(g)  # G = L L^T, A = U L^T
+    out = torch.empty(n, f, dtype=torch.float32, device=dev)
     for r in range(0, n, step):
         e = min(n, r + step)
-        u = torch.randn(e - r, f, generator=g, device="cuda", dtype=torch.float32) / (4_000_000 ** 0.5)
-        out[r:e] = u @ w + 1e-3 * torch.randn(e - r, f, generator=g, device="cuda", dtype=torch.float32)
+        u = torch.linalg.solve_triangular(lower, a_chunk(r)[: e - r].T, upper=False).T
+        noise = torch.randn(e - r, f, generator=gen(2, r), device=dev, dtype=torch.float64)
+        out[r:e] = (u @ w + 1e-3 * noise).to(torch.float32)
     return out.cpu().numpy()
 
 

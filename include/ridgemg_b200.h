@@ -249,6 +249,21 @@ int rmg_synth_sparse_zipf_row_range(uint64_t n, uint64_t f, double mean_nnz, dou
 int rmg_host_csr_export(const rmg_host_csr* h, uint64_t* row_offsets, uint64_t* column_indices, double* values);
 int rmg_host_csr_destroy(rmg_host_csr* h);
 
+/* ---------------------------------------------------------------- ingest
+ * read_matrix_market (matrix_market.cpp:34-148; same variants and errors) into a host
+ * CSR, csr_from_triplets semantics (sparse.cpp:27-73); a binary CSR cache stamped
+ * with the SHA-256 of its arrays (uint64 offsets, uint64 indices, fp64 values with 1.0
+ * for a binary pattern: the bytes bench.py and the fixtures hash); upload straight
+ * from a host CSR.  sha_hex: 65 bytes (64 hex digits + NUL). */
+int rmg_read_matrix_market(const char* path, rmg_host_csr** out, uint64_t* nnz);
+int rmg_host_csr_create(uint64_t n, uint64_t f, const uint64_t* row_offsets, const uint64_t* column_indices,
+                        const double* values, rmg_host_csr** out);
+int rmg_host_csr_shape(const rmg_host_csr* h, uint64_t* n, uint64_t* f, uint64_t* nnz, int32_t* has_values);
+int rmg_host_csr_sha256(const rmg_host_csr* h, char* sha_hex);
+int rmg_host_csr_save(const rmg_host_csr* h, const char* path);
+int rmg_host_csr_load(const char* path, int32_t verify, rmg_host_csr** out, uint64_t* nnz, char* sha_hex);
+int rmg_matrix_create_from_host(rmg_context* ctx, const rmg_host_csr* h, int32_t detect_pattern, rmg_matrix** out);
+
 /* ---------------------------------------------------------------- methods
  * PreparedMethod(x, beta, spec) (krylov.hpp:222-242, krylov.cpp:617-649):
  * clustering, aggregation, coarse matrices, omegas and coarse factorization

@@ -135,7 +135,7 @@ class Checker:
         self.lib = C.CDLL(path)
         for name in ("matrix_from_csr", "coarsen", "synth_sparse_zipf", "synth_dense_clustered") + (("read_matrix_market", "matrix_from_triplets") if kind == "ref" else ()):
             getattr(self.lib, self.prefix + name).restype = C.c_void_p
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _fn(self, name):
         return getattr(self.lib, self.prefix + name)

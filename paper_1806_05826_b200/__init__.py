@@ -13,6 +13,6 @@ from .ridgemg import (  # noqa: F401
     LevelSpec, MethodSpec, PreparedMethod, RhsSample, SolveReport, SolverConfig, SystemSolution, csr_from_triplets,
     default_context, from_dense, generate_rhs, method_from_string, read_matrix_market, rng_normals, shard_rows,
     solve_system, synth_dense_clustered, synth_sparse_zipf, synth_sparse_zipf_row_range, BenchRow, compare_methods,
-    to_csv, clustering_description)
+    to_csv, clustering_description, csr_sha256, save_csr, load_csr)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -108,6 +108,13 @@ SIGNATURES = {
     "rmg_comm_create": [_P, _I32, _I32, _P, _PP],
     "rmg_comm_destroy": [_P],
     "rmg_comm_create_host": [_P, _I32, _I32, _P, _P, _PP],
+    "rmg_read_matrix_market": [C.c_char_p, _PP, _P],
+    "rmg_host_csr_create": [_U64, _U64, _P, _P, _P, _PP],
+    "rmg_host_csr_shape": [_P, _P, _P, _P, _P],
+    "rmg_host_csr_sha256": [_P, C.c_char_p],
+    "rmg_host_csr_save": [_P, C.c_char_p],
+    "rmg_host_csr_load": [C.c_char_p, _I32, _PP, _P, C.c_char_p],
+    "rmg_matrix_create_from_host": [_P, _P, _I32, _PP],
     "rmg_matrix_create_csr_rows": [_P, _P, _U64, _U64, _U64, _U64, _P, _P, _P, _I32, _PP],
     "rmg_synth_sparse_zipf_row_range": [_U64, _U64, _D, _D, _I32, _U64, _U64, _U64, _PP, _P],
     "rmg_matrix_create_csr_sharded": [_P, _P, _U64, _U64, _P, _P, _P, _I32, _PP],

@@ -16,8 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libridgemg_b200.so")
-SOURCES = ["kernels.cu", "dense_level.cu", "dense_setup.cu", "fgmres.cu", "kmeans_gpu.cu", "dense_gram.cu", "spmm_tma.cu", "runtime.cu", "capi.cu", "host_setup.cpp"]
-HEADERS = ["kernels.cuh", "dense_level.cuh", "dense_setup.hpp", "fgmres.cuh", "kmeans_gpu.hpp", "dense_gram.cuh", "spmm_tma.cuh", "runtime.cuh", "host_setup.hpp"]
+SOURCES = ["kernels.cu", "dense_level.cu", "dense_setup.cu", "fgmres.cu", "kmeans_gpu.cu", "dense_gram.cu", "spmm_tma.cu", "runtime.cu", "capi.cu", "host_setup.cpp", "ingest.cpp"]
+HEADERS = ["kernels.cuh", "dense_level.cuh", "dense_setup.hpp", "fgmres.cuh", "kmeans_gpu.hpp", "dense_gram.cuh", "spmm_tma.cuh", "runtime.cuh", "host_setup.hpp", "ingest.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

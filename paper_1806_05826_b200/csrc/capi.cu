@@ -10,6 +10,7 @@
 #include <thread>
 
 #include "ridgemg_b200.h"
+#include "ingest.hpp"
 #include "runtime.cuh"
 
 struct rmg_context {
@@ -555,6 +556,83 @@ int rmg_synth_sparse_zipf_row_range(uint64_t n, uint64_t f, double mean_nnz, dou
                                                            static_cast<int64_t>(row0), static_cast<int64_t>(row1))};
     *out = h;
     if (nnz) *nnz = h->h.nnz();
+  });
+}
+
+int rmg_read_matrix_market(const char* path, rmg_host_csr** out, uint64_t* nnz) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    auto* h = new rmg_host_csr{rmg::read_matrix_market(path)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+  });
+}
+
+int rmg_host_csr_create(uint64_t n, uint64_t f, const uint64_t* rp, const uint64_t* ci, const double* v,
+                        rmg_host_csr** out) {
+  return guard([&] {
+    need(rp, "row_offsets");
+    need(out, "out");
+    rmg::HostCsr h;
+    h.n = static_cast<int64_t>(n);
+    h.f = static_cast<int64_t>(f);
+    h.ptr.assign(rp, rp + n + 1);
+    if (rp[n]) need(ci, "column_indices");
+    h.idx.assign(ci, ci + rp[n]);
+    if (v) h.val.assign(v, v + rp[n]);
+    rmg::validate_csr(h);
+    *out = new rmg_host_csr{std::move(h)};
+  });
+}
+
+int rmg_host_csr_shape(const rmg_host_csr* h, uint64_t* n, uint64_t* f, uint64_t* nnz, int32_t* has_values) {
+  return guard([&] {
+    need(h, "host csr");
+    if (n) *n = static_cast<uint64_t>(h->h.n);
+    if (f) *f = static_cast<uint64_t>(h->h.f);
+    if (nnz) *nnz = static_cast<uint64_t>(h->h.nnz());
+    if (has_values) *has_values = h->h.val.empty() ? 0 : 1;
+  });
+}
+
+int rmg_host_csr_sha256(const rmg_host_csr* h, char* sha_hex) {
+  return guard([&] {
+    need(h, "host csr");
+    need(sha_hex, "sha_hex");
+    const std::string d = rmg::csr_sha256(h->h);
+    std::memcpy(sha_hex, d.c_str(), d.size() + 1);
+  });
+}
+
+int rmg_host_csr_save(const rmg_host_csr* h, const char* path) {
+  return guard([&] {
+    need(h, "host csr");
+    need(path, "path");
+    rmg::save_csr(h->h, path);
+  });
+}
+
+int rmg_host_csr_load(const char* path, int32_t verify, rmg_host_csr** out, uint64_t* nnz, char* sha_hex) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    std::string d;
+    auto* h = new rmg_host_csr{rmg::load_csr(path, verify != 0, &d)};
+    *out = h;
+    if (nnz) *nnz = h->h.nnz();
+    if (sha_hex) std::memcpy(sha_hex, d.c_str(), d.size() + 1);
+  });
+}
+
+int rmg_matrix_create_from_host(rmg_context* ctx, const rmg_host_csr* h, int32_t detect_pattern, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
+    need(h, "host csr");
+    need(out, "out");
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, h->h, detect_pattern != 0);
   });
 }
 

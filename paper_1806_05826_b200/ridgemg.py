@@ -97,45 +97,61 @@ def from_dense(a: np.ndarray) -> FeatureMatrix:
 
 
 def read_matrix_market(path: str) -> FeatureMatrix:
-    """matrix_market.cpp:34-148 (coordinate/array; real/integer/pattern; general/symmetric)."""
-    with open(path) as fh:
-        header = fh.readline().split()
-        if len(header) < 5 or header[0] != "%%MatrixMarket":
-            raise RuntimeError(f"{path}: malformed header")
-        obj, fmt, fld, sym = (h.lower() for h in header[1:5])
-        if obj != "matrix" or fmt not in ("coordinate", "array") or fld not in ("real", "integer", "pattern") \
-                or sym not in ("general", "symmetric") or (fmt == "array" and fld == "pattern"):
-            raise RuntimeError(f"{path}: unsupported Matrix Market variant {obj} {fmt} {fld} {sym}")
-        line = fh.readline()
-        while line and (not line.strip() or line.startswith("%")):
-            line = fh.readline()
-        dims = [int(t) for t in line.split()]
-        body = [ln for ln in fh if ln.strip() and not ln.startswith("%")]
-    rows_, cols_, vals_ = [], [], []
-    if fmt == "coordinate":
-        n, f, nz = dims[:3]
-        if len(body) != nz:
-            raise RuntimeError(f"{path}: entry count mismatch: header declares {nz}, file holds {len(body)}")
-        for ln in body:
-            t = ln.split()
-            r, c = int(t[0]) - 1, int(t[1]) - 1
-            v = 1.0 if fld == "pattern" else float(t[2])
-            rows_.append(r), cols_.append(c), vals_.append(v)
-            if sym == "symmetric" and r != c:
-                rows_.append(c), cols_.append(r), vals_.append(v)
-    else:
-        n, f = dims[:2]
-        vals = [float(t) for ln in body for t in ln.split()]
-        idx = 0
-        for c in range(f):
-            for r in range(c if sym == "symmetric" else 0, n):
-                v = vals[idx]
-                idx += 1
-                if v != 0.0:
-                    rows_.append(r), cols_.append(c), vals_.append(v)
-                    if sym == "symmetric" and r != c:
-                        rows_.append(c), cols_.append(r), vals_.append(v)
-    return csr_from_triplets(n, f, rows_, cols_, vals_)
+    """matrix_market.cpp:34-148 (coordinate / array; real / integer / pattern; general /
+    symmetric), parsed by the library (rmg_read_matrix_market); RuntimeError on
+    malformed input, like the reference."""
+    lib = _lib.load()
+    h, nnz = C.c_void_p(), C.c_uint64()
+    _lib.check(lib.rmg_read_matrix_market(path.encode(), C.byref(h), C.byref(nnz)))
+    n, f = C.c_uint64(), C.c_uint64()
+    _lib.check(lib.rmg_host_csr_shape(h, C.byref(n), C.byref(f), None, None))
+    return _host_csr_to_matrix(h, n.value, f.value, nnz.value, False)
+
+
+def _host_handle(x: FeatureMatrix):
+    lib = _lib.load()
+    rp = np.ascontiguousarray(x.row_offsets, np.uint64)
+    ci = np.ascontiguousarray(x.column_indices, np.uint64)
+    v = None if x.values is None else np.ascontiguousarray(x.values, np.float64)
+    h = C.c_void_p()
+    _lib.check(lib.rmg_host_csr_create(x.n_samples, x.n_features, _ptr(rp), _ptr(ci), _ptr(v), C.byref(h)))
+    return h
+
+
+def csr_sha256(x: FeatureMatrix) -> str:
+    """SHA-256 of (uint64 row offsets, uint64 column indices, fp64 values or 1.0)."""
+    lib = _lib.load()
+    h = _host_handle(x)
+    out = C.create_string_buffer(65)
+    try:
+        _lib.check(lib.rmg_host_csr_sha256(h, out))
+    finally:
+        lib.rmg_host_csr_destroy(h)
+    return out.value.decode()
+
+
+def save_csr(x: FeatureMatrix, path: str) -> str:
+    """The binary CSR cache (ingest.cpp); returns the SHA-256 stamped into it."""
+    lib = _lib.load()
+    h = _host_handle(x)
+    out = C.create_string_buffer(65)
+    try:
+        _lib.check(lib.rmg_host_csr_save(h, path.encode()))
+        _lib.check(lib.rmg_host_csr_sha256(h, out))
+    finally:
+        lib.rmg_host_csr_destroy(h)
+    return out.value.decode()
+
+
+def load_csr(path: str, verify: bool = True) -> tuple:
+    """(FeatureMatrix, SHA-256) from a binary CSR cache; verify re-hashes the arrays."""
+    lib = _lib.load()
+    h, nnz = C.c_void_p(), C.c_uint64()
+    sha = C.create_string_buffer(65)
+    _lib.check(lib.rmg_host_csr_load(path.encode(), int(verify), C.byref(h), C.byref(nnz), sha))
+    n, f, hv = C.c_uint64(), C.c_uint64(), C.c_int32()
+    _lib.check(lib.rmg_host_csr_shape(h, C.byref(n), C.byref(f), None, C.byref(hv)))
+    return _host_csr_to_matrix(h, n.value, f.value, nnz.value, not hv.value), sha.value.decode()
 
 
 def _host_csr_to_matrix(h, n: int, f: int, nnz: int, pattern: bool) -> FeatureMatrix:

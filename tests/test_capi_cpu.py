@@ -144,3 +144,57 @@ def test_checker_generators_match_product(kind, request):
         for rows in (False, True):
             assert _msha(chk.synth_sparse_zipf(*args, row_streams=rows)) == _sha(
                 R.synth_sparse_zipf(*args, row_streams=rows)), (args, rows)
+
+
+@pytest.mark.parametrize("values", [True, False])
+def test_csr_cache_roundtrip_and_sha(tmp_path, values):
+    """The binary CSR cache (ingest.cpp): SHA-256 of the exported arrays equals
+    hashlib's, a save/load round trip is exact, a corrupted file is refused."""
+    x = R.synth_sparse_zipf(3000, 400, 15.0, 1.1, values, 7)
+    assert R.csr_sha256(x) == _sha(x)
+    path = str(tmp_path / "x.csr")
+    assert R.save_csr(x, path) == _sha(x)
+    y, sha = R.load_csr(path)
+    assert sha == _sha(x) and _sha(y) == _sha(x)
+    assert (y.values is None) == (not values)
+    raw = bytearray(open(path, "rb").read())
+    if values:
+        raw[-9] ^= 0x40  # flip a bit in the last value
+    else:  # a pattern's stored values are 1.0 by definition: corrupt a column index instead
+        raw[-8 * x.nnz - 16] ^= 0x01
+    open(path, "wb").write(bytes(raw))
+    with pytest.raises((RuntimeError, ValueError)):  # digest mismatch (or an invalid CSR)
+        R.load_csr(path)
+
+
+@pytest.mark.parametrize("text,msg", [
+    ("%%MatrixMarket matrix coordinate complex general\n2 2 1\n1 1 1 0\n", "unsupported field"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n", "entry count mismatch"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n", "out of range"),
+    ("%%MatrixMarket matrix array pattern general\n2 2\n", "pattern field"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 3 1\n1 1 1.0\n", "square"),
+])
+def test_matrix_market_errors_like_reference(tmp_path, ref, text, msg):
+    """Malformed files are refused with the reference's error (matrix_market.cpp)."""
+    path = str(tmp_path / "bad.mtx")
+    open(path, "w").write(text)
+    with pytest.raises(RuntimeError) as ours:
+        R.read_matrix_market(path)
+    assert msg in str(ours.value)
+    with pytest.raises(Exception) as theirs:
+        ref.read_matrix_market(path)
+    assert msg in str(theirs.value)
+
+
+def test_matrix_market_symmetric_and_array(tmp_path, ref):
+    """symmetric coordinate / array files: mirrored entries, zeros of arrays dropped."""
+    cases = ["%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n1 1 2.0\n3 1 -1.5\n2 2 4\n",
+             "%%MatrixMarket matrix array real general\n2 3\n1\n0\n2.5\n0\n0\n-3\n",
+             "%%MatrixMarket matrix array integer symmetric\n3 3\n1\n2\n0\n4\n5\n6\n"]
+    for i, text in enumerate(cases):
+        path = str(tmp_path / f"m{i}.mtx")
+        open(path, "w").write(text)
+        x = R.read_matrix_market(path)
+        rp, ci, v = ref.read_matrix_market(path).export()
+        assert np.array_equal(x.row_offsets, rp) and np.array_equal(x.column_indices, ci)
+        assert np.array_equal(x.value_array(), v)
