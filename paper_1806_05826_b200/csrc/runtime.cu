@@ -1724,6 +1724,16 @@ void Method::build_dense_grams() {
     size_t free_b = 0, total_b = 0;
     RMG_CK(cudaMemGetInfo(&free_b, &total_b));
     if (!(dense_bytes < sweep_bytes) || dense_bytes > 0.4 * static_cast<double>(free_b)) continue;
+    if (m.dense == nullptr) {  // assembly cost: k_gram_rows visits sum_r nnz_r^2 entries per 6144-column tile
+      const HostCsr& h = m.host_csr();
+      double visits = 0.0;
+      for (int64_t r = 0; r < h.n; ++r) {
+        const double l = static_cast<double>(h.ptr[r + 1] - h.ptr[r]);
+        visits += l * l;
+      }
+      visits *= static_cast<double>((n + 6143) / 6144);
+      if (visits > 1e11) continue;  // ~a minute of setup (cfg 5's 50 000-feature level): keep the sweeps
+    }
     auto d = std::make_unique<DenseGram>();
     d->n = n;
     d->ld = (n + 1) / 2 * 2;
