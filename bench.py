@@ -408,11 +408,11 @@ def dense_algorithmic_bytes(n, f, elem_bytes, sweeps=1):
     return sweeps * n * f * elem_bytes + 8 * (f + 2 * n + 2 * f)
 
 
-def cfg4_shard_matrix(n=500_000, f=1024, seed=0, n_total=4_000_000):
+def cfg4_shard_matrix(n=500_000, f=1024, seed=0, n_total=4_000_000, row0=0):
     """BASELINE cfg 4 (fp32 storage): X = U diag(i^-1.5) V^T + 1e-3 N(0,1) with U the
     n_total x 1024 orthonormal factor of a seeded Gaussian and V = Q of a seeded
-    1024^2 Gaussian; returns the first n rows (n = 500 k: one GPU's shard at 8 GPUs;
-    n = n_total: the whole matrix).  U by CholeskyQR over all n_total rows: G = A^T A
+    1024^2 Gaussian; returns rows [row0, row0 + n) (n = 500 k: one GPU's shard at 8
+    GPUs; n = n_total: the whole matrix).  U by CholeskyQR over all n_total rows: G = A^T A
     summed over row chunks, U = A L^-T (a 4 M x 1024 Gaussian has condition number
     ~1.03, so one pass is orthonormal to ~1e-15).  Seeded torch generators on the GPU
     (one per 64 k-row chunk, so every chunk is reproducible); returned as host float32."""
@@ -434,13 +434,14 @@ def cfg4_shard_matrix(n=500_000, f=1024, seed=0, n_total=4_000_000):
         a = a_chunk(r)
         g += a.T @ a
     lower = torch.linalg.cholesky(g)  # G = L L^T, A = U L^T
-    out = torch.empty(n, f, dtype=torch.float32, device=dev)
-    for r in range(0, n, step):
-        e = min(n, r + step)
-        u = torch.linalg.solve_triangular(lower, a_chunk(r)[: e - r].T, upper=False).T
-        noise = torch.randn(e - r, f, generator=gen(2, r), device=dev, dtype=torch.float64)
-        out[r:e] = (u @ w + 1e-3 * noise).to(torch.float32)
-    return out.cpu().numpy()
+    out = torch.empty(n, f, dtype=torch.float32, device="cpu")
+    for c in range(row0 // step * step, row0 + n, step):  # whole chunks, sliced to the row range
+        ce = min(n_total, c + step)
+        u = torch.linalg.solve_triangular(lower, a_chunk(c).T, upper=False).T
+        noise = torch.randn(ce - c, f, generator=gen(2, c), device=dev, dtype=torch.float64)
+        lo, hi = max(c, row0), min(ce, row0 + n)
+        out[lo - row0:hi - row0] = (u @ w + 1e-3 * noise)[lo - c:hi - c].to(torch.float32).cpu()
+    return out.numpy()
 
 
 def dense_operator_roofline(peak):
@@ -974,7 +975,8 @@ def run_sweep(args, cfg):
         jms, jreps = timed_batches(pj, stream, bcm, wcm, nb, betas, list(range(len(betas))), jc)
         wj = wcm.clone()
         ref_its = fx.get(f"{cfg['ref_method']}/threads1/tol{cfg['tol']:g}", {})
-        same = {"method": cfg["ref_method"], "gpu": "batched block operator, 16 columns in lock step",
+        same = {"method": cfg["ref_method"],
+                "gpu": f"batched block operator, {nb} columns in lock step" if nb > 1 else "single-RHS operator",
                 "gpu_ms_per_solve": statistics.mean(jms) / nb,
                 "gpu_ms_per_solve_by_beta": {f"{b:g}": t / nb for b, t in zip(betas, jms)},
                 "gpu_iterations_b42_by_beta": {f"{b:g}": rs[0].iterations for b, rs in zip(betas, jreps)},
@@ -1005,6 +1007,19 @@ def run_sweep(args, cfg):
             cpu = {"value": None, "unit": "ms/solve", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
     its = [[r.iterations for r in rs] for rs in reps]
+    if nb > 1:
+        roof = {"bound": "hbm", "kernel": f"level-0 block operator X^T (X V) + beta V, k = {nb} (k_spmm_sell + "
+                                          "k_xt_block + k_block_finish), CUDA events on the library stream",
+                "achieved": bb / (t_block * 1e6), "peak": peak, "unit": "GB/s", "frac": bb / (t_block * 1e6) / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": bb, "ms_per_launch": t_block,
+                "peak_kind": peak_kind, "share_of_step": fine_applies * t_block / total}
+    else:  # one right-hand side: the solve runs the single-RHS operator (K1 + K2), not the block one
+        roof = {"bound": "hbm", "kernel": "level-0 operator X^T (X v) + beta v, one RHS (K1 SELL-32 + K2 X^T "
+                                          "pass), L2 flushed, CUDA events on the library stream",
+                "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s", "frac": fb / (cold[0] * 1e6) / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": fb, "ms_per_launch": cold[0],
+                "peak_kind": peak_kind, "share_of_step": fine_applies * cold[0] / total}
+    lock = f"{nb} columns in lock step over the block operator" if nb > 1 else "one right-hand side"
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False, "scaling": "weak",
@@ -1013,16 +1028,12 @@ def run_sweep(args, cfg):
         "config": sweep_config(cfg, m.nnz, sha),
         "algorithm": (f"{cfg['method']}: PCG (krylov.cpp:94-157) preconditioned by a symmetric V-cycle over the "
                       f"config's 4-level hierarchy (damped-Jacobi pre/post smoothing; dense G_k for levels 1-2, "
-                      f"DESIGN.md §4.11, §4.14), 16 columns in lock step over the block operator"),
+                      f"DESIGN.md §4.11, §4.14), {lock}"),
         "execution": (f"{world} GPUs, independent (beta, batch) units round-robin" if world > 1 else "single GPU"),
         "iterations_per_step": its, "converged": all(r.converged for rs in reps for r in rs),
         "betas_per_step": [betas[sched(args.warmup + i)] for i in range(args.steps)],
         "setup_s": setup_s,
-        "roofline": {"bound": "hbm", "kernel": "level-0 block operator X^T (X V) + beta V, k = 16 (k_spmm_sell + "
-                                              "k_xt_block + k_block_finish), CUDA events on the library stream",
-                     "achieved": bb / (t_block * 1e6), "peak": peak, "unit": "GB/s", "frac": bb / (t_block * 1e6) / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": bb, "ms_per_launch": t_block,
-                     "peak_kind": peak_kind, "share_of_step": fine_applies * t_block / total},
+        "roofline": roof,
         "operator_roofline": {"bound": "hbm", "kernel": "K1 (X v, SELL-32) + K2 (X^T pass), one RHS, L2 flushed",
                               "algorithmic_bytes_per_apply": fb, "ms_per_apply": cold[0],
                               "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
@@ -1032,7 +1043,7 @@ def run_sweep(args, cfg):
         "e2e": {"value": e2e_value, "unit": "ms/solve", "h2d_bytes_per_step": x.n_samples * 8 * nb,
                 "d2h_bytes_per_step": x.n_features * 8 * nb,
                 "ms_per_step": [round(v, 2) for v in e2e],
-                "note": "one batched call of 16 right-hand sides per step from pinned host memory"},
+                "note": f"one batched call of {nb} right-hand side(s) per step from pinned host memory"},
         "gpu_launches": int(sum(sum(r.kernel_launches for r in rs) for rs in reps)),
         "clocks": clocks.summary()}), flush=True)
     pm.close()
@@ -1144,6 +1155,100 @@ def run_sharded(args, cfg):
         pg.destroy_process_group()
 
 
+def run_sharded_dense(args, cfg):
+    """`--shard` on cfg 4: the dense X row-sharded with per-rank input -- each rank
+    generates only its rows (cfg4_shard_matrix(row0=...)) and uploads them with
+    rmg_matrix_create_dense_rows; no host CSR anywhere.  The hierarchy is set up
+    sharded on the device: sketched k-means (S = sum_i G_i^T X_i and the column
+    norms all-reduced; exact k-means needs every row of a column on one device),
+    X_k = X_i P per rank, coarse Grams all-reduced.  A step = one solve; strong
+    scaling (total work fixed), value = max-over-ranks ms per solve."""
+    import torch
+    import paper_1806_05826_b200 as R
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    ctx = R.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    obj = [R.Comm.new_unique_id() if rank == 0 else None]
+    if pg:
+        pg.broadcast_object_list(obj, src=0)
+    comm = R.Comm(ctx, world, rank, obj[0])
+    n, f = cfg["n"], cfg["f"]
+    r0, r1 = rank * n // world, (rank + 1) * n // world
+    t0 = time.time()
+    xl = cfg4_shard_matrix(n=r1 - r0, f=f, seed=cfg["seed"], n_total=n, row0=r0)
+    gen_s = time.time() - t0
+    t0 = time.time()
+    m = R.DeviceMatrix.from_dense_rows(xl, n, r0, comm, ctx)
+    del xl
+    scfg = dict(cfg, sketch=32)
+    spec = R.MethodSpec(kind=R.method_from_string(cfg["method"]), levels=level_specs(scfg),
+                        solver=R.SolverConfig(cfg["tol"], cfg["max_iters"]))
+    pm = R.PreparedMethod(m, cfg["beta"], spec)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    dev = torch.device("cuda", local)
+    b = torch.from_numpy(R.rng_normals(42, n)).to(dev)
+    w = torch.empty(f, dtype=torch.float64, device=dev)
+
+    def step():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = pm.solve_device(b.data_ptr(), w.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), rep
+
+    for _ in range(args.warmup):
+        step()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        res = [step() for _ in range(args.steps)]
+    total = sum(r[0] for r in res)
+    if pg:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total = float(t.item())
+    value = total / args.steps
+    cold = pm.time_operator(0, 10, True)
+    if rank == 0:
+        peak, peak_kind = peaks()
+        fb = dense_algorithmic_bytes(r1 - r0, f, 4)
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: cfg 4's seeded low-rank generator, rows generated per rank",
+            "config": {"workload": cfg["workload"].replace("k-means(", "sketched k-means(d=32, "),
+                       "n_samples": n, "n_features": f, "levels": [f] + list(cfg["ks"]), "beta": cfg["beta"],
+                       "tol": cfg["tol"],
+                       "parallelism": f"row-sharded x{world} (per-rank dense input; NCCL all-reduce of the F-vector)"},
+            "algorithm": f"{cfg['method']} over a sharded sketched-k-means hierarchy (DESIGN.md §7)",
+            "iterations": [r[1].iterations for r in res], "converged": all(r[1].converged for r in res),
+            "generate_s": gen_s, "setup_s": setup_s,
+            "roofline": {"bound": "hbm", "kernel": "rank-0 shard fused dense operator (cold L2), no collective",
+                         "algorithmic_bytes_per_launch": fb, "ms_per_launch": cold[0],
+                         "achieved": fb / (cold[0] * 1e6), "peak": peak, "unit": "GB/s",
+                         "frac": fb / (cold[0] * 1e6) / peak, "traffic": None, "peak_kind": peak_kind,
+                         "note": "peak is the measured COPY figure (read + write); a read-only sweep runs above it"},
+            "e2e": None, "gpu_launches": int(sum(r[1].kernel_launches for r in res)),
+            "clocks": clocks.summary()}), flush=True)
+    pm.close()
+    m.close()
+    comm.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1162,6 +1267,8 @@ def main():
         run_reference_arm(args, cfg)
     elif args.config in ("cfg3", "cfg5") and args.shard:
         run_sharded(args, cfg)
+    elif args.config == "cfg4" and args.shard:
+        run_sharded_dense(args, cfg)
     elif args.config in ("cfg3", "cfg5"):
         run_sweep(args, cfg)
     else:

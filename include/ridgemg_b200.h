@@ -208,6 +208,14 @@ int rmg_matrix_create_csr_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n_samp
                                uint64_t n_local, uint64_t n_features, const uint64_t* row_offsets,
                                const uint64_t* column_indices, const double* values, int32_t detect_pattern,
                                rmg_matrix** out);
+/* Per-rank dense input (cfg 4 sharded): this rank's rows [row0, row0 + n_local) of a
+ * dense n_samples x n_features X (row-major, leading dimension ld, fp32 or fp64
+ * storage); no CSR is ever built.  The hierarchy is set up sharded on the device:
+ * kmeans_sketch (S all-reduced, columns normalised by the all-reduced norms) or
+ * imported labels, X_k = X P on every rank's rows, all-reduced coarse Grams. */
+int rmg_matrix_create_dense_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n_samples, uint64_t row0,
+                                 uint64_t n_local, uint64_t n_features, const void* data, uint64_t ld, int32_t fp32,
+                                 rmg_matrix** out);
 /* Replicated-setup variant: every rank passes the FULL matrix (the hierarchy is then
  * built unsharded on every rank); only this rank's nnz-balanced row block is
  * uploaded. */

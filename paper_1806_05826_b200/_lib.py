@@ -116,6 +116,7 @@ SIGNATURES = {
     "rmg_host_csr_load": [C.c_char_p, _I32, _PP, _P, C.c_char_p],
     "rmg_matrix_create_from_host": [_P, _P, _I32, _PP],
     "rmg_matrix_create_csr_rows": [_P, _P, _U64, _U64, _U64, _U64, _P, _P, _P, _I32, _PP],
+    "rmg_matrix_create_dense_rows": [_P, _P, _U64, _U64, _U64, _U64, _P, _U64, _I32, _PP],
     "rmg_synth_sparse_zipf_row_range": [_U64, _U64, _D, _D, _I32, _U64, _U64, _U64, _PP, _P],
     "rmg_matrix_create_csr_sharded": [_P, _P, _U64, _U64, _P, _P, _P, _I32, _PP],
     "rmg_matrix_shard": [_P, _P, _P, _P, _P],

@@ -25,6 +25,9 @@ struct rmg_matrix {
   rmg_matrix(rmg::Context* ctx, int64_t n, int64_t f, const rmg::DenseInput& din) : m(ctx, n, f, din) {}
   rmg_matrix(rmg::Context* ctx, rmg::HostCsr local, int64_t n_global, int64_t row0, bool detect, rmg::Comm* comm)
       : m(ctx, std::move(local), n_global, row0, detect, comm) {}
+  rmg_matrix(rmg::Context* ctx, int64_t n_global, int64_t row0, int64_t n_local, int64_t f,
+             const rmg::DenseInput& din, rmg::Comm* comm)
+      : m(ctx, n_global, row0, n_local, f, din, comm) {}
 };
 struct rmg_host_csr {
   rmg::HostCsr h;
@@ -314,6 +317,24 @@ int rmg_matrix_create_csr_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n, uin
     RMG_CK(cudaSetDevice(ctx->c.device));
     *out = new rmg_matrix(&ctx->c, std::move(h), static_cast<int64_t>(n), static_cast<int64_t>(row0),
                           detect_pattern != 0, &comm->c);
+  });
+}
+
+int rmg_matrix_create_dense_rows(rmg_context* ctx, rmg_comm* comm, uint64_t n, uint64_t row0, uint64_t n_local,
+                                 uint64_t f, const void* data, uint64_t ld, int32_t fp32, rmg_matrix** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto lk_ = hold(&ctx->c);
+    need(comm, "comm");
+    need(out, "out");
+    if (n_local != 0 && f != 0) need(data, "data");
+    rmg::DenseInput din;
+    din.data = data;
+    din.fp32 = fp32 != 0;
+    din.ld = static_cast<int64_t>(ld);
+    RMG_CK(cudaSetDevice(ctx->c.device));
+    *out = new rmg_matrix(&ctx->c, static_cast<int64_t>(n), static_cast<int64_t>(row0), static_cast<int64_t>(n_local),
+                          static_cast<int64_t>(f), din, &comm->c);
   });
 }
 

@@ -388,11 +388,11 @@ __global__ void k_sketch_sparse(const int32_t* __restrict__ ptr, const int32_t* 
 }
 
 // G (n x d, row-major) of +-1 for the dense sketch
-__global__ void k_sketch_signs(int64_t n, int d, uint64_t seed, double* g) {
+__global__ void k_sketch_signs(int64_t n, int d, uint64_t seed, double* g, int64_t row0) {
   const int64_t total = n * d;
   for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    g[q] = sketch_negative(seed, q / d, static_cast<int>(q % d), d) ? -1.0 : 1.0;
+    g[q] = sketch_negative(seed, row0 + q / d, static_cast<int>(q % d), d) ? -1.0 : 1.0;
 }
 
 // S[c][j] = st[j][c]
@@ -418,16 +418,16 @@ void sketch_sparse_gpu(cudaStream_t s, const SparseDev& xt, const double* norm, 
 }
 
 void sketch_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t f, int64_t ld, int d, uint64_t seed,
-                      double* S, int64_t ldS) {
+                      double* S, int64_t ldS, int64_t row0) {
   if (d < 1 || d > 32) throw InvalidArgument("kmeans_sketch: sketch dimension outside [1, 32]");
   const int64_t ldg = even(d);
   DBuf<double> g(static_cast<size_t>(std::max<int64_t>(1, n)) * ldg), st(static_cast<size_t>(std::max<int64_t>(1, f)) * d);
   RMG_CK(cudaMemsetAsync(g.get(), 0, g.size() * sizeof(double), s));
   if (ldg == d) {
-    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g.get());
+    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g.get(), row0);
   } else {  // odd d: fill a d-wide scratch, then pad rows to even width
     DBuf<double> g0(static_cast<size_t>(std::max<int64_t>(1, n)) * d);
-    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g0.get());
+    k_sketch_signs<<<grid_for(n * d), kT, 0, s>>>(n, d, seed, g0.get(), row0);
     RMG_CK(cudaMemcpy2DAsync(g.get(), ldg * sizeof(double), g0.get(), d * sizeof(double), d * sizeof(double), n,
                              cudaMemcpyDeviceToDevice, s));
     RMG_CK(cudaStreamSynchronize(s));

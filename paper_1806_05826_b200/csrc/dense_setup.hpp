@@ -45,6 +45,6 @@ std::vector<double> gram_dense_gpu(cudaStream_t s, const DenseDev& x);
 void sketch_sparse_gpu(cudaStream_t s, const SparseDev& xt, const double* norm, int d, uint64_t seed, double* S,
                        int64_t ldS, int64_t row0 = 0);
 void sketch_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t f, int64_t ld, int d, uint64_t seed,
-                      double* S, int64_t ldS);
+                      double* S, int64_t ldS, int64_t row0 = 0);
 
 }  // namespace rmg

@@ -959,6 +959,39 @@ Matrix::Matrix(Context* c, int64_t n, int64_t f, DBuf<char>&& data, int fp32, in
   init_dense(std::move(data), fp32, ld, n);
 }
 
+Matrix::Matrix(Context* c, int64_t n_glob, int64_t r0, int64_t n_local, int64_t f, const DenseInput& din, Comm* cm)
+    : ctx(c), comm(cm) {
+  if (comm == nullptr) throw InvalidArgument("rmg_matrix_create_dense_rows: needs a communicator");
+  if (r0 < 0 || n_local < 0 || r0 + n_local > n_glob)
+    throw InvalidArgument("rmg_matrix_create_dense_rows: rows [row0, row0 + n_local) outside [0, n_samples)");
+  if (din.ld < f) throw InvalidArgument("dense X: leading dimension below the feature count");
+  host.n = n_local;
+  host.f = f;
+  host_ok = false;
+  n_global = n_glob;
+  rows_only = true;
+  row0 = r0;
+  row1 = r0 + n_local;
+  RMG_CK(cudaSetDevice(ctx->device));
+  alloc_comm_buffers();
+  init_dense_from_host(din.data, din.fp32, din.ld, n_local);
+}
+
+Matrix::Matrix(Context* c, int64_t n_glob, int64_t r0, int64_t n_local, int64_t f, DBuf<char>&& data, int fp32,
+               int64_t ld, Comm* cm)
+    : ctx(c), comm(cm) {
+  host.n = n_local;
+  host.f = f;
+  host_ok = false;
+  n_global = n_glob;
+  rows_only = true;
+  row0 = r0;
+  row1 = r0 + n_local;
+  RMG_CK(cudaSetDevice(ctx->device));
+  alloc_comm_buffers();
+  init_dense(std::move(data), fp32, ld, n_local);
+}
+
 // The canonical CSR of a device-resident dense X (exact zeros not stored, as
 // dense_to_csr), built on first use by host-only setup (leader-follower).
 const HostCsr& Matrix::host_csr() {
@@ -1420,6 +1453,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     int64_t nc = 0;
     std::vector<int64_t> lab;
     const rmg_level_spec& cs = specs_[k].spec;
+    const bool dense_rows = curm.rows_only && curm.dense != nullptr;  // per-rank dense rows
     if (dev && cs.clustering_kind == RMG_CLUSTER_KMEANS) {
       const int64_t k_c = static_cast<int64_t>(cs.target_size);
       if (k_c < 1 || k_c > cur_f) throw InvalidArgument("kmeans: k outside [1, F]");
@@ -1441,7 +1475,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       lab = specs_[k].labels;
     } else if (curm.rows_only) {  // every rank holds only its rows: no exact column clustering
       throw InvalidArgument(
-          "build_hierarchy: a row-sharded matrix (rmg_matrix_create_csr_rows) needs kmeans_sketch or imported "
+          "build_hierarchy: a row-sharded matrix (rmg_matrix_create_csr_rows / _dense_rows) needs kmeans_sketch or imported "
           "labels; exact k-means / leader-follower need every row of a column on one device");
     } else {
       lab = run_clustering(curm.host_csr(), specs_[k], &nc, s);
@@ -1458,6 +1492,11 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       DBuf<char> xcd(std::max<size_t>(1, static_cast<size_t>(curm.n()) * ldc * sizeof(double)));
       coarsen_dense_gpu(s, curm.dense->view, lvl->agg, reinterpret_cast<double*>(xcd.get()), ldc);
       lvl->mat = std::make_unique<Matrix>(ctx_, curm.n(), nc, std::move(xcd), 0, ldc);
+    } else if (dense_rows) {  // X_k = X P on this rank's rows, on the device
+      const int64_t ldc = (nc + 3) / 4 * 4, nl = curm.n_local();
+      DBuf<char> xcd(std::max<size_t>(1, static_cast<size_t>(nl) * ldc * sizeof(double)));
+      coarsen_dense_gpu(s, curm.dense->view, lvl->agg, reinterpret_cast<double*>(xcd.get()), ldc);
+      lvl->mat = std::make_unique<Matrix>(ctx_, curm.n_global, curm.row0, nl, nc, std::move(xcd), 0, ldc, curm.comm);
     } else if (curm.rows_only) {  // X_k = X P is row-local: every rank coarsens its own rows
       lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), curm.n_global, curm.row0, true,
                                           curm.comm);
@@ -1550,7 +1589,8 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
 // (kmeans_dense_gpu, bit-identical arithmetic) on S = G^T X, G an N x d sign
 // matrix, the columns of X unit-normalised first when asked.
 std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& cs, int64_t* nc) {
-  if (m.comm != nullptr && m.dense != nullptr) throw InvalidArgument("kmeans_sketch: sharded dense matrices unsupported");
+  if (m.comm != nullptr && m.dense != nullptr && !m.rows_only)
+    throw InvalidArgument("kmeans_sketch: replicated-setup sharded dense matrices unsupported");
   const int64_t f = m.f(), n = m.n();
   const int64_t k = static_cast<int64_t>(cs.target_size);
   if (k < 1 || k > f) throw InvalidArgument("kmeans: k outside [1, F]");
@@ -1560,7 +1600,25 @@ std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& 
   const int64_t ldS = (f + 1) / 2 * 2;
   DBuf<double> S(static_cast<size_t>(d) * ldS);
   RMG_CK(cudaMemsetAsync(S.get(), 0, S.size() * sizeof(double), s));
-  if (m.dense) {
+  if (m.dense && m.rows_only) {  // this rank's rows; columns scaled by the all-reduced norms
+    const int64_t ldx = (f + 1) / 2 * 2, nl = m.n_local();
+    DBuf<double> xc(static_cast<size_t>(std::max<int64_t>(1, nl)) * ldx);
+    dense_columns_f64(s, m.dense->view, false, xc.get(), ldx);
+    sketch_dense_gpu(s, xc.get(), nl, f, ldx, d, cs.seed, S.get(), ldS, m.row0);
+    m.allreduce_sums(S.get(), S.get(), static_cast<int64_t>(d) * ldS);
+    if (cs.normalize_columns) {  // G^T (X D^-1) = (G^T X) D^-1, D = the global column norms
+      DBuf<double> nrm(std::max<int64_t>(1, f));
+      m.gram_diagonal(0.0, nrm.get());
+      std::vector<double> v(f), hs(static_cast<size_t>(d) * ldS);
+      if (f) RMG_CK(cudaMemcpyAsync(v.data(), nrm.get(), f * 8, cudaMemcpyDeviceToHost, s));
+      RMG_CK(cudaMemcpyAsync(hs.data(), S.get(), hs.size() * 8, cudaMemcpyDeviceToHost, s));
+      ctx_->sync();
+      for (int c = 0; c < d; ++c)
+        for (int64_t j = 0; j < f; ++j)
+          if (v[j] > 0.0) hs[c * ldS + j] /= std::sqrt(v[j]);
+      S.upload(hs.data(), hs.size(), s);
+    }
+  } else if (m.dense) {
     const int64_t ldx = (f + 1) / 2 * 2;
     DBuf<double> xc(static_cast<size_t>(std::max<int64_t>(1, n)) * ldx);
     dense_columns_f64(s, m.dense->view, cs.normalize_columns != 0, xc.get(), ldx);
@@ -1592,7 +1650,17 @@ std::vector<int64_t> Method::sketch_clustering(Matrix& m, const rmg_level_spec& 
 std::vector<double> Method::level_gram(Matrix& m, double beta) {
   const int64_t n = m.f();
   if (m.gram_cache.empty()) {
-    if (m.device_setup()) {
+    if (m.dense != nullptr && m.rows_only) {  // this rank's rows, summed over the ranks
+      std::vector<double> g = gram_dense_gpu(ctx_->stream, m.dense->view);
+      DBuf<double> d;
+      d.upload(g.data(), g.size(), ctx_->stream);
+      if (!g.empty()) {
+        m.allreduce_sums(d.get(), d.get(), static_cast<int64_t>(g.size()));
+        RMG_CK(cudaMemcpyAsync(g.data(), d.get(), g.size() * 8, cudaMemcpyDeviceToHost, ctx_->stream));
+      }
+      ctx_->sync();
+      m.gram_cache = std::move(g);
+    } else if (m.device_setup()) {
       m.gram_cache = gram_dense_gpu(ctx_->stream, m.dense->view);
     } else if ((m.comm != nullptr && !m.rows_only) || m.dense != nullptr ||
                (std::getenv("RMG_HOST_GRAM") != nullptr && m.comm == nullptr)) {
@@ -1620,7 +1688,13 @@ void Method::device_gram(Matrix& m, double* G, int64_t ld) {
   cudaStream_t s = ctx_->stream;
   const int64_t n = m.f();
   if (m.dense != nullptr) {
-    if (m.gram_cache.empty()) m.gram_cache = gram_dense_gpu(s, m.dense->view);
+    if (m.gram_cache.empty()) {
+      if (m.rows_only) {
+        (void)level_gram(m, 0.0);  // fills the all-reduced cache
+      } else {
+        m.gram_cache = gram_dense_gpu(s, m.dense->view);
+      }
+    }
     for (int64_t i = 0; i < n; ++i)
       RMG_CK(cudaMemcpyAsync(G + i * ld, m.gram_cache.data() + i * n, n * 8, cudaMemcpyHostToDevice, s));
     ctx_->sync();
@@ -1740,7 +1814,8 @@ void Method::build_dense_grams() {
     d->G.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * d->ld);
     d->scratch.alloc(static_cast<size_t>(std::max<int64_t>(1, gram_gemm_scratch(n))));
     device_gram(m, d->G.get(), d->ld);
-    if (m.comm != nullptr) m.allreduce_sums(d->G.get(), d->G.get(), n * d->ld);  // replicated G_k
+    if (m.comm != nullptr && m.dense == nullptr)  // replicated G_k (dense levels: summed in level_gram)
+      m.allreduce_sums(d->G.get(), d->G.get(), n * d->ld);
     dg_[k] = std::move(d);
   }
 }

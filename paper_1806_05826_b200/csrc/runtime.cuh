@@ -249,6 +249,11 @@ struct Matrix {
   // rows, or from a device buffer already padded to ld (coarse levels)
   Matrix(Context* c, int64_t n, int64_t f, const DenseInput& din);
   Matrix(Context* c, int64_t n, int64_t f, DBuf<char>&& data, int fp32, int64_t ld);
+  // per-rank dense input: rows [row0, row0 + n_local) of an n_global x f X (host rows,
+  // or a device buffer padded to ld for coarse levels); setup on it is sharded
+  Matrix(Context* c, int64_t n_global, int64_t row0, int64_t n_local, int64_t f, const DenseInput& din, Comm* comm);
+  Matrix(Context* c, int64_t n_global, int64_t row0, int64_t n_local, int64_t f, DBuf<char>&& data, int fp32,
+         int64_t ld, Comm* comm);
   bool host_ok = true;  // host holds the CSR view
   const HostCsr& host_csr();  // built from the device copy on first use
   bool device_setup() const { return dense != nullptr && comm == nullptr && !host_ok; }

@@ -342,6 +342,26 @@ class DeviceMatrix:
         return self
 
     @classmethod
+    def from_dense_rows(cls, a_local, n_samples: int, row0: int, comm: "Comm",
+                        ctx: Optional[Context] = None) -> "DeviceMatrix":
+        """Per-rank dense input (rmg_matrix_create_dense_rows): this rank's rows [row0,
+        row0 + len(a_local)) of a dense n_samples-row X; hierarchy setup sharded."""
+        a = np.asarray(a_local)
+        fp32 = a.dtype == np.float32
+        a = np.ascontiguousarray(a, np.float32 if fp32 else np.float64)
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.x = None
+        self.comm = comm
+        self.h = C.c_void_p()
+        nl, f = a.shape
+        _lib.check(self.lib.rmg_matrix_create_dense_rows(self.ctx.h, comm.h, n_samples, row0, nl, f, _ptr(a), f,
+                                                         int(fp32), C.byref(self.h)))
+        self._query()
+        return self
+
+    @classmethod
     def from_dense(cls, a, ctx: Optional[Context] = None, comm: Optional["Comm"] = None) -> "DeviceMatrix":
         """Dense X (row-major, float64 or float32 storage; arithmetic stays fp64):
         the operator is one fused sweep over X.  n_features <= 1024."""
@@ -372,13 +392,10 @@ class DeviceMatrix:
 
     def _query(self):
         r0, r1, nr, rk = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_int32()
-        if hasattr(self.lib, "rmg_matrix_shard"):
-            _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
-            self.row_range = (r0.value, r1.value)
-        else:
-            self.row_range = (0, x.n_samples)
         n, f, z, pat = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int32()
         _lib.check(self.lib.rmg_matrix_shape(self.h, C.byref(n), C.byref(f), C.byref(z), C.byref(pat)))
+        _lib.check(self.lib.rmg_matrix_shard(self.h, C.byref(r0), C.byref(r1), C.byref(nr), C.byref(rk)))
+        self.row_range = (r0.value, r1.value)
         self.n_samples, self.n_features, self.nnz, self.is_pattern = n.value, f.value, z.value, bool(pat.value)
 
     def close(self):
