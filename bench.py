@@ -1250,6 +1250,8 @@ def run_sharded_dense(args, cfg):
 
 
 def main():
+    # stdout carries exactly one JSON line: keep NCCL's banner off it unless asked for
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
