@@ -854,6 +854,16 @@ def block_bytes(n, f, nnz, pattern, k):
     return 2 * nnz * (4 + s_val) + 4 * (n + 1) + 4 * (f + 1) + 8 * (f + 2 * n + 2 * f) * k
 
 
+def sweep_algorithm_text(cfg, lock):
+    if cfg["method"] == "pcg_vcycle_additive":
+        return (f"pcg_vcycle_additive: PCG (krylov.cpp:94-157) preconditioned by the config's 4-level hierarchy with "
+                f"the finest level entered additively, z = D_0^-1 r + P_0 V_1(P_0^T r), V_1 the symmetric "
+                f"damped-Jacobi V-cycle of levels 1-3 (dense G_k for levels 1-2; DESIGN.md §4.11, §4.14, §4.15), {lock}")
+    return (f"{cfg['method']}: PCG (krylov.cpp:94-157) preconditioned by a symmetric V-cycle over the "
+            f"config's 4-level hierarchy (damped-Jacobi pre/post smoothing; dense G_k for levels 1-2, "
+            f"DESIGN.md §4.11, §4.14), {lock}")
+
+
 def run_sweep(args, cfg):
     """BASELINE cfg 3: a beta sweep over one fixed hierarchy with 16 right-hand sides
     solved as a batched block operator.  A step = one beta's batch (one
@@ -1026,9 +1036,7 @@ def run_sweep(args, cfg):
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
         "config": sweep_config(cfg, m.nnz, sha),
-        "algorithm": (f"{cfg['method']}: PCG (krylov.cpp:94-157) preconditioned by a symmetric V-cycle over the "
-                      f"config's 4-level hierarchy (damped-Jacobi pre/post smoothing; dense G_k for levels 1-2, "
-                      f"DESIGN.md §4.11, §4.14), {lock}"),
+        "algorithm": sweep_algorithm_text(cfg, lock),
         "execution": (f"{world} GPUs, independent (beta, batch) units round-robin" if world > 1 else "single GPU"),
         "iterations_per_step": its, "converged": all(r.converged for rs in reps for r in rs),
         "betas_per_step": [betas[sched(args.warmup + i)] for i in range(args.steps)],
@@ -1263,8 +1271,11 @@ def main():
     ap.add_argument("--no-large-operator", action="store_true",
                     help="skip the cfg5-shard operator roofline (about 20 s of setup)")
     ap.add_argument("--shard", action="store_true", help="row-shard X across ranks (strong scaling)")
+    ap.add_argument("--method", default=None, help="override the config's solver (e.g. pcg_vcycle)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.method:
+        cfg["method"] = args.method
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     elif args.config in ("cfg3", "cfg5") and args.shard:

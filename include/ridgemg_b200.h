@@ -53,7 +53,12 @@ typedef enum {
    * no reference counterpart): plain PCG with a symmetric V-cycle over the
    * same hierarchy, damped-Jacobi pre- and post-smoothing at every level above the coarsest,
    * the coarsest level solved directly */
-  RMG_METHOD_PCG_VCYCLE = 5
+  RMG_METHOD_PCG_VCYCLE = 5,
+  /* extension: PCG with the same hierarchy entered additively at the finest
+   * level -- z = D_0^-1 r + P_0 V_1(P_0^T r), V_1 the symmetric V-cycle of levels >= 1 (dense
+   * coarse Grams where they are smaller than the level's sweep), so an iteration costs one
+   * fine-level operator application instead of three.  SPD, so plain PCG applies. */
+  RMG_METHOD_PCG_VCYCLE_ADDITIVE = 6
 } rmg_method_kind;
 
 /* krylov.hpp:135-146 ClusteringChoice::Kind (+ imported labels for parity runs) */

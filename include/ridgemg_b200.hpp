@@ -95,7 +95,8 @@ struct LevelSpec {
 // krylov.hpp:207-218
 enum class MethodKind { cg = RMG_METHOD_CG, jacobi_cg = RMG_METHOD_JACOBI_CG, fcg_twolevel = RMG_METHOD_FCG_TWOLEVEL,
                         fcg_multilevel = RMG_METHOD_FCG_MULTILEVEL, fgmres_twolevel = RMG_METHOD_FGMRES_TWOLEVEL,
-                        pcg_vcycle = RMG_METHOD_PCG_VCYCLE /* extension */ };
+                        pcg_vcycle = RMG_METHOD_PCG_VCYCLE /* extension */,
+                        pcg_vcycle_additive = RMG_METHOD_PCG_VCYCLE_ADDITIVE /* extension */ };
 
 inline MethodKind method_from_string(const std::string& s) {  // krylov.cpp:574-581
   if (s == "cg") return MethodKind::cg;
@@ -104,6 +105,7 @@ inline MethodKind method_from_string(const std::string& s) {  // krylov.cpp:574-
   if (s == "fcg_multilevel") return MethodKind::fcg_multilevel;
   if (s == "fgmres_twolevel") return MethodKind::fgmres_twolevel;
   if (s == "pcg_vcycle") return MethodKind::pcg_vcycle;
+  if (s == "pcg_vcycle_additive") return MethodKind::pcg_vcycle_additive;
   throw std::invalid_argument("unknown method: '" + s + "'");
 }
 

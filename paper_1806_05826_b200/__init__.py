@@ -8,7 +8,7 @@ this package is its ctypes binding plus a Python mirror of the reference's
 from ._lib import LIB_PATH, RmgCudaError, load  # noqa: F401
 from .ridgemg import (  # noqa: F401
     CG, DIRECT_CHOLESKY, FCG_MULTILEVEL, FCG_TWOLEVEL, FGMRES_TWOLEVEL, IMPORTED, INNER_CG, INNER_FCG, JACOBI_CG, KMEANS,
-    KMEANS_SKETCH, PCG_VCYCLE,
+    KMEANS_SKETCH, PCG_VCYCLE, PCG_VCYCLE_ADDITIVE,
     LEADER_TARGET, LEADER_TOLERANCE, ClusteringChoice, CoarseSolveChoice, Comm, Context, DeviceMatrix, FeatureMatrix,
     LevelSpec, MethodSpec, PreparedMethod, RhsSample, SolveReport, SolverConfig, SystemSolution, csr_from_triplets,
     default_context, from_dense, generate_rhs, method_from_string, read_matrix_market, rng_normals, shard_rows,

@@ -1851,6 +1851,17 @@ __global__ void __launch_bounds__(kThreads) k_vc_add(const double* __restrict__ 
   if (done != nullptr && *done) return;
   grid_stride(n, [&](int64_t i) { e[i] = x1[i] + e[i]; });
 }
+// additive finest level: z = dinv r + w_i e_c(label_i) (Jacobi term first, then the
+// prolonged coarse correction; one pass instead of pre + prolong + add)
+__global__ void __launch_bounds__(kThreads) k_vc_jacobi_prolong(const double* __restrict__ r,
+                                                                const double* __restrict__ dinv,
+                                                                const int32_t* __restrict__ label,
+                                                                const double* __restrict__ weight,
+                                                                const double* __restrict__ ec, double* __restrict__ z,
+                                                                int64_t n, const int32_t* done) {
+  if (done != nullptr && *done) return;
+  grid_stride(n, [&](int64_t i) { z[i] = dinv[i] * r[i] + weight[i] * ec[label[i]]; });
+}
 __global__ void __launch_bounds__(kThreads) k_vc_post(const double* __restrict__ x2, const double* __restrict__ r,
                                                       const double* __restrict__ y2, const double* __restrict__ dinv,
                                                       double w, double* __restrict__ z, int64_t n, const int32_t* done) {
@@ -2004,6 +2015,17 @@ __global__ void __launch_bounds__(kThreads) k_bvc_post(const double* __restrict_
 __global__ void __launch_bounds__(kThreads) k_bsub(const double* __restrict__ r, double* __restrict__ y, int64_t nk) {
   grid_stride(nk, [&](int64_t q) { y[q] = r[q] - y[q]; });
 }
+__global__ void __launch_bounds__(kThreads) k_bvc_jacobi_prolong(const double* __restrict__ r,
+                                                                 const double* __restrict__ dinv,
+                                                                 const int32_t* __restrict__ label,
+                                                                 const double* __restrict__ weight,
+                                                                 const double* __restrict__ ec,
+                                                                 double* __restrict__ z, int64_t n, int k) {
+  grid_stride(n * k, [&](int64_t q) {
+    const int64_t i = q / k;
+    z[q] = dinv[i] * r[q] + weight[i] * ec[(int64_t)label[i] * k + q % k];
+  });
+}
 __global__ void __launch_bounds__(kThreads) k_badd(const double* __restrict__ x1, double* __restrict__ e, int64_t nk) {
   grid_stride(nk, [&](int64_t q) { e[q] = x1[q] + e[q]; });
 }
@@ -2141,6 +2163,15 @@ void launch_vc_sub(const double* r, double* y, int64_t n, const int32_t* done, c
 void launch_vc_add(const double* x1, double* e, int64_t n, const int32_t* done, cudaStream_t s) {
   k_vc_add<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(x1, e, n, done);
   check_launch("vc_add");
+}
+void launch_vc_jacobi_prolong(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                              const double* ec, double* z, int64_t n, const int32_t* done, cudaStream_t s) {
+  k_vc_jacobi_prolong<<<grid_for(n, 148 * 4), kThreads, 0, s>>>(r, dinv, label, weight, ec, z, n, done);
+  check_launch("vc_jacobi_prolong");
+}
+void launch_bvc_jacobi_prolong(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                               const double* ec, double* z, int64_t n, int k, cudaStream_t s) {
+  k_bvc_jacobi_prolong<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(r, dinv, label, weight, ec, z, n, k);
 }
 void launch_vc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
                     int64_t n, const int32_t* done, cudaStream_t s) {

@@ -246,6 +246,11 @@ void launch_vc_pre(const double* r, const double* dinv, double w, double* x1, in
                    cudaStream_t s);
 void launch_vc_sub(const double* r, double* y, int64_t n, const int32_t* done, cudaStream_t s);
 void launch_vc_add(const double* x1, double* e, int64_t n, const int32_t* done, cudaStream_t s);
+// additive finest level (pcg_vcycle_additive): z = dinv r + w_i e_c(label_i)
+void launch_vc_jacobi_prolong(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                              const double* ec, double* z, int64_t n, const int32_t* done, cudaStream_t s);
+void launch_bvc_jacobi_prolong(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                               const double* ec, double* z, int64_t n, int k, cudaStream_t s);
 void launch_vc_post(const double* x2, const double* r, const double* y2, const double* dinv, double w, double* z,
                     int64_t n, const int32_t* done, cudaStream_t s);
 // batched pcg_vcycle (k right-hand sides in lock step; row-major n x k blocks)

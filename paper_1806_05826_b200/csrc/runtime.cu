@@ -1390,7 +1390,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
                const rmg_solver_config& sol)
     : solver(sol), ctx_(x->ctx), fine_(x), beta_(beta), kind_(kind) {
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
-  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_PCG_VCYCLE)
+  if (kind < RMG_METHOD_CG || kind > RMG_METHOD_PCG_VCYCLE_ADDITIVE)
     throw InvalidArgument("unknown method kind " + std::to_string(kind));
   if (solver.max_iters > static_cast<uint64_t>(INT32_MAX)) throw InvalidArgument("max_iters too large");
   const int keep0 = static_cast<int>(std::max<uint64_t>(solver.truncation, 1));
@@ -1406,7 +1406,8 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
   if (n_levels == 0 || levels == nullptr)
     throw InvalidArgument(kind != RMG_METHOD_FCG_MULTILEVEL ? "two-level method requires one level spec"
                                                             : "multilevel method requires level specs");
-  const bool multi = kind == RMG_METHOD_FCG_MULTILEVEL || kind == RMG_METHOD_PCG_VCYCLE;
+  const bool multi = kind == RMG_METHOD_FCG_MULTILEVEL || kind == RMG_METHOD_PCG_VCYCLE ||
+                     kind == RMG_METHOD_PCG_VCYCLE_ADDITIVE;
   const uint64_t L = multi ? n_levels : 1;
   if (L > RMG_MAX_LEVELS) throw InvalidArgument("too many levels");
   for (uint64_t k = 0; k < L; ++k) {
@@ -1421,7 +1422,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     specs_.push_back(ls);
   }
   if (kind != RMG_METHOD_FCG_MULTILEVEL) specs_[0].spec.coarse_kind = RMG_COARSE_DIRECT_CHOLESKY;  // krylov.cpp:632-634
-  if (kind == RMG_METHOD_PCG_VCYCLE)  // intermediate levels are visited by the recursive cycle
+  if (kind == RMG_METHOD_PCG_VCYCLE || kind == RMG_METHOD_PCG_VCYCLE_ADDITIVE)  // intermediate levels are visited by the recursive cycle
     for (uint64_t k = 0; k < L; ++k)
       specs_[k].spec.coarse_kind = k + 1 == L ? RMG_COARSE_DIRECT_CHOLESKY : RMG_COARSE_INNER_FCG;
   // krylov.cpp:495-505
@@ -1572,7 +1573,7 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
     t0 = tnow();
     build_dense_levels(inv);
     tlog("dense_levels", L, t0);
-    if (kind_ == RMG_METHOD_PCG_VCYCLE) {
+    if (vc_kind()) {
       t0 = tnow();
       build_vcycle();
       tlog("vcycle", L, t0);
@@ -1872,7 +1873,7 @@ void Method::set_beta(double beta) {
   build_dense_levels(inv);
   for (size_t k = 1; k < dense_.size(); ++k)
     if (dense_[k]) tune_dense_partials(k);
-  if (kind_ == RMG_METHOD_PCG_VCYCLE) build_vcycle();
+  if (vc_kind()) build_vcycle();
   ctx_->sync();
 }
 
@@ -1882,7 +1883,7 @@ void Method::set_beta(double beta) {
 void Method::build_dense_levels(const std::vector<double>& ainv_host) {
   const size_t L = coarse_.size();
   dense_.resize(L + 1);
-  if (kind_ == RMG_METHOD_PCG_VCYCLE) return;  // no inner Krylov solves
+  if (vc_kind()) return;  // no inner Krylov solves
   if (std::getenv("RMG_DISABLE_DENSE_INNER") != nullptr) return;
   cudaStream_t s = ctx_->stream;
   const unsigned threads = std::max(1u, std::thread::hardware_concurrency());
@@ -2458,7 +2459,7 @@ SolveResult Method::solve_rhs(const double* rhs, double* w_out) {
     run_cg(0, rhs, inv_diag_.get(), true, &res);
   else if (kind_ == RMG_METHOD_FGMRES_TWOLEVEL)
     run_fgmres(rhs, &res);
-  else if (kind_ == RMG_METHOD_PCG_VCYCLE)
+  else if (vc_kind())
     run_pcg_vcycle(rhs, &res);
   else
     run_fcg(0, rhs, true, &res);
@@ -2479,7 +2480,7 @@ void Method::collect_profiles() {
 
 void Method::precondition(const double* r, double* z) {
   if (coarse_.empty()) throw InvalidArgument("precondition: method has no hierarchy");
-  if (kind_ == RMG_METHOD_PCG_VCYCLE)
+  if (vc_kind())
     vcycle(0, r, z, nullptr);
   else
     precond(0, r, z);
@@ -2514,6 +2515,11 @@ void Method::build_vcycle() {
       e = 1.0 / e;
     }
     v->dinv.upload(d.data(), d.size(), s);
+    if (vc_additive(k)) {  // the additive level applies D^-1 itself (weight 1, no smoothing step)
+      v->w = 1.0;
+      vc_.push_back(std::move(v));
+      continue;
+    }
     CounterRng rng(0x5eed + 64 + k);
     std::vector<double> h(n);
     for (double& e : h) e = rng.next_normal();
@@ -2566,6 +2572,23 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
   Matrix& m = level_matrix(k);
   const int64_t nf = m.f();
   VcLevel& v = *vc_[k];
+  const bool last = k + 1 == L;
+  double* rc = last ? rc_last_.get() : work_[k + 1]->b.get();
+  double* ec = last ? ec_last_.get() : work_[k + 1]->x.get();
+  if (vc_additive(k)) {  // z = D^-1 r + P V_{k+1}(P^T r): no operator application at this level
+    XtArgs ra;
+    ra.t = r;
+    ra.out = rc;
+    ra.done = done;
+    launch_xt(c.pt.view, c.pt_sched.view, Epi::Plain, ra, s);
+    if (last)
+      launch_dense_gemv(ainv_.get(), rc, ec, c.mat->f(), done, s);
+    else
+      vcycle(k + 1, rc, ec, done);
+    launch_vc_jacobi_prolong(r, v.dinv.get(), c.label.get(), c.weight.get(), ec, z, nf, done, s);
+    ctx_->launches += 3;
+    return;
+  }
   launch_vc_pre(r, v.dinv.get(), v.w, v.x1.get(), nf, done, s);
   XtArgs a;
   a.v = v.x1.get();
@@ -2578,9 +2601,6 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
   else
     m.apply(v.x1.get(), Epi::Axpby, a, prof(k));
   launch_vc_sub(r, v.y.get(), nf, done, s);  // y = r - A x1
-  const bool last = k + 1 == L;
-  double* rc = last ? rc_last_.get() : work_[k + 1]->b.get();
-  double* ec = last ? ec_last_.get() : work_[k + 1]->x.get();
   XtArgs ra;
   ra.t = v.y.get();
   ra.out = rc;
@@ -2605,7 +2625,7 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
 bool Method::block_capable() const {
   if (fine_->dense != nullptr || fine_->comm != nullptr) return false;
   if (kind_ == RMG_METHOD_CG || kind_ == RMG_METHOD_JACOBI_CG) return true;
-  if (kind_ != RMG_METHOD_PCG_VCYCLE || coarse_.empty()) return false;
+  if (!vc_kind() || coarse_.empty()) return false;
   for (size_t k = 1; k < coarse_.size(); ++k) {
     if (dgram(k) != nullptr) continue;
     const Matrix& m = level_matrix(k);
@@ -2617,7 +2637,7 @@ bool Method::block_capable() const {
 void Method::bprecond(const double* r, double* z, int k) {
   cudaStream_t s = ctx_->stream;  // the capture stream while a graph is recorded
   const int64_t n = fine_->f();
-  if (kind_ == RMG_METHOD_PCG_VCYCLE) {
+  if (vc_kind()) {
     bvcycle(0, r, z, k);
   } else if (kind_ == RMG_METHOD_JACOBI_CG) {  // z = r * (1/d) (krylov.cpp:41-47)
     launch_bvc_pre(r, inv_diag_.get(), 1.0, z, n, k, s);
@@ -2655,6 +2675,16 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
     else
       m.apply_block(in, out, level_beta(lv), k, false);
   };
+  if (vc_additive(lv)) {  // z = D^-1 r + P V_{lv+1}(P^T r)
+    launch_brestrict(c.mptr.get(), c.members.get(), c.weight.get(), r, b.rc.get(), nc, k, s);
+    if (lv + 1 == L)
+      launch_bgemm_inv(ainv_.get(), b.rc.get(), b.ec.get(), nc, k, s);
+    else
+      bvcycle(lv + 1, b.rc.get(), b.ec.get(), k);
+    launch_bvc_jacobi_prolong(r, v.dinv.get(), c.label.get(), c.weight.get(), b.ec.get(), z, nf, k, s);
+    ctx_->launches += 3;
+    return;
+  }
   launch_bvc_pre(r, v.dinv.get(), v.w, b.x1.get(), nf, k, s);
   apply(b.x1.get(), b.y.get());
   launch_bsub(r, b.y.get(), nf * k, s);

@@ -347,12 +347,15 @@ class Method {
   // the level's smoothing weight: Richardson omega_k (krylov.cpp:539-546), or the
   // damped-Jacobi weight for pcg_vcycle
   double omega(size_t k) const {
-    if (kind_ == RMG_METHOD_PCG_VCYCLE) return k < vc_.size() ? vc_[k]->w : 0.0;
+    if (vc_kind()) return k < vc_.size() ? vc_[k]->w : 0.0;
     return k < omega_.size() ? omega_[k] : 0.0;
   }
   const std::vector<int64_t>& labels(size_t k) const;
   Matrix* fine() const { return fine_; }
   int kind() const { return kind_; }
+  // pcg_vcycle and its additive-fine-level variant share the hierarchy, smoothers and cycle
+  bool vc_kind() const { return kind_ == RMG_METHOD_PCG_VCYCLE || kind_ == RMG_METHOD_PCG_VCYCLE_ADDITIVE; }
+  bool vc_additive(size_t k) const { return k == 0 && kind_ == RMG_METHOD_PCG_VCYCLE_ADDITIVE; }
   rmg_solver_config solver;
   double time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms);
   void set_profiling(bool on);

@@ -18,10 +18,11 @@ import numpy as np
 from . import _lib
 
 # ---------------------------------------------------------------- enums (krylov.hpp)
-CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL, FGMRES_TWOLEVEL, PCG_VCYCLE = 0, 1, 2, 3, 4, 5
+CG, JACOBI_CG, FCG_TWOLEVEL, FCG_MULTILEVEL, FGMRES_TWOLEVEL, PCG_VCYCLE, PCG_VCYCLE_ADDITIVE = 0, 1, 2, 3, 4, 5, 6
 METHOD_NAMES = {"cg": CG, "jacobi_cg": JACOBI_CG, "fcg_twolevel": FCG_TWOLEVEL, "fcg_multilevel": FCG_MULTILEVEL,
                 "fgmres_twolevel": FGMRES_TWOLEVEL,
-                "pcg_vcycle": PCG_VCYCLE}  # extension: symmetric Jacobi-smoothed V-cycle
+                "pcg_vcycle": PCG_VCYCLE,  # extension: symmetric Jacobi-smoothed V-cycle
+                "pcg_vcycle_additive": PCG_VCYCLE_ADDITIVE}  # extension: additive finest level (§4.15)
 LEADER_TOLERANCE, LEADER_TARGET, KMEANS, KMEANS_SKETCH, IMPORTED = 0, 1, 2, 3, 100
 DIRECT_CHOLESKY, INNER_CG, INNER_FCG = 0, 1, 2
 

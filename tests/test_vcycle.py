@@ -106,3 +106,86 @@ def test_vcycle_set_beta_and_errors(gpu):
         assert r1.iterations == r2.iterations and np.array_equal(w1, w2)
     with pytest.raises(ValueError):
         R.PreparedMethod(m, 1e-2, R.MethodSpec(kind=R.PCG_VCYCLE, levels=[]))
+
+
+# ---------------------------------------------------------------- pcg_vcycle_additive
+def aspec(ks, tol=1e-10, max_iters=2000):
+    s = spec(ks, tol, max_iters)
+    s.kind = R.PCG_VCYCLE_ADDITIVE
+    return s
+
+
+def restated_additive(pm, r):
+    """z = D_0^-1 r + P_0 V_1(P_0^T r), V_1 the symmetric cycle of levels >= 1 (or the
+    coarsest direct solve for two levels)."""
+    L = pm.n_levels - 1
+    mats = [pm.x.x.dense()] + [pm.level_matrix(k).dense() for k in range(1, L + 1)]
+    betas = [pm.level(k)["beta"] for k in range(L + 1)]
+    ws = [pm.level(k)["omega"] for k in range(L)]
+    labs = [pm.labels(k) for k in range(L)]
+
+    def pmat(k):
+        lab = labs[k]
+        nc = lab.max() + 1
+        size = np.bincount(lab, minlength=nc)
+        p = np.zeros((lab.size, nc))
+        p[np.arange(lab.size), lab] = 1.0 / np.sqrt(size[lab])
+        return p
+
+    def gram(k):
+        return mats[k].T @ mats[k] + betas[k] * np.eye(mats[k].shape[1])
+
+    def cycle(k, rk):
+        if k == L:
+            return np.linalg.solve(gram(k), rk)
+        a, p = gram(k), pmat(k)
+        dinv = 1.0 / np.diag(a)
+        if k == 0:
+            return dinv * rk + p @ cycle(1, p.T @ rk)
+        x1 = ws[k] * dinv * rk
+        x2 = x1 + p @ cycle(k + 1, p.T @ (rk - a @ x1))
+        return x2 + ws[k] * dinv * (rk - a @ x2)
+
+    return cycle(0, r)
+
+
+@pytest.mark.parametrize("ks", [[30], [40, 8], [60, 15, 4]])
+def test_additive_matches_restatement_and_is_spd(gpu, ks):
+    x = random_matrix(300, 120, 7, 0.3)
+    m = R.DeviceMatrix(x)
+    pm = R.PreparedMethod(m, 0.5, aspec(ks))
+    rng = np.random.default_rng(2)
+    u, v = rng.standard_normal(120), rng.standard_normal(120)
+    mu, mv = pm.precondition(u), pm.precondition(v)
+    assert abs(u @ mv - v @ mu) <= 1e-12 * abs(u @ mv)
+    assert u @ mu > 0 and v @ mv > 0
+    assert rel_diff(mv, restated_additive(pm, v)) <= 1e-12
+    assert pm.level(0)["omega"] == 1.0  # the additive level applies D^-1 unweighted
+    for k in range(1, len(ks)):
+        assert 0.0 < pm.level(k)["omega"] < 2.0
+
+
+@pytest.mark.parametrize("ks", [[30], [40, 8]])
+def test_additive_solve_matches_reference_solution(gpu, orc, ks):
+    x = random_matrix(300, 120, 8, 0.3)
+    m = R.DeviceMatrix(x)
+    b = R.rng_normals(42, 300)
+    sol = R.solve_system(m, 0.5, b, aspec(ks))
+    ref = orc.solve(to_checker(orc, x), 0.5, b, "cg", tol=1e-12, max_iters=5000)
+    assert sol.report.converged
+    assert rel_diff(sol.w, ref.w) <= 1e-8
+    assert sol.report.iterations < ref.iterations
+
+
+def test_additive_batch_equals_single(gpu, orc):
+    x = R.synth_sparse_zipf(4000, 600, 20.0, 1.1, False, 5)
+    m = R.DeviceMatrix(x)
+    pm = R.PreparedMethod(m, 0.5, aspec([80, 12]))
+    B = np.stack([R.rng_normals(200 + q, 4000) for q in range(4)], axis=1)
+    W, reps = pm.solve_batch(B)
+    ref = orc.solve(to_checker(orc, x), 0.5, B[:, 0], "cg", tol=1e-12, max_iters=5000)
+    assert rel_diff(W[:, 0], ref.w) <= 1e-8
+    for q in range(4):
+        w1, r1 = pm.solve(B[:, q])
+        assert reps[q].converged and abs(reps[q].iterations - r1.iterations) <= 1
+        assert rel_diff(W[:, q], w1) <= 1e-10
