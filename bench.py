@@ -57,7 +57,7 @@ CONFIGS = {
                  "10000/1000/100 (sketched k-means on unit-normalised columns, DESIGN.md §4.10); 16 right-hand "
                  "sides b_k = normals(42+k) solved as one batched block operator per beta; rel. residual 1e-6",
         kind="zipf", n=1_000_000, f=100_000, mean=50.0, zipf=1.1, abs_values=True, seed=0, beta=1.0,
-        ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
+        ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle_additive", tol=1e-6, max_iters=1000,
         golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32, ref_method="jacobi_cg",
         ref_fixture="cfg3_ref.json"),
     "cfg5": dict(

@@ -9,7 +9,8 @@ normals(42).
 * jacobi_cg (the reference's fastest method here): iterations +-2 of the
   reference's sequential run at every beta of the sweep (tol 1e-6), and w
   within 1e-8 of the reference's tol-1e-12 solution at beta = 10, 1, 1e-3;
-* plain cg and the batched pcg_vcycle over the config's 4-level hierarchy reach
+* plain cg and the batched pcg_vcycle / pcg_vcycle_additive (the bench headline's
+  solver) over the config's 4-level hierarchy reach
   the same solutions (1e-8 at tol 1e-12).  Plain cg's iteration count (~1000-1900
   to 1e-6) is rounding-chaotic -- the reference itself moves from 1044 to 1030
   iterations (beta = 10) between 1 and 8 threads -- so only its solution is held
@@ -66,17 +67,22 @@ def test_jacobi_cg_solution_matches_reference(cfg3, beta):
     pm.close()
 
 
-def test_cg_and_batched_vcycle_reach_reference_solution(cfg3):
+def test_cg_reaches_reference_solution(cfg3):
     _, ws, x, m, b = cfg3
     pm = R.PreparedMethod(m, 10.0, R.MethodSpec(kind=R.CG, solver=R.SolverConfig(1e-12, 20000)))
     w, rep = pm.solve(b)
     assert rep.converged and rel_diff(w, ws["cg_tol1e-12_beta10"]) <= 1e-8
     pm.close()
+
+
+@pytest.mark.parametrize("kind", ["pcg_vcycle", "pcg_vcycle_additive"])  # additive: the bench headline's solver
+def test_batched_vcycle_reaches_reference_solution(cfg3, kind):
+    _, ws, x, m, b = cfg3
     levels = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS_SKETCH, target_size=k, seed=0,
                                                         normalize_columns=True, sketch_dim=32),
                           solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == 2 else R.INNER_FCG))
               for i, k in enumerate([10_000, 1_000, 100])]
-    pv = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.PCG_VCYCLE, levels=levels, solver=R.SolverConfig(1e-12, 1000)))
+    pv = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.method_from_string(kind), levels=levels, solver=R.SolverConfig(1e-12, 1000)))
     B = np.stack([b] + [R.rng_normals(43 + q, x.n_samples) for q in range(3)], axis=1)
     W, reps = pv.solve_batch(B)
     assert all(r.converged for r in reps)
