@@ -578,6 +578,162 @@ __global__ void __launch_bounds__(1024, 1) k_spmm_hot(BlockHotK1 h1, const doubl
   }
 }
 
+// ---- K1 over the chunk-interleaved layout (BlockK1v2) ----
+__device__ __forceinline__ uint2 ldv_u32x2_stream(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ldv_s32x4_stream(const void* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldv_f64x2_stream(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldv_f64x2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// One persistent CTA per SM stages the H1 hottest labels' V rows (plus a zero row
+// for padding) in shared memory, rows at their natural 128-byte stride.  A group of
+// 4 lanes owns a row of X; lane g owns the 16-byte column pairs g and 4 + g.  Even
+// groups read pair g first and 4 + g second, odd groups the other way round: the
+// 8 lanes a shared-memory wavefront serves (two groups) then cover all 32 banks
+// whatever the two labels are -- no swizzle, no conflicts.  Every label / value
+// load is a broadcast inside the group and contiguous across the warp; the next
+// chunk's loads are issued before this chunk's shared-memory reads.  FUSE: the
+// row's cold entries follow in the same kernel, gathered from the label-ordered V
+// in global memory (16-byte loads, 8 in flight per lane), so the L2 gathers of
+// some warps overlap the shared-memory phase of others and T is written once.
+template <bool PAT, bool FUSE>
+__global__ void __launch_bounds__(FUSE ? 512 : 1024, 1) k_spmm_k1v2(BlockK1v2 h, const double* __restrict__ Vp, int k,
+                                                                  int c0, int kc, int64_t s0, int64_t s1,
+                                                                  double* __restrict__ T) {
+  extern __shared__ double vs[];
+  const int H1 = h.H1;
+  for (int e = threadIdx.x; e < (H1 + 1) * 16; e += blockDim.x) {
+    const int r = e >> 4, q = e & 15;
+    vs[e] = (r < H1 && q < kc) ? __ldg(Vp + (int64_t)r * k + c0 + q) : 0.0;
+  }
+  __syncthreads();
+  const double2* __restrict__ vs2 = reinterpret_cast<const double2*>(vs);
+  const int lane = threadIdx.x & 31, g = lane & 3, i = lane >> 2;
+  const int cA = (i & 1) ? 4 + g : g, cB = (i & 1) ? g : 4 + g;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = s0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); sl < s1; sl += nw) {
+    const int row = h.srow[sl * 8 + i];
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const int64_t hb = h.hoff[sl], he = h.hoff[sl + 1];
+    if (hb < he) {
+      const uint16_t* lp = h.hlab + (hb * 8 + i) * 4;
+      const double* xp = PAT ? nullptr : h.hval + (hb * 8 + i) * 4;
+      uint2 ln = ldv_u32x2_stream(lp);
+      double2 xn0 = make_double2(1.0, 1.0), xn1 = make_double2(1.0, 1.0);
+      if (!PAT) {
+        xn0 = ldv_f64x2_stream(xp);
+        xn1 = ldv_f64x2_stream(xp + 2);
+      }
+      for (int64_t j = hb; j < he; ++j) {
+        const uint2 lc = ln;
+        const double2 x0 = xn0, x1 = xn1;
+        if (j + 1 < he) {
+          lp += 32;
+          ln = ldv_u32x2_stream(lp);
+          if (!PAT) {
+            xp += 32;
+            xn0 = ldv_f64x2_stream(xp);
+            xn1 = ldv_f64x2_stream(xp + 2);
+          }
+        }
+        const int l0 = (int)(lc.x & 0xffffu) * 8, l1 = (int)(lc.x >> 16) * 8;
+        const int l2 = (int)(lc.y & 0xffffu) * 8, l3 = (int)(lc.y >> 16) * 8;
+        const double2 A0 = vs2[l0 + cA], B0 = vs2[l0 + cB], A1 = vs2[l1 + cA], B1 = vs2[l1 + cB];
+        const double2 A2 = vs2[l2 + cA], B2 = vs2[l2 + cB], A3 = vs2[l3 + cA], B3 = vs2[l3 + cB];
+        if (PAT) {
+          a0 += A0.x; a1 += A0.y; b0 += B0.x; b1 += B0.y;
+          a0 += A1.x; a1 += A1.y; b0 += B1.x; b1 += B1.y;
+          a0 += A2.x; a1 += A2.y; b0 += B2.x; b1 += B2.y;
+          a0 += A3.x; a1 += A3.y; b0 += B3.x; b1 += B3.y;
+        } else {
+          a0 = fma(x0.x, A0.x, a0); a1 = fma(x0.x, A0.y, a1); b0 = fma(x0.x, B0.x, b0); b1 = fma(x0.x, B0.y, b1);
+          a0 = fma(x0.y, A1.x, a0); a1 = fma(x0.y, A1.y, a1); b0 = fma(x0.y, B1.x, b0); b1 = fma(x0.y, B1.y, b1);
+          a0 = fma(x1.x, A2.x, a0); a1 = fma(x1.x, A2.y, a1); b0 = fma(x1.x, B2.x, b0); b1 = fma(x1.x, B2.y, b1);
+          a0 = fma(x1.y, A3.x, a0); a1 = fma(x1.y, A3.y, a1); b0 = fma(x1.y, B3.x, b0); b1 = fma(x1.y, B3.y, b1);
+        }
+      }
+    }
+    if (FUSE) {  // kc == 16, k even: whole 16-byte pairs of the label-ordered V rows
+      const int64_t cb = h.coff[sl], ce = h.coff[sl + 1];
+      if (cb < ce) {
+        const double* vA = Vp + c0 + 2 * cA;
+        const double* vB = Vp + c0 + 2 * cB;
+        const int32_t* lp = h.clab + (cb * 8 + i) * 4;
+        const double* xp = PAT ? nullptr : h.cval + (cb * 8 + i) * 4;
+        int4 ln = ldv_s32x4_stream(lp);
+        double2 xn0 = make_double2(1.0, 1.0), xn1 = make_double2(1.0, 1.0);
+        if (!PAT) {
+          xn0 = ldv_f64x2_stream(xp);
+          xn1 = ldv_f64x2_stream(xp + 2);
+        }
+        for (int64_t j = cb; j < ce; ++j) {
+          const int4 lc = ln;
+          const double2 x0 = xn0, x1 = xn1;
+          if (j + 1 < ce) {
+            lp += 32;
+            ln = ldv_s32x4_stream(lp);
+            if (!PAT) {
+              xp += 32;
+              xn0 = ldv_f64x2_stream(xp);
+              xn1 = ldv_f64x2_stream(xp + 2);
+            }
+          }
+          const int64_t m0 = (int64_t)max(lc.x, 0) * k, m1 = (int64_t)max(lc.y, 0) * k;
+          const int64_t m2 = (int64_t)max(lc.z, 0) * k, m3 = (int64_t)max(lc.w, 0) * k;
+          const double2 A0 = ldv_f64x2(vA + m0), B0 = ldv_f64x2(vB + m0), A1 = ldv_f64x2(vA + m1),
+                        B1 = ldv_f64x2(vB + m1), A2 = ldv_f64x2(vA + m2), B2 = ldv_f64x2(vB + m2),
+                        A3 = ldv_f64x2(vA + m3), B3 = ldv_f64x2(vB + m3);
+          if (lc.x >= 0) {
+            a0 = PAT ? a0 + A0.x : fma(x0.x, A0.x, a0); a1 = PAT ? a1 + A0.y : fma(x0.x, A0.y, a1);
+            b0 = PAT ? b0 + B0.x : fma(x0.x, B0.x, b0); b1 = PAT ? b1 + B0.y : fma(x0.x, B0.y, b1);
+          }
+          if (lc.y >= 0) {
+            a0 = PAT ? a0 + A1.x : fma(x0.y, A1.x, a0); a1 = PAT ? a1 + A1.y : fma(x0.y, A1.y, a1);
+            b0 = PAT ? b0 + B1.x : fma(x0.y, B1.x, b0); b1 = PAT ? b1 + B1.y : fma(x0.y, B1.y, b1);
+          }
+          if (lc.z >= 0) {
+            a0 = PAT ? a0 + A2.x : fma(x1.x, A2.x, a0); a1 = PAT ? a1 + A2.y : fma(x1.x, A2.y, a1);
+            b0 = PAT ? b0 + B2.x : fma(x1.x, B2.x, b0); b1 = PAT ? b1 + B2.y : fma(x1.x, B2.y, b1);
+          }
+          if (lc.w >= 0) {
+            a0 = PAT ? a0 + A3.x : fma(x1.y, A3.x, a0); a1 = PAT ? a1 + A3.y : fma(x1.y, A3.y, a1);
+            b0 = PAT ? b0 + B3.x : fma(x1.y, B3.x, b0); b1 = PAT ? b1 + B3.y : fma(x1.y, B3.y, b1);
+          }
+        }
+      }
+    }
+    if (row >= 0) {
+      double* o = T + (int64_t)row * k + c0;
+      if (kc == 16 && (k & 1) == 0) {
+        *reinterpret_cast<double2*>(o + 2 * cA) = make_double2(a0, a1);
+        *reinterpret_cast<double2*>(o + 2 * cB) = make_double2(b0, b1);
+      } else {
+        if (2 * cA < kc) o[2 * cA] = a0;
+        if (2 * cA + 1 < kc) o[2 * cA + 1] = a1;
+        if (2 * cB < kc) o[2 * cB] = b0;
+        if (2 * cB + 1 < kc) o[2 * cB + 1] = b1;
+      }
+    }
+  }
+}
+
 // Hot features: one CTA per sample block b stages T[bR .. bR + R) (16 columns) in
 // shared memory once; a group of 4 lanes per hot feature sums its entries of the
 // block in row order, lane g owning columns 4g .. 4g + 3 (two 16-byte shared
@@ -591,77 +747,104 @@ __global__ void __launch_bounds__(kHotBlkThreads, 1) k_xt_hotblk(BlockHot hb, co
   const int b = blockIdx.x;
   const int64_t s0 = (int64_t)b * hb.R;
   const int nb = (int)(N - s0 < (int64_t)hb.R ? N - s0 : (int64_t)hb.R);
-  // row r's 16-byte chunk c (of 8) lives at chunk c ^ (r & 7): the 8 groups of a
-  // warp read 8 different rows, and the swizzle spreads them over the banks
+  // rows at their natural 128-byte stride; row R is zero (the padding target).  A
+  // group of 4 lanes owns a feature, lane g the 16-byte column pairs g and 4 + g;
+  // even groups read pair g first, odd groups pair 4 + g: the two groups a
+  // shared-memory wavefront serves cover all 32 banks for any two rows.
   for (int e = threadIdx.x; e < nb * 16; e += kHotBlkThreads) {
     const int r = e >> 4, q = e & 15;
-    ts[r * 16 + ((((q >> 1) ^ r) & 7) << 1) + (q & 1)] = q < kc ? __ldcg(T + (s0 + r) * k + c0 + q) : 0.0;
+    ts[e] = q < kc ? __ldcg(T + (s0 + r) * k + c0 + q) : 0.0;
   }
+  if (threadIdx.x < 16) ts[hb.R * 16 + threadIdx.x] = 0.0;
   __syncthreads();
   const int g = threadIdx.x & 3;
   const int32_t* __restrict__ p = hb.ptr + (size_t)b * (hb.H + 1);
   const double2* __restrict__ ts2 = reinterpret_cast<const double2*>(ts);
-  // the HL longest features: a warp each, 8 sub-groups taking every 8th entry (8
-  // independent chains), the sub-group partials reduced by a fixed shuffle tree
   const int lane = threadIdx.x & 31, sub = lane >> 2;
+  const int cA = (sub & 1) ? 4 + g : g, cB = (sub & 1) ? g : 4 + g;
+  const int zrow = hb.R * 8;
+  // the HL longest features: a warp each, 8 sub-groups taking every 8th entry (8
+  // independent chains, 4 entries of each in flight), the sub-group partials reduced
+  // by a fixed shuffle tree
   for (int h = threadIdx.x >> 5; h < hb.HL; h += kHotBlkThreads / 32) {
     const int e0 = p[h], e1 = p[h + 1];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int e = e0 + sub; e < e1; e += 8) {
-      const int r = hb.row[e];
-      const double x = PAT ? 1.0 : hb.val[e];
-      const double2 lo = ts2[r * 8 + ((2 * g) ^ (r & 7))], hi = ts2[r * 8 + ((2 * g + 1) ^ (r & 7))];
-      a0 = PAT ? a0 + lo.x : fma(x, lo.x, a0);
-      a1 = PAT ? a1 + lo.y : fma(x, lo.y, a1);
-      a2 = PAT ? a2 + hi.x : fma(x, hi.x, a2);
-      a3 = PAT ? a3 + hi.y : fma(x, hi.y, a3);
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (int e = e0 + sub; e < e1; e += 32) {
+      int r[4];
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = e + 8 * u < e1;
+        r[u] = ok ? (int)ld_stream(hb.row + e + 8 * u) * 8 : zrow;
+        x[u] = (PAT || !ok) ? (ok ? 1.0 : 0.0) : ld_stream(hb.val + e + 8 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 A = ts2[r[u] + cA], B = ts2[r[u] + cB];
+        a0 = PAT ? a0 + A.x : fma(x[u], A.x, a0);
+        a1 = PAT ? a1 + A.y : fma(x[u], A.y, a1);
+        b0 = PAT ? b0 + B.x : fma(x[u], B.x, b0);
+        b1 = PAT ? b1 + B.y : fma(x[u], B.y, b1);
+      }
+    }
+    if (sub & 1) {  // odd sub-groups hold (pair 4 + g, pair g): same columns in every lane g
+      double t0 = a0, t1 = a1;
+      a0 = b0; a1 = b1; b0 = t0; b1 = t1;
     }
 #pragma unroll
     for (int off = 4; off <= 16; off <<= 1) {
       a0 += __shfl_xor_sync(0xffffffffu, a0, off);
       a1 += __shfl_xor_sync(0xffffffffu, a1, off);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, off);
-      a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+      b0 += __shfl_xor_sync(0xffffffffu, b0, off);
+      b1 += __shfl_xor_sync(0xffffffffu, b1, off);
     }
     if (sub == 0) {
-      double2* out = reinterpret_cast<double2*>(hb.part + ((size_t)b * hb.H + h) * 16 + 4 * g);
-      out[0] = make_double2(a0, a1);
-      out[1] = make_double2(a2, a3);
+      double* out = hb.part + ((size_t)b * hb.H + h) * 16;
+      *reinterpret_cast<double2*>(out + 2 * g) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(out + 8 + 2 * g) = make_double2(b0, b1);
     }
   }
-  for (int h = hb.HL + (threadIdx.x >> 2); h < hb.H; h += kHotBlkThreads / 4) {
-    const int e0 = p[h], e1 = p[h + 1];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int e = e0;
-    for (; e + 8 <= e1; e += 8) {
+  // the other hot features: a group of 4 lanes each, 8 entries per round -- lane g
+  // loads entries e + g and e + 4 + g, shuffles inside the group hand them round;
+  // the warp's 8 groups share one trip count (padding entries read the zero row)
+  const int hbase = hb.HL + (threadIdx.x >> 5) * 8;
+  for (int hw = hbase; hw < hb.H; hw += kHotBlkThreads / 4) {
+    const int h = hw + sub;
+    const bool live = h < hb.H;
+    const int e0 = live ? p[h] : 0, e1 = live ? p[h + 1] : 0;
+    int len = e1 - e0;
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (int j = 0; j < len; j += 8) {
+      const int ea = e0 + j + g, eb = ea + 4;
+      const bool oka = ea < e1, okb = eb < e1;
+      const int ra = oka ? (int)ld_stream(hb.row + ea) * 8 : zrow, rb = okb ? (int)ld_stream(hb.row + eb) * 8 : zrow;
+      const double xa = oka ? (PAT ? 1.0 : ld_stream(hb.val + ea)) : 0.0;
+      const double xb = okb ? (PAT ? 1.0 : ld_stream(hb.val + eb)) : 0.0;
       int r[8];
       double x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        r[u] = hb.row[e + u];
-        x[u] = PAT ? 1.0 : hb.val[e + u];
+      for (int u = 0; u < 4; ++u) {
+        r[u] = __shfl_sync(0xffffffffu, ra, u, 4);
+        r[u + 4] = __shfl_sync(0xffffffffu, rb, u, 4);
+        x[u] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xa, u, 4);
+        x[u + 4] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xb, u, 4);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const double2 lo = ts2[r[u] * 8 + ((2 * g) ^ (r[u] & 7))], hi = ts2[r[u] * 8 + ((2 * g + 1) ^ (r[u] & 7))];
-        a0 = PAT ? a0 + lo.x : fma(x[u], lo.x, a0);
-        a1 = PAT ? a1 + lo.y : fma(x[u], lo.y, a1);
-        a2 = PAT ? a2 + hi.x : fma(x[u], hi.x, a2);
-        a3 = PAT ? a3 + hi.y : fma(x[u], hi.y, a3);
+        const double2 A = ts2[r[u] + cA], B = ts2[r[u] + cB];
+        a0 = PAT ? a0 + A.x : fma(x[u], A.x, a0);
+        a1 = PAT ? a1 + A.y : fma(x[u], A.y, a1);
+        b0 = PAT ? b0 + B.x : fma(x[u], B.x, b0);
+        b1 = PAT ? b1 + B.y : fma(x[u], B.y, b1);
       }
     }
-    for (; e < e1; ++e) {
-      const int r = hb.row[e];
-      const double x = PAT ? 1.0 : hb.val[e];
-      const double2 lo = ts2[r * 8 + ((2 * g) ^ (r & 7))], hi = ts2[r * 8 + ((2 * g + 1) ^ (r & 7))];
-      a0 = PAT ? a0 + lo.x : fma(x, lo.x, a0);
-      a1 = PAT ? a1 + lo.y : fma(x, lo.y, a1);
-      a2 = PAT ? a2 + hi.x : fma(x, hi.x, a2);
-      a3 = PAT ? a3 + hi.y : fma(x, hi.y, a3);
+    if (live) {
+      double* out = hb.part + ((size_t)b * hb.H + h) * 16;
+      *reinterpret_cast<double2*>(out + 2 * cA) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(out + 2 * cB) = make_double2(b0, b1);
     }
-    double2* out = reinterpret_cast<double2*>(hb.part + ((size_t)b * hb.H + h) * 16 + 4 * g);
-    out[0] = make_double2(a0, a1);
-    out[1] = make_double2(a2, a3);
   }
 }
 
@@ -2316,9 +2499,32 @@ void spmm_hot(int grid, size_t smem, cudaStream_t s, const SparseDev& x, const d
                                                          t, bs.slice0, bs.n_slices, k, c0, kc, n_hot, 0);
 }
 
+// RMG_BLOCK_K1V2: 0 = the round-2 split K1 (k_spmm_hot + cold SELL pass), 1 = the
+// chunk-interleaved hot pass + the cold SELL pass, 2 (default) = hot and cold fused
+int block_k1v2_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("RMG_BLOCK_K1V2");
+    mode = e != nullptr ? std::max(0, std::min(2, std::atoi(e))) : 2;
+  }
+  return mode;
+}
+
+template <bool PAT, bool FUSE>
+void spmm_k1v2(int sms, cudaStream_t s, const BlockK1v2& h, const double* vk, int k, int c0, int kc, int64_t s0,
+               int64_t s1, double* t) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmm_k1v2<PAT, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    attr = true;
+  }
+  const size_t smem = static_cast<size_t>(h.H1 + 1) * 16 * sizeof(double);
+  k_spmm_k1v2<PAT, FUSE><<<sms, FUSE ? 512 : 1024, smem, s>>>(h, vk, k, c0, kc, s0, s1, t);
+}
+
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const BlockHot& hot, const BlockHotK1& hot1, const double* v, double* out, double beta, int k,
-                        double* t, double* vp, cudaStream_t s) {
+                        const BlockHot& hot, const BlockHotK1& hot1, const BlockK1v2& k1v2, const double* v,
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
   if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
   // TMA gather passes (spmm_tma.cu) when V and T rows are 16-byte aligned
@@ -2351,7 +2557,46 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       const int g1 = grid_for(bs.n_slices * 32, 148 * 8);
       const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
       const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
-      if (bs.n_slices > 0 && hot1.H1 > 0 && x.col_inv != nullptr) {
+      const int v2 = (k1v2.H1 > 0 && x.col_inv != nullptr) ? block_k1v2_mode() : 0;
+      if (bs.n_slices > 0 && v2 > 0 && hot1.H1 > 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int64_t s0 = bs.slice0 * 4, s1 = std::min<int64_t>(k1v2.n_slices8, (bs.slice0 + bs.n_slices) * 4);
+        const bool pat = k1v2.hval == nullptr;
+        const bool fuse = v2 == 2 && kc == 16 && (k & 1) == 0;
+        if (fuse) {
+          if (pat)
+            spmm_k1v2<true, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+          else
+            spmm_k1v2<false, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+        } else {
+          if (pat)
+            spmm_k1v2<true, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+          else
+            spmm_k1v2<false, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+          const SparseDev& xc = hot1.cold;  // the cold entries' SELL pass adds onto T
+          const int gc = grid_for(bs.n_slices * 32, 148 * 8);
+          if (xc.val == nullptr) {
+            if (xc.idx16 != nullptr)
+              k_spmm_sell<true, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                     xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                     c0, kc, 0, 1);
+            else
+              k_spmm_sell<true, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                      xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                      c0, kc, 0, 1);
+          } else {
+            if (xc.idx16 != nullptr)
+              k_spmm_sell<false, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                      xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
+                                                                      c0, kc, 0, 1);
+            else
+              k_spmm_sell<false, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
+                                                                       xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices,
+                                                                       k, c0, kc, 0, 1);
+          }
+        }
+      } else if (bs.n_slices > 0 && hot1.H1 > 0 && x.col_inv != nullptr) {
         // K1 split: hot labels from shared memory (T written), cold SELL pass adds
         const int64_t r0 = bs.slice0 * 32, r1 = std::min<int64_t>(x.rows, (bs.slice0 + bs.n_slices) * 32);
         static bool attr1 = false;
@@ -2438,7 +2683,7 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
             bs, v, out, beta, k, c0, kc, first, last);
     }
     if (hot.H > 0) {  // hot features: from shared-memory T blocks, then folded
-      const size_t smem = static_cast<size_t>(hot.R) * 16 * sizeof(double);
+      const size_t smem = static_cast<size_t>(hot.R + 1) * 16 * sizeof(double);  // + the zero row
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(k_xt_hotblk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);

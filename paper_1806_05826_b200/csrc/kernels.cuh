@@ -211,9 +211,28 @@ struct BlockHotK1 {
   const double* val = nullptr;     // nullptr: binary pattern
   SparseDev cold;                  // the remaining entries, SELL-32, original column indices
 };
+// K1, third layout ("chunk-interleaved"): slices of 8 rows (length
+// sorted inside 1024-row windows), a 4-lane group per row.  A chunk holds 4 entries of
+// each of the slice's 8 rows, [row i][entry g] contiguous: the group's 4 labels are one
+// 8-byte (hot, uint16) or 16-byte (cold, int32) broadcast load, its 4 values two
+// 16-byte loads, and a warp's loads of a chunk are 64 / 128 / 256 contiguous bytes.
+// Hot entries (label < H1) first, in label order (= descending popularity), padded
+// with label H1 (a zero row of the shared-memory block, value 0); cold entries
+// (label >= H1) follow in their own chunk list, padded with -1.
+struct BlockK1v2 {
+  int H1 = 0;
+  int64_t n_slices8 = 0;
+  const int32_t* hoff = nullptr;   // [n_slices8 + 1] first hot chunk of each slice
+  const int32_t* coff = nullptr;   // [n_slices8 + 1] first cold chunk
+  const int32_t* srow = nullptr;   // [n_slices8 * 8] the sample in each slot (-1: none)
+  const uint16_t* hlab = nullptr;  // [hot chunks * 32]
+  const double* hval = nullptr;    // nullptr: binary pattern
+  const int32_t* clab = nullptr;   // [cold chunks * 32] popularity labels
+  const double* cval = nullptr;
+};
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
-                        const BlockHot& hot, const BlockHotK1& hot1, const double* v, double* out, double beta, int k,
-                        double* t, double* vp, cudaStream_t s);
+                        const BlockHot& hot, const BlockHotK1& hot1, const BlockK1v2& k1v2, const double* v,
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

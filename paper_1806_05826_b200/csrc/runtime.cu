@@ -642,6 +642,96 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   }
 }
 
+// K1's chunk-interleaved layout (kernels.cuh, BlockK1v2): rows sorted by (hot chunks,
+// cold chunks) inside 1024-row windows, slices of 8 rows, entries in label order.
+void Matrix::build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int64_t h1) {
+  const int64_t n = xr.n;
+  if (n == 0 || h1 <= 0 || h1 >= 65535) return;
+  const int64_t nslots = (n + 1023) / 1024 * 1024, ns8 = nslots / 8;
+  std::vector<int32_t> hch(n), cch(n);
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t nh = 0;
+    for (int64_t q = xr.ptr[r]; q < xr.ptr[r + 1]; ++q) nh += rank[xr.idx[q]] < h1 ? 1 : 0;
+    hch[r] = static_cast<int32_t>((nh + 3) / 4);
+    cch[r] = static_cast<int32_t>((xr.ptr[r + 1] - xr.ptr[r] - nh + 3) / 4);
+  }
+  std::vector<int32_t> srow(nslots, -1);
+  std::vector<int32_t> order;
+  for (int64_t w0 = 0; w0 < n; w0 += 1024) {
+    const int64_t w1 = std::min(n, w0 + 1024);
+    order.resize(w1 - w0);
+    std::iota(order.begin(), order.end(), static_cast<int32_t>(w0));
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return hch[a] != hch[b] ? hch[a] > hch[b] : cch[a] > cch[b];
+    });
+    std::copy(order.begin(), order.end(), srow.begin() + w0);
+  }
+  std::vector<int32_t> hoff(ns8 + 1, 0), coff(ns8 + 1, 0);
+  int64_t hrun = 0, crun = 0;
+  for (int64_t sl = 0; sl < ns8; ++sl) {
+    int32_t wh = 0, wc = 0;
+    for (int i = 0; i < 8; ++i) {
+      const int32_t r = srow[sl * 8 + i];
+      if (r < 0) continue;
+      wh = std::max(wh, hch[r]);
+      wc = std::max(wc, cch[r]);
+    }
+    hoff[sl] = static_cast<int32_t>(hrun);
+    coff[sl] = static_cast<int32_t>(crun);
+    hrun += wh;
+    crun += wc;
+    if (hrun * 32 > INT32_MAX || crun * 32 > INT32_MAX) return;  // keep the round-2 passes
+  }
+  hoff[ns8] = static_cast<int32_t>(hrun);
+  coff[ns8] = static_cast<int32_t>(crun);
+  std::vector<uint16_t> hlab(static_cast<size_t>(hrun) * 32, static_cast<uint16_t>(h1));
+  std::vector<int32_t> clab(static_cast<size_t>(crun) * 32, -1);
+  std::vector<double> hval(pattern ? 0 : hlab.size(), 0.0), cval(pattern ? 0 : clab.size(), 0.0);
+  std::vector<std::pair<int32_t, int64_t>> row;
+  for (int64_t sl = 0; sl < ns8; ++sl)
+    for (int i = 0; i < 8; ++i) {
+      const int32_t r = srow[sl * 8 + i];
+      if (r < 0) continue;
+      row.clear();
+      for (int64_t q = xr.ptr[r]; q < xr.ptr[r + 1]; ++q) row.emplace_back(rank[xr.idx[q]], q);
+      std::sort(row.begin(), row.end());  // label order = descending popularity
+      int64_t eh = 0, ec = 0;
+      for (const auto& pq : row) {
+        if (pq.first < h1) {
+          const size_t at = ((static_cast<size_t>(hoff[sl]) + eh / 4) * 8 + i) * 4 + eh % 4;
+          hlab[at] = static_cast<uint16_t>(pq.first);
+          if (!pattern) hval[at] = xr.val[pq.second];
+          ++eh;
+        } else {
+          const size_t at = ((static_cast<size_t>(coff[sl]) + ec / 4) * 8 + i) * 4 + ec % 4;
+          clab[at] = pq.first;
+          if (!pattern) cval[at] = xr.val[pq.second];
+          ++ec;
+        }
+      }
+    }
+  cudaStream_t s = ctx->stream;
+  bk_hoff.upload(hoff.data(), hoff.size(), s);
+  bk_coff.upload(coff.data(), coff.size(), s);
+  bk_srow.upload(srow.data(), srow.size(), s);
+  bk_hlab.upload(hlab.data(), std::max<size_t>(1, hlab.size()), s);
+  bk_clab.upload(clab.data(), std::max<size_t>(1, clab.size()), s);
+  if (!pattern) {
+    bk_hval.upload(hval.data(), std::max<size_t>(1, hval.size()), s);
+    bk_cval.upload(cval.data(), std::max<size_t>(1, cval.size()), s);
+  }
+  RMG_CK(cudaStreamSynchronize(s));
+  bk1v2.H1 = static_cast<int>(h1);
+  bk1v2.n_slices8 = ns8;
+  bk1v2.hoff = bk_hoff.get();
+  bk1v2.coff = bk_coff.get();
+  bk1v2.srow = bk_srow.get();
+  bk1v2.hlab = bk_hlab.get();
+  bk1v2.clab = bk_clab.get();
+  bk1v2.hval = pattern ? nullptr : bk_hval.get();
+  bk1v2.cval = pattern ? nullptr : bk_cval.get();
+}
+
 // Block operator schedule: rows of X^T with <= 512 nonzeros
 // are one unit each (a half-warp, elements in order); longer rows are split
 // into items of 512 whose partials are finished in item order.
@@ -674,6 +764,7 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   // K1's hot labels: the H1 most popular columns (the relabeled SELL's
   // labels 0 .. H1-1) from shared memory, the rest in a second SELL layout
   bhot1 = BlockHotK1{};
+  bk1v2 = BlockK1v2{};
   {
     const char* e1 = std::getenv("RMG_BLOCK_HOTK1");  // rows of V kept in shared memory (0: off)
     const int64_t h1 = std::min<int64_t>(xr.f, e1 != nullptr ? std::max<int64_t>(0, std::atoll(e1)) : 1400);
@@ -710,6 +801,7 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
         hptr[r + 1] = static_cast<int32_t>(hlab.size());
         cold.ptr[r + 1] = static_cast<int64_t>(cold.idx.size());
       }
+      build_k1v2(xr, rank, h1);
       if (hlab.size() < static_cast<size_t>(INT32_MAX)) {
         bh1_ptr.upload(hptr.data(), hptr.size(), s);
         bh1_lab.upload(hlab.data(), hlab.size(), s);
@@ -872,7 +964,7 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
-  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, v, out, beta, k,
+  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, bk1v2, v, out, beta, k,
                      bt.get(),
                      bvp.get(), ctx->stream);
   if (sync) ctx->sync();

@@ -226,6 +226,10 @@ struct Matrix {
   DBuf<uint16_t> bh1_lab;
   DBuf<double> bh1_val;
   DeviceSparse bh1_cold;
+  BlockK1v2 bk1v2;             // chunk-interleaved K1 layout (H1 = 0: none)
+  DBuf<int32_t> bk_hoff, bk_coff, bk_srow, bk_clab;
+  DBuf<uint16_t> bk_hlab;
+  DBuf<double> bk_hval, bk_cval;
   DBuf<int32_t> bh_ptr, bh_feat;
   DBuf<uint16_t> bh_row;
   DBuf<double> bh_val, bh_part;
@@ -235,6 +239,7 @@ struct Matrix {
   int64_t bchunk_rows = 0;
   DBuf<double> bseg, bt, bvp;  // + scratch T (N x k) and permuted V (F x k), kept across calls
   void build_block_schedule(const HostCsr& x, const HostCsr& ht);
+  void build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int64_t h1);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
