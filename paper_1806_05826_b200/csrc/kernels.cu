@@ -578,150 +578,146 @@ __global__ void __launch_bounds__(1024, 1) k_spmm_hot(BlockHotK1 h1, const doubl
   }
 }
 
-// ---- K1 over the chunk-interleaved layout (BlockK1v2) ----
-__device__ __forceinline__ uint2 ldv_u32x2_stream(const void* p) {
-  uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ int4 ldv_s32x4_stream(const void* p) {
-  int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double2 ldv_f64x2_stream(const double* p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
+// ---- block passes over chunk-interleaved records (BlockK1v2 / BlockHot) ----
 __device__ __forceinline__ double2 ldv_f64x2(const double* p) {
   double2 v;
   asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
-// One persistent CTA per SM stages the H1 hottest labels' V rows (plus a zero row
-// for padding) in shared memory, rows at their natural 128-byte stride.  A group of
-// 4 lanes owns a row of X; lane g owns the 16-byte column pairs g and 4 + g.  Even
-// groups read pair g first and 4 + g second, odd groups the other way round: the
-// 8 lanes a shared-memory wavefront serves (two groups) then cover all 32 banks
-// whatever the two labels are -- no swizzle, no conflicts.  Every label / value
-// load is a broadcast inside the group and contiguous across the warp; the next
-// chunk's loads are issued before this chunk's shared-memory reads.  FUSE: the
-// row's cold entries follow in the same kernel, gathered from the label-ordered V
-// in global memory (16-byte loads, 8 in flight per lane), so the L2 gathers of
-// some warps overlap the shared-memory phase of others and T is written once.
-template <bool PAT, bool FUSE>
-__global__ void __launch_bounds__(FUSE ? 512 : 1024, 1) k_spmm_k1v2(BlockK1v2 h, const double* __restrict__ Vp, int k,
-                                                                  int c0, int kc, int64_t s0, int64_t s1,
-                                                                  double* __restrict__ T) {
-  extern __shared__ double vs[];
+// A record = 4 entries of each of a slice's 8 rows: int32 label[8][4], then (valued
+// matrices) double value[8][4] -- 384 bytes (pattern: 128).  Every warp owns a
+// contiguous run of records and streams it through a private shared-memory ring with
+// cp.async (16 bytes per lane, kRingDepth records in flight), so the entry stream's
+// DRAM latency is paid once per warp, not once per chunk; a group of 4 lanes reads its
+// row's 4 labels / values of the current record as one 16-byte and two 16-byte
+// shared loads (broadcast inside the group).
+constexpr int kRecLab = 128;
+
+// first slice in [a, b] whose first record is >= target (off ascending)
+__device__ __forceinline__ int64_t first_slice_at(const int32_t* __restrict__ off, int64_t a, int64_t b, int64_t target) {
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (off[m] < target) a = m + 1; else b = m;
+  }
+  return a;
+}
+
+// K1.  One persistent CTA per SM stages the H1 hottest labels' V rows
+// (plus a zero row for padding) in shared memory, rows at their natural 128-byte
+// stride.  A group of 4 lanes owns a row of X; lane g owns the 16-byte column pairs g
+// and 4 + g.  Even groups read pair g first and 4 + g second, odd groups the other
+// way round: the 8 lanes one shared-memory wavefront serves (two groups) cover all
+// 32 banks whatever the two labels are -- no swizzle, no conflicts.  A slice's first
+// nhot records hold hot labels only (shared memory), the rest cold labels (16-byte
+// gathers from the label-ordered V in L2, 8 in flight per lane): the cold gathers of
+// some warps overlap the shared-memory phase of others, and T is written once.
+template <bool PAT, bool VEC, int THREADS, int D>
+__global__ void __launch_bounds__(THREADS, 1) k_spmm_k1v3(BlockK1v2 h, const double* __restrict__ Vp, int k, int c0,
+                                                         int kc, int64_t s0, int64_t s1, double* __restrict__ T) {
+  constexpr int REC = PAT ? kRecLab : kRecLab + 256;
+  constexpr int NS = D + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* vs = reinterpret_cast<double*>(smem_raw);
   const int H1 = h.H1;
-  for (int e = threadIdx.x; e < (H1 + 1) * 16; e += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane & 3, i = lane >> 2;
+  unsigned char* ring = smem_raw + (size_t)(H1 + 1) * 128 + (size_t)warp * NS * REC;
+  // this warp's run of records: an equal share of the launch's records, whole slices
+  const int W = gridDim.x * (THREADS / 32), w = blockIdx.x * (THREADS / 32) + warp;
+  const int64_t r0 = h.off[s0], r1 = h.off[s1], R = r1 - r0;
+  const int64_t sA = first_slice_at(h.off, s0, s1, r0 + R * w / W);
+  const int64_t sB = w == W - 1 ? s1 : first_slice_at(h.off, s0, s1, r0 + R * (w + 1) / W);
+  const int recA = sA < s1 ? h.off[sA] : (int)r1, recB = h.off[sB];
+  const unsigned char* __restrict__ gsrc = reinterpret_cast<const unsigned char*>(h.rec);
+  auto issue = [&](int rec) {
+    if (rec < recB && lane < REC / 16) cp_async16(ring + (rec % NS) * REC + lane * 16, gsrc + (size_t)rec * REC + lane * 16);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d) issue(recA + d);
+  for (int e = threadIdx.x; e < (H1 + 1) * 16; e += THREADS) {
     const int r = e >> 4, q = e & 15;
     vs[e] = (r < H1 && q < kc) ? __ldg(Vp + (int64_t)r * k + c0 + q) : 0.0;
   }
   __syncthreads();
   const double2* __restrict__ vs2 = reinterpret_cast<const double2*>(vs);
-  const int lane = threadIdx.x & 31, g = lane & 3, i = lane >> 2;
   const int cA = (i & 1) ? 4 + g : g, cB = (i & 1) ? g : 4 + g;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t sl = s0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); sl < s1; sl += nw) {
-    const int row = h.srow[sl * 8 + i];
-    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-    const int64_t hb = h.hoff[sl], he = h.hoff[sl + 1];
-    if (hb < he) {
-      const uint16_t* lp = h.hlab + (hb * 8 + i) * 4;
-      const double* xp = PAT ? nullptr : h.hval + (hb * 8 + i) * 4;
-      uint2 ln = ldv_u32x2_stream(lp);
-      double2 xn0 = make_double2(1.0, 1.0), xn1 = make_double2(1.0, 1.0);
-      if (!PAT) {
-        xn0 = ldv_f64x2_stream(xp);
-        xn1 = ldv_f64x2_stream(xp + 2);
-      }
-      for (int64_t j = hb; j < he; ++j) {
-        const uint2 lc = ln;
-        const double2 x0 = xn0, x1 = xn1;
-        if (j + 1 < he) {
-          lp += 32;
-          ln = ldv_u32x2_stream(lp);
-          if (!PAT) {
-            xp += 32;
-            xn0 = ldv_f64x2_stream(xp);
-            xn1 = ldv_f64x2_stream(xp + 2);
-          }
-        }
-        const int l0 = (int)(lc.x & 0xffffu) * 8, l1 = (int)(lc.x >> 16) * 8;
-        const int l2 = (int)(lc.y & 0xffffu) * 8, l3 = (int)(lc.y >> 16) * 8;
-        const double2 A0 = vs2[l0 + cA], B0 = vs2[l0 + cB], A1 = vs2[l1 + cA], B1 = vs2[l1 + cB];
-        const double2 A2 = vs2[l2 + cA], B2 = vs2[l2 + cB], A3 = vs2[l3 + cA], B3 = vs2[l3 + cB];
-        if (PAT) {
-          a0 += A0.x; a1 += A0.y; b0 += B0.x; b1 += B0.y;
-          a0 += A1.x; a1 += A1.y; b0 += B1.x; b1 += B1.y;
-          a0 += A2.x; a1 += A2.y; b0 += B2.x; b1 += B2.y;
-          a0 += A3.x; a1 += A3.y; b0 += B3.x; b1 += B3.y;
-        } else {
-          a0 = fma(x0.x, A0.x, a0); a1 = fma(x0.x, A0.y, a1); b0 = fma(x0.x, B0.x, b0); b1 = fma(x0.x, B0.y, b1);
-          a0 = fma(x0.y, A1.x, a0); a1 = fma(x0.y, A1.y, a1); b0 = fma(x0.y, B1.x, b0); b1 = fma(x0.y, B1.y, b1);
-          a0 = fma(x1.x, A2.x, a0); a1 = fma(x1.x, A2.y, a1); b0 = fma(x1.x, B2.x, b0); b1 = fma(x1.x, B2.y, b1);
-          a0 = fma(x1.y, A3.x, a0); a1 = fma(x1.y, A3.y, a1); b0 = fma(x1.y, B3.x, b0); b1 = fma(x1.y, B3.y, b1);
-        }
-      }
+  const double* vA = Vp + c0 + 2 * cA;
+  const double* vB = Vp + c0 + 2 * cB;
+  int cur = recA;
+  int n_end = 0, n_hot = 0, n_row = -1;  // the next slice's header, loaded one slice ahead
+  if (sA < sB) {
+    n_end = h.off[sA + 1];
+    n_hot = h.nhot[sA];
+    n_row = h.srow[sA * 8 + i];
+  }
+  for (int64_t sl = sA; sl < sB; ++sl) {
+    const int e_end = n_end, e_hot = cur + n_hot, row = n_row;
+    if (sl + 1 < sB) {
+      n_end = h.off[sl + 2];
+      n_hot = h.nhot[sl + 1];
+      n_row = h.srow[(sl + 1) * 8 + i];
     }
-    if (FUSE) {  // kc == 16, k even: whole 16-byte pairs of the label-ordered V rows
-      const int64_t cb = h.coff[sl], ce = h.coff[sl + 1];
-      if (cb < ce) {
-        const double* vA = Vp + c0 + 2 * cA;
-        const double* vB = Vp + c0 + 2 * cB;
-        const int32_t* lp = h.clab + (cb * 8 + i) * 4;
-        const double* xp = PAT ? nullptr : h.cval + (cb * 8 + i) * 4;
-        int4 ln = ldv_s32x4_stream(lp);
-        double2 xn0 = make_double2(1.0, 1.0), xn1 = make_double2(1.0, 1.0);
-        if (!PAT) {
-          xn0 = ldv_f64x2_stream(xp);
-          xn1 = ldv_f64x2_stream(xp + 2);
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (; cur < e_end; ++cur) {
+      cp_async_wait<D - 1>();
+      __syncwarp();
+      issue(cur + D);
+      const unsigned char* slot = ring + (cur % NS) * REC;
+      const int4 lc = *reinterpret_cast<const int4*>(slot + i * 16);
+      double2 x0 = make_double2(1.0, 1.0), x1 = make_double2(1.0, 1.0);
+      if (!PAT) {
+        x0 = *reinterpret_cast<const double2*>(slot + kRecLab + i * 32);
+        x1 = *reinterpret_cast<const double2*>(slot + kRecLab + i * 32 + 16);
+      }
+      double2 A0, B0, A1, B1, A2, B2, A3, B3;
+      if (cur < e_hot) {  // labels < H1, padding = H1 (the zero row, value 0)
+        A0 = vs2[lc.x * 8 + cA]; B0 = vs2[lc.x * 8 + cB]; A1 = vs2[lc.y * 8 + cA]; B1 = vs2[lc.y * 8 + cB];
+        A2 = vs2[lc.z * 8 + cA]; B2 = vs2[lc.z * 8 + cB]; A3 = vs2[lc.w * 8 + cA]; B3 = vs2[lc.w * 8 + cB];
+      } else {  // labels >= H1, padding = -1 (value 0; the gathered row is then discarded)
+        const int64_t m0 = (int64_t)max(lc.x, 0) * k, m1 = (int64_t)max(lc.y, 0) * k;
+        const int64_t m2 = (int64_t)max(lc.z, 0) * k, m3 = (int64_t)max(lc.w, 0) * k;
+        if (VEC) {
+          A0 = ldv_f64x2(vA + m0); B0 = ldv_f64x2(vB + m0); A1 = ldv_f64x2(vA + m1); B1 = ldv_f64x2(vB + m1);
+          A2 = ldv_f64x2(vA + m2); B2 = ldv_f64x2(vB + m2); A3 = ldv_f64x2(vA + m3); B3 = ldv_f64x2(vB + m3);
+        } else {
+          const bool pa0 = 2 * cA < kc, pa1 = 2 * cA + 1 < kc, pb0 = 2 * cB < kc, pb1 = 2 * cB + 1 < kc;
+          auto ldp = [&](const double* p, bool p0, bool p1) {
+            return make_double2(p0 ? __ldg(p) : 0.0, p1 ? __ldg(p + 1) : 0.0);
+          };
+          A0 = ldp(vA + m0, pa0, pa1); B0 = ldp(vB + m0, pb0, pb1); A1 = ldp(vA + m1, pa0, pa1);
+          B1 = ldp(vB + m1, pb0, pb1); A2 = ldp(vA + m2, pa0, pa1); B2 = ldp(vB + m2, pb0, pb1);
+          A3 = ldp(vA + m3, pa0, pa1); B3 = ldp(vB + m3, pb0, pb1);
         }
-        for (int64_t j = cb; j < ce; ++j) {
-          const int4 lc = ln;
-          const double2 x0 = xn0, x1 = xn1;
-          if (j + 1 < ce) {
-            lp += 32;
-            ln = ldv_s32x4_stream(lp);
-            if (!PAT) {
-              xp += 32;
-              xn0 = ldv_f64x2_stream(xp);
-              xn1 = ldv_f64x2_stream(xp + 2);
-            }
-          }
-          const int64_t m0 = (int64_t)max(lc.x, 0) * k, m1 = (int64_t)max(lc.y, 0) * k;
-          const int64_t m2 = (int64_t)max(lc.z, 0) * k, m3 = (int64_t)max(lc.w, 0) * k;
-          const double2 A0 = ldv_f64x2(vA + m0), B0 = ldv_f64x2(vB + m0), A1 = ldv_f64x2(vA + m1),
-                        B1 = ldv_f64x2(vB + m1), A2 = ldv_f64x2(vA + m2), B2 = ldv_f64x2(vB + m2),
-                        A3 = ldv_f64x2(vA + m3), B3 = ldv_f64x2(vB + m3);
-          if (lc.x >= 0) {
-            a0 = PAT ? a0 + A0.x : fma(x0.x, A0.x, a0); a1 = PAT ? a1 + A0.y : fma(x0.x, A0.y, a1);
-            b0 = PAT ? b0 + B0.x : fma(x0.x, B0.x, b0); b1 = PAT ? b1 + B0.y : fma(x0.x, B0.y, b1);
-          }
-          if (lc.y >= 0) {
-            a0 = PAT ? a0 + A1.x : fma(x0.y, A1.x, a0); a1 = PAT ? a1 + A1.y : fma(x0.y, A1.y, a1);
-            b0 = PAT ? b0 + B1.x : fma(x0.y, B1.x, b0); b1 = PAT ? b1 + B1.y : fma(x0.y, B1.y, b1);
-          }
-          if (lc.z >= 0) {
-            a0 = PAT ? a0 + A2.x : fma(x1.x, A2.x, a0); a1 = PAT ? a1 + A2.y : fma(x1.x, A2.y, a1);
-            b0 = PAT ? b0 + B2.x : fma(x1.x, B2.x, b0); b1 = PAT ? b1 + B2.y : fma(x1.x, B2.y, b1);
-          }
-          if (lc.w >= 0) {
-            a0 = PAT ? a0 + A3.x : fma(x1.y, A3.x, a0); a1 = PAT ? a1 + A3.y : fma(x1.y, A3.y, a1);
-            b0 = PAT ? b0 + B3.x : fma(x1.y, B3.x, b0); b1 = PAT ? b1 + B3.y : fma(x1.y, B3.y, b1);
-          }
-        }
+        if (lc.x < 0) { A0 = make_double2(0.0, 0.0); B0 = A0; }
+        if (lc.y < 0) { A1 = make_double2(0.0, 0.0); B1 = A1; }
+        if (lc.z < 0) { A2 = make_double2(0.0, 0.0); B2 = A2; }
+        if (lc.w < 0) { A3 = make_double2(0.0, 0.0); B3 = A3; }
+      }
+      if (PAT) {
+        a0 += A0.x; a1 += A0.y; b0 += B0.x; b1 += B0.y;
+        a0 += A1.x; a1 += A1.y; b0 += B1.x; b1 += B1.y;
+        a0 += A2.x; a1 += A2.y; b0 += B2.x; b1 += B2.y;
+        a0 += A3.x; a1 += A3.y; b0 += B3.x; b1 += B3.y;
+      } else {
+        a0 = fma(x0.x, A0.x, a0); a1 = fma(x0.x, A0.y, a1); b0 = fma(x0.x, B0.x, b0); b1 = fma(x0.x, B0.y, b1);
+        a0 = fma(x0.y, A1.x, a0); a1 = fma(x0.y, A1.y, a1); b0 = fma(x0.y, B1.x, b0); b1 = fma(x0.y, B1.y, b1);
+        a0 = fma(x1.x, A2.x, a0); a1 = fma(x1.x, A2.y, a1); b0 = fma(x1.x, B2.x, b0); b1 = fma(x1.x, B2.y, b1);
+        a0 = fma(x1.y, A3.x, a0); a1 = fma(x1.y, A3.y, a1); b0 = fma(x1.y, B3.x, b0); b1 = fma(x1.y, B3.y, b1);
       }
     }
     if (row >= 0) {
       double* o = T + (int64_t)row * k + c0;
-      if (kc == 16 && (k & 1) == 0) {
+      if (VEC) {
         *reinterpret_cast<double2*>(o + 2 * cA) = make_double2(a0, a1);
         *reinterpret_cast<double2*>(o + 2 * cB) = make_double2(b0, b1);
       } else {
@@ -732,137 +728,119 @@ __global__ void __launch_bounds__(FUSE ? 512 : 1024, 1) k_spmm_k1v2(BlockK1v2 h,
       }
     }
   }
+  cp_async_wait<0>();
 }
 
 // Hot features: one CTA per sample block b stages T[bR .. bR + R) (16 columns) in
-// shared memory once; a group of 4 lanes per hot feature sums its entries of the
-// block in row order, lane g owning columns 4g .. 4g + 3 (two 16-byte shared
-// loads per entry), entries loaded 8 at a time (broadcast within the group).
-constexpr int kHotBlkThreads = 1024;
+// shared memory once (rows at their 128-byte stride, row R zero), then sums the
+// block's segments from it exactly as K1's hot phase does: a group of 4 lanes per
+// segment, records streamed through per-warp cp.async rings, conflict-free reads.
+constexpr int kHotBlkThreads = 512, kHotBlkDepth = 4;
 
 template <bool PAT>
 __global__ void __launch_bounds__(kHotBlkThreads, 1) k_xt_hotblk(BlockHot hb, const double* __restrict__ T, int k,
                                                                 int c0, int kc, int64_t N) {
-  extern __shared__ double ts[];
+  constexpr int REC = PAT ? kRecLab : kRecLab + 256;
+  constexpr int D = kHotBlkDepth, NS = D + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* ts = reinterpret_cast<double*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t s0 = (int64_t)b * hb.R;
   const int nb = (int)(N - s0 < (int64_t)hb.R ? N - s0 : (int64_t)hb.R);
-  // rows at their natural 128-byte stride; row R is zero (the padding target).  A
-  // group of 4 lanes owns a feature, lane g the 16-byte column pairs g and 4 + g;
-  // even groups read pair g first, odd groups pair 4 + g: the two groups a
-  // shared-memory wavefront serves cover all 32 banks for any two rows.
-  for (int e = threadIdx.x; e < nb * 16; e += kHotBlkThreads) {
-    const int r = e >> 4, q = e & 15;
-    ts[e] = q < kc ? __ldcg(T + (s0 + r) * k + c0 + q) : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane & 3, i = lane >> 2;
+  unsigned char* ring = smem_raw + (size_t)(hb.R + 1) * 128 + (size_t)warp * NS * REC;
+  const bool vec = kc == 16 && k == 16 && c0 == 0;  // the block's T rows are one contiguous run
+  if (vec) {
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(T + s0 * 16);
+    for (int e = threadIdx.x; e < nb * 8; e += kHotBlkThreads) cp_async16(smem_raw + (size_t)e * 16, src + (size_t)e * 16);
   }
+  cp_async_commit();
+  // this warp's run of the block's records
+  const int64_t slA = hb.boff[b], slB = hb.boff[b + 1];
+  constexpr int W = kHotBlkThreads / 32;
+  const int64_t r0 = hb.off[slA], r1 = hb.off[slB], Rn = r1 - r0;
+  const int64_t sA = first_slice_at(hb.off, slA, slB, r0 + Rn * warp / W);
+  const int64_t sB = warp == W - 1 ? slB : first_slice_at(hb.off, slA, slB, r0 + Rn * (warp + 1) / W);
+  const int recA = sA < slB ? hb.off[sA] : (int)r1, recB = hb.off[sB];
+  const unsigned char* __restrict__ gsrc = reinterpret_cast<const unsigned char*>(hb.rec);
+  auto issue = [&](int rec) {
+    if (rec < recB && lane < REC / 16) cp_async16(ring + (rec % NS) * REC + lane * 16, gsrc + (size_t)rec * REC + lane * 16);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d) issue(recA + d);
+  if (!vec)
+    for (int e = threadIdx.x; e < nb * 16; e += kHotBlkThreads) {
+      const int r = e >> 4, q = e & 15;
+      ts[e] = q < kc ? __ldcg(T + (s0 + r) * k + c0 + q) : 0.0;
+    }
   if (threadIdx.x < 16) ts[hb.R * 16 + threadIdx.x] = 0.0;
+  cp_async_wait<D>();  // the T rows (the first group); the records stay in flight
   __syncthreads();
-  const int g = threadIdx.x & 3;
-  const int32_t* __restrict__ p = hb.ptr + (size_t)b * (hb.H + 1);
   const double2* __restrict__ ts2 = reinterpret_cast<const double2*>(ts);
-  const int lane = threadIdx.x & 31, sub = lane >> 2;
-  const int cA = (sub & 1) ? 4 + g : g, cB = (sub & 1) ? g : 4 + g;
-  const int zrow = hb.R * 8;
-  // the HL longest features: a warp each, 8 sub-groups taking every 8th entry (8
-  // independent chains, 4 entries of each in flight), the sub-group partials reduced
-  // by a fixed shuffle tree
-  for (int h = threadIdx.x >> 5; h < hb.HL; h += kHotBlkThreads / 32) {
-    const int e0 = p[h], e1 = p[h + 1];
+  const int cA = (i & 1) ? 4 + g : g, cB = (i & 1) ? g : 4 + g;
+  int cur = recA;
+  int n_end = sA < sB ? hb.off[sA + 1] : 0;
+  for (int64_t sl = sA; sl < sB; ++sl) {
+    const int e_end = n_end;
+    if (sl + 1 < sB) n_end = hb.off[sl + 2];
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-    for (int e = e0 + sub; e < e1; e += 32) {
-      int r[4];
-      double x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = e + 8 * u < e1;
-        r[u] = ok ? (int)ld_stream(hb.row + e + 8 * u) * 8 : zrow;
-        x[u] = (PAT || !ok) ? (ok ? 1.0 : 0.0) : ld_stream(hb.val + e + 8 * u);
+    for (; cur < e_end; ++cur) {
+      cp_async_wait<D - 1>();
+      __syncwarp();
+      issue(cur + D);
+      const unsigned char* slot = ring + (cur % NS) * REC;
+      const int4 lc = *reinterpret_cast<const int4*>(slot + i * 16);
+      const double2 A0 = ts2[lc.x * 8 + cA], B0 = ts2[lc.x * 8 + cB], A1 = ts2[lc.y * 8 + cA], B1 = ts2[lc.y * 8 + cB];
+      const double2 A2 = ts2[lc.z * 8 + cA], B2 = ts2[lc.z * 8 + cB], A3 = ts2[lc.w * 8 + cA], B3 = ts2[lc.w * 8 + cB];
+      if (PAT) {
+        a0 += A0.x; a1 += A0.y; b0 += B0.x; b1 += B0.y;
+        a0 += A1.x; a1 += A1.y; b0 += B1.x; b1 += B1.y;
+        a0 += A2.x; a1 += A2.y; b0 += B2.x; b1 += B2.y;
+        a0 += A3.x; a1 += A3.y; b0 += B3.x; b1 += B3.y;
+      } else {
+        const double2 x0 = *reinterpret_cast<const double2*>(slot + kRecLab + i * 32);
+        const double2 x1 = *reinterpret_cast<const double2*>(slot + kRecLab + i * 32 + 16);
+        a0 = fma(x0.x, A0.x, a0); a1 = fma(x0.x, A0.y, a1); b0 = fma(x0.x, B0.x, b0); b1 = fma(x0.x, B0.y, b1);
+        a0 = fma(x0.y, A1.x, a0); a1 = fma(x0.y, A1.y, a1); b0 = fma(x0.y, B1.x, b0); b1 = fma(x0.y, B1.y, b1);
+        a0 = fma(x1.x, A2.x, a0); a1 = fma(x1.x, A2.y, a1); b0 = fma(x1.x, B2.x, b0); b1 = fma(x1.x, B2.y, b1);
+        a0 = fma(x1.y, A3.x, a0); a1 = fma(x1.y, A3.y, a1); b0 = fma(x1.y, B3.x, b0); b1 = fma(x1.y, B3.y, b1);
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double2 A = ts2[r[u] + cA], B = ts2[r[u] + cB];
-        a0 = PAT ? a0 + A.x : fma(x[u], A.x, a0);
-        a1 = PAT ? a1 + A.y : fma(x[u], A.y, a1);
-        b0 = PAT ? b0 + B.x : fma(x[u], B.x, b0);
-        b1 = PAT ? b1 + B.y : fma(x[u], B.y, b1);
-      }
     }
-    if (sub & 1) {  // odd sub-groups hold (pair 4 + g, pair g): same columns in every lane g
-      double t0 = a0, t1 = a1;
-      a0 = b0; a1 = b1; b0 = t0; b1 = t1;
-    }
-#pragma unroll
-    for (int off = 4; off <= 16; off <<= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, off);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, off);
-      b0 += __shfl_xor_sync(0xffffffffu, b0, off);
-      b1 += __shfl_xor_sync(0xffffffffu, b1, off);
-    }
-    if (sub == 0) {
-      double* out = hb.part + ((size_t)b * hb.H + h) * 16;
-      *reinterpret_cast<double2*>(out + 2 * g) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(out + 8 + 2 * g) = make_double2(b0, b1);
-    }
+    double* out = hb.part + ((size_t)sl * 8 + i) * 16;
+    *reinterpret_cast<double2*>(out + 2 * cA) = make_double2(a0, a1);
+    *reinterpret_cast<double2*>(out + 2 * cB) = make_double2(b0, b1);
   }
-  // the other hot features: a group of 4 lanes each, 8 entries per round -- lane g
-  // loads entries e + g and e + 4 + g, shuffles inside the group hand them round;
-  // the warp's 8 groups share one trip count (padding entries read the zero row)
-  const int hbase = hb.HL + (threadIdx.x >> 5) * 8;
-  for (int hw = hbase; hw < hb.H; hw += kHotBlkThreads / 4) {
-    const int h = hw + sub;
-    const bool live = h < hb.H;
-    const int e0 = live ? p[h] : 0, e1 = live ? p[h + 1] : 0;
-    int len = e1 - e0;
-#pragma unroll
-    for (int off = 4; off <= 16; off <<= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, off));
-    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-    for (int j = 0; j < len; j += 8) {
-      const int ea = e0 + j + g, eb = ea + 4;
-      const bool oka = ea < e1, okb = eb < e1;
-      const int ra = oka ? (int)ld_stream(hb.row + ea) * 8 : zrow, rb = okb ? (int)ld_stream(hb.row + eb) * 8 : zrow;
-      const double xa = oka ? (PAT ? 1.0 : ld_stream(hb.val + ea)) : 0.0;
-      const double xb = okb ? (PAT ? 1.0 : ld_stream(hb.val + eb)) : 0.0;
-      int r[8];
-      double x[8];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        r[u] = __shfl_sync(0xffffffffu, ra, u, 4);
-        r[u + 4] = __shfl_sync(0xffffffffu, rb, u, 4);
-        x[u] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xa, u, 4);
-        x[u + 4] = PAT ? 1.0 : __shfl_sync(0xffffffffu, xb, u, 4);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double2 A = ts2[r[u] + cA], B = ts2[r[u] + cB];
-        a0 = PAT ? a0 + A.x : fma(x[u], A.x, a0);
-        a1 = PAT ? a1 + A.y : fma(x[u], A.y, a1);
-        b0 = PAT ? b0 + B.x : fma(x[u], B.x, b0);
-        b1 = PAT ? b1 + B.y : fma(x[u], B.y, b1);
-      }
-    }
-    if (live) {
-      double* out = hb.part + ((size_t)b * hb.H + h) * 16;
-      *reinterpret_cast<double2*>(out + 2 * cA) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(out + 2 * cB) = make_double2(b0, b1);
-    }
-  }
+  cp_async_wait<0>();
 }
 
-// out[feat[h]] = sum over the blocks + beta V: a CTA per hot feature, thread
-// (s, q) sums the blocks b = s (mod 8) in order, the 8 sub-sums added in s order.
-__global__ void __launch_bounds__(128) k_hot_fold(BlockHot hb, const double* __restrict__ V, double* __restrict__ out,
-                                                  double beta, int k, int c0, int kc) {
-  __shared__ double sh[8][16];
+// out[feat[h]] = the feature's partials summed + beta V: a CTA per hot feature, thread
+// (s, q) sums every 64th partial of the (block, segment)-ordered list (8 loads in
+// flight), the 64 sub-sums added in s order.
+constexpr int kFoldSubs = 64;
+__global__ void __launch_bounds__(kFoldSubs * 16) k_hot_fold(BlockHot hb, const double* __restrict__ V,
+                                                            double* __restrict__ out, double beta, int k, int c0,
+                                                            int kc) {
+  __shared__ double sh[kFoldSubs][16];
   const int h = blockIdx.x, q = threadIdx.x & 15, sub = threadIdx.x >> 4;
   double sum = 0.0;
-#pragma unroll 4
-  for (int b = sub; b < hb.nblk; b += 8) sum += __ldcg(hb.part + ((size_t)b * hb.H + h) * 16 + q);
+  const int j1 = hb.fptr[h + 1];
+  for (int j = hb.fptr[h] + sub; j < j1; j += 8 * kFoldSubs) {
+    int id[8];
+    double pv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) id[u] = j + u * kFoldSubs < j1 ? hb.fidx[j + u * kFoldSubs] : -1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pv[u] = id[u] >= 0 ? __ldcg(hb.part + (size_t)id[u] * 16 + q) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sum += pv[u];
+  }
   sh[sub][q] = sum;
   __syncthreads();
   if (sub == 0 && q < kc) {
     double tot = sh[0][q];
-#pragma unroll
-    for (int u = 1; u < 8; ++u) tot += sh[u][q];
+#pragma unroll 8
+    for (int u = 1; u < kFoldSubs; ++u) tot += sh[u][q];
     const int64_t o = (int64_t)hb.feat[h] * k + c0 + q;
     out[o] = tot + beta * V[o];
   }
@@ -2499,8 +2477,8 @@ void spmm_hot(int grid, size_t smem, cudaStream_t s, const SparseDev& x, const d
                                                          t, bs.slice0, bs.n_slices, k, c0, kc, n_hot, 0);
 }
 
-// RMG_BLOCK_K1V2: 0 = the round-2 split K1 (k_spmm_hot + cold SELL pass), 1 = the
-// chunk-interleaved hot pass + the cold SELL pass, 2 (default) = hot and cold fused
+// RMG_BLOCK_K1V2=0: the round-2 split K1 (k_spmm_hot + cold SELL pass) instead of the
+// record-streaming fused pass (read once: the layouts are built accordingly)
 int block_k1v2_mode() {
   static int mode = -1;
   if (mode < 0) {
@@ -2510,16 +2488,20 @@ int block_k1v2_mode() {
   return mode;
 }
 
-template <bool PAT, bool FUSE>
-void spmm_k1v2(int sms, cudaStream_t s, const BlockK1v2& h, const double* vk, int k, int c0, int kc, int64_t s0,
+constexpr int kK1Threads = 512, kK1Depth = 7;
+
+template <bool PAT, bool VEC>
+void spmm_k1v3(int sms, cudaStream_t s, const BlockK1v2& h, const double* vk, int k, int c0, int kc, int64_t s0,
                int64_t s1, double* t) {
   static bool attr = false;
+  const size_t smem = static_cast<size_t>(h.H1 + 1) * 128 +
+                      static_cast<size_t>(kK1Threads / 32) * (kK1Depth + 1) * (PAT ? 128 : 384);
   if (!attr) {
-    cudaFuncSetAttribute(k_spmm_k1v2<PAT, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(k_spmm_k1v3<PAT, VEC, kK1Threads, kK1Depth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
     attr = true;
   }
-  const size_t smem = static_cast<size_t>(h.H1 + 1) * 16 * sizeof(double);
-  k_spmm_k1v2<PAT, FUSE><<<sms, FUSE ? 512 : 1024, smem, s>>>(h, vk, k, c0, kc, s0, s1, t);
+  k_spmm_k1v3<PAT, VEC, kK1Threads, kK1Depth><<<sms, kK1Threads, smem, s>>>(h, vk, k, c0, kc, s0, s1, t);
 }
 
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
@@ -2557,44 +2539,22 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       const int g1 = grid_for(bs.n_slices * 32, 148 * 8);
       const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
       const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
-      const int v2 = (k1v2.H1 > 0 && x.col_inv != nullptr) ? block_k1v2_mode() : 0;
-      if (bs.n_slices > 0 && v2 > 0 && hot1.H1 > 0) {
+      if (bs.n_slices > 0 && k1v2.H1 > 0 && x.col_inv != nullptr) {
+        // K1 fused: hot labels from shared memory, cold ones gathered, records streamed
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const int64_t s0 = bs.slice0 * 4, s1 = std::min<int64_t>(k1v2.n_slices8, (bs.slice0 + bs.n_slices) * 4);
-        const bool pat = k1v2.hval == nullptr;
-        const bool fuse = v2 == 2 && kc == 16 && (k & 1) == 0;
-        if (fuse) {
-          if (pat)
-            spmm_k1v2<true, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+        const bool vec = kc == 16 && (k & 1) == 0;
+        if (k1v2.pattern) {
+          if (vec)
+            spmm_k1v3<true, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
           else
-            spmm_k1v2<false, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+            spmm_k1v3<true, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
         } else {
-          if (pat)
-            spmm_k1v2<true, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
+          if (vec)
+            spmm_k1v3<false, true>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
           else
-            spmm_k1v2<false, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
-          const SparseDev& xc = hot1.cold;  // the cold entries' SELL pass adds onto T
-          const int gc = grid_for(bs.n_slices * 32, 148 * 8);
-          if (xc.val == nullptr) {
-            if (xc.idx16 != nullptr)
-              k_spmm_sell<true, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
-                                                                     xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
-                                                                     c0, kc, 0, 1);
-            else
-              k_spmm_sell<true, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
-                                                                      xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
-                                                                      c0, kc, 0, 1);
-          } else {
-            if (xc.idx16 != nullptr)
-              k_spmm_sell<false, true, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
-                                                                      xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices, k,
-                                                                      c0, kc, 0, 1);
-            else
-              k_spmm_sell<false, false, false><<<gc, kThreads, 0, s>>>(xc.sell_off, xc.sell_row, xc.sell_len, xc.idx,
-                                                                       xc.idx16, xc.val, v, t, bs.slice0, bs.n_slices,
-                                                                       k, c0, kc, 0, 1);
-          }
+            spmm_k1v3<false, false>(sms, s, k1v2, vk, k, c0, kc, s0, s1, t);
         }
       } else if (bs.n_slices > 0 && hot1.H1 > 0 && x.col_inv != nullptr) {
         // K1 split: hot labels from shared memory (T written), cold SELL pass adds
@@ -2683,18 +2643,19 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
             bs, v, out, beta, k, c0, kc, first, last);
     }
     if (hot.H > 0) {  // hot features: from shared-memory T blocks, then folded
-      const size_t smem = static_cast<size_t>(hot.R + 1) * 16 * sizeof(double);  // + the zero row
+      const size_t smem = static_cast<size_t>(hot.R + 1) * 128 +
+                          static_cast<size_t>(kHotBlkThreads / 32) * (kHotBlkDepth + 1) * (hot.pattern ? 128 : 384);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(k_xt_hotblk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-        cudaFuncSetAttribute(k_xt_hotblk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        cudaFuncSetAttribute(k_xt_hotblk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_xt_hotblk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
       }
-      if (hot.val == nullptr)
+      if (hot.pattern)
         k_xt_hotblk<true><<<hot.nblk, kHotBlkThreads, smem, s>>>(hot, t, k, c0, kc, x.rows);
       else
         k_xt_hotblk<false><<<hot.nblk, kHotBlkThreads, smem, s>>>(hot, t, k, c0, kc, x.rows);
-      k_hot_fold<<<hot.H, 128, 0, s>>>(hot, v, out, beta, k, c0, kc);
+      k_hot_fold<<<hot.H, kFoldSubs * 16, 0, s>>>(hot, v, out, beta, k, c0, kc);
     }
   }
   check_launch("ridge_block");

@@ -193,12 +193,17 @@ void launch_dense_diag(const DenseDev& d, double beta, double* out, cudaStream_t
 // gather pass.
 struct BlockHot {
   int H = 0, R = 0, nblk = 0;
-  int HL = 0;                      // the first HL (longest) hot features: a warp each
-  const int32_t* ptr = nullptr;    // [nblk][H + 1] entry offsets
-  const uint16_t* row = nullptr;   // row within the block
-  const double* val = nullptr;     // nullptr: binary pattern
+  // per sample block: the hot features' entries cut into segments of <= 64, sorted by
+  // length, 8 segments to a slice, stored as records like K1's (BlockK1v2; the label
+  // is the row inside the block, padding = R, a zero row of the staged block)
+  const int32_t* boff = nullptr;   // [nblk + 1] first slice of each block
+  const int32_t* off = nullptr;    // [n_slices + 1] first record of each slice
+  const int32_t* rec = nullptr;    // records (96 ints each; pattern: 32)
   const int32_t* feat = nullptr;   // [H] the hot features (most popular first)
-  double* part = nullptr;          // [nblk][H][16]
+  const int32_t* fptr = nullptr;   // [H + 1] each hot feature's partials ...
+  const int32_t* fidx = nullptr;   // ... as rows of part, in (block, segment) order
+  double* part = nullptr;          // [n_slices * 8][16] one partial per segment
+  bool pattern = false;
 };
 // K1 split the same way: the H1 most popular labels' V rows staged in
 // shared memory per persistent CTA and summed per row from a row-major CSR of the
@@ -211,24 +216,21 @@ struct BlockHotK1 {
   const double* val = nullptr;     // nullptr: binary pattern
   SparseDev cold;                  // the remaining entries, SELL-32, original column indices
 };
-// K1, third layout ("chunk-interleaved"): slices of 8 rows (length
-// sorted inside 1024-row windows), a 4-lane group per row.  A chunk holds 4 entries of
-// each of the slice's 8 rows, [row i][entry g] contiguous: the group's 4 labels are one
-// 8-byte (hot, uint16) or 16-byte (cold, int32) broadcast load, its 4 values two
-// 16-byte loads, and a warp's loads of a chunk are 64 / 128 / 256 contiguous bytes.
-// Hot entries (label < H1) first, in label order (= descending popularity), padded
-// with label H1 (a zero row of the shared-memory block, value 0); cold entries
-// (label >= H1) follow in their own chunk list, padded with -1.
+// K1, third layout ("chunk-interleaved records"): slices of 8 rows
+// (sorted by hot / cold length inside 1024-row windows), a 4-lane group per row.  A
+// record holds 4 entries of each of the slice's 8 rows: int32 label[8][4], then (valued
+// matrices) double value[8][4].  A slice's records are contiguous: first the nhot
+// records of its hot entries (label < H1, in label order = descending popularity,
+// padded with label H1 = a zero row of the shared-memory block, value 0), then the
+// records of its cold entries (label >= H1, padded with -1, value 0).
 struct BlockK1v2 {
   int H1 = 0;
   int64_t n_slices8 = 0;
-  const int32_t* hoff = nullptr;   // [n_slices8 + 1] first hot chunk of each slice
-  const int32_t* coff = nullptr;   // [n_slices8 + 1] first cold chunk
+  const int32_t* off = nullptr;    // [n_slices8 + 1] first record of each slice
+  const int32_t* nhot = nullptr;   // [n_slices8] hot records of each slice
   const int32_t* srow = nullptr;   // [n_slices8 * 8] the sample in each slot (-1: none)
-  const uint16_t* hlab = nullptr;  // [hot chunks * 32]
-  const double* hval = nullptr;    // nullptr: binary pattern
-  const int32_t* clab = nullptr;   // [cold chunks * 32] popularity labels
-  const double* cval = nullptr;
+  const int32_t* rec = nullptr;    // records (96 ints each; pattern: 32)
+  bool pattern = false;
 };
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
                         const BlockHot& hot, const BlockHotK1& hot1, const BlockK1v2& k1v2, const double* v,

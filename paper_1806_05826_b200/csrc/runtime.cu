@@ -666,8 +666,8 @@ void Matrix::build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int
     });
     std::copy(order.begin(), order.end(), srow.begin() + w0);
   }
-  std::vector<int32_t> hoff(ns8 + 1, 0), coff(ns8 + 1, 0);
-  int64_t hrun = 0, crun = 0;
+  std::vector<int32_t> off(ns8 + 1, 0), nhot(ns8, 0);
+  int64_t run = 0;
   for (int64_t sl = 0; sl < ns8; ++sl) {
     int32_t wh = 0, wc = 0;
     for (int i = 0; i < 8; ++i) {
@@ -676,17 +676,17 @@ void Matrix::build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int
       wh = std::max(wh, hch[r]);
       wc = std::max(wc, cch[r]);
     }
-    hoff[sl] = static_cast<int32_t>(hrun);
-    coff[sl] = static_cast<int32_t>(crun);
-    hrun += wh;
-    crun += wc;
-    if (hrun * 32 > INT32_MAX || crun * 32 > INT32_MAX) return;  // keep the round-2 passes
+    off[sl] = static_cast<int32_t>(run);
+    nhot[sl] = wh;
+    run += wh + wc;
+    if (run * 96 > INT32_MAX) return;  // keep the round-2 passes
   }
-  hoff[ns8] = static_cast<int32_t>(hrun);
-  coff[ns8] = static_cast<int32_t>(crun);
-  std::vector<uint16_t> hlab(static_cast<size_t>(hrun) * 32, static_cast<uint16_t>(h1));
-  std::vector<int32_t> clab(static_cast<size_t>(crun) * 32, -1);
-  std::vector<double> hval(pattern ? 0 : hlab.size(), 0.0), cval(pattern ? 0 : clab.size(), 0.0);
+  off[ns8] = static_cast<int32_t>(run);
+  const size_t rec_ints = pattern ? 32 : 96;
+  std::vector<int32_t> rec(std::max<size_t>(1, static_cast<size_t>(run) * rec_ints), 0);
+  for (int64_t sl = 0; sl < ns8; ++sl)  // padding labels: H1 in hot records, -1 in cold ones
+    for (int64_t j = off[sl]; j < off[sl + 1]; ++j)
+      std::fill_n(rec.begin() + j * rec_ints, 32, j < off[sl] + nhot[sl] ? static_cast<int32_t>(h1) : -1);
   std::vector<std::pair<int32_t, int64_t>> row;
   for (int64_t sl = 0; sl < ns8; ++sl)
     for (int i = 0; i < 8; ++i) {
@@ -697,39 +697,112 @@ void Matrix::build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int
       std::sort(row.begin(), row.end());  // label order = descending popularity
       int64_t eh = 0, ec = 0;
       for (const auto& pq : row) {
-        if (pq.first < h1) {
-          const size_t at = ((static_cast<size_t>(hoff[sl]) + eh / 4) * 8 + i) * 4 + eh % 4;
-          hlab[at] = static_cast<uint16_t>(pq.first);
-          if (!pattern) hval[at] = xr.val[pq.second];
-          ++eh;
-        } else {
-          const size_t at = ((static_cast<size_t>(coff[sl]) + ec / 4) * 8 + i) * 4 + ec % 4;
-          clab[at] = pq.first;
-          if (!pattern) cval[at] = xr.val[pq.second];
-          ++ec;
-        }
+        const bool is_hot = pq.first < h1;
+        int64_t& e = is_hot ? eh : ec;
+        const size_t j = static_cast<size_t>(off[sl]) + (is_hot ? 0 : nhot[sl]) + e / 4;
+        int32_t* rp = rec.data() + j * rec_ints;
+        rp[i * 4 + e % 4] = pq.first;
+        if (!pattern) std::memcpy(rp + 32 + 2 * (i * 4 + e % 4), &xr.val[pq.second], sizeof(double));
+        ++e;
       }
     }
   cudaStream_t s = ctx->stream;
-  bk_hoff.upload(hoff.data(), hoff.size(), s);
-  bk_coff.upload(coff.data(), coff.size(), s);
+  bk_off.upload(off.data(), off.size(), s);
+  bk_nhot.upload(nhot.data(), std::max<size_t>(1, nhot.size()), s);
   bk_srow.upload(srow.data(), srow.size(), s);
-  bk_hlab.upload(hlab.data(), std::max<size_t>(1, hlab.size()), s);
-  bk_clab.upload(clab.data(), std::max<size_t>(1, clab.size()), s);
-  if (!pattern) {
-    bk_hval.upload(hval.data(), std::max<size_t>(1, hval.size()), s);
-    bk_cval.upload(cval.data(), std::max<size_t>(1, cval.size()), s);
-  }
+  bk_rec.upload(rec.data(), rec.size(), s);
   RMG_CK(cudaStreamSynchronize(s));
   bk1v2.H1 = static_cast<int>(h1);
   bk1v2.n_slices8 = ns8;
-  bk1v2.hoff = bk_hoff.get();
-  bk1v2.coff = bk_coff.get();
+  bk1v2.off = bk_off.get();
+  bk1v2.nhot = bk_nhot.get();
   bk1v2.srow = bk_srow.get();
-  bk1v2.hlab = bk_hlab.get();
-  bk1v2.clab = bk_clab.get();
-  bk1v2.hval = pattern ? nullptr : bk_hval.get();
-  bk1v2.cval = pattern ? nullptr : bk_cval.get();
+  bk1v2.rec = bk_rec.get();
+  bk1v2.pattern = pattern;
+}
+
+// Hot features of the block X^T pass (kernels.cuh, BlockHot): per sample block the hot
+// features' entries, cut into segments of <= 64 (most popular feature first, then
+// ascending samples), sorted by length, 8 to a slice, as records; every segment has a
+// 16-double partial, and fptr / fidx list each feature's partials in (block, segment)
+// order for the fold.
+void Matrix::build_block_hot(const HostCsr& ht, const std::vector<int32_t>& feat, int64_t R, int64_t nblk) {
+  constexpr int64_t kSeg = 64;
+  const int64_t H = static_cast<int64_t>(feat.size());
+  const size_t rec_ints = pattern ? 32 : 96;
+  std::vector<int64_t> cur(H);  // next entry of each hot feature (the blocks are walked in order)
+  for (int64_t h = 0; h < H; ++h) cur[h] = ht.ptr[feat[h]];
+  struct Seg { int32_t h; int64_t q0; int32_t len; };
+  std::vector<Seg> segs;
+  std::vector<int32_t> order;
+  std::vector<int32_t> boff(nblk + 1, 0), off(1, 0), rec;
+  std::vector<std::vector<int32_t>> flist(H);
+  int64_t n_slices = 0, n_rec = 0;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t lim = (b + 1) * R;
+    segs.clear();
+    for (int64_t h = 0; h < H; ++h) {
+      const int64_t q0 = cur[h], qe = ht.ptr[feat[h] + 1];
+      int64_t q = q0;
+      while (q < qe && ht.idx[q] < lim) ++q;
+      cur[h] = q;
+      for (int64_t a = q0; a < q; a += kSeg)
+        segs.push_back(Seg{static_cast<int32_t>(h), a, static_cast<int32_t>(std::min(kSeg, q - a))});
+    }
+    order.resize(segs.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return segs[x].len > segs[y].len; });
+    std::vector<int32_t> slot_of(segs.size());
+    for (size_t p = 0; p < order.size(); ++p) slot_of[order[p]] = static_cast<int32_t>(n_slices * 8 + p);
+    for (size_t sg = 0; sg < segs.size(); ++sg) flist[segs[sg].h].push_back(slot_of[sg]);
+    boff[b] = static_cast<int32_t>(n_slices);
+    const int64_t bs = (static_cast<int64_t>(segs.size()) + 7) / 8;
+    for (int64_t sl = 0; sl < bs; ++sl) {
+      const int64_t first = sl * 8;
+      const int64_t w = (segs[order[first]].len + 3) / 4;  // sorted: the slice's first segment is its longest
+      rec.resize(static_cast<size_t>(n_rec + w) * rec_ints, 0);
+      for (int64_t j = 0; j < w; ++j) std::fill_n(rec.begin() + (n_rec + j) * rec_ints, 32, static_cast<int32_t>(R));
+      for (int i = 0; i < 8 && first + i < static_cast<int64_t>(segs.size()); ++i) {
+        const Seg& sg = segs[order[first + i]];
+        for (int32_t e = 0; e < sg.len; ++e) {
+          int32_t* rp = rec.data() + static_cast<size_t>(n_rec + e / 4) * rec_ints;
+          rp[i * 4 + e % 4] = static_cast<int32_t>(ht.idx[sg.q0 + e] - b * R);
+          if (!pattern) std::memcpy(rp + 32 + 2 * (i * 4 + e % 4), &ht.val[sg.q0 + e], sizeof(double));
+        }
+      }
+      n_rec += w;
+      if (n_rec * 96 > INT32_MAX) return;  // keep the gather pass for everything
+      off.push_back(static_cast<int32_t>(n_rec));
+    }
+    n_slices += bs;
+  }
+  boff[nblk] = static_cast<int32_t>(n_slices);
+  std::vector<int32_t> fptr(H + 1, 0), fidx;
+  for (int64_t h = 0; h < H; ++h) {
+    fidx.insert(fidx.end(), flist[h].begin(), flist[h].end());
+    fptr[h + 1] = static_cast<int32_t>(fidx.size());
+  }
+  cudaStream_t s = ctx->stream;
+  bh_boff.upload(boff.data(), boff.size(), s);
+  bh_off.upload(off.data(), off.size(), s);
+  bh_rec.upload(rec.data(), std::max<size_t>(1, rec.size()), s);
+  bh_feat.upload(feat.data(), feat.size(), s);
+  bh_fptr.upload(fptr.data(), fptr.size(), s);
+  bh_fidx.upload(fidx.data(), std::max<size_t>(1, fidx.size()), s);
+  bh_part.alloc(std::max<size_t>(1, static_cast<size_t>(n_slices) * 8 * 16));
+  RMG_CK(cudaMemsetAsync(bh_part.get(), 0, bh_part.size() * sizeof(double), s));
+  RMG_CK(cudaStreamSynchronize(s));
+  bhot.H = static_cast<int>(H);
+  bhot.R = static_cast<int>(R);
+  bhot.nblk = static_cast<int>(nblk);
+  bhot.boff = bh_boff.get();
+  bhot.off = bh_off.get();
+  bhot.rec = bh_rec.get();
+  bhot.feat = bh_feat.get();
+  bhot.fptr = bh_fptr.get();
+  bhot.fidx = bh_fidx.get();
+  bhot.part = bh_part.get();
+  bhot.pattern = pattern;
 }
 
 // Block operator schedule: rows of X^T with <= 512 nonzeros
@@ -768,13 +841,20 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   {
     const char* e1 = std::getenv("RMG_BLOCK_HOTK1");  // rows of V kept in shared memory (0: off)
     const int64_t h1 = std::min<int64_t>(xr.f, e1 != nullptr ? std::max<int64_t>(0, std::atoll(e1)) : 1400);
+    const char* e2 = std::getenv("RMG_BLOCK_K1V2");  // "0": the round-2 split K1 (kernels.cu)
+    const bool v2 = e2 == nullptr || std::atoi(e2) != 0;
+    std::vector<int32_t> rank;
     if (!tma && h1 > 0 && x.view.col_inv != nullptr && h1 <= 1600) {
       std::vector<int64_t> cnt(xr.f, 0);  // the SELL's popularity ranks (same sort as upload_sell)
       for (int64_t c : xr.idx) ++cnt[c];
-      std::vector<int32_t> inv(xr.f), rank(xr.f);
+      std::vector<int32_t> inv(xr.f);
+      rank.resize(xr.f);
       std::iota(inv.begin(), inv.end(), 0);
       std::stable_sort(inv.begin(), inv.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
       for (int64_t j = 0; j < xr.f; ++j) rank[inv[j]] = static_cast<int32_t>(j);
+      if (v2) build_k1v2(xr, rank, h1);
+    }
+    if (!rank.empty() && bk1v2.H1 == 0) {
       std::vector<int32_t> hptr(xr.n + 1, 0);
       std::vector<uint16_t> hlab;
       std::vector<double> hval;
@@ -801,7 +881,6 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
         hptr[r + 1] = static_cast<int32_t>(hlab.size());
         cold.ptr[r + 1] = static_cast<int64_t>(cold.idx.size());
       }
-      build_k1v2(xr, rank, h1);
       if (hlab.size() < static_cast<size_t>(INT32_MAX)) {
         bh1_ptr.upload(hptr.data(), hptr.size(), s);
         bh1_lab.upload(hlab.data(), hlab.size(), s);
@@ -823,7 +902,14 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   {
     const char* e = std::getenv("RMG_BLOCK_HOTXT");  // "0": off; a number: the per-block minimum
     const double hot_min = e != nullptr ? std::atof(e) : 4.0;  // measured: 4 (2.11 ms) < 8 < 2 < off (2.27 ms)
-    constexpr int64_t R = 1536;  // 1536 rows x 16 doubles = 192 KB of shared memory
+    // rows per sample block: <= 1536 (192 KB of T rows in shared memory), chosen so that
+    // the blocks fill whole waves of one CTA per SM
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int64_t waves = std::max<int64_t>(1, ((n + 1535) / 1536 + sms - 1) / sms);
+    int64_t R = ((n + sms * waves - 1) / (sms * waves) + 7) / 8 * 8;
+    R = std::min<int64_t>(1536, std::max<int64_t>(512, R));
+    if (const char* er = std::getenv("RMG_BLOCK_HOTXT_ROWS")) R = std::min<int64_t>(1536, std::max<int64_t>(8, std::atoll(er)));
     const int64_t nblk = (n + R - 1) / R;
     std::vector<int32_t> feat;
     if (!tma && hot_min > 0.0 && nblk >= 2) {
@@ -837,53 +923,9 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
       }
     }
     const int64_t H = static_cast<int64_t>(feat.size());
-    if (H > 0) {
-      std::vector<int32_t> ptr(static_cast<size_t>(nblk) * (H + 1), 0);
-      for (int64_t h = 0; h < H; ++h)
-        for (int64_t q = ht.ptr[feat[h]]; q < ht.ptr[feat[h] + 1]; ++q)
-          ++ptr[static_cast<size_t>(ht.idx[q] / R) * (H + 1) + h + 1];
-      int64_t run = 0;  // block-major, then feature: offsets into one entry array
-      for (int64_t b = 0; b < nblk; ++b)
-        for (int64_t h = 0; h <= H; ++h) {
-          const size_t o = static_cast<size_t>(b) * (H + 1) + h;
-          const int64_t c = h < H ? ptr[o + 1] : 0;
-          ptr[o] = static_cast<int32_t>(run);
-          run += c;
-          if (run > INT32_MAX) throw InvalidArgument("block operator: hot entries exceed the int32 range");
-        }
-      for (int64_t b = 0; b < nblk; ++b) ptr[static_cast<size_t>(b) * (H + 1) + H] =
-          b + 1 < nblk ? ptr[static_cast<size_t>(b + 1) * (H + 1)] : static_cast<int32_t>(run);
-      std::vector<uint16_t> hrow(run);
-      std::vector<double> hval(pattern ? 0 : run);
-      std::vector<int32_t> cur(ptr);
-      for (int64_t h = 0; h < H; ++h)
-        for (int64_t q = ht.ptr[feat[h]]; q < ht.ptr[feat[h] + 1]; ++q) {
-          const int64_t smp = ht.idx[q], b = smp / R;
-          const int32_t at = cur[static_cast<size_t>(b) * (H + 1) + h]++;
-          hrow[at] = static_cast<uint16_t>(smp - b * R);
-          if (!pattern) hval[at] = ht.val[q];
-        }
+    if (H > 0) build_block_hot(ht, feat, R, nblk);
+    if (bhot.H > 0)
       for (int32_t j : feat) is_hot[j] = 1;
-      bh_ptr.upload(ptr.data(), ptr.size(), s);
-      bh_feat.upload(feat.data(), feat.size(), s);
-      bh_row.upload(hrow.data(), hrow.size(), s);
-      if (!pattern) bh_val.upload(hval.data(), hval.size(), s);
-      bh_part.alloc(static_cast<size_t>(nblk) * H * 16);
-      RMG_CK(cudaStreamSynchronize(s));
-      bhot.H = static_cast<int>(H);
-      const char* el = std::getenv("RMG_BLOCK_HOTXT_LONG");  // entries per block for a warp of its own
-      const int64_t long_min = el != nullptr ? std::max<int64_t>(1, std::atoll(el)) : 32;
-      int64_t hl = 0;
-      while (hl < H && ht.ptr[feat[hl] + 1] - ht.ptr[feat[hl]] >= long_min * nblk) ++hl;
-      bhot.HL = static_cast<int>(hl);
-      bhot.R = static_cast<int>(R);
-      bhot.nblk = static_cast<int>(nblk);
-      bhot.ptr = bh_ptr.get();
-      bhot.row = bh_row.get();
-      bhot.val = pattern ? nullptr : bh_val.get();
-      bhot.feat = bh_feat.get();
-      bhot.part = bh_part.get();
-    }
   }
   if (tma) {  // X's row CSR for the TMA K1 (column order: the reference's summation order per row)
     const std::vector<int32_t> i32 = narrow(xr.idx, "column indices");

@@ -227,18 +227,16 @@ struct Matrix {
   DBuf<double> bh1_val;
   DeviceSparse bh1_cold;
   BlockK1v2 bk1v2;             // chunk-interleaved K1 layout (H1 = 0: none)
-  DBuf<int32_t> bk_hoff, bk_coff, bk_srow, bk_clab;
-  DBuf<uint16_t> bk_hlab;
-  DBuf<double> bk_hval, bk_cval;
-  DBuf<int32_t> bh_ptr, bh_feat;
-  DBuf<uint16_t> bh_row;
-  DBuf<double> bh_val, bh_part;
+  DBuf<int32_t> bk_off, bk_nhot, bk_srow, bk_rec;
+  DBuf<int32_t> bh_boff, bh_off, bh_rec, bh_feat, bh_fptr, bh_fidx;
+  DBuf<double> bh_part;
   std::vector<BlockChunkBufs> bchunk_bufs;
   std::vector<BlockXtSchedule> bviews;
   DBuf<int32_t> bbounds;       // (chunks + 1) x F entry offsets into X^T
   int64_t bchunk_rows = 0;
   DBuf<double> bseg, bt, bvp;  // + scratch T (N x k) and permuted V (F x k), kept across calls
   void build_block_schedule(const HostCsr& x, const HostCsr& ht);
+  void build_block_hot(const HostCsr& ht, const std::vector<int32_t>& feat, int64_t R, int64_t nblk);
   void build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int64_t h1);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
