@@ -57,8 +57,8 @@ CONFIGS = {
                  "10000/1000/100 (sketched k-means on unit-normalised columns, DESIGN.md §4.10); 16 right-hand "
                  "sides b_k = normals(42+k) solved as one batched block operator per beta; rel. residual 1e-6",
         kind="zipf", n=1_000_000, f=100_000, mean=50.0, zipf=1.1, abs_values=True, seed=0, beta=1.0,
-        ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle_additive", tol=1e-6, max_iters=1000,
-        golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32, ref_method="jacobi_cg",
+        ks=[10_000, 1_000, 100], normalize=True, method="pcg_vcycle_additive", additive_levels=[1], tol=1e-6,
+        max_iters=1000, golden="cfg3_none", betas=[1e-3, 1e-2, 1e-1, 1.0, 10.0], n_rhs=16, sketch=32, ref_method="jacobi_cg",
         ref_fixture="cfg3_ref.json"),
     "cfg5": dict(
         workload="cfg5: binary CSR N=16,000,000 x F=500,000 (1.02e9 nonzeros), nnz/row max(1,Poisson(64)), Zipf(1.05) "
@@ -154,7 +154,8 @@ def level_specs(cfg, labels=None):
             cl = R.ClusteringChoice(kind=R.KMEANS, target_size=k, seed=0, kmeans_max_iters=100,
                                     normalize_columns=cfg["normalize"])
         sv = R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if last else R.INNER_FCG, tol=1e-6, max_iters=500)
-        specs.append(R.LevelSpec(clustering=cl, solver=sv))
+        add = cfg["method"] == "pcg_vcycle_additive" and i in cfg.get("additive_levels", [])
+        specs.append(R.LevelSpec(clustering=cl, solver=sv, additive=add))
     return specs
 
 
@@ -856,9 +857,12 @@ def block_bytes(n, f, nnz, pattern, k):
 
 def sweep_algorithm_text(cfg, lock):
     if cfg["method"] == "pcg_vcycle_additive":
+        add = sorted({0} | set(cfg.get("additive_levels", [])))
+        first_mult = max(add) + 1
         return (f"pcg_vcycle_additive: PCG (krylov.cpp:94-157) preconditioned by the config's 4-level hierarchy with "
-                f"the finest level entered additively, z = D_0^-1 r + P_0 V_1(P_0^T r), V_1 the symmetric "
-                f"damped-Jacobi V-cycle of levels 1-3 (dense G_k for levels 1-2; DESIGN.md §4.11, §4.14, §4.15), {lock}")
+                f"level(s) {add} entered additively, z_k = D_k^-1 r_k + P_k M_(k+1)(P_k^T r_k), and the symmetric "
+                f"damped-Jacobi V-cycle on levels {first_mult}-3 (dense G_k where smaller than the level's sweeps; "
+                f"coarsest level direct; DESIGN.md §4.11, §4.14, §4.15), {lock}")
     return (f"{cfg['method']}: PCG (krylov.cpp:94-157) preconditioned by a symmetric V-cycle over the "
             f"config's 4-level hierarchy (damped-Jacobi pre/post smoothing; dense G_k for levels 1-2, "
             f"DESIGN.md §4.11, §4.14), {lock}")

@@ -107,6 +107,10 @@ typedef struct {
   int32_t has_omega_override; /* parity runs: import the oracle's omega_k */
   double omega_override;
   uint64_t sketch_dim;        /* RMG_CLUSTER_KMEANS_SKETCH: rows of the sketch (0: 32) */
+  int32_t additive;           /* RMG_METHOD_PCG_VCYCLE_ADDITIVE only: the level this spec coarsens
+                               * (level i for levels[i]) enters additively, z = D^-1 r + P V(P^T r),
+                               * with no operator application of its own; level 0 always does
+                               * (DESIGN.md section 4.15).  0 elsewhere. */
 } rmg_level_spec;
 
 /* krylov.hpp:25-31 SolveReport; history arrays are caller buffers (may be NULL). */

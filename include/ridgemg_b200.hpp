@@ -90,6 +90,7 @@ struct LevelSpec {
   double beta_override = 0.0;
   bool has_omega_override = false;
   double omega_override = 0.0;
+  bool additive = false;  // pcg_vcycle_additive: this level enters additively too (extension)
 };
 
 // krylov.hpp:207-218
@@ -213,6 +214,7 @@ inline std::vector<rmg_level_spec> to_c(const std::vector<LevelSpec>& levels) {
     s.coarse_truncation = l.solver.truncation;
     s.has_beta_override = l.has_beta_override ? 1 : 0;
     s.beta_override = l.beta_override;
+    s.additive = l.additive ? 1 : 0;
     s.has_omega_override = l.has_omega_override ? 1 : 0;
     s.omega_override = l.omega_override;
   }

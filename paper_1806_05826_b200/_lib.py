@@ -37,6 +37,7 @@ class LevelSpecC(C.Structure):
         ("has_omega_override", C.c_int32),
         ("omega_override", C.c_double),
         ("sketch_dim", C.c_uint64),
+        ("additive", C.c_int32),
     ]
 
 

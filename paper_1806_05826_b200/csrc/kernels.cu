@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_xt_block(const int32_t* __restr
   if (seg < 0) {  // chunks accumulate in chunk order; the last one adds beta V
     const int64_t o = (int64_t)row * k + c0 + q;
     double r = first ? acc : out[o] + acc;
-    if (last) r = r + beta * V[o];
+    if (last && beta != 0.0) r = r + beta * V[o];  // beta = 0: V is never read (the X^T-only pass has none)
     out[o] = r;
   } else {
     bs.seg[(int64_t)seg * kBlockCols + q] = acc;
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(kFoldSubs * 16) k_hot_fold(BlockHot hb, const 
 #pragma unroll 8
     for (int u = 1; u < kFoldSubs; ++u) tot += sh[u][q];
     const int64_t o = (int64_t)hb.feat[h] * k + c0 + q;
-    out[o] = tot + beta * V[o];
+    out[o] = beta != 0.0 ? tot + beta * V[o] : tot;
   }
 }
 
@@ -861,7 +861,7 @@ __global__ void k_block_finish(BlockXtSchedule bs, const double* __restrict__ V,
     if (lane == 0) {
       const int64_t o = (int64_t)m.x * k + c0 + q;
       double r = first ? sum : out[o] + sum;
-      if (last) r = r + beta * V[o];
+      if (last && beta != 0.0) r = r + beta * V[o];
       out[o] = r;
     }
   }
@@ -2074,12 +2074,29 @@ __global__ void __launch_bounds__(kThreads) k_bdot_partial(const double* __restr
   }
 }
 
-__global__ void k_bdot_final(const double* __restrict__ partial, int g, int k, double* __restrict__ out) {
-  const int c = threadIdx.x;
-  if (c >= k) return;
+// out[c] = the g block partials of column c summed: 16 sub-sums over every 16th
+// block (4 loads in flight), added in sub order -- a fixed order
+__global__ void __launch_bounds__(1024) k_bdot_final(const double* __restrict__ partial, int g, int k,
+                                                     double* __restrict__ out) {
+  __shared__ double sh[16][64];
+  const int c = threadIdx.x & 63, sub = threadIdx.x >> 6;
   double s = 0.0;
-  for (int b = 0; b < g; ++b) s += partial[(size_t)b * k + c];
-  out[c] = s;
+  if (c < k)
+    for (int b = sub; b < g; b += 64) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = b + 16 * u < g ? partial[(size_t)(b + 16 * u) * k + c] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s += v[u];
+    }
+  sh[sub][c] = s;
+  __syncthreads();
+  if (sub == 0 && c < k) {
+    double tot = sh[0][c];
+#pragma unroll
+    for (int u = 1; u < 16; ++u) tot += sh[u][c];
+    out[c] = tot;
+  }
 }
 
 // begin: nb = ||rhs||, non-finite check, rz = <r, z>
@@ -2191,21 +2208,36 @@ __global__ void __launch_bounds__(kThreads) k_badd(const double* __restrict__ x1
   grid_stride(nk, [&](int64_t q) { e[q] = x1[q] + e[q]; });
 }
 // rc[s][c] = sum over the members i of s (increasing) of w_i y[i][c]
+// a warp per cluster, lane (h, c): the members e = h (mod 2) in order for column
+// c0 + c (4 loads in flight), the two sub-sums added h = 0 first -- a fixed order
 __global__ void __launch_bounds__(kThreads) k_brestrict(const int32_t* __restrict__ mptr,
                                                         const int32_t* __restrict__ members,
                                                         const double* __restrict__ weight,
                                                         const double* __restrict__ y, double* __restrict__ rc,
                                                         int64_t nc, int k) {
-  grid_stride(nc * k, [&](int64_t q) {
-    const int64_t s = q / k;
-    const int c = (int)(q % k);
-    double acc = 0.0;
-    for (int e = mptr[s]; e < mptr[s + 1]; ++e) {
-      const int i = members[e];
-      acc += weight[i] * y[(int64_t)i * k + c];
+  const int lane = threadIdx.x & 31, h = lane >> 4, c = lane & 15;
+  const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t s = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; s < nc; s += nw) {
+    const int e0 = mptr[s], e1 = mptr[s + 1];
+    for (int c0 = 0; c0 < k; c0 += 16) {
+      const bool okc = c0 + c < k;
+      double acc = 0.0;
+      for (int e = e0 + h; e < e1; e += 8) {
+        double wv[4], yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = okc && e + 2 * u < e1;
+          const int i = ok ? members[e + 2 * u] : 0;
+          wv[u] = ok ? weight[i] : 0.0;
+          yv[u] = ok ? y[(int64_t)i * k + c0 + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += wv[u] * yv[u];
+      }
+      const double other = __shfl_xor_sync(0xffffffffu, acc, 16);
+      if (h == 0 && okc) rc[s * k + c0 + c] = acc + other;
     }
-    rc[q] = acc;
-  });
+  }
 }
 // e[i][c] = w_i ec[label_i][c]
 __global__ void __launch_bounds__(kThreads) k_bprolong(const int32_t* __restrict__ label,
@@ -2217,17 +2249,33 @@ __global__ void __launch_bounds__(kThreads) k_bprolong(const int32_t* __restrict
     e[q] = weight[i] * ec[(int64_t)label[i] * k + q % k];
   });
 }
-// ec = A_c^-1 rc for k columns (row-major nc x nc inverse)
+// ec = A_c^-1 rc for k columns (row-major nc x nc inverse): a warp per row i, lane
+// (h, c) sums the j = h (mod 2) terms of column c0 + c in order (4 in flight), h = 0
+// first -- a fixed order
 __global__ void __launch_bounds__(kThreads) k_bgemm_inv(const double* __restrict__ ainv, const double* __restrict__ rc,
                                                         double* __restrict__ ec, int64_t nc, int k) {
-  grid_stride(nc * k, [&](int64_t q) {
-    const int64_t i = q / k;
-    const int c = (int)(q % k);
+  const int lane = threadIdx.x & 31, h = lane >> 4, c = lane & 15;
+  const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; i < nc; i += nw) {
     const double* row = ainv + i * nc;
-    double acc = 0.0;
-    for (int64_t j = 0; j < nc; ++j) acc += row[j] * rc[j * k + c];
-    ec[q] = acc;
-  });
+    for (int c0 = 0; c0 < k; c0 += 16) {
+      const bool okc = c0 + c < k;
+      double acc = 0.0;
+      for (int64_t j = h; j < nc; j += 8) {
+        double av[4], rv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = okc && j + 2 * u < nc;
+          av[u] = ok ? row[j + 2 * u] : 0.0;
+          rv[u] = ok ? rc[(j + 2 * u) * k + c0 + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += av[u] * rv[u];
+      }
+      const double other = __shfl_xor_sync(0xffffffffu, acc, 16);
+      if (h == 0 && okc) ec[i * k + c0 + c] = acc + other;
+    }
+  }
 }
 // column-major (n x k) <-> row-major (n x k)
 __global__ void __launch_bounds__(kThreads) k_bcol2row(const double* __restrict__ cm, double* __restrict__ rm,
@@ -2252,7 +2300,7 @@ __global__ void __launch_bounds__(kThreads) k_bnonfinite(const double* __restric
 void launch_bdots(const double* a, const double* b, int64_t n, int k, double* partial, int g, double* out,
                   cudaStream_t s) {
   k_bdot_partial<<<g, kThreads, 0, s>>>(a, b, n, k, partial);
-  k_bdot_final<<<1, 64, 0, s>>>(partial, g, k, out);
+  k_bdot_final<<<1, 1024, 0, s>>>(partial, g, k, out);
   check_launch("bdots");
 }
 void launch_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, const double* bad, int k, double* hist,
@@ -2292,14 +2340,14 @@ void launch_badd(const double* x1, double* e, int64_t nk, cudaStream_t s) {
 }
 void launch_brestrict(const int32_t* mptr, const int32_t* members, const double* weight, const double* y, double* rc,
                       int64_t nc, int k, cudaStream_t s) {
-  k_brestrict<<<grid_for(nc * k, 148 * 8), kThreads, 0, s>>>(mptr, members, weight, y, rc, nc, k);
+  k_brestrict<<<grid_for(nc * 32, 148 * 8), kThreads, 0, s>>>(mptr, members, weight, y, rc, nc, k);
 }
 void launch_bprolong(const int32_t* label, const double* weight, const double* ec, double* e, int64_t nf, int k,
                      cudaStream_t s) {
   k_bprolong<<<grid_for(nf * k, 148 * 8), kThreads, 0, s>>>(label, weight, ec, e, nf, k);
 }
 void launch_bgemm_inv(const double* ainv, const double* rc, double* ec, int64_t nc, int k, cudaStream_t s) {
-  k_bgemm_inv<<<grid_for(nc * k, 148 * 8), kThreads, 0, s>>>(ainv, rc, ec, nc, k);
+  k_bgemm_inv<<<grid_for(nc * 32, 148 * 8), kThreads, 0, s>>>(ainv, rc, ec, nc, k);
 }
 void launch_bcol2row(const double* cm, double* rm, int64_t n, int k, cudaStream_t s) {
   k_bcol2row<<<grid_for(n * k, 148 * 8), kThreads, 0, s>>>(cm, rm, n, k);
@@ -2506,11 +2554,12 @@ void spmm_k1v3(int sms, cudaStream_t s, const BlockK1v2& h, const double* vk, in
 
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
                         const BlockHot& hot, const BlockHotK1& hot1, const BlockK1v2& k1v2, const double* v,
-                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s) {
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s, bool xt_only) {
   if (x.rows == 0 || x.cols == 0 || k <= 0) return;
   if (x.sell_off == nullptr) throw std::runtime_error("block operator: needs the SELL layout of X");
   // TMA gather passes (spmm_tma.cu) when V and T rows are 16-byte aligned
-  if (n_chunks > 0 && chunks[0].tk1.units != nullptr && tma_spmm_ok(v, k) && tma_spmm_ok(t, k)) {
+  if (xt_only && beta != 0.0) throw std::runtime_error("block X^T pass: beta must be 0");
+  if (!xt_only && n_chunks > 0 && chunks[0].tk1.units != nullptr && tma_spmm_ok(v, k) && tma_spmm_ok(t, k)) {
     for (int c0 = 0; c0 < k; c0 += kBlockCols) {
       const int kc = std::min(kBlockCols, k - c0);
       for (int c = 0; c < n_chunks; ++c) {
@@ -2527,7 +2576,7 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
     return;
   }
   const double* vk = v;
-  if (x.col_inv != nullptr) {  // relabeled columns: V rows into label order
+  if (!xt_only && x.col_inv != nullptr) {  // relabeled columns: V rows into label order
     k_vperm_block<<<grid_for(x.cols * k, 148 * 8), kThreads, 0, s>>>(v, x.col_inv, vp, x.cols, k);
     vk = vp;
   }
@@ -2539,7 +2588,9 @@ void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSc
       const int g1 = grid_for(bs.n_slices * 32, 148 * 8);
       const int64_t units = static_cast<int64_t>(bs.n_short) + bs.n_items;  // one half-warp each
       const int g2 = static_cast<int>(std::max<int64_t>(1, (units * 16 + kThreads - 1) / kThreads));
-      if (bs.n_slices > 0 && k1v2.H1 > 0 && x.col_inv != nullptr) {
+      if (xt_only) {
+        // t holds the caller's N x k block: only the X^T half runs
+      } else if (bs.n_slices > 0 && k1v2.H1 > 0 && x.col_inv != nullptr) {
         // K1 fused: hot labels from shared memory, cold ones gathered, records streamed
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);

@@ -234,7 +234,7 @@ struct BlockK1v2 {
 };
 void launch_ridge_block(const SparseDev& x, const SparseDev& xt, const BlockXtSchedule* chunks, int n_chunks,
                         const BlockHot& hot, const BlockHotK1& hot1, const BlockK1v2& k1v2, const double* v,
-                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s);
+                        double* out, double beta, int k, double* t, double* vp, cudaStream_t s, bool xt_only = false);
 // hot part of the hybrid X^T pass: writes sums[feat[h]] for every hot row h
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s);

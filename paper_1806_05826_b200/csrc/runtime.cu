@@ -1012,6 +1012,16 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
   if (sync) ctx->sync();
 }
 
+void Matrix::xt_block_cm(const double* b_cm, double* out, int k) {
+  if (dense || comm != nullptr) throw InvalidArgument("block operator: single-GPU CSR matrices only");
+  if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
+  const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k;
+  if (bt.size() < nt) bt.alloc(nt);
+  launch_bcol2row(b_cm, bt.get(), n(), k, ctx->stream);
+  launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, bk1v2, nullptr, out,
+                     0.0, k, bt.get(), nullptr, ctx->stream, true);
+}
+
 // Dense X kept on the device: rows padded to ld = F rounded up to 4 elements
 // (16 B aligned rows), the fused single-sweep operator's scratch.
 void Matrix::init_dense(DBuf<char>&& data, int fp32, int64_t ld, int64_t rows) {
@@ -1924,6 +1934,7 @@ void Method::build_dense_grams() {
   const char* e = std::getenv("RMG_VC_DENSE");
   if (e != nullptr && std::string(e) == "0") return;
   for (size_t k = 1; k < coarse_.size(); ++k) {
+    if (vc_additive(k)) continue;  // an additive level never applies its operator
     Matrix& m = level_matrix(k);
     if (m.comm != nullptr && !m.rows_only) continue;
     const int64_t n = m.f();
@@ -2841,7 +2852,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   RMG_CK(cudaSetDevice(ctx_->device));
   cudaStream_t s = ctx_->stream;
   Matrix& m = *fine_;
-  const int64_t n = m.f(), N = m.n();
+  const int64_t n = m.f();
   const uint64_t maxit = std::max<uint64_t>(solver.max_iters, 1);
   const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (n + 255) / 256)));
   BlockWork& w = bw_;
@@ -2852,7 +2863,6 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
     w.z.alloc(nk);
     w.p.alloc(nk);
     w.ap.alloc(nk);
-    w.rhs_cm.alloc(nk);
     w.partial.alloc(static_cast<size_t>(g) * 64);
     w.dots.alloc(4 * 64);
     w.sc.alloc(64);
@@ -2861,8 +2871,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   if (w.hist.size() < (maxit + 1) * k) w.hist.alloc((maxit + 1) * k);
   double *rr = w.dots.get(), *rz = rr + 64, *pap = rr + 128, *bad = rr + 192;
   const auto t0 = Clock::now();
-  for (int q = 0; q < k; ++q) m.spmv_t(b_cm + static_cast<size_t>(q) * N, w.rhs_cm.get() + static_cast<size_t>(q) * n);
-  launch_bcol2row(w.rhs_cm.get(), w.r.get(), n, k, s);
+  m.xt_block_cm(b_cm, w.r.get(), k);  // rhs = X^T B, one block pass (row-major F x k)
   RMG_CK(cudaMemsetAsync(w.x.get(), 0, nk * sizeof(double), s));
   std::vector<BlockScalars> hs(k);
   for (auto& e : hs) {

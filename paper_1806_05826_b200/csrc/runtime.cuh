@@ -240,6 +240,8 @@ struct Matrix {
   void build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int64_t h1);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
+  // out (F x k, row-major) = X^T B for k columns given column-major (B_cm: k vectors of N): the block X^T pass
+  void xt_block_cm(const double* b_cm, double* out, int k);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
   // per-rank input: `local` holds rows [row0, row0 + local.n) of an n_global-row X
   // (row offsets rebased); every setup step on it is sharded (rmg_matrix_create_csr_rows)
@@ -358,7 +360,11 @@ class Method {
   int kind() const { return kind_; }
   // pcg_vcycle and its additive-fine-level variant share the hierarchy, smoothers and cycle
   bool vc_kind() const { return kind_ == RMG_METHOD_PCG_VCYCLE || kind_ == RMG_METHOD_PCG_VCYCLE_ADDITIVE; }
-  bool vc_additive(size_t k) const { return k == 0 && kind_ == RMG_METHOD_PCG_VCYCLE_ADDITIVE; }
+  // pcg_vcycle_additive: the finest level enters additively, and so does every level
+  // whose spec says so (rmg_level_spec.additive)
+  bool vc_additive(size_t k) const {
+    return kind_ == RMG_METHOD_PCG_VCYCLE_ADDITIVE && (k == 0 || (k < specs_.size() && specs_[k].spec.additive != 0));
+  }
   rmg_solver_config solver;
   double time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms);
   void set_profiling(bool on);

@@ -509,6 +509,7 @@ class LevelSpec:
     solver: CoarseSolveChoice = field(default_factory=CoarseSolveChoice)
     beta_override: Optional[float] = None
     omega_override: Optional[float] = None  # parity runs
+    additive: bool = False  # pcg_vcycle_additive: this level enters additively too
 
 
 @dataclass
@@ -541,6 +542,7 @@ def _level_array(levels: Sequence[LevelSpec]):
         s.kmeans_max_iters = c.kmeans_max_iters
         s.normalize_columns = int(c.normalize_columns)
         s.sketch_dim = c.sketch_dim
+        s.additive = int(lv.additive)
         if c.kind == IMPORTED:
             if c.labels is None:
                 raise ValueError("imported clustering without labels")

@@ -75,12 +75,16 @@ def test_cg_reaches_reference_solution(cfg3):
     pm.close()
 
 
-@pytest.mark.parametrize("kind", ["pcg_vcycle", "pcg_vcycle_additive"])  # additive: the bench headline's solver
+# additive01: the bench headline's solver (levels 0 and 1 additive, bench.CONFIGS["cfg3"]["additive_levels"])
+@pytest.mark.parametrize("kind", ["pcg_vcycle", "pcg_vcycle_additive", "additive01"])
 def test_batched_vcycle_reaches_reference_solution(cfg3, kind):
     _, ws, x, m, b = cfg3
+    add = kind == "additive01"
+    kind = "pcg_vcycle_additive" if add else kind
     levels = [R.LevelSpec(clustering=R.ClusteringChoice(kind=R.KMEANS_SKETCH, target_size=k, seed=0,
                                                         normalize_columns=True, sketch_dim=32),
-                          solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == 2 else R.INNER_FCG))
+                          solver=R.CoarseSolveChoice(kind=R.DIRECT_CHOLESKY if i == 2 else R.INNER_FCG),
+                          additive=add and i == 1)
               for i, k in enumerate([10_000, 1_000, 100])]
     pv = R.PreparedMethod(m, 1.0, R.MethodSpec(kind=R.method_from_string(kind), levels=levels, solver=R.SolverConfig(1e-12, 1000)))
     B = np.stack([b] + [R.rng_normals(43 + q, x.n_samples) for q in range(3)], axis=1)

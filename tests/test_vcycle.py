@@ -109,15 +109,17 @@ def test_vcycle_set_beta_and_errors(gpu):
 
 
 # ---------------------------------------------------------------- pcg_vcycle_additive
-def aspec(ks, tol=1e-10, max_iters=2000):
+def aspec(ks, tol=1e-10, max_iters=2000, additive=()):
     s = spec(ks, tol, max_iters)
     s.kind = R.PCG_VCYCLE_ADDITIVE
+    for k in additive:  # further additive levels (rmg_level_spec.additive)
+        s.levels[k].additive = True
     return s
 
 
-def restated_additive(pm, r):
+def restated_additive(pm, r, additive=(0,)):
     """z = D_0^-1 r + P_0 V_1(P_0^T r), V_1 the symmetric cycle of levels >= 1 (or the
-    coarsest direct solve for two levels)."""
+    coarsest direct solve for two levels); every level in `additive` enters the same way."""
     L = pm.n_levels - 1
     mats = [pm.x.x.dense()] + [pm.level_matrix(k).dense() for k in range(1, L + 1)]
     betas = [pm.level(k)["beta"] for k in range(L + 1)]
@@ -140,8 +142,8 @@ def restated_additive(pm, r):
             return np.linalg.solve(gram(k), rk)
         a, p = gram(k), pmat(k)
         dinv = 1.0 / np.diag(a)
-        if k == 0:
-            return dinv * rk + p @ cycle(1, p.T @ rk)
+        if k in additive:
+            return dinv * rk + p @ cycle(k + 1, p.T @ rk)
         x1 = ws[k] * dinv * rk
         x2 = x1 + p @ cycle(k + 1, p.T @ (rk - a @ x1))
         return x2 + ws[k] * dinv * (rk - a @ x2)
@@ -163,6 +165,29 @@ def test_additive_matches_restatement_and_is_spd(gpu, ks):
     assert pm.level(0)["omega"] == 1.0  # the additive level applies D^-1 unweighted
     for k in range(1, len(ks)):
         assert 0.0 < pm.level(k)["omega"] < 2.0
+
+
+@pytest.mark.parametrize("additive", [(1,), (1, 2), (2,)])
+def test_additive_levels_flag(gpu, orc, additive):
+    """rmg_level_spec.additive: deeper levels entered additively too (no operator
+    application at those levels); M stays SPD and equals the restatement; single and
+    batched solves reach the reference's solution."""
+    x = random_matrix(300, 120, 7, 0.3)
+    m = R.DeviceMatrix(x)
+    pm = R.PreparedMethod(m, 0.5, aspec([60, 15, 4], additive=additive))
+    rng = np.random.default_rng(3)
+    u, v = rng.standard_normal(120), rng.standard_normal(120)
+    mu, mv = pm.precondition(u), pm.precondition(v)
+    assert abs(u @ mv - v @ mu) <= 1e-12 * abs(u @ mv)
+    assert u @ mu > 0 and v @ mv > 0
+    assert rel_diff(mv, restated_additive(pm, v, additive=(0,) + tuple(additive))) <= 1e-12
+    B = np.stack([R.rng_normals(70 + q, 300) for q in range(3)], axis=1)
+    W, reps = pm.solve_batch(B)
+    for q in range(3):
+        ref = orc.solve(to_checker(orc, x), 0.5, B[:, q].copy(), "cg", tol=1e-12, max_iters=5000)
+        w1, r1 = pm.solve(B[:, q].copy())
+        assert reps[q].converged and r1.converged and abs(reps[q].iterations - r1.iterations) <= 1
+        assert rel_diff(W[:, q], ref.w) <= 1e-8 and rel_diff(w1, ref.w) <= 1e-8
 
 
 @pytest.mark.parametrize("ks", [[30], [40, 8]])

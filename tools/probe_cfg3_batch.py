@@ -26,7 +26,7 @@ stream = torch.cuda.current_stream()
 ctx.set_stream(stream.cuda_stream)
 x = bench.make_matrix(cfg)
 m = R.DeviceMatrix(x, ctx)
-spec = R.MethodSpec(kind=R.PCG_VCYCLE, levels=bench.level_specs(cfg), solver=R.SolverConfig(cfg["tol"], 1000))
+spec = R.MethodSpec(kind=R.PCG_VCYCLE if "mult" in sys.argv[2:] else R.PCG_VCYCLE_ADDITIVE, levels=bench.level_specs(cfg), solver=R.SolverConfig(cfg["tol"], 1000))
 pm = R.PreparedMethod(m, beta, spec)
 print(f"setup {time.time() - t0:.1f} s", flush=True)
 for k in range(pm.n_levels):
