@@ -350,6 +350,134 @@ void launch_gram_gemv(const double* G, int64_t ldg, const double* x, double beta
   check("gram_gemv");
 }
 
+// ---------------------------------------------------------------------------
+// G = X^T X of a dense row-major X (fp64 or fp32 storage, fp64 arithmetic) on the
+// FP64 tensor cores: the "dense multi-right-hand-side / beta-sweep variant, where the
+// operator becomes a dense contraction" of the north star.  A CTA owns one 64 x 64
+// tile (ti <= tj) of G and one split of the rows; it stages 16 rows of the tile's two
+// column strips at a time in shared memory (leading dimension 68: the A / B fragment
+// reads of a half-warp hit 16 different bank pairs) while the previous 16 rows are
+// multiplied; warp w computes the 32 x 32 quadrant (w / 2, w % 2): 4 x 4 DMMA tiles
+// per 4-row step.  Split partials are summed in split order by k_syrk_finish, which
+// also mirrors the tile into the lower triangle.
+constexpr int kSyTile = 64, kSyKC = 16, kSyLd = 68, kSyThreads = 128, kSySplitsMax = 64;
+
+template <bool F32>
+__global__ void __launch_bounds__(kSyThreads)
+    k_syrk_dmma(const void* __restrict__ X, int64_t ldx, int64_t rows, int cols, int64_t rows_per_split, int nt,
+                double* __restrict__ P) {
+  __shared__ double sa[2][kSyKC * kSyLd], sb[2][kSyKC * kSyLd];
+  // tile (ti, tj), ti <= tj, from the linear index (row-major over the upper triangle)
+  int ti = 0, rem = blockIdx.x;
+  while (rem >= nt - ti) {
+    rem -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + rem;
+  const int i0 = ti * kSyTile, j0 = tj * kSyTile;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  auto ld = [&](int64_t r, int c) -> double {
+    if (r >= r1 || c >= cols) return 0.0;
+    return F32 ? static_cast<double>(__ldg(static_cast<const float*>(X) + r * ldx + c))
+               : __ldg(static_cast<const double*>(X) + r * ldx + c);
+  };
+  double stage[16];
+  auto fetch = [&](int64_t rr) {  // 16 rows x (64 + 64) columns: 16 elements per thread, coalesced
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + u * kSyThreads, kk = e >> 7, c = e & 127;
+      stage[u] = ld(rr + kk, c < 64 ? i0 + c : j0 + c - 64);
+    }
+  };
+  auto put = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = threadIdx.x + u * kSyThreads, kk = e >> 7, c = e & 127;
+      if (c < 64) sa[buf][kk * kSyLd + c]= stage[u]; else sb[buf][kk * kSyLd + c - 64] = stage[u];
+    }
+  };
+  double acc[4][4][2] = {};
+  int buf = 0;
+  if (r0 < r1) {
+    fetch(r0);
+    put(0);
+  }
+  __syncthreads();
+  for (int64_t rr = r0; rr < r1; rr += kSyKC) {
+    const bool more = rr + kSyKC < r1;
+    if (more) fetch(rr + kSyKC);  // in flight while this chunk is multiplied
+    const double* a = sa[buf];
+    const double* b = sb[buf];
+#pragma unroll
+    for (int k4 = 0; k4 < kSyKC; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        af[t] = a[(k4 + (lane & 3)) * kSyLd + wm + 8 * t + (lane >> 2)];
+        bf[t] = b[(k4 + (lane & 3)) * kSyLd + wn + 8 * t + (lane >> 2)];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt2 = 0; nt2 < 4; ++nt2) dmma(acc[mt][nt2][0], acc[mt][nt2][1], af[mt], bf[nt2]);
+    }
+    if (more) put(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* part = P + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (kSyTile * kSyTile);
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt2 = 0; nt2 < 4; ++nt2)
+      *reinterpret_cast<double2*>(part + (wm + 8 * mt + (lane >> 2)) * kSyTile + wn + 8 * nt2 + 2 * (lane & 3)) =
+          make_double2(acc[mt][nt2][0], acc[mt][nt2][1]);
+}
+
+__global__ void k_syrk_finish(const double* __restrict__ P, int splits, int ntiles, int nt, int cols,
+                              double* __restrict__ G, int64_t ldg) {
+  int ti = 0, rem = blockIdx.x;
+  while (rem >= nt - ti) {
+    rem -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + rem;
+  for (int e = threadIdx.x; e < kSyTile * kSyTile; e += blockDim.x) {
+    double sum = 0.0;
+    for (int sp = 0; sp < splits; ++sp) sum += P[(static_cast<int64_t>(sp) * ntiles + blockIdx.x) * (kSyTile * kSyTile) + e];
+    const int i = ti * kSyTile + e / kSyTile, j = tj * kSyTile + e % kSyTile;
+    if (i < cols && j < cols) {
+      G[static_cast<int64_t>(i) * ldg + j] = sum;
+      G[static_cast<int64_t>(j) * ldg + i] = sum;
+    }
+  }
+}
+
+void syrk_dense_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64_t rows, int64_t cols, double* G,
+                     int64_t ldg) {
+  if (cols <= 0) return;
+  const int nt = static_cast<int>((cols + kSyTile - 1) / kSyTile), ntiles = nt * (nt + 1) / 2;
+  // splits: enough CTAs for ~8 per SM, at least 512 rows each
+  int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({int64_t{kSySplitsMax}, (148 * 8 + ntiles - 1) / ntiles,
+                                                                         (rows + 511) / 512})));
+  const int64_t rps = ((rows + splits - 1) / splits + kSyKC - 1) / kSyKC * kSyKC;
+  splits = static_cast<int>(std::max<int64_t>(1, (rows + rps - 1) / std::max<int64_t>(1, rps)));
+  double* P = nullptr;
+  if (cudaMalloc(&P, static_cast<size_t>(splits) * ntiles * kSyTile * kSyTile * sizeof(double)) != cudaSuccess)
+    throw std::runtime_error("syrk_dense_dmma: out of device memory");
+  const dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(splits));
+  if (fp32)
+    k_syrk_dmma<true><<<grid, kSyThreads, 0, s>>>(X, ldx, rows, static_cast<int>(cols), rps, nt, P);
+  else
+    k_syrk_dmma<false><<<grid, kSyThreads, 0, s>>>(X, ldx, rows, static_cast<int>(cols), rps, nt, P);
+  k_syrk_finish<<<ntiles, 256, 0, s>>>(P, splits, ntiles, nt, static_cast<int>(cols), G, ldg);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(P);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("syrk_dense_dmma: ") + cudaGetErrorString(e));
+  check("syrk_dense");
+}
+
 int64_t gram_gemm_scratch(int64_t n) { return static_cast<int64_t>(kGramSplitsMax) * n * 16; }
 
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,

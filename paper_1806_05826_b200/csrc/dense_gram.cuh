@@ -37,6 +37,13 @@ int64_t gram_gemm_scratch(int64_t n);
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,
                       double* scratch, cudaStream_t s);
 
+// G (cols x cols, row-major, leading dimension ldg) = X^T X of a dense row-major X
+// (rows x cols, leading dimension ldx elements, fp32 != 0: float storage) on the FP64
+// tensor cores, split over row ranges with the partials summed in a fixed order.
+// Synchronizes the stream.  (The dense multi-right-hand-side operator: DESIGN.md §4.16.)
+void syrk_dense_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64_t rows, int64_t cols, double* G,
+                     int64_t ldg);
+
 // X_c = X P on the device (coarsening.cpp:112-148), bit-identical to the host
 // restatement: per row, the products x_ri * w_i (separately rounded) of each
 // coarse column summed from 0.0 in increasing fine-column order, the row's coarse

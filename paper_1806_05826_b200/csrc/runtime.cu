@@ -999,10 +999,31 @@ void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
   for (auto& v : bviews) v.seg = bseg.get();
 }
 
+// Dense X, k right-hand sides: the operator is the dense contraction
+// (X^T X) V + beta V.  G = X^T X (F <= 1024: <= 8 MB, beta-free, kept for the matrix's
+// lifetime, so a beta sweep and every later block apply reuse it) is formed once on the
+// FP64 tensor cores (syrk_dense_dmma), and each apply is one DMMA skinny GEMM.
+void Matrix::ensure_block_gram() {
+  if (bgram.size() > 0) return;
+  const int64_t nf = f();
+  bgram_ld = (nf + 1) / 2 * 2;
+  bgram.alloc(static_cast<size_t>(std::max<int64_t>(1, nf)) * bgram_ld);
+  bgram_scratch.alloc(static_cast<size_t>(std::max<int64_t>(1, gram_gemm_scratch(nf))));
+  RMG_CK(cudaMemsetAsync(bgram.get(), 0, bgram.size() * sizeof(double), ctx->stream));
+  const DenseDev& d = dense->view;
+  syrk_dense_dmma(ctx->stream, d.data, d.fp32, d.ld, d.rows, d.cols, bgram.get(), bgram_ld);
+}
+
 void Matrix::apply_block(const double* v, double* out, double beta, int k, bool sync) {
-  if (dense || comm != nullptr) throw InvalidArgument("block operator: single-GPU CSR matrices only");
+  if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
   if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative");
+  if (dense) {
+    ensure_block_gram();
+    launch_gram_gemm(bgram.get(), bgram_ld, v, beta, out, f(), k, bgram_scratch.get(), ctx->stream);
+    if (sync) ctx->sync();
+    return;
+  }
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
@@ -1013,9 +1034,16 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
 }
 
 void Matrix::xt_block_cm(const double* b_cm, double* out, int k) {
-  if (dense || comm != nullptr) throw InvalidArgument("block operator: single-GPU CSR matrices only");
+  if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
   if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k;
+  if (dense) {  // one fused sweep per column (X is read k times: once per solve, not per iteration)
+    const size_t nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
+    if (bvp.size() < nv) bvp.alloc(nv);
+    for (int q = 0; q < k; ++q) spmv_t(b_cm + static_cast<size_t>(q) * n(), bvp.get() + static_cast<size_t>(q) * f());
+    launch_bcol2row(bvp.get(), out, f(), k, ctx->stream);
+    return;
+  }
   if (bt.size() < nt) bt.alloc(nt);
   launch_bcol2row(b_cm, bt.get(), n(), k, ctx->stream);
   launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, bk1v2, nullptr, out,
@@ -2768,11 +2796,11 @@ void Method::vcycle(size_t k, const double* r, double* z, const int32_t* done) {
 }
 
 bool Method::block_capable() const {
-  if (fine_->dense != nullptr || fine_->comm != nullptr) return false;
+  if (fine_->comm != nullptr) return false;
   if (kind_ == RMG_METHOD_CG || kind_ == RMG_METHOD_JACOBI_CG) return true;
   if (!vc_kind() || coarse_.empty()) return false;
   for (size_t k = 1; k < coarse_.size(); ++k) {
-    if (dgram(k) != nullptr) continue;
+    if (dgram(k) != nullptr || vc_additive(k)) continue;  // an additive level applies no operator
     const Matrix& m = level_matrix(k);
     if (m.dense != nullptr || m.comm != nullptr) return false;
   }
@@ -2847,7 +2875,7 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
 
 std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, int k) {
   if (!block_capable())
-    throw InvalidArgument("solve_block: cg, jacobi_cg or pcg_vcycle over a single-GPU CSR matrix only");
+    throw InvalidArgument("solve_block: cg, jacobi_cg or pcg_vcycle over a single-GPU matrix only");
   if (k < 1 || k > 64) throw InvalidArgument("solve_block: k must be in [1, 64]");
   RMG_CK(cudaSetDevice(ctx_->device));
   cudaStream_t s = ctx_->stream;
@@ -2887,6 +2915,7 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   launch_bpcg_begin(w.sc.get(), rr, rz, bad, k, w.hist.get(), s);
   RMG_CK(cudaMemcpyAsync(w.p.get(), w.z.get(), nk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const double beta0 = level_beta(0);
+  if (m.dense != nullptr) m.ensure_block_gram();  // before any graph capture (it allocates and synchronizes)
   auto iteration = [&] {
     cudaStream_t cs = ctx_->stream;  // the capture stream while a graph is recorded
     m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);

@@ -240,6 +240,9 @@ struct Matrix {
   void build_k1v2(const HostCsr& xr, const std::vector<int32_t>& rank, int64_t h1);
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
+  void ensure_block_gram();    // dense X: G = X^T X on the FP64 tensor cores, once
+  DBuf<double> bgram, bgram_scratch;
+  int64_t bgram_ld = 0;
   // out (F x k, row-major) = X^T B for k columns given column-major (B_cm: k vectors of N): the block X^T pass
   void xt_block_cm(const double* b_cm, double* out, int k);
   Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);

@@ -45,6 +45,23 @@ def test_block_errors(gpu):
         m.ridge_apply_block(0.1, np.zeros((60, 65)))
     with pytest.raises(ValueError):
         m.ridge_apply_block(-1.0, np.zeros((60, 4)))
-    d = R.DeviceMatrix.from_dense(np.ones((10, 4)))
-    with pytest.raises(ValueError):
-        d.ridge_apply_block(0.1, np.zeros((4, 2)))
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("shape,k", [((3000, 130), 16), ((517, 64), 5), ((2000, 1000), 23), ((40, 7), 1)])
+def test_dense_block_matches_numpy(gpu, fp32, shape, k):
+    """Dense X, k right-hand sides: G = X^T X formed once on the FP64
+    tensor cores (DMMA SYRK), each apply G V + beta V a DMMA skinny GEMM."""
+    rng = np.random.default_rng(shape[0] + k)
+    a = rng.standard_normal(shape)
+    if fp32:
+        a = a.astype(np.float32)
+    m = R.DeviceMatrix.from_dense(a)
+    v = rng.standard_normal((shape[1], k))
+    a64 = a.astype(np.float64)
+    for beta in (0.7, 1e-3):  # the second apply reuses G
+        out = m.ridge_apply_block(beta, v)
+        want = a64.T @ (a64 @ v) + beta * v
+        assert rel_diff(out, want) <= 1e-12, rel_diff(out, want)
+        col = m.ridge_apply(beta, v[:, k // 2].copy())
+        assert rel_diff(out[:, k // 2], col) <= 1e-12
