@@ -1014,6 +1014,16 @@ void Matrix::ensure_block_gram() {
   syrk_dense_dmma(ctx->stream, d.data, d.fp32, d.ld, d.rows, d.cols, bgram.get(), bgram_ld);
 }
 
+// First block call on a CSR matrix: build the block layouts from the host CSR.  Not
+// inside a graph capture (it allocates and synchronizes): solve_block calls it first.
+void Matrix::ensure_block_schedule() {
+  if (block_built || dense) return;
+  if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
+  const HostCsr ht = transpose(host);
+  build_block_schedule(host, ht);
+  block_built = true;
+}
+
 void Matrix::apply_block(const double* v, double* out, double beta, int k, bool sync) {
   if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
   if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
@@ -1024,6 +1034,7 @@ void Matrix::apply_block(const double* v, double* out, double beta, int k, bool 
     if (sync) ctx->sync();
     return;
   }
+  ensure_block_schedule();
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k, nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
   if (bt.size() < nt) bt.alloc(nt);
   if (x.view.col_inv != nullptr && bvp.size() < nv) bvp.alloc(nv);
@@ -1044,6 +1055,7 @@ void Matrix::xt_block_cm(const double* b_cm, double* out, int k) {
     launch_bcol2row(bvp.get(), out, f(), k, ctx->stream);
     return;
   }
+  ensure_block_schedule();
   if (bt.size() < nt) bt.alloc(nt);
   launch_bcol2row(b_cm, bt.get(), n(), k, ctx->stream);
   launch_ridge_block(x.view, xt.view, bviews.data(), static_cast<int>(bviews.size()), bhot, bhot1, bk1v2, nullptr, out,
@@ -1273,7 +1285,8 @@ void Matrix::init_sparse(const HostCsr& local) {
   xt.upload(ht, pattern, ctx->stream, false);
   sched.build(ht, ctx->stream, local.f);
   build_hot(ht, local.n);
-  build_block_schedule(local, ht);
+  // the block operator's layouts (K1 records, hot X^T blocks, chunk schedules) are built
+  // on the first block call (ensure_block_schedule): most matrices never see one
   t.alloc(std::max<int64_t>(1, local.n));
   gram_sc.alloc(1);
 }
@@ -2915,7 +2928,12 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   launch_bpcg_begin(w.sc.get(), rr, rz, bad, k, w.hist.get(), s);
   RMG_CK(cudaMemcpyAsync(w.p.get(), w.z.get(), nk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const double beta0 = level_beta(0);
-  if (m.dense != nullptr) m.ensure_block_gram();  // before any graph capture (it allocates and synchronizes)
+  // layouts and scratch of every block operator, before any graph capture (they allocate and synchronize)
+  if (m.dense != nullptr) m.ensure_block_gram();
+  m.ensure_block_schedule();
+  for (size_t lv = 1; lv < coarse_.size() && vc_kind(); ++lv)  // smoothed coarse levels applied as sparse sweeps
+    if (dgram(lv) == nullptr && !vc_additive(lv) && level_matrix(lv).dense == nullptr)
+      level_matrix(lv).ensure_block_schedule();
   auto iteration = [&] {
     cudaStream_t cs = ctx_->stream;  // the capture stream while a graph is recorded
     m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);

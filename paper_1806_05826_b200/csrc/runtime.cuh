@@ -241,6 +241,8 @@ struct Matrix {
   // out = X^T (X V) + beta V, V and out row-major F x k (device pointers)
   void apply_block(const double* v, double* out, double beta, int k, bool sync = true);
   void ensure_block_gram();    // dense X: G = X^T X on the FP64 tensor cores, once
+  void ensure_block_schedule();  // CSR X: the block layouts, on the first block call
+  bool block_built = false;
   DBuf<double> bgram, bgram_scratch;
   int64_t bgram_ld = 0;
   // out (F x k, row-major) = X^T B for k columns given column-major (B_cm: k vectors of N): the block X^T pass
