@@ -63,9 +63,11 @@ CONFIGS = {
     "cfg5": dict(
         workload="cfg5: binary CSR N=16,000,000 x F=500,000 (1.02e9 nonzeros), nnz/row max(1,Poisson(64)), Zipf(1.05) "
                  "columns, on ONE GPU; 4-level hierarchy 50000/5000/500 by sketched k-means (d=32, unit-normalised "
-                 "columns, DESIGN.md §4.10); beta=0.5; solver pcg_vcycle (DESIGN.md §4.11) to rel. residual 1e-6",
+                 "columns, DESIGN.md §4.10); beta=0.5; solver pcg_vcycle_additive (levels 0-1 additive, DESIGN.md §4.15) to "
+                 "rel. residual 1e-6",
         kind="zipf", n=16_000_000, f=500_000, mean=64.0, zipf=1.05, abs_values=False, seed=0, beta=0.5,
-        ks=[50_000, 5_000, 500], normalize=True, method="pcg_vcycle", tol=1e-6, max_iters=1000,
+        ks=[50_000, 5_000, 500], normalize=True, method="pcg_vcycle_additive", additive_levels=[1], tol=1e-6,
+        max_iters=1000,
         golden="cfg5_none", betas=[0.5], n_rhs=1, sketch=32, ref_method="jacobi_cg"),
     "cfg1": dict(
         workload="cfg1: dense clustered N=2000 x F=500 fp64 (row-major dense path); 2-level k-means 50; beta=1e-2; "
@@ -783,7 +785,7 @@ def run_b200(args, cfg):
                 "batched_pcg_vcycle_ms_per_rhs": min(ms) / K,
                 "batched_pcg_vcycle_ms_per_batch": ms,
                 "iterations": [int(r.iterations) for r in reps],
-                "includes": "rhs = X^T B (16 fused sweeps of X) inside every batch",
+                "includes": "rhs = X^T B inside every batch: one DMMA sweep of X for the 16 columns (k_xtb_dmma)",
             }
             pb.close()
         except Exception as e:  # reported, never fatal
@@ -1331,10 +1333,14 @@ def main():
                     help="skip the cfg5-shard operator roofline (about 20 s of setup)")
     ap.add_argument("--shard", action="store_true", help="row-shard X across ranks (strong scaling)")
     ap.add_argument("--method", default=None, help="override the config's solver (e.g. pcg_vcycle)")
+    ap.add_argument("--additive-levels", default=None,
+                    help="pcg_vcycle_additive: comma-separated levels >= 1 entered additively too (rmg_level_spec.additive)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.method:
         cfg["method"] = args.method
+    if args.additive_levels is not None:
+        cfg["additive_levels"] = [int(t) for t in args.additive_levels.split(",") if t]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     elif args.config in ("cfg3", "cfg5") and args.shard:

@@ -478,6 +478,162 @@ void syrk_dense_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64
   check("syrk_dense");
 }
 
+// ---------------------------------------------------------------------------
+// out (F x k) = X^T B for a dense X and k right-hand sides in ONE sweep of X (the rhs
+// of a batched solve; 16 single-vector sweeps before): M = F, N = 16, K = rows on the
+// FP64 tensor cores.  One persistent CTA per SM owns a contiguous row range and streams
+// it through a 3-stage cp.async ring (X rows in their storage type, fp32 converted at
+// the fragment load; the matching rows of B); warp w accumulates the columns
+// [128 w, 128 w + 128) x 16 in registers (16 x 2 DMMA tiles); per-CTA partials are summed
+// in CTA order by k_xtb_finish.  HBM-bound when the DMMA pipe keeps up (fp32 storage).
+constexpr int kXbThreads = 256, kXbStages = 3, kXbLdB = 20;
+
+__device__ __forceinline__ void xb_cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kXbThreads, 1)
+    k_xtb_dmma(const void* __restrict__ X, int64_t ldx, int64_t rows, int cols, const double* __restrict__ Bt,
+               int64_t rows_per_cta, double* __restrict__ P) {
+  constexpr int KC = F32 ? 16 : 8;
+  constexpr int ESZ = F32 ? 4 : 8;
+  extern __shared__ __align__(16) unsigned char xb_sm[];
+  const int cpad = (cols + 15) / 16 * 16;
+  const int ldS = cpad + (F32 ? 8 : 4);  // elements: the 16 lanes of a fragment read hit 16 bank pairs
+  const size_t xbytes = static_cast<size_t>(KC) * ldS * ESZ, sbytes = xbytes + KC * kXbLdB * 8;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  const int nchunks = r0 < r1 ? static_cast<int>((r1 - r0 + KC - 1) / KC) : 0;
+  const int ppr = (cols * ESZ + 15) / 16;  // 16-byte pieces per row of X
+  const unsigned char* xg = static_cast<const unsigned char*>(X);
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      unsigned char* st = xb_sm + static_cast<size_t>(c % kXbStages) * sbytes;
+      const int64_t rb = r0 + static_cast<int64_t>(c) * KC;
+      for (int e = threadIdx.x; e < KC * ppr; e += kXbThreads) {
+        const int kk = e / ppr, pc = e - kk * ppr;
+        unsigned char* dst = st + (static_cast<size_t>(kk) * ldS * ESZ) + pc * 16;
+        if (rb + kk < r1)
+          xb_cp_async16(dst, xg + (rb + kk) * ldx * ESZ + static_cast<size_t>(pc) * 16);
+        else
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      for (int e = threadIdx.x; e < KC * 8; e += kXbThreads) {
+        const int kk = e >> 3, pc = e & 7;
+        unsigned char* dst = st + xbytes + (static_cast<size_t>(kk) * kXbLdB * 8) + pc * 16;
+        if (rb + kk < r1)
+          xb_cp_async16(dst, reinterpret_cast<const unsigned char*>(Bt + (rb + kk) * 16) + pc * 16);
+        else
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[16][2][2] = {};
+#pragma unroll
+  for (int d = 0; d < kXbStages - 1; ++d) issue(d);
+  for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kXbStages - 2) : "memory");
+    __syncthreads();  // chunk c landed for every thread; chunk c - 1's stage is free
+    issue(c + kXbStages - 1);
+    const unsigned char* st = xb_sm + static_cast<size_t>(c % kXbStages) * sbytes;
+    const double* bs = reinterpret_cast<const double*>(st + xbytes);
+#pragma unroll
+    for (int k4 = 0; k4 < KC; k4 += 4) {
+      const int kr = k4 + (lane & 3);
+      const double b0 = bs[kr * kXbLdB + (lane >> 2)], b1 = bs[kr * kXbLdB + 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int f0 = (warp * 16 + j) * 8;
+        if (f0 < cols) {  // warp-uniform
+          const int f = f0 + (lane >> 2);
+          double a;
+          if (F32)
+            a = static_cast<double>(reinterpret_cast<const float*>(st)[kr * ldS + f]);
+          else
+            a = reinterpret_cast<const double*>(st)[kr * ldS + f];
+          if (f >= cols) a = 0.0;
+          dmma(acc[j][0][0], acc[j][0][1], a, b0);
+          dmma(acc[j][1][0], acc[j][1][1], a, b1);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  double* part = P + static_cast<int64_t>(blockIdx.x) * cpad * 16;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int f = (warp * 16 + j) * 8 + (lane >> 2);
+    if (f < cpad) {
+      *reinterpret_cast<double2*>(part + f * 16 + 2 * (lane & 3)) = make_double2(acc[j][0][0], acc[j][0][1]);
+      *reinterpret_cast<double2*>(part + f * 16 + 8 + 2 * (lane & 3)) = make_double2(acc[j][1][0], acc[j][1][1]);
+    }
+  }
+}
+
+// out[f][c0 + q] = the CTA partials summed in CTA order
+__global__ void k_xtb_finish(const double* __restrict__ P, int ncta, int cols, int cpad, int k, int c0, int kc,
+                             double* __restrict__ out) {
+  const int total = cols * kc;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int f = e / kc, q = e - f * kc;
+    double sum = 0.0;
+    for (int b = 0; b < ncta; ++b) sum += P[(static_cast<int64_t>(b) * cpad + f) * 16 + q];
+    out[static_cast<int64_t>(f) * k + c0 + q] = sum;
+  }
+}
+
+// Bt[r][q] = column c0 + q of the column-major block (k vectors of n), zero for q >= kc
+__global__ void k_bcol2row16(const double* __restrict__ cm, int64_t n, int c0, int kc, double* __restrict__ bt) {
+  const int64_t total = n * 16;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e >> 4;
+    const int q = static_cast<int>(e & 15);
+    bt[e] = q < kc ? cm[static_cast<int64_t>(c0 + q) * n + r] : 0.0;
+  }
+}
+
+int64_t xtb_scratch(int64_t rows, int64_t cols) {
+  const int64_t cpad = (cols + 15) / 16 * 16;
+  return rows * 16 + 148 * 2 * cpad * 16;  // the row-major 16-column block of B + per-CTA partials
+}
+
+void launch_xtb_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64_t rows, int64_t cols,
+                     const double* b_cm, int k, double* out, double* scratch) {
+  if (cols <= 0 || k <= 0) return;
+  if (cols > 1024) throw std::runtime_error("xtb_dmma: at most 1024 columns");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  sms = std::min(sms, 296);
+  const int cpad = static_cast<int>((cols + 15) / 16 * 16);
+  const int KC = fp32 ? 16 : 8, esz = fp32 ? 4 : 8;
+  const size_t smem = static_cast<size_t>(kXbStages) * (static_cast<size_t>(KC) * (cpad + (fp32 ? 8 : 4)) * esz + KC * kXbLdB * 8);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_xtb_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_xtb_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int64_t rpc = ((rows + sms - 1) / sms + KC - 1) / KC * KC;
+  const int ncta = static_cast<int>(std::max<int64_t>(1, (rows + rpc - 1) / std::max<int64_t>(1, rpc)));
+  double* bt = scratch;
+  double* P = scratch + rows * 16;
+  for (int c0 = 0; c0 < k; c0 += 16) {
+    const int kc = std::min(16, k - c0);
+    k_bcol2row16<<<148 * 8, 256, 0, s>>>(b_cm, rows, c0, kc, bt);
+    if (fp32)
+      k_xtb_dmma<true><<<ncta, kXbThreads, smem, s>>>(X, ldx, rows, static_cast<int>(cols), bt, rpc, P);
+    else
+      k_xtb_dmma<false><<<ncta, kXbThreads, smem, s>>>(X, ldx, rows, static_cast<int>(cols), bt, rpc, P);
+    k_xtb_finish<<<std::max(1, std::min(148 * 4, static_cast<int>((cols * kc + 255) / 256))), 256, 0, s>>>(
+        P, ncta, static_cast<int>(cols), cpad, k, c0, kc, out);
+  }
+  check("xtb_dmma");
+}
+
 int64_t gram_gemm_scratch(int64_t n) { return static_cast<int64_t>(kGramSplitsMax) * n * 16; }
 
 void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta, double* Y, int64_t n, int k,

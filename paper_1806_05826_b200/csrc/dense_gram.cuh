@@ -44,6 +44,13 @@ void launch_gram_gemm(const double* G, int64_t ldg, const double* V, double beta
 void syrk_dense_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64_t rows, int64_t cols, double* G,
                      int64_t ldg);
 
+// out (cols x k, row-major) = X^T B for the dense X above and a column-major block
+// b_cm (k vectors of `rows`), one sweep of X per 16 columns, on the FP64 tensor cores;
+// per-CTA partials summed in a fixed order.  scratch: xtb_scratch(rows, cols) doubles.
+int64_t xtb_scratch(int64_t rows, int64_t cols);
+void launch_xtb_dmma(cudaStream_t s, const void* X, int fp32, int64_t ldx, int64_t rows, int64_t cols,
+                     const double* b_cm, int k, double* out, double* scratch);
+
 // X_c = X P on the device (coarsening.cpp:112-148), bit-identical to the host
 // restatement: per row, the products x_ri * w_i (separately rounded) of each
 // coarse column summed from 0.0 in increasing fine-column order, the row's coarse

@@ -1048,11 +1048,11 @@ void Matrix::xt_block_cm(const double* b_cm, double* out, int k) {
   if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
   if (k <= 0 || k > 64) throw InvalidArgument("block operator: k must be in [1, 64]");
   const size_t nt = static_cast<size_t>(std::max<int64_t>(1, n())) * k;
-  if (dense) {  // one fused sweep per column (X is read k times: once per solve, not per iteration)
-    const size_t nv = static_cast<size_t>(std::max<int64_t>(1, f())) * k;
-    if (bvp.size() < nv) bvp.alloc(nv);
-    for (int q = 0; q < k; ++q) spmv_t(b_cm + static_cast<size_t>(q) * n(), bvp.get() + static_cast<size_t>(q) * f());
-    launch_bcol2row(bvp.get(), out, f(), k, ctx->stream);
+  if (dense) {  // X^T B in one sweep of X per 16 columns, on the FP64 tensor cores
+    const DenseDev& d = dense->view;
+    const size_t need = static_cast<size_t>(std::max<int64_t>(1, xtb_scratch(d.rows, d.cols)));
+    if (bt.size() < need) bt.alloc(need);
+    launch_xtb_dmma(ctx->stream, d.data, d.fp32, d.ld, d.rows, d.cols, b_cm, k, out, bt.get());
     return;
   }
   ensure_block_schedule();
