@@ -1008,8 +1008,8 @@ def run_sweep(args, cfg):
         pg.destroy_process_group()
         return
 
-    # the dominant kernel: the fine-level block operator (k_spmm_sell + k_xt_block), 3
-    # applications per lock-step PCG iteration (one outside, two inside the V-cycle)
+    # the dominant kernel: the fine-level block operator; pcg_vcycle applies it 3 times per lock-step
+    # PCG iteration (one outside, two inside the V-cycle), pcg_vcycle_additive once
     peak, peak_kind = peaks()
     vb = torch.randn(x.n_features, nb, dtype=torch.float64, device=dev)
     ob = torch.empty_like(vb)
@@ -1079,8 +1079,12 @@ def run_sweep(args, cfg):
 
     its = [[r.iterations for r in rs] for rs in reps]
     if nb > 1:
-        roof = {"bound": "hbm", "kernel": f"level-0 block operator X^T (X V) + beta V, k = {nb} (k_spmm_sell + "
-                                          "k_xt_block + k_block_finish), CUDA events on the library stream",
+        roof = {"bound": "hbm", "kernel": f"level-0 block operator X^T (X V) + beta V, k = {nb} (k_spmm_k1v3 + "
+                                          "k_xt_block + k_xt_hotblk + k_hot_fold + k_block_finish + k_vperm_block; "
+                                          "profiles/r2_block_operator_v3.md), CUDA events on the library stream",
+                "bound_note": "HBM is the reported roofline (SURVEY §8(d) bytes); the kernels themselves sit at 75 % of "
+                              "the shared-memory / L1 data pipe (hot passes) and 0.87 of the random 128-byte gather "
+                              "ceiling (cold pass): profiles/r2_block_operator_v3.md",
                 "achieved": bb / (t_block * 1e6), "peak": peak, "unit": "GB/s", "frac": bb / (t_block * 1e6) / peak,
                 "traffic": traffic, "algorithmic_bytes_per_launch": bb, "ms_per_launch": t_block,
                 "peak_kind": peak_kind, "share_of_step": fine_applies * t_block / total}

@@ -174,7 +174,9 @@ int rmg_ridge_apply(rmg_matrix* m, double beta, const double* w, double* out, in
  * counterpart: the reference applies RidgeOperator once per vector):
  * out = X^T (X V) + beta V with V, out row-major n_features x k, 1 <= k <= 64;
  * column q equals rmg_ridge_apply of column q up to summation order.  Single-GPU
- * CSR matrices. */
+ * matrices: CSR (record-streaming gather passes) or dense, where the
+ * operator is the dense contraction (X^T X) V + beta V on the FP64 tensor cores --
+ * G = X^T X is formed once by a DMMA SYRK on the first call and kept. */
 int rmg_ridge_apply_block(rmg_matrix* m, double beta, const double* v, double* out, uint64_t k, int32_t on_device);
 /* d_j = beta + ||X(:,j)||^2 (gram_diagonal, ridge.cpp:30-37) */
 int rmg_gram_diagonal(rmg_matrix* m, double beta, double* out, int32_t on_device);
@@ -305,8 +307,9 @@ int rmg_method_solve_rhs(rmg_method* pm, const double* rhs, double* w_out,
                          rmg_solve_report* report, int32_t on_device);
 /* k right-hand sides (SURVEY §8(b) k_rhs): b is column-major n_samples x k, w_out
  * column-major n_features x k, reports[k] optional.  Column q equals
- * rmg_method_solve of column q to rounding.  For cg, jacobi_cg and pcg_vcycle on
- * a single-GPU CSR matrix and 2 <= k <= 64 the k columns run in LOCK STEP: every
+ * rmg_method_solve of column q to rounding.  For cg, jacobi_cg, pcg_vcycle and
+ * pcg_vcycle_additive on a single-GPU matrix (CSR or dense) and 2 <= k <= 64 the k
+ * columns run in LOCK STEP: rhs = X^T B is one block pass, every
  * operator application at every level is one block-operator call (rmg_ridge_
  * apply_block; dense coarse Grams as one skinny GEMM), reductions are per column
  * in a fixed order and a converged column freezes.  Other
