@@ -97,6 +97,16 @@ def _worker(rank, world, port, q):
         res["vcycle"] = (rep.converged, rep.iterations, _rel(w, ref12.w))
         res["labels"] = [lab.tolist() for lab in labels]
         pv.close()
+        # pcg_vcycle_additive with levels 0-1 additive (bench cfg 5's solver), sharded vs one device
+        lv = _levels(R, None, [80, 12], labels)
+        lv[1].additive = True
+        spec = R.MethodSpec(kind=R.PCG_VCYCLE_ADDITIVE, levels=lv, solver=R.SolverConfig(1e-10, 2000))
+        pa, pf = R.PreparedMethod(m, 0.3, spec), R.PreparedMethod(mf, 0.3, spec)
+        wa, repa = pa.solve(b)
+        wf, repf = pf.solve(b)
+        res["additive"] = (repa.converged, repa.iterations, repf.iterations, _rel(wa, ref12.w))
+        pa.close()
+        pf.close()
         # the reference's multilevel FCG over the same (imported) labels, sharded vs one device
         spec = R.MethodSpec(kind=R.FCG_MULTILEVEL, levels=_levels(R, None, [80, 12], labels, tol=1e-10),
                             solver=R.SolverConfig(1e-10, 1000))
@@ -143,6 +153,8 @@ def test_two_ranks_one_gpu_host_staged():
             assert abs(its - its_full) <= max(2, its_full // 20), (method, its, its_full)
         cv, its, err = res["vcycle"]
         assert cv and err <= 1e-8, res["vcycle"]
+        cv, its, its_full, err = res["additive"]
+        assert cv and abs(its - its_full) <= 2 and err <= 1e-8, res["additive"]
         cv, its, its_full, d_full, err = res["fcg_ml"]
         assert cv and abs(its - its_full) <= 2 and d_full <= 1e-8 and err <= 1e-8, res["fcg_ml"]
         assert res["kmeans_refused"]
