@@ -2536,7 +2536,7 @@ int block_k1v2_mode() {
   return mode;
 }
 
-constexpr int kK1Threads = 512, kK1Depth = 7;
+constexpr int kK1Threads = 768, kK1Depth = 3;  // measured: 512 / 7 1149 us, 640 / 5 1132, 768 / 3 1120 per apply
 
 template <bool PAT, bool VEC>
 void spmm_k1v3(int sms, cudaStream_t s, const BlockK1v2& h, const double* vk, int k, int c0, int kc, int64_t s0,
