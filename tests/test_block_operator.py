@@ -65,3 +65,38 @@ def test_dense_block_matches_numpy(gpu, fp32, shape, k):
         assert rel_diff(out, want) <= 1e-12, rel_diff(out, want)
         col = m.ridge_apply(beta, v[:, k // 2].copy())
         assert rel_diff(out[:, k // 2], col) <= 1e-12
+
+
+def _triplet_matrix(n, f, nnz, seed, skew):
+    """A ragged matrix from numpy triplets: empty rows, rows with hot entries only, rows
+    with cold entries only (column popularity ~ rank^-skew), n not a multiple of 8."""
+    rng = np.random.default_rng(seed)
+    p = (np.arange(1, f + 1, dtype=np.float64)) ** -skew
+    p /= p.sum()
+    rows = rng.integers(0, n, nnz)
+    rows[rows % 7 == 3] = 0  # one very long row; every 7th row stays empty
+    cols = rng.choice(f, size=nnz, p=p)
+    key = np.unique(rows.astype(np.int64) * f + cols)
+    rr, cc = key // f, key % f
+    vv = rng.standard_normal(len(key))
+    return R.csr_from_triplets(n, f, rr.tolist(), cc.tolist(), vv.tolist()), (rr, cc, vv)
+
+
+@pytest.mark.parametrize("n,f,nnz,skew", [(3001, 25000, 40_000, 1.0), (20011, 26000, 600_000, 1.2),
+                                          (1029, 24600, 3_000, 0.5)])
+@pytest.mark.parametrize("k", [16, 7])
+def test_block_ragged_relabeled(gpu, n, f, nnz, skew, k):
+    """The record-streaming K1 (hot labels from shared memory + cold gathers) and the
+    hot X^T blocks on ragged inputs: empty rows, one row holding a seventh of the
+    nonzeros, a partial last slice / window / sample block; checked against numpy."""
+    x, (rr, cc, vv) = _triplet_matrix(n, f, nnz, n + k, skew)
+    m = R.DeviceMatrix(x, R.default_context())
+    v = np.random.default_rng(5).standard_normal((f, k))
+    out = m.ridge_apply_block(0.25, v)
+    t = np.zeros((n, k))
+    np.add.at(t, rr, vv[:, None] * v[cc])
+    want = np.zeros((f, k))
+    np.add.at(want, cc, vv[:, None] * t[rr])
+    want += 0.25 * v
+    assert rel_diff(out, want) <= 1e-12, rel_diff(out, want)
+    assert np.array_equal(out, m.ridge_apply_block(0.25, v))  # run-to-run bitwise
