@@ -1,1 +1,1 @@
-python -m pytest tests/test_block_operator.py -x -q 2>&1 | tail -8
+time python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -12
