@@ -1,1 +1,4 @@
-for c in 3 4 5; do echo XT_BLOCK_CTAS=$c; RMG_XT_BLOCK_CTAS=$c python tools/probe_block.py 2>&1 | tail -2; done
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
+python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; tail -c 200 gpurun_out/bench_reference.err
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 300 gpurun_out/bench_default.err
