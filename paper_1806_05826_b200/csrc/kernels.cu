@@ -98,6 +98,11 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint4 ld_stream_u32x4(const void* p) {  // 16-byte aligned
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 
 // ------------------------------------------------------------------ K1: t = X v
 // Row-parallel CSR gather; W lanes per row, two rows per lane group in flight
@@ -882,13 +887,30 @@ __global__ void __launch_bounds__(kHotThreads) k_xt_hot(HotXtDev h, const double
   const int64_t s0 = (int64_t)b * h.B;
   const int nb = (int)(h.N - s0 < (int64_t)h.B ? h.N - s0 : (int64_t)h.B);
   for (int j = threadIdx.x; j < nb; j += kHotThreads) ts[j] = __ldcg(t + s0 + j);
+  if (threadIdx.x == 0) ts[h.B] = 0.0;  // the padding entries' slot
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int32_t* __restrict__ p = h.ptr + (size_t)b * h.H;
   double* __restrict__ out = h.partial + (size_t)b * h.H;
-  for (int r = wid; r < h.hA; r += kHotThreads / 32) {  // long rows: warp per row, 4 loads in flight per lane
+  for (int r = wid; r < h.hA; r += kHotThreads / 32) {  // long rows: warp per row
     const int k0 = p[r], k1 = p[r + 1];
     double acc = 0.0;
+    if (PAT) {
+      // 8 indices per 16-byte load (segments are padded to 8 and 16-byte aligned, padding ->
+      // the zero slot), two loads in flight per lane: 4x the bytes in flight of 2-byte loads
+      for (int k = k0 + 8 * lane; k < k1; k += 512) {
+        const uint4 w0 = ld_stream_u32x4(h.idx16 + k);
+        const bool two = k + 256 < k1;
+        uint4 w1 = make_uint4(0u, 0u, 0u, 0u);
+        if (two) w1 = ld_stream_u32x4(h.idx16 + k + 256);
+        acc += ts[w0.x & 0xffffu]; acc += ts[w0.x >> 16]; acc += ts[w0.y & 0xffffu]; acc += ts[w0.y >> 16];
+        acc += ts[w0.z & 0xffffu]; acc += ts[w0.z >> 16]; acc += ts[w0.w & 0xffffu]; acc += ts[w0.w >> 16];
+        if (two) {
+          acc += ts[w1.x & 0xffffu]; acc += ts[w1.x >> 16]; acc += ts[w1.y & 0xffffu]; acc += ts[w1.y >> 16];
+          acc += ts[w1.z & 0xffffu]; acc += ts[w1.z >> 16]; acc += ts[w1.w & 0xffffu]; acc += ts[w1.w >> 16];
+        }
+      }
+    } else
     for (int k = k0 + lane; k < k1; k += 128) {
       int c[4];
 #pragma unroll
@@ -1915,12 +1937,12 @@ void launch_xt_epilogue(const double* sums, int64_t features, Epi epi, const XtA
 void launch_xt_hot(const HotXtDev& h, const double* t, const int32_t* done, const KrylovScalars* sc, double* sums,
                    cudaStream_t s) {
   if (h.H == 0) return;
-  const size_t smem = static_cast<size_t>(h.B) * sizeof(double);
+  const size_t smem = static_cast<size_t>(h.B + 1) * sizeof(double);  // + the padding entries' zero slot
   if (h.val == nullptr) {
-    allow_smem(k_xt_hot<true>, kHotBlockMax * 8);
+    allow_smem(k_xt_hot<true>, kHotBlockMax * 8 + 8);
     k_xt_hot<true><<<h.nblk, kHotThreads, smem, s>>>(h, t, done, sc);
   } else {
-    allow_smem(k_xt_hot<false>, kHotBlockMax * 8);
+    allow_smem(k_xt_hot<false>, kHotBlockMax * 8 + 8);
     k_xt_hot<false><<<h.nblk, kHotThreads, smem, s>>>(h, t, done, sc);
   }
   k_xt_hot_chunks<<<dim3((h.H + kThreads - 1) / kThreads, h.S), kThreads, 0, s>>>(h, done, sc);

@@ -504,11 +504,25 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
   par([&](int64_t h) {
     for (int64_t k = ht.ptr[feat[h]]; k < ht.ptr[feat[h] + 1]; ++k) ++rp[(ht.idx[k] / B) * H + h + 1];
   });
+  // Long rows are read 8 entries (16 bytes) per lane: every (block, long row) segment is
+  // padded to a multiple of 8 entries and every block to a multiple of 8 (so the segments
+  // start 16-byte aligned); padding entries point at the zero slot ts[B] (value 0).
+  std::vector<int32_t> real_cnt(static_cast<size_t>(nblk * H));
+  for (int64_t b = 0; b < nblk; ++b) {
+    int64_t tot = 0;
+    for (int64_t h = 0; h < H; ++h) {
+      int64_t& c = rp[b * H + h + 1];
+      real_cnt[b * H + h] = static_cast<int32_t>(c);
+      if (h < hA) c = (c + 7) / 8 * 8;
+      tot += c;
+    }
+    rp[b * H + H] += (8 - tot % 8) % 8;  // the block's last row takes the block's padding
+  }
   for (size_t q = 0; q + 1 < rp.size(); ++q) rp[q + 1] += rp[q];
   const int64_t hnnz = rp.back();
-  if (hnnz > INT32_MAX) return;
-  std::vector<uint16_t> i16(hnnz);
-  std::vector<double> v(pattern ? 0 : hnnz);
+  if (hnnz > INT32_MAX || B >= 65535) return;
+  std::vector<uint16_t> i16(hnnz, static_cast<uint16_t>(B));
+  std::vector<double> v(pattern ? 0 : hnnz, 0.0);
   par([&](int64_t h) {
     int64_t cur_b = -1, pos = 0;
     for (int64_t k = ht.ptr[feat[h]]; k < ht.ptr[feat[h] + 1]; ++k) {  // samples ascending
@@ -533,7 +547,7 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
       std::vector<uint16_t> bi[16];
       std::vector<double> bv[16];
       for (int64_t b = 0; b < nblk; ++b) {
-        const int64_t q0 = rp[b * H + h], q1 = rp[b * H + h + 1];
+        const int64_t q0 = rp[b * H + h], q1 = q0 + real_cnt[b * H + h];  // the real entries; padding follows
         for (int k = 0; k < 16; ++k) {
           bi[k].clear();
           bv[k].clear();
@@ -555,6 +569,26 @@ void Matrix::build_hot(const HostCsr& ht, int64_t n_samples) {
       }
     });
   }
+  // lane l of the long-row warp reads entries 8 l .. 8 l + 7 of each 256-entry group: store the
+  // group transposed, so that the lanes' u-th entries are consecutive entries of the order above
+  par([&](int64_t h) {
+    if (h >= hA) return;
+    std::vector<uint16_t> ti;
+    std::vector<double> tv;
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int64_t q0 = rp[b * H + h], q1 = rp[b * H + h + 1];
+      for (int64_t g0 = q0; g0 < q1; g0 += 256) {
+        const int64_t g = std::min<int64_t>(256, q1 - g0), lanes = g / 8;
+        ti.assign(i16.begin() + g0, i16.begin() + g0 + g);
+        if (!pattern) tv.assign(v.begin() + g0, v.begin() + g0 + g);
+        for (int64_t l = 0; l < lanes; ++l)
+          for (int64_t u = 0; u < 8; ++u) {
+            i16[g0 + 8 * l + u] = ti[u * lanes + l];
+            if (!pattern) v[g0 + 8 * l + u] = tv[u * lanes + l];
+          }
+      }
+    }
+  });
   std::vector<int32_t> rp32(rp.begin(), rp.end());
   cudaStream_t s = ctx->stream;
   hx->ptr.upload(rp32.data(), rp32.size(), s);
