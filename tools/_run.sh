@@ -1,1 +1,1 @@
-RMG_SETUP_TIMING=1 python bench.py --config cfg5 --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/bench_cfg5_final.json 2> gpurun_out/bench_cfg5_final.err; tail -c 600 gpurun_out/bench_cfg5_final.err
+python -m pytest tests/test_gpu_parity.py tests/test_cfg3_parity.py tests/test_hybrid_xt.py tests/test_full_scale.py -x -q 2>&1 | tail -4
