@@ -473,7 +473,7 @@ Clustering kmeans_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t
     chosen.push_back(static_cast<int64_t>(rng.next_index(f)));
     std::vector<char> used(f, 0);
     used[chosen[0]] = 1;
-    std::vector<double> d2(f, std::numeric_limits<double>::infinity());
+    std::vector<double> d2(f, std::numeric_limits<double>::infinity()), cum(f, 0.0);
     double* dh = nullptr;  // pinned: one D2H of F distances per seeding step
     RMG_CK(cudaMallocHost(&dh, static_cast<size_t>(f) * sizeof(double)));
     struct PinnedFree {
@@ -487,26 +487,27 @@ Clustering kmeans_dense_gpu(cudaStream_t s, const double* xc, int64_t n, int64_t
       col_chain<1>(s, xc, false, ld, n, f, colv.get(), dist.get(), true);
       RMG_CK(cudaMemcpyAsync(dh, dist.get(), f * sizeof(double), cudaMemcpyDeviceToHost, s));
       RMG_CK(cudaStreamSynchronize(s));
+      // one pass: the running total after every column (the reference's second scan re-adds
+      // the same terms in the same order -- skipped zeros add nothing -- so its `run` at j is
+      // cum[j] bit for bit), then the draw is the first j with u < cum[j]
       double total = 0.0;
       for (int64_t j = 0; j < f; ++j) {
         if (used[j]) {
           d2[j] = 0.0;
-          continue;
+        } else {
+          d2[j] = std::min(d2[j], dh[j] * dh[j]);
+          total += d2[j];
         }
-        d2[j] = std::min(d2[j], dh[j] * dh[j]);
-        total += d2[j];
+        cum[j] = total;
       }
       int64_t pick = -1;
       if (total > 0.0) {
         const double u = rng.next_double() * total;
-        double run = 0.0;
-        for (int64_t j = 0; j < f && pick < 0; ++j) {
-          if (used[j] || d2[j] == 0.0) continue;
-          run += d2[j];
-          if (u < run) pick = j;
-        }
-        for (int64_t j = f - 1; pick < 0 && j >= 0; --j)
-          if (!used[j] && d2[j] > 0.0) pick = j;
+        // cum is non-decreasing; the first j with u < cum[j] has d2[j] > 0 (cum rose there)
+        const int64_t j = std::upper_bound(cum.begin(), cum.end(), u) - cum.begin();
+        if (j < f) pick = j;
+        for (int64_t q = f - 1; pick < 0 && q >= 0; --q)
+          if (!used[q] && d2[q] > 0.0) pick = q;
       }
       if (pick < 0) {
         uint64_t idx = rng.next_index(static_cast<uint64_t>(f) - chosen.size());

@@ -1,1 +1,1 @@
-python -m pytest tests/test_gpu_parity.py tests/test_cfg3_parity.py tests/test_hybrid_xt.py tests/test_full_scale.py -x -q 2>&1 | tail -4
+python -m pytest tests/test_sketch.py tests/test_dense_setup.py tests/test_kmeans_gpu.py tests/test_sharded_dense_gpu.py -x -q 2>&1 | tail -4
