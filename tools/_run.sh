@@ -1,1 +1,4 @@
-RMG_SETUP_LOG=1 python bench.py --config cfg5 --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/bench_cfg5_final2.json 2> gpurun_out/bench_cfg5_final2.err; grep "rmg setup" gpurun_out/bench_cfg5_final2.err
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; tail -c 200 gpurun_out/bench_reference.err
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 300 gpurun_out/bench_default.err
