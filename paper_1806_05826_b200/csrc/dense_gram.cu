@@ -44,17 +44,47 @@ __global__ void k_gram_rows(const int32_t* __restrict__ xptr, const int32_t* __r
         rb = xptr[r];
         re = xptr[r + 1];
       }
-      for (int t = 0; t < m; ++t) {
-        const double v = __shfl_sync(kFull, vp, t);
-        const int32_t s0 = __shfl_sync(kFull, rb, t), s1 = __shfl_sync(kFull, re, t);
-        for (int32_t q = s0 + lane; q < s1; q += 32) {
-          const int32_t j = xidx[q];
-          if (j >= c0 && j < c1) {
-            const double xv = xval != nullptr ? xval[q] : 1.0;
-            acc[j - c0] = __dadd_rn(acc[j - c0], __dmul_rn(v, xv));
+      // rows in groups of 8: the first 64 entries of every row of the group are loaded before
+      // any is used (one memory latency per group instead of two per row -- the rows of a
+      // 16 M-row level are TLB-cold), then added row by row in the same order as before
+      constexpr int kRG = 8;
+      for (int t0 = 0; t0 < m; t0 += kRG) {
+        int32_t jj[kRG][2];
+        double xx[kRG][2];
+#pragma unroll
+        for (int g = 0; g < kRG; ++g) {
+          const int t = min(t0 + g, m - 1);
+          const bool live = t0 + g < m;
+          const int32_t s0 = __shfl_sync(kFull, rb, t), s1 = __shfl_sync(kFull, re, t);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int32_t q = s0 + 32 * u + lane;
+            const bool ok = live && q < s1;
+            jj[g][u] = ok ? xidx[q] : -1;
+            xx[g][u] = ok ? (xval != nullptr ? xval[q] : 1.0) : 0.0;
           }
         }
-        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < kRG; ++g) {
+          if (t0 + g < m) {  // warp-uniform
+            const int t = t0 + g;
+            const double v = __shfl_sync(kFull, vp, t);
+            const int32_t s0 = __shfl_sync(kFull, rb, t), s1 = __shfl_sync(kFull, re, t);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int32_t j = jj[g][u];
+              if (j >= c0 && j < c1) acc[j - c0] = __dadd_rn(acc[j - c0], __dmul_rn(v, xx[g][u]));
+            }
+            for (int32_t q = s0 + 64 + lane; q < s1; q += 32) {  // rows longer than 64 entries
+              const int32_t j = xidx[q];
+              if (j >= c0 && j < c1) {
+                const double xv = xval != nullptr ? xval[q] : 1.0;
+                acc[j - c0] = __dadd_rn(acc[j - c0], __dmul_rn(v, xv));
+              }
+            }
+            __syncwarp();
+          }
+        }
       }
     }
     double* out = G + i * ldg + c0;
