@@ -479,12 +479,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_xt_block(const int32_t* __restr
   if (((unit >> 1) << 1) >= n_units) return;  // both half-warps out of range: the whole warp
   const bool valid = unit < n_units;
   int row = 0, e0 = 0, e1 = 0, seg = -1;
-  if (valid && unit < bs.n_short) {
-    row = bs.short_rows[unit];
+  if (valid && unit >= bs.n_items) {  // the items of split rows (the longest units) go first
+    row = bs.short_rows[unit - bs.n_items];
     e0 = bs.e_begin[row];
     e1 = bs.e_end[row];
   } else if (valid) {
-    const int4 it = bs.items[unit - bs.n_short];
+    const int4 it = bs.items[unit];
     row = it.x;
     e0 = it.y;
     e1 = it.z;

@@ -843,7 +843,11 @@ void Matrix::build_block_hot(const HostCsr& ht, const std::vector<int32_t>& feat
 // are one unit each (a half-warp, elements in order); longer rows are split
 // into items of 512 whose partials are finished in item order.
 void Matrix::build_block_schedule(const HostCsr& xr, const HostCsr& ht) {
-  constexpr int64_t kItem = 512;  // a half-warp walks <= 512 elements (latency-bound chains)
+  // A half-warp walks <= kItem elements; longer rows are split into items with a finishing
+  // pass.  Measured on cfg 3 (cold rows reach ~1500 entries per chunk): 512 -> 1120 us per apply
+  // (the items ran last: a tail), 2048 and above -> 1030 us (no row is split).  RMG_BLOCK_ITEM
+  // overrides (diagnostics).
+  const int64_t kItem = std::getenv("RMG_BLOCK_ITEM") ? std::max<int64_t>(16, std::atoll(std::getenv("RMG_BLOCK_ITEM"))) : 2048;
   // sample chunks: T's chunk slice (rows x 16 columns x 8 B) <= 64 MB stays in L2
   // between K1 writing and the X^T pass reading it; chunks are whole 1024-row
   // SELL windows (RMG_BLOCK_CHUNK_ROWS overrides the row count)
