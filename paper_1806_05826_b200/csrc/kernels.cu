@@ -2121,6 +2121,72 @@ __global__ void __launch_bounds__(1024) k_bdot_final(const double* __restrict__ 
   }
 }
 
+// x += alpha p, r -= alpha Ap and the partials of <r, r> in one pass: the rows are dealt to
+// blocks and threads exactly as k_bdot_partial deals them, so the partials (and the sums
+// k_bdot_final forms from them) are those of the separate update + dot, bit for bit.
+__global__ void __launch_bounds__(kThreads) k_bupdate_xr_dot(double* __restrict__ x, double* __restrict__ r,
+                                                             const double* __restrict__ p,
+                                                             const double* __restrict__ ap, const BlockScalars* sc,
+                                                             int64_t n, int k, double* __restrict__ partial) {
+  __shared__ double red[kThreads];
+  const int rl_n = kThreads / k, t = threadIdx.x, rl = t / k, c = t % k;
+  const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = (n < r0 + rows_per ? n : r0 + rows_per);
+  double acc = 0.0;
+  if (rl < rl_n) {
+    const bool frozen = sc[c].done != 0;
+    const double a = sc[c].alpha;
+    for (int64_t i = r0 + rl; i < r1; i += rl_n) {
+      const int64_t q = i * k + c;
+      double rv = r[q];
+      if (!frozen) {
+        x[q] += a * p[q];
+        rv = rv - a * ap[q];
+        r[q] = rv;
+      }
+      acc += rv * rv;
+    }
+  }
+  red[t] = acc;
+  __syncthreads();
+  if (t < k) {
+    double s = 0.0;
+    for (int q = 0; q < rl_n; ++q) s += red[q * k + t];
+    partial[(size_t)blockIdx.x * k + t] = s;
+  }
+}
+
+// z = D^-1 r + P e_c (the additive finest level) and the partials of <r, z> in one pass
+// (same dealing of rows as k_bdot_partial)
+__global__ void __launch_bounds__(kThreads) k_bvc_jacobi_prolong_dot(const double* __restrict__ r,
+                                                                     const double* __restrict__ dinv,
+                                                                     const int32_t* __restrict__ label,
+                                                                     const double* __restrict__ weight,
+                                                                     const double* __restrict__ ec,
+                                                                     double* __restrict__ z, int64_t n, int k,
+                                                                     double* __restrict__ partial) {
+  __shared__ double red[kThreads];
+  const int rl_n = kThreads / k, t = threadIdx.x, rl = t / k, c = t % k;
+  const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = (n < r0 + rows_per ? n : r0 + rows_per);
+  double acc = 0.0;
+  if (rl < rl_n)
+    for (int64_t i = r0 + rl; i < r1; i += rl_n) {
+      const int64_t q = i * k + c;
+      const double rv = r[q];
+      const double zv = dinv[i] * rv + weight[i] * ec[(int64_t)label[i] * k + c];
+      z[q] = zv;
+      acc += rv * zv;
+    }
+  red[t] = acc;
+  __syncthreads();
+  if (t < k) {
+    double s = 0.0;
+    for (int q = 0; q < rl_n; ++q) s += red[q * k + t];
+    partial[(size_t)blockIdx.x * k + t] = s;
+  }
+}
+
 // begin: nb = ||rhs||, non-finite check, rz = <r, z>
 __global__ void k_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, const double* nonfinite, int k,
                              double* hist) {
@@ -2332,6 +2398,20 @@ void launch_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, con
 }
 void launch_bpcg_alpha(BlockScalars* sc, const double* pap, int k, cudaStream_t s) {
   k_bpcg_alpha<<<1, 64, 0, s>>>(sc, pap, k);
+}
+void launch_bdot_final(const double* partial, int g, int k, double* out, cudaStream_t s) {
+  k_bdot_final<<<1, 1024, 0, s>>>(partial, g, k, out);
+}
+void launch_bupdate_xr_dot(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
+                           int k, double* partial, int g, double* rr, cudaStream_t s) {
+  k_bupdate_xr_dot<<<g, kThreads, 0, s>>>(x, r, p, ap, sc, n, k, partial);
+  k_bdot_final<<<1, 1024, 0, s>>>(partial, g, k, rr);
+}
+void launch_bvc_jacobi_prolong_dot(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                                   const double* ec, double* z, int64_t n, int k, double* partial, int g, double* rz,
+                                   cudaStream_t s) {
+  k_bvc_jacobi_prolong_dot<<<g, kThreads, 0, s>>>(r, dinv, label, weight, ec, z, n, k, partial);
+  k_bdot_final<<<1, 1024, 0, s>>>(partial, g, k, rz);
 }
 void launch_bupdate_xr(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
                        int k, cudaStream_t s) {

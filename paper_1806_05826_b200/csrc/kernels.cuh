@@ -286,6 +286,13 @@ void launch_bpcg_begin(BlockScalars* sc, const double* rr, const double* rz, con
 void launch_bpcg_alpha(BlockScalars* sc, const double* pap, int k, cudaStream_t s);
 void launch_bupdate_xr(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
                        int k, cudaStream_t s);
+// the same update with the <r, r> partials formed in the same pass (+ their fixed-order sum into rr)
+void launch_bupdate_xr_dot(double* x, double* r, const double* p, const double* ap, const BlockScalars* sc, int64_t n,
+                           int k, double* partial, int g, double* rr, cudaStream_t s);
+// z = D^-1 r + P e_c with the <r, z> partials formed in the same pass (+ their sum into rz)
+void launch_bvc_jacobi_prolong_dot(const double* r, const double* dinv, const int32_t* label, const double* weight,
+                                   const double* ec, double* z, int64_t n, int k, double* partial, int g, double* rz,
+                                   cudaStream_t s);
 void launch_bpcg_conv(BlockScalars* sc, const double* rr, int k, double* hist, cudaStream_t s);
 void launch_bpcg_beta(BlockScalars* sc, const double* rz, int k, cudaStream_t s);
 void launch_bupdate_p(double* p, const double* z, const BlockScalars* sc, int64_t n, int k, cudaStream_t s);

@@ -2905,7 +2905,13 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
       launch_bgemm_inv(ainv_.get(), b.rc.get(), b.ec.get(), nc, k, s);
     else
       bvcycle(lv + 1, b.rc.get(), b.ec.get(), k);
-    launch_bvc_jacobi_prolong(r, v.dinv.get(), c.label.get(), c.weight.get(), b.ec.get(), z, nf, k, s);
+    if (lv == 0 && brz_partial_ != nullptr) {  // the PCG loop's <r, z> rides on this pass
+      launch_bvc_jacobi_prolong_dot(r, v.dinv.get(), c.label.get(), c.weight.get(), b.ec.get(), z, nf, k, brz_partial_,
+                                    brz_g_, brz_out_, s);
+      brz_done_ = true;
+    } else {
+      launch_bvc_jacobi_prolong(r, v.dinv.get(), c.label.get(), c.weight.get(), b.ec.get(), z, nf, k, s);
+    }
     ctx_->launches += 3;
     return;
   }
@@ -2977,11 +2983,16 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
     m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);
     launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, cs);
     launch_bpcg_alpha(w.sc.get(), pap, k, cs);
-    launch_bupdate_xr(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, cs);
-    launch_bdots(w.r.get(), w.r.get(), n, k, w.partial.get(), g, rr, cs);
+    // x, r and <r, r> in one pass (the partials are launch_bdots')
+    launch_bupdate_xr_dot(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, w.partial.get(), g, rr, cs);
     launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), cs);
+    brz_partial_ = w.partial.get();  // an additive finest level forms <r, z> while it writes z
+    brz_g_ = g;
+    brz_out_ = rz;
+    brz_done_ = false;
     bprecond(w.r.get(), w.z.get(), k);
-    launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
+    brz_partial_ = nullptr;
+    if (!brz_done_) launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
     launch_bpcg_beta(w.sc.get(), rz, k, cs);
     launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, cs);
     ctx_->launches += 12;

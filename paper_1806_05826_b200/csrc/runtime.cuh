@@ -443,6 +443,11 @@ class Method {
   void bvcycle(size_t lv, const double* r, double* z, int k);
   // z = M r for k columns: the V-cycle, Jacobi (z = D^-1 r) or identity (cg)
   void bprecond(const double* r, double* z, int k);
+  // solve_block -> bvcycle: where an additive finest level leaves the partials of <r, z>
+  double* brz_partial_ = nullptr;
+  double* brz_out_ = nullptr;
+  int brz_g_ = 0;
+  bool brz_done_ = false;
   // pcg_vcycle: dense G_k = X_k^T X_k per level k >= 1 where n_k^2 doubles are
   // fewer bytes than an X_k sweep pair; nullptr: sweep X_k
   struct DenseGram {
