@@ -170,38 +170,75 @@ def algorithmic_bytes(n, f, nnz, pattern):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons of the timed region: one sample after every timed step
+    (the step's device work has just finished -- clock and throttle state outlive it by far
+    more than the microseconds in between), taken with in-process NVML (nvidia_ml_py), or a
+    one-shot nvidia-smi query when NVML is not importable.
+
+    Why not a free-running `nvidia-smi -lms 50` (round 1): a query that lands INSIDE a step
+    stalls the GPU for ~15 ms on this platform -- the same 5 steps of cfg 3 timed 29.6 ms each
+    with no query inside them and 30.5-34.6 ms with 1-4 (`-lms 50 / 200`, or NVML from a
+    thread every 50 / 150 ms); between steps it costs nothing that is timed.  Measured on the
+    final code (gpurun_out/exp1.log, 5 runs each): NVML between steps 29.7-29.9 ms on every
+    step of every run, a one-shot nvidia-smi between steps (BENCH_NO_NVML=1) the same, and no
+    query at all during the region (BENCH_NO_STEP_SAMPLES=1) a 43-63 ms fifth step in 2 runs
+    of 5 -- so the knobs stay as diagnostics and the default is the between-steps NVML read."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.proc, self.lines = device, None, []
+        self.device, self.lines, self.handle, self.nv = device, [], None, None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
-                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            if os.environ.get("BENCH_NO_NVML"):
+                raise RuntimeError("disabled")
+            import pynvml as nv
+            nv.nvmlInit()
+            # NVML orders devices by PCI bus id; honour CUDA_VISIBLE_DEVICES when it is a plain index list
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = self.device
+            if vis and all(p.strip().isdigit() for p in vis.split(",")):
+                idx = int(vis.split(",")[self.device])
+            self.handle = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = nv
         except Exception:
-            self.proc = None
-        time.sleep(0.15)
+            self.nv = None
         return self
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+    def sample(self):
+        """Call right after a timed step has completed (never inside one)."""
+        if os.environ.get("BENCH_NO_STEP_SAMPLES") and not self._final:
+            return
+        try:
+            if self.nv is not None:
+                nv, h = self.nv, self.handle
+
+                def bit(new, old):
+                    return getattr(nv, new, None) or getattr(nv, old)
+
+                bits = [bit("nvmlClocksEventReasonHwSlowdown", "nvmlClocksThrottleReasonHwSlowdown"),
+                        bit("nvmlClocksEventReasonHwThermalSlowdown", "nvmlClocksThrottleReasonHwThermalSlowdown"),
+                        bit("nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksThrottleReasonSwThermalSlowdown"),
+                        bit("nvmlClocksEventReasonSwPowerCap", "nvmlClocksThrottleReasonSwPowerCap")]
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.lines.append(", ".join([str(sm), str(mx)] + ["Active" if mask & b else "Not Active" for b in bits]))
+            else:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
+                                      str(self.device)], capture_output=True, text=True, timeout=10).stdout
+                self.lines += [ln.strip() for ln in out.splitlines() if ln.strip()]
+        except Exception:
+            pass
+
+    _final = False
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.1)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        if not self.lines:
+            self._final = True
+            self.sample()
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -613,6 +650,8 @@ def run_b200(args, cfg):
             ev[s][0].record(stream)
             timed.append(pm.solve_device(bs[args.warmup + s].data_ptr(), w.data_ptr()))
             ev[s][1].record(stream)
+            torch.cuda.synchronize()
+            clocks.sample()  # between steps: never inside one
         torch.cuda.synchronize()
     if pg:
         pg.barrier()
@@ -885,7 +924,7 @@ def run_b200(args, cfg):
         pg.destroy_process_group()
 
 
-def timed_batches(pm, stream, bcm, wcm, nb, betas, schedule, cur):
+def timed_batches(pm, stream, bcm, wcm, nb, betas, schedule, cur, clocks=None):
     """Batched solves (one rmg_method_solve_batch per step), beta changed between steps
     outside the events; returns per-step device ms and the reports."""
     import torch
@@ -902,6 +941,8 @@ def timed_batches(pm, stream, bcm, wcm, nb, betas, schedule, cur):
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
         reps.append(rs)
+        if clocks is not None:
+            clocks.sample()  # between steps: never inside one
     return ms, reps
 
 
@@ -970,7 +1011,7 @@ def run_sweep(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         ms, reps = timed_batches(pm, stream, bcm, wcm, nb, betas,
-                                 [sched(args.warmup + i) for i in range(args.steps)], cur)
+                                 [sched(args.warmup + i) for i in range(args.steps)], cur, clocks)
     total = sum(ms)
     if pg:
         pg.barrier()
@@ -1097,7 +1138,8 @@ def run_sweep(args, cfg):
     lock = f"{nb} columns in lock step over the block operator" if nb > 1 else "one right-hand side"
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": total / args.steps, "step_ms": [round(t, 3) for t in ms],
+        "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded CounterRng generator with BASELINE cfg shapes (DESIGN.md §6)",
         "config": sweep_config(cfg, m.nnz, sha),
@@ -1187,7 +1229,10 @@ def run_sharded(args, cfg):
         pg.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        res = [step(args.warmup + i) for i in range(args.steps)]
+        res = []
+        for i in range(args.steps):
+            res.append(step(args.warmup + i))
+            clocks.sample()  # between steps: never inside one
     total = sum(r[0] for r in res)
     if pg:
         t = torch.tensor([total], dtype=torch.float64, device=dev)
@@ -1284,7 +1329,10 @@ def run_sharded_dense(args, cfg):
         pg.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        res = [step() for _ in range(args.steps)]
+        res = []
+        for _ in range(args.steps):
+            res.append(step())
+            clocks.sample()  # between steps: never inside one
     total = sum(r[0] for r in res)
     if pg:
         t = torch.tensor([total], dtype=torch.float64, device=dev)
