@@ -45,16 +45,46 @@ void validate_csr(const HostCsr& m) {
   if (m.ptr[0] != 0 || m.ptr[m.n] != m.nnz()) throw InvalidArgument("FeatureMatrix: row_offsets do not span the nonzeros");
   if (!m.val.empty() && static_cast<int64_t>(m.val.size()) != m.nnz())
     throw InvalidArgument("FeatureMatrix: values length != nnz");
-  for (int64_t r = 0; r < m.n; ++r) {
-    if (m.ptr[r + 1] < m.ptr[r]) throw InvalidArgument("FeatureMatrix: row_offsets decrease at row " + std::to_string(r));
-    for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) {
-      const int64_t c = m.idx[k];
-      if (c < 0 || c >= m.f) throw InvalidArgument("FeatureMatrix: column index out of range in row " + std::to_string(r));
-      if (k > m.ptr[r] && c <= m.idx[k - 1])
-        throw InvalidArgument("FeatureMatrix: column indices not strictly increasing in row " + std::to_string(r));
-      if (!m.val.empty() && !std::isfinite(m.val[k])) throw InvalidArgument("FeatureMatrix: non-finite value");
+  // Row blocks on threads (cfg 5 validates four 1e9-entry levels); the error reported is the
+  // sequential scan's: every block stops at its first, the lowest block's wins.
+  const int64_t T = m.nnz() < (int64_t{1} << 22)
+                        ? 1
+                        : std::max<int64_t>(1, std::min<int64_t>(32, std::thread::hardware_concurrency()));
+  std::vector<std::string> err(static_cast<size_t>(T));
+  auto body = [&](int64_t t) {
+    const int64_t ra = m.n * t / T, rb = m.n * (t + 1) / T;
+    for (int64_t r = ra; r < rb; ++r) {
+      if (m.ptr[r + 1] < m.ptr[r]) {
+        err[t] = "FeatureMatrix: row_offsets decrease at row " + std::to_string(r);
+        return;
+      }
+      if (m.ptr[r] < 0 || m.ptr[r + 1] > m.nnz()) {  // offsets that leave [0, nnz] must not index idx
+        err[t] = "FeatureMatrix: row_offsets do not span the nonzeros";
+        return;
+      }
+      for (int64_t k = m.ptr[r]; k < m.ptr[r + 1]; ++k) {
+        const int64_t c = m.idx[k];
+        if (c < 0 || c >= m.f) {
+          err[t] = "FeatureMatrix: column index out of range in row " + std::to_string(r);
+          return;
+        }
+        if (k > m.ptr[r] && c <= m.idx[k - 1]) {
+          err[t] = "FeatureMatrix: column indices not strictly increasing in row " + std::to_string(r);
+          return;
+        }
+        if (!m.val.empty() && !std::isfinite(m.val[k])) {
+          err[t] = "FeatureMatrix: non-finite value";
+          return;
+        }
+      }
     }
-  }
+  };
+  std::vector<std::thread> pool;
+  for (int64_t t = 1; t < T; ++t) pool.emplace_back(body, t);
+  body(0);
+  for (auto& th : pool) th.join();
+  for (const std::string& e : err)
+    if (!e.empty()) throw InvalidArgument(e);
 }
 
 // X^T as CSR with the samples of every feature in increasing order.  Threaded over

@@ -135,10 +135,23 @@ int lanes_for(double avg) {
 
 std::vector<int32_t> narrow(const std::vector<int64_t>& v, const char* what) {
   std::vector<int32_t> o(v.size());
-  for (size_t i = 0; i < v.size(); ++i) {
-    if (v[i] < 0 || v[i] > INT32_MAX) throw InvalidArgument(std::string(what) + " exceeds the int32 device index range");
-    o[i] = static_cast<int32_t>(v[i]);
-  }
+  const size_t T = v.size() < (size_t{1} << 22) ? 1 : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<char> bad(T, 0);
+  auto body = [&](size_t t) {
+    for (size_t i = v.size() * t / T; i < v.size() * (t + 1) / T; ++i) {
+      if (v[i] < 0 || v[i] > INT32_MAX) {
+        bad[t] = 1;
+        return;
+      }
+      o[i] = static_cast<int32_t>(v[i]);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < T; ++t) pool.emplace_back(body, t);
+  body(0);
+  for (auto& th : pool) th.join();
+  for (char b : bad)
+    if (b) throw InvalidArgument(std::string(what) + " exceeds the int32 device index range");
   return o;
 }
 
@@ -1057,6 +1070,7 @@ void Matrix::ensure_block_gram() {
 void Matrix::ensure_block_schedule() {
   if (block_built || dense) return;
   if (comm != nullptr) throw InvalidArgument("block operator: single-GPU matrices only");
+  ensure_operator();  // the block layouts follow the K1 layout's column relabeling
   const HostCsr ht = transpose(host);
   build_block_schedule(host, ht);
   block_built = true;
@@ -1244,13 +1258,18 @@ const HostCsr& Matrix::host_csr() {
   return host;
 }
 
-Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din)
+Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const DenseInput* din, bool defer_operator)
     : ctx(c), host(std::move(h)), comm(cm) {
+  defer_op = defer_operator && cm == nullptr && din == nullptr;  // the deferred build reads `host` = the local rows
+  const auto tv = std::chrono::steady_clock::now();
   validate_csr(host);
   pattern = host.val.empty();
   if (!pattern && detect_pattern)
     pattern = std::all_of(host.val.begin(), host.val.end(), [](double v) { return v == 1.0; });
   if (host.val.empty()) host.val.assign(host.nnz(), 1.0);
+  if (std::getenv("RMG_SETUP_LOG") != nullptr && host.nnz() > (1 << 24))
+    std::fprintf(stderr, "[rmg setup]   upload %-10s %8.3f s\n", "validate",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tv).count());
   RMG_CK(cudaSetDevice(ctx->device));
   row0 = 0;
   row1 = host.n;
@@ -1277,8 +1296,10 @@ Matrix::Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* cm, const Dense
   init_sparse(local);
 }
 
-Matrix::Matrix(Context* c, HostCsr local, int64_t n_glob, int64_t r0, bool detect_pattern, Comm* cm)
+Matrix::Matrix(Context* c, HostCsr local, int64_t n_glob, int64_t r0, bool detect_pattern, Comm* cm,
+               bool defer_operator)
     : ctx(c), host(std::move(local)), comm(cm) {
+  defer_op = defer_operator;
   validate_csr(host);
   if (comm == nullptr) throw InvalidArgument("rmg_matrix_create_csr_rows: needs a communicator");
   if (r0 < 0 || n_glob < 0 || r0 + host.n > n_glob)
@@ -1312,6 +1333,39 @@ void Matrix::init_sparse(const HostCsr& local) {
   if (comm != nullptr) alloc_comm_buffers();
   // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
   // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
+  const bool slog = std::getenv("RMG_SETUP_LOG") != nullptr && local.nnz() > (1 << 24);
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {  // RMG_SETUP_LOG: where a large level's upload goes
+    if (!slog) return;
+    RMG_CK(cudaStreamSynchronize(ctx->stream));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rmg setup]   upload %-10s %8.3f s\n", what, std::chrono::duration<double>(now - tp).count());
+    tp = now;
+  };
+  if (!defer_op) {
+    upload_k1(local);
+    lap("K1 layout");
+  }
+  const HostCsr ht = transpose(local);
+  lap("transpose");
+  xt.upload(ht, pattern, ctx->stream, false);
+  lap("X^T copy");
+  sched.build(ht, ctx->stream, local.f);
+  lap("X^T sched");
+  if (!defer_op) {
+    build_hot(ht, local.n);
+    lap("hot blocks");
+  }
+  op_ready = !defer_op;
+  // the block operator's layouts (K1 records, hot X^T blocks, chunk schedules) are built
+  // on the first block call (ensure_block_schedule): most matrices never see one
+  t.alloc(std::max<int64_t>(1, local.n));
+  gram_sc.alloc(1);
+}
+
+void Matrix::upload_k1(const HostCsr& local) {
+  // Column relabeling pays once v (F doubles) outgrows L1 (measured on the
+  // cfg 5 shard, profiles/r1_operator.md); RMG_RELABEL=0/1 overrides.
   const char* rl = std::getenv("RMG_RELABEL");
   const bool relabel = rl != nullptr ? std::string(rl) == "1" : local.f * 8 > 192 * 1024;
   const char* k1 = std::getenv("RMG_K1");  // "csr": the row-CSR K1 (diagnostics)
@@ -1319,14 +1373,18 @@ void Matrix::init_sparse(const HostCsr& local) {
     x.upload(local, pattern, ctx->stream, local.f <= 65536, relabel);
   else
     x.upload_sell(local, pattern, ctx->stream, local.f <= 65536, relabel);
-  const HostCsr ht = transpose(local);
-  xt.upload(ht, pattern, ctx->stream, false);
-  sched.build(ht, ctx->stream, local.f);
-  build_hot(ht, local.n);
-  // the block operator's layouts (K1 records, hot X^T blocks, chunk schedules) are built
-  // on the first block call (ensure_block_schedule): most matrices never see one
-  t.alloc(std::max<int64_t>(1, local.n));
-  gram_sc.alloc(1);
+}
+
+// the layouts a deferred level skipped at construction (K1, hot X^T blocks), on its first application
+void Matrix::ensure_operator() {
+  if (op_ready) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RMG_CK(cudaStreamIsCapturing(ctx->stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone)
+    throw RuntimeError("Matrix::ensure_operator: a deferred level was first applied inside a graph capture");
+  upload_k1(host);
+  build_hot(transpose(host), host.n);
+  op_ready = true;
 }
 
 namespace {
@@ -1414,6 +1472,7 @@ void Matrix::apply(const double* v, Epi epi, const XtArgs& args, OpProfile* prof
     }
     return;
   }
+  ensure_operator();
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows(x.view, v, t.get(), args.done, ctx->stream);
   if (prof) prof->mark(ctx->stream);
@@ -1433,6 +1492,7 @@ void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* s
     }
     return;
   }
+  ensure_operator();
   if (prof) prof->mark(ctx->stream);
   launch_spmv_rows_ring(x.view, v_ring, stride, sc, t.get(), ctx->stream);
   if (prof) prof->mark(ctx->stream);
@@ -1442,6 +1502,7 @@ void Matrix::apply_ring(const double* v_ring, int stride, const KrylovScalars* s
 }
 
 void Matrix::spmv(const double* v, double* y) {
+  if (!dense) ensure_operator();
   auto rows = [&](double* yy) {
     if (dense)
       launch_dense_spmv(dense->view, v, yy, ctx->stream);
@@ -1663,6 +1724,12 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       std::fprintf(stderr, "[rmg setup] level %llu %-12s %8.3f s\n", static_cast<unsigned long long>(k), what,
                    std::chrono::duration<double>(tnow() - t0).count());
   };
+  // V-cycle kinds: a coarse level that enters additively or keeps a dense Gram matrix never
+  // applies X_k, so its K1 layout and hot X^T blocks wait for a first application
+  // (Matrix::ensure_operator; build_vcycle applies the levels that smooth); RMG_EAGER_LEVELS=1
+  // builds them all at once as before
+  const bool defer_coarse = (kind == RMG_METHOD_PCG_VCYCLE || kind == RMG_METHOD_PCG_VCYCLE_ADDITIVE) &&
+                            std::getenv("RMG_EAGER_LEVELS") == nullptr;
   double beta_run = beta;
   for (uint64_t k = 0; k < L; ++k) {
     auto t0 = tnow();
@@ -1723,9 +1790,9 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
       lvl->mat = std::make_unique<Matrix>(ctx_, curm.n_global, curm.row0, nl, nc, std::move(xcd), 0, ldc, curm.comm);
     } else if (curm.rows_only) {  // X_k = X P is row-local: every rank coarsens its own rows
       lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), curm.n_global, curm.row0, true,
-                                          curm.comm);
+                                          curm.comm, defer_coarse);
     } else {
-      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), true);
+      lvl->mat = std::make_unique<Matrix>(ctx_, coarsen_level(curm, lvl->agg), true, nullptr, nullptr, defer_coarse);
     }
     lvl->beta = next_beta;
     lvl->label.upload(lvl->agg.label.data(), lvl->agg.label.size(), s);
@@ -1759,6 +1826,11 @@ Method::Method(Matrix* x, double beta, int kind, const rmg_level_spec* levels, u
         throw InvalidArgument("TwoLevelPreconditioner: omega must be positive");
       omega_.push_back(specs_[k].spec.omega_override);
       lambda_.push_back(0.0);
+      continue;
+    }
+    if (k >= 1 && !level_matrix(k).op_ready) {  // V-cycle kinds take their weights in build_vcycle
+      lambda_.push_back(0.0);
+      omega_.push_back(0.0);
       continue;
     }
     uint64_t its;
@@ -1951,6 +2023,15 @@ HostCsr Method::coarsen_level(Matrix& m, const Aggregation& agg) {
   const int64_t n = h.n, nnz = h.nnz();
   DBuf<int32_t> xp, xi, lab, cnt, ci;
   DBuf<double> xv, wt, cv;
+  const bool slog = std::getenv("RMG_SETUP_LOG") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!slog) return;
+    ctx_->sync();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rmg setup]   coarsen %-9s %8.3f s\n", what, std::chrono::duration<double>(now - tl).count());
+    tl = now;
+  };
   {
     const std::vector<int32_t> p32 = narrow(h.ptr, "row offsets"), i32 = narrow(h.idx, "column indices");
     xp.upload(p32.data(), p32.size(), s);
@@ -1962,9 +2043,7 @@ HostCsr Method::coarsen_level(Matrix& m, const Aggregation& agg) {
   cnt.alloc(std::max<int64_t>(1, n));
   ci.alloc(std::max<int64_t>(1, nnz));
   cv.alloc(std::max<int64_t>(1, nnz));
-  const bool slog = std::getenv("RMG_SETUP_LOG") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  if (slog) ctx_->sync();
+  lap("stage");
   auto t1 = std::chrono::steady_clock::now();
   coarsen_rows_gpu(s, xp.get(), xi.get(), m.pattern ? nullptr : xv.get(), n, lab.get(), wt.get(), cnt.get(), ci.get(),
                    cv.get());
@@ -1973,13 +2052,14 @@ HostCsr Method::coarsen_level(Matrix& m, const Aggregation& agg) {
     std::fprintf(stderr, "[rmg setup]   coarsen kernel %.3f s\n",
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count());
   }
-  (void)t0;
+  tl = std::chrono::steady_clock::now();
   std::vector<int32_t> hc(n), hi(nnz);
   std::vector<double> hv(nnz);
   RMG_CK(cudaMemcpyAsync(hc.data(), cnt.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   RMG_CK(cudaMemcpyAsync(hi.data(), ci.get(), nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   RMG_CK(cudaMemcpyAsync(hv.data(), cv.get(), nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
   ctx_->sync();
+  lap("D2H");
   HostCsr c;
   c.n = n;
   c.f = agg.n_coarse;
@@ -2000,6 +2080,7 @@ HostCsr Method::coarsen_level(Matrix& m, const Aggregation& agg) {
   for (unsigned t = 1; t < T; ++t) pool.emplace_back(body, t);
   body(0);
   for (auto& th : pool) th.join();
+  lap("compact");
   return c;
 }
 
@@ -3138,6 +3219,7 @@ uint64_t Method::run_pcg_vcycle(const double* rhs, SolveResult* out) {
 double Method::time_operator(size_t level, uint64_t reps, bool flush, double* k1_ms, double* k2_ms) {
   if (level >= static_cast<size_t>(n_levels())) throw InvalidArgument("level index out of range");
   Matrix& m = level_matrix(level);
+  if (!m.dense) m.ensure_operator();
   cudaStream_t s = ctx_->stream;
   DBuf<double> v(std::max<int64_t>(1, m.f())), out(std::max<int64_t>(1, m.f()));
   launch_fill(v.get(), 1.0, m.f(), s);

@@ -247,10 +247,19 @@ struct Matrix {
   int64_t bgram_ld = 0;
   // out (F x k, row-major) = X^T B for k columns given column-major (B_cm: k vectors of N): the block X^T pass
   void xt_block_cm(const double* b_cm, double* out, int k);
-  Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr);
+  // defer_operator: a coarse level of a V-cycle hierarchy that may never apply X_k (it enters
+  // additively, or its Gram matrix is kept dense): the K1 layout and the hot X^T blocks are
+  // built by ensure_operator() on the first application instead (never inside a graph capture:
+  // build_vcycle applies every level that smooths once, at prepare)
+  Matrix(Context* c, HostCsr h, bool detect_pattern, Comm* comm = nullptr, const DenseInput* din = nullptr,
+         bool defer_operator = false);
   // per-rank input: `local` holds rows [row0, row0 + local.n) of an n_global-row X
   // (row offsets rebased); every setup step on it is sharded (rmg_matrix_create_csr_rows)
-  Matrix(Context* c, HostCsr local, int64_t n_global, int64_t row0, bool detect_pattern, Comm* comm);
+  Matrix(Context* c, HostCsr local, int64_t n_global, int64_t row0, bool detect_pattern, Comm* comm,
+         bool defer_operator = false);
+  bool defer_op = false, op_ready = true;
+  void ensure_operator();
+  void upload_k1(const HostCsr& local);
   int64_t n_global = -1;
   bool rows_only = false;  // host holds only this rank's rows
   void init_sparse(const HostCsr& local);
