@@ -214,3 +214,39 @@ def test_additive_batch_equals_single(gpu, orc):
         w1, r1 = pm.solve(B[:, q])
         assert reps[q].converged and abs(reps[q].iterations - r1.iterations) <= 1
         assert rel_diff(W[:, q], w1) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["pcg_vcycle", "pcg_vcycle_additive"])
+def test_deferred_coarse_layouts_equal_eager(gpu, monkeypatch, kind):
+    """Coarse levels of a V-cycle hierarchy build their K1 layout and hot X^T blocks on a
+    first application only (Matrix::ensure_operator); RMG_EAGER_LEVELS=1 builds them at
+    prepare as before.  Same preconditioner, same solves (single and batched) either way;
+    timing a deferred level's operator builds its layouts on the spot."""
+    x = R.synth_sparse_zipf(5000, 700, 18.0, 1.1, True, 9)
+    m = R.DeviceMatrix(x)
+    sp = aspec([90, 20, 5], additive=(1,)) if kind == "pcg_vcycle_additive" else spec([90, 20, 5])
+    b = R.rng_normals(11, 5000)
+    B = np.stack([R.rng_normals(300 + q, 5000) for q in range(3)], axis=1)
+    v = np.random.default_rng(4).standard_normal(700)
+    out = {}
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("RMG_EAGER_LEVELS", "1")
+        else:
+            monkeypatch.delenv("RMG_EAGER_LEVELS", raising=False)
+        pm = R.PreparedMethod(m, 0.3, sp)
+        w, rep = pm.solve(b.copy())
+        W, reps = pm.solve_batch(B)
+        pm.set_beta(0.05)  # rebuilds the cycle: the deferred levels stay consistent
+        w2, rep2 = pm.solve(b.copy())
+        out[eager] = (pm.precondition(v), w, rep.iterations, W, [r.iterations for r in reps], w2, rep2.iterations)
+        assert rep.converged and rep2.converged and all(r.converged for r in reps)
+        for lv in range(1, pm.n_levels):
+            assert pm.time_operator(lv, 1, False)[0] > 0.0
+        pm.close()
+    d, e = out[False], out[True]
+    assert rel_diff(d[0], e[0]) <= 1e-12
+    assert rel_diff(d[1], e[1]) <= 1e-9 and abs(d[2] - e[2]) <= 1
+    assert rel_diff(d[3], e[3]) <= 1e-9 and all(abs(a - c) <= 1 for a, c in zip(d[4], e[4]))
+    assert rel_diff(d[5], e[5]) <= 1e-9 and abs(d[6] - e[6]) <= 1
