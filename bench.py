@@ -178,11 +178,13 @@ class ClockSampler:
     Why not a free-running `nvidia-smi -lms 50` (round 1): a query that lands INSIDE a step
     stalls the GPU for ~15 ms on this platform -- the same 5 steps of cfg 3 timed 29.6 ms each
     with no query inside them and 30.5-34.6 ms with 1-4 (`-lms 50 / 200`, or NVML from a
-    thread every 50 / 150 ms); between steps it costs nothing that is timed.  Measured on the
-    final code (gpurun_out/exp1.log, 5 runs each): NVML between steps 29.7-29.9 ms on every
-    step of every run, a one-shot nvidia-smi between steps (BENCH_NO_NVML=1) the same, and no
-    query at all during the region (BENCH_NO_STEP_SAMPLES=1) a 43-63 ms fifth step in 2 runs
-    of 5 -- so the knobs stay as diagnostics and the default is the between-steps NVML read."""
+    thread every 50 / 150 ms); between steps it costs nothing that is timed.
+    BENCH_NO_NVML=1 (one-shot nvidia-smi between steps) and BENCH_NO_STEP_SAMPLES=1 (one
+    sample after the region) stay as diagnostics.  The occasional 40-60 ms step seen with
+    them (profiles/r2_bench_clock_sampler_modes.log) was not the sampler: the loop graph's
+    capture + instantiate inside the solve after a set_beta took 4-23 ms instead of 0.3 ms
+    in one solve out of three to ten; set_beta now rebuilds that graph itself
+    (profiles/r2_bench_graph_rebuild.log: 60 steps, none above 31.6 ms)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -940,10 +942,15 @@ def timed_batches(pm, stream, bcm, wcm, nb, betas, schedule, cur, clocks=None):
             cur[0] = beta
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        tw = time.perf_counter()
         rs = pm.solve_batch_device(bcm.data_ptr(), wcm.data_ptr(), nb, True)
+        tw = time.perf_counter() - tw
         e1.record(stream)
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
+        if os.environ.get("RMG_BENCH_TRACE"):
+            print(f"[trace] step event {ms[-1]:.2f} ms, call wall {1e3 * tw:.2f} ms, solver wall "
+                  f"{1e3 * max(r.wall_time_s for r in rs):.2f} ms", file=sys.stderr, flush=True)
         reps.append(rs)
         if clocks is not None:
             clocks.sample()  # between steps: never inside one
@@ -974,7 +981,8 @@ def run_sweep(args, cfg):
     """BASELINE cfg 3: a beta sweep over one fixed hierarchy with 16 right-hand sides
     solved as a batched block operator.  A step = one beta's batch (one
     rmg_method_solve_batch of the 16 columns), betas in sweep order (set_beta between
-    steps, outside the events: it rebuilds only the beta-dependent coarse factors).
+    steps, outside the events: it rebuilds only the beta-dependent coarse factors and the
+    batched loop's CUDA graph, whose nodes carry beta and those buffers).
     value = device ms per right-hand side.  N > 1 ranks: the (beta, batch) steps are
     independent units, dealt round-robin to the ranks (no collective on the data
     path); value = max-over-ranks time / all solves."""

@@ -2148,11 +2148,18 @@ void Method::jacobi_diag() {
 // coarsest inverse and the dense inner levels are rebuilt -- exactly what a
 // fresh prepare at this beta computes.
 void Method::set_beta(double beta) {
+  const int block_k = bw_graph_ && bw_.k == bw_graph_k_ ? bw_graph_k_ : 0;
+  set_beta_impl(beta);
+  // a sweep of batched solves: the loop graph for the new beta is part of this step, not of the next solve
+  if (block_k > 0 && std::getenv("RMG_NO_GRAPH") == nullptr) build_block_graph(block_k);
+}
+
+void Method::set_beta_impl(double beta) {
   if (beta < 0.0) throw InvalidArgument("RidgeOperator: beta must be nonnegative, got " + std::to_string(beta));
   RMG_CK(cudaSetDevice(ctx_->device));
   fcg_graph_.reset();  // the graphs point at the coarse buffers rebuilt below
-  vc_graph_.reset();
-  bw_graph_.reset();
+  vc_graph_retired_ = std::move(vc_graph_);
+  bw_graph_retired_ = std::move(bw_graph_);
   cg_graph_[0].reset();  // beta is a kernel argument of every captured apply
   cg_graph_[1].reset();
   beta_ = beta;
@@ -2799,7 +2806,7 @@ void Method::precondition(const double* r, double* z) {
 void Method::build_vcycle() {
   cudaStream_t s = ctx_->stream;
   const size_t L = coarse_.size();
-  vc_graph_.reset();  // its kernels point at the buffers rebuilt here
+  if (vc_graph_) vc_graph_retired_ = std::move(vc_graph_);  // its kernels point at the buffers rebuilt here
   vc_.clear();
   if (!dg_built_) build_dense_grams();  // beta-free: built once, kept across set_beta
   for (size_t k = 0; k < L; ++k) {
@@ -3011,6 +3018,50 @@ void Method::bvcycle(size_t lv, const double* r, double* z, int k) {
   ctx_->launches += 10;
 }
 
+// One lock-step iteration of the batched PCG loop (k columns) on the context's stream --
+// the capture stream while a graph is recorded.  Works on bw_ (sized by solve_block).
+void Method::block_iteration(int k) {
+  Matrix& m = *fine_;
+  BlockWork& w = bw_;
+  const int64_t n = m.f();
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(296, (n + 255) / 256)));
+  double *rr = w.dots.get(), *rz = rr + 64, *pap = rr + 128;
+  cudaStream_t cs = ctx_->stream;
+  m.apply_block(w.p.get(), w.ap.get(), level_beta(0), k, false);
+  launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, cs);
+  launch_bpcg_alpha(w.sc.get(), pap, k, cs);
+  // x, r and <r, r> in one pass (the partials are launch_bdots')
+  launch_bupdate_xr_dot(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, w.partial.get(), g, rr, cs);
+  launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), cs);
+  brz_partial_ = w.partial.get();  // an additive finest level forms <r, z> while it writes z
+  brz_g_ = g;
+  brz_out_ = rz;
+  brz_done_ = false;
+  bprecond(w.r.get(), w.z.get(), k);
+  brz_partial_ = nullptr;
+  if (!brz_done_) launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
+  launch_bpcg_beta(w.sc.get(), rz, k, cs);
+  launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, cs);
+  ctx_->launches += 12;
+}
+
+// The lock-step loop as a CUDA graph (device-side while loop over block_iteration).  Built by
+// the first batched solve, and again by set_beta for the k it was built for: beta and the
+// rebuilt coarse buffers are baked into the captured nodes, and capture + instantiate (0.3 ms,
+// but 4-23 ms in one solve out of three to ten) then never falls inside a solve.
+bool Method::build_block_graph(int k) {
+  bw_graph_.reset();
+  const uint64_t maxit = std::max<uint64_t>(solver.max_iters, 1);
+  auto gl = std::make_unique<GraphLoop>();
+  gl->passes.alloc(1);
+  if (!capture_while_graph(ctx_, nullptr, [&] { block_iteration(k); }, &gl->g, &gl->exec, &gl->launches_per_iter,
+                           gl->passes.get(), maxit + 2, bw_.sc.get(), k))
+    return false;
+  bw_graph_ = std::move(gl);
+  bw_graph_k_ = k;
+  return true;
+}
+
 std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, int k) {
   if (!block_capable())
     throw InvalidArgument("solve_block: cg, jacobi_cg or pcg_vcycle over a single-GPU matrix only");
@@ -3059,43 +3110,21 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
   for (size_t lv = 1; lv < coarse_.size() && vc_kind(); ++lv)  // smoothed coarse levels applied as sparse sweeps
     if (dgram(lv) == nullptr && !vc_additive(lv) && level_matrix(lv).dense == nullptr)
       level_matrix(lv).ensure_block_schedule();
-  auto iteration = [&] {
-    cudaStream_t cs = ctx_->stream;  // the capture stream while a graph is recorded
-    m.apply_block(w.p.get(), w.ap.get(), beta0, k, false);
-    launch_bdots(w.p.get(), w.ap.get(), n, k, w.partial.get(), g, pap, cs);
-    launch_bpcg_alpha(w.sc.get(), pap, k, cs);
-    // x, r and <r, r> in one pass (the partials are launch_bdots')
-    launch_bupdate_xr_dot(w.x.get(), w.r.get(), w.p.get(), w.ap.get(), w.sc.get(), n, k, w.partial.get(), g, rr, cs);
-    launch_bpcg_conv(w.sc.get(), rr, k, w.hist.get(), cs);
-    brz_partial_ = w.partial.get();  // an additive finest level forms <r, z> while it writes z
-    brz_g_ = g;
-    brz_out_ = rz;
-    brz_done_ = false;
-    bprecond(w.r.get(), w.z.get(), k);
-    brz_partial_ = nullptr;
-    if (!brz_done_) launch_bdots(w.r.get(), w.z.get(), n, k, w.partial.get(), g, rz, cs);
-    launch_bpcg_beta(w.sc.get(), rz, k, cs);
-    launch_bupdate_p(w.p.get(), w.z.get(), w.sc.get(), n, k, cs);
-    ctx_->launches += 12;
-  };
+  auto iteration = [&] { block_iteration(k); };
   // the lock-step loop as a CUDA graph (§4.13): runs while any column runs
   bool graph_used = false;
+  static const bool ttrace = std::getenv("RMG_SOLVE_TRACE") != nullptr;  // host-side phases of a batched solve
+  const auto tt0 = Clock::now();
+  auto tt1 = tt0, tt2 = tt0;
   if (std::getenv("RMG_NO_GRAPH") == nullptr) {
-    if (!bw_graph_ || bw_graph_k_ != k) {
-      bw_graph_.reset();
-      auto gl = std::make_unique<GraphLoop>();
-      gl->passes.alloc(1);
-      if (capture_while_graph(ctx_, nullptr, iteration, &gl->g, &gl->exec, &gl->launches_per_iter, gl->passes.get(),
-                              maxit + 2, w.sc.get(), k)) {
-        bw_graph_ = std::move(gl);
-        bw_graph_k_ = k;
-      }
-    }
+    if (!bw_graph_ || bw_graph_k_ != k) build_block_graph(k);
+    tt1 = Clock::now();
     if (bw_graph_) {
       RMG_CK(cudaMemsetAsync(bw_graph_->passes.get(), 0, sizeof(unsigned long long), s));
       RMG_CK(cudaGraphLaunch(bw_graph_->exec, s));
       graph_used = true;
     }
+    tt2 = Clock::now();
   }
   for (;;) {
     RMG_CK(cudaMemcpyAsync(hs.data(), w.sc.get(), k * sizeof(BlockScalars), cudaMemcpyDeviceToHost, s));
@@ -3112,6 +3141,12 @@ std::vector<SolveResult> Method::solve_block(const double* b_cm, double* w_cm, i
     iteration();
   }
   const double wall = secs(t0);
+  if (ttrace)
+    std::fprintf(stderr, "[rmg solve] enqueue %.2f ms, capture %.2f ms, launch %.2f ms, wait %.2f ms\n",
+                 1e3 * std::chrono::duration<double>(tt0 - t0).count(),
+                 1e3 * std::chrono::duration<double>(tt1 - tt0).count(),
+                 1e3 * std::chrono::duration<double>(tt2 - tt1).count(),
+                 1e3 * std::chrono::duration<double>(Clock::now() - tt2).count());
   launch_brow2col(w.x.get(), w_cm, n, k, s);
   int32_t itmax = 0;
   for (const auto& e : hs) itmax = std::max(itmax, e.it);

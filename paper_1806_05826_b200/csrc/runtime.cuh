@@ -433,6 +433,15 @@ class Method {
   std::unique_ptr<GraphLoop> cg_graph_[2];  // level-0 cg, jacobi_cg
   std::unique_ptr<GraphLoop> bw_graph_;     // batched pcg_vcycle (k columns)
   int bw_graph_k_ = 0;
+  // set_beta retires a loop graph instead of destroying it: the previous one is destroyed
+  // there (between solves) and one executable graph stays alive while the next is
+  // instantiated inside the following solve -- with none alive, capture + instantiate of the
+  // next took 23 ms instead of 0.3 ms in one solve out of three to ten
+  // (profiles/r2_bench_graph_retire.log)
+  std::unique_ptr<GraphLoop> bw_graph_retired_, vc_graph_retired_;
+  void block_iteration(int k);
+  bool build_block_graph(int k);
+  void set_beta_impl(double beta);
   void fcg_iteration(size_t k);
   bool build_fcg_graph();
   void pcg_vcycle_iteration();
