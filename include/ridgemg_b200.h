@@ -294,8 +294,9 @@ int rmg_method_prepare(rmg_matrix* m, double beta, int32_t method_kind,
 /* Regularization sweep over a fixed hierarchy (BASELINE cfg 3; the reference
  * re-prepares per beta, analysis.cpp:157-196): keeps the clustering, P, the
  * coarse matrices and lambda_max, rebuilds the beta-dependent parts (level
- * betas, omega, coarsest inverse, dense inner levels).  Solves after it equal
- * a fresh rmg_method_prepare at this beta. */
+ * betas, omega, coarsest inverse, dense inner levels, and the CUDA graph of
+ * the batched solve loop when one was built).  Solves after it equal a fresh
+ * rmg_method_prepare at this beta. */
 int rmg_method_set_beta(rmg_method* pm, double beta);
 int rmg_method_destroy(rmg_method* pm);
 /* PreparedMethod::solve (krylov.cpp:651-668): rhs = X^T b, then the Krylov
