@@ -2149,9 +2149,11 @@ void Method::jacobi_diag() {
 // fresh prepare at this beta computes.
 void Method::set_beta(double beta) {
   const int block_k = bw_graph_ && bw_.k == bw_graph_k_ ? bw_graph_k_ : 0;
+  const bool had_vc = vc_graph_ != nullptr;
   set_beta_impl(beta);
-  // a sweep of batched solves: the loop graph for the new beta is part of this step, not of the next solve
+  // a sweep of solves: the loop graphs for the new beta are part of this step, not of the next solve
   if (block_k > 0 && std::getenv("RMG_NO_GRAPH") == nullptr) build_block_graph(block_k);
+  if (had_vc && !vc_graph_ && !profiling_) build_vcycle_graph();
 }
 
 void Method::set_beta_impl(double beta) {
